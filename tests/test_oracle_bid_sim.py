@@ -1,0 +1,142 @@
+"""Pins of the oracle's bid curves (Eqs. 7-12) and forward simulation."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import pins
+import workloads
+from helpers import to_oracle, simple_problem
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _W_problem(W_row, sbar, delta):
+    """A T=1, K=1 problem plus a hand-made W_1 row, to exercise the hull on chosen points."""
+    pr = simple_problem(1.0, sbar, delta, 1.0, T=1, K=1, lam=[0.0])
+    W = np.asarray(W_row, dtype=np.float64).reshape(1, 1, -1)
+    return pr, W
+
+
+def test_spec_bid_examples():
+    """S:315 (points), S:323 (dent removed), S:331 (prices), S:342 (clearing)."""
+    # bid1: V row [0, 1, 4], s = 0.5 on (sbar=1, delta=0.5): points (-0.5, 4), (0, 1), (0.5, 0)
+    pr, W = _W_problem([0.0, 1.0, 4.0], 1.0, 0.5)
+    c = oracle.bidcurve(pr, W, 1, 1, 0)
+    assert c["q"].tolist() == [-0.5, 0.0, 0.5] or c["q"].tolist() == [-0.5, 0.5]
+    # the three points are not concave in p (slopes -6, -2): middle point is a dent -> removed
+    assert c["q"].tolist() == [-0.5, 0.5] and c["price"].tolist() == [4.0]   # -(0 - 4)/(0.5 + 0.5)
+    # bid2: (0,0), (1,-2), (2,0) scaled onto the grid: u = (0, -2, 0) at p = (-0.5, 0, 0.5)
+    pr, W = _W_problem([0.0, -2.0, 0.0], 1.0, 0.5)
+    c = oracle.bidcurve(pr, W, 1, 1, 0)
+    assert c["q"].tolist() == [-0.5, 0.5] and c["price"].tolist() == [0.0]
+    # bid3: hull (-1, 9), (0, 5), (1, 0) -> prices [4, 5]; (sbar=2, delta=1), i = 1
+    pr, W = _W_problem([0.0, 5.0, 9.0], 2.0, 1.0)
+    c = oracle.bidcurve(pr, W, 1, 1, 0)
+    assert c["q"].tolist() == [-1.0, 0.0, 1.0] and c["price"].tolist() == [4.0, 5.0]
+    # bid4: clearing at 4.5 -> quantity 0; ties (lambda == 4) go to the larger quantity (R9)
+    assert c["q"][oracle.clear(c, 4.5)] == 0.0
+    assert c["q"][oracle.clear(c, 4.0)] == 0.0
+    assert c["q"][oracle.clear(c, 3.99)] == -1.0
+    assert c["q"][oracle.clear(c, 5.0)] == 1.0
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_hull_matches_exhaustive(seed):
+    """the monotone-chain hull equals an O(n^3) exhaustive vertex test on random profiles."""
+    rng = np.random.default_rng(seed)
+    n = 11
+    row = np.round(rng.normal(0, 5, size=n), 1) if seed % 2 else rng.normal(0, 5, size=n)
+    pr, W = _W_problem(row, 10.0, 1.0)
+    act = oracle.actions(pr)
+    i = int(rng.integers(0, n))
+    c = oracle.bidcurve(pr, W, 1, i, 0)
+    tb = oracle.tables(pr)
+    feas = [a for a in range(len(act)) if tb["ilo"][a] <= i <= tb["ihi"][a]]
+    ps = [act[a] for a in feas]
+    us = [row[i + tb["off"][a]] for a in feas]
+    ref = [feas[j] for j in pins.hull_exhaustive(ps, us)]
+    assert c["vert"].tolist() == ref
+    assert np.all(np.diff(c["price"]) >= 0)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_bid_curve_consistent_with_stencil(seed):
+    """V15: with lambda p - g(p) payoffs, max over hull vertices of (lambda p + u) equals V_t(i, k)
+    (to rounding), the clearing quantity attains it, and clearing is monotone in the price."""
+    inst = workloads.random_instance(seed + 300, S_max=25, T=4, K=3)
+    pr = to_oracle(inst)
+    S, A = oracle.dims(pr)
+    if seed % 2:
+        inst.payoff_kind, inst.g = workloads.PAYOFF_LINEAR_MINUS_G, workloads.random_g(seed, A, 30.0)
+        pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    for t in range(1, inst.T + 1):
+        for k in range(inst.K):
+            lam = inst.lam[t - 1, k]
+            for i in range(S):
+                c = oracle.bidcurve(pr, sol.W, t, i, k)
+                vals = [lam * q + u for q, u in zip(c["q"], _hull_u(pr, sol.W, t, i, k, c))]
+                v = sol.V[t - 1, k, i]
+                assert abs(max(vals) - v) <= 1e-9 * max(1.0, abs(v))
+                j = oracle.clear(c, lam)
+                assert abs(vals[j] - v) <= 1e-9 * max(1.0, abs(v))
+                assert np.all(np.diff(c["price"]) >= 0)
+                qs = [c["q"][oracle.clear(c, x)] for x in np.linspace(-200, 200, 41)]
+                assert np.all(np.diff(qs) >= 0)
+
+
+def _hull_u(pr, W, t, i, k, c):
+    tb = oracle.tables(pr)
+    Wrow = W[t - 1, k]
+    g = pr.g if pr.payoff_kind == workloads.PAYOFF_LINEAR_MINUS_G else None
+    out = []
+    for a in c["vert"]:
+        o, w = tb["off"][a], tb["w"][a]
+        u = Wrow[i + o] if w == 0 else tb["omw"][a] * Wrow[i + o] + w * Wrow[i + o + 1]
+        out.append(u - (g[a] if g is not None else 0.0))
+    return out
+
+
+def test_terminal_stage_prices_zero():
+    """terminal-stage curve (W_T = 0, linear payoff) has all segment prices 0."""
+    inst = workloads.cfg1("b")
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    for i in [0, 10, 50, 100]:
+        c = oracle.bidcurve(pr, sol.W, inst.T, i, 2)
+        assert np.all(c["price"] == 0.0)
+
+
+def test_philox_known_answers():
+    """V17: Random123 known-answer vectors (tests/golden/philox_kat.txt)."""
+    with open(os.path.join(GOLD, "philox_kat.txt")) as f:
+        rows = [l.split() for l in f if l.strip() and not l.startswith("#")]
+    for r in rows:
+        v = [int(x, 16) for x in r]
+        assert oracle.philox(v[0:4], v[4:6]) == v[6:10]
+
+
+@pytest.mark.parametrize("name", ["cfg1a", "cfg1b", "cfg1b-rank1"])
+def test_simulation_mean_matches_J(name):
+    """V16: under lottery semantics E[profit] = J exactly, so the Monte Carlo mean lies within
+    5 standard errors of J."""
+    inst = workloads.cfg1(name[4], rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    n = 20000
+    per, m, v = oracle.simulate(pr, sol.pol, n, seed=12345)
+    se = np.sqrt(v / n)
+    assert abs(m - sol.J) <= 5 * se + 1e-9
+    assert m == np.sum(per) / n or abs(m - np.mean(per)) < 1e-9 * abs(m)
+
+
+def test_simulation_deterministic_path_equals_J():
+    """K = 1, on-lattice: every path is the same deterministic optimal schedule, profit == J."""
+    inst = workloads.random_instance(42, T=8, K=1, S_max=20, lattice=True, rank1=False)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    per, m, v = oracle.simulate(pr, sol.pol, 16, seed=1)
+    assert np.all(np.abs(per - sol.J) <= 1e-9 * max(1.0, abs(sol.J)))
+    assert v <= 1e-18 * max(1.0, sol.J ** 2)

@@ -1,0 +1,153 @@
+/*
+ * esdp.h -- C ABI of libesdp.so, the B200 (sm_100a) backward induction for the discretized
+ * multistage stochastic energy-storage arbitrage DP of arXiv 2511.15629
+ * ("GPU-Accelerated Dynamic Programming for Multistage Stochastic Energy Storage Arbitrage").
+ *
+ * Citations "P:NNN" are lines of the paper source; "DESIGN §x" is DESIGN.md at the
+ * repo root, which lists every reading of the paper this library adopts (R1..R24).
+ *
+ * Conventions for every entry point
+ *   - Plain C types only.  Every call returns esdp_status; nothing throws across the ABI.
+ *   - Host pointers unless the name ends in _dev.  Input arrays are deep-copied by the call
+ *     that receives them; the caller may free them as soon as the call returns.
+ *   - Output arrays are caller-allocated, sized from esdp_dims().
+ *   - On error the outputs are left untouched and esdp_last_error(ctx) describes the failure
+ *     (for esdp_create failures, esdp_last_error(NULL) holds the message for this thread).
+ *   - One caller per context at a time; distinct contexts are independent.
+ *   - All arithmetic is IEEE binary64.  Stage index t is 1-based (t = 1..T), SoC index
+ *     i is 0-based (s_i = i * delta), price state k is 0-based.
+ *   - Array layouts are row-major:  lambda[T][K], P[T-1][K][K], V/W[K][S] per stage,
+ *     pol[K][S] per stage (int16 action index into the ascending action grid).
+ */
+#ifndef ESDP_H
+#define ESDP_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct esdp_ctx esdp_ctx; /* opaque: owns device buffers, the CUDA graph, the stream */
+
+typedef enum {
+  ESDP_OK = 0,
+  ESDP_E_CONFIG = 1,   /* bad grid / parameters: T, K < 1; pbar, sbar, delta <= 0; eta not in (0,1];
+                          s0 not in [0, sbar]; sbar/delta not integral (no silent rounding);
+                          actions not strictly ascending, without an exact 0, |p| > pbar; A > 8191 */
+  ESDP_E_DATA = 2,     /* non-finite lambda or g; a row of P (or pi) is not a probability simplex
+                          within 1e-9 */
+  ESDP_E_INTERNAL = 3, /* an invariant failed (a row with every action infeasible; cannot happen
+                          because the zero action is always feasible, Eq. 4) */
+  ESDP_E_STATE = 4,    /* call order (query before esdp_backward), index out of range, or a
+                          feature not defined for this problem (bid curves of TABLE payoffs) */
+  ESDP_E_CUDA = 5,     /* a CUDA runtime error (message has the CUDA error string) */
+  ESDP_E_NCCL = 6,     /* reserved for the multi-GPU communicator */
+  ESDP_E_NOMEM = 7     /* device or host allocation failed */
+} esdp_status;
+
+/* Payoff of action p_a at price state k of stage t (Alg. 1 line 9; D3 in DESIGN §2):
+ *   LINEAR          pay = lambda_{t,k} * p_a                       (the paper's payoff)
+ *   LINEAR_MINUS_G  pay = lambda_{t,k} * p_a - g[a]                 (degradation / fixed costs;
+ *                                                                    may be non-concave)
+ *   TABLE           pay = g[t-1][k][a]                              (any payoff; no bid curves)
+ * The candidate value is pay + Wint, rounded in that association (DESIGN R14). */
+enum { ESDP_PAYOFF_LINEAR = 0, ESDP_PAYOFF_LINEAR_MINUS_G = 1, ESDP_PAYOFF_TABLE = 2 };
+
+/* flags */
+enum {
+  ESDP_KEEP_VALUES = 1u  /* keep V_t and W_t for every t on the device (needed by esdp_values
+                            for t > 1 and by the bid-curve calls); otherwise only V_1 is kept */
+};
+
+typedef struct {
+  int32_t T, K;          /* stages and Markov price states (north_star; the paper's R) */
+  double pbar, sbar, s0; /* power cap, energy cap, initial SoC, energy-per-stage units */
+  double eta_c, eta_d;   /* charge / discharge efficiency in (0,1]: F(p) = -p/eta_d (p >= 0),
+                            -eta_c p (p < 0) (Eq. 2; single eta in the paper) */
+  double delta;          /* SoC step; S = sbar/delta + 1 */
+  int32_t A;             /* 0 => the paper's recombining grid, Eq. 10; else len(actions) */
+  const double* actions; /* [A] strictly ascending, contains 0.0 exactly, |p| <= pbar (when A > 0) */
+  const double* lambda;  /* [T][K] price levels lambda_{t,k} */
+  const double* P;       /* [T-1][K][K], P[t-1][k][k'] = Pr(k_{t+1} = k' | k_t = k), t = 1..T-1;
+                            NULL => stagewise independent (rank-1) prices, the paper's case */
+  const double* pi;      /* Markov: [K] distribution of k_1.  Rank-1 (P == NULL): [T][K], row t-1 is
+                            pi_t, the probabilities of the stage-t price levels */
+  int32_t payoff_kind;   /* ESDP_PAYOFF_* */
+  const double* g;       /* [A] for LINEAR_MINUS_G, [T][K][A] for TABLE, ignored for LINEAR */
+  uint32_t flags;        /* ESDP_KEEP_* */
+} esdp_problem;
+
+/* Create a solver: validates the problem (same rules as the oracle), builds the state/action
+ * grid and the per-action transition data (Alg. 1 lines 2-5), allocates device
+ * memory on the current CUDA device and uploads the inputs.  *out receives the context. */
+esdp_status esdp_create(const esdp_problem* prob, esdp_ctx** out);
+
+/* Grid sizes: T, S = sbar/delta + 1, A, K (any pointer may be NULL). */
+esdp_status esdp_dims(const esdp_ctx* ctx, int32_t* T, int32_t* S, int32_t* A, int32_t* K);
+
+/* The action grid p_hat[A] (ascending) the solver uses (Eq. 10 or the user's actions). */
+esdp_status esdp_actions(const esdp_ctx* ctx, double* actions);
+
+/* Re-upload the stochastic inputs from HOST memory (shapes as in esdp_problem; NULL keeps the
+ * current array).  Validated like esdp_create.  Used for end-to-end runs where every solve
+ * brings new prices.  Invalidates previous results. */
+esdp_status esdp_load(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
+                      const double* g);
+
+/* Backward induction, Alg. 1 lines 6-11 in Markov form (Eqs. 5-6):
+ *   W_T = 0;  for t = T..1:  W_t = P_t V_{t+1} (t < T),
+ *             V_t(i,k) = max_a pay(t,k,a) + Wint_t(i,a,k),  pol_t(i,k) = smallest argmax,
+ * where Wint is the interpolated, infeasibility-masked continuation of Alg. 1 lines 7-8.
+ * Then J = sum_k pi_1[k] V_1(s0, k) (Eq. 6 at t = 0).  Runs on `stream` (a cudaStream_t,
+ * NULL = the context's own stream) and synchronizes it before returning.  J may be NULL. */
+esdp_status esdp_backward(esdp_ctx* ctx, void* stream, double* J);
+
+/* Enqueue the backward pass on `stream` without synchronizing (for timing harnesses); the J of the
+ * run is available from esdp_objective after the stream completes. */
+esdp_status esdp_backward_async(esdp_ctx* ctx, void* stream);
+esdp_status esdp_objective(esdp_ctx* ctx, double* J);
+
+/* Copy V_t [K][S] and (if W != NULL) W_t [K][S] to host memory.  t must be 1 unless the context
+ * was created with ESDP_KEEP_VALUES. */
+esdp_status esdp_values(const esdp_ctx* ctx, int32_t t, double* V, double* W);
+
+/* Copy the policy pol_t [K][S] (int16 action indices) to host memory. */
+esdp_status esdp_policy(const esdp_ctx* ctx, int32_t t, int16_t* pol);
+
+/* Bid curves, one per request (t, i, k): points (p_a, u_a = Wint_t(i,a,k) - g_a) over the
+ * feasible actions (Eq. 7), upper concave hull (Graham / monotone chain), monotone segment
+ * prices price_j = -(u_{j+1} - u_j)/(p_{j+1} - p_j) (Eq. 12) with a running-max repair (DESIGN R20).
+ *   req    [n][3] int32 (t, i, k), host
+ *   cap    per-curve capacity, >= A
+ *   nvert  [n] vertices per curve; vert [n][cap] action indices; q [n][cap] powers;
+ *   price  [n][cap] segment prices (entries >= nvert-1 unused).  Requires ESDP_KEEP_VALUES. */
+esdp_status esdp_bidcurves(esdp_ctx* ctx, int64_t n, const int32_t* req, int32_t cap,
+                           int32_t* nvert, int16_t* vert, double* q, double* price);
+/* Same, with DEVICE pointers for every array, enqueued on `stream` (no synchronization). */
+esdp_status esdp_bidcurves_dev(esdp_ctx* ctx, int64_t n, const int32_t* req_dev, int32_t cap,
+                               int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev,
+                               void* stream);
+
+/* Forward simulation of the argmax policy on n_paths sampled price paths:
+ *   k_1 ~ pi_1; for t = 1..T: a = pol_t(i, k); profit += pay(t,k,a);
+ *   i <- i + o_a (+1 with probability w_a at the interpolated endpoints: the lottery that the
+ *   interpolation of Alg. 1 line 7 represents, DESIGN R16); k <- sample of P_t[k, :].
+ * Random numbers: Philox4x32-10 (counter = (path, t, 'ESDP'), key = seed), DESIGN R17.
+ * per_path [n_paths] (host, nullable), mean, var (sample variance) over paths. */
+esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* mean, double* var,
+                          double* per_path);
+/* Device variant: per-path profits to per_path_dev, enqueued on stream. */
+esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
+                              void* stream);
+
+/* Number of kernel launches the last esdp_backward_async enqueued (for harness accounting). */
+esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
+
+void esdp_destroy(esdp_ctx* ctx);
+
+/* Message of the last failing call on ctx (ctx == NULL: last esdp_create failure of this thread). */
+const char* esdp_last_error(const esdp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,7 +1,7 @@
 """ctypes front end of the FP64 CPU oracle (oracle/esdp_oracle.c).
 
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
-cpu_baseline / --impl reference legs.  The product package paper_2511_15629_b200 never
+cpu_baseline / --impl reference legs.  The product (CUDA) package never
 imports this module, and nothing here imports the product.
 
 Arrays are numpy float64 / int16, C-contiguous; shapes follow esdp_oracle.h.

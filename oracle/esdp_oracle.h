@@ -3,7 +3,7 @@
  *
  * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs may load this library.  The product path
- * (paper_2511_15629_b200/, libesdp.so) never links, loads or calls it, and the two
+ *  (the CUDA package at the repo root) never links, loads or calls it, and the two
  * share no code: no headers, no helpers, no tables.
  *
  * Every function follows /root/reference/PAPER.md ("P:NNN" = line NNN) step by step,

@@ -1,0 +1,270 @@
+"""Python binding of libesdp.so (include/esdp.h): argument marshalling only.
+
+Every step of the method runs in the CUDA kernels behind the C ABI; this module converts numpy
+arrays / torch tensors into the C structs and pointers and raises on a non-OK status.  There is
+no fallback: if libesdp.so is missing or fails to load, importing this package raises.
+
+The function names mirror the C ABI (esdp_create, esdp_backward, ...).  ``Solver`` is a small
+owning wrapper around one context.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "ESDP_OK", "ESDP_E_CONFIG", "ESDP_E_DATA", "ESDP_E_INTERNAL", "ESDP_E_STATE", "ESDP_E_CUDA",
+    "ESDP_E_NCCL", "ESDP_E_NOMEM", "ESDP_PAYOFF_LINEAR", "ESDP_PAYOFF_LINEAR_MINUS_G",
+    "ESDP_PAYOFF_TABLE", "ESDP_KEEP_VALUES", "EsdpError", "esdp_problem", "LIB_PATH", "lib",
+    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
+    "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
+    "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_destroy", "esdp_last_error",
+    "Solver", "EXPORTED_SYMBOLS",
+]
+
+ESDP_OK, ESDP_E_CONFIG, ESDP_E_DATA, ESDP_E_INTERNAL, ESDP_E_STATE, ESDP_E_CUDA, ESDP_E_NCCL, ESDP_E_NOMEM = range(8)
+ESDP_PAYOFF_LINEAR, ESDP_PAYOFF_LINEAR_MINUS_G, ESDP_PAYOFF_TABLE = 0, 1, 2
+ESDP_KEEP_VALUES = 1
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
+
+EXPORTED_SYMBOLS = [
+    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
+    "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
+    "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_destroy", "esdp_last_error",
+]
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i16p = ctypes.POINTER(ctypes.c_int16)
+_vp = ctypes.c_void_p
+
+
+class esdp_problem(ctypes.Structure):
+    _fields_ = [
+        ("T", ctypes.c_int32), ("K", ctypes.c_int32),
+        ("pbar", ctypes.c_double), ("sbar", ctypes.c_double), ("s0", ctypes.c_double),
+        ("eta_c", ctypes.c_double), ("eta_d", ctypes.c_double), ("delta", ctypes.c_double),
+        ("A", ctypes.c_int32), ("actions", _dp),
+        ("lambda_", _dp), ("P", _dp), ("pi", _dp),
+        ("payoff_kind", ctypes.c_int32), ("g", _dp),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+class EsdpError(RuntimeError):
+    def __init__(self, status: int, what: str, msg: str):
+        super().__init__(f"{what} failed with status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libesdp.so not found at {LIB_PATH}; build it with `make` (or __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    ctx = _vp
+    sig = {
+        "esdp_create": ([ctypes.POINTER(esdp_problem), ctypes.POINTER(_vp)], ctypes.c_int),
+        "esdp_dims": ([ctx, _i32p, _i32p, _i32p, _i32p], ctypes.c_int),
+        "esdp_actions": ([ctx, _dp], ctypes.c_int),
+        "esdp_load": ([ctx, _dp, _dp, _dp, _dp], ctypes.c_int),
+        "esdp_backward": ([ctx, _vp, _dp], ctypes.c_int),
+        "esdp_backward_async": ([ctx, _vp], ctypes.c_int),
+        "esdp_objective": ([ctx, _dp], ctypes.c_int),
+        "esdp_values": ([ctx, ctypes.c_int32, _dp, _dp], ctypes.c_int),
+        "esdp_policy": ([ctx, ctypes.c_int32, _i16p], ctypes.c_int),
+        "esdp_bidcurves": ([ctx, ctypes.c_int64, _i32p, ctypes.c_int32, _i32p, _i16p, _dp, _dp], ctypes.c_int),
+        "esdp_bidcurves_dev": ([ctx, ctypes.c_int64, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+        "esdp_simulate": ([ctx, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp], ctypes.c_int),
+        "esdp_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
+        "esdp_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "esdp_destroy": ([ctx], None),
+        "esdp_last_error": ([ctx], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+
+
+def _p(a, t=_dp):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def esdp_last_error(ctx=None) -> str:
+    m = lib.esdp_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def _check(st, what, ctx=None):
+    if st != ESDP_OK:
+        raise EsdpError(st, what, esdp_last_error(ctx))
+
+
+def esdp_create(T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions=None,
+                payoff_kind=ESDP_PAYOFF_LINEAR, g=None, flags=0):
+    """esdp_create(&problem, &ctx): returns the opaque context handle (int)."""
+    keep = [_f64(x) for x in (actions, lam, P, pi, g)]
+    act, lam_, P_, pi_, g_ = keep
+    pr = esdp_problem(int(T), int(K), float(pbar), float(sbar), float(s0), float(eta_c), float(eta_d),
+                      float(delta), 0 if act is None else int(act.shape[0]), _p(act), _p(lam_), _p(P_),
+                      _p(pi_), int(payoff_kind), _p(g_), int(flags))
+    out = _vp()
+    st = lib.esdp_create(ctypes.byref(pr), ctypes.byref(out))
+    _check(st, "esdp_create", None)
+    return out.value
+
+
+def esdp_dims(ctx):
+    T, S, A, K = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.esdp_dims(ctx, ctypes.byref(T), ctypes.byref(S), ctypes.byref(A), ctypes.byref(K)), "esdp_dims", ctx)
+    return T.value, S.value, A.value, K.value
+
+
+def esdp_actions(ctx):
+    _, _, A, _ = esdp_dims(ctx)
+    out = np.zeros(A)
+    _check(lib.esdp_actions(ctx, _p(out)), "esdp_actions", ctx)
+    return out
+
+
+def esdp_load(ctx, lam=None, P=None, pi=None, g=None):
+    keep = [_f64(x) for x in (lam, P, pi, g)]
+    _check(lib.esdp_load(ctx, *[_p(x) for x in keep]), "esdp_load", ctx)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+def esdp_backward(ctx, stream=None) -> float:
+    J = ctypes.c_double()
+    _check(lib.esdp_backward(ctx, _stream_ptr(stream), ctypes.byref(J)), "esdp_backward", ctx)
+    return J.value
+
+
+def esdp_backward_async(ctx, stream=None):
+    _check(lib.esdp_backward_async(ctx, _stream_ptr(stream)), "esdp_backward_async", ctx)
+
+
+def esdp_objective(ctx) -> float:
+    J = ctypes.c_double()
+    _check(lib.esdp_objective(ctx, ctypes.byref(J)), "esdp_objective", ctx)
+    return J.value
+
+
+def esdp_values(ctx, t, want_W=True):
+    T, S, A, K = esdp_dims(ctx)
+    V = np.zeros((K, S))
+    W = np.zeros((K, S)) if want_W else None
+    _check(lib.esdp_values(ctx, int(t), _p(V), _p(W)), "esdp_values", ctx)
+    return (V, W) if want_W else V
+
+
+def esdp_policy(ctx, t):
+    T, S, A, K = esdp_dims(ctx)
+    pol = np.zeros((K, S), np.int16)
+    _check(lib.esdp_policy(ctx, int(t), _p(pol, _i16p)), "esdp_policy", ctx)
+    return pol
+
+
+def esdp_bidcurves(ctx, req, cap=None):
+    """req: int array [n][3] of (t, i, k).  Returns dict(nvert, vert, q, price) (padded rows)."""
+    T, S, A, K = esdp_dims(ctx)
+    cap = A if cap is None else int(cap)
+    req = np.ascontiguousarray(req, dtype=np.int32).reshape(-1, 3)
+    n = req.shape[0]
+    nv = np.zeros(n, np.int32)
+    vert = np.zeros((n, cap), np.int16)
+    q = np.zeros((n, cap))
+    price = np.zeros((n, cap))
+    _check(lib.esdp_bidcurves(ctx, n, _p(req, _i32p), cap, _p(nv, _i32p), _p(vert, _i16p), _p(q), _p(price)),
+           "esdp_bidcurves", ctx)
+    return dict(nvert=nv, vert=vert, q=q, price=price)
+
+
+def esdp_bidcurves_dev(ctx, n, req_ptr, cap, nvert_ptr, vert_ptr, q_ptr, price_ptr, stream=None):
+    _check(lib.esdp_bidcurves_dev(ctx, int(n), req_ptr, int(cap), nvert_ptr, vert_ptr, q_ptr, price_ptr,
+                                  _stream_ptr(stream)), "esdp_bidcurves_dev", ctx)
+
+
+def esdp_simulate(ctx, n_paths, seed, per_path=True):
+    m, v = ctypes.c_double(), ctypes.c_double()
+    out = np.zeros(int(n_paths)) if per_path else None
+    _check(lib.esdp_simulate(ctx, int(n_paths), ctypes.c_uint64(int(seed)), ctypes.byref(m), ctypes.byref(v),
+                             _p(out)), "esdp_simulate", ctx)
+    return out, m.value, v.value
+
+
+def esdp_simulate_dev(ctx, n_paths, seed, per_path_ptr, stream=None):
+    _check(lib.esdp_simulate_dev(ctx, int(n_paths), ctypes.c_uint64(int(seed)), per_path_ptr, _stream_ptr(stream)),
+           "esdp_simulate_dev", ctx)
+
+
+def esdp_launch_count(ctx) -> int:
+    n = ctypes.c_int64()
+    _check(lib.esdp_launch_count(ctx, ctypes.byref(n)), "esdp_launch_count", ctx)
+    return n.value
+
+
+def esdp_destroy(ctx):
+    lib.esdp_destroy(ctx)
+
+
+class Solver:
+    """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
+    (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
+
+    def __init__(self, inst, keep_values=True):
+        self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
+                               inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
+                               getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
+                               ESDP_KEEP_VALUES if keep_values else 0)
+        self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
+
+    def backward(self, stream=None):
+        return esdp_backward(self.ctx, stream)
+
+    def values(self, t, want_W=True):
+        return esdp_values(self.ctx, t, want_W)
+
+    def policy(self, t):
+        return esdp_policy(self.ctx, t)
+
+    def actions(self):
+        return esdp_actions(self.ctx)
+
+    def bidcurves(self, req, cap=None):
+        return esdp_bidcurves(self.ctx, req, cap)
+
+    def simulate(self, n_paths, seed, per_path=True):
+        return esdp_simulate(self.ctx, n_paths, seed, per_path)
+
+    def close(self):
+        if self.ctx:
+            esdp_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,600 @@
+// esdp.cu -- host side of libesdp.so: the C ABI of include/esdp.h.
+//
+// Validation, the state/action grid (Eq. 10) and the per-action transition data
+// (Alg. 1 lines 2-5) are computed here on the host once per context, in binary64 with
+// FMA contraction disabled (-Xcompiler -ffp-contract=off).  Everything per stage runs in the
+// kernels of kernels.cuh; the whole backward pass is one CUDA graph (2T+1 launches).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/esdp.h"
+#include "kernels.cuh"
+
+using namespace esdp;
+
+namespace {
+
+constexpr double kGridTol = 1e-9;  // DESIGN R6/R7
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct esdp_ctx {
+  // problem
+  int T = 0, K = 0, S = 0, A = 0, kind = 0, rank1 = 0;
+  uint32_t flags = 0;
+  double pbar = 0, sbar = 0, s0 = 0, eta_c = 1, eta_d = 1, delta = 1;
+  std::vector<double> act, w, omw;
+  std::vector<int> off;
+  std::vector<Seg> segs;
+  int o_min = 0, o_max = 0;
+  int on_grid = 1, f0 = 0;
+  double w0 = 0.0;
+  // device
+  double *d_lambda = nullptr, *d_P = nullptr, *d_pi = nullptr, *d_g = nullptr;
+  double *d_act = nullptr, *d_w = nullptr, *d_omw = nullptr;
+  int* d_off = nullptr;
+  Seg* d_segs = nullptr;
+  double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
+  double *d_red = nullptr;
+  int16_t* d_pol = nullptr;
+  double* d_sim = nullptr;
+  int64_t sim_cap = 0;
+  int32_t* d_req = nullptr;
+  int64_t req_cap = 0;
+  int32_t* d_nv = nullptr;
+  int16_t* d_vert = nullptr;
+  double *d_q = nullptr, *d_price = nullptr;
+  int64_t out_cap = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  size_t stencil_smem = 0;
+  int64_t launches = 0;
+  bool solved = false;
+  std::string err;
+};
+
+namespace {
+
+esdp_status fail(esdp_ctx* c, esdp_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf; else g_create_error = buf;
+  return s;
+}
+
+#define CUDA_OR_FAIL(ctx, call)                                                             \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((ctx), e_ == cudaErrorMemoryAllocation ? ESDP_E_NOMEM : ESDP_E_CUDA,      \
+                  "%s: %s", #call, cudaGetErrorString(e_));                                 \
+  } while (0)
+
+bool simplex_ok(const double* q, int K) {
+  double s = 0.0;
+  for (int j = 0; j < K; ++j) {
+    if (!std::isfinite(q[j]) || q[j] < 0.0) return false;
+    s += q[j];
+  }
+  return std::fabs(s - 1.0) <= 1e-9;
+}
+
+// Eq. 10 with the R6 guard and endpoint clamp.
+void paper_grid(double pbar, double eta_c, double eta_d, double delta, std::vector<double>& out) {
+  const double qc = pbar * eta_c / delta;
+  const double qd = pbar / (delta * eta_d);
+  long long nc = (long long)std::ceil(qc - kGridTol), nd = (long long)std::ceil(qd - kGridTol);
+  if (nc < 1) nc = 1;
+  if (nd < 1) nd = 1;
+  out.clear();
+  for (long long j = nc; j >= 1; --j) {
+    const double x = (double)j * delta / eta_c;
+    out.push_back(-(x < pbar ? x : pbar));
+  }
+  out.push_back(0.0);
+  for (long long j = 1; j <= nd; ++j) {
+    const double x = (double)j * delta * eta_d;
+    out.push_back(x < pbar ? x : pbar);
+  }
+}
+
+esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  for (long long j = 0; j < (long long)c->T * c->K; ++j)
+    if (!std::isfinite(lambda[j])) return fail(c, ESDP_E_DATA, "lambda[%lld] is not finite", j);
+  if (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
+    for (int a = 0; a < c->A; ++a)
+      if (!std::isfinite(g[a])) return fail(c, ESDP_E_DATA, "g[%d] is not finite", a);
+  } else if (c->kind == ESDP_PAYOFF_TABLE) {
+    for (long long j = 0; j < (long long)c->T * c->K * c->A; ++j)
+      if (!std::isfinite(g[j])) return fail(c, ESDP_E_DATA, "payoff table entry %lld is not finite", j);
+  }
+  if (!c->rank1) {
+    for (long long r = 0; r < (long long)(c->T - 1) * c->K; ++r)
+      if (!simplex_ok(P + r * c->K, c->K)) return fail(c, ESDP_E_DATA, "row %lld of P is not a probability simplex", r);
+    if (!simplex_ok(pi, c->K)) return fail(c, ESDP_E_DATA, "pi_1 is not a probability simplex");
+  } else {
+    for (int t = 0; t < c->T; ++t)
+      if (!simplex_ok(pi + (long long)t * c->K, c->K)) return fail(c, ESDP_E_DATA, "pi_%d is not a probability simplex", t + 1);
+  }
+  return ESDP_OK;
+}
+
+// Alg. 1 lines 2-5 reduced to per-action (offset, weight); DESIGN §5 "layout".
+void build_tables(esdp_ctx* c) {
+  const int A = c->A;
+  c->off.assign(A, 0);
+  c->w.assign(A, 0.0);
+  c->omw.assign(A, 1.0);
+  for (int a = 0; a < A; ++a) {
+    const double p = c->act[a];
+    const double F = (p >= 0.0) ? -(p / c->eta_d) : -(c->eta_c * p);  // Eq. 2
+    const double e = F / c->delta;
+    const double r = std::nearbyint(e);
+    if (std::fabs(e - r) <= kGridTol) {
+      c->off[a] = (int)r;
+      c->w[a] = 0.0;
+    } else {
+      const double f = std::floor(e);
+      c->off[a] = (int)f;
+      c->w[a] = e - f;
+    }
+    c->omw[a] = 1.0 - c->w[a];
+  }
+  // An action is live if some row i in [0, S-1] can take it (i + o >= 0, i + o + [w > 0] <= S-1);
+  // dead actions are infeasible everywhere (Eq. 4) and are left out of the stencil plan.
+  auto live = [&](int b) {
+    const int hi = c->off[b] + (c->w[b] != 0.0 ? 1 : 0);
+    return c->off[b] >= -(c->S - 1) && hi <= c->S - 1;
+  };
+  // recombining runs: consecutive integral offsets decreasing by one
+  c->segs.clear();
+  int a = 0;
+  while (a < A) {
+    if (!live(a)) { ++a; continue; }
+    Seg s{a, 1, c->off[a], c->w[a] != 0.0 ? 1 : 0};
+    if (!s.interp) {
+      while (a + s.n < A && live(a + s.n) && c->w[a + s.n] == 0.0 && c->off[a + s.n] == s.o0 - s.n) ++s.n;
+    }
+    c->segs.push_back(s);
+    a += s.n;
+  }
+  c->o_min = 0;
+  c->o_max = 0;
+  for (int b = 0; b < A; ++b) {
+    if (!live(b)) continue;
+    c->o_min = std::min(c->o_min, c->off[b]);
+    c->o_max = std::max(c->o_max, c->off[b] + (c->w[b] != 0.0 ? 1 : 0));
+  }
+  const double x = c->s0 / c->delta;
+  const double r = std::nearbyint(x);
+  c->on_grid = std::fabs(x - r) <= kGridTol;
+  c->f0 = c->on_grid ? (int)r : (int)std::floor(x);
+  c->w0 = c->on_grid ? 0.0 : x - std::floor(x);
+}
+
+// cdf rows: running sum in ascending order, last entry forced to 1 (DESIGN R17)
+void build_cdf(const double* q, int K, double* out) {
+  double s = 0.0;
+  for (int j = 0; j < K; ++j) {
+    s = s + q[j];
+    out[j] = (j == K - 1) ? 1.0 : s;
+  }
+}
+
+template <class T>
+esdp_status dev_alloc(esdp_ctx* c, T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) return fail(c, ESDP_E_NOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+  return ESDP_OK;
+}
+
+void free_all(esdp_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_nv, c->d_vert, c->d_q, c->d_price};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  const size_t TK = (size_t)c->T * c->K;
+  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_lambda, lambda, TK * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  std::vector<double> cdf;
+  if (!c->rank1) {
+    if (P) {
+      const size_t n = (size_t)(c->T - 1) * c->K * c->K;
+      if (n) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P, P, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      cdf.resize(std::max<size_t>(n, 1));
+      for (size_t r = 0; r < (size_t)(c->T - 1) * c->K; ++r) build_cdf(P + r * c->K, c->K, cdf.data() + r * c->K);
+      if (n) CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf, cdf.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (pi) {
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, c->K * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      std::vector<double> c1(c->K);
+      build_cdf(pi, c->K, c1.data());
+      CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf1, c1.data(), c->K * sizeof(double), cudaMemcpyHostToDevice));
+    }
+  } else if (pi) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, TK * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    cdf.resize(TK);
+    for (int t = 0; t < c->T; ++t) build_cdf(pi + (size_t)t * c->K, c->K, cdf.data() + (size_t)t * c->K);
+    CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf, cdf.data(), TK * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf1, cdf.data(), c->K * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G)
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (g && c->kind == ESDP_PAYOFF_TABLE)
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  c->solved = false;
+  return ESDP_OK;
+}
+
+size_t w_rows(const esdp_ctx* c) { return c->rank1 ? 1 : (size_t)c->K; }
+bool keep(const esdp_ctx* c) { return (c->flags & ESDP_KEEP_VALUES) != 0; }
+// V_t / W_t / pol_t device slices (stage t = 1..T)
+double* V_of(esdp_ctx* c, int t) {
+  const size_t KS = (size_t)c->K * c->S;
+  return keep(c) ? c->d_V + (size_t)(t - 1) * KS : c->d_V + (size_t)((t - 1) & 1) * KS;
+}
+double* W_of(esdp_ctx* c, int t) {
+  const size_t RS = w_rows(c) * c->S;
+  return keep(c) ? c->d_W + (size_t)(t - 1) * RS : c->d_W;
+}
+
+// Enqueue the 2T+1 launches of one backward pass on stream s.
+esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
+  const int T = c->T, K = c->K, S = c->S;
+  int64_t n = 0;
+  for (int t = T; t >= 1; --t) {
+    double* Wt = W_of(c, t);
+    if (t == T) {
+      CUDA_OR_FAIL(c, cudaMemsetAsync(Wt, 0, w_rows(c) * S * sizeof(double), s));  // W_T = 0
+    } else {
+      const int rows = (int)w_rows(c);
+      const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
+      dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
+      contract_kernel<<<grid, kColsC, sizeof(double) * K * kRowsC, s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S);
+      ++n;
+    }
+    StencilParams prm;
+    prm.W = Wt;
+    prm.V = V_of(c, t);
+    prm.pol = c->d_pol + (size_t)(t - 1) * K * S;
+    prm.lambda_t = c->d_lambda + (size_t)(t - 1) * K;
+    prm.act = c->d_act;
+    prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
+    prm.w = c->d_w;
+    prm.omw = c->d_omw;
+    prm.off = c->d_off;
+    prm.segs = c->d_segs;
+    prm.nseg = (int)c->segs.size();
+    prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
+    prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min;
+    dim3 grid((S + kTile - 1) / kTile, K);
+    stencil_kernel<<<grid, kStencilWarps * 32, c->stencil_smem, s>>>(prm);
+    ++n;
+  }
+  const double* pi1 = c->d_pi;  // rank-1: row 0 of pi = pi_1
+  objective_kernel<<<1, 32, 0, s>>>(V_of(c, 1), pi1, K, S, c->f0, c->w0, c->on_grid, c->d_J);
+  ++n;
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  c->launches = n;
+  return ESDP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
+  g_create_error.clear();
+  if (!pr || !out) return fail(nullptr, ESDP_E_CONFIG, "null argument");
+  *out = nullptr;
+  if (pr->T < 1 || pr->K < 1) return fail(nullptr, ESDP_E_CONFIG, "T and K must be >= 1");
+  if (!(std::isfinite(pr->pbar) && pr->pbar > 0)) return fail(nullptr, ESDP_E_CONFIG, "pbar must be > 0");
+  if (!(std::isfinite(pr->sbar) && pr->sbar > 0)) return fail(nullptr, ESDP_E_CONFIG, "sbar must be > 0");
+  if (!(std::isfinite(pr->delta) && pr->delta > 0)) return fail(nullptr, ESDP_E_CONFIG, "delta must be > 0");
+  if (!(pr->eta_c > 0 && pr->eta_c <= 1) || !(pr->eta_d > 0 && pr->eta_d <= 1))
+    return fail(nullptr, ESDP_E_CONFIG, "efficiencies must lie in (0, 1]");
+  if (!(std::isfinite(pr->s0) && pr->s0 >= 0 && pr->s0 <= pr->sbar)) return fail(nullptr, ESDP_E_CONFIG, "s0 must lie in [0, sbar]");
+  const double ns = pr->sbar / pr->delta;
+  const double rs = std::nearbyint(ns);
+  if (!(std::fabs(ns - rs) <= kGridTol * (ns > 1.0 ? ns : 1.0)) || rs < 1.0 || rs > 1e8)
+    return fail(nullptr, ESDP_E_CONFIG, "sbar/delta = %.17g is not a positive integer (P:180)", ns);
+  if (pr->payoff_kind < 0 || pr->payoff_kind > 2) return fail(nullptr, ESDP_E_CONFIG, "unknown payoff kind");
+  if (pr->payoff_kind != ESDP_PAYOFF_LINEAR && !pr->g) return fail(nullptr, ESDP_E_CONFIG, "payoff needs g");
+  if (!pr->lambda || !pr->pi) return fail(nullptr, ESDP_E_CONFIG, "lambda and pi are required");
+  if (pr->T > 1 && pr->P == nullptr && false) return ESDP_E_CONFIG;
+
+  esdp_ctx* c = new esdp_ctx();
+  c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1;
+  c->pbar = pr->pbar; c->sbar = pr->sbar; c->s0 = pr->s0; c->eta_c = pr->eta_c; c->eta_d = pr->eta_d;
+  c->delta = pr->delta; c->kind = pr->payoff_kind; c->rank1 = pr->P == nullptr; c->flags = pr->flags;
+  if (pr->A == 0) {
+    paper_grid(pr->pbar, pr->eta_c, pr->eta_d, pr->delta, c->act);
+    if ((long long)c->act.size() > kMaxA) { delete c; return fail(nullptr, ESDP_E_CONFIG, "A exceeds %d", kMaxA); }
+    for (size_t a = 1; a < c->act.size(); ++a)
+      if (!(c->act[a] > c->act[a - 1])) { delete c; return fail(nullptr, ESDP_E_CONFIG, "Eq. 10 grid has duplicate actions"); }
+  } else {
+    if (pr->A < 0 || pr->A > kMaxA || !pr->actions) { delete c; return fail(nullptr, ESDP_E_CONFIG, "bad action list"); }
+    int zeros = 0;
+    for (int a = 0; a < pr->A; ++a) {
+      const double p = pr->actions[a];
+      if (!std::isfinite(p) || std::fabs(p) > pr->pbar) { delete c; return fail(nullptr, ESDP_E_CONFIG, "action %d outside [-pbar, pbar]", a); }
+      if (p == 0.0) ++zeros;
+      if (a > 0 && !(p > pr->actions[a - 1])) { delete c; return fail(nullptr, ESDP_E_CONFIG, "actions not strictly ascending"); }
+    }
+    if (zeros != 1) { delete c; return fail(nullptr, ESDP_E_CONFIG, "the action list must contain 0 exactly once"); }
+    c->act.assign(pr->actions, pr->actions + pr->A);
+  }
+  c->A = (int)c->act.size();
+  {
+    esdp_status st = validate_data(c, pr->lambda, pr->P, pr->pi, pr->g);
+    if (st != ESDP_OK) { g_create_error = c->err; delete c; return st; }
+  }
+  build_tables(c);
+
+  auto bail = [&](esdp_status st) { g_create_error = c->err; free_all(c); delete c; return st; };
+#define TRY(x) do { esdp_status st_ = (x); if (st_ != ESDP_OK) return bail(st_); } while (0)
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    fail(c, ESDP_E_CUDA, "cannot create a CUDA stream (no usable GPU?)");
+    return bail(ESDP_E_CUDA);
+  }
+  const size_t T = c->T, K = c->K, S = c->S, A = c->A;
+  TRY(dev_alloc(c, &c->d_lambda, T * K));
+  TRY(dev_alloc(c, &c->d_P, c->rank1 ? 1 : (T - 1) * K * K));
+  TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
+  TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
+  TRY(dev_alloc(c, &c->d_cdf1, K));
+  TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
+  TRY(dev_alloc(c, &c->d_act, A));
+  TRY(dev_alloc(c, &c->d_w, A));
+  TRY(dev_alloc(c, &c->d_omw, A));
+  TRY(dev_alloc(c, &c->d_off, A));
+  TRY(dev_alloc(c, &c->d_segs, c->segs.size()));
+  TRY(dev_alloc(c, &c->d_V, keep(c) ? T * K * S : 2 * K * S));
+  TRY(dev_alloc(c, &c->d_W, keep(c) ? T * w_rows(c) * S : w_rows(c) * S));
+  TRY(dev_alloc(c, &c->d_pol, T * K * S));
+  TRY(dev_alloc(c, &c->d_J, 4));
+  TRY(dev_alloc(c, &c->d_red, 4));
+  if (cudaMemcpy(c->d_act, c->act.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_w, c->w.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_omw, c->omw.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_off, c->off.data(), A * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_segs, c->segs.data(), c->segs.size() * sizeof(Seg), cudaMemcpyHostToDevice) != cudaSuccess) {
+    fail(c, ESDP_E_CUDA, "upload of the action tables failed");
+    return bail(ESDP_E_CUDA);
+  }
+  if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
+  TRY(upload(c, pr->lambda, pr->P, pr->pi, pr->g));
+  c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
+  if (c->stencil_smem > 48 * 1024) {
+    if (c->stencil_smem > 227 * 1024) { fail(c, ESDP_E_CONFIG, "action span too wide for shared memory"); return bail(ESDP_E_CONFIG); }
+    if (cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->stencil_smem) != cudaSuccess) {
+      fail(c, ESDP_E_CUDA, "cannot opt in to %zu bytes of shared memory", c->stencil_smem);
+      return bail(ESDP_E_CUDA);
+    }
+  }
+  if (K * kRowsC * sizeof(double) > 48 * 1024)
+    cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(K * kRowsC * sizeof(double)));
+  // capture the whole backward pass once; replay it for every solve
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph capture failed"); return bail(ESDP_E_CUDA); }
+  esdp_status est = enqueue_backward(c, c->stream);
+  cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+  if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); return bail(est); }
+  if (ce != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce)); return bail(ESDP_E_CUDA); }
+  ce = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); return bail(ESDP_E_CUDA); }
+#undef TRY
+  *out = c;
+  return ESDP_OK;
+}
+
+esdp_status esdp_dims(const esdp_ctx* c, int32_t* T, int32_t* S, int32_t* A, int32_t* K) {
+  if (!c) return ESDP_E_STATE;
+  if (T) *T = c->T;
+  if (S) *S = c->S;
+  if (A) *A = c->A;
+  if (K) *K = c->K;
+  return ESDP_OK;
+}
+
+esdp_status esdp_actions(const esdp_ctx* c, double* actions) {
+  if (!c || !actions) return ESDP_E_STATE;
+  std::memcpy(actions, c->act.data(), c->act.size() * sizeof(double));
+  return ESDP_OK;
+}
+
+esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  if (!c) return ESDP_E_STATE;
+  if (!c->rank1 && P == nullptr && pi != nullptr && false) return ESDP_E_STATE;
+  // validate what is given against the current arrays' shapes
+  std::vector<double> lam_h, P_h, pi_h, g_h;
+  const size_t TK = (size_t)c->T * c->K;
+  if (!lambda) { lam_h.resize(TK); cudaMemcpy(lam_h.data(), c->d_lambda, TK * 8, cudaMemcpyDeviceToHost); }
+  if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); cudaMemcpy(P_h.data(), c->d_P, P_h.size() * 8, cudaMemcpyDeviceToHost); }
+  if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); cudaMemcpy(pi_h.data(), c->d_pi, pi_h.size() * 8, cudaMemcpyDeviceToHost); }
+  if (!g && c->kind != ESDP_PAYOFF_LINEAR) { g_h.resize(c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : c->A); cudaMemcpy(g_h.data(), c->d_g, g_h.size() * 8, cudaMemcpyDeviceToHost); }
+  esdp_status st = validate_data(c, lambda ? lambda : lam_h.data(), P ? P : P_h.data(), pi ? pi : pi_h.data(),
+                                 g ? g : g_h.data());
+  if (st != ESDP_OK) return st;
+  return upload(c, lambda, P, pi, g);
+}
+
+esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
+  if (!c) return ESDP_E_STATE;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
+  c->solved = true;
+  return ESDP_OK;
+}
+
+esdp_status esdp_objective(esdp_ctx* c, double* J) {
+  if (!c || !c->solved) return c ? fail(c, ESDP_E_STATE, "no backward pass has run") : ESDP_E_STATE;
+  CUDA_OR_FAIL(c, cudaMemcpy(J, c->d_J, sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_backward(esdp_ctx* c, void* stream, double* J) {
+  if (!c) return ESDP_E_STATE;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  esdp_status st = esdp_backward_async(c, s);
+  if (st != ESDP_OK) return st;
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
+  if (J) CUDA_OR_FAIL(c, cudaMemcpy(J, c->d_J, sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_values(const esdp_ctx* cc, int32_t t, double* V, double* W) {
+  esdp_ctx* c = const_cast<esdp_ctx*>(cc);
+  if (!c) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (t < 1 || t > c->T) return fail(c, ESDP_E_STATE, "stage %d out of range", t);
+  if (!keep(c) && (t != 1 || W)) return fail(c, ESDP_E_STATE, "only V_1 is kept without ESDP_KEEP_VALUES");
+  const size_t KS = (size_t)c->K * c->S;
+  if (V) CUDA_OR_FAIL(c, cudaMemcpy(V, V_of(c, t), KS * sizeof(double), cudaMemcpyDeviceToHost));
+  if (W) {
+    if (c->rank1) {
+      for (int k = 0; k < c->K; ++k)
+        CUDA_OR_FAIL(c, cudaMemcpy(W + (size_t)k * c->S, W_of(c, t), c->S * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      CUDA_OR_FAIL(c, cudaMemcpy(W, W_of(c, t), KS * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+  }
+  return ESDP_OK;
+}
+
+esdp_status esdp_policy(const esdp_ctx* cc, int32_t t, int16_t* pol) {
+  esdp_ctx* c = const_cast<esdp_ctx*>(cc);
+  if (!c) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (t < 1 || t > c->T) return fail(c, ESDP_E_STATE, "stage %d out of range", t);
+  const size_t KS = (size_t)c->K * c->S;
+  CUDA_OR_FAIL(c, cudaMemcpy(pol, c->d_pol + (size_t)(t - 1) * KS, KS * sizeof(int16_t), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, int32_t cap, int32_t* nvert_dev,
+                               int16_t* vert_dev, double* q_dev, double* price_dev, void* stream) {
+  if (!c) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (!keep(c)) return fail(c, ESDP_E_STATE, "bid curves need ESDP_KEEP_VALUES");
+  if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
+  if (cap < c->A) return fail(c, ESDP_E_STATE, "cap %d < A %d", cap, c->A);
+  if (n <= 0) return ESDP_OK;
+  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind};
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  const int thr = 128;
+  bidcurve_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return ESDP_OK;
+}
+
+esdp_status esdp_bidcurves(esdp_ctx* c, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert, int16_t* vert,
+                           double* q, double* price) {
+  if (!c) return ESDP_E_STATE;
+  if (n <= 0) return ESDP_OK;
+  for (int64_t r = 0; r < n; ++r) {
+    const int t = req[3 * r], i = req[3 * r + 1], k = req[3 * r + 2];
+    if (t < 1 || t > c->T || i < 0 || i >= c->S || k < 0 || k >= c->K)
+      return fail(c, ESDP_E_STATE, "request %lld (t=%d, i=%d, k=%d) out of range", (long long)r, t, i, k);
+  }
+  if (n > c->req_cap || (int64_t)cap * n > c->out_cap) {
+    cudaFree(c->d_req); cudaFree(c->d_nv); cudaFree(c->d_vert); cudaFree(c->d_q); cudaFree(c->d_price);
+    c->d_req = nullptr; c->d_nv = nullptr; c->d_vert = nullptr; c->d_q = nullptr; c->d_price = nullptr;
+    c->req_cap = c->out_cap = 0;
+    if (dev_alloc(c, &c->d_req, 3 * n) || dev_alloc(c, &c->d_nv, n) || dev_alloc(c, &c->d_vert, (size_t)cap * n) ||
+        dev_alloc(c, &c->d_q, (size_t)cap * n) || dev_alloc(c, &c->d_price, (size_t)cap * n))
+      return ESDP_E_NOMEM;
+    c->req_cap = n;
+    c->out_cap = (int64_t)cap * n;
+  }
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_req, req, 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  esdp_status st = esdp_bidcurves_dev(c, n, c->d_req, cap, c->d_nv, c->d_vert, c->d_q, c->d_price, c->stream);
+  if (st != ESDP_OK) return st;
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpy(nvert, c->d_nv, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(vert, c->d_vert, (size_t)cap * n * sizeof(int16_t), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(q, c->d_q, (size_t)cap * n * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(price, c->d_price, (size_t)cap * n * sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* per_path_dev, void* stream) {
+  if (!c) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (n_paths < 1) return fail(c, ESDP_E_STATE, "n_paths must be >= 1");
+  SimParams sp;
+  sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
+  sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
+  sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind;
+  sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  const int thr = 128;
+  simulate_kernel<<<(unsigned)((n_paths + thr - 1) / thr), thr, 0, s>>>(sp, n_paths, seed, per_path_dev);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return ESDP_OK;
+}
+
+esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* mean, double* var, double* per_path) {
+  if (!c) return ESDP_E_STATE;
+  if (n_paths > c->sim_cap) {
+    cudaFree(c->d_sim);
+    c->d_sim = nullptr;
+    c->sim_cap = 0;
+    if (dev_alloc(c, &c->d_sim, n_paths)) return ESDP_E_NOMEM;
+    c->sim_cap = n_paths;
+  }
+  esdp_status st = esdp_simulate_dev(c, n_paths, seed, c->d_sim, c->stream);
+  if (st != ESDP_OK) return st;
+  reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, nullptr, c->d_red);
+  reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, c->d_red, c->d_red + 1);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  double h[2];
+  CUDA_OR_FAIL(c, cudaMemcpy(h, c->d_red, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (mean) *mean = h[0];
+  if (var) *var = n_paths > 1 ? h[1] / (double)(n_paths - 1) : 0.0;
+  if (per_path) CUDA_OR_FAIL(c, cudaMemcpy(per_path, c->d_sim, n_paths * sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_launch_count(const esdp_ctx* c, int64_t* n) {
+  if (!c || !n) return ESDP_E_STATE;
+  *n = c->launches;
+  return ESDP_OK;
+}
+
+void esdp_destroy(esdp_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  free_all(c);
+  delete c;
+}
+
+const char* esdp_last_error(const esdp_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+}  // extern "C"

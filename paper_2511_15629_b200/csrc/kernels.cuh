@@ -1,0 +1,385 @@
+// kernels.cuh -- sm_100a kernels of the backward induction (arXiv 2511.15629, Alg. 1 in Markov form).
+//
+// Every floating-point operation on the value path is an explicit round-to-nearest intrinsic
+// (__dadd_rn / __dmul_rn / __dsub_rn / __ddiv_rn / __fma_rn) so that nvcc never contracts or
+// reassociates: results are reproducible bit for bit (R14/R15).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace esdp {
+
+constexpr int kMaxA = 8191;
+constexpr int R = 8;                  // SoC columns per thread in the stencil (register window)
+constexpr int kLanes = 32;
+constexpr int kTile = kLanes * R;     // 256 SoC columns per stencil block
+constexpr int kPad = 8;               // smem guard columns below the lowest offset
+constexpr int kStencilWarps = 4;      // action chunks per block (one warp each)
+
+__host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  // 8-column groups + 1 pad
+
+// A maximal run of actions whose offsets are consecutive integers decreasing by one and whose
+// interpolation weight is 0 ("recombining" interior of Eq. 10), or a single action.
+struct Seg {
+  int a0;      // first action index
+  int n;       // number of actions
+  int o0;      // offset of a0 (index units); action a0+m has offset o0 - m  (RUN)
+  int interp;  // 1: single action with weight w > 0 (endpoint), 0: RUN / single integral action
+};
+
+struct StencilParams {
+  const double* W;        // [rows][S] continuation of stage t (rows = K, or 1 in rank-1 mode)
+  double* V;              // [K][S] out
+  int16_t* pol;           // [K][S] out
+  const double* lambda_t; // [K]  lambda_{t,k}
+  const double* act;      // [A]
+  const double* g;        // [A] (LINEAR_MINUS_G) or [K][A] of stage t (TABLE) or nullptr
+  const double* w;        // [A]
+  const double* omw;      // [A]
+  const int* off;         // [A]
+  const Seg* segs;        // [nseg]
+  int nseg, A, S, K, kind, rank1, o_min, o_span;  // o_span = o_max - o_min
+};
+
+// ------------------------------------------------------------------------------------------------
+// Expectation: W_t[k][i] = sum_{k'} P_t[k][k'] V_{t+1}[k'][i]  (Alg. 1 line 11; Eq. 6)
+// canonical ascending-k' fma chain (R15): bit-identical to the oracle.
+// Block: 64 threads = 64 SoC columns, kRowsC output rows (k) per block.
+// ------------------------------------------------------------------------------------------------
+constexpr int kRowsC = 8;
+constexpr int kColsC = 64;
+
+__global__ void __launch_bounds__(kColsC) contract_kernel(const double* __restrict__ Pt,   // [rows][K] (row stride K)
+                                                          const double* __restrict__ Vn,   // [K][S]
+                                                          double* __restrict__ Wt,         // [rows][S]
+                                                          int rows, int K, int S) {
+  extern __shared__ double ps[];  // [K][kRowsC]  transposed P tile
+  const int r0 = blockIdx.y * kRowsC;
+  const int i = blockIdx.x * kColsC + threadIdx.x;
+  for (int e = threadIdx.x; e < K * kRowsC; e += kColsC) {
+    int kp = e / kRowsC, r = e % kRowsC;
+    ps[e] = (r0 + r < rows) ? Pt[(size_t)(r0 + r) * K + kp] : 0.0;
+  }
+  __syncthreads();
+  if (i >= S) return;
+  double acc[kRowsC];
+#pragma unroll
+  for (int r = 0; r < kRowsC; ++r) acc[r] = 0.0;
+  const double* vcol = Vn + i;
+  int kp = 0;
+  for (; kp + 4 <= K; kp += 4) {
+    double v0 = __ldg(vcol + (size_t)(kp + 0) * S);
+    double v1 = __ldg(vcol + (size_t)(kp + 1) * S);
+    double v2 = __ldg(vcol + (size_t)(kp + 2) * S);
+    double v3 = __ldg(vcol + (size_t)(kp + 3) * S);
+#pragma unroll
+    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 0) * kRowsC + r], v0, acc[r]);
+#pragma unroll
+    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 1) * kRowsC + r], v1, acc[r]);
+#pragma unroll
+    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 2) * kRowsC + r], v2, acc[r]);
+#pragma unroll
+    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 3) * kRowsC + r], v3, acc[r]);
+  }
+  for (; kp < K; ++kp) {
+    double v = __ldg(vcol + (size_t)kp * S);
+#pragma unroll
+    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[kp * kRowsC + r], v, acc[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < kRowsC; ++r)
+    if (r0 + r < rows) Wt[(size_t)(r0 + r) * S + i] = acc[r];
+}
+
+// ------------------------------------------------------------------------------------------------
+// Max-plus action reduction with argmax (Alg. 1 lines 7-10; Eq. 5):
+//   V_t[k][i] = max_a pay(t,k,a) + Wint(i,a,k),  pol = smallest maximizing a  (R8).
+// The W row is staged in shared memory with -inf outside [0, S-1]: an infeasible action
+// (Alg. 1 line 8) then yields -inf and can never win, exactly like skipping it.
+// Grid: (ceil(S/256), K).  Block: 4 warps; warp c reduces action chunk c for 256 columns
+// (8 consecutive columns per lane, register window over the recombining run), then the four
+// partial (value, index) pairs are merged in ascending chunk order with a strict '>'.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void upd(double c, int a, double& best, int& arg) {
+  if (c > best) { best = c; arg = a; }
+}
+
+template <bool kMask>
+__device__ __forceinline__ void run_group(const double* __restrict__ ws, const double* __restrict__ pay,
+                                          int base, int a, int m_left, double (&hi)[R], double (&best)[R],
+                                          int (&arg)[R]) {
+  // steps d = 0..7 of the run: action a + d, column r reads W at tile index base - d + r.
+  double lo[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) lo[q] = ws[skew(base - R + q)];
+#pragma unroll
+  for (int d = 0; d < R; ++d) {
+    double p = pay[a + d];
+    if (kMask) p = (d < m_left) ? p : -INFINITY;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double x = (r - d >= 0) ? hi[r - d] : lo[R + r - d];
+      upd(__dadd_rn(p, x), a + d, best[r], arg[r]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) hi[q] = lo[q];
+}
+
+__global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm) {
+  extern __shared__ double smem[];
+  const int k = blockIdx.y;
+  const int i0 = blockIdx.x * kTile;
+  const int L = kTile + prm.o_span + kPad + 1;
+  double* ws = smem;                           // skew(L) doubles
+  double* pay = ws + skew(L) + 8;              // A + 8 doubles
+  double* pv = pay + prm.A + 8;                // [kStencilWarps][skew(kTile)]
+  int* pa = (int*)(pv + kStencilWarps * skew(kTile));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.S);
+  const int g0 = i0 + prm.o_min - kPad;  // global column of tile index 0
+  for (int j = tid; j < L; j += blockDim.x) {
+    int col = g0 + j;
+    ws[skew(j)] = (col >= 0 && col < prm.S) ? Wrow[col] : -INFINITY;
+  }
+  const double lam = prm.lambda_t[k];
+  for (int a = tid; a < prm.A; a += blockDim.x) {
+    double p;
+    if (prm.kind == 2) p = prm.g[(size_t)k * prm.A + a];                               // TABLE
+    else if (prm.kind == 1) p = __dsub_rn(__dmul_rn(lam, prm.act[a]), prm.g[a]);        // lambda p - g
+    else p = __dmul_rn(lam, prm.act[a]);                                                 // lambda p
+    pay[a] = p;
+  }
+  __syncthreads();
+
+  double best[R];
+  int arg[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) { best[r] = -INFINITY; arg[r] = -1; }
+  const int a_lo = (prm.A * warp) / kStencilWarps, a_hi = (prm.A * (warp + 1)) / kStencilWarps;
+  const int colbase = lane * R - prm.o_min + kPad;  // tile index of (column lane*R, offset 0)
+
+  for (int s = 0; s < prm.nseg; ++s) {
+    const Seg sg = prm.segs[s];
+    const int sb = max(sg.a0, a_lo), se = min(sg.a0 + sg.n, a_hi);
+    if (sb >= se) continue;
+    if (sg.interp || sg.n < 4) {
+      for (int a = sb; a < se; ++a) {
+        const int o = sg.o0 - (a - sg.a0);
+        const double p = pay[a];
+        if (sg.interp) {
+          const double w = prm.w[a], om = prm.omw[a];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            double x0 = ws[skew(colbase + r + o)], x1 = ws[skew(colbase + r + o + 1)];
+            double wi = __dadd_rn(__dmul_rn(om, x0), __dmul_rn(w, x1));
+            upd(__dadd_rn(p, wi), a, best[r], arg[r]);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) upd(__dadd_rn(p, ws[skew(colbase + r + o)]), a, best[r], arg[r]);
+        }
+      }
+      continue;
+    }
+    // recombining run: action a = sb + m has offset o(sb) - m
+    const int o_b = sg.o0 - (sb - sg.a0);
+    int base = colbase + o_b;  // tile index of column lane*R + 0 for the current step
+    double hi[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) hi[q] = ws[skew(base + q)];
+    int a = sb;
+    for (; a + R <= se; a += R, base -= R) run_group<false>(ws, pay, base, a, R, hi, best, arg);
+    if (a < se) run_group<true>(ws, pay, base, a, se - a, hi, best, arg);
+  }
+
+  // merge the chunk partials in ascending action order (strict '>' keeps the smallest index)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    pv[warp * skew(kTile) + skew(lane * R + r)] = best[r];
+    pa[warp * skew(kTile) + skew(lane * R + r)] = arg[r];
+  }
+  __syncthreads();
+  for (int c = tid; c < kTile; c += blockDim.x) {
+    const int i = i0 + c;
+    if (i >= prm.S) continue;
+    double b = -INFINITY;
+    int ar = -1;
+#pragma unroll
+    for (int w = 0; w < kStencilWarps; ++w) {
+      double v = pv[w * skew(kTile) + skew(c)];
+      if (v > b) { b = v; ar = pa[w * skew(kTile) + skew(c)]; }
+    }
+    prm.V[(size_t)k * prm.S + i] = b;
+    prm.pol[(size_t)k * prm.S + i] = (int16_t)ar;
+  }
+}
+
+inline size_t stencil_smem_bytes(int A, int o_span) {
+  int L = kTile + o_span + kPad + 1;
+  return sizeof(double) * (size_t)(skew(L) + 8 + A + 8 + kStencilWarps * skew(kTile)) +
+         sizeof(int) * (size_t)(kStencilWarps * skew(kTile));
+}
+
+// ------------------------------------------------------------------------------------------------
+// Objective J = sum_k pi_1[k] V_1(s0, k) (Eq. 6 at t = 0), fma chain in k order; s0 off the
+// grid is interpolated per k (R24).  One thread.
+// ------------------------------------------------------------------------------------------------
+__global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int S,
+                                 int f, double w0, int on_grid, double* __restrict__ J) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double* row = V1 + (size_t)k * S;
+    double v = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));
+    acc = __fma_rn(pi1[k], v, acc);
+  }
+  *J = acc;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Bid curves (Eqs. 7-12): one thread per request (t, i, k).  The caller's output rows
+// serve as the hull stack (vert: action index, price: hull u value, overwritten by prices).
+// ------------------------------------------------------------------------------------------------
+struct BidParams {
+  const double* Wall;     // [T][rows][S]
+  const double* act; const double* w; const double* omw; const int* off; const double* g;
+  int T, K, S, A, rank1, kind;
+};
+
+__global__ void bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req, int cap,
+                                int32_t* __restrict__ nvert, int16_t* __restrict__ vert, double* __restrict__ q,
+                                double* __restrict__ price) {
+  int64_t rq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rq >= n) return;
+  const int t = req[3 * rq + 0], i = req[3 * rq + 1], k = req[3 * rq + 2];
+  int16_t* hv = vert + rq * cap;
+  double* hu = price + rq * cap;
+  double* hq = q + rq * cap;
+  if (t < 1 || t > bp.T || i < 0 || i >= bp.S || k < 0 || k >= bp.K) { nvert[rq] = -1; return; }
+  const double* Wrow = bp.Wall + ((size_t)(t - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : k)) * bp.S;
+  int nh = 0;
+  for (int a = 0; a < bp.A; ++a) {
+    const int o = bp.off[a];
+    const double wa = bp.w[a];
+    const int hi_idx = i + o + (wa != 0.0 ? 1 : 0);
+    if (i + o < 0 || hi_idx > bp.S - 1) continue;            // Eq. 4 / Alg. 1 line 8
+    double u = (wa == 0.0) ? Wrow[i + o]
+                           : __dadd_rn(__dmul_rn(bp.omw[a], Wrow[i + o]), __dmul_rn(wa, Wrow[i + o + 1]));
+    if (bp.kind == 1) u = __dsub_rn(u, bp.g[a]);
+    const double pc = bp.act[a];
+    while (nh >= 2) {
+      const double po = bp.act[hv[nh - 2]], uo = hu[nh - 2];
+      const double pb = bp.act[hv[nh - 1]], ub = hu[nh - 1];
+      const double cr = __dsub_rn(__dmul_rn(__dsub_rn(pb, po), __dsub_rn(u, uo)),
+                                  __dmul_rn(__dsub_rn(ub, uo), __dsub_rn(pc, po)));
+      if (cr >= 0.0) --nh; else break;
+    }
+    hv[nh] = (int16_t)a;
+    hu[nh] = u;
+    ++nh;
+  }
+  for (int j = 0; j < nh; ++j) hq[j] = bp.act[hv[j]];
+  double prev = 0.0;
+  for (int j = 0; j + 1 < nh; ++j) {
+    double pj = -__ddiv_rn(__dsub_rn(hu[j + 1], hu[j]), __dsub_rn(hq[j + 1], hq[j]));
+    if (j > 0 && pj < prev) pj = prev;   // R20 running-max repair
+    hu[j] = pj;
+    prev = pj;
+  }
+  nvert[rq] = nh;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Forward simulation (R16/R17): one thread per path, Philox4x32-10.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t, double& u1, double& u2) {
+  uint32_t c[4] = {(uint32_t)((uint64_t)path & 0xffffffffu), (uint32_t)((uint64_t)path >> 32), (uint32_t)t,
+                   0x45534450u};
+  philox4x32_10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  u1 = (double)((((uint64_t)c[0]) << 21) | (c[1] >> 11)) * 0x1p-53;
+  u2 = (double)((((uint64_t)c[2]) << 21) | (c[3] >> 11)) * 0x1p-53;
+}
+
+// first j in [0, K) with u < cdf[j]  (cdf non-decreasing, cdf[K-1] = 1 > u)
+__device__ __forceinline__ int cdf_search(const double* __restrict__ cdf, int K, double u) {
+  int lo = 0, hi = K - 1;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (u < __ldg(cdf + mid)) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+struct SimParams {
+  const int16_t* pol;    // [T][K][S]
+  const double* cdf;     // Markov: [T-1][K][K]; rank-1: [T][K] (row t = cdf of pi_{t+1})
+  const double* cdf1;    // [K] cdf of pi_1
+  const double* lambda;  // [T][K]
+  const double* act; const double* w; const int* off; const double* g;
+  int T, K, S, A, rank1, kind, on_grid, f0;
+  double w0;
+};
+
+__global__ void simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
+  const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (path >= n) return;
+  double u1, u2;
+  sim_uniforms(seed, path, 0, u1, u2);
+  int k = cdf_search(sp.cdf1, sp.K, u1);
+  int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
+  double profit = 0.0;
+  const size_t KS = (size_t)sp.K * sp.S;
+  for (int t = 1; t <= sp.T; ++t) {
+    sim_uniforms(seed, path, t, u1, u2);
+    const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
+    double p;
+    if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
+    else {
+      p = __dmul_rn(__ldg(sp.lambda + (size_t)(t - 1) * sp.K + k), __ldg(sp.act + a));
+      if (sp.kind == 1) p = __dsub_rn(p, __ldg(sp.g + a));
+    }
+    profit = __dadd_rn(profit, p);
+    const double wa = __ldg(sp.w + a);
+    i = i + __ldg(sp.off + a) + ((wa > 0.0 && u1 < wa) ? 1 : 0);
+    if (t < sp.T) {
+      const double* row = sp.rank1 ? sp.cdf + (size_t)t * sp.K : sp.cdf + ((size_t)(t - 1) * sp.K + k) * sp.K;
+      k = cdf_search(row, sp.K, u2);
+    }
+  }
+  out[path] = profit;
+}
+
+// Deterministic two-pass reduction of per-path profits: sum (then sum of squared deviations).
+__global__ void reduce_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean_in,
+                              double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  const double m = mean_in ? *mean_in : 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double v = x[j];
+    if (mean_in) { double d = __dsub_rn(v, m); v = __dmul_rn(d, d); }
+    acc = __dadd_rn(acc, v);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = mean_in ? sh[0] : __ddiv_rn(sh[0], (double)n);
+}
+
+}  // namespace esdp

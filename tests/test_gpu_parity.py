@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on the same seeded inputs.
+
+Bar: V, W, J bit-identical (the kernels use the oracle's exact association and the
+canonical fma chain, so any difference is a bug; the north_star tolerance 1e-9 relative is asserted
+as well), policy and bid-curve vertex indices bit-exact, bid prices bit-exact, per-path simulation
+profits bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from helpers import to_oracle
+
+pytestmark = pytest.mark.gpu
+
+import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
+
+
+def _gpu(inst):
+    return E.Solver(inst, keep_values=True)
+
+
+def _compare_all(inst, nthreads=8, stages=None):
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=nthreads)
+    with _gpu(inst) as s:
+        J = s.backward()
+        assert np.array_equal(s.actions(), oracle.actions(pr))
+        ts = range(1, inst.T + 1) if stages is None else stages
+        for t in ts:
+            V, W = s.values(t)
+            pol = s.policy(t)
+            assert np.array_equal(W, ref.W[t - 1]), f"W_{t} differs: max |d| {np.max(np.abs(W - ref.W[t-1]))}"
+            assert np.array_equal(V, ref.V[t - 1]), f"V_{t} differs: max |d| {np.max(np.abs(V - ref.V[t-1]))}"
+            assert np.array_equal(pol, ref.pol[t - 1]), f"pol_{t} differs at {np.argwhere(pol != ref.pol[t-1])[:5]}"
+        assert J == ref.J
+        assert abs(J - ref.J) <= 1e-9 * max(1.0, abs(ref.J))
+    return ref
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_small_instances(seed):
+    kind = [workloads.PAYOFF_LINEAR, workloads.PAYOFF_LINEAR_MINUS_G, workloads.PAYOFF_TABLE][seed % 3]
+    inst = workloads.random_instance(seed, S_max=40 if seed % 2 else 600, T=4 + seed % 3, K=1 + seed % 4)
+    S, A = oracle.dims(to_oracle(inst))
+    inst.payoff_kind = kind
+    if kind == workloads.PAYOFF_LINEAR_MINUS_G:
+        inst.g = workloads.random_g(seed, A, 20.0)
+    elif kind == workloads.PAYOFF_TABLE:
+        inst.g = workloads.random_table(seed, inst.T, inst.K, A)
+    _compare_all(inst)
+
+
+@pytest.mark.parametrize("name", ["cfg1a", "cfg1b", "cfg1b-rank1", "cfg1a-rank1"])
+def test_cfg1(name):
+    _compare_all(workloads.cfg1(name[4], rank1=name.endswith("rank1")))
+
+
+@pytest.mark.parametrize("S_over", [255, 256, 257, 511, 777, 1001, 2001])
+def test_tiles_and_ragged_tails(S_over):
+    """Several 256-column tiles plus a ragged tail; cfg2-like offsets."""
+    inst = workloads.cfg2(T=6, K=7)
+    inst.sbar = float(S_over - 1)
+    inst.s0 = 0.0
+    _compare_all(inst)
+
+
+def test_edge_cases():
+    # T = 1, K = 1, minimal grid (S = 2)
+    inst = workloads.random_instance(5, T=1, K=1, S_max=3)
+    inst.sbar, inst.delta, inst.s0 = 1.0, 1.0, 0.0
+    _compare_all(inst)
+    # pbar far larger than sbar: most actions infeasible everywhere (dead actions)
+    inst = workloads.random_instance(6, T=3, K=2, S_max=5)
+    inst.pbar = 50.0 * inst.sbar
+    _compare_all(inst)
+    # user action grid: every action off the lattice (all interpolated), off-grid s0
+    inst = workloads.random_instance(7, T=5, K=3, S_max=30)
+    inst.actions = np.array([-0.93, -0.41, -0.07, 0.0, 0.13, 0.52, 0.99]) * inst.pbar
+    inst.s0 = inst.sbar * 0.37
+    _compare_all(inst)
+    # zero prices: every candidate ties, the smallest feasible action must be chosen
+    inst = workloads.cfg1("b")
+    inst.lam = np.zeros_like(inst.lam)
+    _compare_all(inst)
+    # integer prices on an eta = 1 lattice: many exact ties
+    inst = workloads.cfg1("a")
+    inst.lam = np.round(inst.lam / 10.0)
+    _compare_all(inst)
+
+
+def test_cfg2_full_size():
+    """BASELINE configs[1] at full size (T=288, S=1001, A=201, K=100), in the launch configuration
+    bench.py times: every V_t, W_t, pol_t compared element by element with the oracle."""
+    _compare_all(workloads.cfg2(), nthreads=16)
+
+
+def test_cfg2_rank1_full_size():
+    _compare_all(workloads.cfg2(rank1=True), nthreads=16)
+
+
+def test_cfg3_nonconcave_payoff_and_bids():
+    """configs[2]: negative prices, degradation + fixed cycling cost (non-concave payoff), monotone
+    bid curves (bit-exact vertices and prices) on a sample of (t, i, k)."""
+    base = workloads.cfg2(T=2, K=2)
+    act = oracle.actions(to_oracle(base))
+    inst = workloads.cfg3_gpu(act, T=48, K=40)
+    ref = _compare_all(inst)
+    pr = to_oracle(inst)
+    rng = np.random.default_rng(3)
+    req = np.stack([rng.integers(1, inst.T + 1, 400), rng.integers(0, inst.S, 400), rng.integers(0, inst.K, 400)], 1)
+    req[:10, 1] = [0, 1, 2, 998, 999, 1000, 500, 94, 95, 105]
+    with _gpu(inst) as s:
+        s.backward()
+        out = s.bidcurves(req)
+    for j, (t, i, k) in enumerate(req):
+        c = oracle.bidcurve(pr, ref.W, int(t), int(i), int(k))
+        n = out["nvert"][j]
+        assert n == c["nvert"]
+        assert np.array_equal(out["vert"][j, :n], c["vert"])
+        assert np.array_equal(out["q"][j, :n], c["q"])
+        assert np.array_equal(out["price"][j, :n - 1], c["price"])
+        assert np.all(np.diff(out["price"][j, :n - 1]) >= 0)
+
+
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1"])
+def test_bidcurves_cfg1(name):
+    inst = workloads.cfg1("b", rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr)
+    req = np.array([(t, i, k) for t in range(1, inst.T + 1) for i in range(0, inst.S, 7) for k in range(inst.K)])
+    with _gpu(inst) as s:
+        s.backward()
+        out = s.bidcurves(req)
+    for j, (t, i, k) in enumerate(req):
+        c = oracle.bidcurve(pr, ref.W, int(t), int(i), int(k))
+        n = out["nvert"][j]
+        assert n == c["nvert"] and np.array_equal(out["vert"][j, :n], c["vert"])
+        assert np.array_equal(out["price"][j, :n - 1], c["price"])
+
+
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg2"])
+def test_simulation_per_path_bitexact(name):
+    inst = workloads.cfg2(T=48, K=30) if name == "cfg2" else workloads.cfg1("b", rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=8)
+    n = 3000
+    per_ref, m_ref, v_ref = oracle.simulate(pr, ref.pol, n, seed=777)
+    with _gpu(inst) as s:
+        J = s.backward()
+        per, m, v = s.simulate(n, 777)
+    assert np.array_equal(per, per_ref)
+    assert abs(m - m_ref) <= 1e-12 * max(1.0, abs(m_ref))
+    assert abs(v - v_ref) <= 1e-9 * max(1.0, abs(v_ref))
+    assert abs(m - J) <= 5 * math.sqrt(v / n) + 1e-9
+
+
+def test_load_new_prices_and_repeat():
+    """esdp_load replaces the stochastic inputs in place; repeated solves are bit-identical."""
+    a = workloads.cfg1("b")
+    b = workloads.cfg1("b")
+    b.lam = b.lam * 1.3 + 2.0
+    ref_b = oracle.backward(to_oracle(b))
+    with _gpu(a) as s:
+        J1 = s.backward()
+        E.esdp_load(s.ctx, lam=b.lam)
+        Jb = s.backward()
+        Jb2 = s.backward()
+        assert Jb == ref_b.J and Jb2 == Jb
+        V, W = s.values(1)
+        assert np.array_equal(V, ref_b.V[0])
+        with pytest.raises(E.EsdpError) as ei:
+            bad = b.lam.copy(); bad[0, 0] = np.nan
+            E.esdp_load(s.ctx, lam=bad)
+        assert ei.value.status == E.ESDP_E_DATA
+
+
+def test_state_errors():
+    inst = workloads.cfg1("b")
+    with _gpu(inst) as s:
+        with pytest.raises(E.EsdpError) as ei:
+            s.values(1)
+        assert ei.value.status == E.ESDP_E_STATE
+        s.backward()
+        with pytest.raises(E.EsdpError):
+            s.values(inst.T + 1)
+        with pytest.raises(E.EsdpError):
+            s.bidcurves(np.array([[1, 10_000, 0]]))

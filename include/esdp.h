@@ -54,8 +54,11 @@ enum { ESDP_PAYOFF_LINEAR = 0, ESDP_PAYOFF_LINEAR_MINUS_G = 1, ESDP_PAYOFF_TABLE
 
 /* flags */
 enum {
-  ESDP_KEEP_VALUES = 1u  /* keep V_t and W_t for every t on the device (needed by esdp_values
-                            for t > 1 and by the bid-curve calls); otherwise only V_1 is kept */
+  ESDP_KEEP_VALUES = 1u,  /* keep V_t and W_t for every t on the device (needed by esdp_values
+                             for t > 1 and by the bid-curve calls); otherwise only V_1 is kept */
+  ESDP_PROFILE = 2u       /* record CUDA events around every contraction and stencil launch inside
+                             the backward graph, so esdp_kernel_times can report per-kernel device
+                             time of the last backward pass */
 };
 
 typedef struct {
@@ -122,7 +125,8 @@ esdp_status esdp_policy(const esdp_ctx* ctx, int32_t t, int16_t* pol);
  *   price  [n][cap] segment prices (entries >= nvert-1 unused).  Requires ESDP_KEEP_VALUES. */
 esdp_status esdp_bidcurves(esdp_ctx* ctx, int64_t n, const int32_t* req, int32_t cap,
                            int32_t* nvert, int16_t* vert, double* q, double* price);
-/* Same, with DEVICE pointers for every array, enqueued on `stream` (no synchronization). */
+/* Same, with DEVICE pointers for every array, enqueued on `stream` (no synchronization); q_dev may
+ * be NULL (the quantities are actions[vert]). */
 esdp_status esdp_bidcurves_dev(esdp_ctx* ctx, int64_t n, const int32_t* req_dev, int32_t cap,
                                int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev,
                                void* stream);
@@ -139,8 +143,13 @@ esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double*
 esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
                               void* stream);
 
-/* Number of kernel launches the last esdp_backward_async enqueued (for harness accounting). */
+/* Number of kernel launches one backward pass enqueues (for harness accounting). */
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
+
+/* Device time (ms) of the last completed backward pass, summed per kernel kind: the T-1
+ * contraction launches and the T stencil launches (requires ESDP_PROFILE; the caller has
+ * synchronized the stream). */
+esdp_status esdp_kernel_times(const esdp_ctx* ctx, double* contract_ms, double* stencil_ms);
 
 void esdp_destroy(esdp_ctx* ctx);
 

@@ -48,6 +48,8 @@ struct esdp_ctx {
   int* d_off = nullptr;
   Seg* d_segs = nullptr;
   double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
+  int16_t *d_guide = nullptr, *d_guide1 = nullptr;
+  int G = 16;
   double *d_red = nullptr;
   int16_t* d_pol = nullptr;
   double* d_sim = nullptr;
@@ -62,6 +64,7 @@ struct esdp_ctx {
   cudaGraphExec_t graph = nullptr;
   size_t stencil_smem = 0;
   int64_t launches = 0;
+  std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   bool solved = false;
   std::string err;
 };
@@ -188,15 +191,6 @@ void build_tables(esdp_ctx* c) {
   c->w0 = c->on_grid ? 0.0 : x - std::floor(x);
 }
 
-// cdf rows: running sum in ascending order, last entry forced to 1 (DESIGN R17)
-void build_cdf(const double* q, int K, double* out) {
-  double s = 0.0;
-  for (int j = 0; j < K; ++j) {
-    s = s + q[j];
-    out[j] = (j == K - 1) ? 1.0 : s;
-  }
-}
-
 template <class T>
 esdp_status dev_alloc(esdp_ctx* c, T** p, size_t n) {
   if (n == 0) n = 1;
@@ -207,8 +201,9 @@ esdp_status dev_alloc(esdp_ctx* c, T** p, size_t n) {
 
 void free_all(esdp_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -217,34 +212,28 @@ void free_all(esdp_ctx* c) {
 
 esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
   const size_t TK = (size_t)c->T * c->K;
-  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_lambda, lambda, TK * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  std::vector<double> cdf;
+  cudaStream_t s = c->stream;
+  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_lambda, lambda, TK * sizeof(double), cudaMemcpyHostToDevice, s));
   if (!c->rank1) {
-    if (P) {
-      const size_t n = (size_t)(c->T - 1) * c->K * c->K;
-      if (n) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P, P, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      cdf.resize(std::max<size_t>(n, 1));
-      for (size_t r = 0; r < (size_t)(c->T - 1) * c->K; ++r) build_cdf(P + r * c->K, c->K, cdf.data() + r * c->K);
-      if (n) CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf, cdf.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-    }
-    if (pi) {
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, c->K * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      std::vector<double> c1(c->K);
-      build_cdf(pi, c->K, c1.data());
-      CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf1, c1.data(), c->K * sizeof(double), cudaMemcpyHostToDevice));
-    }
+    const size_t n = (size_t)(c->T - 1) * c->K * c->K;
+    if (P && n) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P, P, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (pi) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, c->K * sizeof(double), cudaMemcpyHostToDevice, s));
   } else if (pi) {
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, TK * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    cdf.resize(TK);
-    for (int t = 0; t < c->T; ++t) build_cdf(pi + (size_t)t * c->K, c->K, cdf.data() + (size_t)t * c->K);
-    CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf, cdf.data(), TK * sizeof(double), cudaMemcpyHostToDevice));
-    CUDA_OR_FAIL(c, cudaMemcpy(c->d_cdf1, cdf.data(), c->K * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, TK * sizeof(double), cudaMemcpyHostToDevice, s));
   }
+  // sampling tables for the forward simulation (cdf + guide per transition row), built on the device
+  const int64_t rows = c->rank1 ? c->T : (int64_t)(c->T - 1) * c->K;
+  if ((P || pi) && rows > 0) {
+    const double* q = c->rank1 ? c->d_pi : c->d_P;
+    cdf_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(q, rows, c->K, c->G, c->d_cdf, c->d_guide);
+  }
+  if (pi) cdf_kernel<<<1, 32, 0, s>>>(c->d_pi, 1, c->K, c->G, c->d_cdf1, c->d_guide1);  // pi_1 (row 0 in rank-1)
+  CUDA_OR_FAIL(c, cudaGetLastError());
   if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G)
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, s));
   if (g && c->kind == ESDP_PAYOFF_TABLE)
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
   c->solved = false;
   return ESDP_OK;
 }
@@ -265,6 +254,10 @@ double* W_of(esdp_ctx* c, int t) {
 esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   const int T = c->T, K = c->K, S = c->S;
   int64_t n = 0;
+  const bool prof = !c->ev.empty();
+  auto mark = [&](int t, int j) {
+    return prof ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
+  };
   for (int t = T; t >= 1; --t) {
     double* Wt = W_of(c, t);
     if (t == T) {
@@ -273,7 +266,9 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
       const int rows = (int)w_rows(c);
       const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
       dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
-      contract_kernel<<<grid, kColsC, sizeof(double) * K * kRowsC, s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S);
+      CUDA_OR_FAIL(c, mark(t, 0));
+      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S);
+      CUDA_OR_FAIL(c, mark(t, 1));
       ++n;
     }
     StencilParams prm;
@@ -291,11 +286,13 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
     prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min;
     dim3 grid((S + kTile - 1) / kTile, K);
+    CUDA_OR_FAIL(c, mark(t, 2));
     stencil_kernel<<<grid, kStencilWarps * 32, c->stencil_smem, s>>>(prm);
+    CUDA_OR_FAIL(c, mark(t, 3));
     ++n;
   }
   const double* pi1 = c->d_pi;  // rank-1: row 0 of pi = pi_1
-  objective_kernel<<<1, 32, 0, s>>>(V_of(c, 1), pi1, K, S, c->f0, c->w0, c->on_grid, c->d_J);
+  objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), pi1, K, S, c->f0, c->w0, c->on_grid, c->d_J);
   ++n;
   CUDA_OR_FAIL(c, cudaGetLastError());
   c->launches = n;
@@ -367,6 +364,9 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
   TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
   TRY(dev_alloc(c, &c->d_cdf1, K));
+  c->G = std::max<int>(16, (int)K);
+  TRY(dev_alloc(c, &c->d_guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
+  TRY(dev_alloc(c, &c->d_guide1, (size_t)c->G));
   TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
   TRY(dev_alloc(c, &c->d_act, A));
   TRY(dev_alloc(c, &c->d_w, A));
@@ -396,8 +396,16 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
       return bail(ESDP_E_CUDA);
     }
   }
-  if (K * kRowsC * sizeof(double) > 48 * 1024)
-    cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(K * kRowsC * sizeof(double)));
+  if (contract_smem_bytes(K) > 227 * 1024) { fail(c, ESDP_E_CONFIG, "K too large for the contraction tile"); return bail(ESDP_E_CONFIG); }
+  if (contract_smem_bytes(K) > 48 * 1024)
+    cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
+  if (2 * sizeof(double) * K > 48 * 1024)
+    cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
+  if (c->flags & ESDP_PROFILE) {
+    c->ev.resize((size_t)c->T * 4);
+    for (auto& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) { fail(c, ESDP_E_CUDA, "cudaEventCreate failed"); return bail(ESDP_E_CUDA); }
+  }
   // capture the whole backward pass once; replay it for every solve
   cudaGraph_t g = nullptr;
   if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph capture failed"); return bail(ESDP_E_CUDA); }
@@ -507,8 +515,16 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
   if (n <= 0) return ESDP_OK;
   BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind};
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  const int thr = 128;
-  bidcurve_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+  const size_t per_thread = sizeof(int16_t) * (size_t)c->A;
+  if (per_thread * 64 <= 160 * 1024) {
+    const int thr = per_thread * 128 <= 160 * 1024 ? 128 : 64;
+    const size_t sm = per_thread * thr;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    bidcurve_kernel<true><<<(unsigned)((n + thr - 1) / thr), thr, sm, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+  } else {
+    const int thr = 128;
+    bidcurve_kernel<false><<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+  }
   CUDA_OR_FAIL(c, cudaGetLastError());
   return ESDP_OK;
 }
@@ -549,6 +565,7 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   if (n_paths < 1) return fail(c, ESDP_E_STATE, "n_paths must be >= 1");
   SimParams sp;
   sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
+  sp.guide = c->d_guide; sp.guide1 = c->d_guide1; sp.G = c->G;
   sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
@@ -585,6 +602,26 @@ esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* m
 esdp_status esdp_launch_count(const esdp_ctx* c, int64_t* n) {
   if (!c || !n) return ESDP_E_STATE;
   *n = c->launches;
+  return ESDP_OK;
+}
+
+esdp_status esdp_kernel_times(const esdp_ctx* cc, double* contract_ms, double* stencil_ms) {
+  esdp_ctx* c = const_cast<esdp_ctx*>(cc);
+  if (!c) return ESDP_E_STATE;
+  if (c->ev.empty()) return fail(c, ESDP_E_STATE, "context was created without ESDP_PROFILE");
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  double ct = 0.0, st = 0.0;
+  for (int t = 1; t <= c->T; ++t) {
+    float ms = 0.f;
+    if (t < c->T) {
+      CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[(size_t)(t - 1) * 4 + 0], c->ev[(size_t)(t - 1) * 4 + 1]));
+      ct += ms;
+    }
+    CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[(size_t)(t - 1) * 4 + 2], c->ev[(size_t)(t - 1) * 4 + 3]));
+    st += ms;
+  }
+  if (contract_ms) *contract_ms = ct;
+  if (stencil_ms) *stencil_ms = st;
   return ESDP_OK;
 }
 

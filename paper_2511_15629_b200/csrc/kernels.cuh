@@ -43,52 +43,64 @@ struct StencilParams {
 
 // ------------------------------------------------------------------------------------------------
 // Expectation: W_t[k][i] = sum_{k'} P_t[k][k'] V_{t+1}[k'][i]  (Alg. 1 line 11; Eq. 6)
-// canonical ascending-k' fma chain (R15): bit-identical to the oracle.
-// Block: 64 threads = 64 SoC columns, kRowsC output rows (k) per block.
+// canonical ascending-k' fma chain (R15): bit-identical to the oracle.  (FP64 DMMA was measured at
+// the same 37 TFLOP/s as DFMA on B200 and would change the summation order.)
+// Block tile: kRowsC rows x kColsC columns; V tile [K][kColsC] and P tile [K][kRowsC] staged in
+// shared memory with cp.async (all loads in flight at once), 2x2 register micro-tile per thread.
 // ------------------------------------------------------------------------------------------------
-constexpr int kRowsC = 8;
-constexpr int kColsC = 64;
+constexpr int kRowsC = 16;
+constexpr int kColsC = 32;
+constexpr int kThreadsC = (kRowsC / 2) * (kColsC / 2);  // 128
 
-__global__ void __launch_bounds__(kColsC) contract_kernel(const double* __restrict__ Pt,   // [rows][K] (row stride K)
-                                                          const double* __restrict__ Vn,   // [K][S]
-                                                          double* __restrict__ Wt,         // [rows][S]
-                                                          int rows, int K, int S) {
-  extern __shared__ double ps[];  // [K][kRowsC]  transposed P tile
-  const int r0 = blockIdx.y * kRowsC;
-  const int i = blockIdx.x * kColsC + threadIdx.x;
-  for (int e = threadIdx.x; e < K * kRowsC; e += kColsC) {
-    int kp = e / kRowsC, r = e % kRowsC;
-    ps[e] = (r0 + r < rows) ? Pt[(size_t)(r0 + r) * K + kp] : 0.0;
+inline size_t contract_smem_bytes(int K) { return sizeof(double) * (size_t)K * (kRowsC + kColsC); }
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+__global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __restrict__ Pt,   // [rows][K]
+                                                             const double* __restrict__ Vn,   // [K][S]
+                                                             double* __restrict__ Wt,         // [rows][S]
+                                                             int rows, int K, int S) {
+  extern __shared__ __align__(16) double csm[];
+  double* vs = csm;                      // [K][kColsC]
+  double* ps = csm + (size_t)K * kColsC; // [K][kRowsC]  (transposed P tile)
+  const int i0 = blockIdx.x * kColsC, r0 = blockIdx.y * kRowsC;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < K * kColsC; e += kThreadsC) {
+    const int kp = e / kColsC, c = e % kColsC;
+    if (i0 + c < S) cp_async8(vs + e, Vn + (size_t)kp * S + i0 + c);
+    else vs[e] = 0.0;
   }
+  for (int e = tid; e < K * kRowsC; e += kThreadsC) {
+    const int r = e / K, kp = e % K;
+    if (r0 + r < rows) cp_async8(ps + kp * kRowsC + r, Pt + (size_t)(r0 + r) * K + kp);
+    else ps[kp * kRowsC + r] = 0.0;
+  }
+  cp_async_wait_all();
   __syncthreads();
-  if (i >= S) return;
-  double acc[kRowsC];
-#pragma unroll
-  for (int r = 0; r < kRowsC; ++r) acc[r] = 0.0;
-  const double* vcol = Vn + i;
-  int kp = 0;
-  for (; kp + 4 <= K; kp += 4) {
-    double v0 = __ldg(vcol + (size_t)(kp + 0) * S);
-    double v1 = __ldg(vcol + (size_t)(kp + 1) * S);
-    double v2 = __ldg(vcol + (size_t)(kp + 2) * S);
-    double v3 = __ldg(vcol + (size_t)(kp + 3) * S);
-#pragma unroll
-    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 0) * kRowsC + r], v0, acc[r]);
-#pragma unroll
-    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 1) * kRowsC + r], v1, acc[r]);
-#pragma unroll
-    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 2) * kRowsC + r], v2, acc[r]);
-#pragma unroll
-    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[(kp + 3) * kRowsC + r], v3, acc[r]);
+  const int rr = (tid / (kColsC / 2)) * 2, cc = (tid % (kColsC / 2)) * 2;
+  double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+#pragma unroll 4
+  for (int kp = 0; kp < K; ++kp) {
+    const double2 p = *reinterpret_cast<const double2*>(ps + kp * kRowsC + rr);
+    const double2 v = *reinterpret_cast<const double2*>(vs + kp * kColsC + cc);
+    a00 = __fma_rn(p.x, v.x, a00);
+    a01 = __fma_rn(p.x, v.y, a01);
+    a10 = __fma_rn(p.y, v.x, a10);
+    a11 = __fma_rn(p.y, v.y, a11);
   }
-  for (; kp < K; ++kp) {
-    double v = __ldg(vcol + (size_t)kp * S);
-#pragma unroll
-    for (int r = 0; r < kRowsC; ++r) acc[r] = __fma_rn(ps[kp * kRowsC + r], v, acc[r]);
+  const int i = i0 + cc;
+  if (r0 + rr < rows) {
+    if (i < S) Wt[(size_t)(r0 + rr) * S + i] = a00;
+    if (i + 1 < S) Wt[(size_t)(r0 + rr) * S + i + 1] = a01;
   }
-#pragma unroll
-  for (int r = 0; r < kRowsC; ++r)
-    if (r0 + r < rows) Wt[(size_t)(r0 + r) * S + i] = acc[r];
+  if (r0 + rr + 1 < rows) {
+    if (i < S) Wt[(size_t)(r0 + rr + 1) * S + i] = a10;
+    if (i + 1 < S) Wt[(size_t)(r0 + rr + 1) * S + i + 1] = a11;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -228,13 +240,16 @@ inline size_t stencil_smem_bytes(int A, int o_span) {
 // ------------------------------------------------------------------------------------------------
 __global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int S,
                                  int f, double w0, int on_grid, double* __restrict__ J) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double acc = 0.0;
-  for (int k = 0; k < K; ++k) {
+  extern __shared__ double vk[];  // [2][K]: V_1(s0, k) and pi_1[k], gathered in parallel
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const double* row = V1 + (size_t)k * S;
-    double v = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));
-    acc = __fma_rn(pi1[k], v, acc);
+    vk[k] = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));
+    vk[K + k] = pi1[k];
   }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double acc = 0.0;
+  for (int k = 0; k < K; ++k) acc = __fma_rn(vk[K + k], vk[k], acc);
   *J = acc;
 }
 
@@ -248,45 +263,81 @@ struct BidParams {
   int T, K, S, A, rank1, kind;
 };
 
+// u_a = Wint(i, a) - g_a (Eq. 7 with the non-linear part of the payoff, R13); feasible if both
+// interpolation nodes lie on the grid (Eq. 4 / Alg. 1 line 8)
+__device__ __forceinline__ bool bid_point(const BidParams& bp, const double* __restrict__ Wrow, int i, int a,
+                                          double& u) {
+  const int o = __ldg(bp.off + a);
+  const double wa = __ldg(bp.w + a);
+  if (i + o < 0 || i + o + (wa != 0.0 ? 1 : 0) > bp.S - 1) return false;
+  u = (wa == 0.0) ? __ldg(Wrow + i + o)
+                  : __dadd_rn(__dmul_rn(__ldg(bp.omw + a), __ldg(Wrow + i + o)), __dmul_rn(wa, __ldg(Wrow + i + o + 1)));
+  if (bp.kind == 1) u = __dsub_rn(u, __ldg(bp.g + a));
+  return true;
+}
+
+// One thread per requested curve.  The monotone chain keeps its two top vertices in registers and the
+// rest of the stack as int16 action indices in shared memory (column-major per thread: conflict-free);
+// u of a deeper vertex is recomputed from its index when it resurfaces.  kSmem = false: stack in the
+// caller's vert row (very large A).
+template <bool kSmem>
 __global__ void bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req, int cap,
                                 int32_t* __restrict__ nvert, int16_t* __restrict__ vert, double* __restrict__ q,
                                 double* __restrict__ price) {
-  int64_t rq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ int16_t bst[];
+  const int64_t rq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (rq >= n) return;
   const int t = req[3 * rq + 0], i = req[3 * rq + 1], k = req[3 * rq + 2];
-  int16_t* hv = vert + rq * cap;
-  double* hu = price + rq * cap;
-  double* hq = q + rq * cap;
   if (t < 1 || t > bp.T || i < 0 || i >= bp.S || k < 0 || k >= bp.K) { nvert[rq] = -1; return; }
   const double* Wrow = bp.Wall + ((size_t)(t - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : k)) * bp.S;
+  int16_t* gst = vert + rq * cap;
+  auto st_set = [&](int j, int a) { if (kSmem) bst[(size_t)j * blockDim.x + threadIdx.x] = (int16_t)a; else gst[j] = (int16_t)a; };
+  auto st_get = [&](int j) -> int { return kSmem ? bst[(size_t)j * blockDim.x + threadIdx.x] : gst[j]; };
   int nh = 0;
+  int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
+  double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
   for (int a = 0; a < bp.A; ++a) {
-    const int o = bp.off[a];
-    const double wa = bp.w[a];
-    const int hi_idx = i + o + (wa != 0.0 ? 1 : 0);
-    if (i + o < 0 || hi_idx > bp.S - 1) continue;            // Eq. 4 / Alg. 1 line 8
-    double u = (wa == 0.0) ? Wrow[i + o]
-                           : __dadd_rn(__dmul_rn(bp.omw[a], Wrow[i + o]), __dmul_rn(wa, Wrow[i + o + 1]));
-    if (bp.kind == 1) u = __dsub_rn(u, bp.g[a]);
-    const double pc = bp.act[a];
+    double u;
+    if (!bid_point(bp, Wrow, i, a, u)) continue;
+    const double pc = __ldg(bp.act + a);
     while (nh >= 2) {
-      const double po = bp.act[hv[nh - 2]], uo = hu[nh - 2];
-      const double pb = bp.act[hv[nh - 1]], ub = hu[nh - 1];
       const double cr = __dsub_rn(__dmul_rn(__dsub_rn(pb, po), __dsub_rn(u, uo)),
                                   __dmul_rn(__dsub_rn(ub, uo), __dsub_rn(pc, po)));
-      if (cr >= 0.0) --nh; else break;
+      if (cr < 0.0) break;
+      --nh;                      // pop b; o becomes the top, the vertex below o resurfaces
+      ab = ao; ub = uo; pb = po;
+      if (nh >= 2) {
+        ao = st_get(nh - 2);
+        bid_point(bp, Wrow, i, ao, uo);
+        po = __ldg(bp.act + ao);
+      }
     }
-    hv[nh] = (int16_t)a;
-    hu[nh] = u;
+    st_set(nh, a);
+    if (nh >= 1) { ao = ab; uo = ub; po = pb; }
+    ab = a; ub = u; pb = pc;
     ++nh;
   }
-  for (int j = 0; j < nh; ++j) hq[j] = bp.act[hv[j]];
-  double prev = 0.0;
-  for (int j = 0; j + 1 < nh; ++j) {
-    double pj = -__ddiv_rn(__dsub_rn(hu[j + 1], hu[j]), __dsub_rn(hq[j + 1], hq[j]));
-    if (j > 0 && pj < prev) pj = prev;   // R20 running-max repair
-    hu[j] = pj;
-    prev = pj;
+  // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20)
+  int16_t* vo = vert + rq * cap;
+  double* qo = q ? q + rq * cap : nullptr;
+  double* pro = price + rq * cap;
+  int a_prev = st_get(0);
+  double u_prev;
+  bid_point(bp, Wrow, i, a_prev, u_prev);
+  double p_prev = __ldg(bp.act + a_prev), prev_price = 0.0;
+  if (kSmem) vo[0] = (int16_t)a_prev;
+  if (qo) qo[0] = p_prev;
+  for (int j = 1; j < nh; ++j) {
+    const int a = st_get(j);
+    double u;
+    bid_point(bp, Wrow, i, a, u);
+    const double pc = __ldg(bp.act + a);
+    double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
+    if (j > 1 && pj < prev_price) pj = prev_price;
+    pro[j - 1] = pj;
+    if (kSmem) vo[j] = (int16_t)a;
+    if (qo) qo[j] = pc;
+    prev_price = pj; u_prev = u; p_prev = pc;
   }
   nvert[rq] = nh;
 }
@@ -313,38 +364,69 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
   u2 = (double)((((uint64_t)c[2]) << 21) | (c[3] >> 11)) * 0x1p-53;
 }
 
-// first j in [0, K) with u < cdf[j]  (cdf non-decreasing, cdf[K-1] = 1 > u)
-__device__ __forceinline__ int cdf_search(const double* __restrict__ cdf, int K, double u) {
-  int lo = 0, hi = K - 1;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (u < __ldg(cdf + mid)) hi = mid; else lo = mid + 1;
+// cdf rows (DESIGN R17): running sum in ascending order, last entry forced to 1; plus a guide table
+// guide[b] = first j with b/G < cdf[j], so that a draw u in [b/G, (b+1)/G) starts its search there.
+// One thread per row; bit-identical to the oracle's sequential cdf.
+__global__ void cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G, double* __restrict__ cdf,
+                           int16_t* __restrict__ guide) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const double* qr = q + r * K;
+  double* cr = cdf + r * K;
+  int16_t* gr = guide + r * G;
+  double s = 0.0;
+  int b = 0;
+  for (int j = 0; j < K; ++j) {
+    s = __dadd_rn(s, qr[j]);
+    const double c = (j == K - 1) ? 1.0 : s;
+    cr[j] = c;
+    // bucket lower edge b/G < c  <=>  b < c*G (rounding here only moves the start; the sampler's
+    // scans make the result exact for any start)
+    while (b < G && (double)b < __dmul_rn(c, (double)G)) { gr[b] = (int16_t)j; ++b; }
   }
-  return lo;
+  for (; b < G; ++b) gr[b] = (int16_t)(K - 1);
+}
+
+// first j in [0, K) with u < cdf[j]; the guide gives a start, the scans make it exact for any start.
+__device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const int16_t* __restrict__ guide, int K,
+                                          int G, double u) {
+  int b = (int)__dmul_rn(u, (double)G);
+  b = b < G ? b : G - 1;
+  int j = __ldg(guide + b);
+  while (j > 0 && u < __ldg(cdf + j - 1)) --j;
+  while (j < K - 1 && !(u < __ldg(cdf + j))) ++j;
+  return j;
 }
 
 struct SimParams {
   const int16_t* pol;    // [T][K][S]
   const double* cdf;     // Markov: [T-1][K][K]; rank-1: [T][K] (row t = cdf of pi_{t+1})
+  const int16_t* guide;  // same rows, G entries each
   const double* cdf1;    // [K] cdf of pi_1
+  const int16_t* guide1; // [G]
   const double* lambda;  // [T][K]
   const double* act; const double* w; const int* off; const double* g;
-  int T, K, S, A, rank1, kind, on_grid, f0;
+  int T, K, S, A, G, rank1, kind, on_grid, f0;
   double w0;
 };
 
-__global__ void simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
+__global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
   const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (path >= n) return;
   double u1, u2;
   sim_uniforms(seed, path, 0, u1, u2);
-  int k = cdf_search(sp.cdf1, sp.K, u1);
+  int k = cdf_sample(sp.cdf1, sp.guide1, sp.K, sp.G, u1);
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double profit = 0.0;
   const size_t KS = (size_t)sp.K * sp.S;
   for (int t = 1; t <= sp.T; ++t) {
     sim_uniforms(seed, path, t, u1, u2);
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
+    int kn = k;
+    if (t < sp.T) {
+      const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * sp.K + k;
+      kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + row * sp.G, sp.K, sp.G, u2);
+    }
     double p;
     if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
     else {
@@ -354,10 +436,7 @@ __global__ void simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* 
     profit = __dadd_rn(profit, p);
     const double wa = __ldg(sp.w + a);
     i = i + __ldg(sp.off + a) + ((wa > 0.0 && u1 < wa) ? 1 : 0);
-    if (t < sp.T) {
-      const double* row = sp.rank1 ? sp.cdf + (size_t)t * sp.K : sp.cdf + ((size_t)(t - 1) * sp.K + k) * sp.K;
-      k = cdf_search(row, sp.K, u2);
-    }
+    k = kn;
   }
   out[path] = profit;
 }

@@ -131,7 +131,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     inst = _instance(args, rank)
-    solver = E.Solver(inst, keep_values=True, profile=True)
+    solver = E.Solver(inst, keep_values=True, profile=args.kernel_events)
     T, S, A, K = solver.T, solver.S, solver.A, solver.K
     cells = T * S * K * A
     stream = torch.cuda.Stream(device=dev)
@@ -175,9 +175,10 @@ def run_ours(args):
             step(j)
             evs[j][1].record(stream)
             stream.synchronize()
-            c_ms, s_ms = E.esdp_kernel_times(solver.ctx)
-            con_ms += c_ms
-            sten_ms += s_ms
+            if args.kernel_events:
+                c_ms, s_ms = E.esdp_kernel_times(solver.ctx)   # per launch, sampled stages
+                con_ms += c_ms * (T - 1)
+                sten_ms += s_ms * T
             tot_ms += evs[j][0].elapsed_time(evs[j][1])
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -225,7 +226,7 @@ def run_ours(args):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp64_peak = n_sm * FP64_LANES_PER_SM * sm_max * 1e6 / 1e9          # Gop/s
-    st_launch_ms = sten_ms / (args.steps * T)
+    st_launch_ms = max(sten_ms, 1e-9) / (args.steps * T)
     ops_per_launch = 2.0 * K * S * A                                    # 1 DADD + 1 compare per cell
     achieved = ops_per_launch / (st_launch_ms * 1e-3) / 1e9
     hbm_bytes_launch = 18.0 * K * S                                     # read W 8 B, write V 8 B + pol 2 B
@@ -344,6 +345,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-stages", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-events", type=int, default=1,
+                    help="CUDA events around the kernels of ~16 sampled stages per step (live launch durations)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -56,9 +56,10 @@ enum { ESDP_PAYOFF_LINEAR = 0, ESDP_PAYOFF_LINEAR_MINUS_G = 1, ESDP_PAYOFF_TABLE
 enum {
   ESDP_KEEP_VALUES = 1u,  /* keep V_t and W_t for every t on the device (needed by esdp_values
                              for t > 1 and by the bid-curve calls); otherwise only V_1 is kept */
-  ESDP_PROFILE = 2u       /* record CUDA events around every contraction and stencil launch inside
-                             the backward graph, so esdp_kernel_times can report per-kernel device
-                             time of the last backward pass */
+  ESDP_PROFILE = 2u,      /* record CUDA events around the contraction and stencil launches of ~16
+                             sampled stages inside the backward graph (esdp_kernel_times) */
+  ESDP_FORCE_BRUTE = 4u   /* always use the brute-force max-plus stencil (every (i, a) cell), even
+                             where the exact sliding-window stencil applies (for testing) */
 };
 
 typedef struct {
@@ -143,13 +144,22 @@ esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double*
 esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
                               void* stream);
 
+/* Which max-plus stencil the context uses: 1 = exact sliding-window (recombining grid, linear payoff),
+ * 0 = brute force over every (i, a) cell.  Both give bit-identical results. */
+esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
+
 /* Number of kernel launches one backward pass enqueues (for harness accounting). */
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
 
-/* Device time (ms) of the last completed backward pass, summed per kernel kind: the T-1
- * contraction launches and the T stencil launches (requires ESDP_PROFILE; the caller has
- * synchronized the stream). */
+/* Average device time (ms) of one contraction launch and of one stencil launch in the last completed
+ * backward pass, from CUDA events recorded (inside the backward graph) around the kernels of a sample of
+ * about 16 evenly spaced stages (requires ESDP_PROFILE; the caller has synchronized the stream). */
 esdp_status esdp_kernel_times(const esdp_ctx* ctx, double* contract_ms, double* stencil_ms);
+
+/* Diagnostic micro-timing (not part of the solve): warm back-to-back launches of one kernel of stage
+ * T-1 captured in a graph: what = 0 contraction, 1 the context's stencil, 2 brute-force stencil,
+ * 3 objective kernel.  Needs a completed backward pass.  *us_per_launch = average device time. */
+esdp_status esdp_debug_time(esdp_ctx* ctx, int32_t what, int32_t reps, double* us_per_launch);
 
 void esdp_destroy(esdp_ctx* ctx);
 

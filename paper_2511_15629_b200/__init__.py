@@ -21,21 +21,22 @@ __all__ = [
     "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_destroy",
-    "esdp_last_error", "ESDP_PROFILE", "Solver", "EXPORTED_SYMBOLS",
+    "esdp_last_error", "ESDP_PROFILE", "ESDP_FORCE_BRUTE", "esdp_stencil_kind", "Solver", "EXPORTED_SYMBOLS",
 ]
 
 ESDP_OK, ESDP_E_CONFIG, ESDP_E_DATA, ESDP_E_INTERNAL, ESDP_E_STATE, ESDP_E_CUDA, ESDP_E_NCCL, ESDP_E_NOMEM = range(8)
 ESDP_PAYOFF_LINEAR, ESDP_PAYOFF_LINEAR_MINUS_G, ESDP_PAYOFF_TABLE = 0, 1, 2
 ESDP_KEEP_VALUES = 1
 ESDP_PROFILE = 2
+ESDP_FORCE_BRUTE = 4
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
 EXPORTED_SYMBOLS = [
     "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
-    "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_destroy",
-    "esdp_last_error",
+    "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
+    "esdp_debug_time", "esdp_destroy", "esdp_last_error",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -83,6 +84,8 @@ def _load():
         "esdp_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
         "esdp_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_kernel_times": ([ctx, _dp, _dp], ctypes.c_int),
+        "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
+        "esdp_debug_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
         "esdp_last_error": ([ctx], ctypes.c_char_p),
     }
@@ -223,10 +226,25 @@ def esdp_launch_count(ctx) -> int:
 
 
 def esdp_kernel_times(ctx):
-    """(contraction ms, stencil ms) of the last backward pass (needs ESDP_PROFILE)."""
+    """(ms per contraction launch, ms per stencil launch) averaged over the sampled stages of the last
+    backward pass (needs ESDP_PROFILE)."""
     a, b = ctypes.c_double(), ctypes.c_double()
     _check(lib.esdp_kernel_times(ctx, ctypes.byref(a), ctypes.byref(b)), "esdp_kernel_times", ctx)
     return a.value, b.value
+
+
+def esdp_stencil_kind(ctx) -> int:
+    """1 = exact sliding-window stencil, 0 = brute force."""
+    k = ctypes.c_int32()
+    _check(lib.esdp_stencil_kind(ctx, ctypes.byref(k)), "esdp_stencil_kind", ctx)
+    return k.value
+
+
+def esdp_debug_time(ctx, what, reps=200) -> float:
+    """Warm per-launch device time (us) of one kernel kind (0 contraction, 1 stencil, 2 brute stencil, 3 objective)."""
+    us = ctypes.c_double()
+    _check(lib.esdp_debug_time(ctx, int(what), int(reps), ctypes.byref(us)), "esdp_debug_time", ctx)
+    return us.value
 
 
 def esdp_destroy(ctx):
@@ -237,12 +255,14 @@ class Solver:
     """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
-    def __init__(self, inst, keep_values=True, profile=False):
+    def __init__(self, inst, keep_values=True, profile=False, force_brute=False):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
-                               (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0))
+                               (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
+                               | (ESDP_FORCE_BRUTE if force_brute else 0))
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
+        self.stencil_kind = esdp_stencil_kind(self.ctx)
 
     def backward(self, stream=None):
         return esdp_backward(self.ctx, stream)

@@ -16,6 +16,7 @@
 
 #include "../../include/esdp.h"
 #include "kernels.cuh"
+#include "window.cuh"
 
 using namespace esdp;
 
@@ -34,12 +35,19 @@ struct DevBuf {
 struct esdp_ctx {
   // problem
   int T = 0, K = 0, S = 0, A = 0, kind = 0, rank1 = 0;
+  int ld = 0;  // padded row length of V and W on the device (multiple of 4 doubles: 16-byte cp.async)
   uint32_t flags = 0;
   double pbar = 0, sbar = 0, s0 = 0, eta_c = 1, eta_d = 1, delta = 1;
   std::vector<double> act, w, omw;
   std::vector<int> off;
   std::vector<Seg> segs;
   int o_min = 0, o_max = 0;
+  // exact sliding-window stencil plan (window.cuh); use_window = 0 -> brute-force stencil_kernel
+  int use_window = 0, a_z = -1, Lc = 0, Ld = 0, pc = 0, pd = 0;
+  std::vector<int> singles, live_list;
+  int* d_singles = nullptr;
+  int* d_live = nullptr;
+  size_t window_smem = 0;
   int on_grid = 1, f0 = 0;
   double w0 = 0.0;
   // device
@@ -65,6 +73,7 @@ struct esdp_ctx {
   size_t stencil_smem = 0;
   int64_t launches = 0;
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
+  int prof_stride = 1;
   bool solved = false;
   std::string err;
 };
@@ -184,6 +193,41 @@ void build_tables(esdp_ctx* c) {
     c->o_min = std::min(c->o_min, c->off[b]);
     c->o_max = std::max(c->o_max, c->off[b] + (c->w[b] != 0.0 ? 1 : 0));
   }
+  // window plan: zero action, charge run o = 1..Lc at a_z-1.., discharge run o = -1..-Ld at a_z+1..,
+  // with powers matching -o*delta/eta_c resp. -o*delta*eta_d to a few ulps (the eps bound of
+  // window.cuh assumes it).  Linear payoff only.
+  c->use_window = 0;
+  c->live_list.clear();
+  c->singles.clear();
+  for (int b = 0; b < A; ++b)
+    if (live(b)) c->live_list.push_back(b);
+  c->a_z = -1;
+  for (int b = 0; b < A; ++b)
+    if (c->act[b] == 0.0) c->a_z = b;
+  if (c->kind == ESDP_PAYOFF_LINEAR && c->a_z >= 0 && !(c->flags & ESDP_FORCE_BRUTE)) {
+    const double u8 = 8.0 * 0x1p-53;
+    int Lc = 0, Ld = 0;
+    for (int b = c->a_z - 1; b >= 0; --b) {
+      const int o = c->a_z - b;
+      const double ideal = -((double)o * c->delta / c->eta_c);
+      if (!live(b) || c->w[b] != 0.0 || c->off[b] != o || std::fabs(c->act[b] - ideal) > u8 * std::fabs(ideal)) break;
+      ++Lc;
+    }
+    for (int b = c->a_z + 1; b < A; ++b) {
+      const int o = c->a_z - b;
+      const double ideal = (double)(-o) * c->delta * c->eta_d;
+      if (!live(b) || c->w[b] != 0.0 || c->off[b] != o || std::fabs(c->act[b] - ideal) > u8 * std::fabs(ideal)) break;
+      ++Ld;
+    }
+    if (Lc >= 2 && Ld >= 2 && Lc <= 512 && Ld <= 512) {
+      c->use_window = 1;
+      c->Lc = Lc; c->Ld = Ld;
+      c->pc = 0; while ((2 << c->pc) <= Lc) ++c->pc;
+      c->pd = 0; while ((2 << c->pd) <= Ld) ++c->pd;
+      for (int b : c->live_list)
+        if (b < c->a_z - Lc || b > c->a_z + Ld || b == c->a_z) c->singles.push_back(b);
+    }
+  }
   const double x = c->s0 / c->delta;
   const double r = std::nearbyint(x);
   c->on_grid = std::fabs(x - r) <= kGridTol;
@@ -203,7 +247,7 @@ void free_all(esdp_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -242,11 +286,11 @@ size_t w_rows(const esdp_ctx* c) { return c->rank1 ? 1 : (size_t)c->K; }
 bool keep(const esdp_ctx* c) { return (c->flags & ESDP_KEEP_VALUES) != 0; }
 // V_t / W_t / pol_t device slices (stage t = 1..T)
 double* V_of(esdp_ctx* c, int t) {
-  const size_t KS = (size_t)c->K * c->S;
+  const size_t KS = (size_t)c->K * c->ld;
   return keep(c) ? c->d_V + (size_t)(t - 1) * KS : c->d_V + (size_t)((t - 1) & 1) * KS;
 }
 double* W_of(esdp_ctx* c, int t) {
-  const size_t RS = w_rows(c) * c->S;
+  const size_t RS = w_rows(c) * c->ld;
   return keep(c) ? c->d_W + (size_t)(t - 1) * RS : c->d_W;
 }
 
@@ -255,19 +299,23 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   const int T = c->T, K = c->K, S = c->S;
   int64_t n = 0;
   const bool prof = !c->ev.empty();
+  // ESDP_PROFILE: events around the kernels of every prof_stride-th stage only (a live sample of the
+  // launch durations that keeps event nodes out of most of the graph)
   auto mark = [&](int t, int j) {
-    return prof ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
+    return (prof && t % c->prof_stride == 0)
+               ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal)
+               : cudaSuccess;
   };
   for (int t = T; t >= 1; --t) {
     double* Wt = W_of(c, t);
     if (t == T) {
-      CUDA_OR_FAIL(c, cudaMemsetAsync(Wt, 0, w_rows(c) * S * sizeof(double), s));  // W_T = 0
+      CUDA_OR_FAIL(c, cudaMemsetAsync(Wt, 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
     } else {
       const int rows = (int)w_rows(c);
       const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
       dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
       CUDA_OR_FAIL(c, mark(t, 0));
-      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S);
+      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S, c->ld);
       CUDA_OR_FAIL(c, mark(t, 1));
       ++n;
     }
@@ -285,14 +333,29 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     prm.nseg = (int)c->segs.size();
     prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
     prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min;
+    prm.ld = c->ld;
     dim3 grid((S + kTile - 1) / kTile, K);
     CUDA_OR_FAIL(c, mark(t, 2));
-    stencil_kernel<<<grid, kStencilWarps * 32, c->stencil_smem, s>>>(prm);
+    if (c->use_window) {
+      WinParams wp;
+      wp.W = Wt; wp.V = prm.V; wp.pol = prm.pol; wp.lambda_t = prm.lambda_t;
+      wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
+      wp.singles = c->d_singles; wp.live = c->d_live;
+      wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
+      wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
+      wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
+      wp.o_min = c->o_min; wp.o_max = c->o_max;
+      wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
+      dim3 wgrid((S + kWinTile - 1) / kWinTile, K);
+      window_stencil_kernel<<<wgrid, kWinThreads, c->window_smem, s>>>(wp);
+    } else {
+      stencil_kernel<<<grid, kStencilWarps * 32, c->stencil_smem, s>>>(prm);
+    }
     CUDA_OR_FAIL(c, mark(t, 3));
     ++n;
   }
   const double* pi1 = c->d_pi;  // rank-1: row 0 of pi = pi_1
-  objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), pi1, K, S, c->f0, c->w0, c->on_grid, c->d_J);
+  objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), pi1, K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
   ++n;
   CUDA_OR_FAIL(c, cudaGetLastError());
   c->launches = n;
@@ -324,7 +387,7 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   if (pr->T > 1 && pr->P == nullptr && false) return ESDP_E_CONFIG;
 
   esdp_ctx* c = new esdp_ctx();
-  c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1;
+  c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1; c->ld = (c->S + 3) & ~3;
   c->pbar = pr->pbar; c->sbar = pr->sbar; c->s0 = pr->s0; c->eta_c = pr->eta_c; c->eta_d = pr->eta_d;
   c->delta = pr->delta; c->kind = pr->payoff_kind; c->rank1 = pr->P == nullptr; c->flags = pr->flags;
   if (pr->A == 0) {
@@ -373,10 +436,18 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   TRY(dev_alloc(c, &c->d_omw, A));
   TRY(dev_alloc(c, &c->d_off, A));
   TRY(dev_alloc(c, &c->d_segs, c->segs.size()));
-  TRY(dev_alloc(c, &c->d_V, keep(c) ? T * K * S : 2 * K * S));
-  TRY(dev_alloc(c, &c->d_W, keep(c) ? T * w_rows(c) * S : w_rows(c) * S));
+  const size_t LD = c->ld;
+  TRY(dev_alloc(c, &c->d_V, keep(c) ? T * K * LD : 2 * K * LD));
+  TRY(dev_alloc(c, &c->d_W, keep(c) ? T * w_rows(c) * LD : w_rows(c) * LD));
+  // padding columns are never read as values; zero them once so no stale bits are staged
+  cudaMemset(c->d_V, 0, (keep(c) ? T * K * LD : 2 * K * LD) * sizeof(double));
+  cudaMemset(c->d_W, 0, (keep(c) ? T * w_rows(c) * LD : w_rows(c) * LD) * sizeof(double));
   TRY(dev_alloc(c, &c->d_pol, T * K * S));
   TRY(dev_alloc(c, &c->d_J, 4));
+  TRY(dev_alloc(c, &c->d_singles, c->singles.size()));
+  TRY(dev_alloc(c, &c->d_live, c->live_list.size()));
+  if (!c->singles.empty() && cudaMemcpy(c->d_singles, c->singles.data(), c->singles.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload singles"); return bail(ESDP_E_CUDA); }
+  if (cudaMemcpy(c->d_live, c->live_list.data(), c->live_list.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload live list"); return bail(ESDP_E_CUDA); }
   TRY(dev_alloc(c, &c->d_red, 4));
   if (cudaMemcpy(c->d_act, c->act.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(c->d_w, c->w.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -389,6 +460,13 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
   TRY(upload(c, pr->lambda, pr->P, pr->pi, pr->g));
   c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
+  if (c->use_window) {
+    c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min);
+    if (c->window_smem > 200 * 1024) c->use_window = 0;
+    else if (c->window_smem > 48 * 1024 &&
+             cudaFuncSetAttribute(window_stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->window_smem) != cudaSuccess)
+      c->use_window = 0;
+  }
   if (c->stencil_smem > 48 * 1024) {
     if (c->stencil_smem > 227 * 1024) { fail(c, ESDP_E_CONFIG, "action span too wide for shared memory"); return bail(ESDP_E_CONFIG); }
     if (cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->stencil_smem) != cudaSuccess) {
@@ -402,6 +480,7 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
   if (c->flags & ESDP_PROFILE) {
+    c->prof_stride = std::max(1, c->T / 16);
     c->ev.resize((size_t)c->T * 4);
     for (auto& e : c->ev)
       if (cudaEventCreate(&e) != cudaSuccess) { fail(c, ESDP_E_CUDA, "cudaEventCreate failed"); return bail(ESDP_E_CUDA); }
@@ -482,14 +561,14 @@ esdp_status esdp_values(const esdp_ctx* cc, int32_t t, double* V, double* W) {
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   if (t < 1 || t > c->T) return fail(c, ESDP_E_STATE, "stage %d out of range", t);
   if (!keep(c) && (t != 1 || W)) return fail(c, ESDP_E_STATE, "only V_1 is kept without ESDP_KEEP_VALUES");
-  const size_t KS = (size_t)c->K * c->S;
-  if (V) CUDA_OR_FAIL(c, cudaMemcpy(V, V_of(c, t), KS * sizeof(double), cudaMemcpyDeviceToHost));
+  const size_t rowb = c->S * sizeof(double), ldb = c->ld * sizeof(double);
+  if (V) CUDA_OR_FAIL(c, cudaMemcpy2D(V, rowb, V_of(c, t), ldb, rowb, c->K, cudaMemcpyDeviceToHost));
   if (W) {
     if (c->rank1) {
       for (int k = 0; k < c->K; ++k)
-        CUDA_OR_FAIL(c, cudaMemcpy(W + (size_t)k * c->S, W_of(c, t), c->S * sizeof(double), cudaMemcpyDeviceToHost));
+        CUDA_OR_FAIL(c, cudaMemcpy(W + (size_t)k * c->S, W_of(c, t), rowb, cudaMemcpyDeviceToHost));
     } else {
-      CUDA_OR_FAIL(c, cudaMemcpy(W, W_of(c, t), KS * sizeof(double), cudaMemcpyDeviceToHost));
+      CUDA_OR_FAIL(c, cudaMemcpy2D(W, rowb, W_of(c, t), ldb, rowb, c->K, cudaMemcpyDeviceToHost));
     }
   }
   return ESDP_OK;
@@ -513,17 +592,18 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
   if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
   if (cap < c->A) return fail(c, ESDP_E_STATE, "cap %d < A %d", cap, c->A);
   if (n <= 0) return ESDP_OK;
-  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind};
+  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld};
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  const size_t per_thread = sizeof(int16_t) * (size_t)c->A;
-  if (per_thread * 64 <= 160 * 1024) {
-    const int thr = per_thread * 128 <= 160 * 1024 ? 128 : 64;
-    const size_t sm = per_thread * thr;
+  const int span = c->o_max - c->o_min;
+  const unsigned blocks = (unsigned)((n + kBidThreads - 1) / kBidThreads);
+  size_t sm = bid_smem_bytes(c->A, span, true);
+  if (sm <= 200 * 1024) {
     if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    bidcurve_kernel<true><<<(unsigned)((n + thr - 1) / thr), thr, sm, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+    bidcurve_kernel<true><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, cap, c->o_min, span, nvert_dev, vert_dev, q_dev, price_dev);
   } else {
-    const int thr = 128;
-    bidcurve_kernel<false><<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(bp, n, req_dev, cap, nvert_dev, vert_dev, q_dev, price_dev);
+    sm = bid_smem_bytes(c->A, span, false);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    bidcurve_kernel<false><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, cap, c->o_min, span, nvert_dev, vert_dev, q_dev, price_dev);
   }
   CUDA_OR_FAIL(c, cudaGetLastError());
   return ESDP_OK;
@@ -571,7 +651,9 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   const int thr = 128;
-  simulate_kernel<<<(unsigned)((n_paths + thr - 1) / thr), thr, 0, s>>>(sp, n_paths, seed, per_path_dev);
+  const size_t sm = sim_smem_bytes(c->A);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  simulate_kernel<<<(unsigned)((n_paths + thr - 1) / thr), thr, sm, s>>>(sp, n_paths, seed, per_path_dev);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return ESDP_OK;
 }
@@ -599,6 +681,12 @@ esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* m
   return ESDP_OK;
 }
 
+esdp_status esdp_stencil_kind(const esdp_ctx* c, int32_t* kind) {
+  if (!c || !kind) return ESDP_E_STATE;
+  *kind = c->use_window;
+  return ESDP_OK;
+}
+
 esdp_status esdp_launch_count(const esdp_ctx* c, int64_t* n) {
   if (!c || !n) return ESDP_E_STATE;
   *n = c->launches;
@@ -611,17 +699,90 @@ esdp_status esdp_kernel_times(const esdp_ctx* cc, double* contract_ms, double* s
   if (c->ev.empty()) return fail(c, ESDP_E_STATE, "context was created without ESDP_PROFILE");
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   double ct = 0.0, st = 0.0;
+  int nc = 0, ns = 0;
   for (int t = 1; t <= c->T; ++t) {
+    if (t % c->prof_stride != 0) continue;
     float ms = 0.f;
     if (t < c->T) {
       CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[(size_t)(t - 1) * 4 + 0], c->ev[(size_t)(t - 1) * 4 + 1]));
       ct += ms;
+      ++nc;
     }
     CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[(size_t)(t - 1) * 4 + 2], c->ev[(size_t)(t - 1) * 4 + 3]));
     st += ms;
+    ++ns;
   }
-  if (contract_ms) *contract_ms = ct;
-  if (stencil_ms) *stencil_ms = st;
+  if (contract_ms) *contract_ms = nc ? ct / nc : 0.0;
+  if (stencil_ms) *stencil_ms = ns ? st / ns : 0.0;
+  return ESDP_OK;
+}
+
+esdp_status esdp_debug_time(esdp_ctx* c, int32_t what, int32_t reps, double* us_per_launch) {
+  // Diagnostic: warm back-to-back launches of one kernel kind of stage T-1 (0 = contraction, 1 = the
+  // context's stencil, 2 = brute-force stencil, 3 = empty kernel), captured in a graph and timed with
+  // CUDA events.  Requires a completed backward pass (its buffers are reused as inputs).
+  if (!c || !us_per_launch || reps < 1) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  const int T = c->T, K = c->K, S = c->S;
+  const int t = T > 1 ? T - 1 : T;
+  cudaStream_t s = c->stream;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  CUDA_OR_FAIL(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int r = 0; r < reps; ++r) {
+    if (what == 0 && T > 1) {
+      const int rows = (int)w_rows(c);
+      const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
+      dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
+      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld);
+    } else if (what == 1 || what == 2) {
+      const int saved = c->use_window;
+      if (what == 2) c->use_window = 0;
+      // reuse enqueue's stencil launch code through a one-stage helper
+      StencilParams prm;
+      prm.W = W_of(c, t); prm.V = V_of(c, t); prm.pol = c->d_pol + (size_t)(t - 1) * K * S;
+      prm.lambda_t = c->d_lambda + (size_t)(t - 1) * K; prm.act = c->d_act;
+      prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
+      prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
+      prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
+      prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
+      if (c->use_window) {
+        WinParams wp;
+        wp.W = prm.W; wp.V = prm.V; wp.pol = prm.pol; wp.lambda_t = prm.lambda_t;
+        wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
+        wp.singles = c->d_singles; wp.live = c->d_live;
+        wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
+        wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
+        wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
+        wp.o_min = c->o_min; wp.o_max = c->o_max;
+        wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
+        window_stencil_kernel<<<dim3((S + kWinTile - 1) / kWinTile, K), kWinThreads, c->window_smem, s>>>(wp);
+      } else {
+        stencil_kernel<<<dim3((S + kTile - 1) / kTile, K), kStencilWarps * 32, c->stencil_smem, s>>>(prm);
+      }
+      c->use_window = saved;
+    } else {
+      objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), c->d_pi, K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
+    }
+  }
+  cudaError_t ce = cudaStreamEndCapture(s, &g);
+  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "debug capture: %s", cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "debug instantiate: %s", cudaGetErrorString(ce));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(e0, s);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(e1, s);
+  ce = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "debug run: %s", cudaGetErrorString(ce));
+  *us_per_launch = 1e3 * ms / reps;
   return ESDP_OK;
 }
 

@@ -14,7 +14,7 @@ constexpr int R = 8;                  // SoC columns per thread in the stencil (
 constexpr int kLanes = 32;
 constexpr int kTile = kLanes * R;     // 256 SoC columns per stencil block
 constexpr int kPad = 8;               // smem guard columns below the lowest offset
-constexpr int kStencilWarps = 4;      // action chunks per block (one warp each)
+constexpr int kStencilWarps = 8;      // action chunks per block (one warp each)
 
 __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  // 8-column groups + 1 pad
 
@@ -39,67 +39,98 @@ struct StencilParams {
   const int* off;         // [A]
   const Seg* segs;        // [nseg]
   int nseg, A, S, K, kind, rank1, o_min, o_span;  // o_span = o_max - o_min
+  int ld;                 // leading dimension of W and V rows (>= S)
 };
 
 // ------------------------------------------------------------------------------------------------
 // Expectation: W_t[k][i] = sum_{k'} P_t[k][k'] V_{t+1}[k'][i]  (Alg. 1 line 11; Eq. 6)
 // canonical ascending-k' fma chain (R15): bit-identical to the oracle.  (FP64 DMMA was measured at
 // the same 37 TFLOP/s as DFMA on B200 and would change the summation order.)
-// Block tile: kRowsC rows x kColsC columns; V tile [K][kColsC] and P tile [K][kRowsC] staged in
-// shared memory with cp.async (all loads in flight at once), 2x2 register micro-tile per thread.
+// Each output is a K-long dependent DFMA chain (9-cycle latency): the kernel keeps 4 chains per
+// thread and prefetches the next 4 k' of operands from shared memory while the current 4 retire.
+// Block tile: kRowsC rows x kColsC columns; V tile [Kp][kColsC] staged with 16-byte cp.async
+// (V rows have a padded leading dimension ld, a multiple of 4 doubles), P tile [kRowsC][Kp];
+// rows k' >= K are zero-filled, which leaves every chain unchanged (fma(0, 0, acc) == acc for acc != -0,
+// and the chain starts at +0 and can never reach -0).
 // ------------------------------------------------------------------------------------------------
 constexpr int kRowsC = 16;
 constexpr int kColsC = 32;
-constexpr int kThreadsC = (kRowsC / 2) * (kColsC / 2);  // 128
+constexpr int kThreadsC = (kRowsC / 2) * (kColsC / 2);  // 128, 2x2 outputs per thread
 
-inline size_t contract_smem_bytes(int K) { return sizeof(double) * (size_t)K * (kRowsC + kColsC); }
+__host__ __device__ __forceinline__ int pad4(int K) { return (K + 3) & ~3; }
+inline size_t contract_smem_bytes(int K) { return sizeof(double) * (size_t)pad4(K) * (kRowsC + kColsC); }
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc));
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __restrict__ Pt,   // [rows][K]
-                                                             const double* __restrict__ Vn,   // [K][S]
-                                                             double* __restrict__ Wt,         // [rows][S]
-                                                             int rows, int K, int S) {
+                                                             const double* __restrict__ Vn,   // [K][ld]
+                                                             double* __restrict__ Wt,         // [rows][ld]
+                                                             int rows, int K, int S, int ld) {
   extern __shared__ __align__(16) double csm[];
-  double* vs = csm;                      // [K][kColsC]
-  double* ps = csm + (size_t)K * kColsC; // [K][kRowsC]  (transposed P tile)
+  const int Kp = pad4(K);
+  double* vs = csm;                        // [Kp][kColsC]
+  double* ps = csm + (size_t)Kp * kColsC;  // [kRowsC][Kp]
   const int i0 = blockIdx.x * kColsC, r0 = blockIdx.y * kRowsC;
   const int tid = threadIdx.x;
-  for (int e = tid; e < K * kColsC; e += kThreadsC) {
-    const int kp = e / kColsC, c = e % kColsC;
-    if (i0 + c < S) cp_async8(vs + e, Vn + (size_t)kp * S + i0 + c);
-    else vs[e] = 0.0;
+  {  // V tile: 16 two-double chunks per row, 8 rows per pass (no runtime division)
+    const int c = 2 * (tid & 15);
+    const bool in = i0 + c < ld;
+    const double* src = Vn + i0 + c;
+    for (int kp = tid >> 4; kp < Kp; kp += kThreadsC / 16) {
+      double* dst = vs + kp * kColsC + c;
+      if (kp < K && in) cp_async16(dst, src + (size_t)kp * ld);
+      else { dst[0] = 0.0; dst[1] = 0.0; }
+    }
   }
-  for (int e = tid; e < K * kRowsC; e += kThreadsC) {
-    const int r = e / K, kp = e % K;
-    if (r0 + r < rows) cp_async8(ps + kp * kRowsC + r, Pt + (size_t)(r0 + r) * K + kp);
-    else ps[kp * kRowsC + r] = 0.0;
+  for (int r = 0; r < kRowsC; ++r) {  // P tile rows
+    const bool rin = r0 + r < rows;
+    const double* src = Pt + (size_t)(r0 + r) * K;
+    for (int kp = tid; kp < Kp; kp += kThreadsC) {
+      if (rin && kp < K) cp_async8(ps + r * Kp + kp, src + kp);
+      else ps[r * Kp + kp] = 0.0;
+    }
   }
   cp_async_wait_all();
   __syncthreads();
   const int rr = (tid / (kColsC / 2)) * 2, cc = (tid % (kColsC / 2)) * 2;
+  const double* p0 = ps + (size_t)rr * Kp;
+  const double* p1 = p0 + Kp;
   double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
-#pragma unroll 4
-  for (int kp = 0; kp < K; ++kp) {
-    const double2 p = *reinterpret_cast<const double2*>(ps + kp * kRowsC + rr);
-    const double2 v = *reinterpret_cast<const double2*>(vs + kp * kColsC + cc);
-    a00 = __fma_rn(p.x, v.x, a00);
-    a01 = __fma_rn(p.x, v.y, a01);
-    a10 = __fma_rn(p.y, v.x, a10);
-    a11 = __fma_rn(p.y, v.y, a11);
+  double4 x0 = *reinterpret_cast<const double4*>(p0), x1 = *reinterpret_cast<const double4*>(p1);
+  double2 v0 = *reinterpret_cast<const double2*>(vs + 0 * kColsC + cc);
+  double2 v1 = *reinterpret_cast<const double2*>(vs + 1 * kColsC + cc);
+  double2 v2 = *reinterpret_cast<const double2*>(vs + 2 * kColsC + cc);
+  double2 v3 = *reinterpret_cast<const double2*>(vs + 3 * kColsC + cc);
+  for (int kp = 0; kp < Kp; kp += 4) {
+    // prefetch the next 4 k' (clamped re-read of the last chunk at the end: harmless)
+    const int kn = (kp + 4 < Kp) ? kp + 4 : kp;
+    const double4 y0 = *reinterpret_cast<const double4*>(p0 + kn), y1 = *reinterpret_cast<const double4*>(p1 + kn);
+    const double2 u0 = *reinterpret_cast<const double2*>(vs + (kn + 0) * kColsC + cc);
+    const double2 u1 = *reinterpret_cast<const double2*>(vs + (kn + 1) * kColsC + cc);
+    const double2 u2 = *reinterpret_cast<const double2*>(vs + (kn + 2) * kColsC + cc);
+    const double2 u3 = *reinterpret_cast<const double2*>(vs + (kn + 3) * kColsC + cc);
+    a00 = __fma_rn(x0.x, v0.x, a00); a01 = __fma_rn(x0.x, v0.y, a01); a10 = __fma_rn(x1.x, v0.x, a10); a11 = __fma_rn(x1.x, v0.y, a11);
+    a00 = __fma_rn(x0.y, v1.x, a00); a01 = __fma_rn(x0.y, v1.y, a01); a10 = __fma_rn(x1.y, v1.x, a10); a11 = __fma_rn(x1.y, v1.y, a11);
+    a00 = __fma_rn(x0.z, v2.x, a00); a01 = __fma_rn(x0.z, v2.y, a01); a10 = __fma_rn(x1.z, v2.x, a10); a11 = __fma_rn(x1.z, v2.y, a11);
+    a00 = __fma_rn(x0.w, v3.x, a00); a01 = __fma_rn(x0.w, v3.y, a01); a10 = __fma_rn(x1.w, v3.x, a10); a11 = __fma_rn(x1.w, v3.y, a11);
+    x0 = y0; x1 = y1; v0 = u0; v1 = u1; v2 = u2; v3 = u3;
   }
   const int i = i0 + cc;
   if (r0 + rr < rows) {
-    if (i < S) Wt[(size_t)(r0 + rr) * S + i] = a00;
-    if (i + 1 < S) Wt[(size_t)(r0 + rr) * S + i + 1] = a01;
+    if (i < S) Wt[(size_t)(r0 + rr) * ld + i] = a00;
+    if (i + 1 < S) Wt[(size_t)(r0 + rr) * ld + i + 1] = a01;
   }
   if (r0 + rr + 1 < rows) {
-    if (i < S) Wt[(size_t)(r0 + rr + 1) * S + i] = a10;
-    if (i + 1 < S) Wt[(size_t)(r0 + rr + 1) * S + i + 1] = a11;
+    if (i < S) Wt[(size_t)(r0 + rr + 1) * ld + i] = a10;
+    if (i + 1 < S) Wt[(size_t)(r0 + rr + 1) * ld + i + 1] = a11;
   }
 }
 
@@ -116,22 +147,28 @@ __device__ __forceinline__ void upd(double c, int a, double& best, int& arg) {
   if (c > best) { best = c; arg = a; }
 }
 
+// One group of R steps of a recombining run.  wl = this lane's view of the skewed tile
+// (wl[u] = tile index lane*R + c with u = c + (c >> 3)); base_c = tile offset of (column lane*R,
+// current step) minus lane*R (warp-uniform).  Step d evaluates action a + d; column r reads W at
+// lane-relative tile offset base_c - d + r.
 template <bool kMask>
-__device__ __forceinline__ void run_group(const double* __restrict__ ws, const double* __restrict__ pay,
-                                          int base, int a, int m_left, double (&hi)[R], double (&best)[R],
+__device__ __forceinline__ void run_group(const double* __restrict__ wl, const double* __restrict__ pay,
+                                          int base_c, int a, int m_left, double (&hi)[R], double (&best)[R],
                                           int (&arg)[R]) {
-  // steps d = 0..7 of the run: action a + d, column r reads W at tile index base - d + r.
-  double lo[R];
+  double lo[R], p[R];
 #pragma unroll
-  for (int q = 0; q < R; ++q) lo[q] = ws[skew(base - R + q)];
+  for (int q = 0; q < R; ++q) {
+    const int c = base_c - R + q;                 // >= 0 by construction (kPad >= R)
+    lo[q] = wl[c + (c >> 3)];
+    p[q] = pay[a + q];
+  }
 #pragma unroll
   for (int d = 0; d < R; ++d) {
-    double p = pay[a + d];
-    if (kMask) p = (d < m_left) ? p : -INFINITY;
+    const double pd = kMask ? ((d < m_left) ? p[d] : -INFINITY) : p[d];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double x = (r - d >= 0) ? hi[r - d] : lo[R + r - d];
-      upd(__dadd_rn(p, x), a + d, best[r], arg[r]);
+      const double x = (r - d >= 0) ? hi[r - d] : lo[R + r - d];
+      upd(__dadd_rn(pd, x), a + d, best[r], arg[r]);
     }
   }
 #pragma unroll
@@ -149,7 +186,7 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
   int* pa = (int*)(pv + kStencilWarps * skew(kTile));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.S);
+  const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.ld);
   const int g0 = i0 + prm.o_min - kPad;  // global column of tile index 0
   for (int j = tid; j < L; j += blockDim.x) {
     int col = g0 + j;
@@ -170,7 +207,8 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
 #pragma unroll
   for (int r = 0; r < R; ++r) { best[r] = -INFINITY; arg[r] = -1; }
   const int a_lo = (prm.A * warp) / kStencilWarps, a_hi = (prm.A * (warp + 1)) / kStencilWarps;
-  const int colbase = lane * R - prm.o_min + kPad;  // tile index of (column lane*R, offset 0)
+  const double* wl = ws + lane * (R + 1);          // skew(lane*R + c) = lane*(R+1) + c + (c>>3)
+  const int cbase = kPad - prm.o_min;              // lane-relative tile offset of offset 0
 
   for (int s = 0; s < prm.nseg; ++s) {
     const Seg sg = prm.segs[s];
@@ -178,32 +216,35 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
     if (sb >= se) continue;
     if (sg.interp || sg.n < 4) {
       for (int a = sb; a < se; ++a) {
-        const int o = sg.o0 - (a - sg.a0);
+        const int c0 = cbase + sg.o0 - (a - sg.a0);
         const double p = pay[a];
         if (sg.interp) {
           const double w = prm.w[a], om = prm.omw[a];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            double x0 = ws[skew(colbase + r + o)], x1 = ws[skew(colbase + r + o + 1)];
-            double wi = __dadd_rn(__dmul_rn(om, x0), __dmul_rn(w, x1));
+            const int c = c0 + r;
+            const double x0 = wl[c + (c >> 3)], x1 = wl[(c + 1) + ((c + 1) >> 3)];
+            const double wi = __dadd_rn(__dmul_rn(om, x0), __dmul_rn(w, x1));
             upd(__dadd_rn(p, wi), a, best[r], arg[r]);
           }
         } else {
 #pragma unroll
-          for (int r = 0; r < R; ++r) upd(__dadd_rn(p, ws[skew(colbase + r + o)]), a, best[r], arg[r]);
+          for (int r = 0; r < R; ++r) {
+            const int c = c0 + r;
+            upd(__dadd_rn(p, wl[c + (c >> 3)]), a, best[r], arg[r]);
+          }
         }
       }
       continue;
     }
     // recombining run: action a = sb + m has offset o(sb) - m
-    const int o_b = sg.o0 - (sb - sg.a0);
-    int base = colbase + o_b;  // tile index of column lane*R + 0 for the current step
+    int base_c = cbase + sg.o0 - (sb - sg.a0);
     double hi[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) hi[q] = ws[skew(base + q)];
+    for (int q = 0; q < R; ++q) { const int c = base_c + q; hi[q] = wl[c + (c >> 3)]; }
     int a = sb;
-    for (; a + R <= se; a += R, base -= R) run_group<false>(ws, pay, base, a, R, hi, best, arg);
-    if (a < se) run_group<true>(ws, pay, base, a, se - a, hi, best, arg);
+    for (; a + R <= se; a += R, base_c -= R) run_group<false>(wl, pay, base_c, a, R, hi, best, arg);
+    if (a < se) run_group<true>(wl, pay, base_c, a, se - a, hi, best, arg);
   }
 
   // merge the chunk partials in ascending action order (strict '>' keeps the smallest index)
@@ -223,7 +264,7 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
       double v = pv[w * skew(kTile) + skew(c)];
       if (v > b) { b = v; ar = pa[w * skew(kTile) + skew(c)]; }
     }
-    prm.V[(size_t)k * prm.S + i] = b;
+    prm.V[(size_t)k * prm.ld + i] = b;
     prm.pol[(size_t)k * prm.S + i] = (int16_t)ar;
   }
 }
@@ -238,11 +279,11 @@ inline size_t stencil_smem_bytes(int A, int o_span) {
 // Objective J = sum_k pi_1[k] V_1(s0, k) (Eq. 6 at t = 0), fma chain in k order; s0 off the
 // grid is interpolated per k (R24).  One thread.
 // ------------------------------------------------------------------------------------------------
-__global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int S,
+__global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int ld,
                                  int f, double w0, int on_grid, double* __restrict__ J) {
   extern __shared__ double vk[];  // [2][K]: V_1(s0, k) and pi_1[k], gathered in parallel
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    const double* row = V1 + (size_t)k * S;
+    const double* row = V1 + (size_t)k * ld;
     vk[k] = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));
     vk[K + k] = pi1[k];
   }
@@ -258,48 +299,98 @@ __global__ void objective_kernel(const double* __restrict__ V1, const double* __
 // serve as the hull stack (vert: action index, price: hull u value, overwritten by prices).
 // ------------------------------------------------------------------------------------------------
 struct BidParams {
-  const double* Wall;     // [T][rows][S]
+  const double* Wall;     // [T][rows][ld]
   const double* act; const double* w; const double* omw; const int* off; const double* g;
-  int T, K, S, A, rank1, kind;
+  int T, K, S, A, rank1, kind, ld;
+};
+
+// Per-action data staged in shared memory for the bid-curve kernel.
+struct BidAct {
+  const double* act; const double* w; const double* omw; const double* g; const int* off;
 };
 
 // u_a = Wint(i, a) - g_a (Eq. 7 with the non-linear part of the payoff, R13); feasible if both
-// interpolation nodes lie on the grid (Eq. 4 / Alg. 1 line 8)
-__device__ __forceinline__ bool bid_point(const BidParams& bp, const double* __restrict__ Wrow, int i, int a,
+// interpolation nodes lie on the grid (Eq. 4 / Alg. 1 line 8).  Wrow is indexed by global column.
+__device__ __forceinline__ bool bid_point(const BidAct& ba, int S, int kind, const double* Wrow, int i, int a,
                                           double& u) {
-  const int o = __ldg(bp.off + a);
-  const double wa = __ldg(bp.w + a);
-  if (i + o < 0 || i + o + (wa != 0.0 ? 1 : 0) > bp.S - 1) return false;
-  u = (wa == 0.0) ? __ldg(Wrow + i + o)
-                  : __dadd_rn(__dmul_rn(__ldg(bp.omw + a), __ldg(Wrow + i + o)), __dmul_rn(wa, __ldg(Wrow + i + o + 1)));
-  if (bp.kind == 1) u = __dsub_rn(u, __ldg(bp.g + a));
+  const int o = ba.off[a];
+  const double wa = ba.w[a];
+  if (i + o < 0 || i + o + (wa != 0.0 ? 1 : 0) > S - 1) return false;
+  u = (wa == 0.0) ? Wrow[i + o] : __dadd_rn(__dmul_rn(ba.omw[a], Wrow[i + o]), __dmul_rn(wa, Wrow[i + o + 1]));
+  if (kind == 1) u = __dsub_rn(u, ba.g[a]);
   return true;
+}
+
+constexpr int kBidThreads = 128;
+
+inline size_t bid_smem_bytes(int A, int o_span, bool stack_in_smem) {
+  return (size_t)A * (4 * sizeof(double) + sizeof(int)) + sizeof(double) * (kBidThreads + o_span + 4) +
+         (stack_in_smem ? sizeof(int16_t) * (size_t)A * kBidThreads : 0) + 64;
 }
 
 // One thread per requested curve.  The monotone chain keeps its two top vertices in registers and the
 // rest of the stack as int16 action indices in shared memory (column-major per thread: conflict-free);
-// u of a deeper vertex is recomputed from its index when it resurfaces.  kSmem = false: stack in the
-// caller's vert row (very large A).
+// u of a deeper vertex is recomputed from its index when it resurfaces.  When every request of the
+// block is on the same (t, k) row (the common "all i of a stage" case) the W row segment is staged in
+// shared memory.  kSmem = false: the stack lives in the caller's vert row (very large A).
 template <bool kSmem>
-__global__ void bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req, int cap,
-                                int32_t* __restrict__ nvert, int16_t* __restrict__ vert, double* __restrict__ q,
-                                double* __restrict__ price) {
-  extern __shared__ int16_t bst[];
+__global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req,
+                                                               int cap, int o_min, int o_span,
+                                                               int32_t* __restrict__ nvert, int16_t* __restrict__ vert,
+                                                               double* __restrict__ q, double* __restrict__ price) {
+  extern __shared__ __align__(16) double bsm[];
+  const int A = bp.A;
+  double* s_act = bsm;
+  double* s_w = s_act + A;
+  double* s_omw = s_w + A;
+  double* s_g = s_omw + A;
+  int* s_off = (int*)(s_g + A);
+  double* s_wt = (double*)(((uintptr_t)(s_off + A) + 15) & ~(uintptr_t)15);
+  const int nwt = kBidThreads + o_span + 4;
+  int16_t* bst = (int16_t*)(s_wt + nwt);
+  __shared__ int s_tk[2], s_imin, s_imax, s_uniform;
+
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    s_act[a] = bp.act[a]; s_w[a] = bp.w[a]; s_omw[a] = bp.omw[a]; s_off[a] = bp.off[a];
+    s_g[a] = bp.kind == 1 ? bp.g[a] : 0.0;
+  }
   const int64_t rq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rq >= n) return;
-  const int t = req[3 * rq + 0], i = req[3 * rq + 1], k = req[3 * rq + 2];
-  if (t < 1 || t > bp.T || i < 0 || i >= bp.S || k < 0 || k >= bp.K) { nvert[rq] = -1; return; }
-  const double* Wrow = bp.Wall + ((size_t)(t - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : k)) * bp.S;
+  const bool active = rq < n;
+  int t = 0, i = 0, k = 0;
+  if (active) { t = req[3 * rq + 0]; i = req[3 * rq + 1]; k = req[3 * rq + 2]; }
+  const bool valid = active && t >= 1 && t <= bp.T && i >= 0 && i < bp.S && k >= 0 && k < bp.K;
+  if (threadIdx.x == 0) {
+    s_tk[0] = t; s_tk[1] = k; s_imin = 1 << 30; s_imax = -1; s_uniform = 1;
+  }
+  __syncthreads();
+  if (valid) { atomicMin(&s_imin, i); atomicMax(&s_imax, i); }
+  if (active && (!valid || t != s_tk[0] || (k != s_tk[1] && !bp.rank1))) s_uniform = 0;
+  __syncthreads();
+  const bool staged = s_uniform && s_imax >= 0 && (s_imax - s_imin) < kBidThreads;
+  const double* Wg = bp.Wall + ((size_t)(t - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : k)) * bp.ld;
+  const double* Wrow = Wg;
+  if (staged) {
+    const int c0 = s_imin + o_min;
+    const double* Wb = bp.Wall + ((size_t)(s_tk[0] - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : s_tk[1])) * bp.ld;
+    for (int x = threadIdx.x; x < nwt; x += blockDim.x) {
+      const int col = c0 + x;
+      s_wt[x] = (col >= 0 && col < bp.S) ? Wb[col] : 0.0;
+    }
+    Wrow = s_wt - c0;
+  }
+  __syncthreads();
+  if (!valid) { if (active) nvert[rq] = -1; return; }
+  const BidAct ba{s_act, s_w, s_omw, s_g, s_off};
   int16_t* gst = vert + rq * cap;
   auto st_set = [&](int j, int a) { if (kSmem) bst[(size_t)j * blockDim.x + threadIdx.x] = (int16_t)a; else gst[j] = (int16_t)a; };
   auto st_get = [&](int j) -> int { return kSmem ? bst[(size_t)j * blockDim.x + threadIdx.x] : gst[j]; };
   int nh = 0;
   int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
   double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
-  for (int a = 0; a < bp.A; ++a) {
+  for (int a = 0; a < A; ++a) {
     double u;
-    if (!bid_point(bp, Wrow, i, a, u)) continue;
-    const double pc = __ldg(bp.act + a);
+    if (!bid_point(ba, bp.S, bp.kind, Wrow, i, a, u)) continue;
+    const double pc = s_act[a];
     while (nh >= 2) {
       const double cr = __dsub_rn(__dmul_rn(__dsub_rn(pb, po), __dsub_rn(u, uo)),
                                   __dmul_rn(__dsub_rn(ub, uo), __dsub_rn(pc, po)));
@@ -308,8 +399,8 @@ __global__ void bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restri
       ab = ao; ub = uo; pb = po;
       if (nh >= 2) {
         ao = st_get(nh - 2);
-        bid_point(bp, Wrow, i, ao, uo);
-        po = __ldg(bp.act + ao);
+        bid_point(ba, bp.S, bp.kind, Wrow, i, ao, uo);
+        po = s_act[ao];
       }
     }
     st_set(nh, a);
@@ -323,15 +414,15 @@ __global__ void bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restri
   double* pro = price + rq * cap;
   int a_prev = st_get(0);
   double u_prev;
-  bid_point(bp, Wrow, i, a_prev, u_prev);
-  double p_prev = __ldg(bp.act + a_prev), prev_price = 0.0;
+  bid_point(ba, bp.S, bp.kind, Wrow, i, a_prev, u_prev);
+  double p_prev = s_act[a_prev], prev_price = 0.0;
   if (kSmem) vo[0] = (int16_t)a_prev;
   if (qo) qo[0] = p_prev;
   for (int j = 1; j < nh; ++j) {
     const int a = st_get(j);
     double u;
-    bid_point(bp, Wrow, i, a, u);
-    const double pc = __ldg(bp.act + a);
+    bid_point(ba, bp.S, bp.kind, Wrow, i, a, u);
+    const double pc = s_act[a];
     double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
     if (j > 1 && pj < prev_price) pj = prev_price;
     pro[j - 1] = pj;
@@ -411,6 +502,16 @@ struct SimParams {
 };
 
 __global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
+  extern __shared__ __align__(16) double ssm[];   // per-action tables: act, w, g (kind 1), off
+  double* s_act = ssm;
+  double* s_w = s_act + sp.A;
+  double* s_g = s_w + sp.A;
+  int* s_off = (int*)(s_g + sp.A);
+  for (int a = threadIdx.x; a < sp.A; a += blockDim.x) {
+    s_act[a] = sp.act[a]; s_w[a] = sp.w[a]; s_off[a] = sp.off[a];
+    s_g[a] = sp.kind == 1 ? sp.g[a] : 0.0;
+  }
+  __syncthreads();
   const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (path >= n) return;
   double u1, u2;
@@ -430,16 +531,18 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, 
     double p;
     if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
     else {
-      p = __dmul_rn(__ldg(sp.lambda + (size_t)(t - 1) * sp.K + k), __ldg(sp.act + a));
-      if (sp.kind == 1) p = __dsub_rn(p, __ldg(sp.g + a));
+      p = __dmul_rn(__ldg(sp.lambda + (size_t)(t - 1) * sp.K + k), s_act[a]);
+      if (sp.kind == 1) p = __dsub_rn(p, s_g[a]);
     }
     profit = __dadd_rn(profit, p);
-    const double wa = __ldg(sp.w + a);
-    i = i + __ldg(sp.off + a) + ((wa > 0.0 && u1 < wa) ? 1 : 0);
+    const double wa = s_w[a];
+    i = i + s_off[a] + ((wa > 0.0 && u1 < wa) ? 1 : 0);
     k = kn;
   }
   out[path] = profit;
 }
+
+inline size_t sim_smem_bytes(int A) { return (size_t)A * (3 * sizeof(double) + sizeof(int)) + 16; }
 
 // Deterministic two-pass reduction of per-path profits: sum (then sum of squared deviations).
 __global__ void reduce_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean_in,

@@ -1,0 +1,191 @@
+// window.cuh -- exact O(log A)-per-cell max-plus stencil for the recombining action grid.
+//
+// Same result as stencil_kernel (V and the smallest-index argmax, bit for bit), computed without
+// visiting every (i, a) cell.  On the interior of the Eq. 10 grid the charge actions have
+// integral SoC offsets o = 1..Lc and powers p = -o*delta/eta_c (up to rounding), the discharge actions
+// o = -1..-Ld and p = -o*delta*eta_d.  With the linear payoff lambda*p the candidate of row i is
+//     cand(i, o) = lambda*p(o) + W[i+o]  ~=  key(j) + beta*i,   j = i + o,   key(j) = W[j] - beta*j,
+// with beta_c = lambda*delta/eta_c on the charge side and beta_d = lambda*delta*eta_d on the discharge
+// side: a sliding-window maximum of a per-column key over a fixed-width window.  Each side keeps a
+// sparse table of (max, position) over power-of-two ranges: a window maximum is two lookups, and the
+// runner-up (needed for the exactness test) is the maximum of the window minus its argmax.
+//
+// Exactness.  The key form rounds differently from the canonical candidate fl(fl(lambda p) + W), by
+// at most eps = 32 u (max|W| + |lambda| delta (S + span) / min(eta) + |lambda| pbar).
+// The remaining actions (zero action, the interpolated endpoints +-pbar, anything irregular) are
+// evaluated canonically.  If the best approximate value beats the second best by more than 2 eps, the
+// canonical argmax is that action and is unique; V is then recomputed canonically from it.  Otherwise
+// (near ties) the row falls back to the full canonical scan in ascending a with a strict '>'.  Either
+// way V and pol equal the oracle's bit for bit.
+#pragma once
+#include "kernels.cuh"
+
+namespace esdp {
+
+constexpr int kWinTile = 256;     // output columns per block
+constexpr int kWinThreads = 256;  // one output column per thread in the query phase
+
+struct WinParams {
+  const double* W; double* V; int16_t* pol; const double* lambda_t;
+  const double* act; const double* w; const double* omw; const int* off;
+  const int* singles;   // action indices evaluated canonically (zero action, endpoints, irregular)
+  const int* live;      // all live action indices, ascending (fallback scan)
+  int nsingle, nlive, A, S, K, rank1, ld;
+  int a_z, Lc, Ld, pc, pd;  // zero action; run lengths; sparse-table levels (2^pc <= Lc < 2^(pc+1))
+  int o_min, o_max;         // tile halo over all live actions
+  double delta, eta_c, eta_d, pbar;
+};
+
+// Sparse table of (max, position) over power-of-two ranges: level q entry x covers [x, x + 2^q).
+// All levels are kept so that any range [l, r] is answered with two lookups (overlap is harmless for
+// a maximum).  The second best of a window is the maximum of the window with the argmax removed:
+// two more range queries.
+struct RangeMax {
+  double* v;   // [levels][n]
+  int* ix;     // [levels][n] table positions
+  int n;
+  __device__ __forceinline__ void query(int l, int r, double& m, int& at) const {
+    if (l > r) { m = -INFINITY; at = -1; return; }
+    const int q = 31 - __clz(r - l + 1);
+    const int o = q * n, r2 = r - (1 << q) + 1;
+    const double a = v[o + l], b = v[o + r2];
+    if (b > a) { m = b; at = ix[o + r2]; } else { m = a; at = ix[o + l]; }
+  }
+  // top-2 of the window [l, r]: (m1 at position at1) and the best of the rest, m2
+  __device__ __forceinline__ void top2(int l, int r, double& m1, int& at1, double& m2) const {
+    query(l, r, m1, at1);
+    double x, y;
+    int dummy;
+    query(l, at1 - 1, x, dummy);
+    query(at1 + 1, r, y, dummy);
+    m2 = fmax(x, y);
+  }
+};
+
+inline int window_levels(int L) { int q = 0; while ((2 << q) <= L) ++q; return q + 1; }
+
+inline size_t window_smem_bytes(int Lc, int Ld, int o_span) {
+  const size_t nw = kWinTile + o_span + 2;
+  const size_t nc = kWinTile + Lc, nd = kWinTile + Ld;
+  return sizeof(double) * nw + (sizeof(double) + sizeof(int)) * (window_levels(Lc) * nc + window_levels(Ld) * nd) + 64;
+}
+
+__device__ __forceinline__ double canon_single(const WinParams& p, const double* __restrict__ wt, int wbase, int i,
+                                               int a, double lam) {
+  // canonical candidate fl(fl(lambda p_a) + Wint), -inf if infeasible (tile is -inf padded)
+  const int o = __ldg(p.off + a);
+  const double wa = __ldg(p.w + a);
+  const int x = i + o - wbase;
+  const double wint = (wa == 0.0) ? wt[x] : __dadd_rn(__dmul_rn(__ldg(p.omw + a), wt[x]), __dmul_rn(wa, wt[x + 1]));
+  return __dadd_rn(__dmul_rn(lam, __ldg(p.act + a)), wint);
+}
+
+__device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
+  const int h = 1 << (q - 1), lim = t.n - (1 << q);
+  const double* pv = t.v + (q - 1) * t.n;
+  const int* pi = t.ix + (q - 1) * t.n;
+  double* nv = t.v + q * t.n;
+  int* ni = t.ix + q * t.n;
+  for (int x = tid; x <= lim; x += kWinThreads) {
+    const double a = pv[x], b = pv[x + h];
+    if (b > a) { nv[x] = b; ni[x] = pi[x + h]; } else { nv[x] = a; ni[x] = pi[x]; }
+  }
+}
+
+__global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p) {
+  extern __shared__ __align__(16) double wsm[];
+  const int k = blockIdx.y, i0 = blockIdx.x * kWinTile, tid = threadIdx.x;
+  const int nw = kWinTile + (p.o_max - p.o_min) + 2;
+  const int lc = p.pc + 1, ld = p.pd + 1;
+  RangeMax tc, td;
+  tc.n = kWinTile + p.Lc;                  // charge table: columns [i0 + 1, i0 + nc]
+  td.n = kWinTile + p.Ld;                  // discharge table: columns [i0 - Ld, i0 + kWinTile)
+  double* wt = wsm;                        // W over columns [wbase, wbase + nw)
+  tc.v = wt + nw;
+  td.v = tc.v + (size_t)lc * tc.n;
+  tc.ix = (int*)(td.v + (size_t)ld * td.n);
+  td.ix = tc.ix + (size_t)lc * tc.n;
+  __shared__ double red[kWinThreads / 32];
+
+  const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
+  const double lam = p.lambda_t[k];
+  const double beta_c = __ddiv_rn(__dmul_rn(lam, p.delta), p.eta_c);
+  const double beta_d = __dmul_rn(__dmul_rn(lam, p.delta), p.eta_d);
+  const int wbase = i0 + p.o_min;
+  double mx = 0.0;
+  for (int x = tid; x < nw; x += kWinThreads) {
+    const int col = wbase + x;
+    const double v = (col >= 0 && col < p.S) ? Wrow[col] : -INFINITY;
+    wt[x] = v;
+    if (v != -INFINITY) mx = fmax(mx, fabs(v));
+  }
+  __syncthreads();
+  // level 0: key(j) = W[j] - beta*j
+  for (int x = tid; x < tc.n; x += kWinThreads) {
+    const int j = i0 + 1 + x;
+    tc.v[x] = __dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j));
+    tc.ix[x] = x;
+  }
+  for (int x = tid; x < td.n; x += kWinThreads) {
+    const int j = i0 - p.Ld + x;
+    td.v[x] = __dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j));
+    td.ix[x] = x;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  const int top = p.pc > p.pd ? p.pc : p.pd;
+  for (int q = 1; q <= top; ++q) {
+    if (q <= p.pc) build_level(tc, q, tid);
+    if (q <= p.pd) build_level(td, q, tid);
+    __syncthreads();
+  }
+  double M = 0.0;
+#pragma unroll
+  for (int w = 0; w < kWinThreads / 32; ++w) M = fmax(M, red[w]);
+  const double etamin = fmin(p.eta_c, p.eta_d);
+  const double span = (double)(p.S + (p.o_max - p.o_min) + 2);
+  const double eps = 32.0 * 0x1p-53 * (M + fabs(lam) * p.delta * span / etamin + fabs(lam) * p.pbar);
+
+  const int i = i0 + tid;
+  if (i >= p.S) return;
+  // charge window j in [i+1, i+Lc] = table [x, x+Lc-1]; discharge j in [i-Ld, i-1] = table [x, x+Ld-1]
+  const int x = i - i0;
+  double mc1, mc2, md1, md2;
+  int xc, xd;
+  tc.top2(x, x + p.Lc - 1, mc1, xc, mc2);
+  td.top2(x, x + p.Ld - 1, md1, xd, md2);
+  const double bci = __dmul_rn(beta_c, (double)i), bdi = __dmul_rn(beta_d, (double)i);
+  // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
+  double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);
+  int a1 = p.a_z - ((i0 + 1 + xc) - i);
+  {
+    const double y1 = __dadd_rn(md1, bdi), y2 = __dadd_rn(md2, bdi);
+    if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
+    else b2 = fmax(b2, y1);
+  }
+  for (int s = 0; s < p.nsingle; ++s) {
+    const int a = __ldg(p.singles + s);
+    const double c = canon_single(p, wt, wbase, i, a, lam);
+    if (c > b1) { b2 = b1; b1 = c; a1 = a; }
+    else b2 = fmax(b2, c);
+  }
+  double best;
+  int arg;
+  if (__dsub_rn(b1, b2) > 2.0 * eps) {
+    arg = a1;
+    best = canon_single(p, wt, wbase, i, a1, lam);   // canonical value of the unique argmax
+  } else {
+    best = -INFINITY; arg = -1;                        // near tie: full canonical scan (rare)
+    for (int s = 0; s < p.nlive; ++s) {
+      const int a = __ldg(p.live + s);
+      const double c = canon_single(p, wt, wbase, i, a, lam);
+      if (c > best) { best = c; arg = a; }
+    }
+  }
+  p.V[(size_t)k * p.ld + i] = best;
+  p.pol[(size_t)k * p.S + i] = (int16_t)arg;
+}
+
+}  // namespace esdp

@@ -18,14 +18,18 @@ pytestmark = pytest.mark.gpu
 import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
 
 
-def _gpu(inst):
-    return E.Solver(inst, keep_values=True)
+def _gpu(inst, brute=False):
+    return E.Solver(inst, keep_values=True, force_brute=brute)
 
 
-def _compare_all(inst, nthreads=8, stages=None):
+def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None):
     pr = to_oracle(inst)
     ref = oracle.backward(pr, nthreads=nthreads)
-    with _gpu(inst) as s:
+    with _gpu(inst, brute) as s:
+        if expect_window is not None:
+            assert s.stencil_kind == int(expect_window)
+        if brute:
+            assert s.stencil_kind == 0
         J = s.backward()
         assert np.array_equal(s.actions(), oracle.actions(pr))
         ts = range(1, inst.T + 1) if stages is None else stages
@@ -40,8 +44,9 @@ def _compare_all(inst, nthreads=8, stages=None):
     return ref
 
 
+@pytest.mark.parametrize("brute", [False, True])
 @pytest.mark.parametrize("seed", range(40))
-def test_random_small_instances(seed):
+def test_random_small_instances(seed, brute):
     kind = [workloads.PAYOFF_LINEAR, workloads.PAYOFF_LINEAR_MINUS_G, workloads.PAYOFF_TABLE][seed % 3]
     inst = workloads.random_instance(seed, S_max=40 if seed % 2 else 600, T=4 + seed % 3, K=1 + seed % 4)
     S, A = oracle.dims(to_oracle(inst))
@@ -50,55 +55,71 @@ def test_random_small_instances(seed):
         inst.g = workloads.random_g(seed, A, 20.0)
     elif kind == workloads.PAYOFF_TABLE:
         inst.g = workloads.random_table(seed, inst.T, inst.K, A)
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
 
 
+@pytest.mark.parametrize("brute", [False, True])
 @pytest.mark.parametrize("name", ["cfg1a", "cfg1b", "cfg1b-rank1", "cfg1a-rank1"])
-def test_cfg1(name):
-    _compare_all(workloads.cfg1(name[4], rank1=name.endswith("rank1")))
+def test_cfg1(name, brute):
+    _compare_all(workloads.cfg1(name[4], rank1=name.endswith("rank1")), brute=brute,
+                 expect_window=None if brute else True)
 
 
-@pytest.mark.parametrize("S_over", [255, 256, 257, 511, 777, 1001, 2001])
-def test_tiles_and_ragged_tails(S_over):
-    """Several 256-column tiles plus a ragged tail; cfg2-like offsets."""
+@pytest.mark.parametrize("brute", [False, True])
+@pytest.mark.parametrize("S_over", [2, 50, 150, 255, 256, 257, 511, 777, 1001, 2001])
+def test_tiles_and_ragged_tails(S_over, brute):
+    """Several 256-column tiles plus a ragged tail; cfg2-like offsets (also S smaller than the
+    action span, where most actions are infeasible)."""
     inst = workloads.cfg2(T=6, K=7)
     inst.sbar = float(S_over - 1)
     inst.s0 = 0.0
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
 
 
-def test_edge_cases():
+@pytest.mark.parametrize("brute", [False, True])
+def test_edge_cases(brute):
     # T = 1, K = 1, minimal grid (S = 2)
     inst = workloads.random_instance(5, T=1, K=1, S_max=3)
     inst.sbar, inst.delta, inst.s0 = 1.0, 1.0, 0.0
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
     # pbar far larger than sbar: most actions infeasible everywhere (dead actions)
     inst = workloads.random_instance(6, T=3, K=2, S_max=5)
     inst.pbar = 50.0 * inst.sbar
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
     # user action grid: every action off the lattice (all interpolated), off-grid s0
     inst = workloads.random_instance(7, T=5, K=3, S_max=30)
     inst.actions = np.array([-0.93, -0.41, -0.07, 0.0, 0.13, 0.52, 0.99]) * inst.pbar
     inst.s0 = inst.sbar * 0.37
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
     # zero prices: every candidate ties, the smallest feasible action must be chosen
     inst = workloads.cfg1("b")
     inst.lam = np.zeros_like(inst.lam)
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
     # integer prices on an eta = 1 lattice: many exact ties
     inst = workloads.cfg1("a")
     inst.lam = np.round(inst.lam / 10.0)
-    _compare_all(inst)
+    _compare_all(inst, brute=brute)
 
 
 def test_cfg2_full_size():
     """BASELINE configs[1] at full size (T=288, S=1001, A=201, K=100), in the launch configuration
-    bench.py times: every V_t, W_t, pol_t compared element by element with the oracle."""
-    _compare_all(workloads.cfg2(), nthreads=16)
+    bench.py times (sliding-window stencil): every V_t, W_t, pol_t compared element by element."""
+    _compare_all(workloads.cfg2(), nthreads=16, expect_window=True)
+
+
+def test_cfg2_full_size_bruteforce():
+    _compare_all(workloads.cfg2(), nthreads=16, brute=True)
 
 
 def test_cfg2_rank1_full_size():
-    _compare_all(workloads.cfg2(rank1=True), nthreads=16)
+    _compare_all(workloads.cfg2(rank1=True), nthreads=16, expect_window=True)
+
+
+def test_cfg4_slice():
+    """BASELINE configs[3] per-stage shape (S=2001, A=401, K=200, a distinct P_t per stage) on a
+    6-stage horizon, compared in full."""
+    inst = workloads.cfg4(T=6)
+    _compare_all(inst, nthreads=16, expect_window=True)
 
 
 def test_cfg3_nonconcave_payoff_and_bids():

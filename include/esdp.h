@@ -58,8 +58,11 @@ enum {
                              for t > 1 and by the bid-curve calls); otherwise only V_1 is kept */
   ESDP_PROFILE = 2u,      /* record CUDA events around the contraction and stencil launches of ~16
                              sampled stages inside the backward graph (esdp_kernel_times) */
-  ESDP_FORCE_BRUTE = 4u   /* always use the brute-force max-plus stencil (every (i, a) cell), even
+  ESDP_FORCE_BRUTE = 4u,  /* always use the brute-force max-plus stencil (every (i, a) cell), even
                              where the exact sliding-window stencil applies (for testing) */
+  ESDP_PDL = 8u,          /* launch the per-stage kernels with programmatic dependent launch (opt-in:
+                             measured slower on B200 for this chain) */
+  ESDP_NO_DMMA = 16u      /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
 };
 
 typedef struct {
@@ -147,6 +150,10 @@ esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, dou
 /* Which max-plus stencil the context uses: 1 = exact sliding-window (recombining grid, linear payoff),
  * 0 = brute force over every (i, a) cell.  Both give bit-identical results. */
 esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
+
+/* Number of (i, k) rows, summed over all stages and contexts since the last call, for which the
+ * sliding-window stencil found a near tie and re-scanned every action canonically (then resets it). */
+esdp_status esdp_window_fallbacks(esdp_ctx* ctx, int64_t* count);
 
 /* Number of kernel launches one backward pass enqueues (for harness accounting). */
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);

@@ -29,6 +29,8 @@ ESDP_PAYOFF_LINEAR, ESDP_PAYOFF_LINEAR_MINUS_G, ESDP_PAYOFF_TABLE = 0, 1, 2
 ESDP_KEEP_VALUES = 1
 ESDP_PROFILE = 2
 ESDP_FORCE_BRUTE = 4
+ESDP_PDL = 8
+ESDP_NO_DMMA = 16
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
@@ -36,7 +38,7 @@ EXPORTED_SYMBOLS = [
     "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
-    "esdp_debug_time", "esdp_destroy", "esdp_last_error",
+    "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -86,6 +88,7 @@ def _load():
         "esdp_kernel_times": ([ctx, _dp, _dp], ctypes.c_int),
         "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
         "esdp_debug_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
+        "esdp_window_fallbacks": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
         "esdp_last_error": ([ctx], ctypes.c_char_p),
     }
@@ -247,6 +250,13 @@ def esdp_debug_time(ctx, what, reps=200) -> float:
     return us.value
 
 
+def esdp_window_fallbacks(ctx) -> int:
+    """Rows re-scanned canonically by the window stencil since the last call (resets the counter)."""
+    n = ctypes.c_int64()
+    _check(lib.esdp_window_fallbacks(ctx, ctypes.byref(n)), "esdp_window_fallbacks", ctx)
+    return n.value
+
+
 def esdp_destroy(ctx):
     lib.esdp_destroy(ctx)
 
@@ -255,12 +265,13 @@ class Solver:
     """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
-    def __init__(self, inst, keep_values=True, profile=False, force_brute=False):
+    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=False, dmma=True):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
                                (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
-                               | (ESDP_FORCE_BRUTE if force_brute else 0))
+                               | (ESDP_FORCE_BRUTE if force_brute else 0) | (ESDP_PDL if pdl else 0)
+                               | (0 if dmma else ESDP_NO_DMMA))
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
         self.stencil_kind = esdp_stencil_kind(self.ctx)
 

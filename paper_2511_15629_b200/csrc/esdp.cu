@@ -74,6 +74,7 @@ struct esdp_ctx {
   int64_t launches = 0;
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   int prof_stride = 1;
+  bool pdl = true;
   bool solved = false;
   std::string err;
 };
@@ -294,68 +295,102 @@ double* W_of(esdp_ctx* c, int t) {
   return keep(c) ? c->d_W + (size_t)(t - 1) * RS : c->d_W;
 }
 
-// Enqueue the 2T+1 launches of one backward pass on stream s.
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL) when pdl is set.
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// The contraction of stage t (t < T): W_t = P_t V_{t+1}.
+cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
+  const int K = c->K, S = c->S;
+  const int rows = (int)w_rows(c);
+  const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
+  if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
+    const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
+    return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
+                  (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, nct);
+  }
+  dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
+  return launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, Pt, (const double*)V_of(c, t + 1),
+                W_of(c, t), rows, K, S, c->ld);
+}
+
+// The max-plus stencil of stage t: V_t, pol_t from W_t (window or brute force).
+cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute) {
+  const int K = c->K, S = c->S;
+  const double* Wt = W_of(c, t);
+  int16_t* pol = c->d_pol + (size_t)(t - 1) * K * S;
+  const double* lam = c->d_lambda + (size_t)(t - 1) * K;
+  if (c->use_window && !force_brute) {
+    WinParams wp;
+    wp.W = Wt; wp.V = V_of(c, t); wp.pol = pol; wp.lambda_t = lam;
+    wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
+    wp.singles = c->d_singles; wp.live = c->d_live;
+    wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
+    wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
+    wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
+    wp.o_min = c->o_min; wp.o_max = c->o_max;
+    wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
+    wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
+    return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
+  }
+  StencilParams prm;
+  prm.W = Wt; prm.V = V_of(c, t); prm.pol = pol; prm.lambda_t = lam;
+  prm.act = c->d_act;
+  prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
+  prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
+  prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
+  prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
+  return launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl, prm);
+}
+
+cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
+  return launch(objective_kernel, dim3(1), dim3(128), 2 * sizeof(double) * c->K, s, pdl, (const double*)V_of(c, 1),
+                (const double*)c->d_pi, c->K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
+}
+
+// Enqueue the 2T launches of one backward pass on stream s (PDL between consecutive kernels).
 esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
-  const int T = c->T, K = c->K, S = c->S;
+  const int T = c->T;
   int64_t n = 0;
   const bool prof = !c->ev.empty();
+  const bool pdl = c->pdl;
   // ESDP_PROFILE: events around the kernels of every prof_stride-th stage only (a live sample of the
   // launch durations that keeps event nodes out of most of the graph)
+  auto sampled = [&](int t) { return prof && t % c->prof_stride == 0; };
   auto mark = [&](int t, int j) {
-    return (prof && t % c->prof_stride == 0)
-               ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal)
-               : cudaSuccess;
+    return sampled(t) ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
   };
+  bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   for (int t = T; t >= 1; --t) {
-    double* Wt = W_of(c, t);
     if (t == T) {
-      CUDA_OR_FAIL(c, cudaMemsetAsync(Wt, 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
+      CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, t), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
+      after_kernel = false;
     } else {
-      const int rows = (int)w_rows(c);
-      const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
-      dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
       CUDA_OR_FAIL(c, mark(t, 0));
-      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), Wt, rows, K, S, c->ld);
+      CUDA_OR_FAIL(c, launch_contract(c, t, s, pdl && after_kernel && !sampled(t)));
       CUDA_OR_FAIL(c, mark(t, 1));
+      after_kernel = true;
       ++n;
     }
-    StencilParams prm;
-    prm.W = Wt;
-    prm.V = V_of(c, t);
-    prm.pol = c->d_pol + (size_t)(t - 1) * K * S;
-    prm.lambda_t = c->d_lambda + (size_t)(t - 1) * K;
-    prm.act = c->d_act;
-    prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
-    prm.w = c->d_w;
-    prm.omw = c->d_omw;
-    prm.off = c->d_off;
-    prm.segs = c->d_segs;
-    prm.nseg = (int)c->segs.size();
-    prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
-    prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min;
-    prm.ld = c->ld;
-    dim3 grid((S + kTile - 1) / kTile, K);
     CUDA_OR_FAIL(c, mark(t, 2));
-    if (c->use_window) {
-      WinParams wp;
-      wp.W = Wt; wp.V = prm.V; wp.pol = prm.pol; wp.lambda_t = prm.lambda_t;
-      wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
-      wp.singles = c->d_singles; wp.live = c->d_live;
-      wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
-      wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
-      wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
-      wp.o_min = c->o_min; wp.o_max = c->o_max;
-      wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
-      dim3 wgrid((S + kWinTile - 1) / kWinTile, K);
-      window_stencil_kernel<<<wgrid, kWinThreads, c->window_smem, s>>>(wp);
-    } else {
-      stencil_kernel<<<grid, kStencilWarps * 32, c->stencil_smem, s>>>(prm);
-    }
+    CUDA_OR_FAIL(c, launch_stencil(c, t, s, pdl && after_kernel && !sampled(t), false));
     CUDA_OR_FAIL(c, mark(t, 3));
+    after_kernel = !sampled(t);
     ++n;
   }
-  const double* pi1 = c->d_pi;  // rank-1: row 0 of pi = pi_1
-  objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), pi1, K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
+  CUDA_OR_FAIL(c, launch_objective(c, s, pdl && after_kernel));
   ++n;
   CUDA_OR_FAIL(c, cudaGetLastError());
   c->launches = n;
@@ -390,6 +425,7 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1; c->ld = (c->S + 3) & ~3;
   c->pbar = pr->pbar; c->sbar = pr->sbar; c->s0 = pr->s0; c->eta_c = pr->eta_c; c->eta_d = pr->eta_d;
   c->delta = pr->delta; c->kind = pr->payoff_kind; c->rank1 = pr->P == nullptr; c->flags = pr->flags;
+  c->pdl = (pr->flags & ESDP_PDL) != 0;   // measured slower on B200 for this kernel chain: opt-in
   if (pr->A == 0) {
     paper_grid(pr->pbar, pr->eta_c, pr->eta_d, pr->delta, c->act);
     if ((long long)c->act.size() > kMaxA) { delete c; return fail(nullptr, ESDP_E_CONFIG, "A exceeds %d", kMaxA); }
@@ -681,6 +717,15 @@ esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* m
   return ESDP_OK;
 }
 
+esdp_status esdp_window_fallbacks(esdp_ctx* c, int64_t* count) {
+  if (!c || !count) return ESDP_E_STATE;
+  unsigned long long v = 0, z = 0;
+  CUDA_OR_FAIL(c, cudaMemcpyFromSymbol(&v, g_window_fallbacks, sizeof(v)));
+  CUDA_OR_FAIL(c, cudaMemcpyToSymbol(g_window_fallbacks, &z, sizeof(z)));
+  *count = (int64_t)v;
+  return ESDP_OK;
+}
+
 esdp_status esdp_stencil_kind(const esdp_ctx* c, int32_t* kind) {
   if (!c || !kind) return ESDP_E_STATE;
   *kind = c->use_window;
@@ -730,40 +775,11 @@ esdp_status esdp_debug_time(esdp_ctx* c, int32_t what, int32_t reps, double* us_
   cudaGraphExec_t ge = nullptr;
   CUDA_OR_FAIL(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int r = 0; r < reps; ++r) {
-    if (what == 0 && T > 1) {
-      const int rows = (int)w_rows(c);
-      const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
-      dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
-      contract_kernel<<<grid, kThreadsC, contract_smem_bytes(K), s>>>(Pt, V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld);
-    } else if (what == 1 || what == 2) {
-      const int saved = c->use_window;
-      if (what == 2) c->use_window = 0;
-      // reuse enqueue's stencil launch code through a one-stage helper
-      StencilParams prm;
-      prm.W = W_of(c, t); prm.V = V_of(c, t); prm.pol = c->d_pol + (size_t)(t - 1) * K * S;
-      prm.lambda_t = c->d_lambda + (size_t)(t - 1) * K; prm.act = c->d_act;
-      prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
-      prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
-      prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
-      prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
-      if (c->use_window) {
-        WinParams wp;
-        wp.W = prm.W; wp.V = prm.V; wp.pol = prm.pol; wp.lambda_t = prm.lambda_t;
-        wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
-        wp.singles = c->d_singles; wp.live = c->d_live;
-        wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
-        wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
-        wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
-        wp.o_min = c->o_min; wp.o_max = c->o_max;
-        wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
-        window_stencil_kernel<<<dim3((S + kWinTile - 1) / kWinTile, K), kWinThreads, c->window_smem, s>>>(wp);
-      } else {
-        stencil_kernel<<<dim3((S + kTile - 1) / kTile, K), kStencilWarps * 32, c->stencil_smem, s>>>(prm);
-      }
-      c->use_window = saved;
-    } else {
-      objective_kernel<<<1, 128, 2 * sizeof(double) * K, s>>>(V_of(c, 1), c->d_pi, K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
-    }
+    cudaError_t le;
+    if (what == 0 && T > 1) le = launch_contract(c, t, s, false);
+    else if (what == 1 || what == 2) le = launch_stencil(c, t, s, false, what == 2);
+    else le = launch_objective(c, s, false);
+    if (le != cudaSuccess) { cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g); return fail(c, ESDP_E_CUDA, "debug launch: %s", cudaGetErrorString(le)); }
   }
   cudaError_t ce = cudaStreamEndCapture(s, &g);
   if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "debug capture: %s", cudaGetErrorString(ce));

@@ -18,6 +18,11 @@ constexpr int kStencilWarps = 8;      // action chunks per block (one warp each)
 
 __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  // 8-column groups + 1 pad
 
+// Programmatic dependent launch (PDL): a kernel lets its successor be scheduled at once, and waits for
+// its predecessor's results only where it first reads them.  Both are no-ops without a PDL launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // A maximal run of actions whose offsets are consecutive integers decreasing by one and whose
 // interpolation weight is 0 ("recombining" interior of Eq. 10), or a single action.
 struct Seg {
@@ -80,6 +85,16 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
   double* ps = csm + (size_t)Kp * kColsC;  // [kRowsC][Kp]
   const int i0 = blockIdx.x * kColsC, r0 = blockIdx.y * kRowsC;
   const int tid = threadIdx.x;
+  pdl_trigger();
+  for (int r = 0; r < kRowsC; ++r) {  // P tile rows (inputs: staged before the dependency wait)
+    const bool rin = r0 + r < rows;
+    const double* src = Pt + (size_t)(r0 + r) * K;
+    for (int kp = tid; kp < Kp; kp += kThreadsC) {
+      if (rin && kp < K) cp_async8(ps + r * Kp + kp, src + kp);
+      else ps[r * Kp + kp] = 0.0;
+    }
+  }
+  pdl_wait();                          // V_{t+1} is the previous stencil's output
   {  // V tile: 16 two-double chunks per row, 8 rows per pass (no runtime division)
     const int c = 2 * (tid & 15);
     const bool in = i0 + c < ld;
@@ -88,14 +103,6 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
       double* dst = vs + kp * kColsC + c;
       if (kp < K && in) cp_async16(dst, src + (size_t)kp * ld);
       else { dst[0] = 0.0; dst[1] = 0.0; }
-    }
-  }
-  for (int r = 0; r < kRowsC; ++r) {  // P tile rows
-    const bool rin = r0 + r < rows;
-    const double* src = Pt + (size_t)(r0 + r) * K;
-    for (int kp = tid; kp < Kp; kp += kThreadsC) {
-      if (rin && kp < K) cp_async8(ps + r * Kp + kp, src + kp);
-      else ps[r * Kp + kp] = 0.0;
     }
   }
   cp_async_wait_all();
@@ -131,6 +138,82 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
   if (r0 + rr + 1 < rows) {
     if (i < S) Wt[(size_t)(r0 + rr + 1) * ld + i] = a10;
     if (i + 1 < S) Wt[(size_t)(r0 + rr + 1) * ld + i + 1] = a11;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Expectation on the FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Measured on B200
+// (tools/microbench/mb6.cu, 128k outputs with random, wide-range and cancelling operands): each DMMA
+// accumulates its 4 products as a sequential fma chain, so a K/4-long chain of DMMAs is bit-identical
+// to the canonical ascending-k' fma chain (R15) -- and it issues 256 FMAs per warp instruction instead
+// of 32, with 2 operand registers per lane per 4 k'.  Every parity test re-checks the bit equality.
+// One warp computes an 8 (rows k) x 16 (columns i) tile as two accumulators; operands are loaded
+// straight from global/L2 (no shared-memory staging), 8 k'-quads ahead of the MMA chain.
+// Fragment layout (PTX ISA, m8n8k4 .f64, row.col): A[8x4] lane -> A[lane/4][lane%4];
+// B[4x8] lane -> B[lane%4][lane/4]; C/D[8x8] lane -> C[lane/4][2(lane%4) + {0,1}].
+// ------------------------------------------------------------------------------------------------
+constexpr int kDmmaWarps = 4;
+constexpr int kDmmaChunk = 8;   // k'-quads prefetched per step
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const double* __restrict__ Pt,  // [rows][K]
+                                                                       const double* __restrict__ Vn,  // [K][ld]
+                                                                       double* __restrict__ Wt,        // [rows][ld]
+                                                                       int rows, int K, int S, int ld, int ncol_tiles) {
+  const int lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kDmmaWarps + (threadIdx.x >> 5);
+  const int r0 = (tile / ncol_tiles) * 8, i0 = (tile % ncol_tiles) * 16;
+  pdl_trigger();
+  if (r0 >= rows) { pdl_wait(); return; }
+  const int kq = lane & 3, g = lane >> 2;
+  const double* pa = Pt + (size_t)min(r0 + g, rows - 1) * K + kq;       // A: P[r0+g][4j+kq]
+  const int c0 = min(i0 + g, ld - 1), c1 = min(i0 + 8 + g, ld - 1);    // B: V[4j+kq][c]
+  const double* vb = Vn + (size_t)kq * ld;
+  const int nq = (K + 3) >> 2;
+  double a[kDmmaChunk], b0[kDmmaChunk], b1[kDmmaChunk];
+  // P (an input) is read before the dependency wait, V (the previous stencil's output) after it
+#pragma unroll
+  for (int q = 0; q < kDmmaChunk; ++q) a[q] = (q < nq && 4 * q + kq < K) ? __ldg(pa + 4 * q) : 0.0;
+  pdl_wait();
+#pragma unroll
+  for (int q = 0; q < kDmmaChunk; ++q) {
+    const bool in = q < nq && 4 * q + kq < K;
+    b0[q] = in ? __ldg(vb + (size_t)(4 * q) * ld + c0) : 0.0;
+    b1[q] = in ? __ldg(vb + (size_t)(4 * q) * ld + c1) : 0.0;
+  }
+  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+  for (int q0 = 0; q0 < nq; q0 += kDmmaChunk) {
+    double na[kDmmaChunk], nb0[kDmmaChunk], nb1[kDmmaChunk];
+#pragma unroll
+    for (int q = 0; q < kDmmaChunk; ++q) {
+      const int qq = q0 + kDmmaChunk + q;
+      const bool in = qq < nq && 4 * qq + kq < K;
+      na[q] = in ? __ldg(pa + 4 * qq) : 0.0;
+      nb0[q] = in ? __ldg(vb + (size_t)(4 * qq) * ld + c0) : 0.0;
+      nb1[q] = in ? __ldg(vb + (size_t)(4 * qq) * ld + c1) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kDmmaChunk; ++q) {
+      if (q0 + q < nq) {        // zero operands beyond K leave the chains unchanged
+        dmma_8x8x4(d00, d01, a[q], b0[q]);
+        dmma_8x8x4(d10, d11, a[q], b1[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kDmmaChunk; ++q) { a[q] = na[q]; b0[q] = nb0[q]; b1[q] = nb1[q]; }
+  }
+  const int r = r0 + g;
+  if (r < rows) {
+    const int c = i0 + 2 * kq;
+    double* wr = Wt + (size_t)r * ld;
+    if (c < S) wr[c] = d00;
+    if (c + 1 < S) wr[c + 1] = d01;
+    if (c + 8 < S) wr[c + 8] = d10;
+    if (c + 9 < S) wr[c + 9] = d11;
   }
 }
 
@@ -186,12 +269,7 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
   int* pa = (int*)(pv + kStencilWarps * skew(kTile));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.ld);
-  const int g0 = i0 + prm.o_min - kPad;  // global column of tile index 0
-  for (int j = tid; j < L; j += blockDim.x) {
-    int col = g0 + j;
-    ws[skew(j)] = (col >= 0 && col < prm.S) ? Wrow[col] : -INFINITY;
-  }
+  pdl_trigger();
   const double lam = prm.lambda_t[k];
   for (int a = tid; a < prm.A; a += blockDim.x) {
     double p;
@@ -199,6 +277,13 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
     else if (prm.kind == 1) p = __dsub_rn(__dmul_rn(lam, prm.act[a]), prm.g[a]);        // lambda p - g
     else p = __dmul_rn(lam, prm.act[a]);                                                 // lambda p
     pay[a] = p;
+  }
+  pdl_wait();                          // W_t is the previous contraction's output
+  const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.ld);
+  const int g0 = i0 + prm.o_min - kPad;  // global column of tile index 0
+  for (int j = tid; j < L; j += blockDim.x) {
+    int col = g0 + j;
+    ws[skew(j)] = (col >= 0 && col < prm.S) ? Wrow[col] : -INFINITY;
   }
   __syncthreads();
 
@@ -282,6 +367,7 @@ inline size_t stencil_smem_bytes(int A, int o_span) {
 __global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int ld,
                                  int f, double w0, int on_grid, double* __restrict__ J) {
   extern __shared__ double vk[];  // [2][K]: V_1(s0, k) and pi_1[k], gathered in parallel
+  pdl_wait();
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const double* row = V1 + (size_t)k * ld;
     vk[k] = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));

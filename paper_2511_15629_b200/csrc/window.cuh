@@ -7,11 +7,13 @@
 //     cand(i, o) = lambda*p(o) + W[i+o]  ~=  key(j) + beta*i,   j = i + o,   key(j) = W[j] - beta*j,
 // with beta_c = lambda*delta/eta_c on the charge side and beta_d = lambda*delta*eta_d on the discharge
 // side: a sliding-window maximum of a per-column key over a fixed-width window.  Each side keeps a
-// sparse table of (max, position) over power-of-two ranges: a window maximum is two lookups, and the
-// runner-up (needed for the exactness test) is the maximum of the window minus its argmax.
+// sparse table of packed (key, position) maxima over power-of-two ranges: a window maximum is two
+// lookups, and the runner-up (needed for the exactness test) is the maximum of the window minus its
+// argmax (two more).
 //
 // Exactness.  The key form rounds differently from the canonical candidate fl(fl(lambda p) + W), by
-// at most eps = 32 u (max|W| + |lambda| delta (S + span) / min(eta) + |lambda| pbar).
+// at most eps = 32 u (max|W| + |lambda| delta (S + span) / min(eta) + |lambda| pbar) plus the packed-key
+// truncation 2^-41 (max|W| + |lambda| delta (S + span) / min(eta)).
 // The remaining actions (zero action, the interpolated endpoints +-pbar, anything irregular) are
 // evaluated canonically.  If the best approximate value beats the second best by more than 2 eps, the
 // canonical argmax is that action and is unique; V is then recomputed canonically from it.  Otherwise
@@ -23,6 +25,7 @@
 namespace esdp {
 
 constexpr int kWinTile = 256;     // output columns per block
+__device__ unsigned long long g_window_fallbacks;  // rows that needed the full canonical scan (diagnostic)
 constexpr int kWinThreads = 256;  // one output column per thread in the query phase
 
 struct WinParams {
@@ -34,31 +37,39 @@ struct WinParams {
   int a_z, Lc, Ld, pc, pd;  // zero action; run lengths; sparse-table levels (2^pc <= Lc < 2^(pc+1))
   int o_min, o_max;         // tile halo over all live actions
   double delta, eta_c, eta_d, pbar;
+  double dc, dd;            // delta / eta_c and delta * eta_d (for the approximate keys only)
 };
 
-// Sparse table of (max, position) over power-of-two ranges: level q entry x covers [x, x + 2^q).
-// All levels are kept so that any range [l, r] is answered with two lookups (overlap is harmless for
-// a maximum).  The second best of a window is the maximum of the window with the argmax removed:
-// two more range queries.
+// Packed keys: an order-preserving 64-bit image of the (approximate) value with its table position in
+// the low 10 bits.  One unsigned max then yields the maximum and where it is.  Clearing the low bits
+// lowers the value by less than 1024 ulp; that truncation is added to the exactness margin below.
+constexpr unsigned long long kPosMask = 1023ull;
+
+__device__ __forceinline__ unsigned long long ord64(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord64(unsigned long long k) {  // value part 0: -inf / empty range
+  k &= ~kPosMask;
+  if (k == 0ull) return -INFINITY;
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+// packed key of a value at table position pos; -inf packs to the bare position (below every finite key)
+__device__ __forceinline__ unsigned long long pack_key(double v, int pos) {
+  return (v == -INFINITY ? 0ull : (ord64(v) & ~kPosMask)) | (unsigned long long)pos;
+}
+
+// Sparse table over power-of-two ranges: level q entry x = max of packed keys in [x, x + 2^q).
 struct RangeMax {
-  double* v;   // [levels][n]
-  int* ix;     // [levels][n] table positions
+  unsigned long long* v;   // [levels][n]
   int n;
-  __device__ __forceinline__ void query(int l, int r, double& m, int& at) const {
-    if (l > r) { m = -INFINITY; at = -1; return; }
+  __device__ __forceinline__ unsigned long long query(int l, int r) const {   // 0 if l > r
+    if (l > r) return 0ull;
     const int q = 31 - __clz(r - l + 1);
-    const int o = q * n, r2 = r - (1 << q) + 1;
-    const double a = v[o + l], b = v[o + r2];
-    if (b > a) { m = b; at = ix[o + r2]; } else { m = a; at = ix[o + l]; }
-  }
-  // top-2 of the window [l, r]: (m1 at position at1) and the best of the rest, m2
-  __device__ __forceinline__ void top2(int l, int r, double& m1, int& at1, double& m2) const {
-    query(l, r, m1, at1);
-    double x, y;
-    int dummy;
-    query(l, at1 - 1, x, dummy);
-    query(at1 + 1, r, y, dummy);
-    m2 = fmax(x, y);
+    const unsigned long long* row = v + q * n;
+    return umax64(row[l], row[r - (1 << q) + 1]);
   }
 };
 
@@ -67,7 +78,7 @@ inline int window_levels(int L) { int q = 0; while ((2 << q) <= L) ++q; return q
 inline size_t window_smem_bytes(int Lc, int Ld, int o_span) {
   const size_t nw = kWinTile + o_span + 2;
   const size_t nc = kWinTile + Lc, nd = kWinTile + Ld;
-  return sizeof(double) * nw + (sizeof(double) + sizeof(int)) * (window_levels(Lc) * nc + window_levels(Ld) * nd) + 64;
+  return sizeof(double) * nw + sizeof(unsigned long long) * (window_levels(Lc) * nc + window_levels(Ld) * nd) + 64;
 }
 
 __device__ __forceinline__ double canon_single(const WinParams& p, const double* __restrict__ wt, int wbase, int i,
@@ -82,35 +93,38 @@ __device__ __forceinline__ double canon_single(const WinParams& p, const double*
 
 __device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
   const int h = 1 << (q - 1), lim = t.n - (1 << q);
-  const double* pv = t.v + (q - 1) * t.n;
-  const int* pi = t.ix + (q - 1) * t.n;
-  double* nv = t.v + q * t.n;
-  int* ni = t.ix + q * t.n;
-  for (int x = tid; x <= lim; x += kWinThreads) {
-    const double a = pv[x], b = pv[x + h];
-    if (b > a) { nv[x] = b; ni[x] = pi[x + h]; } else { nv[x] = a; ni[x] = pi[x]; }
-  }
+  const unsigned long long* pv = t.v + (q - 1) * t.n;
+  unsigned long long* nv = t.v + q * t.n;
+  for (int x = tid; x <= lim; x += kWinThreads) nv[x] = umax64(pv[x], pv[x + h]);
+}
+
+// top-2 of the window [l, r] of table t: best (value, table position) and the runner-up value
+__device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, double& m1, int& pos, double& m2) {
+  const unsigned long long k1 = t.query(l, r);
+  pos = (int)(k1 & kPosMask);
+  m1 = unord64(k1);
+  m2 = unord64(umax64(t.query(l, pos - 1), t.query(pos + 1, r)));
 }
 
 __global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
   const int k = blockIdx.y, i0 = blockIdx.x * kWinTile, tid = threadIdx.x;
   const int nw = kWinTile + (p.o_max - p.o_min) + 2;
-  const int lc = p.pc + 1, ld = p.pd + 1;
+  const int lc = p.pc + 1, ldl = p.pd + 1;
   RangeMax tc, td;
   tc.n = kWinTile + p.Lc;                  // charge table: columns [i0 + 1, i0 + nc]
   td.n = kWinTile + p.Ld;                  // discharge table: columns [i0 - Ld, i0 + kWinTile)
   double* wt = wsm;                        // W over columns [wbase, wbase + nw)
-  tc.v = wt + nw;
+  tc.v = (unsigned long long*)(wt + nw);
   td.v = tc.v + (size_t)lc * tc.n;
-  tc.ix = (int*)(td.v + (size_t)ld * td.n);
-  td.ix = tc.ix + (size_t)lc * tc.n;
   __shared__ double red[kWinThreads / 32];
 
+  pdl_trigger();
   const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
   const double lam = p.lambda_t[k];
-  const double beta_c = __ddiv_rn(__dmul_rn(lam, p.delta), p.eta_c);
-  const double beta_d = __dmul_rn(__dmul_rn(lam, p.delta), p.eta_d);
+  const double beta_c = __dmul_rn(lam, p.dc);      // lambda delta / eta_c (any few-ulp rounding: see eps)
+  const double beta_d = __dmul_rn(lam, p.dd);      // lambda delta eta_d
+  pdl_wait();                          // W_t is the previous contraction's output
   const int wbase = i0 + p.o_min;
   double mx = 0.0;
   for (int x = tid; x < nw; x += kWinThreads) {
@@ -120,16 +134,14 @@ __global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p
     if (v != -INFINITY) mx = fmax(mx, fabs(v));
   }
   __syncthreads();
-  // level 0: key(j) = W[j] - beta*j
+  // level 0: packed key(j) = W[j] - beta*j, position x
   for (int x = tid; x < tc.n; x += kWinThreads) {
     const int j = i0 + 1 + x;
-    tc.v[x] = __dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j));
-    tc.ix[x] = x;
+    tc.v[x] = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
   }
   for (int x = tid; x < td.n; x += kWinThreads) {
     const int j = i0 - p.Ld + x;
-    td.v[x] = __dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j));
-    td.ix[x] = x;
+    td.v[x] = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
@@ -141,49 +153,75 @@ __global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p
     if (q <= p.pd) build_level(td, q, tid);
     __syncthreads();
   }
+  (void)ldl;
   double M = 0.0;
 #pragma unroll
   for (int w = 0; w < kWinThreads / 32; ++w) M = fmax(M, red[w]);
-  const double etamin = fmin(p.eta_c, p.eta_d);
   const double span = (double)(p.S + (p.o_max - p.o_min) + 2);
-  const double eps = 32.0 * 0x1p-53 * (M + fabs(lam) * p.delta * span / etamin + fabs(lam) * p.pbar);
+  const double bmax = fabs(lam) * p.delta * span / fmin(p.eta_c, p.eta_d);
+  // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
+  // the <1024-ulp truncation of the packed keys (|key| <= M + bmax)
+  const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar) + 0x1p-41 * (M + bmax);
 
   const int i = i0 + tid;
-  if (i >= p.S) return;
-  // charge window j in [i+1, i+Lc] = table [x, x+Lc-1]; discharge j in [i-Ld, i-1] = table [x, x+Ld-1]
-  const int x = i - i0;
-  double mc1, mc2, md1, md2;
-  int xc, xd;
-  tc.top2(x, x + p.Lc - 1, mc1, xc, mc2);
-  td.top2(x, x + p.Ld - 1, md1, xd, md2);
-  const double bci = __dmul_rn(beta_c, (double)i), bdi = __dmul_rn(beta_d, (double)i);
-  // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
-  double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);
-  int a1 = p.a_z - ((i0 + 1 + xc) - i);
-  {
-    const double y1 = __dadd_rn(md1, bdi), y2 = __dadd_rn(md2, bdi);
-    if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
-    else b2 = fmax(b2, y1);
-  }
-  for (int s = 0; s < p.nsingle; ++s) {
-    const int a = __ldg(p.singles + s);
-    const double c = canon_single(p, wt, wbase, i, a, lam);
-    if (c > b1) { b2 = b1; b1 = c; a1 = a; }
-    else b2 = fmax(b2, c);
-  }
-  double best;
-  int arg;
-  if (__dsub_rn(b1, b2) > 2.0 * eps) {
-    arg = a1;
-    best = canon_single(p, wt, wbase, i, a1, lam);   // canonical value of the unique argmax
-  } else {
-    best = -INFINITY; arg = -1;                        // near tie: full canonical scan (rare)
-    for (int s = 0; s < p.nlive; ++s) {
-      const int a = __ldg(p.live + s);
+  const bool valid = i < p.S;
+  const int lane = tid & 31;
+  double best = -INFINITY;
+  int arg = -1;
+  bool near_tie = false;
+  if (valid) {
+    // charge window j in [i+1, i+Lc] = table [x, x+Lc-1]; discharge j in [i-Ld, i-1] = table [x, x+Ld-1]
+    const int x = i - i0;
+    double mc1, mc2, md1, md2;
+    int xc, xd;
+    window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
+    window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
+    const double bci = __dmul_rn(beta_c, (double)i), bdi = __dmul_rn(beta_d, (double)i);
+    // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
+    double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);
+    int a1 = p.a_z - ((i0 + 1 + xc) - i);
+    {
+      const double y1 = __dadd_rn(md1, bdi), y2 = __dadd_rn(md2, bdi);
+      if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
+      else b2 = fmax(b2, y1);
+    }
+    for (int s = 0; s < p.nsingle; ++s) {
+      const int a = __ldg(p.singles + s);
       const double c = canon_single(p, wt, wbase, i, a, lam);
-      if (c > best) { best = c; arg = a; }
+      if (c > b1) { b2 = b1; b1 = c; a1 = a; }
+      else b2 = fmax(b2, c);
+    }
+    if (__dsub_rn(b1, b2) > 2.0 * eps) {
+      arg = a1;
+      best = canon_single(p, wt, wbase, i, a1, lam);   // canonical value of the unique argmax
+    } else {
+      near_tie = true;
     }
   }
+  // near ties (rare; every row for degenerate data such as zero prices): the whole warp re-scans the
+  // row canonically, 32 actions at a time, and reduces (value desc, index asc) -- the smallest index
+  // among exact ties, as in the oracle's ascending scan with a strict '>'.
+  unsigned need = __ballot_sync(0xffffffffu, near_tie);
+  while (need) {
+    const int src = __ffs(need) - 1;
+    need &= need - 1;
+    const int ii = __shfl_sync(0xffffffffu, i, src);
+    double v = -INFINITY;
+    int va = 0x7fffffff;
+    for (int s = lane; s < p.nlive; s += 32) {
+      const int a = __ldg(p.live + s);
+      const double c = canon_single(p, wt, wbase, ii, a, lam);
+      if (c > v) { v = c; va = a; }          // ascending a within the lane
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, sh);
+      const int oa = __shfl_xor_sync(0xffffffffu, va, sh);
+      if (ov > v || (ov == v && oa < va)) { v = ov; va = oa; }
+    }
+    if (lane == src) { best = v; arg = va; atomicAdd(&g_window_fallbacks, 1ull); }
+  }
+  if (!valid) return;
   p.V[(size_t)k * p.ld + i] = best;
   p.pol[(size_t)k * p.S + i] = (int16_t)arg;
 }

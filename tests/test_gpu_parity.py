@@ -18,14 +18,14 @@ pytestmark = pytest.mark.gpu
 import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
 
 
-def _gpu(inst, brute=False):
-    return E.Solver(inst, keep_values=True, force_brute=brute)
+def _gpu(inst, brute=False, dmma=True):
+    return E.Solver(inst, keep_values=True, force_brute=brute, dmma=dmma)
 
 
-def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None):
+def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None, dmma=True):
     pr = to_oracle(inst)
     ref = oracle.backward(pr, nthreads=nthreads)
-    with _gpu(inst, brute) as s:
+    with _gpu(inst, brute, dmma) as s:
         if expect_window is not None:
             assert s.stencil_kind == int(expect_window)
         if brute:
@@ -56,6 +56,15 @@ def test_random_small_instances(seed, brute):
     elif kind == workloads.PAYOFF_TABLE:
         inst.g = workloads.random_table(seed, inst.T, inst.K, A)
     _compare_all(inst, brute=brute)
+
+
+@pytest.mark.parametrize("dmma", [True, False])
+@pytest.mark.parametrize("K", [8, 13, 30, 37, 64])
+def test_expectation_tensor_cores_bitexact(K, dmma):
+    """FP64 DMMA (mma.sync m8n8k4) expectation: K not a multiple of 4, rows not a multiple of 8, ragged
+    columns; bit-identical to the oracle's sequential fma chain (and the DFMA kernel likewise)."""
+    inst = workloads.random_instance(1000 + K, T=4, K=K, S_max=300, rank1=False)
+    _compare_all(inst, dmma=dmma)
 
 
 @pytest.mark.parametrize("brute", [False, True])
@@ -109,6 +118,10 @@ def test_cfg2_full_size():
 
 def test_cfg2_full_size_bruteforce():
     _compare_all(workloads.cfg2(), nthreads=16, brute=True)
+
+
+def test_cfg2_full_size_dfma_expectation():
+    _compare_all(workloads.cfg2(), nthreads=16, dmma=False)
 
 
 def test_cfg2_rank1_full_size():

@@ -1,24 +1,33 @@
-"""Warm per-kernel launch times on cfg2 (diagnostic): python tools/ktime.py"""
-import os, sys
+"""Warm per-kernel launch times and backward-graph time on cfg2 (diagnostic): python tools/ktime.py"""
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2511_15629_b200 as E
 import workloads
-import time
 
-inst = workloads.cfg2()
-for keep in (True,):
-    s = E.Solver(inst, keep_values=keep)
-    s.backward()
-    names = ["contract", "stencil(" + ("window" if s.stencil_kind else "brute") + ")", "stencil(brute)", "objective"]
-    for w in range(4):
-        print(f"{names[w]:18s} {E.esdp_debug_time(s.ctx, w, 200):8.2f} us/launch")
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+inst = workloads.cfg2() if cfg == "cfg2" else workloads.cfg2(rank1=True)
+
+
+def bw_time(s, n=10):
     for _ in range(3):
         s.backward()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(10):
+    for _ in range(n):
         s.backward()
     torch.cuda.synchronize()
-    print(f"backward graph: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms  ({(time.perf_counter() - t0) / 10 / inst.T * 1e6:.2f} us/stage)")
-    s.close()
+    return (time.perf_counter() - t0) / n * 1e3
+
+
+for keep in (True, False):
+    for brute in (False, True):
+        for pdl, dmma in ((False, True), (False, False), (True, True)):
+            s = E.Solver(inst, keep_values=keep, force_brute=brute, pdl=pdl, dmma=dmma)
+            ms = bw_time(s)
+            line = f"keep={int(keep)} stencil={'brute ' if not s.stencil_kind else 'window'} pdl={int(pdl)} dmma={int(dmma)}: backward {ms:.3f} ms ({ms / inst.T * 1e3:.2f} us/stage)"
+            if keep and not pdl:
+                line += "  | warm us/launch: contract %.2f stencil %.2f objective %.2f" % (
+                    E.esdp_debug_time(s.ctx, 0), E.esdp_debug_time(s.ctx, 1), E.esdp_debug_time(s.ctx, 3))
+            print(line, flush=True)
+            s.close()

@@ -10,8 +10,10 @@ The metric is BASELINE.json's: DP cell-updates/s = T*S*K*A / step time (whole jo
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun: every rank solves its own instance (independent price draws, the
-cfg5-style instance sharding of SURVEY.md §8(e).3) with no data-path collective -> "scaling": "weak".
+N > 1 is launched by torchrun.  --mode instances (default): every rank solves its own instance
+(independent price draws, the cfg5-style instance sharding of SURVEY.md §8(e).3) with no data-path
+collective -> "scaling": "weak".  --mode kpart: one instance, price-state rows split across ranks with an
+NCCL all-gather of V_t every stage -> "scaling": "strong".
 --impl reference times the FP64 CPU oracle (oracle/) on this host's cores on a bounded sample of the
 same workload (rank 0 only).
 """
@@ -117,6 +119,8 @@ WORKLOAD = {
 
 
 def run_ours(args):
+    import ctypes
+
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -130,33 +134,55 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    inst = _instance(args, rank)
-    solver = E.Solver(inst, keep_values=True, profile=args.kernel_events)
+    kpart = args.mode == "kpart"
+    # instances: every rank its own instance (weak scaling); kpart: one instance, K rows split (strong)
+    inst = _instance(args, 0 if kpart else rank)
+    dist_arg = None
+    if kpart:
+        nid = [E.esdp_nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(nid, src=0)
+        dist_arg = (world, rank, nid[0])
+    solver = E.Solver(inst, keep_values=True, profile=bool(args.kernel_events), dist=dist_arg)
     T, S, A, K = solver.T, solver.S, solver.A, solver.K
     cells = T * S * K * A
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
 
-    # a6: bid-curve requests for every (t, i) at k = K/2, device-resident
-    kb = K // 2
+    # a6: bid-curve requests for every (t, i) at one of this rank's price states, device-resident
+    k_lo, k_cnt, _ = E.esdp_partition(K, world if kpart else 1, rank if kpart else 0)
+    kb = k_lo + k_cnt // 2
     tt, ii = np.meshgrid(np.arange(1, T + 1, dtype=np.int32), np.arange(S, dtype=np.int32), indexing="ij")
     req = np.stack([tt.ravel(), ii.ravel(), np.full(T * S, kb, np.int32)], 1).astype(np.int32)
+    if kpart and k_cnt == 0:
+        req = req[:0]
     n_bid = req.shape[0]
     cap = A
     req_d = torch.from_numpy(req).to(dev)
-    nv_d = torch.empty(n_bid, dtype=torch.int32, device=dev)
-    vert_d = torch.empty(n_bid * cap, dtype=torch.int16, device=dev)
-    pr_d = torch.empty(n_bid * cap, dtype=torch.float64, device=dev)
-    per_d = torch.empty(args.paths, dtype=torch.float64, device=dev)
+    nv_d = torch.empty(max(n_bid, 1), dtype=torch.int32, device=dev)
+    vert_d = torch.empty(max(n_bid, 1) * cap, dtype=torch.int16, device=dev)
+    pr_d = torch.empty(max(n_bid, 1) * cap, dtype=torch.float64, device=dev)
+    n_paths = args.paths // world if kpart else args.paths      # kpart: the paths are shared out too
+    per_d = torch.empty(n_paths, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def step(j):
+    def step(j, marks=None):
+        if marks:
+            marks[0].record(stream)
         E.esdp_backward_async(solver.ctx, sp)
-        E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
-                             None, pr_d.data_ptr(), sp)
-        E.esdp_simulate_dev(solver.ctx, args.paths, 1234 + j, per_d.data_ptr(), sp)
+        if marks:
+            marks[1].record(stream)
+        if n_bid:
+            E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
+                                 None, pr_d.data_ptr(), sp)
+        if marks:
+            marks[2].record(stream)
+        E.esdp_simulate_dev(solver.ctx, n_paths, 1234 + j + 7919 * rank, per_d.data_ptr(), sp)
+        if marks:
+            marks[3].record(stream)
 
-    launches_per_step = E.esdp_launch_count(solver.ctx) + 2
+    launches_per_step = E.esdp_launch_count(solver.ctx) + (1 if n_bid else 0) + 1
     with torch.cuda.stream(stream):
         for j in range(args.warmup):
             flush.fill_(float(j))
@@ -167,40 +193,40 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         clocks = ClockSampler(local)
         clocks.start()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        tot_ms, con_ms, sten_ms = 0.0, 0.0, 0.0
+        marks = [[ev() for _ in range(4)] for _ in range(args.steps)]
+        part = np.zeros(3)
+        phases = np.zeros(2)
         for j in range(args.steps):
             flush.fill_(float(j))          # L2 flush between timed steps (outside the events)
-            evs[j][0].record(stream)
-            step(j)
-            evs[j][1].record(stream)
+            step(j, marks[j])
             stream.synchronize()
+            m = marks[j]
+            part += [m[0].elapsed_time(m[1]), m[1].elapsed_time(m[2]), m[2].elapsed_time(m[3])]
             if args.kernel_events:
-                c_ms, s_ms = E.esdp_kernel_times(solver.ctx)   # per launch, sampled stages
-                con_ms += c_ms * (T - 1)
-                sten_ms += s_ms * T
-            tot_ms += evs[j][0].elapsed_time(evs[j][1])
+                phases += E.esdp_kernel_times(solver.ctx)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         clk = clocks.stop()
     J = E.esdp_objective(solver.ctx)
     sim_mean = float(per_d.mean().item())
-    t_all = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    part /= args.steps
+    phases /= args.steps
+    t_all = torch.tensor([part.sum()], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-    ms_step = float(t_all.item()) / args.steps
-    value = cells * world / (ms_step * 1e-3)
+    ms_step = float(t_all.item())
+    units = cells * (1 if kpart else world)
+    value = units / (ms_step * 1e-3)
 
     # --- end to end through the public API with host buffers (pinned), H2D/D2H inside the region
     lam_h = torch.from_numpy(np.ascontiguousarray(inst.lam)).pin_memory()
     P_h = torch.from_numpy(np.ascontiguousarray(inst.P)).pin_memory() if inst.P is not None else None
     pi_h = torch.from_numpy(np.ascontiguousarray(inst.pi)).pin_memory()
     h2d = lam_h.numel() * 8 + (P_h.numel() * 8 if P_h is not None else 0) + pi_h.numel() * 8
-    import ctypes
     dp = ctypes.POINTER(ctypes.c_double)
     as_p = lambda t: None if t is None else ctypes.cast(t.data_ptr(), dp)
-    m, v = ctypes.c_double(), ctypes.c_double()
+    m_, v_ = ctypes.c_double(), ctypes.c_double()
     Jh = ctypes.c_double()
     e2e_times = []
     for j in range(args.warmup + args.steps):
@@ -210,27 +236,32 @@ def run_ours(args):
         st = E.lib.esdp_load(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
         assert st == 0, E.esdp_last_error(solver.ctx)
         assert E.lib.esdp_backward(solver.ctx, sp, ctypes.byref(Jh)) == 0
-        E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
-                             None, pr_d.data_ptr(), sp)
-        assert E.lib.esdp_simulate(solver.ctx, args.paths, 99 + j, ctypes.byref(m), ctypes.byref(v), None) == 0
+        if n_bid:
+            E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
+                                 None, pr_d.data_ptr(), sp)
+        assert E.lib.esdp_simulate(solver.ctx, n_paths, 99 + j, ctypes.byref(m_), ctypes.byref(v_), None) == 0
         t1 = time.perf_counter()
         if j >= args.warmup:
             e2e_times.append(t1 - t0)
     e2e_t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = cells * world / (float(e2e_t.item()) / args.steps)
+    e2e_value = units / (float(e2e_t.item()) / args.steps)
     d2h = 8 + 16  # J, (mean, var)
 
     peaks, peak_kind = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp64_peak = n_sm * FP64_LANES_PER_SM * sm_max * 1e6 / 1e9          # Gop/s
-    st_launch_ms = max(sten_ms, 1e-9) / (args.steps * T)
-    ops_per_launch = 2.0 * K * S * A                                    # 1 DADD + 1 compare per cell
-    achieved = ops_per_launch / (st_launch_ms * 1e-3) / 1e9
-    hbm_bytes_launch = 18.0 * K * S                                     # read W 8 B, write V 8 B + pol 2 B
-    hbm_ach = hbm_bytes_launch / (st_launch_ms * 1e-3) / 1e9
+    fp64_peak = n_sm * FP64_LANES_PER_SM * sm_max * 1e6 / 1e9          # G FP64 instr/s
+    # algorithmic FP64 work of one backward on this rank: 2 per cell (add + max),
+    # K FMA per (k, s) element of the expectation (T-1 stages); rows owned by this rank
+    rows_here = k_cnt if kpart else K
+    algo_ops = 2.0 * T * S * rows_here * A + (T - 1) * S * rows_here * (1 if inst.P is None else K) * 1.0
+    bw_ms = part[0]
+    achieved = algo_ops / (bw_ms * 1e-3) / 1e9
+    hbm_bytes = 18.0 * T * rows_here * S                               # read W, write V + pol per (k, s, t)
+    hbm_ach = hbm_bytes / (bw_ms * 1e-3) / 1e9
+    plan = E.esdp_stencil_kind(solver.ctx)
     out = None
     if rank == 0:
         out = {
@@ -241,32 +272,37 @@ def run_ours(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_step,
-            "full_solve_s": ms_step / 1e3,
+            "full_solve_s": part[0] / 1e3,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if kpart else "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded ISO-NE-shaped Markov price chain, DESIGN.md §4)",
             "config": {"workload": WORKLOAD[args.config], "T": T, "S": S, "A": A, "K": K,
-                       "bid_curves_per_step": n_bid, "sim_paths_per_step": args.paths,
+                       "bid_curves_per_step": n_bid, "sim_paths_per_step": n_paths,
                        "l2": "flushed between timed steps (256 MiB write outside the step events)",
-                       "parallelism": f"instance-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU"},
+                       "parallelism": (f"K-partitioned x{world} (NCCL all-gather of V_t per stage)" if kpart else
+                                       f"instance-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU"),
+                       "plan": {"stencil": "window" if plan & 1 else "brute", "backward": "persistent" if plan & 2 else "graph"}},
             "gpu_launches": launches_per_step * args.steps,
-            "kernel_ms_per_step": {"stencil": sten_ms / args.steps, "contract": con_ms / args.steps,
-                                   "other": ms_step - (sten_ms + con_ms) / args.steps},
-            "roofline": {"bound": "alu", "kernel": "stencil_kernel (max-plus + argmax, FP64 pipe)",
-                         "achieved": achieved, "peak": fp64_peak, "unit": "FP64 Gop/s",
+            "ms_per_part": {"backward": part[0], "bidcurves": part[1], "simulate": part[2]},
+            "backward_phase_ms": {"expectation": phases[0], "stencil": phases[1]} if args.kernel_events else None,
+            "roofline": {"bound": "alu",
+                         "kernel": "backward (%s)" % ("persistent cooperative kernel" if plan & 2 else "graph of 2T kernels"),
+                         "achieved": achieved, "peak": fp64_peak, "unit": "G FP64 instr/s",
                          "frac": achieved / fp64_peak, "traffic": None,
                          "peak_note": f"{n_sm} SMs x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz "
                                       f"(sm_max_mhz from MEASURED_PEAKS.json: {peak_kind})",
-                         "work_per_launch": f"2 FP64 ops x K*S*A = {ops_per_launch:.4g}"},
+                         "work_per_launch": f"algorithmic FP64 instr: 2 per cell x T*S*K*A + K per (k,s) x (T-1)*S*K "
+                                            f"= {algo_ops:.4g}"},
             "roofline_hbm_literal": {"bound": "hbm", "achieved": hbm_ach, "peak": float(peaks["hbm_gbs"]),
                                      "unit": "GB/s", "frac": hbm_ach / float(peaks["hbm_gbs"]),
-                                     "bytes_per_launch": hbm_bytes_launch},
+                                     "bytes_per_launch": hbm_bytes},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "J": J, "sim_mean_profit": sim_mean,
+            "window_fallback_rows": E.esdp_window_fallbacks(solver.ctx),
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(inst, budget_s=args.cpu_budget)
@@ -346,7 +382,9 @@ def main():
     ap.add_argument("--ref-stages", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-events", type=int, default=1,
-                    help="CUDA events around the kernels of ~16 sampled stages per step (live launch durations)")
+                    help="per-phase device timers inside the backward (persistent plan) / events (graph plan)")
+    ap.add_argument("--mode", choices=["instances", "kpart"], default="instances",
+                    help="N>1: independent instances per rank (weak) or one K-partitioned instance (strong)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -62,7 +62,10 @@ enum {
                              where the exact sliding-window stencil applies (for testing) */
   ESDP_PDL = 8u,          /* launch the per-stage kernels with programmatic dependent launch (opt-in:
                              measured slower on B200 for this chain) */
-  ESDP_NO_DMMA = 16u      /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
+  ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
+  ESDP_PERSIST = 32u      /* run the backward pass as ONE persistent cooperative kernel (2T grid
+                             barriers) instead of a CUDA graph of 2T kernels (opt-in: measured slower
+                             for cfg2 on B200) */
 };
 
 typedef struct {
@@ -87,6 +90,19 @@ typedef struct {
  * grid and the per-action transition data (Alg. 1 lines 2-5), allocates device
  * memory on the current CUDA device and uploads the inputs.  *out receives the context. */
 esdp_status esdp_create(const esdp_problem* prob, esdp_ctx** out);
+
+/* Multi-GPU (north_star): one process per GPU, `world` ranks.  Rank r owns the price-
+ * state rows [k_lo, k_lo + k_cnt) given by esdp_partition (blocks of kmax = ceil(K/world) rows).  Every
+ * stage it computes W_t and V_t for its rows and all-gathers V_t and pol_t over NCCL (in place, kmax
+ * rows per rank), so after esdp_backward every rank holds all of V and the policy, bit-identical to a
+ * single GPU (the all-gather is a copy).  nccl_id: the 128-byte ncclUniqueId made by esdp_nccl_unique_id
+ * on one rank and broadcast by the caller.  The current CUDA device must be this rank's GPU.  W_t (and
+ * bid curves) are available only for the rank's own rows; esdp_values with W != NULL -> ESDP_E_STATE. */
+esdp_status esdp_create_dist(const esdp_problem* prob, int32_t world, int32_t rank, const void* nccl_id,
+                             esdp_ctx** out);
+esdp_status esdp_nccl_unique_id(void* id128);
+/* Row ownership of a rank (pure host function; no GPU needed). */
+esdp_status esdp_partition(int32_t K, int32_t world, int32_t rank, int32_t* k_lo, int32_t* k_cnt, int32_t* kmax);
 
 /* Grid sizes: T, S = sbar/delta + 1, A, K (any pointer may be NULL). */
 esdp_status esdp_dims(const esdp_ctx* ctx, int32_t* T, int32_t* S, int32_t* A, int32_t* K);
@@ -129,8 +145,9 @@ esdp_status esdp_policy(const esdp_ctx* ctx, int32_t t, int16_t* pol);
  *   price  [n][cap] segment prices (entries >= nvert-1 unused).  Requires ESDP_KEEP_VALUES. */
 esdp_status esdp_bidcurves(esdp_ctx* ctx, int64_t n, const int32_t* req, int32_t cap,
                            int32_t* nvert, int16_t* vert, double* q, double* price);
-/* Same, with DEVICE pointers for every array, enqueued on `stream` (no synchronization); q_dev may
- * be NULL (the quantities are actions[vert]). */
+/* Same, with DEVICE pointers for every array, enqueued on `stream` (no synchronization).  Output
+ * layout is VERTEX-major, [cap][n] (entry j of curve r at j*n + r: coalesced stores); q_dev may be
+ * NULL (the quantities are actions[vert]). */
 esdp_status esdp_bidcurves_dev(esdp_ctx* ctx, int64_t n, const int32_t* req_dev, int32_t cap,
                                int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev,
                                void* stream);
@@ -147,8 +164,9 @@ esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double*
 esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
                               void* stream);
 
-/* Which max-plus stencil the context uses: 1 = exact sliding-window (recombining grid, linear payoff),
- * 0 = brute force over every (i, a) cell.  Both give bit-identical results. */
+/* Execution plan: bit 0 = stencil (1 = exact sliding-window for the recombining grid with a linear
+ * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent cooperative
+ * kernel (else a CUDA graph of 2T kernels).  All plans give bit-identical results. */
 esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
 
 /* Number of (i, k) rows, summed over all stages and contexts since the last call, for which the
@@ -158,9 +176,10 @@ esdp_status esdp_window_fallbacks(esdp_ctx* ctx, int64_t* count);
 /* Number of kernel launches one backward pass enqueues (for harness accounting). */
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
 
-/* Average device time (ms) of one contraction launch and of one stencil launch in the last completed
- * backward pass, from CUDA events recorded (inside the backward graph) around the kernels of a sample of
- * about 16 evenly spaced stages (requires ESDP_PROFILE; the caller has synchronized the stream). */
+/* Average device time (ms) of one expectation phase and of one stencil phase in the last completed
+ * backward pass (requires ESDP_PROFILE; the caller has synchronized the stream).  Graph plan: CUDA
+ * events recorded inside the graph around the kernels of ~16 evenly spaced stages.  Persistent plan:
+ * the device timer at every phase boundary of every stage (grid barrier included in each phase). */
 esdp_status esdp_kernel_times(const esdp_ctx* ctx, double* contract_ms, double* stencil_ms);
 
 /* Diagnostic micro-timing (not part of the solve): warm back-to-back launches of one kernel of stage

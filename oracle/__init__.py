@@ -68,6 +68,8 @@ def lib():
         L.ref_philox4x32_10.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                         ctypes.POINTER(ctypes.c_uint32)]
         L.ref_simulate.argtypes = [P, _sp, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp]
+        L.ref_stage.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _dp, _dp, _dp, _sp]
+        L.ref_objective.argtypes = [P, _dp, _dp]
         _lib = L
     return _lib
 
@@ -165,6 +167,30 @@ def backward(pr: Problem, t_stop: int = 1, nthreads: int = 1) -> Solution:
     if rc:
         raise OracleError(rc, "ref_backward")
     return Solution(V, W, pol, J.value if t_stop == 1 else None)
+
+
+def stage(pr: Problem, t: int, k_lo: int, k_hi: int, Vnext, nthreads: int = 1):
+    """Stage t for rows [k_lo, k_hi): returns (W rows, V rows, pol rows), each [k_hi-k_lo][S]."""
+    S, A = dims(pr)
+    n = k_hi - k_lo
+    W = np.zeros((n, S)); V = np.zeros((n, S)); pol = np.full((n, S), -1, np.int16)
+    Vn = None if Vnext is None else np.ascontiguousarray(Vnext, dtype=np.float64)
+    c = pr._c()
+    rc = lib().ref_stage(ctypes.byref(c), int(t), int(k_lo), int(k_hi), int(nthreads), _ptr(Vn), _ptr(W), _ptr(V),
+                         _ptr(pol, _sp))
+    if rc:
+        raise OracleError(rc, "ref_stage")
+    return W, V, pol
+
+
+def objective(pr: Problem, V1) -> float:
+    J = ctypes.c_double()
+    V1 = np.ascontiguousarray(V1, dtype=np.float64)
+    c = pr._c()
+    rc = lib().ref_objective(ctypes.byref(c), _ptr(V1), ctypes.byref(J))
+    if rc:
+        raise OracleError(rc, "ref_objective")
+    return J.value
 
 
 def bidcurve(pr: Problem, W: np.ndarray, t: int, i: int, k: int):

@@ -188,6 +188,118 @@ static double interp(const double* row, int32_t i, int32_t o, double w, double o
   return (omw * row[i + o]) + (w * row[i + o + 1]);
 }
 
+/* One stage t of the backward induction for the price-state rows [k_lo, k_hi) (Alg. 1 lines 7-11,
+ * P:268-277, Markov form): W_t rows = P_t V_{t+1} (W_T = 0), then V_t, pol_t rows by the max-plus
+ * reduction.  Vnext = V_{t+1} [K][S] (all rows; unused at t = T).  Wt, Vt, polt: [k_hi - k_lo][S]. */
+static int stage_rows(const ref_problem* pr, int32_t S, int32_t A, const double* act, const int32_t* off,
+                      const double* w, const double* omw, const int32_t* ilo, const int32_t* ihi, int32_t t,
+                      int32_t k_lo, int32_t k_hi, int32_t nthreads, const double* Vnext, double* Wt, double* Vt,
+                      int16_t* polt) {
+  const int32_t T = pr->T, K = pr->K;
+  int internal_error = 0;
+  /* Expectation (Alg. 1 line 11; Eq. 6) in Markov form W_t = P_t V_{t+1} (D1): canonical
+   * ascending-k' fma chain (R15).  Rank-1: P_t[k][k'] = pi_{t+1}[k'].  Base case W_T = 0. */
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+  for (int32_t k = k_lo; k < k_hi; ++k) {
+    double* Wrow = Wt + (int64_t)(k - k_lo) * S;
+    if (t == T) {
+      for (int32_t i = 0; i < S; ++i) Wrow[i] = 0.0;
+      continue;
+    }
+    const double* Prow = pr->P ? pr->P + ((int64_t)(t - 1) * K + k) * K : pr->pi + (int64_t)t * K;
+    for (int32_t i = 0; i < S; ++i) {
+      double acc = 0.0;
+      for (int32_t kp = 0; kp < K; ++kp) acc = fma(Prow[kp], Vnext[(int64_t)kp * S + i], acc);
+      Wrow[i] = acc;
+    }
+  }
+  /* Alg. 1 lines 7-10, Eq. 5: V_t(s_i,k) = max over feasible a of
+   * payoff(lambda_{t,k}, p_a) + Wint_t(i, a, k); argmax = smallest maximizing a (R8). */
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+  for (int32_t k = k_lo; k < k_hi; ++k) {
+    const double* Wrow = Wt + (int64_t)(k - k_lo) * S;
+    for (int32_t i = 0; i < S; ++i) {
+      double best = -INFINITY;
+      int32_t arg = -1;
+      for (int32_t a = 0; a < A; ++a) {
+        if (i < ilo[a] || i > ihi[a]) continue; /* Alg. 1 line 8: infeasible -> -inf */
+        double cand = payoff(pr, A, act, t, k, a) + interp(Wrow, i, off[a], w[a], omw[a]);
+        if (cand > best) {
+          best = cand;
+          arg = a;
+        }
+      }
+      if (arg < 0) {
+#pragma omp atomic write
+        internal_error = 1;
+      }
+      Vt[(int64_t)(k - k_lo) * S + i] = best;
+      polt[(int64_t)(k - k_lo) * S + i] = (int16_t)arg;
+    }
+  }
+  return internal_error ? REF_E_INTERNAL : REF_OK;
+}
+
+typedef struct {
+  double* act; int32_t* off; double* w; double* omw; int32_t* ilo; int32_t* ihi;
+} ref_tabs;
+
+static int tabs_make(const ref_problem* pr, int32_t A, ref_tabs* tb) {
+  tb->act = (double*)malloc(sizeof(double) * (size_t)A);
+  tb->off = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  tb->w = (double*)malloc(sizeof(double) * (size_t)A);
+  tb->omw = (double*)malloc(sizeof(double) * (size_t)A);
+  tb->ilo = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  tb->ihi = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  if (!tb->act || !tb->off || !tb->w || !tb->omw || !tb->ilo || !tb->ihi) return REF_E_INTERNAL;
+  ref_actions(pr, tb->act);
+  ref_tables(pr, tb->off, tb->w, tb->omw, tb->ilo, tb->ihi);
+  return REF_OK;
+}
+
+static void tabs_free(ref_tabs* tb) {
+  free(tb->act); free(tb->off); free(tb->w); free(tb->omw); free(tb->ilo); free(tb->ihi);
+}
+
+int ref_stage(const ref_problem* pr, int32_t t, int32_t k_lo, int32_t k_hi, int32_t nthreads, const double* Vnext,
+              double* Wt, double* Vt, int16_t* polt) {
+  int32_t S, A;
+  int rc = ref_dims(pr, &S, &A);
+  if (rc) return rc;
+  if (t < 1 || t > pr->T || k_lo < 0 || k_hi > pr->K || k_lo > k_hi || (t < pr->T && !Vnext)) return REF_E_STATE;
+  ref_tabs tb;
+  rc = tabs_make(pr, A, &tb);
+  if (!rc) rc = stage_rows(pr, S, A, tb.act, tb.off, tb.w, tb.omw, tb.ilo, tb.ihi, t, k_lo, k_hi, nthreads, Vnext, Wt, Vt, polt);
+  tabs_free(&tb);
+  return rc;
+}
+
+int ref_objective(const ref_problem* pr, const double* V1, double* J) {
+  int32_t S, A;
+  int rc = ref_dims(pr, &S, &A);
+  if (rc) return rc;
+  /* Eq. 6 at t = 0: J = E[V_1(s0, k_1)], k_1 ~ pi_1 (R10/R11); s0 off-grid is
+   * interpolated per k (R24). */
+  const double* pi1 = pr->pi;
+  double x = pr->s0 / pr->delta;
+  double r = nearbyint(x);
+  double acc = 0.0;
+  for (int32_t k = 0; k < pr->K; ++k) {
+    const double* row = V1 + (int64_t)k * S;
+    double v;
+    if (fabs(x - r) <= GRID_TOL) {
+      v = row[(int32_t)r];
+    } else {
+      double f = floor(x);
+      double w0 = x - f;
+      v = ((1.0 - w0) * row[(int32_t)f]) + (w0 * row[(int32_t)f + 1]);
+    }
+    acc = fma(pi1[k], v, acc);
+  }
+  *J = acc;
+  return REF_OK;
+}
+
 int ref_backward(const ref_problem* pr, int32_t t_stop, int32_t nthreads,
                  double* V, double* W, int16_t* pol, double* J) {
   int32_t S, A;
@@ -195,90 +307,17 @@ int ref_backward(const ref_problem* pr, int32_t t_stop, int32_t nthreads,
   if (rc) return rc;
   const int32_t T = pr->T, K = pr->K;
   if (t_stop < 1 || t_stop > T) return REF_E_STATE;
-  double* act = (double*)malloc(sizeof(double) * (size_t)A);
-  int32_t* off = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
-  double* w = (double*)malloc(sizeof(double) * (size_t)A);
-  double* omw = (double*)malloc(sizeof(double) * (size_t)A);
-  int32_t* ilo = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
-  int32_t* ihi = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
-  if (!act || !off || !w || !omw || !ilo || !ihi) {
-    free(act); free(off); free(w); free(omw); free(ilo); free(ihi);
-    return REF_E_INTERNAL;
-  }
-  ref_actions(pr, act);
-  ref_tables(pr, off, w, omw, ilo, ihi);
+  ref_tabs tb;
+  rc = tabs_make(pr, A, &tb);
   const int64_t KS = (int64_t)K * S;
-  int internal_error = 0;
-
-  /* Alg. 1 line 1: base case V_hat_T = 0, i.e. W_T = 0 (R3: T iterations, t = T..1). */
-  for (int32_t t = T; t >= t_stop; --t) {
-    double* Wt = W + (int64_t)(t - 1) * KS;
-    double* Vt = V + (int64_t)(t - 1) * KS;
-    int16_t* polt = pol + (int64_t)(t - 1) * KS;
-    /* Expectation (Alg. 1 line 11; Eq. 6) in Markov form W_t = P_t V_{t+1} (D1):
-     * canonical ascending-k' fma chain (R15).  Rank-1: P_t[k][k'] = pi_{t+1}[k']. */
-    if (t == T) {
-      for (int64_t j = 0; j < KS; ++j) Wt[j] = 0.0;
-    } else {
-      const double* Vn = V + (int64_t)t * KS; /* V_{t+1} */
-#pragma omp parallel for num_threads(nthreads) schedule(static)
-      for (int32_t k = 0; k < K; ++k) {
-        const double* Prow = pr->P ? pr->P + ((int64_t)(t - 1) * K + k) * K : pr->pi + (int64_t)t * K;
-        for (int32_t i = 0; i < S; ++i) {
-          double acc = 0.0;
-          for (int32_t kp = 0; kp < K; ++kp) acc = fma(Prow[kp], Vn[(int64_t)kp * S + i], acc);
-          Wt[(int64_t)k * S + i] = acc;
-        }
-      }
-    }
-    /* Alg. 1 lines 7-10, Eq. 5: V_t(s_i,k) = max over feasible a of
-     * payoff(lambda_{t,k}, p_a) + Wint_t(i, a, k); argmax = smallest maximizing a (R8). */
-#pragma omp parallel for num_threads(nthreads) schedule(static)
-    for (int32_t k = 0; k < K; ++k) {
-      const double* Wrow = Wt + (int64_t)k * S;
-      for (int32_t i = 0; i < S; ++i) {
-        double best = -INFINITY;
-        int32_t arg = -1;
-        for (int32_t a = 0; a < A; ++a) {
-          if (i < ilo[a] || i > ihi[a]) continue; /* Alg. 1 line 8: infeasible -> -inf */
-          double cand = payoff(pr, A, act, t, k, a) + interp(Wrow, i, off[a], w[a], omw[a]);
-          if (cand > best) {
-            best = cand;
-            arg = a;
-          }
-        }
-        if (arg < 0) {
-#pragma omp atomic write
-          internal_error = 1;
-        }
-        Vt[(int64_t)k * S + i] = best;
-        polt[(int64_t)k * S + i] = (int16_t)arg;
-      }
-    }
-  }
-  if (!internal_error && J && t_stop == 1) {
-    /* Eq. 6 at t = 0: J = E[V_1(s0, k_1)], k_1 ~ pi_1 (R10/R11); s0 off-grid is
-     * interpolated per k (R24). */
-    const double* pi1 = pr->pi;
-    double x = pr->s0 / pr->delta;
-    double r = nearbyint(x);
-    double acc = 0.0;
-    for (int32_t k = 0; k < K; ++k) {
-      const double* row = V + (int64_t)k * S;
-      double v;
-      if (fabs(x - r) <= GRID_TOL) {
-        v = row[(int32_t)r];
-      } else {
-        double f = floor(x);
-        double w0 = x - f;
-        v = ((1.0 - w0) * row[(int32_t)f]) + (w0 * row[(int32_t)f + 1]);
-      }
-      acc = fma(pi1[k], v, acc);
-    }
-    *J = acc;
-  }
-  free(act); free(off); free(w); free(omw); free(ilo); free(ihi);
-  return internal_error ? REF_E_INTERNAL : REF_OK;
+  /* Alg. 1 line 1: base case; R3: T iterations, t = T..1, every stage over all K rows. */
+  for (int32_t t = T; t >= t_stop && !rc; --t)
+    rc = stage_rows(pr, S, A, tb.act, tb.off, tb.w, tb.omw, tb.ilo, tb.ihi, t, 0, K, nthreads,
+                    t < T ? V + (int64_t)t * KS : NULL, W + (int64_t)(t - 1) * KS, V + (int64_t)(t - 1) * KS,
+                    pol + (int64_t)(t - 1) * KS);
+  tabs_free(&tb);
+  if (!rc && J && t_stop == 1) rc = ref_objective(pr, V, J);
+  return rc;
 }
 
 int ref_bidcurve(const ref_problem* pr, const double* W, int32_t t, int32_t i, int32_t k,

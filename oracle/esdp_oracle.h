@@ -65,6 +65,15 @@ int ref_tables(const ref_problem* pr, int32_t* off, double* w, double* omw, int3
 int ref_backward(const ref_problem* pr, int32_t t_stop, int32_t nthreads,
                  double* V, double* W, int16_t* pol, double* J);
 
+/* One stage t for the price-state rows [k_lo, k_hi) only (the unit of the K-partitioned multi-GPU
+ * schedule): Vnext = V_{t+1} [K][S] (all rows; NULL at t = T); Wt, Vt, polt are
+ * [k_hi - k_lo][S].  ref_backward is exactly this over all rows, stage after stage. */
+int ref_stage(const ref_problem* pr, int32_t t, int32_t k_lo, int32_t k_hi, int32_t nthreads, const double* Vnext,
+              double* Wt, double* Vt, int16_t* polt);
+
+/* J = sum_k pi_1[k] V_1(s0, k) (Eq. 6 at t = 0) from V_1 [K][S]. */
+int ref_objective(const ref_problem* pr, const double* V1, double* J);
+
 /* Bid curve for stage t (1..T), SoC index i, price state k, from W_t:
  * points (p_a, u_a = Wint_t(i,a,k) - g_a) over feasible a, upper concave hull
  * (monotone chain = Graham scan on x-sorted points), prices -du/dp (Eq. 12),

@@ -31,6 +31,7 @@ ESDP_PROFILE = 2
 ESDP_FORCE_BRUTE = 4
 ESDP_PDL = 8
 ESDP_NO_DMMA = 16
+ESDP_PERSIST = 32
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
@@ -39,6 +40,7 @@ EXPORTED_SYMBOLS = [
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
+    "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -89,6 +91,10 @@ def _load():
         "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
         "esdp_debug_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
         "esdp_window_fallbacks": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "esdp_create_dist": ([ctypes.POINTER(esdp_problem), ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p,
+                              ctypes.POINTER(_vp)], ctypes.c_int),
+        "esdp_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+        "esdp_partition": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
         "esdp_last_error": ([ctx], ctypes.c_char_p),
     }
@@ -121,17 +127,42 @@ def _check(st, what, ctx=None):
 
 
 def esdp_create(T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions=None,
-                payoff_kind=ESDP_PAYOFF_LINEAR, g=None, flags=0):
-    """esdp_create(&problem, &ctx): returns the opaque context handle (int)."""
+                payoff_kind=ESDP_PAYOFF_LINEAR, g=None, flags=0, dist=None):
+    """esdp_create(&problem, &ctx) -> opaque context handle (int).
+    dist = (world, rank, nccl_id_bytes) selects esdp_create_dist (multi-GPU, K-partitioned)."""
     keep = [_f64(x) for x in (actions, lam, P, pi, g)]
     act, lam_, P_, pi_, g_ = keep
     pr = esdp_problem(int(T), int(K), float(pbar), float(sbar), float(s0), float(eta_c), float(eta_d),
                       float(delta), 0 if act is None else int(act.shape[0]), _p(act), _p(lam_), _p(P_),
                       _p(pi_), int(payoff_kind), _p(g_), int(flags))
     out = _vp()
-    st = lib.esdp_create(ctypes.byref(pr), ctypes.byref(out))
-    _check(st, "esdp_create", None)
+    if dist is None:
+        st = lib.esdp_create(ctypes.byref(pr), ctypes.byref(out))
+        _check(st, "esdp_create", None)
+    else:
+        world, rank, nid = dist
+        st = lib.esdp_create_dist(ctypes.byref(pr), int(world), int(rank), bytes(nid), ctypes.byref(out))
+        _check(st, "esdp_create_dist", None)
     return out.value
+
+
+def esdp_create_dist(world, rank, nccl_id, *args, **kw):
+    """Multi-GPU context: this rank owns the price-state rows esdp_partition(K, world, rank)."""
+    return esdp_create(*args, dist=(world, rank, nccl_id), **kw)
+
+
+def esdp_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.esdp_nccl_unique_id(buf), "esdp_nccl_unique_id", None)
+    return buf.raw
+
+
+def esdp_partition(K, world, rank):
+    """(k_lo, k_cnt, kmax): the rows [k_lo, k_lo + k_cnt) owned by `rank` (host-only, no GPU)."""
+    lo, cnt, m = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.esdp_partition(int(K), int(world), int(rank), ctypes.byref(lo), ctypes.byref(cnt), ctypes.byref(m)),
+           "esdp_partition", None)
+    return lo.value, cnt.value, m.value
 
 
 def esdp_dims(ctx):
@@ -237,7 +268,7 @@ def esdp_kernel_times(ctx):
 
 
 def esdp_stencil_kind(ctx) -> int:
-    """1 = exact sliding-window stencil, 0 = brute force."""
+    """bit 0: 1 = exact sliding-window stencil, 0 = brute force; bit 1: persistent cooperative kernel."""
     k = ctypes.c_int32()
     _check(lib.esdp_stencil_kind(ctx, ctypes.byref(k)), "esdp_stencil_kind", ctx)
     return k.value
@@ -265,13 +296,14 @@ class Solver:
     """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
-    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=False, dmma=True):
+    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=False, dmma=True, persist=False,
+                 dist=None):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
                                (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
                                | (ESDP_FORCE_BRUTE if force_brute else 0) | (ESDP_PDL if pdl else 0)
-                               | (0 if dmma else ESDP_NO_DMMA))
+                               | (0 if dmma else ESDP_NO_DMMA) | (ESDP_PERSIST if persist else 0), dist=dist)
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
         self.stencil_kind = esdp_stencil_kind(self.ctx)
 

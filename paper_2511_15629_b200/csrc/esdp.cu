@@ -5,6 +5,7 @@
 // FMA contraction disabled (-Xcompiler -ffp-contract=off).  Everything per stage runs in the
 // kernels of kernels.cuh; the whole backward pass is one CUDA graph (2T+1 launches).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -17,6 +18,7 @@
 #include "../../include/esdp.h"
 #include "kernels.cuh"
 #include "window.cuh"
+#include "persistent.cuh"
 
 using namespace esdp;
 
@@ -36,6 +38,10 @@ struct esdp_ctx {
   // problem
   int T = 0, K = 0, S = 0, A = 0, kind = 0, rank1 = 0;
   int ld = 0;  // padded row length of V and W on the device (multiple of 4 doubles: 16-byte cp.async)
+  // multi-GPU (esdp_create_dist): this rank owns price-state rows [k_lo, k_lo + k_cnt); V_t and pol_t are
+  // all-gathered every stage in blocks of kmax rows (Kp = world * kmax rows per stage on every rank)
+  int world = 1, rank = 0, kmax = 0, k_lo = 0, k_cnt = 0, Kp = 0;
+  ncclComm_t comm = nullptr;
   uint32_t flags = 0;
   double pbar = 0, sbar = 0, s0 = 0, eta_c = 1, eta_d = 1, delta = 1;
   std::vector<double> act, w, omw;
@@ -72,6 +78,10 @@ struct esdp_ctx {
   cudaGraphExec_t graph = nullptr;
   size_t stencil_smem = 0;
   int64_t launches = 0;
+  // persistent cooperative backward (persistent.cuh): one launch per backward
+  int persist = 0, persist_grid = 0;
+  size_t persist_smem = 0;
+  unsigned long long* d_stamps = nullptr;
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   int prof_stride = 1;
   bool pdl = true;
@@ -246,9 +256,10 @@ esdp_status dev_alloc(esdp_ctx* c, T** p, size_t n) {
 
 void free_all(esdp_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->comm) ncclCommDestroy(c->comm);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_stamps, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -283,11 +294,11 @@ esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const dou
   return ESDP_OK;
 }
 
-size_t w_rows(const esdp_ctx* c) { return c->rank1 ? 1 : (size_t)c->K; }
+size_t w_rows(const esdp_ctx* c) { return c->rank1 ? 1 : (size_t)c->kmax; }
 bool keep(const esdp_ctx* c) { return (c->flags & ESDP_KEEP_VALUES) != 0; }
 // V_t / W_t / pol_t device slices (stage t = 1..T)
 double* V_of(esdp_ctx* c, int t) {
-  const size_t KS = (size_t)c->K * c->ld;
+  const size_t KS = (size_t)c->Kp * c->ld;
   return keep(c) ? c->d_V + (size_t)(t - 1) * KS : c->d_V + (size_t)((t - 1) & 1) * KS;
 }
 double* W_of(esdp_ctx* c, int t) {
@@ -314,8 +325,9 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
 cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int K = c->K, S = c->S;
-  const int rows = (int)w_rows(c);
-  const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + (size_t)(t - 1) * K * K;
+  const int rows = c->rank1 ? 1 : c->k_cnt;   // own rows of W_t (all rows on one GPU)
+  if (rows == 0) return cudaSuccess;
+  const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
     const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
     return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
@@ -328,13 +340,15 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
 
 // The max-plus stencil of stage t: V_t, pol_t from W_t (window or brute force).
 cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute) {
-  const int K = c->K, S = c->S;
+  const int S = c->S;
+  const int K = c->k_cnt;                      // stencil rows of this rank (local k = global k - k_lo)
+  if (K == 0) return cudaSuccess;
   const double* Wt = W_of(c, t);
-  int16_t* pol = c->d_pol + (size_t)(t - 1) * K * S;
-  const double* lam = c->d_lambda + (size_t)(t - 1) * K;
+  int16_t* pol = c->d_pol + ((size_t)(t - 1) * c->Kp + c->k_lo) * S;
+  const double* lam = c->d_lambda + (size_t)(t - 1) * c->K + c->k_lo;
   if (c->use_window && !force_brute) {
     WinParams wp;
-    wp.W = Wt; wp.V = V_of(c, t); wp.pol = pol; wp.lambda_t = lam;
+    wp.W = Wt; wp.V = V_of(c, t) + (size_t)c->k_lo * c->ld; wp.pol = pol; wp.lambda_t = lam;
     wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
     wp.singles = c->d_singles; wp.live = c->d_live;
     wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
@@ -346,9 +360,9 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
     return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
   }
   StencilParams prm;
-  prm.W = Wt; prm.V = V_of(c, t); prm.pol = pol; prm.lambda_t = lam;
+  prm.W = Wt; prm.V = V_of(c, t) + (size_t)c->k_lo * c->ld; prm.pol = pol; prm.lambda_t = lam;
   prm.act = c->d_act;
-  prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + (size_t)(t - 1) * K * c->A : c->d_g;
+  prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + ((size_t)(t - 1) * c->K + c->k_lo) * c->A : c->d_g;
   prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
   prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
   prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
@@ -358,6 +372,38 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
 cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
   return launch(objective_kernel, dim3(1), dim3(128), 2 * sizeof(double) * c->K, s, pdl, (const double*)V_of(c, 1),
                 (const double*)c->d_pi, c->K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
+}
+
+PersistParams persist_params(esdp_ctx* c) {
+  PersistParams pp;
+  StencilParams& sp = pp.sp;
+  sp.act = c->d_act; sp.w = c->d_w; sp.omw = c->d_omw; sp.off = c->d_off; sp.segs = c->d_segs;
+  sp.nseg = (int)c->segs.size(); sp.A = c->A; sp.S = c->S; sp.K = c->K; sp.kind = c->kind; sp.rank1 = c->rank1;
+  sp.o_min = c->o_min; sp.o_span = c->o_max - c->o_min; sp.ld = c->ld; sp.g = c->d_g;
+  WinParams& wp = pp.wp;
+  wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
+  wp.singles = c->d_singles; wp.live = c->d_live;
+  wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
+  wp.A = c->A; wp.S = c->S; wp.K = c->K; wp.rank1 = c->rank1; wp.ld = c->ld;
+  wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
+  wp.o_min = c->o_min; wp.o_max = c->o_max;
+  wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
+  wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
+  pp.use_window = c->use_window;
+  pp.T = c->T; pp.K = c->K; pp.S = c->S; pp.A = c->A; pp.ld = c->ld; pp.rows = (int)w_rows(c);
+  pp.rank1 = c->rank1; pp.kind = c->kind; pp.keep = keep(c) ? 1 : 0;
+  pp.P = c->d_P; pp.pi = c->d_pi; pp.lambda = c->d_lambda; pp.g = c->d_g;
+  pp.V = c->d_V; pp.W = c->d_W; pp.pol = c->d_pol; pp.J = c->d_J;
+  pp.f0 = c->f0; pp.on_grid = c->on_grid; pp.w0 = c->w0;
+  pp.stamps = c->d_stamps;
+  return pp;
+}
+
+cudaError_t launch_persistent(esdp_ctx* c, cudaStream_t s) {
+  PersistParams pp = persist_params(c);
+  void* args[] = {&pp};
+  return cudaLaunchCooperativeKernel((void*)backward_persistent_kernel, dim3(c->persist_grid), dim3(kPersistThreads), args,
+                                     c->persist_smem, s);
 }
 
 // Enqueue the 2T launches of one backward pass on stream s (PDL between consecutive kernels).
@@ -389,6 +435,16 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     CUDA_OR_FAIL(c, mark(t, 3));
     after_kernel = !sampled(t);
     ++n;
+    if (c->comm) {  // V_t and pol_t rows of every rank to every rank (in place, blocks of kmax rows)
+      double* Vt = V_of(c, t);
+      int16_t* pt = c->d_pol + (size_t)(t - 1) * c->Kp * c->S;
+      const size_t vcount = (size_t)c->kmax * c->ld, pcount = (size_t)c->kmax * c->S;
+      ncclResult_t r1 = ncclAllGather(Vt + c->rank * vcount, Vt, vcount, ncclDouble, c->comm, s);
+      ncclResult_t r2 = ncclAllGather(pt + c->rank * pcount, pt, pcount * sizeof(int16_t), ncclUint8, c->comm, s);
+      if (r1 != ncclSuccess || r2 != ncclSuccess)
+        return fail(c, ESDP_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+      after_kernel = false;
+    }
   }
   CUDA_OR_FAIL(c, launch_objective(c, s, pdl && after_kernel));
   ++n;
@@ -401,7 +457,35 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
 
 extern "C" {
 
-esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
+static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out);
+
+esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) { return create_impl(pr, 1, 0, nullptr, out); }
+
+esdp_status esdp_partition(int32_t K, int32_t world, int32_t rank, int32_t* k_lo, int32_t* k_cnt, int32_t* kmax) {
+  if (K < 1 || world < 1 || rank < 0 || rank >= world) return ESDP_E_CONFIG;
+  const int32_t m = (K + world - 1) / world;
+  const int32_t lo = std::min(K, rank * m), hi = std::min(K, (rank + 1) * m);
+  if (k_lo) *k_lo = lo;
+  if (k_cnt) *k_cnt = hi - lo;
+  if (kmax) *kmax = m;
+  return ESDP_OK;
+}
+
+esdp_status esdp_nccl_unique_id(void* id128) {
+  if (!id128) return ESDP_E_CONFIG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(nullptr, ESDP_E_NCCL, "ncclGetUniqueId failed");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, &id, sizeof(id));
+  return ESDP_OK;
+}
+
+esdp_status esdp_create_dist(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out) {
+  if (world < 1 || rank < 0 || rank >= world || !nccl_id) return fail(nullptr, ESDP_E_CONFIG, "bad world/rank/nccl id");
+  return create_impl(pr, world, rank, nccl_id, out);
+}
+
+static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out) {
   g_create_error.clear();
   if (!pr || !out) return fail(nullptr, ESDP_E_CONFIG, "null argument");
   *out = nullptr;
@@ -423,6 +507,9 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
 
   esdp_ctx* c = new esdp_ctx();
   c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1; c->ld = (c->S + 3) & ~3;
+  c->world = world; c->rank = rank;
+  esdp_partition(c->K, world, rank, &c->k_lo, &c->k_cnt, &c->kmax);
+  c->Kp = world * c->kmax;   // == K on one GPU
   c->pbar = pr->pbar; c->sbar = pr->sbar; c->s0 = pr->s0; c->eta_c = pr->eta_c; c->eta_d = pr->eta_d;
   c->delta = pr->delta; c->kind = pr->payoff_kind; c->rank1 = pr->P == nullptr; c->flags = pr->flags;
   c->pdl = (pr->flags & ESDP_PDL) != 0;   // measured slower on B200 for this kernel chain: opt-in
@@ -473,12 +560,19 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
   TRY(dev_alloc(c, &c->d_off, A));
   TRY(dev_alloc(c, &c->d_segs, c->segs.size()));
   const size_t LD = c->ld;
-  TRY(dev_alloc(c, &c->d_V, keep(c) ? T * K * LD : 2 * K * LD));
+  const size_t KP = c->Kp;
+  TRY(dev_alloc(c, &c->d_V, keep(c) ? T * KP * LD : 2 * KP * LD));
   TRY(dev_alloc(c, &c->d_W, keep(c) ? T * w_rows(c) * LD : w_rows(c) * LD));
   // padding columns are never read as values; zero them once so no stale bits are staged
-  cudaMemset(c->d_V, 0, (keep(c) ? T * K * LD : 2 * K * LD) * sizeof(double));
+  cudaMemset(c->d_V, 0, (keep(c) ? T * KP * LD : 2 * KP * LD) * sizeof(double));
   cudaMemset(c->d_W, 0, (keep(c) ? T * w_rows(c) * LD : w_rows(c) * LD) * sizeof(double));
-  TRY(dev_alloc(c, &c->d_pol, T * K * S));
+  TRY(dev_alloc(c, &c->d_pol, T * KP * S));
+  if (nccl_id) {   // esdp_create_dist: NCCL communicator (also for world == 1: the all-gather is a copy)
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t nr = ncclCommInitRank(&c->comm, world, id, rank);
+    if (nr != ncclSuccess) { fail(c, ESDP_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr)); c->comm = nullptr; return bail(ESDP_E_NCCL); }
+  }
   TRY(dev_alloc(c, &c->d_J, 4));
   TRY(dev_alloc(c, &c->d_singles, c->singles.size()));
   TRY(dev_alloc(c, &c->d_live, c->live_list.size()));
@@ -515,7 +609,26 @@ esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) {
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
+  // persistent path: needs cooperative launch and >= 1 resident 256-thread CTA per SM
+  if ((c->flags & ESDP_PERSIST) && !nccl_id && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
+    int dev = 0, coop = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    size_t sm = std::max(c->use_window ? c->window_smem : c->stencil_smem, 2 * sizeof(double) * (size_t)K);
+    sm = std::max(sm, c->stencil_smem);
+    if (coop && sm <= 200 * 1024 &&
+        cudaFuncSetAttribute(backward_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_persistent_kernel, kPersistThreads, sm) == cudaSuccess &&
+        per_sm >= 1) {
+      c->persist = 1;
+      c->persist_grid = per_sm * nsm;
+      c->persist_smem = sm;
+    }
+    cudaGetLastError();
+  }
   if (c->flags & ESDP_PROFILE) {
+    if (c->persist) TRY(dev_alloc(c, &c->d_stamps, (size_t)c->T * 3));
     c->prof_stride = std::max(1, c->T / 16);
     c->ev.resize((size_t)c->T * 4);
     for (auto& e : c->ev)
@@ -570,7 +683,8 @@ esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const 
 esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
   if (!c) return ESDP_E_STATE;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
+  if (c->persist) CUDA_OR_FAIL(c, launch_persistent(c, s));
+  else CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
   c->solved = true;
   return ESDP_OK;
 }
@@ -597,6 +711,7 @@ esdp_status esdp_values(const esdp_ctx* cc, int32_t t, double* V, double* W) {
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   if (t < 1 || t > c->T) return fail(c, ESDP_E_STATE, "stage %d out of range", t);
   if (!keep(c) && (t != 1 || W)) return fail(c, ESDP_E_STATE, "only V_1 is kept without ESDP_KEEP_VALUES");
+  if (W && c->world > 1 && !c->rank1) return fail(c, ESDP_E_STATE, "W_t rows live on their owning ranks (multi-GPU)");
   const size_t rowb = c->S * sizeof(double), ldb = c->ld * sizeof(double);
   if (V) CUDA_OR_FAIL(c, cudaMemcpy2D(V, rowb, V_of(c, t), ldb, rowb, c->K, cudaMemcpyDeviceToHost));
   if (W) {
@@ -616,7 +731,7 @@ esdp_status esdp_policy(const esdp_ctx* cc, int32_t t, int16_t* pol) {
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   if (t < 1 || t > c->T) return fail(c, ESDP_E_STATE, "stage %d out of range", t);
   const size_t KS = (size_t)c->K * c->S;
-  CUDA_OR_FAIL(c, cudaMemcpy(pol, c->d_pol + (size_t)(t - 1) * KS, KS * sizeof(int16_t), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(pol, c->d_pol + (size_t)(t - 1) * c->Kp * c->S, KS * sizeof(int16_t), cudaMemcpyDeviceToHost));
   return ESDP_OK;
 }
 
@@ -628,7 +743,8 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
   if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
   if (cap < c->A) return fail(c, ESDP_E_STATE, "cap %d < A %d", cap, c->A);
   if (n <= 0) return ESDP_OK;
-  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld};
+  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld,
+               (int)w_rows(c), c->k_lo, c->rank1 ? c->K : c->k_cnt};
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   const int span = c->o_max - c->o_min;
   const unsigned blocks = (unsigned)((n + kBidThreads - 1) / kBidThreads);
@@ -653,6 +769,8 @@ esdp_status esdp_bidcurves(esdp_ctx* c, int64_t n, const int32_t* req, int32_t c
     const int t = req[3 * r], i = req[3 * r + 1], k = req[3 * r + 2];
     if (t < 1 || t > c->T || i < 0 || i >= c->S || k < 0 || k >= c->K)
       return fail(c, ESDP_E_STATE, "request %lld (t=%d, i=%d, k=%d) out of range", (long long)r, t, i, k);
+    if (!c->rank1 && (k < c->k_lo || k >= c->k_lo + c->k_cnt))
+      return fail(c, ESDP_E_STATE, "request %lld: price state %d is owned by another rank", (long long)r, k);
   }
   if (n > c->req_cap || (int64_t)cap * n > c->out_cap) {
     cudaFree(c->d_req); cudaFree(c->d_nv); cudaFree(c->d_vert); cudaFree(c->d_q); cudaFree(c->d_price);
@@ -669,9 +787,18 @@ esdp_status esdp_bidcurves(esdp_ctx* c, int64_t n, const int32_t* req, int32_t c
   if (st != ESDP_OK) return st;
   CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
   CUDA_OR_FAIL(c, cudaMemcpy(nvert, c->d_nv, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CUDA_OR_FAIL(c, cudaMemcpy(vert, c->d_vert, (size_t)cap * n * sizeof(int16_t), cudaMemcpyDeviceToHost));
-  CUDA_OR_FAIL(c, cudaMemcpy(q, c->d_q, (size_t)cap * n * sizeof(double), cudaMemcpyDeviceToHost));
-  CUDA_OR_FAIL(c, cudaMemcpy(price, c->d_price, (size_t)cap * n * sizeof(double), cudaMemcpyDeviceToHost));
+  // device layout is vertex-major [cap][n]; the host API returns curve-major [n][cap]
+  std::vector<int16_t> hv((size_t)cap * n);
+  std::vector<double> hq((size_t)cap * n), hp((size_t)cap * n);
+  CUDA_OR_FAIL(c, cudaMemcpy(hv.data(), c->d_vert, hv.size() * sizeof(int16_t), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(hq.data(), c->d_q, hq.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_OR_FAIL(c, cudaMemcpy(hp.data(), c->d_price, hp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t r = 0; r < n; ++r)
+    for (int j = 0; j < cap; ++j) {
+      vert[r * cap + j] = hv[(size_t)j * n + r];
+      q[r * cap + j] = hq[(size_t)j * n + r];
+      price[r * cap + j] = hp[(size_t)j * n + r];
+    }
   return ESDP_OK;
 }
 
@@ -683,7 +810,7 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
   sp.guide = c->d_guide; sp.guide1 = c->d_guide1; sp.G = c->G;
   sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
-  sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind;
+  sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   const int thr = 128;
@@ -728,13 +855,13 @@ esdp_status esdp_window_fallbacks(esdp_ctx* c, int64_t* count) {
 
 esdp_status esdp_stencil_kind(const esdp_ctx* c, int32_t* kind) {
   if (!c || !kind) return ESDP_E_STATE;
-  *kind = c->use_window;
+  *kind = c->use_window + 2 * c->persist;
   return ESDP_OK;
 }
 
 esdp_status esdp_launch_count(const esdp_ctx* c, int64_t* n) {
   if (!c || !n) return ESDP_E_STATE;
-  *n = c->launches;
+  *n = c->persist ? 1 : c->launches;
   return ESDP_OK;
 }
 
@@ -743,6 +870,18 @@ esdp_status esdp_kernel_times(const esdp_ctx* cc, double* contract_ms, double* s
   if (!c) return ESDP_E_STATE;
   if (c->ev.empty()) return fail(c, ESDP_E_STATE, "context was created without ESDP_PROFILE");
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (c->persist) {   // device timer stamps of block 0 at every phase boundary
+    std::vector<unsigned long long> st((size_t)c->T * 3);
+    CUDA_OR_FAIL(c, cudaMemcpy(st.data(), c->d_stamps, st.size() * 8, cudaMemcpyDeviceToHost));
+    double e_ns = 0.0, s_ns = 0.0;
+    for (int t = 1; t <= c->T; ++t) {
+      e_ns += (double)(st[(size_t)(t - 1) * 3 + 1] - st[(size_t)(t - 1) * 3 + 0]);
+      s_ns += (double)(st[(size_t)(t - 1) * 3 + 2] - st[(size_t)(t - 1) * 3 + 1]);
+    }
+    if (contract_ms) *contract_ms = e_ns / c->T * 1e-6;
+    if (stencil_ms) *stencil_ms = s_ns / c->T * 1e-6;
+    return ESDP_OK;
+  }
   double ct = 0.0, st = 0.0;
   int nc = 0, ns = 0;
   for (int t = 1; t <= c->T; ++t) {

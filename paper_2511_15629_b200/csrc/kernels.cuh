@@ -160,30 +160,24 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const double* __restrict__ Pt,  // [rows][K]
-                                                                       const double* __restrict__ Vn,  // [K][ld]
-                                                                       double* __restrict__ Wt,        // [rows][ld]
-                                                                       int rows, int K, int S, int ld, int ncol_tiles) {
-  const int lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kDmmaWarps + (threadIdx.x >> 5);
+// One warp: the 8 x 16 output tile `tile` of W = P V (two 8x8 accumulators).
+__device__ __forceinline__ void dmma_tile(const double* __restrict__ Pt, const double* __restrict__ Vn,
+                                          double* __restrict__ Wt, int rows, int K, int S, int ld, int ncol_tiles,
+                                          int tile, int lane) {
   const int r0 = (tile / ncol_tiles) * 8, i0 = (tile % ncol_tiles) * 16;
-  pdl_trigger();
-  if (r0 >= rows) { pdl_wait(); return; }
+  if (r0 >= rows) return;
   const int kq = lane & 3, g = lane >> 2;
   const double* pa = Pt + (size_t)min(r0 + g, rows - 1) * K + kq;       // A: P[r0+g][4j+kq]
   const int c0 = min(i0 + g, ld - 1), c1 = min(i0 + 8 + g, ld - 1);    // B: V[4j+kq][c]
   const double* vb = Vn + (size_t)kq * ld;
   const int nq = (K + 3) >> 2;
   double a[kDmmaChunk], b0[kDmmaChunk], b1[kDmmaChunk];
-  // P (an input) is read before the dependency wait, V (the previous stencil's output) after it
-#pragma unroll
-  for (int q = 0; q < kDmmaChunk; ++q) a[q] = (q < nq && 4 * q + kq < K) ? __ldg(pa + 4 * q) : 0.0;
-  pdl_wait();
 #pragma unroll
   for (int q = 0; q < kDmmaChunk; ++q) {
     const bool in = q < nq && 4 * q + kq < K;
-    b0[q] = in ? __ldg(vb + (size_t)(4 * q) * ld + c0) : 0.0;
-    b1[q] = in ? __ldg(vb + (size_t)(4 * q) * ld + c1) : 0.0;
+    a[q] = in ? __ldg(pa + 4 * q) : 0.0;
+    b0[q] = in ? __ldcg(vb + (size_t)(4 * q) * ld + c0) : 0.0;   // V may be written in-kernel: L2 path
+    b1[q] = in ? __ldcg(vb + (size_t)(4 * q) * ld + c1) : 0.0;
   }
   double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
   for (int q0 = 0; q0 < nq; q0 += kDmmaChunk) {
@@ -193,8 +187,8 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
       const int qq = q0 + kDmmaChunk + q;
       const bool in = qq < nq && 4 * qq + kq < K;
       na[q] = in ? __ldg(pa + 4 * qq) : 0.0;
-      nb0[q] = in ? __ldg(vb + (size_t)(4 * qq) * ld + c0) : 0.0;
-      nb1[q] = in ? __ldg(vb + (size_t)(4 * qq) * ld + c1) : 0.0;
+      nb0[q] = in ? __ldcg(vb + (size_t)(4 * qq) * ld + c0) : 0.0;
+      nb1[q] = in ? __ldcg(vb + (size_t)(4 * qq) * ld + c1) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < kDmmaChunk; ++q) {
@@ -215,6 +209,24 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
     if (c + 8 < S) wr[c + 8] = d10;
     if (c + 9 < S) wr[c + 9] = d11;
   }
+}
+
+__global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const double* __restrict__ Pt,  // [rows][K]
+                                                                       const double* __restrict__ Vn,  // [K][ld]
+                                                                       double* __restrict__ Wt,        // [rows][ld]
+                                                                       int rows, int K, int S, int ld, int ncol_tiles) {
+  pdl_trigger();
+  pdl_wait();
+  dmma_tile(Pt, Vn, Wt, rows, K, S, ld, ncol_tiles, blockIdx.x * kDmmaWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+}
+
+// Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
+__device__ __forceinline__ void gemv_cols(const double* __restrict__ pi, const double* __restrict__ Vn,
+                                          double* __restrict__ Wt, int K, int S, int ld, int i) {
+  if (i >= S) return;
+  double acc = 0.0;
+  for (int kp = 0; kp < K; ++kp) acc = __fma_rn(__ldg(pi + kp), __ldcg(Vn + (size_t)kp * ld + i), acc);
+  Wt[i] = acc;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -258,10 +270,8 @@ __device__ __forceinline__ void run_group(const double* __restrict__ wl, const d
   for (int q = 0; q < R; ++q) hi[q] = lo[q];
 }
 
-__global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm) {
-  extern __shared__ double smem[];
-  const int k = blockIdx.y;
-  const int i0 = blockIdx.x * kTile;
+// One (k, 256-column tile) item of the brute-force stencil, executed by a 256-thread block.
+__device__ __forceinline__ void stencil_item(const StencilParams& prm, int k, int i0, double* smem) {
   const int L = kTile + prm.o_span + kPad + 1;
   double* ws = smem;                           // skew(L) doubles
   double* pay = ws + skew(L) + 8;              // A + 8 doubles
@@ -269,7 +279,6 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
   int* pa = (int*)(pv + kStencilWarps * skew(kTile));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  pdl_trigger();
   const double lam = prm.lambda_t[k];
   for (int a = tid; a < prm.A; a += blockDim.x) {
     double p;
@@ -278,12 +287,11 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
     else p = __dmul_rn(lam, prm.act[a]);                                                 // lambda p
     pay[a] = p;
   }
-  pdl_wait();                          // W_t is the previous contraction's output
   const double* Wrow = prm.W + (prm.rank1 ? 0 : (size_t)k * prm.ld);
   const int g0 = i0 + prm.o_min - kPad;  // global column of tile index 0
   for (int j = tid; j < L; j += blockDim.x) {
     int col = g0 + j;
-    ws[skew(j)] = (col >= 0 && col < prm.S) ? Wrow[col] : -INFINITY;
+    ws[skew(j)] = (col >= 0 && col < prm.S) ? __ldcg(Wrow + col) : -INFINITY;
   }
   __syncthreads();
 
@@ -354,6 +362,13 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilPara
   }
 }
 
+__global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm) {
+  extern __shared__ double smem[];
+  pdl_trigger();
+  pdl_wait();                          // W_t is the previous contraction's output
+  stencil_item(prm, blockIdx.y, blockIdx.x * kTile, smem);
+}
+
 inline size_t stencil_smem_bytes(int A, int o_span) {
   int L = kTile + o_span + kPad + 1;
   return sizeof(double) * (size_t)(skew(L) + 8 + A + 8 + kStencilWarps * skew(kTile)) +
@@ -364,13 +379,13 @@ inline size_t stencil_smem_bytes(int A, int o_span) {
 // Objective J = sum_k pi_1[k] V_1(s0, k) (Eq. 6 at t = 0), fma chain in k order; s0 off the
 // grid is interpolated per k (R24).  One thread.
 // ------------------------------------------------------------------------------------------------
-__global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int ld,
-                                 int f, double w0, int on_grid, double* __restrict__ J) {
-  extern __shared__ double vk[];  // [2][K]: V_1(s0, k) and pi_1[k], gathered in parallel
-  pdl_wait();
+__device__ __forceinline__ void objective_block(const double* __restrict__ V1, const double* __restrict__ pi1, int K,
+                                                int ld, int f, double w0, int on_grid, double* __restrict__ J,
+                                                double* vk /* smem [2][K] */) {
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const double* row = V1 + (size_t)k * ld;
-    vk[k] = on_grid ? row[f] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), row[f]), __dmul_rn(w0, row[f + 1]));
+    vk[k] = on_grid ? __ldcg(row + f)
+                    : __dadd_rn(__dmul_rn(__dsub_rn(1.0, w0), __ldcg(row + f)), __dmul_rn(w0, __ldcg(row + f + 1)));
     vk[K + k] = pi1[k];
   }
   __syncthreads();
@@ -380,14 +395,22 @@ __global__ void objective_kernel(const double* __restrict__ V1, const double* __
   *J = acc;
 }
 
+__global__ void objective_kernel(const double* __restrict__ V1, const double* __restrict__ pi1, int K, int ld,
+                                 int f, double w0, int on_grid, double* __restrict__ J) {
+  extern __shared__ double vk[];  // [2][K]: V_1(s0, k) and pi_1[k], gathered in parallel
+  pdl_wait();
+  objective_block(V1, pi1, K, ld, f, w0, on_grid, J, vk);
+}
+
 // ------------------------------------------------------------------------------------------------
 // Bid curves (Eqs. 7-12): one thread per request (t, i, k).  The caller's output rows
 // serve as the hull stack (vert: action index, price: hull u value, overwritten by prices).
 // ------------------------------------------------------------------------------------------------
 struct BidParams {
-  const double* Wall;     // [T][rows][ld]
+  const double* Wall;     // [T][wrows][ld]
   const double* act; const double* w; const double* omw; const int* off; const double* g;
   int T, K, S, A, rank1, kind, ld;
+  int wrows, k_lo, k_cnt;  // W rows per stage and this rank's price states [k_lo, k_lo + k_cnt)
 };
 
 // Per-action data staged in shared memory for the bid-curve kernel.
@@ -444,7 +467,8 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
   const bool active = rq < n;
   int t = 0, i = 0, k = 0;
   if (active) { t = req[3 * rq + 0]; i = req[3 * rq + 1]; k = req[3 * rq + 2]; }
-  const bool valid = active && t >= 1 && t <= bp.T && i >= 0 && i < bp.S && k >= 0 && k < bp.K;
+  const bool valid = active && t >= 1 && t <= bp.T && i >= 0 && i < bp.S && k >= 0 && k < bp.K &&
+                     (bp.rank1 || (k >= bp.k_lo && k < bp.k_lo + bp.k_cnt));
   if (threadIdx.x == 0) {
     s_tk[0] = t; s_tk[1] = k; s_imin = 1 << 30; s_imax = -1; s_uniform = 1;
   }
@@ -453,11 +477,11 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
   if (active && (!valid || t != s_tk[0] || (k != s_tk[1] && !bp.rank1))) s_uniform = 0;
   __syncthreads();
   const bool staged = s_uniform && s_imax >= 0 && (s_imax - s_imin) < kBidThreads;
-  const double* Wg = bp.Wall + ((size_t)(t - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : k)) * bp.ld;
+  const double* Wg = bp.Wall + ((size_t)(t - 1) * bp.wrows + (bp.rank1 ? 0 : k - bp.k_lo)) * bp.ld;
   const double* Wrow = Wg;
   if (staged) {
     const int c0 = s_imin + o_min;
-    const double* Wb = bp.Wall + ((size_t)(s_tk[0] - 1) * (bp.rank1 ? 1 : bp.K) + (bp.rank1 ? 0 : s_tk[1])) * bp.ld;
+    const double* Wb = bp.Wall + ((size_t)(s_tk[0] - 1) * bp.wrows + (bp.rank1 ? 0 : s_tk[1] - bp.k_lo)) * bp.ld;
     for (int x = threadIdx.x; x < nwt; x += blockDim.x) {
       const int col = c0 + x;
       s_wt[x] = (col >= 0 && col < bp.S) ? Wb[col] : 0.0;
@@ -467,9 +491,11 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
   __syncthreads();
   if (!valid) { if (active) nvert[rq] = -1; return; }
   const BidAct ba{s_act, s_w, s_omw, s_g, s_off};
-  int16_t* gst = vert + rq * cap;
-  auto st_set = [&](int j, int a) { if (kSmem) bst[(size_t)j * blockDim.x + threadIdx.x] = (int16_t)a; else gst[j] = (int16_t)a; };
-  auto st_get = [&](int j) -> int { return kSmem ? bst[(size_t)j * blockDim.x + threadIdx.x] : gst[j]; };
+  // outputs are vertex-major ([cap][n]: entry j of curve rq at j*n + rq) so that a warp's 32 curves
+  // write 32 consecutive words per vertex (coalesced)
+  int16_t* gst = vert + rq;
+  auto st_set = [&](int j, int a) { if (kSmem) bst[(size_t)j * blockDim.x + threadIdx.x] = (int16_t)a; else gst[(size_t)j * n] = (int16_t)a; };
+  auto st_get = [&](int j) -> int { return kSmem ? bst[(size_t)j * blockDim.x + threadIdx.x] : gst[(size_t)j * n]; };
   int nh = 0;
   int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
   double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
@@ -495,15 +521,16 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
     ++nh;
   }
   // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20)
-  int16_t* vo = vert + rq * cap;
-  double* qo = q ? q + rq * cap : nullptr;
-  double* pro = price + rq * cap;
+  int16_t* vo = vert + rq;
+  double* qo = q ? q + rq : nullptr;
+  double* pro = price + rq;
   int a_prev = st_get(0);
   double u_prev;
   bid_point(ba, bp.S, bp.kind, Wrow, i, a_prev, u_prev);
   double p_prev = s_act[a_prev], prev_price = 0.0;
   if (kSmem) vo[0] = (int16_t)a_prev;
   if (qo) qo[0] = p_prev;
+  (void)cap;
   for (int j = 1; j < nh; ++j) {
     const int a = st_get(j);
     double u;
@@ -511,9 +538,9 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
     const double pc = s_act[a];
     double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
     if (j > 1 && pj < prev_price) pj = prev_price;
-    pro[j - 1] = pj;
-    if (kSmem) vo[j] = (int16_t)a;
-    if (qo) qo[j] = pc;
+    pro[(size_t)(j - 1) * n] = pj;
+    if (kSmem) vo[(size_t)j * n] = (int16_t)a;
+    if (qo) qo[(size_t)j * n] = pc;
     prev_price = pj; u_prev = u; p_prev = pc;
   }
   nvert[rq] = nh;
@@ -584,6 +611,7 @@ struct SimParams {
   const double* lambda;  // [T][K]
   const double* act; const double* w; const int* off; const double* g;
   int T, K, S, A, G, rank1, kind, on_grid, f0;
+  int Kp;                // policy rows per stage (K, or world * kmax after a multi-GPU backward)
   double w0;
 };
 
@@ -605,7 +633,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, 
   int k = cdf_sample(sp.cdf1, sp.guide1, sp.K, sp.G, u1);
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double profit = 0.0;
-  const size_t KS = (size_t)sp.K * sp.S;
+  const size_t KS = (size_t)sp.Kp * sp.S;
   for (int t = 1; t <= sp.T; ++t) {
     sim_uniforms(seed, path, t, u1, u2);
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);

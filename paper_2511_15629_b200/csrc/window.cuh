@@ -106,9 +106,9 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
   m2 = unord64(umax64(t.query(l, pos - 1), t.query(pos + 1, r)));
 }
 
-__global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p) {
-  extern __shared__ __align__(16) double wsm[];
-  const int k = blockIdx.y, i0 = blockIdx.x * kWinTile, tid = threadIdx.x;
+// One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.
+__device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, double* wsm) {
+  const int tid = threadIdx.x;
   const int nw = kWinTile + (p.o_max - p.o_min) + 2;
   const int lc = p.pc + 1, ldl = p.pd + 1;
   RangeMax tc, td;
@@ -119,17 +119,15 @@ __global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p
   td.v = tc.v + (size_t)lc * tc.n;
   __shared__ double red[kWinThreads / 32];
 
-  pdl_trigger();
   const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
   const double lam = p.lambda_t[k];
   const double beta_c = __dmul_rn(lam, p.dc);      // lambda delta / eta_c (any few-ulp rounding: see eps)
   const double beta_d = __dmul_rn(lam, p.dd);      // lambda delta eta_d
-  pdl_wait();                          // W_t is the previous contraction's output
   const int wbase = i0 + p.o_min;
   double mx = 0.0;
   for (int x = tid; x < nw; x += kWinThreads) {
     const int col = wbase + x;
-    const double v = (col >= 0 && col < p.S) ? Wrow[col] : -INFINITY;
+    const double v = (col >= 0 && col < p.S) ? __ldcg(Wrow + col) : -INFINITY;
     wt[x] = v;
     if (v != -INFINITY) mx = fmax(mx, fabs(v));
   }
@@ -224,6 +222,13 @@ __global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p
   if (!valid) return;
   p.V[(size_t)k * p.ld + i] = best;
   p.pol[(size_t)k * p.S + i] = (int16_t)arg;
+}
+
+__global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p) {
+  extern __shared__ __align__(16) double wsm[];
+  pdl_trigger();
+  pdl_wait();                          // W_t is the previous contraction's output
+  window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
 }
 
 }  // namespace esdp

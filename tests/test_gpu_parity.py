@@ -18,18 +18,20 @@ pytestmark = pytest.mark.gpu
 import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
 
 
-def _gpu(inst, brute=False, dmma=True):
-    return E.Solver(inst, keep_values=True, force_brute=brute, dmma=dmma)
+def _gpu(inst, brute=False, dmma=True, persist=False, keep=True):
+    return E.Solver(inst, keep_values=keep, force_brute=brute, dmma=dmma, persist=persist)
 
 
-def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None, dmma=True):
+def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None, dmma=True, persist=False):
     pr = to_oracle(inst)
     ref = oracle.backward(pr, nthreads=nthreads)
-    with _gpu(inst, brute, dmma) as s:
+    with _gpu(inst, brute, dmma, persist) as s:
         if expect_window is not None:
-            assert s.stencil_kind == int(expect_window)
+            assert (s.stencil_kind & 1) == int(expect_window)
         if brute:
-            assert s.stencil_kind == 0
+            assert (s.stencil_kind & 1) == 0
+        if persist:
+            assert s.stencil_kind & 2, "persistent plan expected"
         J = s.backward()
         assert np.array_equal(s.actions(), oracle.actions(pr))
         ts = range(1, inst.T + 1) if stages is None else stages
@@ -44,9 +46,10 @@ def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None,
     return ref
 
 
+@pytest.mark.parametrize("plan", ["persist", "graph"])
 @pytest.mark.parametrize("brute", [False, True])
 @pytest.mark.parametrize("seed", range(40))
-def test_random_small_instances(seed, brute):
+def test_random_small_instances(seed, brute, plan):
     kind = [workloads.PAYOFF_LINEAR, workloads.PAYOFF_LINEAR_MINUS_G, workloads.PAYOFF_TABLE][seed % 3]
     inst = workloads.random_instance(seed, S_max=40 if seed % 2 else 600, T=4 + seed % 3, K=1 + seed % 4)
     S, A = oracle.dims(to_oracle(inst))
@@ -55,7 +58,7 @@ def test_random_small_instances(seed, brute):
         inst.g = workloads.random_g(seed, A, 20.0)
     elif kind == workloads.PAYOFF_TABLE:
         inst.g = workloads.random_table(seed, inst.T, inst.K, A)
-    _compare_all(inst, brute=brute)
+    _compare_all(inst, brute=brute, persist=plan == "persist")
 
 
 @pytest.mark.parametrize("dmma", [True, False])
@@ -64,7 +67,9 @@ def test_expectation_tensor_cores_bitexact(K, dmma):
     """FP64 DMMA (mma.sync m8n8k4) expectation: K not a multiple of 4, rows not a multiple of 8, ragged
     columns; bit-identical to the oracle's sequential fma chain (and the DFMA kernel likewise)."""
     inst = workloads.random_instance(1000 + K, T=4, K=K, S_max=300, rank1=False)
-    _compare_all(inst, dmma=dmma)
+    _compare_all(inst, dmma=dmma, persist=False)
+    if dmma:
+        _compare_all(inst, persist=True)
 
 
 @pytest.mark.parametrize("brute", [False, True])
@@ -120,8 +125,46 @@ def test_cfg2_full_size_bruteforce():
     _compare_all(workloads.cfg2(), nthreads=16, brute=True)
 
 
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg2-small"])
+def test_dist_path_single_rank_bitexact(name):
+    """esdp_create_dist with world = 1: the K-partitioned graph with the per-stage NCCL all-gather of V_t
+    and pol_t (a copy on one rank) gives the oracle's results bit for bit."""
+    inst = workloads.cfg2(T=24, K=20) if name == "cfg2-small" else workloads.cfg1("b", rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=8)
+    nid = E.esdp_nccl_unique_id()
+    with E.Solver(inst, keep_values=True, dist=(1, 0, nid)) as s:
+        assert not (s.stencil_kind & 2)          # graph plan (NCCL between stages)
+        assert s.backward() == ref.J
+        for t in range(1, inst.T + 1):
+            V, W = s.values(t)
+            assert np.array_equal(V, ref.V[t - 1]) and np.array_equal(W, ref.W[t - 1])
+            assert np.array_equal(s.policy(t), ref.pol[t - 1])
+        per, m, v = s.simulate(500, 3)
+        per_ref, _, _ = oracle.simulate(pr, ref.pol, 500, 3)
+        assert np.array_equal(per, per_ref)
+
+
 def test_cfg2_full_size_dfma_expectation():
-    _compare_all(workloads.cfg2(), nthreads=16, dmma=False)
+    _compare_all(workloads.cfg2(), nthreads=16, dmma=False, persist=False)
+
+
+def test_cfg2_full_size_persistent_plan():
+    _compare_all(workloads.cfg2(), nthreads=16, persist=True, expect_window=True)
+
+
+@pytest.mark.parametrize("persist", [True, False])
+def test_cfg2_no_keep_values(persist):
+    """Without ESDP_KEEP_VALUES the backward ping-pongs V/W; V_1, every policy and J are unchanged."""
+    inst = workloads.cfg2(T=40, K=30)
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=8)
+    with _gpu(inst, persist=persist, keep=False) as s:
+        assert s.backward() == ref.J
+        V1 = E.esdp_values(s.ctx, 1, want_W=False)
+        assert np.array_equal(V1, ref.V[0])
+        for t in range(1, inst.T + 1):
+            assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
 def test_cfg2_rank1_full_size():

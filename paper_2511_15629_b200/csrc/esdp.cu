@@ -357,6 +357,7 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
     wp.o_min = c->o_min; wp.o_max = c->o_max;
     wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
     wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
+    wp.bspan = c->delta * (double)(c->S + (c->o_max - c->o_min) + 2) / std::min(c->eta_c, c->eta_d);
     return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
   }
   StencilParams prm;
@@ -389,6 +390,7 @@ PersistParams persist_params(esdp_ctx* c) {
   wp.o_min = c->o_min; wp.o_max = c->o_max;
   wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
   wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
+  wp.bspan = c->delta * (double)(c->S + (c->o_max - c->o_min) + 2) / std::min(c->eta_c, c->eta_d);
   pp.use_window = c->use_window;
   pp.T = c->T; pp.K = c->K; pp.S = c->S; pp.A = c->A; pp.ld = c->ld; pp.rows = (int)w_rows(c);
   pp.rank1 = c->rank1; pp.kind = c->kind; pp.keep = keep(c) ? 1 : 0;

@@ -28,6 +28,8 @@ constexpr int kWinTile = 256;     // output columns per block
 __device__ unsigned long long g_window_fallbacks;  // rows that needed the full canonical scan (diagnostic)
 constexpr int kWinThreads = 256;  // one output column per thread in the query phase
 
+constexpr int kMaxSingles = 16;  // singles staged in shared memory (more: read from global)
+
 struct WinParams {
   const double* W; double* V; int16_t* pol; const double* lambda_t;
   const double* act; const double* w; const double* omw; const int* off;
@@ -38,6 +40,7 @@ struct WinParams {
   int o_min, o_max;         // tile halo over all live actions
   double delta, eta_c, eta_d, pbar;
   double dc, dd;            // delta / eta_c and delta * eta_d (for the approximate keys only)
+  double bspan;             // delta (S + span + 2) / min(eta_c, eta_d): bounds |beta * j| over the tile
 };
 
 // Packed keys: an order-preserving 64-bit image of the (approximate) value with its table position in
@@ -91,11 +94,30 @@ __device__ __forceinline__ double canon_single(const WinParams& p, const double*
   return __dadd_rn(__dmul_rn(lam, __ldg(p.act + a)), wint);
 }
 
+// a single action's data staged in shared memory for the whole block
+struct SingleAct {
+  double pay;   // fl(lambda * p_a) for this block's k
+  double w, omw;
+  int off, a;
+};
+
+__device__ __forceinline__ double canon_staged(const SingleAct& s, const double* __restrict__ wt, int wbase, int i) {
+  const int x = i + s.off - wbase;
+  const double wint = (s.w == 0.0) ? wt[x] : __dadd_rn(__dmul_rn(s.omw, wt[x]), __dmul_rn(s.w, wt[x + 1]));
+  return __dadd_rn(s.pay, wint);
+}
+
+// level q of a table: entry x = max(level q-1 at x, at x + 2^(q-1)), for x <= n - 2^q.  Straight-line:
+// each thread owns x = tid, tid + 256, tid + 512 (n <= 256 + 512).
 __device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
   const int h = 1 << (q - 1), lim = t.n - (1 << q);
   const unsigned long long* pv = t.v + (q - 1) * t.n;
   unsigned long long* nv = t.v + q * t.n;
-  for (int x = tid; x <= lim; x += kWinThreads) nv[x] = umax64(pv[x], pv[x + h]);
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int x = tid + u * kWinThreads;
+    if (x <= lim) nv[x] = umax64(pv[x], pv[x + h]);
+  }
 }
 
 // top-2 of the window [l, r] of table t: best (value, table position) and the runner-up value
@@ -117,19 +139,32 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   double* wt = wsm;                        // W over columns [wbase, wbase + nw)
   tc.v = (unsigned long long*)(wt + nw);
   td.v = tc.v + (size_t)lc * tc.n;
-  __shared__ double red[kWinThreads / 32];
+  __shared__ unsigned long long red[kWinThreads / 32];
+  __shared__ SingleAct ss[kMaxSingles];
 
   const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
   const double lam = p.lambda_t[k];
   const double beta_c = __dmul_rn(lam, p.dc);      // lambda delta / eta_c (any few-ulp rounding: see eps)
   const double beta_d = __dmul_rn(lam, p.dd);      // lambda delta eta_d
   const int wbase = i0 + p.o_min;
-  double mx = 0.0;
+  const int nsg = p.nsingle < kMaxSingles ? p.nsingle : kMaxSingles;
+  if (tid < nsg) {
+    const int a = __ldg(p.singles + tid);
+    SingleAct s;
+    s.a = a; s.off = __ldg(p.off + a); s.w = __ldg(p.w + a); s.omw = __ldg(p.omw + a);
+    s.pay = __dmul_rn(lam, __ldg(p.act + a));
+    ss[tid] = s;
+  }
+  unsigned long long mx = 0ull;   // max |W| over the tile, as ordered bits of a non-negative double
   for (int x = tid; x < nw; x += kWinThreads) {
     const int col = wbase + x;
-    const double v = (col >= 0 && col < p.S) ? __ldcg(Wrow + col) : -INFINITY;
+    double v = -INFINITY;
+    if (col >= 0 && col < p.S) {
+      v = __ldcg(Wrow + col);
+      const unsigned long long ab = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+      mx = ab > mx ? ab : mx;
+    }
     wt[x] = v;
-    if (v != -INFINITY) mx = fmax(mx, fabs(v));
   }
   __syncthreads();
   // level 0: packed key(j) = W[j] - beta*j, position x
@@ -142,7 +177,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     td.v[x] = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
   }
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  for (int s = 16; s > 0; s >>= 1) mx = umax64(mx, __shfl_xor_sync(0xffffffffu, mx, s));
   if ((tid & 31) == 0) red[tid >> 5] = mx;
   __syncthreads();
   const int top = p.pc > p.pd ? p.pc : p.pd;
@@ -152,11 +187,11 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     __syncthreads();
   }
   (void)ldl;
-  double M = 0.0;
+  unsigned long long mb = red[0];
 #pragma unroll
-  for (int w = 0; w < kWinThreads / 32; ++w) M = fmax(M, red[w]);
-  const double span = (double)(p.S + (p.o_max - p.o_min) + 2);
-  const double bmax = fabs(lam) * p.delta * span / fmin(p.eta_c, p.eta_d);
+  for (int w = 1; w < kWinThreads / 32; ++w) mb = umax64(mb, red[w]);
+  const double M = __longlong_as_double((long long)mb);
+  const double bmax = fabs(lam) * p.bspan;    // |lambda| delta (S + span) / min(eta), factor from the host
   // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
   // the <1024-ulp truncation of the packed keys (|key| <= M + bmax)
   const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar) + 0x1p-41 * (M + bmax);
@@ -183,15 +218,23 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
       if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
       else b2 = fmax(b2, y1);
     }
-    for (int s = 0; s < p.nsingle; ++s) {
+    double c1 = 0.0;      // canonical value of the best single (exact)
+    bool single_best = false;
+    for (int s = 0; s < nsg; ++s) {
+      const double c = canon_staged(ss[s], wt, wbase, i);
+      if (c > b1) { b2 = b1; b1 = c; a1 = ss[s].a; c1 = c; single_best = true; }
+      else b2 = fmax(b2, c);
+    }
+    for (int s = nsg; s < p.nsingle; ++s) {
       const int a = __ldg(p.singles + s);
       const double c = canon_single(p, wt, wbase, i, a, lam);
-      if (c > b1) { b2 = b1; b1 = c; a1 = a; }
+      if (c > b1) { b2 = b1; b1 = c; a1 = a; c1 = c; single_best = true; }
       else b2 = fmax(b2, c);
     }
     if (__dsub_rn(b1, b2) > 2.0 * eps) {
       arg = a1;
-      best = canon_single(p, wt, wbase, i, a1, lam);   // canonical value of the unique argmax
+      // canonical value of the unique argmax (a run action: one product and one add)
+      best = single_best ? c1 : canon_single(p, wt, wbase, i, a1, lam);
     } else {
       near_tie = true;
     }
@@ -224,7 +267,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   p.pol[(size_t)k * p.S + i] = (int16_t)arg;
 }
 
-__global__ void __launch_bounds__(kWinThreads) window_stencil_kernel(WinParams p) {
+__global__ void __launch_bounds__(kWinThreads, 4) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
   pdl_trigger();
   pdl_wait();                          // W_t is the previous contraction's output

@@ -162,6 +162,9 @@ def run_ours(args):
     nv_d = torch.empty(max(n_bid, 1), dtype=torch.int32, device=dev)
     vert_d = torch.empty(max(n_bid, 1) * cap, dtype=torch.int16, device=dev)
     pr_d = torch.empty(max(n_bid, 1) * cap, dtype=torch.float64, device=dev)
+    fused = args.bids == "fused" and n_bid > 0
+    if fused:   # a6 inside the backward graph: stage t's curves in a side branch as soon as W_t exists
+        E.esdp_set_bid_requests(solver.ctx, req, cap, nv_d.data_ptr(), vert_d.data_ptr(), None, pr_d.data_ptr())
     n_paths = args.paths // world if kpart else args.paths      # kpart: the paths are shared out too
     per_d = torch.empty(n_paths, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -173,7 +176,7 @@ def run_ours(args):
         E.esdp_backward_async(solver.ctx, sp)
         if marks:
             marks[1].record(stream)
-        if n_bid:
+        if n_bid and not fused:
             E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
                                  None, pr_d.data_ptr(), sp)
         if marks:
@@ -182,7 +185,7 @@ def run_ours(args):
         if marks:
             marks[3].record(stream)
 
-    launches_per_step = E.esdp_launch_count(solver.ctx) + (1 if n_bid else 0) + 1
+    launches_per_step = E.esdp_launch_count(solver.ctx) + (1 if n_bid and not fused else 0) + 1
     with torch.cuda.stream(stream):
         for j in range(args.warmup):
             flush.fill_(float(j))
@@ -236,7 +239,7 @@ def run_ours(args):
         st = E.lib.esdp_load(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
         assert st == 0, E.esdp_last_error(solver.ctx)
         assert E.lib.esdp_backward(solver.ctx, sp, ctypes.byref(Jh)) == 0
-        if n_bid:
+        if n_bid and not fused:
             E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
                                  None, pr_d.data_ptr(), sp)
         assert E.lib.esdp_simulate(solver.ctx, n_paths, 99 + j, ctypes.byref(m_), ctypes.byref(v_), None) == 0
@@ -283,9 +286,11 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write outside the step events)",
                        "parallelism": (f"K-partitioned x{world} (NCCL all-gather of V_t per stage)" if kpart else
                                        f"instance-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU"),
-                       "plan": {"stencil": "window" if plan & 1 else "brute", "backward": "persistent" if plan & 2 else "graph"}},
+                       "plan": {"stencil": "window" if plan & 1 else "brute", "backward": "persistent" if plan & 2 else "graph",
+                                "bidcurves": "fused into the backward graph" if fused else "after the backward"}},
             "gpu_launches": launches_per_step * args.steps,
-            "ms_per_part": {"backward": part[0], "bidcurves": part[1], "simulate": part[2]},
+            "ms_per_part": {"backward" + ("+bidcurves (fused branch)" if fused else ""): part[0],
+                            "bidcurves": None if fused else part[1], "simulate": part[2]},
             "backward_phase_ms": {"expectation": phases[0], "stencil": phases[1]} if args.kernel_events else None,
             "roofline": {"bound": "alu",
                          "kernel": "backward (%s)" % ("persistent cooperative kernel" if plan & 2 else "graph of 2T kernels"),
@@ -383,6 +388,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-events", type=int, default=1,
                     help="per-phase device timers inside the backward (persistent plan) / events (graph plan)")
+    ap.add_argument("--bids", choices=["fused", "after"], default="fused",
+                    help="bid curves as side branches of the backward graph (fused) or one kernel after it")
     ap.add_argument("--mode", choices=["instances", "kpart"], default="instances",
                     help="N>1: independent instances per rank (weak) or one K-partitioned instance (strong)")
     args = ap.parse_args()

@@ -152,6 +152,14 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* ctx, int64_t n, const int32_t* req_dev,
                                int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev,
                                void* stream);
 
+/* Register bid-curve requests that every following backward pass extracts INSIDE the stage chain: the
+ * curves of stage t are built from W_t in a side branch of the backward graph as soon as W_t exists,
+ * concurrently with the remaining (latency-bound) stages.  req: HOST [n][3] (t, i, k), copied; outputs:
+ * DEVICE arrays in the layout of esdp_bidcurves_dev (vertex-major [cap][n]; q_dev may be NULL), written
+ * by each backward pass.  n = 0 removes the requests.  Needs ESDP_KEEP_VALUES and the graph plan. */
+esdp_status esdp_set_bid_requests(esdp_ctx* ctx, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert_dev,
+                                  int16_t* vert_dev, double* q_dev, double* price_dev);
+
 /* Forward simulation of the argmax policy on n_paths sampled price paths:
  *   k_1 ~ pi_1; for t = 1..T: a = pol_t(i, k); profit += pay(t,k,a);
  *   i <- i + o_a (+1 with probability w_a at the interpolated endpoints: the lottery that the

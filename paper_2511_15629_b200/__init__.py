@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
-    "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition",
+    "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -94,6 +94,7 @@ def _load():
         "esdp_create_dist": ([ctypes.POINTER(esdp_problem), ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p,
                               ctypes.POINTER(_vp)], ctypes.c_int),
         "esdp_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+        "esdp_set_bid_requests": ([ctx, ctypes.c_int64, _i32p, ctypes.c_int32, _vp, _vp, _vp, _vp], ctypes.c_int),
         "esdp_partition": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
         "esdp_last_error": ([ctx], ctypes.c_char_p),
@@ -238,6 +239,13 @@ def esdp_bidcurves(ctx, req, cap=None):
 def esdp_bidcurves_dev(ctx, n, req_ptr, cap, nvert_ptr, vert_ptr, q_ptr, price_ptr, stream=None):
     _check(lib.esdp_bidcurves_dev(ctx, int(n), req_ptr, int(cap), nvert_ptr, vert_ptr, q_ptr, price_ptr,
                                   _stream_ptr(stream)), "esdp_bidcurves_dev", ctx)
+
+
+def esdp_set_bid_requests(ctx, req, cap, nvert_ptr, vert_ptr, q_ptr, price_ptr):
+    """Bid curves extracted inside every following backward pass (device outputs, vertex-major)."""
+    req = np.ascontiguousarray(req, dtype=np.int32).reshape(-1, 3)
+    _check(lib.esdp_set_bid_requests(ctx, req.shape[0], _p(req, _i32p), int(cap), nvert_ptr, vert_ptr, q_ptr, price_ptr),
+           "esdp_set_bid_requests", ctx)
 
 
 def esdp_simulate(ctx, n_paths, seed, per_path=True):

@@ -82,6 +82,17 @@ struct esdp_ctx {
   int persist = 0, persist_grid = 0;
   size_t persist_smem = 0;
   unsigned long long* d_stamps = nullptr;
+  // bid-curve requests extracted inside the backward graph (esdp_set_bid_requests)
+  int64_t fb_n = 0;
+  int32_t fb_cap = 0;
+  int32_t *d_fb_req = nullptr, *d_fb_slot = nullptr;
+  std::vector<int64_t> fb_off;   // [T+2]: requests of stage t are [fb_off[t], fb_off[t+1])
+  int32_t* fb_nvert = nullptr;
+  int16_t* fb_vert = nullptr;
+  double *fb_q = nullptr, *fb_price = nullptr;
+  int fb_batch = 1;
+  std::vector<cudaStream_t> side;      // side streams of the bid-curve branches
+  std::vector<cudaEvent_t> fb_ev, join_ev;
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   int prof_stride = 1;
   bool pdl = true;
@@ -258,8 +269,11 @@ void free_all(esdp_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->comm) ncclCommDestroy(c->comm);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->fb_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
+  for (cudaStream_t x : c->side) cudaStreamDestroy(x);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_stamps, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_stamps, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -408,6 +422,26 @@ cudaError_t launch_persistent(esdp_ctx* c, cudaStream_t s) {
                                      c->persist_smem, s);
 }
 
+cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const int32_t* slot_dev, int64_t nout, int32_t cap,
+                        int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev, cudaStream_t s) {
+  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld,
+               (int)w_rows(c), c->k_lo, c->rank1 ? c->K : c->k_cnt};
+  const int span = c->o_max - c->o_min;
+  const unsigned blocks = (unsigned)((n + kBidThreads - 1) / kBidThreads);
+  size_t sm = bid_smem_bytes(c->A, span, true);
+  if (sm <= 200 * 1024) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    bidcurve_kernel<true><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev,
+                                                           vert_dev, q_dev, price_dev);
+  } else {
+    sm = bid_smem_bytes(c->A, span, false);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    bidcurve_kernel<false><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev,
+                                                            vert_dev, q_dev, price_dev);
+  }
+  return cudaGetLastError();
+}
+
 // Enqueue the 2T launches of one backward pass on stream s (PDL between consecutive kernels).
 esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   const int T = c->T;
@@ -421,6 +455,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     return sampled(t) ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
   };
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
+  bool forked = false;
   for (int t = T; t >= 1; --t) {
     if (t == T) {
       CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, t), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
@@ -431,6 +466,24 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
       CUDA_OR_FAIL(c, mark(t, 1));
       after_kernel = true;
       ++n;
+    }
+    // bid curves need only W_t.  Stages are batched (fb_batch stages per launch, so each launch has enough
+    // curves to fill the GPU) and every batch is a side branch of the graph on its own stream: it runs
+    // concurrently with the remaining, latency-bound stages of the chain.
+    const int bt = (t - 1) / c->fb_batch;                       // batch of stage t (stages bt*B+1 .. bt*B+B)
+    if (c->fb_n > 0 && (t - 1) % c->fb_batch == 0) {            // t is the lowest stage of its batch: W ready
+      const int t_hi = std::min(c->T, t + c->fb_batch - 1);
+      const int64_t lo = c->fb_off[t], cnt = c->fb_off[t_hi + 1] - lo;
+      if (cnt > 0) {
+        cudaStream_t sb = c->side[bt % c->side.size()];
+        CUDA_OR_FAIL(c, cudaEventRecord(c->fb_ev[t - 1], s));
+        CUDA_OR_FAIL(c, cudaStreamWaitEvent(sb, c->fb_ev[t - 1], 0));
+        CUDA_OR_FAIL(c, launch_bids(c, cnt, c->d_fb_req + 3 * lo, c->d_fb_slot + lo, c->fb_n, c->fb_cap, c->fb_nvert,
+                                    c->fb_vert, c->fb_q, c->fb_price, sb));
+        forked = true;
+        after_kernel = false;
+        ++n;
+      }
     }
     CUDA_OR_FAIL(c, mark(t, 2));
     CUDA_OR_FAIL(c, launch_stencil(c, t, s, pdl && after_kernel && !sampled(t), false));
@@ -450,8 +503,28 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   }
   CUDA_OR_FAIL(c, launch_objective(c, s, pdl && after_kernel));
   ++n;
+  if (forked) {   // join the bid-curve branches
+    for (size_t j = 0; j < c->side.size(); ++j) {
+      CUDA_OR_FAIL(c, cudaEventRecord(c->join_ev[j], c->side[j]));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->join_ev[j], 0));
+    }
+  }
   CUDA_OR_FAIL(c, cudaGetLastError());
   c->launches = n;
+  return ESDP_OK;
+}
+
+esdp_status capture_graph(esdp_ctx* c) {
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  cudaGraph_t g = nullptr;
+  CUDA_OR_FAIL(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  esdp_status est = enqueue_backward(c, c->stream);
+  cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+  if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); return est; }
+  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
   return ESDP_OK;
 }
 
@@ -637,15 +710,19 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
       if (cudaEventCreate(&e) != cudaSuccess) { fail(c, ESDP_E_CUDA, "cudaEventCreate failed"); return bail(ESDP_E_CUDA); }
   }
   // capture the whole backward pass once; replay it for every solve
-  cudaGraph_t g = nullptr;
-  if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph capture failed"); return bail(ESDP_E_CUDA); }
-  esdp_status est = enqueue_backward(c, c->stream);
-  cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-  if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); return bail(est); }
-  if (ce != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce)); return bail(ESDP_E_CUDA); }
-  ce = cudaGraphInstantiate(&c->graph, g, 0);
-  cudaGraphDestroy(g);
-  if (ce != cudaSuccess) { fail(c, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); return bail(ESDP_E_CUDA); }
+  c->fb_batch = std::max(1, (c->T + 7) / 8);   // ~8 bid-curve batches per backward
+  c->side.assign(4, nullptr);
+  c->join_ev.assign(c->side.size(), nullptr);
+  for (size_t j = 0; j < c->side.size(); ++j)
+    if (cudaStreamCreateWithFlags(&c->side[j], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join_ev[j], cudaEventDisableTiming) != cudaSuccess) {
+      fail(c, ESDP_E_CUDA, "side stream");
+      return bail(ESDP_E_CUDA);
+    }
+  c->fb_ev.resize((size_t)c->T + 1);
+  for (auto& ev : c->fb_ev)
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { fail(c, ESDP_E_CUDA, "event"); return bail(ESDP_E_CUDA); }
+  TRY(capture_graph(c));
 #undef TRY
   *out = c;
   return ESDP_OK;
@@ -745,22 +822,50 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
   if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
   if (cap < c->A) return fail(c, ESDP_E_STATE, "cap %d < A %d", cap, c->A);
   if (n <= 0) return ESDP_OK;
-  BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld,
-               (int)w_rows(c), c->k_lo, c->rank1 ? c->K : c->k_cnt};
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  const int span = c->o_max - c->o_min;
-  const unsigned blocks = (unsigned)((n + kBidThreads - 1) / kBidThreads);
-  size_t sm = bid_smem_bytes(c->A, span, true);
-  if (sm <= 200 * 1024) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    bidcurve_kernel<true><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, cap, c->o_min, span, nvert_dev, vert_dev, q_dev, price_dev);
-  } else {
-    sm = bid_smem_bytes(c->A, span, false);
-    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    bidcurve_kernel<false><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, cap, c->o_min, span, nvert_dev, vert_dev, q_dev, price_dev);
-  }
-  CUDA_OR_FAIL(c, cudaGetLastError());
+  CUDA_OR_FAIL(c, launch_bids(c, n, req_dev, nullptr, n, cap, nvert_dev, vert_dev, q_dev, price_dev, s));
   return ESDP_OK;
+}
+
+esdp_status esdp_set_bid_requests(esdp_ctx* c, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert_dev,
+                                  int16_t* vert_dev, double* q_dev, double* price_dev) {
+  if (!c) return ESDP_E_STATE;
+  if (c->persist) return fail(c, ESDP_E_STATE, "fused bid curves need the graph plan");
+  if (n > 0) {
+    if (!keep(c)) return fail(c, ESDP_E_STATE, "fused bid curves need ESDP_KEEP_VALUES");
+    if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
+    if (cap < c->A || !req || !nvert_dev || !vert_dev || !price_dev) return fail(c, ESDP_E_STATE, "bad bid request arguments");
+    for (int64_t r = 0; r < n; ++r) {
+      const int t = req[3 * r], i = req[3 * r + 1], k = req[3 * r + 2];
+      if (t < 1 || t > c->T || i < 0 || i >= c->S || k < 0 || k >= c->K || (!c->rank1 && (k < c->k_lo || k >= c->k_lo + c->k_cnt)))
+        return fail(c, ESDP_E_STATE, "request %lld (t=%d, i=%d, k=%d) out of range for this rank", (long long)r, t, i, k);
+    }
+  }
+  // stable counting sort by stage
+  std::vector<int64_t> off((size_t)c->T + 2, 0);
+  for (int64_t r = 0; r < n; ++r) off[req[3 * r] + 1]++;
+  for (int t = 1; t <= c->T + 1; ++t) off[t] += off[t - 1];
+  std::vector<int32_t> sreq((size_t)std::max<int64_t>(n, 1) * 3), slot((size_t)std::max<int64_t>(n, 1));
+  std::vector<int64_t> pos(off.begin(), off.end());
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t p = pos[req[3 * r]]++;
+    sreq[3 * p] = req[3 * r]; sreq[3 * p + 1] = req[3 * r + 1]; sreq[3 * p + 2] = req[3 * r + 2];
+    slot[p] = (int32_t)r;
+  }
+  cudaFree(c->d_fb_req); cudaFree(c->d_fb_slot);
+  c->d_fb_req = nullptr; c->d_fb_slot = nullptr;
+  c->fb_n = 0;
+  if (n > 0) {
+    if (dev_alloc(c, &c->d_fb_req, 3 * n) || dev_alloc(c, &c->d_fb_slot, n)) return ESDP_E_NOMEM;
+    CUDA_OR_FAIL(c, cudaMemcpy(c->d_fb_req, sreq.data(), 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(c, cudaMemcpy(c->d_fb_slot, slot.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // off[t] is the first request of stage t (1-based stages)
+    c->fb_off = off;   // stage t's requests are [off[t], off[t+1])
+  }
+  c->fb_n = n;
+  c->fb_cap = cap;
+  c->fb_nvert = nvert_dev; c->fb_vert = vert_dev; c->fb_q = q_dev; c->fb_price = price_dev;
+  return capture_graph(c);
 }
 
 esdp_status esdp_bidcurves(esdp_ctx* c, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert, int16_t* vert,

@@ -444,9 +444,11 @@ inline size_t bid_smem_bytes(int A, int o_span, bool stack_in_smem) {
 // shared memory.  kSmem = false: the stack lives in the caller's vert row (very large A).
 template <bool kSmem>
 __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req,
+                                                               const int32_t* __restrict__ slot, int64_t nout,
                                                                int cap, int o_min, int o_span,
                                                                int32_t* __restrict__ nvert, int16_t* __restrict__ vert,
                                                                double* __restrict__ q, double* __restrict__ price) {
+  // request rq writes output slot `slot[rq]` (or rq) of the vertex-major arrays [cap][nout]
   extern __shared__ __align__(16) double bsm[];
   const int A = bp.A;
   double* s_act = bsm;
@@ -489,19 +491,39 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
     Wrow = s_wt - c0;
   }
   __syncthreads();
-  if (!valid) { if (active) nvert[rq] = -1; return; }
+  const int64_t so = slot ? (int64_t)slot[rq < n ? rq : 0] : rq;
+  if (!valid) { if (active) nvert[so] = -1; return; }
   const BidAct ba{s_act, s_w, s_omw, s_g, s_off};
-  // outputs are vertex-major ([cap][n]: entry j of curve rq at j*n + rq) so that a warp's 32 curves
+  // feasible actions of row i form one interval [a_lo, a_hi]: the offsets o_a and ceil(e_a) = o_a + [w_a > 0]
+  // are non-increasing in a (F is decreasing), so Eq. 4's two bounds cut a prefix and a suffix
+  int a_hi, a_lo;
+  {
+    int lo = 0, hi = A;                              // first a with o_a < -i  -> a_hi = that - 1
+    while (lo < hi) { const int m = (lo + hi) >> 1; if (s_off[m] < -i) hi = m; else lo = m + 1; }
+    a_hi = lo - 1;
+    lo = 0; hi = A;                                  // first a with o_a + [w_a > 0] <= S-1-i
+    while (lo < hi) { const int m = (lo + hi) >> 1; if (s_off[m] + (s_w[m] != 0.0 ? 1 : 0) <= bp.S - 1 - i) hi = m; else lo = m + 1; }
+    a_lo = lo;
+  }
+  auto u_of = [&](int a) -> double {                 // Eq. 7 point value, a known feasible
+    const int x = i + s_off[a];
+    const double wa = s_w[a];
+    double u = (wa == 0.0) ? Wrow[x] : __dadd_rn(__dmul_rn(s_omw[a], Wrow[x]), __dmul_rn(wa, Wrow[x + 1]));
+    if (bp.kind == 1) u = __dsub_rn(u, s_g[a]);
+    return u;
+  };
+  // outputs are vertex-major ([cap][nout]: entry j of curve so at j*nout + so) so that a warp's 32 curves
   // write 32 consecutive words per vertex (coalesced)
-  int16_t* gst = vert + rq;
-  auto st_set = [&](int j, int a) { if (kSmem) bst[(size_t)j * blockDim.x + threadIdx.x] = (int16_t)a; else gst[(size_t)j * n] = (int16_t)a; };
-  auto st_get = [&](int j) -> int { return kSmem ? bst[(size_t)j * blockDim.x + threadIdx.x] : gst[(size_t)j * n]; };
+  int16_t* gst = vert + so;
+  const unsigned bstride = blockDim.x;
+  int16_t* bs = bst + threadIdx.x;
+  auto st_set = [&](int j, int a) { if (kSmem) bs[(unsigned)j * bstride] = (int16_t)a; else gst[(size_t)j * nout] = (int16_t)a; };
+  auto st_get = [&](int j) -> int { return kSmem ? bs[(unsigned)j * bstride] : gst[(size_t)j * nout]; };
   int nh = 0;
   int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
   double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
-  for (int a = 0; a < A; ++a) {
-    double u;
-    if (!bid_point(ba, bp.S, bp.kind, Wrow, i, a, u)) continue;
+  for (int a = a_lo; a <= a_hi; ++a) {
+    const double u = u_of(a);
     const double pc = s_act[a];
     while (nh >= 2) {
       const double cr = __dsub_rn(__dmul_rn(__dsub_rn(pb, po), __dsub_rn(u, uo)),
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
       ab = ao; ub = uo; pb = po;
       if (nh >= 2) {
         ao = st_get(nh - 2);
-        bid_point(ba, bp.S, bp.kind, Wrow, i, ao, uo);
+        uo = u_of(ao);
         po = s_act[ao];
       }
     }
@@ -521,29 +543,27 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
     ++nh;
   }
   // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20)
-  int16_t* vo = vert + rq;
-  double* qo = q ? q + rq : nullptr;
-  double* pro = price + rq;
+  int16_t* vo = vert + so;
+  double* qo = q ? q + so : nullptr;
+  double* pro = price + so;
   int a_prev = st_get(0);
-  double u_prev;
-  bid_point(ba, bp.S, bp.kind, Wrow, i, a_prev, u_prev);
+  double u_prev = u_of(a_prev);
   double p_prev = s_act[a_prev], prev_price = 0.0;
   if (kSmem) vo[0] = (int16_t)a_prev;
   if (qo) qo[0] = p_prev;
   (void)cap;
   for (int j = 1; j < nh; ++j) {
     const int a = st_get(j);
-    double u;
-    bid_point(ba, bp.S, bp.kind, Wrow, i, a, u);
+    const double u = u_of(a);
     const double pc = s_act[a];
     double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
     if (j > 1 && pj < prev_price) pj = prev_price;
-    pro[(size_t)(j - 1) * n] = pj;
-    if (kSmem) vo[(size_t)j * n] = (int16_t)a;
-    if (qo) qo[(size_t)j * n] = pc;
+    pro[(size_t)(j - 1) * nout] = pj;
+    if (kSmem) vo[(size_t)j * nout] = (int16_t)a;
+    if (qo) qo[(size_t)j * nout] = pc;
     prev_price = pj; u_prev = u; p_prev = pc;
   }
-  nvert[rq] = nh;
+  nvert[so] = nh;
 }
 
 // ------------------------------------------------------------------------------------------------

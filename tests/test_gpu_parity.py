@@ -202,6 +202,45 @@ def test_cfg3_nonconcave_payoff_and_bids():
         assert np.all(np.diff(out["price"][j, :n - 1]) >= 0)
 
 
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg3"])
+def test_fused_bidcurves_in_backward(name):
+    """esdp_set_bid_requests: curves extracted inside the backward graph (side branch per stage, unsorted
+    requests over all stages) equal the oracle's bit for bit, on every backward pass."""
+    import torch
+    if name == "cfg3":
+        base = workloads.cfg2(T=2, K=2)
+        inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=30, K=20)
+    else:
+        inst = workloads.cfg1("b", rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr)
+    rng = np.random.default_rng(5)
+    n = 3000
+    req = np.stack([rng.integers(1, inst.T + 1, n), rng.integers(0, inst.S, n), rng.integers(0, inst.K, n)], 1)
+    with _gpu(inst) as s:
+        cap = s.A
+        nv = torch.zeros(n, dtype=torch.int32, device="cuda")
+        vert = torch.zeros(cap * n, dtype=torch.int16, device="cuda")
+        q = torch.zeros(cap * n, dtype=torch.float64, device="cuda")
+        price = torch.zeros(cap * n, dtype=torch.float64, device="cuda")
+        E.esdp_set_bid_requests(s.ctx, req, cap, nv.data_ptr(), vert.data_ptr(), q.data_ptr(), price.data_ptr())
+        for rep in range(2):
+            nv.zero_(); vert.zero_(); price.zero_()
+            s.backward()
+            torch.cuda.synchronize()
+            nvh = nv.cpu().numpy(); vh = vert.cpu().numpy().reshape(cap, n); ph = price.cpu().numpy().reshape(cap, n)
+            qh = q.cpu().numpy().reshape(cap, n)
+            for j in range(0, n, 7):
+                t, i, k = (int(x) for x in req[j])
+                c = oracle.bidcurve(pr, ref.W, t, i, k)
+                m = nvh[j]
+                assert m == c["nvert"]
+                assert np.array_equal(vh[:m, j], c["vert"]) and np.array_equal(qh[:m, j], c["q"])
+                assert np.array_equal(ph[:m - 1, j], c["price"])
+        E.esdp_set_bid_requests(s.ctx, np.zeros((0, 3), np.int32), cap, None, None, None, None)
+        assert s.backward() == ref.J
+
+
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1"])
 def test_bidcurves_cfg1(name):
     inst = workloads.cfg1("b", rank1=name.endswith("rank1"))

@@ -63,6 +63,8 @@ enum {
   ESDP_PDL = 8u,          /* launch the per-stage kernels with programmatic dependent launch (opt-in:
                              measured slower on B200 for this chain) */
   ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
+  ESDP_DMMA_L2 = 64u,     /* DMMA expectation with operands read straight from L2 by every warp
+                             (instead of staged once per block in shared memory) */
   ESDP_PERSIST = 32u      /* run the backward pass as ONE persistent cooperative kernel (2T grid
                              barriers) instead of a CUDA graph of 2T kernels (opt-in: measured slower
                              for cfg2 on B200) */

@@ -32,6 +32,7 @@ ESDP_FORCE_BRUTE = 4
 ESDP_PDL = 8
 ESDP_NO_DMMA = 16
 ESDP_PERSIST = 32
+ESDP_DMMA_L2 = 64
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 

@@ -96,6 +96,7 @@ struct esdp_ctx {
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   int prof_stride = 1;
   bool pdl = true;
+  int dmma2 = 0;   // shared-memory-staged DMMA expectation (set when its tile fits)
   bool solved = false;
   std::string err;
 };
@@ -343,6 +344,11 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   if (rows == 0) return cudaSuccess;
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
+    if (c->dmma2) {
+      const int ncb = (S + kDC * 16 - 1) / (kDC * 16), nrb = (rows + kDR * 8 - 1) / (kDR * 8);
+      return launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, pdl, Pt,
+                    (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
+    }
     const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
     return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
                   (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, nct);
@@ -680,6 +686,10 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     }
   }
   if (contract_smem_bytes(K) > 227 * 1024) { fail(c, ESDP_E_CONFIG, "K too large for the contraction tile"); return bail(ESDP_E_CONFIG); }
+  c->dmma2 = !(c->flags & ESDP_DMMA_L2) && contract_dmma2_smem(K) <= 200 * 1024;
+  if (c->dmma2 && contract_dmma2_smem(K) > 48 * 1024 &&
+      cudaFuncSetAttribute(contract_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K)) != cudaSuccess)
+    c->dmma2 = 0;
   if (contract_smem_bytes(K) > 48 * 1024)
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)

@@ -220,6 +220,86 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
   dmma_tile(Pt, Vn, Wt, rows, K, S, ld, ncol_tiles, blockIdx.x * kDmmaWarps + (threadIdx.x >> 5), threadIdx.x & 31);
 }
 
+// Shared-memory-staged DMMA expectation: a block computes kDR*8 rows x kDC*16 columns of W.  The P rows
+// [kDR*8][Kp] and the V tile [Kp][kDC*16] are staged once per block with cp.async (so every L2 byte is
+// read by one block, not by every warp), then each warp runs its 8x16 tile's DMMA chain from shared
+// memory.  cfg2: 7 x 21 = 147 blocks of 6 warps (one per SM).
+constexpr int kDR = 2, kDC = 3;
+constexpr int kD2Threads = kDR * kDC * 32;
+
+inline size_t contract_dmma2_smem(int K) {
+  const int Kp = (K + 3) & ~3;
+  return sizeof(double) * (size_t)Kp * (kDR * 8 + kDC * 16);
+}
+
+__global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
+                                                                   const double* __restrict__ Vn,   // [K][ld]
+                                                                   double* __restrict__ Wt,         // [rows][ld]
+                                                                   int rows, int K, int S, int ld, int ncb) {
+  extern __shared__ __align__(16) double dsm[];
+  const int Kp = (K + 3) & ~3;
+  constexpr int RB = kDR * 8, CB = kDC * 16;
+  double* as = dsm;                     // [RB][Kp]
+  double* bs = dsm + (size_t)RB * Kp;   // [Kp][CB]
+  const int r0 = (blockIdx.x / ncb) * RB, i0 = (blockIdx.x % ncb) * CB;
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  // P rows (an input), staged before the dependency wait: 16-byte cp.async when K is even (rows then
+  // start 16-byte aligned), else 8-byte
+  if ((K & 1) == 0) {
+    const int hp = Kp >> 1;
+    for (int e = tid; e < RB * hp; e += kD2Threads) {
+      const int r = e / hp, kp = 2 * (e - r * hp);
+      double* dst = as + r * Kp + kp;
+      if (r0 + r < rows && kp < K) cp_async16(dst, Pt + (size_t)(r0 + r) * K + kp);
+      else { dst[0] = 0.0; dst[1] = 0.0; }
+    }
+  } else {
+    for (int r = 0; r < RB; ++r) {
+      const bool rin = r0 + r < rows;
+      const double* src = Pt + (size_t)(r0 + r) * K;
+      for (int kp = tid; kp < Kp; kp += kD2Threads) {
+        if (rin && kp < K) cp_async8(as + r * Kp + kp, src + kp);
+        else as[r * Kp + kp] = 0.0;
+      }
+    }
+  }
+  pdl_wait();
+  {  // V tile: CB/2 two-double chunks per row
+    constexpr int CH = CB / 2;
+    for (int e = tid; e < Kp * CH; e += kD2Threads) {
+      const int kp = e / CH, c = 2 * (e - kp * CH);
+      double* dst = bs + kp * CB + c;
+      if (kp < K && i0 + c < ld) cp_async16(dst, Vn + (size_t)kp * ld + i0 + c);
+      else { dst[0] = 0.0; dst[1] = 0.0; }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
+  const int wr = warp / kDC, wc = warp % kDC;           // this warp's 8x16 tile inside the block
+  const double* arow = as + (size_t)(wr * 8 + g) * Kp + kq;
+  const double* bcol = bs + (size_t)kq * CB + wc * 16 + g;
+  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+  const int nq = Kp >> 2;
+#pragma unroll 4
+  for (int q = 0; q < nq; ++q) {
+    const double a = arow[4 * q];
+    const double b0 = bcol[(size_t)(4 * q) * CB], b1 = bcol[(size_t)(4 * q) * CB + 8];
+    dmma_8x8x4(d00, d01, a, b0);
+    dmma_8x8x4(d10, d11, a, b1);
+  }
+  const int r = r0 + wr * 8 + g;
+  if (r < rows) {
+    const int c = i0 + wc * 16 + 2 * kq;
+    double* wrp = Wt + (size_t)r * ld;
+    if (c < S) wrp[c] = d00;
+    if (c + 1 < S) wrp[c + 1] = d01;
+    if (c + 8 < S) wrp[c + 8] = d10;
+    if (c + 9 < S) wrp[c + 9] = d11;
+  }
+}
+
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
 __device__ __forceinline__ void gemv_cols(const double* __restrict__ pi, const double* __restrict__ Vn,
                                           double* __restrict__ Wt, int K, int S, int ld, int i) {

@@ -20,12 +20,21 @@ def bw_time(s, n=10):
     return (time.perf_counter() - t0) / n * 1e3
 
 
-for keep in (True, False):
-    for brute in (False, True):
-        for pdl, dmma in ((False, True), (False, False), (True, True)):
-            s = E.Solver(inst, keep_values=keep, force_brute=brute, pdl=pdl, dmma=dmma)
+for keep in (True,):
+    for brute in (False,):
+        for pdl, dmma in ((False, True), (False, "l2"), (False, False)):
+            if dmma == "l2":
+                import types
+                s = E.Solver.__new__(E.Solver)
+                s.ctx = E.esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
+                                      inst.lam, inst.P, inst.pi, None, 0, None,
+                                      (E.ESDP_KEEP_VALUES if keep else 0) | (E.ESDP_FORCE_BRUTE if brute else 0) | E.ESDP_DMMA_L2)
+                s.T, s.S, s.A, s.K = E.esdp_dims(s.ctx)
+                s.stencil_kind = E.esdp_stencil_kind(s.ctx)
+            else:
+                s = E.Solver(inst, keep_values=keep, force_brute=brute, pdl=pdl, dmma=dmma)
             ms = bw_time(s)
-            line = f"keep={int(keep)} stencil={'brute ' if not s.stencil_kind else 'window'} pdl={int(pdl)} dmma={int(dmma)}: backward {ms:.3f} ms ({ms / inst.T * 1e3:.2f} us/stage)"
+            line = f"keep={int(keep)} stencil={'brute ' if not s.stencil_kind else 'window'} pdl={int(pdl)} dmma={dmma}: backward {ms:.3f} ms ({ms / inst.T * 1e3:.2f} us/stage)"
             if keep and not pdl:
                 line += "  | warm us/launch: contract %.2f stencil %.2f objective %.2f" % (
                     E.esdp_debug_time(s.ctx, 0), E.esdp_debug_time(s.ctx, 1), E.esdp_debug_time(s.ctx, 3))

@@ -102,9 +102,13 @@ def _instance(args, rank):
         inst = workloads.cfg2(rank1=True)
     elif args.config == "cfg1":
         inst = workloads.cfg1("b")
+    elif args.config == "cfg4":
+        inst = workloads.cfg4()
+    elif args.config == "table1":
+        inst = workloads.table1_deterministic(0.01)
     else:
         raise SystemExit(f"unknown config {args.config}")
-    if rank:
+    if rank and args.config.startswith("cfg2"):
         # independent instance per rank (weak scaling): a different seeded jitter of the prices
         lam, _, _ = workloads.price_chain(inst.T, inst.K, 5.0 / 60.0, seed=workloads.SEED_BASE + 1000 + rank)
         inst.lam = lam
@@ -115,6 +119,8 @@ WORKLOAD = {
     "cfg2": "cfg2: ISO-NE-shaped 5-min RT day, Markov prices (T=288, S=1001, A=201, K=100, eta_c=eta_d=0.95)",
     "cfg2-rank1": "cfg2 with stagewise-independent prices (the paper's Alg. 1 case)",
     "cfg1": "cfg1b: T=24, S=101, A=21, K=5",
+    "cfg4": "cfg4: full-year hourly horizon, per-stage P_t (T=8760, S=2001, A=401, K=200)",
+    "table1": "NEXT-3 Table-1 analog: deterministic (K=1) hourly year, T=8784, S=401, A=203 (delta=0.01)",
 }
 
 
@@ -318,6 +324,77 @@ def run_ours(args):
     return out
 
 
+def run_sweep(args):
+    """cfg5: a batch of storage configurations (different pbar, eta -> different action grids) solved
+    concurrently, one context per instance on its own CUDA stream; each instance = backward + 1024
+    simulated paths.  Latency-bound single instances overlap, so the GPU fills up."""
+    import numpy as np
+    import torch
+    import workloads
+    import paper_2511_15629_b200 as E
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.instances
+    idx = [rank * n + j for j in range(n)]     # instance sharding across ranks (no communication)
+    insts = workloads.cfg5_instances(idx)
+    solvers = [E.Solver(x, keep_values=False) for x in insts]
+    streams = [torch.cuda.Stream(device=dev) for _ in solvers]
+    master = torch.cuda.Stream(device=dev)
+    paths = 1024
+    outs = [torch.empty(paths, dtype=torch.float64, device=dev) for _ in solvers]
+    cells = sum(s.T * s.S * s.K * s.A for s in solvers)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(j):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(master)
+        ends = []
+        for s, st, o in zip(solvers, streams, outs):
+            st.wait_event(e0)
+            E.esdp_backward_async(s.ctx, st.cuda_stream)
+            E.esdp_simulate_dev(s.ctx, paths, 17 + j, o.data_ptr(), st.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            ends.append(ev)
+        for ev in ends:
+            master.wait_event(ev)
+        e1.record(master)
+        return e0, e1
+
+    for j in range(args.warmup):
+        step(j)
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = 0.0
+    for j in range(args.steps):
+        with torch.cuda.stream(master):
+            flush.fill_(float(j))
+        e0, e1 = step(j)
+        master.synchronize()
+        ms += e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ms /= args.steps
+    As = [s.A for s in solvers]
+    out = {"metric": "DP cell-updates/sec (T*S*K*A)", "value": cells / (ms * 1e-3), "unit": "cell-updates/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (cfg2 price chain; cfg5 storage sweep)",
+           "config": {"workload": "cfg5 sweep sample: %d storage configurations per GPU solved concurrently "
+                                  "(pbar/delta in [10.42, 99], eta in [0.80, 0.99]; T=288, S=1001, K=100; A=%d..%d), "
+                                  "1024 simulated paths each" % (n, min(As), max(As)),
+                      "instances_per_gpu": n, "l2": "flushed between timed steps"},
+           "gpu_launches": sum(E.esdp_launch_count(s.ctx) + 1 for s in solvers) * args.steps,
+           "clocks": clk}
+    for s in solvers:
+        s.close()
+    return out if rank == 0 else None
+
+
 def cpu_baseline(inst, budget_s=20.0, n_stages=None):
     """The FP64 oracle as it stands, on this host's cores, on a bounded sample of the same workload:
     the last n stages of the backward pass (t = T .. T-n+1, every (k, i) row)."""
@@ -381,7 +458,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOAD))
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOAD) + ["cfg5"])
+    ap.add_argument("--instances", type=int, default=16, help="cfg5: storage configurations per GPU")
     ap.add_argument("--paths", type=int, default=65536)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-stages", type=int, default=24)
@@ -395,7 +473,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif args.config == "cfg5":
+        out = run_sweep(args)
+    else:
+        out = run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)
 

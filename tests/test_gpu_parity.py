@@ -171,6 +171,14 @@ def test_cfg2_rank1_full_size():
     _compare_all(workloads.cfg2(rank1=True), nthreads=16, expect_window=True)
 
 
+@pytest.mark.parametrize("delta", [0.1, 0.01])
+def test_table1_deterministic_year(delta):
+    """NEXT-3 (Table 1 analog): K = 1, T = 8784 hourly stages, the paper's 4-h battery at
+    delta = 0.10 (S=41, A=22) and 0.01 (S=401, A=203); every stage bit-identical to the oracle."""
+    inst = workloads.table1_deterministic(delta)
+    _compare_all(inst, nthreads=16)
+
+
 def test_cfg4_slice():
     """BASELINE configs[3] per-stage shape (S=2001, A=401, K=200, a distinct P_t per stage) on a
     6-stage horizon, compared in full."""

@@ -251,3 +251,22 @@ def test_policy_is_smallest_exact_argmax(seed):
                 m = max(c for c, _ in cands)
                 first = min(a for c, a in cands if c == m)
                 assert sol.pol[t - 1, k, i] == first, (t, k, i)
+
+
+def test_table1_year_trend():
+    """NEXT-3 / Table 1: deterministic hourly year (T = 8784), 4-h battery, eta = sqrt(0.85):
+    the DP is a restriction of the LP (DP <= LP), the gap shrinks as delta is refined through
+    0.10 / 0.05 / 0.02 / 0.01 (A = 22 / 42 / 103 / 203), and is a small fraction of a percent at 0.01
+    (paper: -0.19 / -0.13 / -0.04 / -0.02 %)."""
+    inst = workloads.table1_deterministic(0.1)
+    lp, _ = pins.lp_value(inst.lam[:, 0], 1.0, 4.0, 0.0, inst.eta_c, inst.eta_d)
+    gaps = []
+    for d, A in [(0.1, 22), (0.05, 42), (0.02, 103), (0.01, 203)]:
+        inst = workloads.table1_deterministic(d)
+        pr = to_oracle(inst)
+        assert oracle.dims(pr)[1] == A
+        J = _solve(pr, nthreads=8).J
+        assert J <= lp + 1e-6
+        gaps.append((lp - J) / lp)
+    assert gaps[0] > gaps[1] > gaps[2] > gaps[3] > 0.0
+    assert gaps[0] < 0.005 and gaps[3] < 0.001

@@ -178,6 +178,20 @@ def cfg3_gpu(actions: np.ndarray, T: int = 288, K: int = 100, rank1: bool = Fals
                     1.0, lam, base.P, base.pi, None, PAYOFF_LINEAR_MINUS_G, degradation_g(actions))
 
 
+def table1_deterministic(delta: float = 0.01, T: int = 8784, seed: int = SEED_BASE + 6) -> Instance:
+    """NEXT-3: Table 1 analog: deterministic prices (K = 1), a 4-hour battery with pbar = 1,
+    eta = sqrt(0.85), one year of hourly stages; delta in {0.10, 0.05, 0.02, 0.01} gives
+    A = 22 / 42 / 103 / 203 and S = 41 / 81 / 201 / 401 (Table 1 / Table 3 sizes)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    h = np.arange(T) % 24
+    day = np.arange(T) // 24
+    lam = da_shape(h.astype(np.float64)) * (1.0 + 0.25 * np.cos(2 * np.pi * (day - 15.0) / 365.0))
+    lam = lam + rng.laplace(0.0, 6.0, size=T)
+    eta = math.sqrt(0.85)
+    return Instance(f"table1-delta{delta}", T, 1, 1.0, 4.0, 0.0, eta, eta, delta,
+                    np.ascontiguousarray(lam.reshape(T, 1)), np.ones((T - 1, 1, 1)), np.ones(1))
+
+
 def cfg4(T: int = 8760, K: int = 200) -> Instance:
     """Full-year hourly horizon: T=8760, S=2001, A=401, K=200, per-stage P_t (pbar/delta = 199)."""
     lam, P, pi1 = price_chain(T, K, 1.0, per_stage_rho=True, seed=SEED_BASE + 4, season=True)
@@ -191,6 +205,19 @@ def cfg5_sweep(n: int = 1024):
     etas = np.linspace(0.80, 0.99, 32)
     for j in range(n):
         out.append(dict(pbar=float(np.round(ratios[j // 32 % 32], 6)), eta=float(etas[j % 32])))
+    return out
+
+
+def cfg5_instances(idx, T: int = 288, K: int = 100):
+    """Instances idx of the cfg5 sweep: cfg2's price chain (shared lambda, P), pbar/delta in [10.42, 99]
+    (8 h down to 0.84 h at 5-min stages), eta_c = eta_d in [0.80, 0.99]; sbar/delta = 1000."""
+    sweep = cfg5_sweep()
+    base = cfg2(T=T, K=K)
+    out = []
+    for j in idx:
+        c = sweep[j % len(sweep)]
+        out.append(Instance(f"cfg5[{j}]", T, K, c["pbar"], 1000.0, 500.0, c["eta"], c["eta"], 1.0, base.lam, base.P,
+                            base.pi, meta=dict(sweep_index=j)))
     return out
 
 

@@ -462,6 +462,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   };
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   bool forked = false;
+  std::vector<char> side_used(c->side.size(), 0);
   for (int t = T; t >= 1; --t) {
     if (t == T) {
       CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, t), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
@@ -482,6 +483,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
       const int64_t lo = c->fb_off[t], cnt = c->fb_off[t_hi + 1] - lo;
       if (cnt > 0) {
         cudaStream_t sb = c->side[bt % c->side.size()];
+        side_used[bt % c->side.size()] = 1;
         CUDA_OR_FAIL(c, cudaEventRecord(c->fb_ev[t - 1], s));
         CUDA_OR_FAIL(c, cudaStreamWaitEvent(sb, c->fb_ev[t - 1], 0));
         CUDA_OR_FAIL(c, launch_bids(c, cnt, c->d_fb_req + 3 * lo, c->d_fb_slot + lo, c->fb_n, c->fb_cap, c->fb_nvert,
@@ -511,6 +513,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   ++n;
   if (forked) {   // join the bid-curve branches
     for (size_t j = 0; j < c->side.size(); ++j) {
+      if (!side_used[j]) continue;   // only streams that joined the capture
       CUDA_OR_FAIL(c, cudaEventRecord(c->join_ev[j], c->side[j]));
       CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->join_ev[j], 0));
     }

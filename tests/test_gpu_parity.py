@@ -247,6 +247,10 @@ def test_fused_bidcurves_in_backward(name):
                 assert np.array_equal(ph[:m - 1, j], c["price"])
         E.esdp_set_bid_requests(s.ctx, np.zeros((0, 3), np.int32), cap, None, None, None, None)
         assert s.backward() == ref.J
+        # requests on a few stages only (some side streams unused)
+        few = req[np.isin(req[:, 0], [1, inst.T])]
+        E.esdp_set_bid_requests(s.ctx, few, cap, nv.data_ptr(), vert.data_ptr(), q.data_ptr(), price.data_ptr())
+        assert s.backward() == ref.J
 
 
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1"])

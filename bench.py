@@ -299,7 +299,7 @@ def run_ours(args):
                             "bidcurves": None if fused else part[1], "simulate": part[2]},
             "backward_phase_ms": {"expectation": phases[0], "stencil": phases[1]} if args.kernel_events else None,
             "roofline": {"bound": "alu",
-                         "kernel": "backward (%s)" % ("persistent cooperative kernel" if plan & 2 else "graph of 2T kernels"),
+                         "kernel": "backward (%s)" % ("persistent dataflow kernel" if plan & 2 else "graph of 2T kernels"),
                          "achieved": achieved, "peak": fp64_peak, "unit": "G FP64 instr/s",
                          "frac": achieved / fp64_peak, "traffic": None,
                          "peak_note": f"{n_sm} SMs x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz "

@@ -65,8 +65,9 @@ enum {
   ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
   ESDP_DMMA_L2 = 64u,     /* DMMA expectation with operands read straight from L2 by every warp
                              (instead of staged once per block in shared memory) */
-  ESDP_PERSIST = 32u      /* run the backward pass as ONE persistent cooperative kernel (2T grid
-                             barriers) instead of a CUDA graph of 2T kernels (opt-in: measured slower
+  ESDP_PERSIST = 32u      /* single GPU: run the backward pass as ONE persistent dataflow kernel (a
+                             device-side ready queue of per-tile stencil / expectation tasks, no grid
+                             barrier) instead of a CUDA graph of 2T kernels (opt-in: measured slower
                              for cfg2 on B200) */
 };
 
@@ -175,7 +176,7 @@ esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, dou
                               void* stream);
 
 /* Execution plan: bit 0 = stencil (1 = exact sliding-window for the recombining grid with a linear
- * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent cooperative
+ * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent dataflow
  * kernel (else a CUDA graph of 2T kernels).  All plans give bit-identical results. */
 esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
 
@@ -189,7 +190,7 @@ esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
 /* Average device time (ms) of one expectation phase and of one stencil phase in the last completed
  * backward pass (requires ESDP_PROFILE; the caller has synchronized the stream).  Graph plan: CUDA
  * events recorded inside the graph around the kernels of ~16 evenly spaced stages.  Persistent plan:
- * the device timer at every phase boundary of every stage (grid barrier included in each phase). */
+ * contract_ms = 0 and stencil_ms = the whole dataflow kernel's time / T. */
 esdp_status esdp_kernel_times(const esdp_ctx* ctx, double* contract_ms, double* stencil_ms);
 
 /* Diagnostic micro-timing (not part of the solve): warm back-to-back launches of one kernel of stage

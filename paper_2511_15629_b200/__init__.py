@@ -277,7 +277,7 @@ def esdp_kernel_times(ctx):
 
 
 def esdp_stencil_kind(ctx) -> int:
-    """bit 0: 1 = exact sliding-window stencil, 0 = brute force; bit 1: persistent cooperative kernel."""
+    """bit 0: 1 = exact sliding-window stencil, 0 = brute force; bit 1: persistent dataflow kernel."""
     k = ctypes.c_int32()
     _check(lib.esdp_stencil_kind(ctx, ctypes.byref(k)), "esdp_stencil_kind", ctx)
     return k.value

@@ -78,10 +78,14 @@ struct esdp_ctx {
   cudaGraphExec_t graph = nullptr;
   size_t stencil_smem = 0;
   int64_t launches = 0;
-  // persistent cooperative backward (persistent.cuh): one launch per backward
+  // persistent dataflow backward (persistent.cuh): one launch per backward
   int persist = 0, persist_grid = 0;
   size_t persist_smem = 0;
-  unsigned long long* d_stamps = nullptr;
+  int df_ntc = 0, df_ecw = 0, df_ncb = 0, df_nrg = 0, df_period = 0, df_ntasks = 0, df_n0 = 0;
+  size_t df_init_off = 0;
+  int *d_df_tab = nullptr;   // schedule tables (build_schedule)
+  int *d_df_cnt = nullptr;   // ready queue and dependency counters (reset per launch)
+  size_t df_cnt_n = 0;
   // bid-curve requests extracted inside the backward graph (esdp_set_bid_requests)
   int64_t fb_n = 0;
   int32_t fb_cap = 0;
@@ -274,7 +278,7 @@ void free_all(esdp_ctx* c) {
   for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_stamps, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -417,15 +421,91 @@ PersistParams persist_params(esdp_ctx* c) {
   pp.P = c->d_P; pp.pi = c->d_pi; pp.lambda = c->d_lambda; pp.g = c->d_g;
   pp.V = c->d_V; pp.W = c->d_W; pp.pol = c->d_pol; pp.J = c->d_J;
   pp.f0 = c->f0; pp.on_grid = c->on_grid; pp.w0 = c->w0;
-  pp.stamps = c->d_stamps;
+  pp.Kp = c->Kp;
+  pp.ntc = c->df_ntc; pp.ecw = c->df_ecw; pp.ncb = c->df_ncb; pp.nrg = c->df_nrg; pp.period = c->df_period;
+  pp.ntasks = c->df_ntasks;
+  pp.pat = c->d_df_tab;
+  pp.pos_s = pp.pat + c->df_period;
+  pp.pos_e = pp.pos_s + (size_t)c->K * c->df_ntc;
+  pp.e_need = pp.pos_e + (size_t)c->df_nrg * c->df_ncb;
+  pp.e_dep = pp.e_need + c->df_ntc;
+  pp.e_feed = pp.e_dep + 2 * c->df_ncb;
+  pp.c_feeds = pp.e_feed + 2 * c->df_ncb;
+  pp.ctl = c->d_df_cnt;
+  pp.queue = pp.ctl + 4;
+  pp.s_done = pp.queue + c->df_ntasks;
+  pp.e_cnt = pp.s_done + (size_t)c->T * c->df_ntc;
+  pp.e_ready = pp.e_cnt + (size_t)c->T * c->df_nrg * c->df_ntc;
   return pp;
 }
 
 cudaError_t launch_persistent(esdp_ctx* c, cudaStream_t s) {
   PersistParams pp = persist_params(c);
-  void* args[] = {&pp};
-  return cudaLaunchCooperativeKernel((void*)backward_persistent_kernel, dim3(c->persist_grid), dim3(kPersistThreads), args,
-                                     c->persist_smem, s);
+  cudaError_t e = cudaMemsetAsync(c->d_df_cnt, 0, c->df_cnt_n * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(c->d_df_cnt, c->d_df_tab + c->df_init_off, (4 + (size_t)c->df_n0) * sizeof(int),
+                      cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  backward_persistent_kernel<<<c->persist_grid, kPersistThreads, c->persist_smem, s>>>(pp);
+  return cudaGetLastError();
+}
+
+// Task schedule of the dataflow kernel (persistent.cuh): dependency ranges and one stage's ticket
+// pattern -- the S tasks of tile c (all rows), then every not yet issued E task of the next stage whose
+// input tiles are all issued by then.  Returns the host tables laid out as d_df_tab expects.
+std::vector<int> build_schedule(esdp_ctx* c) {
+  const int S = c->S, K = c->K;
+  const int ntc = (S + kWinTile - 1) / kWinTile;
+  const int ecw = c->rank1 ? kPersistThreads : kDfCols;
+  const int ncb = (S + ecw - 1) / ecw;
+  const int nrg = c->rank1 ? 1 : (K + kDfRows - 1) / kDfRows;
+  std::vector<int> need(ntc, 0), dep(2 * ncb), feed(2 * ncb);
+  for (int cb = 0; cb < ncb; ++cb) {
+    const int x0 = cb * ecw, x1 = std::min(S, x0 + ecw) - 1;    // columns of the block
+    int flo = ntc, fhi = -1;                                      // tiles whose W reads cover them
+    for (int tc = 0; tc < ntc; ++tc) {
+      const int r0 = std::max(0, tc * kWinTile + c->o_min - 1);
+      const int r1 = std::min(S - 1, tc * kWinTile + kWinTile + c->o_max + 1);
+      if (r0 <= x1 && x0 <= r1) { flo = std::min(flo, tc); fhi = tc; ++need[tc]; }
+    }
+    feed[2 * cb] = flo; feed[2 * cb + 1] = fhi;
+    int dlo = x0 / kWinTile, dhi = x1 / kWinTile;                // V_{t+1} tiles it reads
+    if (!keep(c)) { dlo = std::min(dlo, flo); dhi = std::max(dhi, fhi); }   // one W buffer: wait for its readers
+    dep[2 * cb] = dlo; dep[2 * cb + 1] = dhi;
+  }
+  std::vector<int> pat, pos_s((size_t)K * ntc), pos_e((size_t)nrg * ncb), cfeeds(2 * ntc);
+  std::vector<char> issued(ncb, 0);
+  for (int tc = 0; tc < ntc; ++tc) {
+    for (int k = 0; k < K; ++k) { pos_s[(size_t)k * ntc + tc] = (int)pat.size(); pat.push_back(kTaskS | (k << 1) | (tc << 16)); }
+    for (int cb = 0; cb < ncb; ++cb)
+      if (!issued[cb] && dep[2 * cb + 1] <= tc) {
+        issued[cb] = 1;
+        for (int rg = 0; rg < nrg; ++rg) { pos_e[(size_t)rg * ncb + cb] = (int)pat.size(); pat.push_back(kTaskE | (rg << 1) | (cb << 16)); }
+      }
+    int lo = ncb, hi = -1;   // E blocks whose input tiles include tc (a contiguous range: dep is monotone)
+    for (int cb = 0; cb < ncb; ++cb)
+      if (dep[2 * cb] <= tc && tc <= dep[2 * cb + 1]) { lo = std::min(lo, cb); hi = cb; }
+    cfeeds[2 * tc] = lo; cfeeds[2 * tc + 1] = hi;
+  }
+  const int period = (int)pat.size();
+  c->df_ntc = ntc; c->df_ecw = ecw; c->df_ncb = ncb; c->df_nrg = nrg; c->df_period = period;
+  c->df_ntasks = c->T * K * ntc + (c->T - 1) * nrg * ncb + 1;
+  c->df_n0 = K * ntc;                                           // the S tasks of stage T: ready at launch
+  // counter block: ctl[4] | queue[ntasks] | s_done[T][ntc] | e_cnt[T][nrg][ntc] | e_ready[T][ncb]
+  c->df_cnt_n = 4 + (size_t)c->df_ntasks + (size_t)c->T * ntc + (size_t)c->T * nrg * ntc + (size_t)c->T * ncb;
+  // host tables: pattern | pos_s | pos_e | e_need | e_dep | e_feed | c_feeds | init (ctl + first queue slots)
+  std::vector<int> tab = pat;
+  tab.insert(tab.end(), pos_s.begin(), pos_s.end());
+  tab.insert(tab.end(), pos_e.begin(), pos_e.end());
+  tab.insert(tab.end(), need.begin(), need.end());
+  tab.insert(tab.end(), dep.begin(), dep.end());
+  tab.insert(tab.end(), feed.begin(), feed.end());
+  tab.insert(tab.end(), cfeeds.begin(), cfeeds.end());
+  c->df_init_off = tab.size();
+  tab.push_back(0); tab.push_back(c->df_n0); tab.push_back(0); tab.push_back(0);   // head, tail, stage-1 tiles
+  for (int tc = 0; tc < ntc; ++tc)
+    for (int k = 0; k < K; ++k) tab.push_back(pos_s[(size_t)k * ntc + tc] + 1);   // period 0 = stage T
+  return tab;
 }
 
 cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const int32_t* slot_dev, int64_t nout, int32_t cap,
@@ -460,6 +540,20 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   auto mark = [&](int t, int j) {
     return sampled(t) ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
   };
+  if (c->persist) {   // one dataflow kernel; bid curves (if any) after it, on the same stream
+    CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, T), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
+    if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[0], s, cudaEventRecordExternal));
+    CUDA_OR_FAIL(c, launch_persistent(c, s));
+    if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[1], s, cudaEventRecordExternal));
+    ++n;
+    if (c->fb_n > 0) {
+      CUDA_OR_FAIL(c, launch_bids(c, c->fb_n, c->d_fb_req, c->d_fb_slot, c->fb_n, c->fb_cap, c->fb_nvert, c->fb_vert,
+                                  c->fb_q, c->fb_price, s));
+      ++n;
+    }
+    c->launches = n;
+    return ESDP_OK;
+  }
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   bool forked = false;
   std::vector<char> side_used(c->side.size(), 0);
@@ -697,18 +791,25 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
-  // persistent path: needs cooperative launch and >= 1 resident 256-thread CTA per SM
-  if ((c->flags & ESDP_PERSIST) && !nccl_id && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
-    int dev = 0, coop = 0, nsm = 0, per_sm = 0;
+  // persistent dataflow path (single GPU; Markov uses the DMMA expectation; K < 2^15)
+  if ((c->flags & ESDP_PERSIST) && !nccl_id && K < 32768 && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
+    int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     size_t sm = std::max(c->use_window ? c->window_smem : c->stencil_smem, 2 * sizeof(double) * (size_t)K);
     sm = std::max(sm, c->stencil_smem);
-    if (coop && sm <= 200 * 1024 &&
+    if (!c->rank1) sm = std::max(sm, contract_dmma2_smem(K, kDfDC));
+    if (sm <= 200 * 1024 &&
         cudaFuncSetAttribute(backward_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_persistent_kernel, kPersistThreads, sm) == cudaSuccess &&
         per_sm >= 1) {
+      std::vector<int> tab = build_schedule(c);
+      TRY(dev_alloc(c, &c->d_df_tab, tab.size()));
+      TRY(dev_alloc(c, &c->d_df_cnt, c->df_cnt_n));
+      if (cudaMemcpy(c->d_df_tab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+        fail(c, ESDP_E_CUDA, "upload of the task schedule failed");
+        return bail(ESDP_E_CUDA);
+      }
       c->persist = 1;
       c->persist_grid = per_sm * nsm;
       c->persist_smem = sm;
@@ -716,7 +817,6 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     cudaGetLastError();
   }
   if (c->flags & ESDP_PROFILE) {
-    if (c->persist) TRY(dev_alloc(c, &c->d_stamps, (size_t)c->T * 3));
     c->prof_stride = std::max(1, c->T / 16);
     c->ev.resize((size_t)c->T * 4);
     for (auto& e : c->ev)
@@ -775,8 +875,7 @@ esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const 
 esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
   if (!c) return ESDP_E_STATE;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  if (c->persist) CUDA_OR_FAIL(c, launch_persistent(c, s));
-  else CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
+  CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
   c->solved = true;
   return ESDP_OK;
 }
@@ -843,7 +942,6 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
 esdp_status esdp_set_bid_requests(esdp_ctx* c, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert_dev,
                                   int16_t* vert_dev, double* q_dev, double* price_dev) {
   if (!c) return ESDP_E_STATE;
-  if (c->persist) return fail(c, ESDP_E_STATE, "fused bid curves need the graph plan");
   if (n > 0) {
     if (!keep(c)) return fail(c, ESDP_E_STATE, "fused bid curves need ESDP_KEEP_VALUES");
     if (c->kind == ESDP_PAYOFF_TABLE) return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
@@ -981,7 +1079,7 @@ esdp_status esdp_stencil_kind(const esdp_ctx* c, int32_t* kind) {
 
 esdp_status esdp_launch_count(const esdp_ctx* c, int64_t* n) {
   if (!c || !n) return ESDP_E_STATE;
-  *n = c->persist ? 1 : c->launches;
+  *n = c->launches;
   return ESDP_OK;
 }
 
@@ -990,16 +1088,11 @@ esdp_status esdp_kernel_times(const esdp_ctx* cc, double* contract_ms, double* s
   if (!c) return ESDP_E_STATE;
   if (c->ev.empty()) return fail(c, ESDP_E_STATE, "context was created without ESDP_PROFILE");
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
-  if (c->persist) {   // device timer stamps of block 0 at every phase boundary
-    std::vector<unsigned long long> st((size_t)c->T * 3);
-    CUDA_OR_FAIL(c, cudaMemcpy(st.data(), c->d_stamps, st.size() * 8, cudaMemcpyDeviceToHost));
-    double e_ns = 0.0, s_ns = 0.0;
-    for (int t = 1; t <= c->T; ++t) {
-      e_ns += (double)(st[(size_t)(t - 1) * 3 + 1] - st[(size_t)(t - 1) * 3 + 0]);
-      s_ns += (double)(st[(size_t)(t - 1) * 3 + 2] - st[(size_t)(t - 1) * 3 + 1]);
-    }
-    if (contract_ms) *contract_ms = e_ns / c->T * 1e-6;
-    if (stencil_ms) *stencil_ms = s_ns / c->T * 1e-6;
+  if (c->persist) {   // one kernel: its whole time per stage is reported as the stencil phase
+    float ms = 0.f;
+    CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    if (contract_ms) *contract_ms = 0.0;
+    if (stencil_ms) *stencil_ms = ms / c->T;
     return ESDP_OK;
   }
   double ct = 0.0, st = 0.0;
@@ -1071,3 +1164,10 @@ void esdp_destroy(esdp_ctx* c) {
 const char* esdp_last_error(const esdp_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
 
 }  // extern "C"
+
+#ifdef ESDP_DF_TRACE
+extern "C" int esdp_df_trace(unsigned long long* out, int n) {   // diagnostic build only
+  if (n > esdp::kTraceMax) n = esdp::kTraceMax;
+  return (int)cudaMemcpyFromSymbol(out, esdp::g_df_trace, (size_t)n * 32);
+}
+#endif

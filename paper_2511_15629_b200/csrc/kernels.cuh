@@ -227,23 +227,24 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
 constexpr int kDR = 2, kDC = 3;
 constexpr int kD2Threads = kDR * kDC * 32;
 
-inline size_t contract_dmma2_smem(int K) {
+inline size_t contract_dmma2_smem(int K, int DC = kDC) {
   const int Kp = (K + 3) & ~3;
-  return sizeof(double) * (size_t)Kp * (kDR * 8 + kDC * 16);
+  return sizeof(double) * (size_t)Kp * (kDR * 8 + DC * 16);
 }
 
-__global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
-                                                                   const double* __restrict__ Vn,   // [K][ld]
-                                                                   double* __restrict__ Wt,         // [rows][ld]
-                                                                   int rows, int K, int S, int ld, int ncb) {
-  extern __shared__ __align__(16) double dsm[];
+// One (kDR*8) x (DC*16) tile of W_t = P_t V_{t+1} by kDR*DC warps: P rows and the V column block are
+// staged in shared memory (cp.async), then every warp runs its 8x16 DMMA chain over k'.  kPdl: the P
+// staging (an input) happens before the programmatic dependency wait, the V staging after it.
+template <int DC, bool kPdl>
+__device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const double* __restrict__ Vn,
+                                           double* __restrict__ Wt, int rows, int K, int S, int ld, int r0, int i0,
+                                           double* dsm) {
+  constexpr int kD2Threads = kDR * DC * 32, kDC = DC;
   const int Kp = (K + 3) & ~3;
   constexpr int RB = kDR * 8, CB = kDC * 16;
   double* as = dsm;                     // [RB][Kp]
   double* bs = dsm + (size_t)RB * Kp;   // [Kp][CB]
-  const int r0 = (blockIdx.x / ncb) * RB, i0 = (blockIdx.x % ncb) * CB;
   const int tid = threadIdx.x;
-  pdl_trigger();
   // P rows (an input), staged before the dependency wait: 16-byte cp.async when K is even (rows then
   // start 16-byte aligned), else 8-byte
   if ((K & 1) == 0) {
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double
       }
     }
   }
-  pdl_wait();
+  if (kPdl) pdl_wait();
   {  // V tile: CB/2 two-double chunks per row
     constexpr int CH = CB / 2;
     for (int e = tid; e < Kp * CH; e += kD2Threads) {
@@ -298,6 +299,15 @@ __global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double
     if (c + 8 < S) wrp[c + 8] = d10;
     if (c + 9 < S) wrp[c + 9] = d11;
   }
+}
+
+__global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
+                                                                   const double* __restrict__ Vn,   // [K][ld]
+                                                                   double* __restrict__ Wt,         // [rows][ld]
+                                                                   int rows, int K, int S, int ld, int ncb) {
+  extern __shared__ __align__(16) double dsm[];
+  pdl_trigger();
+  dmma2_tile<kDC, true>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (kDR * 8), (blockIdx.x % ncb) * (kDC * 16), dsm);
 }
 
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.

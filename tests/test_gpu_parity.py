@@ -167,6 +167,28 @@ def test_cfg2_no_keep_values(persist):
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
+@pytest.mark.parametrize("rank1", [False, True])
+@pytest.mark.parametrize("seed", range(6))
+def test_dataflow_plan_no_keep_values(seed, rank1):
+    """Persistent dataflow kernel with one W buffer and ping-pong V (the write-after-read edges of the
+    task schedule): several column tiles, ragged tails, window and brute force; V_1, pol, J exact."""
+    inst = workloads.random_instance(500 + seed, T=7, K=3 + 7 * seed, S_max=1300, rank1=rank1)
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=8)
+    for brute in (False, True):
+        with E.Solver(inst, keep_values=False, force_brute=brute, persist=True) as s:
+            assert s.stencil_kind & 2
+            for _ in range(2):
+                assert s.backward() == ref.J
+            assert np.array_equal(E.esdp_values(s.ctx, 1, want_W=False), ref.V[0])
+            for t in range(1, inst.T + 1):
+                assert np.array_equal(s.policy(t), ref.pol[t - 1])
+
+
+def test_cfg2_rank1_full_size_persistent_plan():
+    _compare_all(workloads.cfg2(rank1=True), nthreads=16, persist=True, expect_window=True)
+
+
 def test_cfg2_rank1_full_size():
     _compare_all(workloads.cfg2(rank1=True), nthreads=16, expect_window=True)
 
@@ -210,8 +232,9 @@ def test_cfg3_nonconcave_payoff_and_bids():
         assert np.all(np.diff(out["price"][j, :n - 1]) >= 0)
 
 
+@pytest.mark.parametrize("persist", [False, True])
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg3"])
-def test_fused_bidcurves_in_backward(name):
+def test_fused_bidcurves_in_backward(name, persist):
     """esdp_set_bid_requests: curves extracted inside the backward graph (side branch per stage, unsorted
     requests over all stages) equal the oracle's bit for bit, on every backward pass."""
     import torch
@@ -225,7 +248,8 @@ def test_fused_bidcurves_in_backward(name):
     rng = np.random.default_rng(5)
     n = 3000
     req = np.stack([rng.integers(1, inst.T + 1, n), rng.integers(0, inst.S, n), rng.integers(0, inst.K, n)], 1)
-    with _gpu(inst) as s:
+    with _gpu(inst, persist=persist) as s:
+        assert bool(s.stencil_kind & 2) == persist
         cap = s.A
         nv = torch.zeros(n, dtype=torch.int32, device="cuda")
         vert = torch.zeros(cap * n, dtype=torch.int16, device="cuda")

@@ -30,7 +30,7 @@ typedef struct esdp_ctx esdp_ctx; /* opaque: owns device buffers, the CUDA graph
 
 typedef enum {
   ESDP_OK = 0,
-  ESDP_E_CONFIG = 1,   /* bad grid / parameters: T, K < 1; pbar, sbar, delta <= 0; eta not in (0,1];
+  ESDP_E_CONFIG = 1,   /* bad grid / parameters: T, K < 1; K > 32767; pbar, sbar, delta <= 0; eta not in (0,1];
                           s0 not in [0, sbar]; sbar/delta not integral (no silent rounding);
                           actions not strictly ascending, without an exact 0, |p| > pbar; A > 8191 */
   ESDP_E_DATA = 2,     /* non-finite lambda or g; a row of P (or pi) is not a probability simplex

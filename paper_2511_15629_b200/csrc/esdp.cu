@@ -668,6 +668,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (!pr || !out) return fail(nullptr, ESDP_E_CONFIG, "null argument");
   *out = nullptr;
   if (pr->T < 1 || pr->K < 1) return fail(nullptr, ESDP_E_CONFIG, "T and K must be >= 1");
+  if (pr->K > 32767) return fail(nullptr, ESDP_E_CONFIG, "K exceeds 32767 (16-bit sampler guide entries)");
   if (!(std::isfinite(pr->pbar) && pr->pbar > 0)) return fail(nullptr, ESDP_E_CONFIG, "pbar must be > 0");
   if (!(std::isfinite(pr->sbar) && pr->sbar > 0)) return fail(nullptr, ESDP_E_CONFIG, "sbar must be > 0");
   if (!(std::isfinite(pr->delta) && pr->delta > 0)) return fail(nullptr, ESDP_E_CONFIG, "delta must be > 0");
@@ -728,7 +729,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
   TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
   TRY(dev_alloc(c, &c->d_cdf1, K));
-  c->G = std::max<int>(16, (int)K);
+  c->G = std::max<int>(64, 4 * (int)K);   // guide buckets per cdf row (most of them pure: one load per draw)
   TRY(dev_alloc(c, &c->d_guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
   TRY(dev_alloc(c, &c->d_guide1, (size_t)c->G));
   TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));

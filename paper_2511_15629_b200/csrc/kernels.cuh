@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double
                                                                    double* __restrict__ Wt,         // [rows][ld]
                                                                    int rows, int K, int S, int ld, int ncb) {
   extern __shared__ __align__(16) double dsm[];
-  pdl_trigger();
   dmma2_tile<kDC, true>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (kDR * 8), (blockIdx.x % ncb) * (kDC * 16), dsm);
+  pdl_trigger();   // late trigger: dependents launch as this grid drains, without holding SM slots early
 }
 
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
@@ -454,9 +454,9 @@ __device__ __forceinline__ void stencil_item(const StencilParams& prm, int k, in
 
 __global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm) {
   extern __shared__ double smem[];
-  pdl_trigger();
   pdl_wait();                          // W_t is the previous contraction's output
   stencil_item(prm, blockIdx.y, blockIdx.x * kTile, smem);
+  pdl_trigger();
 }
 
 inline size_t stencil_smem_bytes(int A, int o_span) {
@@ -680,6 +680,8 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
 
 // cdf rows (DESIGN R17): running sum in ascending order, last entry forced to 1; plus a guide table
 // guide[b] = first j with b/G < cdf[j], so that a draw u in [b/G, (b+1)/G) starts its search there.
+// A bucket whose whole u range (widened by 2^-49 for the rounding of u*G and b/G) maps to one j is
+// "pure" and stores ~j (< 0): the sampler returns it without touching the cdf row.
 // One thread per row; bit-identical to the oracle's sequential cdf.
 __global__ void cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G, double* __restrict__ cdf,
                            int16_t* __restrict__ guide) {
@@ -699,16 +701,32 @@ __global__ void cdf_kernel(const double* __restrict__ q, int64_t rows, int K, in
     while (b < G && (double)b < __dmul_rn(c, (double)G)) { gr[b] = (int16_t)j; ++b; }
   }
   for (; b < G; ++b) gr[b] = (int16_t)(K - 1);
+  const double m = 0x1p-49;
+  for (b = 0; b < G; ++b) {
+    const int j = gr[b];
+    const double lo = __ddiv_rn((double)b, (double)G), hi = __ddiv_rn((double)(b + 1), (double)G);
+    const bool below = j == 0 || cr[j - 1] < __dsub_rn(lo, m);      // every u of the bucket >= cdf[j-1]
+    const bool above = j == K - 1 || cr[j] > __dadd_rn(hi, m);      // every u of the bucket <  cdf[j]
+    if (below && above) gr[b] = (int16_t)~j;
+  }
 }
 
-// first j in [0, K) with u < cdf[j]; the guide gives a start, the scans make it exact for any start.
+// first j in [0, K) with u < cdf[j]; pure buckets answer directly, otherwise the guide gives a start and
+// the scans make it exact for any start (both neighbours are loaded together).
 __device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const int16_t* __restrict__ guide, int K,
                                           int G, double u) {
   int b = (int)__dmul_rn(u, (double)G);
   b = b < G ? b : G - 1;
   int j = __ldg(guide + b);
-  while (j > 0 && u < __ldg(cdf + j - 1)) --j;
-  while (j < K - 1 && !(u < __ldg(cdf + j))) ++j;
+  if (j < 0) return ~j;
+  const double cl = j > 0 ? __ldg(cdf + j - 1) : -1.0, ch = __ldg(cdf + j);
+  if (u < cl) {
+    --j;
+    while (j > 0 && u < __ldg(cdf + j - 1)) --j;
+  } else if (!(u < ch)) {
+    ++j;
+    while (j < K - 1 && !(u < __ldg(cdf + j))) ++j;
+  }
   return j;
 }
 

@@ -269,9 +269,9 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
 
 __global__ void __launch_bounds__(kWinThreads, 4) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
-  pdl_trigger();
   pdl_wait();                          // W_t is the previous contraction's output
   window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
+  pdl_trigger();
 }
 
 }  // namespace esdp

@@ -22,7 +22,7 @@ def bw_time(s, n=10):
 
 for keep in (True,):
     for brute in (False,):
-        for pdl, dmma in ((False, True), (False, "l2"), (False, False)):
+        for pdl, dmma in ((False, True), (True, True), (False, "l2"), (False, False)):
             if dmma == "l2":
                 import types
                 s = E.Solver.__new__(E.Solver)
@@ -41,8 +41,8 @@ for keep in (True,):
             print(line, flush=True)
             s.close()
 
-for keep in (True, False):
-    for brute in (False, True):
+for keep in (True,):
+    for brute in (False,):
         s = E.Solver(inst, keep_values=keep, force_brute=brute, persist=True)
         assert s.stencil_kind & 2
         ms = bw_time(s)

@@ -106,6 +106,11 @@ def _instance(args, rank):
         inst = workloads.cfg4()
     elif args.config == "table1":
         inst = workloads.table1_deterministic(0.01)
+    elif args.config == "cfg3":
+        import paper_2511_15629_b200 as E
+        with E.Solver(workloads.cfg2(T=2, K=2)) as s:   # the Eq. 10 action grid of cfg2 (product's own)
+            act = s.actions()
+        inst = workloads.cfg3_gpu(act)
     else:
         raise SystemExit(f"unknown config {args.config}")
     if rank and args.config.startswith("cfg2"):
@@ -120,6 +125,7 @@ WORKLOAD = {
     "cfg2-rank1": "cfg2 with stagewise-independent prices (the paper's Alg. 1 case)",
     "cfg1": "cfg1b: T=24, S=101, A=21, K=5",
     "cfg4": "cfg4: full-year hourly horizon, per-stage P_t (T=8760, S=2001, A=401, K=200)",
+    "cfg3": "cfg3ii: cfg2 dimensions, prices shifted <= 0, non-concave payoff lambda p - 2|p| - 25 [p != 0]",
     "table1": "NEXT-3 Table-1 analog: deterministic (K=1) hourly year, T=8784, S=401, A=203 (delta=0.01)",
 }
 
@@ -149,7 +155,8 @@ def run_ours(args):
         if world > 1:
             dist.broadcast_object_list(nid, src=0)
         dist_arg = (world, rank, nid[0])
-    solver = E.Solver(inst, keep_values=True, profile=bool(args.kernel_events), dist=dist_arg)
+    solver = E.Solver(inst, keep_values=True, profile=bool(args.kernel_events), dist=dist_arg,
+                      force_brute=args.stencil == "brute", persist=args.plan == "persistent")
     T, S, A, K = solver.T, solver.S, solver.A, solver.K
     cells = T * S * K * A
     stream = torch.cuda.Stream(device=dev)
@@ -468,6 +475,10 @@ def main():
                     help="per-phase device timers inside the backward (persistent plan) / events (graph plan)")
     ap.add_argument("--bids", choices=["fused", "after"], default="fused",
                     help="bid curves as side branches of the backward graph (fused) or one kernel after it")
+    ap.add_argument("--stencil", choices=["auto", "brute"], default="auto",
+                    help="auto: exact sliding-window stencil where it applies; brute: every (i, a) cell")
+    ap.add_argument("--plan", choices=["graph", "persistent"], default="graph",
+                    help="backward as a CUDA graph of 2T kernels, or one persistent dataflow kernel (1 GPU)")
     ap.add_argument("--mode", choices=["instances", "kpart"], default="instances",
                     help="N>1: independent instances per rank (weak) or one K-partitioned instance (strong)")
     args = ap.parse_args()

@@ -61,6 +61,8 @@ struct esdp_ctx {
   double *d_act = nullptr, *d_w = nullptr, *d_omw = nullptr;
   int* d_off = nullptr;
   Seg* d_segs = nullptr;
+  double* d_gfit = nullptr;   // [6] affine fit of g on the window runs (window.cuh WinParams::gfit)
+  double gfit[6] = {0, 0, 0, 0, 0, 0};
   double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
   int16_t *d_guide = nullptr, *d_guide1 = nullptr;
   int G = 16;
@@ -175,7 +177,25 @@ esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, co
 }
 
 // Alg. 1 lines 2-5 reduced to per-action (offset, weight); DESIGN §5 "layout".
-void build_tables(esdp_ctx* c) {
+// Affine fit of g over the window runs (NEXT-1 for payoffs lambda p - g(p) that are affine on each side,
+// e.g. cfg3's linear degradation + fixed cycling cost): g(charge o) ~ gc0 + gc1 o, g(discharge |o|) ~
+// gd0 + gd1 |o|.  f = {gc0, gc1, gd0, gd1, max deviation (+ slack for its own rounding), max |g|}.
+// All zero for the linear payoff.
+void fit_g(const esdp_ctx* c, const double* g, double f[6]) {
+  for (int j = 0; j < 6; ++j) f[j] = 0.0;
+  if (c->kind != ESDP_PAYOFF_LINEAR_MINUS_G || !g || c->a_z < 0 || c->Lc < 2 || c->Ld < 2) return;
+  const int az = c->a_z, Lc = c->Lc, Ld = c->Ld;
+  const double gc1 = (g[az - Lc] - g[az - 1]) / (double)(Lc - 1), gc0 = g[az - 1] - gc1;
+  const double gd1 = (g[az + Ld] - g[az + 1]) / (double)(Ld - 1), gd0 = g[az + 1] - gd1;
+  double dev = 0.0, gmax = 0.0;
+  for (int o = 1; o <= Lc; ++o) dev = std::max(dev, std::fabs(g[az - o] - (gc0 + gc1 * o)));
+  for (int o = 1; o <= Ld; ++o) dev = std::max(dev, std::fabs(g[az + o] - (gd0 + gd1 * o)));
+  for (int b : c->live_list) gmax = std::max(gmax, std::fabs(g[b]));
+  const double slack = 8.0 * 0x1p-53 * (gmax + std::fabs(gc0) + std::fabs(gd0) + std::fabs(gc1) * Lc + std::fabs(gd1) * Ld);
+  f[0] = gc0; f[1] = gc1; f[2] = gd0; f[3] = gd1; f[4] = dev + slack; f[5] = gmax;
+}
+
+void build_tables(esdp_ctx* c, const double* g) {
   const int A = c->A;
   c->off.assign(A, 0);
   c->w.assign(A, 0.0);
@@ -222,7 +242,7 @@ void build_tables(esdp_ctx* c) {
   }
   // window plan: zero action, charge run o = 1..Lc at a_z-1.., discharge run o = -1..-Ld at a_z+1..,
   // with powers matching -o*delta/eta_c resp. -o*delta*eta_d to a few ulps (the eps bound of
-  // window.cuh assumes it).  Linear payoff only.
+  // window.cuh assumes it).  Linear payoff, or lambda p - g(p) with g affine on each run (fit_g).
   c->use_window = 0;
   c->live_list.clear();
   c->singles.clear();
@@ -231,7 +251,8 @@ void build_tables(esdp_ctx* c) {
   c->a_z = -1;
   for (int b = 0; b < A; ++b)
     if (c->act[b] == 0.0) c->a_z = b;
-  if (c->kind == ESDP_PAYOFF_LINEAR && c->a_z >= 0 && !(c->flags & ESDP_FORCE_BRUTE)) {
+  if ((c->kind == ESDP_PAYOFF_LINEAR || c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) && c->a_z >= 0 &&
+      !(c->flags & ESDP_FORCE_BRUTE)) {
     const double u8 = 8.0 * 0x1p-53;
     int Lc = 0, Ld = 0;
     for (int b = c->a_z - 1; b >= 0; --b) {
@@ -246,9 +267,12 @@ void build_tables(esdp_ctx* c) {
       if (!live(b) || c->w[b] != 0.0 || c->off[b] != o || std::fabs(c->act[b] - ideal) > u8 * std::fabs(ideal)) break;
       ++Ld;
     }
-    if (Lc >= 2 && Ld >= 2 && Lc <= 512 && Ld <= 512) {
+    c->Lc = Lc; c->Ld = Ld;
+    double f[6];
+    fit_g(c, g, f);
+    const bool affine = c->kind == ESDP_PAYOFF_LINEAR || f[4] <= 1e-9 * (1.0 + f[5]);
+    if (Lc >= 2 && Ld >= 2 && Lc <= 512 && Ld <= 512 && affine) {
       c->use_window = 1;
-      c->Lc = Lc; c->Ld = Ld;
       c->pc = 0; while ((2 << c->pc) <= Lc) ++c->pc;
       c->pd = 0; while ((2 << c->pd) <= Ld) ++c->pd;
       for (int b : c->live_list)
@@ -278,7 +302,7 @@ void free_all(esdp_ctx* c) {
   for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -304,8 +328,14 @@ esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const dou
   }
   if (pi) cdf_kernel<<<1, 32, 0, s>>>(c->d_pi, 1, c->K, c->G, c->d_cdf1, c->d_guide1);  // pi_1 (row 0 in rank-1)
   CUDA_OR_FAIL(c, cudaGetLastError());
-  if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G)
+  if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, s));
+    // a later g that is not affine on the runs only widens eps (more canonical fallbacks, same result)
+    if (c->use_window) {
+      fit_g(c, g, c->gfit);
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice, s));
+    }
+  }
   if (g && c->kind == ESDP_PAYOFF_TABLE)
     CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, s));
   CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
@@ -381,7 +411,8 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
     wp.o_min = c->o_min; wp.o_max = c->o_max;
     wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
     wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
-    wp.bspan = c->delta * (double)(c->S + (c->o_max - c->o_min) + 2) / std::min(c->eta_c, c->eta_d);
+    wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
+    wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
     return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
   }
   StencilParams prm;
@@ -414,7 +445,8 @@ PersistParams persist_params(esdp_ctx* c) {
   wp.o_min = c->o_min; wp.o_max = c->o_max;
   wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
   wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
-  wp.bspan = c->delta * (double)(c->S + (c->o_max - c->o_min) + 2) / std::min(c->eta_c, c->eta_d);
+  wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
+  wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
   pp.use_window = c->use_window;
   pp.T = c->T; pp.K = c->K; pp.S = c->S; pp.A = c->A; pp.ld = c->ld; pp.rows = (int)w_rows(c);
   pp.rank1 = c->rank1; pp.kind = c->kind; pp.keep = keep(c) ? 1 : 0;
@@ -514,16 +546,21 @@ cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const in
                (int)w_rows(c), c->k_lo, c->rank1 ? c->K : c->k_cnt};
   const int span = c->o_max - c->o_min;
   const unsigned blocks = (unsigned)((n + kBidThreads - 1) / kBidThreads);
-  size_t sm = bid_smem_bytes(c->A, span, true);
-  if (sm <= 200 * 1024) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    bidcurve_kernel<true><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev,
-                                                           vert_dev, q_dev, price_dev);
+  const bool g = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  auto go = [&](auto kern, size_t sm) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev, vert_dev, q_dev,
+                                         price_dev);
+  };
+  if (c->A <= 255) {
+    const size_t sm = bid_smem_bytes(c->A, span, true, 1);
+    if (g) go(bidcurve_kernel<true, uint8_t, true>, sm); else go(bidcurve_kernel<true, uint8_t, false>, sm);
+  } else if (bid_smem_bytes(c->A, span, true, 2) <= 200 * 1024) {
+    const size_t sm = bid_smem_bytes(c->A, span, true, 2);
+    if (g) go(bidcurve_kernel<true, int16_t, true>, sm); else go(bidcurve_kernel<true, int16_t, false>, sm);
   } else {
-    sm = bid_smem_bytes(c->A, span, false);
-    if (sm > 48 * 1024) cudaFuncSetAttribute(bidcurve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    bidcurve_kernel<false><<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev,
-                                                            vert_dev, q_dev, price_dev);
+    const size_t sm = bid_smem_bytes(c->A, span, false, 2);
+    if (g) go(bidcurve_kernel<false, int16_t, true>, sm); else go(bidcurve_kernel<false, int16_t, false>, sm);
   }
   return cudaGetLastError();
 }
@@ -714,7 +751,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     esdp_status st = validate_data(c, pr->lambda, pr->P, pr->pi, pr->g);
     if (st != ESDP_OK) { g_create_error = c->err; delete c; return st; }
   }
-  build_tables(c);
+  build_tables(c, pr->g);
 
   auto bail = [&](esdp_status st) { g_create_error = c->err; free_all(c); delete c; return st; };
 #define TRY(x) do { esdp_status st_ = (x); if (st_ != ESDP_OK) return bail(st_); } while (0)
@@ -767,6 +804,8 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     return bail(ESDP_E_CUDA);
   }
   if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
+  TRY(dev_alloc(c, &c->d_gfit, 6));
+  if (cudaMemcpy(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload g fit"); return bail(ESDP_E_CUDA); }
   TRY(upload(c, pr->lambda, pr->P, pr->pi, pr->g));
   c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
   if (c->use_window) {

@@ -522,38 +522,133 @@ __device__ __forceinline__ bool bid_point(const BidAct& ba, int S, int kind, con
 
 constexpr int kBidThreads = 128;
 
-inline size_t bid_smem_bytes(int A, int o_span, bool stack_in_smem) {
-  return (size_t)A * (4 * sizeof(double) + sizeof(int)) + sizeof(double) * (kBidThreads + o_span + 4) +
-         (stack_in_smem ? sizeof(int16_t) * (size_t)A * kBidThreads : 0) + 64;
+// stack entries: 8-bit action indices when A <= 255, else 16-bit
+inline size_t bid_smem_bytes(int A, int o_span, bool stack_in_smem, size_t idx_bytes) {
+  return (((size_t)A * (4 * sizeof(double) + sizeof(int)) + 15) & ~(size_t)15) + sizeof(double) * (kBidThreads + o_span + 4) +
+         (stack_in_smem ? idx_bytes * (size_t)A * kBidThreads : 0) + 64;
+}
+
+// Per-action tables of the bid-curve kernel (shared memory).
+struct BidTables {
+  const double* act; const double* w; const double* omw; const double* g;
+  const int* ow;          // 2 o_a + [w_a != 0]
+};
+
+// The monotone chain and the price emission of one curve (t, i, k): Wi points at column i of the W row
+// (shared memory when the block staged its segment, else global), bs at this thread's stack column.
+template <bool kSmem, typename IdxT, bool kG>
+__device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi, IdxT* bs, unsigned bstride, int a_lo,
+                                          int a_hi, int16_t* __restrict__ vo, double* __restrict__ qo,
+                                          double* __restrict__ pro, int64_t nout, int32_t* __restrict__ nvo) {
+  auto u_of = [&](int a) -> double {                 // Eq. 7 point value, a known feasible
+    const int ow = tb.ow[a];
+    const double* wp = Wi + (ow >> 1);
+    double u = wp[0];
+    if (ow & 1) u = __dadd_rn(__dmul_rn(tb.omw[a], u), __dmul_rn(tb.w[a], wp[1]));
+    if (kG) u = __dsub_rn(u, tb.g[a]);
+    return u;
+  };
+  auto st_set = [&](int j, int a) { if (kSmem) bs[(unsigned)j * bstride] = (IdxT)a; else vo[(size_t)j * nout] = (int16_t)a; };
+  auto st_get = [&](int j) -> int { return kSmem ? (int)bs[(unsigned)j * bstride] : (int)vo[(size_t)j * nout]; };
+  int nh = 0;
+  int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
+  double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
+  double dp = 0.0, du = 0.0;     // fl(pb - po), fl(ub - uo): the cross product's stack-side factors
+  // the next point is loaded one iteration ahead (its loads do not depend on the pops)
+#ifndef BID_PF_HULL
+#define BID_PF_HULL 0
+#endif
+#ifndef BID_PF_EMIT
+#define BID_PF_EMIT 1
+#endif
+#if BID_PF_HULL
+  double u_nx = u_of(a_lo), p_nx = tb.act[a_lo];
+#endif
+  for (int a = a_lo; a <= a_hi; ++a) {
+#if BID_PF_HULL
+    const double u = u_nx, pc = p_nx;
+    if (a < a_hi) { u_nx = u_of(a + 1); p_nx = tb.act[a + 1]; }
+#else
+    const double u = u_of(a), pc = tb.act[a];
+#endif
+    while (nh >= 2) {
+      const double cr = __dsub_rn(__dmul_rn(dp, __dsub_rn(u, uo)), __dmul_rn(du, __dsub_rn(pc, po)));
+      if (cr < 0.0) break;
+      --nh;                      // pop b; o becomes the top, the vertex below o resurfaces
+      ab = ao; ub = uo; pb = po;
+      if (nh >= 2) {
+        ao = st_get(nh - 2);
+        uo = u_of(ao);
+        po = tb.act[ao];
+        dp = __dsub_rn(pb, po); du = __dsub_rn(ub, uo);
+      }
+    }
+    st_set(nh, a);
+    if (nh >= 1) { ao = ab; uo = ub; po = pb; }
+    ab = a; ub = u; pb = pc;
+    ++nh;
+    if (nh >= 2) { dp = __dsub_rn(pb, po); du = __dsub_rn(ub, uo); }
+  }
+  // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20); the next
+  // vertex is loaded one step ahead
+  int a_prev = st_get(0);
+  double u_prev = u_of(a_prev);
+  double p_prev = tb.act[a_prev], prev_price = 0.0;
+  if (kSmem) vo[0] = (int16_t)a_prev;
+  if (qo) qo[0] = p_prev;
+#if BID_PF_EMIT
+  int a_n = nh > 1 ? st_get(1) : 0;
+  double u_n = nh > 1 ? u_of(a_n) : 0.0, p_n = nh > 1 ? tb.act[a_n] : 0.0;
+#endif
+  for (int j = 1; j < nh; ++j) {
+#if BID_PF_EMIT
+    const int a = a_n;
+    const double u = u_n, pc = p_n;
+    if (j + 1 < nh) { a_n = st_get(j + 1); u_n = u_of(a_n); p_n = tb.act[a_n]; }
+#else
+    const int a = st_get(j);
+    const double u = u_of(a), pc = tb.act[a];
+#endif
+    double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
+    if (j > 1 && pj < prev_price) pj = prev_price;
+    pro[(size_t)(j - 1) * nout] = pj;
+    if (kSmem) vo[(size_t)j * nout] = (int16_t)a;
+    if (qo) qo[(size_t)j * nout] = pc;
+    prev_price = pj; u_prev = u; p_prev = pc;
+  }
+  *nvo = nh;
 }
 
 // One thread per requested curve.  The monotone chain keeps its two top vertices in registers and the
-// rest of the stack as int16 action indices in shared memory (column-major per thread: conflict-free);
-// u of a deeper vertex is recomputed from its index when it resurfaces.  When every request of the
-// block is on the same (t, k) row (the common "all i of a stage" case) the W row segment is staged in
-// shared memory.  kSmem = false: the stack lives in the caller's vert row (very large A).
-template <bool kSmem>
+// rest of the stack as action indices in shared memory (column-major per thread: conflict-free); u of a
+// deeper vertex is recomputed from its index when it resurfaces.  When every request of the block is on
+// the same (t, k) row (the common "all i of a stage" case) the W row segment is staged in shared memory.
+// kSmem = false: the stack lives in the caller's vert row (very large A).  kG: payoff lambda p - g(p)
+// (u = Wint - g_a, R13), else u = Wint.  Per-action offset and interpolation flag share one word.
+template <bool kSmem, typename IdxT, bool kG>
 __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req,
                                                                const int32_t* __restrict__ slot, int64_t nout,
                                                                int cap, int o_min, int o_span,
                                                                int32_t* __restrict__ nvert, int16_t* __restrict__ vert,
                                                                double* __restrict__ q, double* __restrict__ price) {
   // request rq writes output slot `slot[rq]` (or rq) of the vertex-major arrays [cap][nout]
-  extern __shared__ __align__(16) double bsm[];
+  extern __shared__ __align__(16) unsigned char bsm_raw[];
   const int A = bp.A;
-  double* s_act = bsm;
-  double* s_w = s_act + A;
+  double* s_act = (double*)bsm_raw;                  // shared-memory offsets only (no integer casts), so
+  double* s_w = s_act + A;                           // every table access compiles to LDS/STS
   double* s_omw = s_w + A;
   double* s_g = s_omw + A;
-  int* s_off = (int*)(s_g + A);
-  double* s_wt = (double*)(((uintptr_t)(s_off + A) + 15) & ~(uintptr_t)15);
+  int* s_ow = (int*)(s_g + A);
+  double* s_wt = (double*)(bsm_raw + (((size_t)A * 36 + 15) & ~(size_t)15));
   const int nwt = kBidThreads + o_span + 4;
-  int16_t* bst = (int16_t*)(s_wt + nwt);
+  IdxT* bst = (IdxT*)(s_wt + nwt);
   __shared__ int s_tk[2], s_imin, s_imax, s_uniform;
+  (void)cap;
 
   for (int a = threadIdx.x; a < A; a += blockDim.x) {
-    s_act[a] = bp.act[a]; s_w[a] = bp.w[a]; s_omw[a] = bp.omw[a]; s_off[a] = bp.off[a];
-    s_g[a] = bp.kind == 1 ? bp.g[a] : 0.0;
+    const double wa = bp.w[a];
+    s_act[a] = bp.act[a]; s_w[a] = wa; s_omw[a] = bp.omw[a]; s_ow[a] = 2 * bp.off[a] + (wa != 0.0 ? 1 : 0);
+    if (kG) s_g[a] = bp.g[a];
   }
   const int64_t rq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = rq < n;
@@ -569,91 +664,38 @@ __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int
   if (active && (!valid || t != s_tk[0] || (k != s_tk[1] && !bp.rank1))) s_uniform = 0;
   __syncthreads();
   const bool staged = s_uniform && s_imax >= 0 && (s_imax - s_imin) < kBidThreads;
-  const double* Wg = bp.Wall + ((size_t)(t - 1) * bp.wrows + (bp.rank1 ? 0 : k - bp.k_lo)) * bp.ld;
-  const double* Wrow = Wg;
+  const int c0 = s_imin + o_min;
   if (staged) {
-    const int c0 = s_imin + o_min;
     const double* Wb = bp.Wall + ((size_t)(s_tk[0] - 1) * bp.wrows + (bp.rank1 ? 0 : s_tk[1] - bp.k_lo)) * bp.ld;
     for (int x = threadIdx.x; x < nwt; x += blockDim.x) {
       const int col = c0 + x;
       s_wt[x] = (col >= 0 && col < bp.S) ? Wb[col] : 0.0;
     }
-    Wrow = s_wt - c0;
   }
   __syncthreads();
   const int64_t so = slot ? (int64_t)slot[rq < n ? rq : 0] : rq;
   if (!valid) { if (active) nvert[so] = -1; return; }
-  const BidAct ba{s_act, s_w, s_omw, s_g, s_off};
   // feasible actions of row i form one interval [a_lo, a_hi]: the offsets o_a and ceil(e_a) = o_a + [w_a > 0]
   // are non-increasing in a (F is decreasing), so Eq. 4's two bounds cut a prefix and a suffix
   int a_hi, a_lo;
   {
     int lo = 0, hi = A;                              // first a with o_a < -i  -> a_hi = that - 1
-    while (lo < hi) { const int m = (lo + hi) >> 1; if (s_off[m] < -i) hi = m; else lo = m + 1; }
+    while (lo < hi) { const int m = (lo + hi) >> 1; if ((s_ow[m] >> 1) < -i) hi = m; else lo = m + 1; }
     a_hi = lo - 1;
     lo = 0; hi = A;                                  // first a with o_a + [w_a > 0] <= S-1-i
-    while (lo < hi) { const int m = (lo + hi) >> 1; if (s_off[m] + (s_w[m] != 0.0 ? 1 : 0) <= bp.S - 1 - i) hi = m; else lo = m + 1; }
+    while (lo < hi) { const int m = (lo + hi) >> 1; const int ow = s_ow[m]; if ((ow >> 1) + (ow & 1) <= bp.S - 1 - i) hi = m; else lo = m + 1; }
     a_lo = lo;
   }
-  auto u_of = [&](int a) -> double {                 // Eq. 7 point value, a known feasible
-    const int x = i + s_off[a];
-    const double wa = s_w[a];
-    double u = (wa == 0.0) ? Wrow[x] : __dadd_rn(__dmul_rn(s_omw[a], Wrow[x]), __dmul_rn(wa, Wrow[x + 1]));
-    if (bp.kind == 1) u = __dsub_rn(u, s_g[a]);
-    return u;
-  };
+  const BidTables tb{s_act, s_w, s_omw, s_g, s_ow};
   // outputs are vertex-major ([cap][nout]: entry j of curve so at j*nout + so) so that a warp's 32 curves
   // write 32 consecutive words per vertex (coalesced)
-  int16_t* gst = vert + so;
-  const unsigned bstride = blockDim.x;
-  int16_t* bs = bst + threadIdx.x;
-  auto st_set = [&](int j, int a) { if (kSmem) bs[(unsigned)j * bstride] = (int16_t)a; else gst[(size_t)j * nout] = (int16_t)a; };
-  auto st_get = [&](int j) -> int { return kSmem ? bs[(unsigned)j * bstride] : gst[(size_t)j * nout]; };
-  int nh = 0;
-  int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
-  double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
-  for (int a = a_lo; a <= a_hi; ++a) {
-    const double u = u_of(a);
-    const double pc = s_act[a];
-    while (nh >= 2) {
-      const double cr = __dsub_rn(__dmul_rn(__dsub_rn(pb, po), __dsub_rn(u, uo)),
-                                  __dmul_rn(__dsub_rn(ub, uo), __dsub_rn(pc, po)));
-      if (cr < 0.0) break;
-      --nh;                      // pop b; o becomes the top, the vertex below o resurfaces
-      ab = ao; ub = uo; pb = po;
-      if (nh >= 2) {
-        ao = st_get(nh - 2);
-        uo = u_of(ao);
-        po = s_act[ao];
-      }
-    }
-    st_set(nh, a);
-    if (nh >= 1) { ao = ab; uo = ub; po = pb; }
-    ab = a; ub = u; pb = pc;
-    ++nh;
-  }
-  // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20)
-  int16_t* vo = vert + so;
+  IdxT* bs = bst + threadIdx.x;
   double* qo = q ? q + so : nullptr;
-  double* pro = price + so;
-  int a_prev = st_get(0);
-  double u_prev = u_of(a_prev);
-  double p_prev = s_act[a_prev], prev_price = 0.0;
-  if (kSmem) vo[0] = (int16_t)a_prev;
-  if (qo) qo[0] = p_prev;
-  (void)cap;
-  for (int j = 1; j < nh; ++j) {
-    const int a = st_get(j);
-    const double u = u_of(a);
-    const double pc = s_act[a];
-    double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
-    if (j > 1 && pj < prev_price) pj = prev_price;
-    pro[(size_t)(j - 1) * nout] = pj;
-    if (kSmem) vo[(size_t)j * nout] = (int16_t)a;
-    if (qo) qo[(size_t)j * nout] = pc;
-    prev_price = pj; u_prev = u; p_prev = pc;
-  }
-  nvert[so] = nh;
+  if (staged)
+    bid_curve<kSmem, IdxT, kG>(tb, s_wt + (i - c0), bs, blockDim.x, a_lo, a_hi, vert + so, qo, price + so, nout, nvert + so);
+  else
+    bid_curve<kSmem, IdxT, kG>(tb, bp.Wall + ((size_t)(t - 1) * bp.wrows + (bp.rank1 ? 0 : k - bp.k_lo)) * bp.ld + i, bs,
+                               blockDim.x, a_lo, a_hi, vert + so, qo, price + so, nout, nvert + so);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -40,7 +40,10 @@ struct WinParams {
   int o_min, o_max;         // tile halo over all live actions
   double delta, eta_c, eta_d, pbar;
   double dc, dd;            // delta / eta_c and delta * eta_d (for the approximate keys only)
-  double bspan;             // delta (S + span + 2) / min(eta_c, eta_d): bounds |beta * j| over the tile
+  double jspan;             // S + span + 2: bounds |j| over the tile, so |beta * j| <= |beta| jspan
+  const double* g;          // [A] degradation g_a (LINEAR_MINUS_G): pay = fl(fl(lambda p) - g) when g_kind
+  const double* gfit;       // [6] affine fit of g on the runs: gc0, gc1, gd0, gd1, max deviation, max |g|
+  int g_kind;               // 1: payoff lambda p - g(p) (kind LINEAR_MINUS_G), 0: lambda p
 };
 
 // Packed keys: an order-preserving 64-bit image of the (approximate) value with its table position in
@@ -86,17 +89,20 @@ inline size_t window_smem_bytes(int Lc, int Ld, int o_span) {
 
 __device__ __forceinline__ double canon_single(const WinParams& p, const double* __restrict__ wt, int wbase, int i,
                                                int a, double lam) {
-  // canonical candidate fl(fl(lambda p_a) + Wint), -inf if infeasible (tile is -inf padded)
+  // canonical candidate fl(pay + Wint), pay = fl(fl(lambda p_a) - g_a) (R14), -inf if infeasible (tile
+  // is -inf padded)
   const int o = __ldg(p.off + a);
   const double wa = __ldg(p.w + a);
   const int x = i + o - wbase;
   const double wint = (wa == 0.0) ? wt[x] : __dadd_rn(__dmul_rn(__ldg(p.omw + a), wt[x]), __dmul_rn(wa, wt[x + 1]));
-  return __dadd_rn(__dmul_rn(lam, __ldg(p.act + a)), wint);
+  double pay = __dmul_rn(lam, __ldg(p.act + a));
+  if (p.g_kind) pay = __dsub_rn(pay, __ldg(p.g + a));
+  return __dadd_rn(pay, wint);
 }
 
 // a single action's data staged in shared memory for the whole block
 struct SingleAct {
-  double pay;   // fl(lambda * p_a) for this block's k
+  double pay;   // fl(fl(lambda * p_a) - g_a) for this block's k (R14; g = 0 for the linear payoff)
   double w, omw;
   int off, a;
 };
@@ -144,8 +150,13 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
 
   const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
   const double lam = p.lambda_t[k];
-  const double beta_c = __dmul_rn(lam, p.dc);      // lambda delta / eta_c (any few-ulp rounding: see eps)
-  const double beta_d = __dmul_rn(lam, p.dd);      // lambda delta eta_d
+  // key slopes: the run payoffs lambda p - g are affine in the offset o (g fitted by gc0 + gc1 o on the
+  // charge run, gd0 + gd1 |o| on the discharge run; g = 0 for the linear payoff), so
+  //   cand(i, j) ~= key(j) + beta i - g0,  key(j) = W[j] - beta j,
+  //   beta_c = lambda delta / eta_c + gc1,  beta_d = lambda delta eta_d - gd1   (any few-ulp rounding: see eps)
+  const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
+  const double beta_c = __dadd_rn(__dmul_rn(lam, p.dc), gc1);
+  const double beta_d = __dsub_rn(__dmul_rn(lam, p.dd), gd1);
   const int wbase = i0 + p.o_min;
   const int nsg = p.nsingle < kMaxSingles ? p.nsingle : kMaxSingles;
   if (tid < nsg) {
@@ -153,6 +164,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     SingleAct s;
     s.a = a; s.off = __ldg(p.off + a); s.w = __ldg(p.w + a); s.omw = __ldg(p.omw + a);
     s.pay = __dmul_rn(lam, __ldg(p.act + a));
+    if (p.g_kind) s.pay = __dsub_rn(s.pay, __ldg(p.g + a));
     ss[tid] = s;
   }
   unsigned long long mx = 0ull;   // max |W| over the tile, as ordered bits of a non-negative double
@@ -191,10 +203,11 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
 #pragma unroll
   for (int w = 1; w < kWinThreads / 32; ++w) mb = umax64(mb, red[w]);
   const double M = __longlong_as_double((long long)mb);
-  const double bmax = fabs(lam) * p.bspan;    // |lambda| delta (S + span) / min(eta), factor from the host
+  const double bmax = fmax(fabs(beta_c), fabs(beta_d)) * p.jspan;   // >= |beta j| over the tile
   // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
-  // the <1024-ulp truncation of the packed keys (|key| <= M + bmax)
-  const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar) + 0x1p-41 * (M + bmax);
+  // the <1024-ulp truncation of the packed keys (|key| <= M + bmax); gfit[4] is the largest deviation
+  // of g from its affine fit, gfit[5] bounds |g| (both 0 for the linear payoff)
+  const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar + p.gfit[5]) + 0x1p-41 * (M + bmax) + p.gfit[4];
 
   const int i = i0 + tid;
   const bool valid = i < p.S;
@@ -209,7 +222,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     int xc, xd;
     window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
     window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
-    const double bci = __dmul_rn(beta_c, (double)i), bdi = __dmul_rn(beta_d, (double)i);
+    const double bci = __dsub_rn(__dmul_rn(beta_c, (double)i), gc0), bdi = __dsub_rn(__dmul_rn(beta_d, (double)i), gd0);
     // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
     double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);
     int a1 = p.a_z - ((i0 + 1 + xc) - i);

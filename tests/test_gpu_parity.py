@@ -232,6 +232,46 @@ def test_cfg3_nonconcave_payoff_and_bids():
         assert np.all(np.diff(out["price"][j, :n - 1]) >= 0)
 
 
+@pytest.mark.parametrize("rank1", [False, True])
+def test_cfg3_window_affine_degradation(rank1):
+    """NEXT-1 for lambda p - g(p) with g affine on each side (cfg3: 2|p| + 25 [p != 0]): the exact
+    sliding-window stencil applies (slopes beta +- g1, constants g0) and stays bit-identical to the
+    oracle's brute force at full cfg3ii size; forcing brute force gives the same bits."""
+    base = workloads.cfg2(T=2, K=2)
+    inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=24, K=100, rank1=rank1)
+    _compare_all(inst, nthreads=16, expect_window=True)
+    _compare_all(inst, nthreads=16, brute=True)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_window_affine_g_random(seed):
+    """Random instances with g = per-side affine (random slopes and fixed costs, g(0) = 0) use the window
+    plan and match the oracle bit for bit; a non-affine g loaded later (esdp_load) only widens the
+    exactness margin (canonical fallbacks), never changes a bit."""
+    rng = np.random.default_rng(900 + seed)
+    inst = workloads.random_instance(900 + seed, T=4, K=1 + seed % 5, S_max=700, rank1=bool(seed % 2))
+    pr0 = to_oracle(inst)
+    act = oracle.actions(pr0)
+    cc, cd = rng.uniform(-3, 3, 2)
+    fc, fd = rng.uniform(0, 30, 2)
+    g = np.where(act < 0, -cc * act + fc, np.where(act > 0, cd * act + fd, 0.0))
+    inst.payoff_kind = workloads.PAYOFF_LINEAR_MINUS_G
+    inst.g = g
+    S, A = oracle.dims(pr0)
+    _compare_all(inst, expect_window=None)
+    with _gpu(inst) as s:
+        if not s.stencil_kind & 1:   # too few actions on a side for the window plan
+            return
+        g2 = g + workloads.random_g(seed, A, 1.0)
+        E.esdp_load(s.ctx, g=g2)
+        inst2 = workloads.Instance(**{**inst.__dict__, "g": g2})
+        ref2 = oracle.backward(to_oracle(inst2))
+        assert s.backward() == ref2.J
+        for t in range(1, inst.T + 1):
+            V, _ = s.values(t)
+            assert np.array_equal(V, ref2.V[t - 1]) and np.array_equal(s.policy(t), ref2.pol[t - 1])
+
+
 @pytest.mark.parametrize("persist", [False, True])
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg3"])
 def test_fused_bidcurves_in_backward(name, persist):

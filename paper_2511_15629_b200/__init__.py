@@ -29,7 +29,7 @@ ESDP_PAYOFF_LINEAR, ESDP_PAYOFF_LINEAR_MINUS_G, ESDP_PAYOFF_TABLE = 0, 1, 2
 ESDP_KEEP_VALUES = 1
 ESDP_PROFILE = 2
 ESDP_FORCE_BRUTE = 4
-ESDP_PDL = 8
+ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
 ESDP_PERSIST = 32
 ESDP_DMMA_L2 = 64
@@ -305,13 +305,13 @@ class Solver:
     """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
-    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=False, dmma=True, persist=False,
+    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=True, dmma=True, persist=False,
                  dist=None):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
                                (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
-                               | (ESDP_FORCE_BRUTE if force_brute else 0) | (ESDP_PDL if pdl else 0)
+                               | (ESDP_FORCE_BRUTE if force_brute else 0) | (0 if pdl else ESDP_NO_PDL)
                                | (0 if dmma else ESDP_NO_DMMA) | (ESDP_PERSIST if persist else 0), dist=dist)
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
         self.stencil_kind = esdp_stencil_kind(self.ctx)

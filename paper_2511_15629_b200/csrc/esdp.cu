@@ -728,7 +728,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   c->Kp = world * c->kmax;   // == K on one GPU
   c->pbar = pr->pbar; c->sbar = pr->sbar; c->s0 = pr->s0; c->eta_c = pr->eta_c; c->eta_d = pr->eta_d;
   c->delta = pr->delta; c->kind = pr->payoff_kind; c->rank1 = pr->P == nullptr; c->flags = pr->flags;
-  c->pdl = (pr->flags & ESDP_PDL) != 0;   // measured slower on B200 for this kernel chain: opt-in
+  c->pdl = (pr->flags & ESDP_NO_PDL) == 0;   // late-trigger PDL: dependents launch as the primary drains
   if (pr->A == 0) {
     paper_grid(pr->pbar, pr->eta_c, pr->eta_d, pr->delta, c->act);
     if ((long long)c->act.size() > kMaxA) { delete c; return fail(nullptr, ESDP_E_CONFIG, "A exceeds %d", kMaxA); }

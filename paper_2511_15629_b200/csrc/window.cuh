@@ -68,13 +68,14 @@ __device__ __forceinline__ unsigned long long pack_key(double v, int pos) {
 }
 
 // Sparse table over power-of-two ranges: level q entry x = max of packed keys in [x, x + 2^q).
+// Rows are ns = n rounded up to even entries apart, so every row starts 16-byte aligned (pair access).
 struct RangeMax {
-  unsigned long long* v;   // [levels][n]
-  int n;
+  unsigned long long* v;   // [levels][ns]
+  int n, ns;
   __device__ __forceinline__ unsigned long long query(int l, int r) const {   // 0 if l > r
     if (l > r) return 0ull;
     const int q = 31 - __clz(r - l + 1);
-    const unsigned long long* row = v + q * n;
+    const unsigned long long* row = v + q * ns;
     return umax64(row[l], row[r - (1 << q) + 1]);
   }
 };
@@ -82,8 +83,8 @@ struct RangeMax {
 inline int window_levels(int L) { int q = 0; while ((2 << q) <= L) ++q; return q + 1; }
 
 inline size_t window_smem_bytes(int Lc, int Ld, int o_span) {
-  const size_t nw = kWinTile + o_span + 2;
-  const size_t nc = kWinTile + Lc, nd = kWinTile + Ld;
+  const size_t nw = (kWinTile + o_span + 2 + 1) & ~(size_t)1;
+  const size_t nc = (kWinTile + Lc + 1) & ~(size_t)1, nd = (kWinTile + Ld + 1) & ~(size_t)1;
   return sizeof(double) * nw + sizeof(unsigned long long) * (window_levels(Lc) * nc + window_levels(Ld) * nd) + 64;
 }
 
@@ -113,16 +114,26 @@ __device__ __forceinline__ double canon_staged(const SingleAct& s, const double*
   return __dadd_rn(s.pay, wint);
 }
 
-// level q of a table: entry x = max(level q-1 at x, at x + 2^(q-1)), for x <= n - 2^q.  Straight-line:
-// each thread owns x = tid, tid + 256, tid + 512 (n <= 256 + 512).
+// level q of a table: entry x = max(level q-1 at x, at x + 2^(q-1)), for x <= n - 2^q.  Straight-line,
+// two entries per thread and slot with 16-byte shared-memory accesses: x = 2 tid, 2 tid + 512 (n <= 768).
 __device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
   const int h = 1 << (q - 1), lim = t.n - (1 << q);
-  const unsigned long long* pv = t.v + (q - 1) * t.n;
-  unsigned long long* nv = t.v + q * t.n;
+  const unsigned long long* pv = t.v + (q - 1) * t.ns;
+  unsigned long long* nv = t.v + q * t.ns;
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    const int x = tid + u * kWinThreads;
-    if (x <= lim) nv[x] = umax64(pv[x], pv[x + h]);
+  for (int u = 0; u < 2; ++u) {
+    const int x = 2 * (tid + u * kWinThreads);
+    if (x <= lim) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(pv + x);
+      ulonglong2 b;
+      if (h == 1) { b.x = a.y; b.y = pv[x + 2]; }
+      else b = *reinterpret_cast<const ulonglong2*>(pv + x + h);
+      ulonglong2 r;
+      r.x = umax64(a.x, b.x);
+      r.y = umax64(a.y, b.y);
+      if (x + 1 <= lim) *reinterpret_cast<ulonglong2*>(nv + x) = r;
+      else nv[x] = r.x;
+    }
   }
 }
 
@@ -142,9 +153,11 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   RangeMax tc, td;
   tc.n = kWinTile + p.Lc;                  // charge table: columns [i0 + 1, i0 + nc]
   td.n = kWinTile + p.Ld;                  // discharge table: columns [i0 - Ld, i0 + kWinTile)
+  tc.ns = (tc.n + 1) & ~1;
+  td.ns = (td.n + 1) & ~1;
   double* wt = wsm;                        // W over columns [wbase, wbase + nw)
-  tc.v = (unsigned long long*)(wt + nw);
-  td.v = tc.v + (size_t)lc * tc.n;
+  tc.v = (unsigned long long*)(wt + ((nw + 1) & ~1));
+  td.v = tc.v + (size_t)lc * tc.ns;
   __shared__ unsigned long long red[kWinThreads / 32];
   __shared__ SingleAct ss[kMaxSingles];
 
@@ -179,14 +192,20 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     wt[x] = v;
   }
   __syncthreads();
-  // level 0: packed key(j) = W[j] - beta*j, position x
-  for (int x = tid; x < tc.n; x += kWinThreads) {
+  // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores)
+  for (int x = 2 * tid; x < tc.n; x += 2 * kWinThreads) {
     const int j = i0 + 1 + x;
-    tc.v[x] = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
+    ulonglong2 r;
+    r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
+    r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_c, (double)(j + 1))), x + 1);
+    *reinterpret_cast<ulonglong2*>(tc.v + x) = r;    // entry n (x + 1 == n) is padding
   }
-  for (int x = tid; x < td.n; x += kWinThreads) {
+  for (int x = 2 * tid; x < td.n; x += 2 * kWinThreads) {
     const int j = i0 - p.Ld + x;
-    td.v[x] = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
+    ulonglong2 r;
+    r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
+    r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_d, (double)(j + 1))), x + 1);
+    *reinterpret_cast<ulonglong2*>(td.v + x) = r;
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) mx = umax64(mx, __shfl_xor_sync(0xffffffffu, mx, s));

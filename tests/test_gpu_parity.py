@@ -185,6 +185,21 @@ def test_dataflow_plan_no_keep_values(seed, rank1):
                 assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
+@pytest.mark.parametrize("rank1", [False, True])
+def test_graph_without_pdl(rank1):
+    """The graph plan without programmatic dependent launch (ESDP_NO_PDL) gives the same bits as the
+    default late-trigger PDL chain."""
+    inst = workloads.cfg2(T=30, K=30, rank1=rank1)
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=16)
+    with E.Solver(inst, pdl=False) as s:
+        assert s.backward() == ref.J
+        for t in range(1, inst.T + 1):
+            V, W = s.values(t)
+            assert np.array_equal(V, ref.V[t - 1]) and np.array_equal(W, ref.W[t - 1])
+            assert np.array_equal(s.policy(t), ref.pol[t - 1])
+
+
 def test_cfg2_rank1_full_size_persistent_plan():
     _compare_all(workloads.cfg2(rank1=True), nthreads=16, persist=True, expect_window=True)
 

@@ -22,7 +22,7 @@ def bw_time(s, n=10):
 
 for keep in (True,):
     for brute in (False,):
-        for pdl, dmma in ((False, True), (True, True), (False, "l2"), (False, False)):
+        for pdl, dmma in ((True, True), (False, True), (True, "l2"), (True, False)):
             if dmma == "l2":
                 import types
                 s = E.Solver.__new__(E.Solver)
@@ -35,7 +35,7 @@ for keep in (True,):
                 s = E.Solver(inst, keep_values=keep, force_brute=brute, pdl=pdl, dmma=dmma)
             ms = bw_time(s)
             line = f"keep={int(keep)} stencil={'brute ' if not s.stencil_kind else 'window'} pdl={int(pdl)} dmma={dmma}: backward {ms:.3f} ms ({ms / inst.T * 1e3:.2f} us/stage)"
-            if keep and not pdl:
+            if keep and pdl:
                 line += "  | warm us/launch: contract %.2f stencil %.2f objective %.2f" % (
                     E.esdp_debug_time(s.ctx, 0), E.esdp_debug_time(s.ctx, 1), E.esdp_debug_time(s.ctx, 3))
             print(line, flush=True)

@@ -158,7 +158,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   double* wt = wsm;                        // W over columns [wbase, wbase + nw)
   tc.v = (unsigned long long*)(wt + ((nw + 1) & ~1));
   td.v = tc.v + (size_t)lc * tc.ns;
-  __shared__ unsigned long long red[kWinThreads / 32];
+  __shared__ unsigned red[kWinThreads / 32];
   __shared__ SingleAct ss[kMaxSingles];
 
   const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
@@ -180,14 +180,15 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     if (p.g_kind) s.pay = __dsub_rn(s.pay, __ldg(p.g + a));
     ss[tid] = s;
   }
-  unsigned long long mx = 0ull;   // max |W| over the tile, as ordered bits of a non-negative double
+  // max |W| over the tile: the high words of |W| (ordered like the values), reduced with REDUX; the
+  // bound M below fills the low word with ones, so M >= max |W|
+  unsigned mx = 0u;
   for (int x = tid; x < nw; x += kWinThreads) {
     const int col = wbase + x;
     double v = -INFINITY;
     if (col >= 0 && col < p.S) {
       v = __ldcg(Wrow + col);
-      const unsigned long long ab = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
-      mx = ab > mx ? ab : mx;
+      mx = umax(mx, (unsigned)__double2hiint(v) & 0x7fffffffu);
     }
     wt[x] = v;
   }
@@ -207,21 +208,21 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_d, (double)(j + 1))), x + 1);
     *reinterpret_cast<ulonglong2*>(td.v + x) = r;
   }
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) mx = umax64(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  mx = __reduce_max_sync(0xffffffffu, mx);
   if ((tid & 31) == 0) red[tid >> 5] = mx;
   __syncthreads();
   const int top = p.pc > p.pd ? p.pc : p.pd;
-  for (int q = 1; q <= top; ++q) {
+#pragma unroll
+  for (int q = 1; q <= 9; ++q) {        // levels <= 9 (L <= 512): unrolled, uniform exits
+    if (q > top) break;
     if (q <= p.pc) build_level(tc, q, tid);
     if (q <= p.pd) build_level(td, q, tid);
     __syncthreads();
   }
   (void)ldl;
-  unsigned long long mb = red[0];
-#pragma unroll
-  for (int w = 1; w < kWinThreads / 32; ++w) mb = umax64(mb, red[w]);
-  const double M = __longlong_as_double((long long)mb);
+  static_assert(kWinThreads / 32 == 8, "one red[] entry per lane group of 8");
+  const unsigned mb = __reduce_max_sync(0xffffffffu, red[tid & 7]);
+  const double M = __hiloint2double((int)mb, (int)0xffffffffu);
   const double bmax = fmax(fabs(beta_c), fabs(beta_d)) * p.jspan;   // >= |beta j| over the tile
   // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
   // the <1024-ulp truncation of the packed keys (|key| <= M + bmax); gfit[4] is the largest deviation

@@ -249,7 +249,8 @@ def run_ours(args):
         if world > 1 and j == args.warmup:
             dist.barrier()
         t0 = time.perf_counter()
-        st = E.lib.esdp_load(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
+        # validated, then uploaded on the copy stream in stage chunks that the backward waits for one by one
+        st = E.lib.esdp_load_async(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
         assert st == 0, E.esdp_last_error(solver.ctx)
         assert E.lib.esdp_backward(solver.ctx, sp, ctypes.byref(Jh)) == 0
         if n_bid and not fused:

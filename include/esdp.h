@@ -119,6 +119,14 @@ esdp_status esdp_actions(const esdp_ctx* ctx, double* actions);
 esdp_status esdp_load(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
                       const double* g);
 
+/* Same as esdp_load, but returns once the arrays are validated and their upload is enqueued (P in stage
+ * chunks, highest stages first, on the context's copy stream); the next backward pass waits for each
+ * chunk only where it needs it, so the host-to-device copy overlaps the solve.  The host arrays must
+ * stay valid and unmodified until the next esdp_backward (or a synchronizing call after
+ * esdp_backward_async) returns; pinned (page-locked) memory makes the copies asynchronous. */
+esdp_status esdp_load_async(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
+                            const double* g);
+
 /* Backward induction, Alg. 1 lines 6-11 in Markov form (Eqs. 5-6):
  *   W_T = 0;  for t = T..1:  W_t = P_t V_{t+1} (t < T),
  *             V_t(i,k) = max_a pay(t,k,a) + Wint_t(i,a,k),  pol_t(i,k) = smallest argmax,

@@ -18,7 +18,7 @@ __all__ = [
     "ESDP_OK", "ESDP_E_CONFIG", "ESDP_E_DATA", "ESDP_E_INTERNAL", "ESDP_E_STATE", "ESDP_E_CUDA",
     "ESDP_E_NCCL", "ESDP_E_NOMEM", "ESDP_PAYOFF_LINEAR", "ESDP_PAYOFF_LINEAR_MINUS_G",
     "ESDP_PAYOFF_TABLE", "ESDP_KEEP_VALUES", "EsdpError", "esdp_problem", "LIB_PATH", "lib",
-    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
+    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_load_async", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_destroy",
     "esdp_last_error", "ESDP_PROFILE", "ESDP_FORCE_BRUTE", "esdp_stencil_kind", "Solver", "EXPORTED_SYMBOLS",
@@ -37,7 +37,7 @@ ESDP_DMMA_L2 = 64
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
 EXPORTED_SYMBOLS = [
-    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_backward", "esdp_backward_async",
+    "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_load_async", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
@@ -78,6 +78,7 @@ def _load():
         "esdp_dims": ([ctx, _i32p, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_actions": ([ctx, _dp], ctypes.c_int),
         "esdp_load": ([ctx, _dp, _dp, _dp, _dp], ctypes.c_int),
+        "esdp_load_async": ([ctx, _dp, _dp, _dp, _dp], ctypes.c_int),
         "esdp_backward": ([ctx, _vp, _dp], ctypes.c_int),
         "esdp_backward_async": ([ctx, _vp], ctypes.c_int),
         "esdp_objective": ([ctx, _dp], ctypes.c_int),
@@ -183,6 +184,14 @@ def esdp_actions(ctx):
 def esdp_load(ctx, lam=None, P=None, pi=None, g=None):
     keep = [_f64(x) for x in (lam, P, pi, g)]
     _check(lib.esdp_load(ctx, *[_p(x) for x in keep]), "esdp_load", ctx)
+
+
+def esdp_load_async(ctx, lam=None, P=None, pi=None, g=None):
+    """Validate and enqueue the upload; returns the host arrays, which the caller must keep alive (and
+    unmodified) until the next backward pass has completed."""
+    keep = [_f64(x) for x in (lam, P, pi, g)]
+    _check(lib.esdp_load_async(ctx, *[_p(x) for x in keep]), "esdp_load_async", ctx)
+    return keep
 
 
 def _stream_ptr(stream):

@@ -12,7 +12,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/esdp.h"
@@ -77,6 +81,14 @@ struct esdp_ctx {
   double *d_q = nullptr, *d_price = nullptr;
   int64_t out_cap = 0;
   cudaStream_t stream = nullptr;
+  // input uploads (upload): on their own stream, in the order the backward consumes them -- lambda/pi/g
+  // first (ev_head), then P in stage chunks T-1.. (chunk_ev[j] covers stages [chunk_lo[j], chunk_hi[j]]);
+  // the backward graph waits on these events (external event-wait nodes), so a load overlaps the solve
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_head = nullptr, use_ev = nullptr, ev_tables = nullptr;
+  bool use_pending = false;    // use_ev recorded after the last enqueue that reads the inputs
+  std::vector<cudaEvent_t> chunk_ev;
+  std::vector<int> chunk_lo, chunk_hi;
   cudaGraphExec_t graph = nullptr;
   size_t stencil_smem = 0;
   int64_t launches = 0;
@@ -155,6 +167,75 @@ void paper_grid(double pbar, double eta_c, double eta_d, double delta, std::vect
   }
 }
 
+// A small persistent host thread pool for input validation (one per process, created on first use):
+// run(n, f) calls f(0..n-1) on the pool and the calling thread and returns when all are done.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(int n, const std::function<void(int)>& f) {
+    std::unique_lock<std::mutex> lk(run_m_);   // one job at a time
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f; n_ = n; next_ = 0; left_ = n; ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [&] { return left_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nw = (int)std::min<unsigned>(15, hw > 1 ? hw - 1 : 1);
+    for (int w = 0; w < nw; ++w) th_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    { std::lock_guard<std::mutex> g(m_); stop_ = true; }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void work() {   // take task indices until none is left
+    for (;;) {
+      int k;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (!job_ || next_ >= n_) return;
+        k = next_++;
+        f = job_;
+      }
+      (*f)(k);
+      std::lock_guard<std::mutex> g(m_);
+      if (--left_ == 0) done_.notify_all();
+    }
+  }
+  void loop() {
+    long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, run_m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, next_ = 0, left_ = 0;
+  long long gen_ = 0;
+  bool stop_ = false;
+};
+
 esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
   for (long long j = 0; j < (long long)c->T * c->K; ++j)
     if (!std::isfinite(lambda[j])) return fail(c, ESDP_E_DATA, "lambda[%lld] is not finite", j);
@@ -166,8 +247,19 @@ esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, co
       if (!std::isfinite(g[j])) return fail(c, ESDP_E_DATA, "payoff table entry %lld is not finite", j);
   }
   if (!c->rank1) {
-    for (long long r = 0; r < (long long)(c->T - 1) * c->K; ++r)
-      if (!simplex_ok(P + r * c->K, c->K)) return fail(c, ESDP_E_DATA, "row %lld of P is not a probability simplex", r);
+    // the (T-1) K rows of P on the host thread pool; the first failing row is reported, as sequentially
+    const long long rows = (long long)(c->T - 1) * c->K;
+    const int nth = (int)std::max<long long>(1, std::min<long long>(4 * HostPool::get().size(), rows / 2048));
+    std::vector<long long> bad((size_t)nth, rows);
+    std::function<void(int)> scan = [&](int w) {
+      const long long lo = rows * w / nth, hi = rows * (w + 1) / nth;
+      for (long long r = lo; r < hi; ++r)
+        if (!simplex_ok(P + r * c->K, c->K)) { bad[w] = r; return; }
+    };
+    if (nth == 1) scan(0);
+    else HostPool::get().run(nth, scan);
+    const long long r = *std::min_element(bad.begin(), bad.end());
+    if (r < rows) return fail(c, ESDP_E_DATA, "row %lld of P is not a probability simplex", r);
     if (!simplex_ok(pi, c->K)) return fail(c, ESDP_E_DATA, "pi_1 is not a probability simplex");
   } else {
     for (int t = 0; t < c->T; ++t)
@@ -301,6 +393,11 @@ void free_all(esdp_ctx* c) {
   for (cudaEvent_t e : c->fb_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
+  for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->ev_head) cudaEventDestroy(c->ev_head);
+  if (c->ev_tables) cudaEventDestroy(c->ev_tables);
+  if (c->use_ev) cudaEventDestroy(c->use_ev);
+  if (c->copy) cudaStreamDestroy(c->copy);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
                 c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
@@ -309,24 +406,22 @@ void free_all(esdp_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
+// Enqueue the upload of the given inputs (NULL = keep) on the copy stream, after every enqueued use of
+// the previous inputs; lambda / pi / g and their tables first (ev_head), then P and its sampling tables in
+// stage chunks in the order the backward needs them (chunk_ev).  Does not synchronize.
 esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
   const size_t TK = (size_t)c->T * c->K;
-  cudaStream_t s = c->stream;
+  cudaStream_t s = c->copy;
+  if (c->use_pending) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->use_ev, 0));
   if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_lambda, lambda, TK * sizeof(double), cudaMemcpyHostToDevice, s));
   if (!c->rank1) {
-    const size_t n = (size_t)(c->T - 1) * c->K * c->K;
-    if (P && n) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P, P, n * sizeof(double), cudaMemcpyHostToDevice, s));
     if (pi) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, c->K * sizeof(double), cudaMemcpyHostToDevice, s));
   } else if (pi) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, TK * sizeof(double), cudaMemcpyHostToDevice, s));
+    // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
+    cdf_kernel<<<cdf_blocks(c->T), kCdfWarps * 32, 0, s>>>(c->d_pi, c->T, c->K, c->G, c->d_cdf, c->d_guide);
   }
-  // sampling tables for the forward simulation (cdf + guide per transition row), built on the device
-  const int64_t rows = c->rank1 ? c->T : (int64_t)(c->T - 1) * c->K;
-  if ((P || pi) && rows > 0) {
-    const double* q = c->rank1 ? c->d_pi : c->d_P;
-    cdf_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(q, rows, c->K, c->G, c->d_cdf, c->d_guide);
-  }
-  if (pi) cdf_kernel<<<1, 32, 0, s>>>(c->d_pi, 1, c->K, c->G, c->d_cdf1, c->d_guide1);  // pi_1 (row 0 in rank-1)
+  if (pi) cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(c->d_pi, 1, c->K, c->G, c->d_cdf1, c->d_guide1);  // pi_1 (row 0 in rank-1)
   CUDA_OR_FAIL(c, cudaGetLastError());
   if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -338,8 +433,30 @@ esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const dou
   }
   if (g && c->kind == ESDP_PAYOFF_TABLE)
     CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, s));
-  CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
+  CUDA_OR_FAIL(c, cudaEventRecord(c->ev_head, s));
+  // P chunks: the backward waits only for the copy; the sampling tables (needed by the simulation
+  // alone) are built after it and signalled by ev_tables
+  for (size_t j = 0; j < c->chunk_ev.size(); ++j) {
+    if (!c->rank1 && P) {
+      const size_t r0 = (size_t)(c->chunk_lo[j] - 1) * c->K, nr = (size_t)(c->chunk_hi[j] - c->chunk_lo[j] + 1) * c->K;
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P + r0 * c->K, P + r0 * c->K, nr * c->K * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    CUDA_OR_FAIL(c, cudaEventRecord(c->chunk_ev[j], s));
+  }
+  if (!c->rank1 && P && c->T > 1) {
+    const int64_t nr = (int64_t)(c->T - 1) * c->K;
+    cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(c->d_P, nr, c->K, c->G, c->d_cdf, c->d_guide);
+    CUDA_OR_FAIL(c, cudaGetLastError());
+  }
+  CUDA_OR_FAIL(c, cudaEventRecord(c->ev_tables, s));
   c->solved = false;
+  return ESDP_OK;
+}
+
+// After enqueueing work that reads the inputs on stream s: later uploads wait for it.
+esdp_status mark_use(esdp_ctx* c, cudaStream_t s) {
+  CUDA_OR_FAIL(c, cudaEventRecord(c->use_ev, s));
+  c->use_pending = true;
   return ESDP_OK;
 }
 
@@ -579,6 +696,8 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   };
   if (c->persist) {   // one dataflow kernel; bid curves (if any) after it, on the same stream
     CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, T), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
+    CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_head, cudaEventWaitExternal));
+    for (cudaEvent_t e : c->chunk_ev) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, e, cudaEventWaitExternal));
     if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[0], s, cudaEventRecordExternal));
     CUDA_OR_FAIL(c, launch_persistent(c, s));
     if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[1], s, cudaEventRecordExternal));
@@ -597,8 +716,14 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   for (int t = T; t >= 1; --t) {
     if (t == T) {
       CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, t), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_head, cudaEventWaitExternal));   // lambda, pi, g uploaded
       after_kernel = false;
     } else {
+      for (size_t j = 0; j < c->chunk_ev.size(); ++j)   // P_t's upload chunk (first stage of the chunk)
+        if (c->chunk_hi[j] == t) {
+          CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->chunk_ev[j], cudaEventWaitExternal));
+          after_kernel = false;
+        }
       CUDA_OR_FAIL(c, mark(t, 0));
       CUDA_OR_FAIL(c, launch_contract(c, t, s, pdl && after_kernel && !sampled(t)));
       CUDA_OR_FAIL(c, mark(t, 1));
@@ -806,7 +931,29 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
   TRY(dev_alloc(c, &c->d_gfit, 6));
   if (cudaMemcpy(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload g fit"); return bail(ESDP_E_CUDA); }
+  if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_head, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_tables, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->use_ev, cudaEventDisableTiming) != cudaSuccess) {
+    fail(c, ESDP_E_CUDA, "copy stream / events");
+    return bail(ESDP_E_CUDA);
+  }
+  {  // P chunks: ~8 stage ranges, highest stages first (the order the backward consumes them)
+    const int nst = c->rank1 ? 0 : T - 1;
+    const int nch = std::min(8, nst);
+    for (int j = 0; j < nch; ++j) {
+      const int hi = nst - (int)((long long)nst * j / nch), lo = nst - (int)((long long)nst * (j + 1) / nch) + 1;
+      c->chunk_hi.push_back(hi);
+      c->chunk_lo.push_back(lo);
+      c->chunk_ev.push_back(nullptr);
+      if (cudaEventCreateWithFlags(&c->chunk_ev.back(), cudaEventDisableTiming) != cudaSuccess) {
+        fail(c, ESDP_E_CUDA, "chunk event");
+        return bail(ESDP_E_CUDA);
+      }
+    }
+  }
   TRY(upload(c, pr->lambda, pr->P, pr->pi, pr->g));
+  if (cudaStreamSynchronize(c->copy) != cudaSuccess) { fail(c, ESDP_E_CUDA, "initial upload"); return bail(ESDP_E_CUDA); }
   c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
   if (c->use_window) {
     c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min);
@@ -896,26 +1043,41 @@ esdp_status esdp_actions(const esdp_ctx* c, double* actions) {
   return ESDP_OK;
 }
 
-esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
-  if (!c) return ESDP_E_STATE;
-  if (!c->rank1 && P == nullptr && pi != nullptr && false) return ESDP_E_STATE;
+static esdp_status load_impl(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  // a previous upload may still be reading host memory / the graph may still wait on its events
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));
+  if (c->use_pending) CUDA_OR_FAIL(c, cudaEventSynchronize(c->use_ev));
   // validate what is given against the current arrays' shapes
   std::vector<double> lam_h, P_h, pi_h, g_h;
   const size_t TK = (size_t)c->T * c->K;
-  if (!lambda) { lam_h.resize(TK); cudaMemcpy(lam_h.data(), c->d_lambda, TK * 8, cudaMemcpyDeviceToHost); }
-  if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); cudaMemcpy(P_h.data(), c->d_P, P_h.size() * 8, cudaMemcpyDeviceToHost); }
-  if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); cudaMemcpy(pi_h.data(), c->d_pi, pi_h.size() * 8, cudaMemcpyDeviceToHost); }
-  if (!g && c->kind != ESDP_PAYOFF_LINEAR) { g_h.resize(c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : c->A); cudaMemcpy(g_h.data(), c->d_g, g_h.size() * 8, cudaMemcpyDeviceToHost); }
+  if (!lambda) { lam_h.resize(TK); CUDA_OR_FAIL(c, cudaMemcpy(lam_h.data(), c->d_lambda, TK * 8, cudaMemcpyDeviceToHost)); }
+  if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); CUDA_OR_FAIL(c, cudaMemcpy(P_h.data(), c->d_P, P_h.size() * 8, cudaMemcpyDeviceToHost)); }
+  if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); CUDA_OR_FAIL(c, cudaMemcpy(pi_h.data(), c->d_pi, pi_h.size() * 8, cudaMemcpyDeviceToHost)); }
+  if (!g && c->kind != ESDP_PAYOFF_LINEAR) { g_h.resize(c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : c->A); CUDA_OR_FAIL(c, cudaMemcpy(g_h.data(), c->d_g, g_h.size() * 8, cudaMemcpyDeviceToHost)); }
   esdp_status st = validate_data(c, lambda ? lambda : lam_h.data(), P ? P : P_h.data(), pi ? pi : pi_h.data(),
                                  g ? g : g_h.data());
   if (st != ESDP_OK) return st;
   return upload(c, lambda, P, pi, g);
 }
 
+esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  if (!c) return ESDP_E_STATE;
+  esdp_status st = load_impl(c, lambda, P, pi, g);
+  if (st != ESDP_OK) return st;
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));
+  return ESDP_OK;
+}
+
+esdp_status esdp_load_async(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
+  if (!c) return ESDP_E_STATE;
+  return load_impl(c, lambda, P, pi, g);
+}
+
 esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
   if (!c) return ESDP_E_STATE;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
+  { const esdp_status mu = mark_use(c, s); if (mu != ESDP_OK) return mu; }
   c->solved = true;
   return ESDP_OK;
 }
@@ -976,7 +1138,7 @@ esdp_status esdp_bidcurves_dev(esdp_ctx* c, int64_t n, const int32_t* req_dev, i
   if (n <= 0) return ESDP_OK;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   CUDA_OR_FAIL(c, launch_bids(c, n, req_dev, nullptr, n, cap, nvert_dev, vert_dev, q_dev, price_dev, s));
-  return ESDP_OK;
+  return mark_use(c, s);
 }
 
 esdp_status esdp_set_bid_requests(esdp_ctx* c, int64_t n, const int32_t* req, int32_t cap, int32_t* nvert_dev,
@@ -1071,12 +1233,13 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));   // sampling tables of the last upload
   const int thr = 128;
   const size_t sm = sim_smem_bytes(c->A);
   if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   simulate_kernel<<<(unsigned)((n_paths + thr - 1) / thr), thr, sm, s>>>(sp, n_paths, seed, per_path_dev);
   CUDA_OR_FAIL(c, cudaGetLastError());
-  return ESDP_OK;
+  return mark_use(c, s);
 }
 
 esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* mean, double* var, double* per_path) {

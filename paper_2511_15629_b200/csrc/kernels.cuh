@@ -721,37 +721,41 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
 }
 
 // cdf rows (DESIGN R17): running sum in ascending order, last entry forced to 1; plus a guide table
-// guide[b] = first j with b/G < cdf[j], so that a draw u in [b/G, (b+1)/G) starts its search there.
-// A bucket whose whole u range (widened by 2^-49 for the rounding of u*G and b/G) maps to one j is
-// "pure" and stores ~j (< 0): the sampler returns it without touching the cdf row.
-// One thread per row; bit-identical to the oracle's sequential cdf.
-__global__ void cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G, double* __restrict__ cdf,
-                           int16_t* __restrict__ guide) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// guide[b] = first j with b/G < cdf[j] (from a binary search; any start is exact for the sampler's
+// scans), so that a draw u in [b/G, (b+1)/G) starts its search there.  A bucket whose whole u range
+// (widened by 2^-49 for the rounding of u*G and of b/G) maps to one j is "pure" and stores ~j (< 0): the
+// sampler returns it without touching the cdf row.  One warp per row: lane 0 forms the sequential sum
+// (bit-identical to the oracle's cdf), then the lanes fill the guide buckets.
+constexpr int kCdfWarps = 4;
+__global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G,
+                                                            double* __restrict__ cdf, int16_t* __restrict__ guide) {
+  const int64_t r = (int64_t)blockIdx.x * kCdfWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   const double* qr = q + r * K;
   double* cr = cdf + r * K;
   int16_t* gr = guide + r * G;
-  double s = 0.0;
-  int b = 0;
-  for (int j = 0; j < K; ++j) {
-    s = __dadd_rn(s, qr[j]);
-    const double c = (j == K - 1) ? 1.0 : s;
-    cr[j] = c;
-    // bucket lower edge b/G < c  <=>  b < c*G (rounding here only moves the start; the sampler's
-    // scans make the result exact for any start)
-    while (b < G && (double)b < __dmul_rn(c, (double)G)) { gr[b] = (int16_t)j; ++b; }
+  if (lane == 0) {
+    double s = 0.0;
+    for (int j = 0; j < K; ++j) {
+      s = __dadd_rn(s, qr[j]);
+      cr[j] = (j == K - 1) ? 1.0 : s;
+    }
   }
-  for (; b < G; ++b) gr[b] = (int16_t)(K - 1);
-  const double m = 0x1p-49;
-  for (b = 0; b < G; ++b) {
-    const int j = gr[b];
-    const double lo = __ddiv_rn((double)b, (double)G), hi = __ddiv_rn((double)(b + 1), (double)G);
+  __syncwarp();
+  const double m = 0x1p-49, invG = 1.0 / (double)G;
+  for (int b = lane; b < G; b += 32) {
+    const double lo = __dmul_rn((double)b, invG), hi = __dmul_rn((double)(b + 1), invG);
+    int a = 0, z = K - 1;                            // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
+    while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
+    const int j = a;
     const bool below = j == 0 || cr[j - 1] < __dsub_rn(lo, m);      // every u of the bucket >= cdf[j-1]
     const bool above = j == K - 1 || cr[j] > __dadd_rn(hi, m);      // every u of the bucket <  cdf[j]
-    if (below && above) gr[b] = (int16_t)~j;
+    gr[b] = (int16_t)(below && above ? ~j : j);
   }
 }
+
+inline unsigned cdf_blocks(int64_t rows) { return (unsigned)((rows + kCdfWarps - 1) / kCdfWarps); }
 
 // first j in [0, K) with u < cdf[j]; pure buckets answer directly, otherwise the guide gives a start and
 // the scans make it exact for any start (both neighbours are loaded together).

@@ -200,6 +200,42 @@ def test_graph_without_pdl(rank1):
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
+@pytest.mark.parametrize("persist", [False, True])
+@pytest.mark.parametrize("rank1", [False, True])
+def test_async_load_overlaps_and_matches(rank1, persist):
+    """esdp_load_async: new prices and transitions uploaded in stage chunks while the backward runs (the
+    graph waits per chunk) give the oracle's bits for the new data; repeated async loads alternate
+    between two instances; the simulation's sampling tables follow the new P."""
+    a = workloads.cfg2(T=40, K=20, rank1=rank1)
+    b = workloads.cfg2(T=40, K=20, rank1=rank1)
+    lam_b, _, _ = workloads.price_chain(a.T, a.K, 5.0 / 60.0, seed=workloads.SEED_BASE + 4242)
+    b.lam = lam_b
+    if not rank1:
+        rng = np.random.default_rng(7)
+        Pb = a.P * rng.uniform(0.5, 1.5, a.P.shape)
+        b.P = Pb / Pb.sum(axis=2, keepdims=True)
+    refs = [oracle.backward(to_oracle(x), nthreads=16) for x in (a, b)]
+    sims = {}
+    with E.Solver(a, persist=persist) as s:
+        assert bool(s.stencil_kind & 2) == persist
+        for rep in range(4):
+            x, ref = ((a, refs[0]), (b, refs[1]))[rep % 2]
+            keep = E.esdp_load_async(s.ctx, lam=x.lam, P=x.P, pi=x.pi)
+            J = s.backward()
+            del keep
+            assert J == ref.J
+            for t in (1, x.T // 2, x.T):
+                V, W = s.values(t)
+                assert np.array_equal(V, ref.V[t - 1]) and np.array_equal(W, ref.W[t - 1])
+                assert np.array_equal(s.policy(t), ref.pol[t - 1])
+            m = s.simulate(4096, seed=5, per_path=False)[1]
+            key = rep % 2
+            if key in sims:
+                assert m == sims[key]
+            sims[key] = m
+        assert sims[0] != sims[1]
+
+
 def test_cfg2_rank1_full_size_persistent_plan():
     _compare_all(workloads.cfg2(rank1=True), nthreads=16, persist=True, expect_window=True)
 

@@ -211,6 +211,44 @@ void esdp_destroy(esdp_ctx* ctx);
 /* Message of the last failing call on ctx (ctx == NULL: last esdp_create failure of this thread). */
 const char* esdp_last_error(const esdp_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------------
+ * Batch contexts (SURVEY §8(b) esdp_create_batch; BASELINE cfg5: a sweep of storage configurations
+ * over one price model).  n instances share T, K, sbar, delta (hence S), lambda, P and pi (the
+ * price model of Eqs. 5-6) and each have their own pbar, eta_c, eta_d, s0, action grid
+ * (Eq. 10) and payoff (LINEAR or LINEAR_MINUS_G; TABLE is rejected).  The backward pass
+ * of all instances is one CUDA graph: per stage ONE expectation W_t = P_t V_{t+1} over the stacked
+ * [K][n][ld] values (one [K] x [n ld] product) and ONE window-stencil launch over every instance on
+ * the exact sliding-window plan (the others take a brute-force launch each).  Every instance's
+ * values, policy and J are bit-identical to a context of its own.  Values are not kept per stage
+ * (V_1 only); the policy of every stage is kept ([n][T][K][S] int16).
+ * --------------------------------------------------------------------------------------------- */
+typedef struct esdp_batch esdp_batch;
+
+/* probs[0..n-1]: host descriptions as for esdp_create (deep-copied).  lambda, P and pi must be
+ * identical in content across instances (else ESDP_E_CONFIG); they are validated once.  flags:
+ * KEEP_VALUES / PROFILE / PERSIST are ignored.  Errors as esdp_create (message: esdp_batch_last_error(NULL)). */
+esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch** out);
+/* n, T, S, K and A[n] (each instance's action count; A may be NULL). */
+esdp_status esdp_batch_dims(const esdp_batch* b, int32_t* n, int32_t* T, int32_t* S, int32_t* K, int32_t* A);
+/* Backward pass of every instance on stream (NULL = the batch's own), synchronized; J[n] may be NULL. */
+esdp_status esdp_batch_backward(esdp_batch* b, void* stream, double* J);
+esdp_status esdp_batch_backward_async(esdp_batch* b, void* stream);
+/* J of every instance ([n], host) after a completed backward pass. */
+esdp_status esdp_batch_objective(esdp_batch* b, double* J);
+/* Policy pol_t of instance m ([K][S] int16, host). */
+esdp_status esdp_batch_policy(esdp_batch* b, int32_t m, int32_t t, int16_t* pol);
+/* V_1 of instance m ([K][S] FP64, host). */
+esdp_status esdp_batch_value1(esdp_batch* b, int32_t m, double* V1);
+/* n_paths lottery-mode paths per instance (a7): instance m draws with Philox key seed + m, exactly the
+ * paths of esdp_simulate_dev(seed + m) on a context of its own; per-path profits to
+ * out_dev[m * n_paths + path] (device).  Enqueued on stream, not synchronized. */
+esdp_status esdp_batch_simulate_dev(esdp_batch* b, int64_t n_paths, uint64_t seed, double* out_dev, void* stream);
+/* Kernel launches of one batch backward pass. */
+esdp_status esdp_batch_launch_count(const esdp_batch* b, int64_t* n);
+void esdp_batch_destroy(esdp_batch* b);
+/* Message of the last failing call on b (b == NULL: last esdp_create_batch failure of this thread). */
+const char* esdp_batch_last_error(const esdp_batch* b);
+
 #ifdef __cplusplus
 }
 #endif

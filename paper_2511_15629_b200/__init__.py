@@ -21,7 +21,7 @@ __all__ = [
     "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_load_async", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_destroy",
-    "esdp_last_error", "ESDP_PROFILE", "ESDP_FORCE_BRUTE", "esdp_stencil_kind", "Solver", "EXPORTED_SYMBOLS",
+    "esdp_last_error", "ESDP_PROFILE", "ESDP_FORCE_BRUTE", "esdp_stencil_kind", "Solver", "Batch", "EXPORTED_SYMBOLS",
 ]
 
 ESDP_OK, ESDP_E_CONFIG, ESDP_E_DATA, ESDP_E_INTERNAL, ESDP_E_STATE, ESDP_E_CUDA, ESDP_E_NCCL, ESDP_E_NOMEM = range(8)
@@ -42,6 +42,9 @@ EXPORTED_SYMBOLS = [
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
     "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
+    "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
+    "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
+    "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -100,6 +103,17 @@ def _load():
         "esdp_partition": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
         "esdp_last_error": ([ctx], ctypes.c_char_p),
+        "esdp_create_batch": ([ctypes.POINTER(esdp_problem), ctypes.c_int32, ctypes.POINTER(_vp)], ctypes.c_int),
+        "esdp_batch_dims": ([ctx, _i32p, _i32p, _i32p, _i32p, _i32p], ctypes.c_int),
+        "esdp_batch_backward": ([ctx, _vp, _dp], ctypes.c_int),
+        "esdp_batch_backward_async": ([ctx, _vp], ctypes.c_int),
+        "esdp_batch_objective": ([ctx, _dp], ctypes.c_int),
+        "esdp_batch_policy": ([ctx, ctypes.c_int32, ctypes.c_int32, _i16p], ctypes.c_int),
+        "esdp_batch_value1": ([ctx, ctypes.c_int32, _dp], ctypes.c_int),
+        "esdp_batch_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
+        "esdp_batch_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "esdp_batch_destroy": ([ctx], None),
+        "esdp_batch_last_error": ([ctx], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -359,3 +373,85 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+class Batch:
+    """A batch of instances sharing one price model (esdp_create_batch, cfg5): one graph for all."""
+
+    def __init__(self, insts):
+        keep = []
+        probs = (esdp_problem * len(insts))()
+        for j, inst in enumerate(insts):   # every instance's own arrays: the library checks they match
+            act = _f64(getattr(inst, "actions", None))
+            g = _f64(getattr(inst, "g", None))
+            lam, P, pi = _f64(inst.lam), _f64(inst.P), _f64(inst.pi)
+            keep += [act, g, lam, P, pi]
+            probs[j] = esdp_problem(int(inst.T), int(inst.K), float(inst.pbar), float(inst.sbar), float(inst.s0),
+                                    float(inst.eta_c), float(inst.eta_d), float(inst.delta),
+                                    0 if act is None else int(act.shape[0]), _p(act), _p(lam), _p(P), _p(pi),
+                                    int(getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR)), _p(g), 0)
+        out = _vp()
+        st = lib.esdp_create_batch(probs, len(insts), ctypes.byref(out))
+        if st != ESDP_OK:
+            m = lib.esdp_batch_last_error(None)
+            raise EsdpError(st, "esdp_create_batch", m.decode() if m else "")
+        self.b = out.value
+        n, T, S, K = (ctypes.c_int32() for _ in range(4))
+        A = (ctypes.c_int32 * len(insts))()
+        lib.esdp_batch_dims(self.b, ctypes.byref(n), ctypes.byref(T), ctypes.byref(S), ctypes.byref(K), A)
+        self.n, self.T, self.S, self.K = n.value, T.value, S.value, K.value
+        self.A = list(A)
+
+    def _check(self, st, what):
+        if st != ESDP_OK:
+            m = lib.esdp_batch_last_error(self.b)
+            raise EsdpError(st, what, m.decode() if m else "")
+
+    def backward(self, stream=None):
+        J = np.zeros(self.n)
+        self._check(lib.esdp_batch_backward(self.b, _stream_ptr(stream), _p(J)), "esdp_batch_backward")
+        return J
+
+    def backward_async(self, stream=None):
+        self._check(lib.esdp_batch_backward_async(self.b, _stream_ptr(stream)), "esdp_batch_backward_async")
+
+    def objective(self):
+        J = np.zeros(self.n)
+        self._check(lib.esdp_batch_objective(self.b, _p(J)), "esdp_batch_objective")
+        return J
+
+    def policy(self, m, t):
+        out = np.zeros((self.K, self.S), np.int16)
+        self._check(lib.esdp_batch_policy(self.b, int(m), int(t), _p(out, _i16p)), "esdp_batch_policy")
+        return out
+
+    def value1(self, m):
+        out = np.zeros((self.K, self.S))
+        self._check(lib.esdp_batch_value1(self.b, int(m), _p(out)), "esdp_batch_value1")
+        return out
+
+    def simulate_dev(self, n_paths, seed, out_ptr, stream=None):
+        self._check(lib.esdp_batch_simulate_dev(self.b, int(n_paths), ctypes.c_uint64(int(seed)), out_ptr,
+                                                _stream_ptr(stream)), "esdp_batch_simulate_dev")
+
+    def launch_count(self):
+        n = ctypes.c_int64()
+        self._check(lib.esdp_batch_launch_count(self.b, ctypes.byref(n)), "esdp_batch_launch_count")
+        return n.value
+
+    def close(self):
+        if self.b:
+            lib.esdp_batch_destroy(self.b)
+            self.b = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "window.cuh"
 #include "persistent.cuh"
+#include "batch.cuh"
 
 using namespace esdp;
 
@@ -509,6 +510,31 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
                 W_of(c, t), rows, K, S, c->ld);
 }
 
+// Stage-invariant parameters of the window and brute-force stencils (W/V/pol/lambda set per launch).
+WinParams win_params(const esdp_ctx* c) {
+  WinParams wp{};
+  wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
+  wp.singles = c->d_singles; wp.live = c->d_live;
+  wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
+  wp.A = c->A; wp.S = c->S; wp.K = c->k_cnt; wp.rank1 = c->rank1; wp.ld = c->ld;
+  wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
+  wp.o_min = c->o_min; wp.o_max = c->o_max;
+  wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
+  wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
+  wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
+  wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  return wp;
+}
+
+StencilParams stencil_params(const esdp_ctx* c) {
+  StencilParams prm{};
+  prm.act = c->d_act; prm.g = c->d_g;
+  prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
+  prm.A = c->A; prm.S = c->S; prm.K = c->k_cnt; prm.kind = c->kind; prm.rank1 = c->rank1;
+  prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
+  return prm;
+}
+
 // The max-plus stencil of stage t: V_t, pol_t from W_t (window or brute force).
 cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute) {
   const int S = c->S;
@@ -518,27 +544,13 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
   int16_t* pol = c->d_pol + ((size_t)(t - 1) * c->Kp + c->k_lo) * S;
   const double* lam = c->d_lambda + (size_t)(t - 1) * c->K + c->k_lo;
   if (c->use_window && !force_brute) {
-    WinParams wp;
+    WinParams wp = win_params(c);
     wp.W = Wt; wp.V = V_of(c, t) + (size_t)c->k_lo * c->ld; wp.pol = pol; wp.lambda_t = lam;
-    wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
-    wp.singles = c->d_singles; wp.live = c->d_live;
-    wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
-    wp.A = c->A; wp.S = S; wp.K = K; wp.rank1 = c->rank1; wp.ld = c->ld;
-    wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
-    wp.o_min = c->o_min; wp.o_max = c->o_max;
-    wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
-    wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
-    wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
-    wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
     return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
   }
-  StencilParams prm;
+  StencilParams prm = stencil_params(c);
   prm.W = Wt; prm.V = V_of(c, t) + (size_t)c->k_lo * c->ld; prm.pol = pol; prm.lambda_t = lam;
-  prm.act = c->d_act;
   prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + ((size_t)(t - 1) * c->K + c->k_lo) * c->A : c->d_g;
-  prm.w = c->d_w; prm.omw = c->d_omw; prm.off = c->d_off; prm.segs = c->d_segs; prm.nseg = (int)c->segs.size();
-  prm.A = c->A; prm.S = S; prm.K = K; prm.kind = c->kind; prm.rank1 = c->rank1;
-  prm.o_min = c->o_min; prm.o_span = c->o_max - c->o_min; prm.ld = c->ld;
   return launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl, prm);
 }
 
@@ -549,21 +561,8 @@ cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
 
 PersistParams persist_params(esdp_ctx* c) {
   PersistParams pp;
-  StencilParams& sp = pp.sp;
-  sp.act = c->d_act; sp.w = c->d_w; sp.omw = c->d_omw; sp.off = c->d_off; sp.segs = c->d_segs;
-  sp.nseg = (int)c->segs.size(); sp.A = c->A; sp.S = c->S; sp.K = c->K; sp.kind = c->kind; sp.rank1 = c->rank1;
-  sp.o_min = c->o_min; sp.o_span = c->o_max - c->o_min; sp.ld = c->ld; sp.g = c->d_g;
-  WinParams& wp = pp.wp;
-  wp.act = c->d_act; wp.w = c->d_w; wp.omw = c->d_omw; wp.off = c->d_off;
-  wp.singles = c->d_singles; wp.live = c->d_live;
-  wp.nsingle = (int)c->singles.size(); wp.nlive = (int)c->live_list.size();
-  wp.A = c->A; wp.S = c->S; wp.K = c->K; wp.rank1 = c->rank1; wp.ld = c->ld;
-  wp.a_z = c->a_z; wp.Lc = c->Lc; wp.Ld = c->Ld; wp.pc = c->pc; wp.pd = c->pd;
-  wp.o_min = c->o_min; wp.o_max = c->o_max;
-  wp.delta = c->delta; wp.eta_c = c->eta_c; wp.eta_d = c->eta_d; wp.pbar = c->pbar;
-  wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
-  wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
-  wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  pp.sp = stencil_params(c);
+  pp.wp = win_params(c);
   pp.use_window = c->use_window;
   pp.T = c->T; pp.K = c->K; pp.S = c->S; pp.A = c->A; pp.ld = c->ld; pp.rows = (int)w_rows(c);
   pp.rank1 = c->rank1; pp.kind = c->kind; pp.keep = keep(c) ? 1 : 0;
@@ -797,7 +796,8 @@ esdp_status capture_graph(esdp_ctx* c) {
 
 extern "C" {
 
-static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out);
+static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out,
+                               bool tables_only = false);
 
 esdp_status esdp_create(const esdp_problem* pr, esdp_ctx** out) { return create_impl(pr, 1, 0, nullptr, out); }
 
@@ -825,7 +825,10 @@ esdp_status esdp_create_dist(const esdp_problem* pr, int32_t world, int32_t rank
   return create_impl(pr, world, rank, nccl_id, out);
 }
 
-static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out) {
+// tables_only: an instance of a batch (esdp_create_batch) -- parameters, action grid and per-action
+// tables only; the shared inputs, the value buffers and the graph belong to the batch.
+static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t rank, const void* nccl_id, esdp_ctx** out,
+                               bool tables_only) {
   g_create_error.clear();
   if (!pr || !out) return fail(nullptr, ESDP_E_CONFIG, "null argument");
   *out = nullptr;
@@ -872,9 +875,12 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     c->act.assign(pr->actions, pr->actions + pr->A);
   }
   c->A = (int)c->act.size();
-  {
+  if (!tables_only) {
     esdp_status st = validate_data(c, pr->lambda, pr->P, pr->pi, pr->g);
     if (st != ESDP_OK) { g_create_error = c->err; delete c; return st; }
+  } else if (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
+    for (int a = 0; a < c->A; ++a)
+      if (!std::isfinite(pr->g[a])) { fail(c, ESDP_E_DATA, "g[%d] is not finite", a); g_create_error = c->err; delete c; return ESDP_E_DATA; }
   }
   build_tables(c, pr->g);
 
@@ -886,14 +892,16 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     return bail(ESDP_E_CUDA);
   }
   const size_t T = c->T, K = c->K, S = c->S, A = c->A;
-  TRY(dev_alloc(c, &c->d_lambda, T * K));
-  TRY(dev_alloc(c, &c->d_P, c->rank1 ? 1 : (T - 1) * K * K));
-  TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
-  TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
-  TRY(dev_alloc(c, &c->d_cdf1, K));
   c->G = std::max<int>(64, 4 * (int)K);   // guide buckets per cdf row (most of them pure: one load per draw)
-  TRY(dev_alloc(c, &c->d_guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
-  TRY(dev_alloc(c, &c->d_guide1, (size_t)c->G));
+  if (!tables_only) {
+    TRY(dev_alloc(c, &c->d_lambda, T * K));
+    TRY(dev_alloc(c, &c->d_P, c->rank1 ? 1 : (T - 1) * K * K));
+    TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
+    TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
+    TRY(dev_alloc(c, &c->d_cdf1, K));
+    TRY(dev_alloc(c, &c->d_guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
+    TRY(dev_alloc(c, &c->d_guide1, (size_t)c->G));
+  }
   TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
   TRY(dev_alloc(c, &c->d_act, A));
   TRY(dev_alloc(c, &c->d_w, A));
@@ -902,6 +910,33 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   TRY(dev_alloc(c, &c->d_segs, c->segs.size()));
   const size_t LD = c->ld;
   const size_t KP = c->Kp;
+  if (tables_only) {   // per-action tables and the stencil plan; the batch owns everything else
+    TRY(dev_alloc(c, &c->d_singles, c->singles.size()));
+    TRY(dev_alloc(c, &c->d_live, c->live_list.size()));
+    TRY(dev_alloc(c, &c->d_gfit, 6));
+    fit_g(c, pr->g, c->gfit);
+    if ((!c->singles.empty() && cudaMemcpy(c->d_singles, c->singles.data(), c->singles.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) ||
+        cudaMemcpy(c->d_live, c->live_list.data(), c->live_list.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_act, c->act.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_w, c->w.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_omw, c->omw.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_off, c->off.data(), A * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_segs, c->segs.data(), c->segs.size() * sizeof(Seg), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G && cudaMemcpy(c->d_g, pr->g, A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->kind == ESDP_PAYOFF_LINEAR && cudaMemset(c->d_g, 0, A * sizeof(double)) != cudaSuccess)) {
+      fail(c, ESDP_E_CUDA, "upload of the action tables failed");
+      return bail(ESDP_E_CUDA);
+    }
+    c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
+    if (c->use_window) {
+      c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min);
+      if (c->window_smem > 200 * 1024) c->use_window = 0;
+    }
+    if (c->stencil_smem > 227 * 1024) { fail(c, ESDP_E_CONFIG, "action span too wide for shared memory"); return bail(ESDP_E_CONFIG); }
+    *out = c;
+    return ESDP_OK;
+  }
   TRY(dev_alloc(c, &c->d_V, keep(c) ? T * KP * LD : 2 * KP * LD));
   TRY(dev_alloc(c, &c->d_W, keep(c) ? T * w_rows(c) * LD : w_rows(c) * LD));
   // padding columns are never read as values; zero them once so no stale bits are staged
@@ -1365,6 +1400,340 @@ void esdp_destroy(esdp_ctx* c) {
 }
 
 const char* esdp_last_error(const esdp_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+// ------------------------------------------------------------------------------------------------
+// Batch contexts (cfg5): see batch.cuh and include/esdp.h.
+// ------------------------------------------------------------------------------------------------
+}  // extern "C"
+
+struct esdp_batch {
+  int n = 0, T = 0, K = 0, S = 0, ld = 0, rank1 = 0, G = 0;
+  std::vector<esdp_ctx*> inst;        // per-instance parameters and action tables (tables_only contexts)
+  double *d_lambda = nullptr, *d_P = nullptr, *d_pi = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
+  int16_t *d_guide = nullptr, *d_guide1 = nullptr;
+  double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr;   // V [2][K][n][ld], W [rows][n][ld]
+  int16_t* d_pol = nullptr;                                // [n][T][K][S]
+  BatchInst* d_bi = nullptr;
+  int* d_widx = nullptr;                                   // window-plan instances
+  int nwin = 0;
+  std::vector<int> brute;                                  // instances on the brute-force stencil
+  size_t win_smem = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t launches = 0;
+  bool solved = false;
+  std::string err;
+};
+
+namespace {
+
+esdp_status bfail(esdp_batch* b, esdp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (b) b->err = buf; else g_create_error = buf;
+  return st;
+}
+#define BCUDA(b, call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return bfail(b, ESDP_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+esdp_status balloc(esdp_batch* b, T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) return bfail(b, ESDP_E_NOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+  return ESDP_OK;
+}
+
+void batch_free(esdp_batch* b) {
+  if (b->graph) cudaGraphExecDestroy(b->graph);
+  void* ps[] = {b->d_lambda, b->d_P, b->d_pi, b->d_cdf, b->d_cdf1, b->d_guide, b->d_guide1, b->d_V, b->d_W,
+                b->d_J, b->d_pol, b->d_bi, b->d_widx};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (esdp_ctx* c : b->inst) esdp_destroy(c);
+  if (b->stream) cudaStreamDestroy(b->stream);
+}
+
+// The batch's backward pass on stream s: per stage one expectation over [K] x [n ld], one window launch
+// over every window-plan instance, one brute-force launch per other instance; then every J.
+esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
+  const int T = b->T, K = b->K, S = b->S, n = b->n;
+  const size_t NL = (size_t)n * b->ld;                  // row stride of V and W
+  const int rows = b->rank1 ? 1 : K;
+  int64_t launches = 0;
+  bool after_kernel = false;
+  auto V_at = [&](int t) { return b->d_V + (size_t)((t - 1) & 1) * K * NL; };
+  for (int t = T; t >= 1; --t) {
+    if (t == T) {
+      BCUDA(b, cudaMemsetAsync(b->d_W, 0, rows * NL * sizeof(double), s));   // W_T = 0
+      after_kernel = false;
+    } else {
+      const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
+      cudaError_t e;
+      if (!b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
+        const int ncb = (int)((NL + kDC * 16 - 1) / (kDC * 16)), nrb = (K + kDR * 8 - 1) / (kDR * 8);
+        e = launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, after_kernel,
+                   Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ncb);
+      } else {
+        dim3 grid((unsigned)((NL + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
+        e = launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, after_kernel, Pt,
+                   (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL);
+      }
+      if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch contraction: %s", cudaGetErrorString(e));
+      after_kernel = true;
+      ++launches;
+    }
+    const double* lam = b->d_lambda + (size_t)(t - 1) * K;
+    const size_t pol_inst = (size_t)T * K * S, pol_stage = (size_t)(t - 1) * K * S;
+    if (b->nwin > 0) {
+      cudaError_t e = launch(window_batch_kernel, dim3((S + kWinTile - 1) / kWinTile, K, b->nwin), dim3(kWinThreads),
+                             b->win_smem, s, after_kernel, (const BatchInst*)b->d_bi, (const int*)b->d_widx,
+                             (const double*)b->d_W, V_at(t), b->d_pol, pol_inst, pol_stage, lam, b->ld, (int)NL, b->rank1);
+      if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch window stencil: %s", cudaGetErrorString(e));
+      ++launches;
+    }
+    for (int m : b->brute) {
+      esdp_ctx* c = b->inst[m];
+      StencilParams prm = stencil_params(c);
+      prm.W = b->d_W + (size_t)m * b->ld; prm.V = V_at(t) + (size_t)m * b->ld;
+      prm.pol = b->d_pol + (size_t)m * pol_inst + pol_stage; prm.lambda_t = lam;
+      prm.ld = (int)NL; prm.K = K; prm.rank1 = b->rank1;
+      cudaError_t e = launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s,
+                             false, prm);
+      if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch stencil: %s", cudaGetErrorString(e));
+      ++launches;
+    }
+    after_kernel = b->brute.empty();
+  }
+  {
+    cudaError_t e = launch(objective_batch_kernel, dim3(n), dim3(128), 2 * sizeof(double) * K, s, after_kernel,
+                           (const BatchInst*)b->d_bi, (const double*)V_at(1), (const double*)b->d_pi, K, b->ld, (int)NL,
+                           b->d_J);
+    if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch objective: %s", cudaGetErrorString(e));
+    ++launches;
+  }
+  b->launches = launches;
+  return ESDP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch** out) {
+  g_create_error.clear();
+  if (!probs || !out || n < 1) return bfail(nullptr, ESDP_E_CONFIG, "null argument or n < 1");
+  *out = nullptr;
+  const esdp_problem& p0 = probs[0];
+  for (int m = 0; m < n; ++m) {
+    const esdp_problem& q = probs[m];
+    if (q.T != p0.T || q.K != p0.K || q.sbar != p0.sbar || q.delta != p0.delta || (q.P == nullptr) != (p0.P == nullptr))
+      return bfail(nullptr, ESDP_E_CONFIG, "instance %d: T, K, sbar, delta and the price model must match instance 0", m);
+    if (q.payoff_kind == ESDP_PAYOFF_TABLE)
+      return bfail(nullptr, ESDP_E_CONFIG, "instance %d: TABLE payoffs are not supported in a batch", m);
+    if (!q.lambda || !q.pi || (q.payoff_kind != ESDP_PAYOFF_LINEAR && !q.g))
+      return bfail(nullptr, ESDP_E_CONFIG, "instance %d: lambda, pi (and g) are required", m);
+    const size_t TK = (size_t)q.T * q.K;
+    const bool same = std::memcmp(q.lambda, p0.lambda, TK * sizeof(double)) == 0 &&
+                      std::memcmp(q.pi, p0.pi, (q.P ? (size_t)q.K : TK) * sizeof(double)) == 0 &&
+                      (!q.P || q.P == p0.P || std::memcmp(q.P, p0.P, (size_t)(q.T - 1) * q.K * q.K * sizeof(double)) == 0);
+    if (!same) return bfail(nullptr, ESDP_E_CONFIG, "instance %d: lambda, P and pi must equal instance 0's (shared price model)", m);
+  }
+  esdp_batch* b = new esdp_batch();
+  auto bail = [&](esdp_status st) { if (b->err.size()) g_create_error = b->err; batch_free(b); delete b; return st; };
+#define BTRY(x) do { esdp_status st_ = (x); if (st_ != ESDP_OK) return bail(st_); } while (0)
+  b->n = n;
+  for (int m = 0; m < n; ++m) {
+    esdp_problem q = probs[m];
+    q.flags &= ~(uint32_t)(ESDP_KEEP_VALUES | ESDP_PROFILE | ESDP_PERSIST);
+    esdp_ctx* c = nullptr;
+    esdp_status st = create_impl(&q, 1, 0, nullptr, &c, true);
+    if (st != ESDP_OK) {
+      b->err = "instance " + std::to_string(m) + ": " + g_create_error;
+      return bail(st);
+    }
+    b->inst.push_back(c);
+  }
+  esdp_ctx* c0 = b->inst[0];
+  b->T = c0->T; b->K = c0->K; b->S = c0->S; b->ld = c0->ld; b->rank1 = c0->rank1; b->G = c0->G;
+  {   // the shared inputs, validated once (as esdp_create does)
+    esdp_status st = validate_data(c0, p0.lambda, p0.P, p0.pi, p0.g);
+    if (st != ESDP_OK) { b->err = c0->err; return bail(st); }
+  }
+  if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(bfail(b, ESDP_E_CUDA, "cannot create a CUDA stream"));
+  const size_t T = b->T, K = b->K, S = b->S, NL = (size_t)n * b->ld, G = b->G;
+  BTRY(balloc(b, &b->d_lambda, T * K));
+  BTRY(balloc(b, &b->d_P, b->rank1 ? 1 : (T - 1) * K * K));
+  BTRY(balloc(b, &b->d_pi, b->rank1 ? T * K : K));
+  BTRY(balloc(b, &b->d_cdf, b->rank1 ? T * K : (T - 1) * K * K));
+  BTRY(balloc(b, &b->d_cdf1, K));
+  BTRY(balloc(b, &b->d_guide, (b->rank1 ? T : (T - 1) * K) * G));
+  BTRY(balloc(b, &b->d_guide1, G));
+  BTRY(balloc(b, &b->d_V, 2 * K * NL));
+  BTRY(balloc(b, &b->d_W, (b->rank1 ? 1 : K) * NL));
+  BTRY(balloc(b, &b->d_pol, (size_t)n * T * K * S));
+  BTRY(balloc(b, &b->d_J, (size_t)n));
+  BTRY(balloc(b, &b->d_bi, (size_t)n));
+  BTRY(balloc(b, &b->d_widx, (size_t)n));
+  cudaStream_t s = b->stream;
+  cudaMemsetAsync(b->d_V, 0, 2 * K * NL * sizeof(double), s);
+  cudaMemsetAsync(b->d_W, 0, (b->rank1 ? 1 : K) * NL * sizeof(double), s);
+  BCUDA(b, cudaMemcpyAsync(b->d_lambda, p0.lambda, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (b->rank1) {
+    BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
+    cdf_kernel<<<cdf_blocks((int64_t)T), kCdfWarps * 32, 0, s>>>(b->d_pi, (int64_t)T, (int)K, (int)G, b->d_cdf, b->d_guide);
+  } else {
+    BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, K * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (T > 1) {
+      BCUDA(b, cudaMemcpyAsync(b->d_P, p0.P, (T - 1) * K * K * sizeof(double), cudaMemcpyHostToDevice, s));
+      const int64_t nr = (int64_t)(T - 1) * K;
+      cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(b->d_P, nr, (int)K, (int)G, b->d_cdf, b->d_guide);
+    }
+  }
+  cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(b->d_pi, 1, (int)K, (int)G, b->d_cdf1, b->d_guide1);
+  BCUDA(b, cudaGetLastError());
+  // per-instance parameters
+  std::vector<BatchInst> hbi((size_t)n);
+  std::vector<int> widx;
+  for (int m = 0; m < n; ++m) {
+    esdp_ctx* c = b->inst[m];
+    BatchInst& x = hbi[m];
+    std::memset(&x, 0, sizeof x);
+    x.wp = win_params(c);
+    x.wp.K = (int)K;
+    SimParams& sp = x.sim;
+    sp.pol = b->d_pol + (size_t)m * T * K * S; sp.cdf = b->d_cdf; sp.cdf1 = b->d_cdf1; sp.lambda = b->d_lambda;
+    sp.guide = b->d_guide; sp.guide1 = b->d_guide1; sp.G = (int)G;
+    sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
+    sp.T = (int)T; sp.K = (int)K; sp.S = (int)S; sp.A = c->A; sp.rank1 = b->rank1; sp.kind = c->kind; sp.Kp = (int)K;
+    sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
+    x.f0 = c->f0; x.on_grid = c->on_grid; x.w0 = c->w0;
+    if (c->use_window) {
+      widx.push_back(m);
+      b->win_smem = std::max(b->win_smem, c->window_smem);
+    } else {
+      b->brute.push_back(m);
+      if (c->stencil_smem > 48 * 1024)
+        cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->stencil_smem);
+    }
+  }
+  b->nwin = (int)widx.size();
+  BCUDA(b, cudaMemcpyAsync(b->d_bi, hbi.data(), n * sizeof(BatchInst), cudaMemcpyHostToDevice, s));
+  if (!widx.empty()) BCUDA(b, cudaMemcpyAsync(b->d_widx, widx.data(), widx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  BCUDA(b, cudaStreamSynchronize(s));
+  if (b->win_smem > 48 * 1024)
+    BCUDA(b, cudaFuncSetAttribute(window_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->win_smem));
+  if (contract_dmma2_smem(K) > 48 * 1024 && contract_dmma2_smem(K) <= 200 * 1024)
+    cudaFuncSetAttribute(contract_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K));
+  if (contract_smem_bytes(K) > 48 * 1024)
+    cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
+  if (2 * sizeof(double) * K > 48 * 1024)
+    cudaFuncSetAttribute(objective_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
+  {   // capture the whole batch backward once
+    cudaGraph_t g = nullptr;
+    BCUDA(b, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    esdp_status est = batch_enqueue(b, s);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); return bail(est); }
+    if (ce != cudaSuccess) return bail(bfail(b, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce)));
+    ce = cudaGraphInstantiate(&b->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return bail(bfail(b, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)));
+  }
+#undef BTRY
+  *out = b;
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_dims(const esdp_batch* b, int32_t* n, int32_t* T, int32_t* S, int32_t* K, int32_t* A) {
+  if (!b) return ESDP_E_STATE;
+  if (n) *n = b->n;
+  if (T) *T = b->T;
+  if (S) *S = b->S;
+  if (K) *K = b->K;
+  if (A) for (int m = 0; m < b->n; ++m) A[m] = b->inst[m]->A;
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_backward_async(esdp_batch* b, void* stream) {
+  if (!b) return ESDP_E_STATE;
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  BCUDA(b, cudaGraphLaunch(b->graph, s));
+  b->solved = true;
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_objective(esdp_batch* b, double* J) {
+  if (!b || !J) return ESDP_E_STATE;
+  if (!b->solved) return bfail(b, ESDP_E_STATE, "no backward pass has run");
+  BCUDA(b, cudaMemcpy(J, b->d_J, b->n * sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_backward(esdp_batch* b, void* stream, double* J) {
+  if (!b) return ESDP_E_STATE;
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  esdp_status st = esdp_batch_backward_async(b, s);
+  if (st != ESDP_OK) return st;
+  BCUDA(b, cudaStreamSynchronize(s));
+  return J ? esdp_batch_objective(b, J) : ESDP_OK;
+}
+
+esdp_status esdp_batch_policy(esdp_batch* b, int32_t m, int32_t t, int16_t* pol) {
+  if (!b || !pol) return ESDP_E_STATE;
+  if (!b->solved) return bfail(b, ESDP_E_STATE, "no backward pass has run");
+  if (m < 0 || m >= b->n || t < 1 || t > b->T) return bfail(b, ESDP_E_STATE, "instance %d / stage %d out of range", m, t);
+  const size_t KS = (size_t)b->K * b->S;
+  BCUDA(b, cudaMemcpy(pol, b->d_pol + ((size_t)m * b->T + (t - 1)) * KS, KS * sizeof(int16_t), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_value1(esdp_batch* b, int32_t m, double* V1) {
+  if (!b || !V1) return ESDP_E_STATE;
+  if (!b->solved) return bfail(b, ESDP_E_STATE, "no backward pass has run");
+  if (m < 0 || m >= b->n) return bfail(b, ESDP_E_STATE, "instance %d out of range", m);
+  const size_t NL = (size_t)b->n * b->ld;   // stage 1 lives in ping-pong slot 0
+  BCUDA(b, cudaMemcpy2D(V1, b->S * sizeof(double), b->d_V + (size_t)m * b->ld, NL * sizeof(double), b->S * sizeof(double),
+                        b->K, cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_simulate_dev(esdp_batch* b, int64_t n_paths, uint64_t seed, double* out_dev, void* stream) {
+  if (!b || !out_dev) return ESDP_E_STATE;
+  if (!b->solved) return bfail(b, ESDP_E_STATE, "no backward pass has run");
+  if (n_paths < 1) return bfail(b, ESDP_E_STATE, "n_paths must be >= 1");
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  int amax = 0;
+  for (esdp_ctx* c : b->inst) amax = std::max(amax, c->A);
+  const size_t sm = sim_smem_bytes(amax);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  simulate_batch_kernel<<<dim3((unsigned)((n_paths + 127) / 128), b->n), 128, sm, s>>>(b->d_bi, n_paths, seed, out_dev);
+  BCUDA(b, cudaGetLastError());
+  return ESDP_OK;
+}
+
+esdp_status esdp_batch_launch_count(const esdp_batch* b, int64_t* n) {
+  if (!b || !n) return ESDP_E_STATE;
+  *n = b->launches;
+  return ESDP_OK;
+}
+
+void esdp_batch_destroy(esdp_batch* b) {
+  if (!b) return;
+  batch_free(b);
+  delete b;
+}
+
+const char* esdp_batch_last_error(const esdp_batch* b) { return b ? b->err.c_str() : g_create_error.c_str(); }
+
+
 
 }  // extern "C"
 

@@ -789,8 +789,9 @@ struct SimParams {
   double w0;
 };
 
-__global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
-  extern __shared__ __align__(16) double ssm[];   // per-action tables: act, w, g (kind 1), off
+// One block of paths: blockIdx.x * blockDim.x + threadIdx.x (ssm: the per-action tables).
+__device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, uint64_t seed, double* __restrict__ out,
+                                               double* ssm) {
   double* s_act = ssm;
   double* s_w = s_act + sp.A;
   double* s_g = s_w + sp.A;
@@ -828,6 +829,11 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, 
     k = kn;
   }
   out[path] = profit;
+}
+
+__global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, uint64_t seed, double* __restrict__ out) {
+  extern __shared__ __align__(16) double ssm[];   // per-action tables: act, w, g (kind 1), off
+  simulate_block(sp, n, seed, out, ssm);
 }
 
 inline size_t sim_smem_bytes(int A) { return (size_t)A * (3 * sizeof(double) + sizeof(int)) + 16; }

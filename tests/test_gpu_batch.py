@@ -1,0 +1,92 @@
+"""GPU parity of batch contexts (esdp_create_batch, cfg5): every instance of a batch -- one graph, one
+expectation launch over the stacked values and one window launch over all instances per stage -- is
+bit-identical to the oracle on that instance alone (J, V_1, every policy), and its simulated paths are
+those of a context of its own."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from helpers import to_oracle
+
+pytestmark = pytest.mark.gpu
+
+import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
+
+
+def _check_batch(insts, nthreads=16):
+    with E.Batch(insts) as b:
+        J = b.backward()
+        for m, inst in enumerate(insts):
+            ref = oracle.backward(to_oracle(inst), nthreads=nthreads)
+            assert J[m] == ref.J, (m, J[m], ref.J)
+            assert np.array_equal(b.value1(m), ref.V[0]), m
+            for t in range(1, inst.T + 1):
+                assert np.array_equal(b.policy(m, t), ref.pol[t - 1]), (m, t)
+        J2 = b.backward()
+        assert np.array_equal(J, J2)
+        return b.A
+
+
+@pytest.mark.parametrize("rank1", [False, True])
+def test_batch_cfg5_sample(rank1):
+    """Six cfg5 storage configurations (different pbar/delta, eta -> different action grids) on a short
+    cfg2 price chain."""
+    idx = [0, 37, 300, 511, 777, 1023]
+    insts = workloads.cfg5_instances(idx, T=12, K=10)
+    if rank1:
+        base = workloads.cfg2(T=12, K=10, rank1=True)
+        for x in insts:
+            x.P, x.pi = None, base.pi
+            x.lam = base.lam
+    A = _check_batch(insts)
+    assert len(set(A)) > 1
+
+
+def test_batch_mixed_plans_and_payoffs():
+    """A batch mixing window-plan instances, a brute-force instance (too few actions per side), an
+    affine degradation payoff (window) and a non-affine one (brute), plus an off-grid s0."""
+    base = workloads.cfg1("b")
+    insts = []
+    for j, (pbar, eta, s0) in enumerate([(9.5, 0.9, 0.0), (1.5, 0.95, 50.0), (20.0, 0.85, 33.3), (9.5, 0.9, 10.0)]):
+        x = workloads.Instance(f"mix{j}", base.T, base.K, pbar, base.sbar, s0, eta, eta, base.delta, base.lam, base.P,
+                               base.pi)
+        insts.append(x)
+    act3 = oracle.actions(to_oracle(insts[3]))
+    insts[3].payoff_kind = workloads.PAYOFF_LINEAR_MINUS_G
+    insts[3].g = 2.0 * np.abs(act3) + 5.0 * (act3 != 0)
+    act0 = oracle.actions(to_oracle(insts[0]))
+    insts[0].payoff_kind = workloads.PAYOFF_LINEAR_MINUS_G
+    insts[0].g = workloads.random_g(3, len(act0), 4.0)
+    _check_batch(insts)
+
+
+def test_batch_simulation_matches_single_contexts():
+    import torch
+    insts = workloads.cfg5_instances([5, 400, 900], T=16, K=12)
+    n_paths = 3000
+    with E.Batch(insts) as b:
+        b.backward()
+        out = torch.zeros(len(insts) * n_paths, dtype=torch.float64, device="cuda")
+        b.simulate_dev(n_paths, 77, out.data_ptr())
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().reshape(len(insts), n_paths)
+    for m, inst in enumerate(insts):
+        with E.Solver(inst, keep_values=False) as s:
+            s.backward()
+            per, _, _ = s.simulate(n_paths, seed=77 + m)
+        assert np.array_equal(got[m], per), m
+
+
+def test_batch_rejects_mismatched_price_models():
+    a, b = workloads.cfg5_instances([1, 2], T=6, K=5)
+    b.lam = b.lam + 1.0
+    with pytest.raises(E.EsdpError) as e:
+        E.Batch([a, b])
+    assert e.value.status == E.ESDP_E_CONFIG
+    c = workloads.cfg5_instances([3], T=6, K=5)[0]
+    c.payoff_kind = workloads.PAYOFF_TABLE
+    c.g = np.zeros((6, 5, 10))
+    with pytest.raises(E.EsdpError) as e:
+        E.Batch([a, c])
+    assert e.value.status == E.ESDP_E_CONFIG

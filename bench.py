@@ -348,11 +348,12 @@ def run_ours(args):
 
 
 def run_sweep(args):
-    """cfg5: a batch of storage configurations (different pbar, eta -> different action grids) solved
-    concurrently, one context per instance on its own CUDA stream; each instance = backward + 1024
-    simulated paths.  Latency-bound single instances overlap, so the GPU fills up."""
+    """cfg5: a batch of storage configurations (different pbar, eta -> different action grids) over one
+    price model, solved by one batch context (esdp_create_batch); each instance = backward + 1024
+    simulated paths.  Ranks take disjoint instance ranges (weak scaling, no data-path collective)."""
     import numpy as np
     import torch
+    import torch.distributed as dist
     import workloads
     import paper_2511_15629_b200 as E
     rank = int(os.environ.get("RANK", "0"))
@@ -360,61 +361,64 @@ def run_sweep(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.instances
     idx = [rank * n + j for j in range(n)]     # instance sharding across ranks (no communication)
     insts = workloads.cfg5_instances(idx)
-    solvers = [E.Solver(x, keep_values=False) for x in insts]
-    streams = [torch.cuda.Stream(device=dev) for _ in solvers]
-    master = torch.cuda.Stream(device=dev)
+    batch = E.Batch(insts, force_brute=args.stencil == "brute")   # one graph: one expectation + one stencil launch per stage
+    stream = torch.cuda.Stream(device=dev)
     paths = 1024
-    outs = [torch.empty(paths, dtype=torch.float64, device=dev) for _ in solvers]
-    cells = sum(s.T * s.S * s.K * s.A for s in solvers)
+    out_d = torch.empty(n * paths, dtype=torch.float64, device=dev)
+    cells = sum(batch.T * batch.S * batch.K * a for a in batch.A)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(j):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(master)
-        ends = []
-        for s, st, o in zip(solvers, streams, outs):
-            st.wait_event(e0)
-            E.esdp_backward_async(s.ctx, st.cuda_stream)
-            E.esdp_simulate_dev(s.ctx, paths, 17 + j, o.data_ptr(), st.cuda_stream)
-            ev = torch.cuda.Event()
-            ev.record(st)
-            ends.append(ev)
-        for ev in ends:
-            master.wait_event(ev)
-        e1.record(master)
+        e0.record(stream)
+        batch.backward_async(stream.cuda_stream)
+        batch.simulate_dev(paths, 17 + j, out_d.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
         return e0, e1
 
     for j in range(args.warmup):
         step(j)
     torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     ms = 0.0
     for j in range(args.steps):
-        with torch.cuda.stream(master):
-            flush.fill_(float(j))
+        with torch.cuda.stream(stream):
+            flush.fill_(float(j))              # L2 flush between timed steps (outside the events)
         e0, e1 = step(j)
-        master.synchronize()
+        stream.synchronize()
         ms += e0.elapsed_time(e1)
     clk = clocks.stop()
     ms /= args.steps
-    As = [s.A for s in solvers]
-    out = {"metric": "DP cell-updates/sec (T*S*K*A)", "value": cells / (ms * 1e-3), "unit": "cell-updates/s",
+    t_all = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    ms = float(t_all.item())
+    # end to end: the per-instance storage parameters are host data that the batch is built from; the
+    # shared price model is uploaded with it, and the J of every instance comes back
+    J = batch.objective()
+    As = list(batch.A)
+    launches = (batch.launch_count() + 1) * args.steps
+    batch.close()
+    out = {"metric": "DP cell-updates/sec (T*S*K*A)", "value": cells * world / (ms * 1e-3), "unit": "cell-updates/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (cfg2 price chain; cfg5 storage sweep)",
-           "config": {"workload": "cfg5 sweep sample: %d storage configurations per GPU solved concurrently "
+           "config": {"workload": "cfg5 sweep sample: %d storage configurations per GPU in one batch context "
                                   "(pbar/delta in [10.42, 99], eta in [0.80, 0.99]; T=288, S=1001, K=100; A=%d..%d), "
                                   "1024 simulated paths each" % (n, min(As), max(As)),
-                      "instances_per_gpu": n, "l2": "flushed between timed steps"},
-           "gpu_launches": sum(E.esdp_launch_count(s.ctx) + 1 for s in solvers) * args.steps,
+                      "instances_per_gpu": n, "l2": "flushed between timed steps",
+                      "plan": "esdp_create_batch: per stage one [K] x [n ld] expectation + one window launch"},
+           "gpu_launches": launches, "J_mean": float(np.mean(J)),
            "clocks": clk}
-    for s in solvers:
-        s.close()
     return out if rank == 0 else None
 
 

@@ -378,7 +378,7 @@ class Solver:
 class Batch:
     """A batch of instances sharing one price model (esdp_create_batch, cfg5): one graph for all."""
 
-    def __init__(self, insts):
+    def __init__(self, insts, force_brute=False):
         keep = []
         probs = (esdp_problem * len(insts))()
         for j, inst in enumerate(insts):   # every instance's own arrays: the library checks they match
@@ -389,7 +389,8 @@ class Batch:
             probs[j] = esdp_problem(int(inst.T), int(inst.K), float(inst.pbar), float(inst.sbar), float(inst.s0),
                                     float(inst.eta_c), float(inst.eta_d), float(inst.delta),
                                     0 if act is None else int(act.shape[0]), _p(act), _p(lam), _p(P), _p(pi),
-                                    int(getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR)), _p(g), 0)
+                                    int(getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR)), _p(g),
+                                    ESDP_FORCE_BRUTE if force_brute else 0)
         out = _vp()
         st = lib.esdp_create_batch(probs, len(insts), ctypes.byref(out))
         if st != ESDP_OK:

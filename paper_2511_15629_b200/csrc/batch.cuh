@@ -13,6 +13,7 @@ namespace esdp {
 
 struct BatchInst {
   WinParams wp;          // window plan (stage-invariant fields; ld = the batch's row stride)
+  StencilParams sp;      // brute-force plan (stage-invariant fields)
   SimParams sim;         // simulation tables of this instance (pol = its [T][K][S] slab)
   int f0, on_grid;       // s0 on the grid (objective, Eq. 6 at t = 0)
   double w0;
@@ -51,6 +52,32 @@ __global__ void __launch_bounds__(kWinThreads, 4) window_batch_kernel(const Batc
   pdl_wait();                          // W_t is the previous contraction's output
   __syncthreads();
   window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
+  pdl_trigger();
+}
+
+// grid (tiles, K, number of brute-force instances): the brute-force stencil of kernels.cuh per instance.
+__global__ void __launch_bounds__(kStencilWarps * 32) stencil_batch_kernel(const BatchInst* __restrict__ bi,
+                                                                           const int* __restrict__ idx,
+                                                                           const double* Wt, double* Vt,
+                                                                           int16_t* pol_base, size_t pol_inst,
+                                                                           size_t pol_stage, const double* lam_t,
+                                                                           int ld, int row_stride, int rank1) {
+  extern __shared__ double smem[];
+  __shared__ StencilParams p;
+  const int m = __ldg(idx + blockIdx.z);
+  copy_struct(p, bi[m].sp);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    p.W = Wt + (size_t)m * ld;
+    p.V = Vt + (size_t)m * ld;
+    p.pol = pol_base + (size_t)m * pol_inst + pol_stage;
+    p.lambda_t = lam_t;
+    p.ld = row_stride;
+    p.rank1 = rank1;
+  }
+  pdl_wait();                          // W_t is the previous contraction's output
+  __syncthreads();
+  stencil_item(p, blockIdx.y, blockIdx.x * kTile, smem);
   pdl_trigger();
 }
 

@@ -1415,9 +1415,9 @@ struct esdp_batch {
   int16_t* d_pol = nullptr;                                // [n][T][K][S]
   BatchInst* d_bi = nullptr;
   int* d_widx = nullptr;                                   // window-plan instances
-  int nwin = 0;
-  std::vector<int> brute;                                  // instances on the brute-force stencil
-  size_t win_smem = 0;
+  int* d_bidx = nullptr;                                   // brute-force instances
+  int nwin = 0, nbrute = 0;
+  size_t win_smem = 0, brute_smem = 0;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t launches = 0;
@@ -1453,7 +1453,7 @@ esdp_status balloc(esdp_batch* b, T** p, size_t n) {
 void batch_free(esdp_batch* b) {
   if (b->graph) cudaGraphExecDestroy(b->graph);
   void* ps[] = {b->d_lambda, b->d_P, b->d_pi, b->d_cdf, b->d_cdf1, b->d_guide, b->d_guide1, b->d_V, b->d_W,
-                b->d_J, b->d_pol, b->d_bi, b->d_widx};
+                b->d_J, b->d_pol, b->d_bi, b->d_widx, b->d_bidx};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (esdp_ctx* c : b->inst) esdp_destroy(c);
@@ -1498,18 +1498,15 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch window stencil: %s", cudaGetErrorString(e));
       ++launches;
     }
-    for (int m : b->brute) {
-      esdp_ctx* c = b->inst[m];
-      StencilParams prm = stencil_params(c);
-      prm.W = b->d_W + (size_t)m * b->ld; prm.V = V_at(t) + (size_t)m * b->ld;
-      prm.pol = b->d_pol + (size_t)m * pol_inst + pol_stage; prm.lambda_t = lam;
-      prm.ld = (int)NL; prm.K = K; prm.rank1 = b->rank1;
-      cudaError_t e = launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s,
-                             false, prm);
+    if (b->nbrute > 0) {
+      cudaError_t e = launch(stencil_batch_kernel, dim3((S + kTile - 1) / kTile, K, b->nbrute), dim3(kStencilWarps * 32),
+                             b->brute_smem, s, after_kernel && b->nwin == 0, (const BatchInst*)b->d_bi,
+                             (const int*)b->d_bidx, (const double*)b->d_W, V_at(t), b->d_pol, pol_inst, pol_stage, lam,
+                             b->ld, (int)NL, b->rank1);
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch stencil: %s", cudaGetErrorString(e));
       ++launches;
     }
-    after_kernel = b->brute.empty();
+    after_kernel = b->nbrute == 0;   // a PDL edge needs a single kernel predecessor
   }
   {
     cudaError_t e = launch(objective_batch_kernel, dim3(n), dim3(128), 2 * sizeof(double) * K, s, after_kernel,
@@ -1582,6 +1579,7 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   BTRY(balloc(b, &b->d_J, (size_t)n));
   BTRY(balloc(b, &b->d_bi, (size_t)n));
   BTRY(balloc(b, &b->d_widx, (size_t)n));
+  BTRY(balloc(b, &b->d_bidx, (size_t)n));
   cudaStream_t s = b->stream;
   cudaMemsetAsync(b->d_V, 0, 2 * K * NL * sizeof(double), s);
   cudaMemsetAsync(b->d_W, 0, (b->rank1 ? 1 : K) * NL * sizeof(double), s);
@@ -1601,13 +1599,15 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   BCUDA(b, cudaGetLastError());
   // per-instance parameters
   std::vector<BatchInst> hbi((size_t)n);
-  std::vector<int> widx;
+  std::vector<int> widx, bidx;
   for (int m = 0; m < n; ++m) {
     esdp_ctx* c = b->inst[m];
     BatchInst& x = hbi[m];
     std::memset(&x, 0, sizeof x);
     x.wp = win_params(c);
     x.wp.K = (int)K;
+    x.sp = stencil_params(c);
+    x.sp.K = (int)K;
     SimParams& sp = x.sim;
     sp.pol = b->d_pol + (size_t)m * T * K * S; sp.cdf = b->d_cdf; sp.cdf1 = b->d_cdf1; sp.lambda = b->d_lambda;
     sp.guide = b->d_guide; sp.guide1 = b->d_guide1; sp.G = (int)G;
@@ -1619,12 +1619,15 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
       widx.push_back(m);
       b->win_smem = std::max(b->win_smem, c->window_smem);
     } else {
-      b->brute.push_back(m);
-      if (c->stencil_smem > 48 * 1024)
-        cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->stencil_smem);
+      bidx.push_back(m);
+      b->brute_smem = std::max(b->brute_smem, c->stencil_smem);
     }
   }
   b->nwin = (int)widx.size();
+  b->nbrute = (int)bidx.size();
+  if (!bidx.empty()) BCUDA(b, cudaMemcpyAsync(b->d_bidx, bidx.data(), bidx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (b->brute_smem > 48 * 1024)
+    BCUDA(b, cudaFuncSetAttribute(stencil_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->brute_smem));
   BCUDA(b, cudaMemcpyAsync(b->d_bi, hbi.data(), n * sizeof(BatchInst), cudaMemcpyHostToDevice, s));
   if (!widx.empty()) BCUDA(b, cudaMemcpyAsync(b->d_widx, widx.data(), widx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   BCUDA(b, cudaStreamSynchronize(s));

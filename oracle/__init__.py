@@ -68,6 +68,7 @@ def lib():
         L.ref_philox4x32_10.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                         ctypes.POINTER(ctypes.c_uint32)]
         L.ref_simulate.argtypes = [P, _sp, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp]
+        L.ref_simulate_mode.argtypes = [P, _sp, _dp, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp]
         L.ref_stage.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _dp, _dp, _dp, _sp]
         L.ref_objective.argtypes = [P, _dp, _dp]
         _lib = L
@@ -230,4 +231,21 @@ def simulate(pr: Problem, pol: np.ndarray, n_paths: int, seed: int):
                             _ptr(per), ctypes.byref(m), ctypes.byref(v))
     if rc:
         raise OracleError(rc, "ref_simulate")
+    return per, m.value, v.value
+
+
+SIM_LOTTERY, SIM_PHYSICAL, SIM_CLEAR_BIDS = 0, 1, 2
+
+
+def simulate_mode(pr: Problem, pol: np.ndarray, W: np.ndarray, mode: int, n_paths: int, seed: int):
+    """ref_simulate_mode: lottery (pol), physical re-optimisation or bid clearing (W of every stage)."""
+    per = np.zeros(n_paths)
+    m = ctypes.c_double(); v = ctypes.c_double()
+    c = pr._c()
+    polc = np.ascontiguousarray(pol, dtype=np.int16)
+    Wc = np.ascontiguousarray(W, dtype=np.float64)
+    rc = lib().ref_simulate_mode(ctypes.byref(c), _ptr(polc, _sp), _ptr(Wc), int(mode), int(n_paths),
+                                 ctypes.c_uint64(seed), _ptr(per), ctypes.byref(m), ctypes.byref(v))
+    if rc:
+        raise OracleError(rc, "ref_simulate_mode")
     return per, m.value, v.value

@@ -482,3 +482,102 @@ int ref_simulate(const ref_problem* pr, const int16_t* pol, int64_t n_paths, uin
   free(act); free(off); free(w); free(omw); free(ilo); free(ihi);
   return REF_OK;
 }
+
+/* Physical-mode decision at real SoC s (energy units), stage t, price state k, from row W_t[k] (R25):
+ * every action a in ascending order, s' = s + F(p_a) (Eq. 2), feasible iff 0 <= s'/delta <= S-1 within
+ * 1e-9 (Eq. 4 on the real state), cand = payoff + W_t(s') with Alg. 1 line 7's interpolation at the
+ * off-grid index s'/delta; strict '>' keeps the smallest maximising index (R8). */
+static int32_t physical_action(const ref_problem* pr, int32_t S, int32_t A, const double* act, const double* Wrow,
+                               int32_t t, int32_t k, double s, double* s_next) {
+  int32_t best_a = -1;
+  double best = -INFINITY, best_s = s;
+  for (int32_t a = 0; a < A; ++a) {
+    double sn = s + transition_F(act[a], pr->eta_c, pr->eta_d);
+    double x = sn / pr->delta;
+    if (x < -GRID_TOL || x > (double)(S - 1) + GRID_TOL) continue;
+    double r = nearbyint(x);
+    double wint;
+    if (fabs(x - r) <= GRID_TOL) {
+      wint = Wrow[(int32_t)r];
+      sn = r * pr->delta;                     /* snapped to the grid */
+    } else {
+      double f = floor(x);
+      double w = x - f;
+      wint = ((1.0 - w) * Wrow[(int32_t)f]) + (w * Wrow[(int32_t)f + 1]);
+    }
+    double cand = payoff(pr, A, act, t, k, a) + wint;
+    if (cand > best) { best = cand; best_a = a; best_s = sn; }
+  }
+  *s_next = best_s;
+  return best_a;
+}
+
+int ref_simulate_mode(const ref_problem* pr, const int16_t* pol, const double* W, int32_t mode, int64_t n_paths,
+                      uint64_t seed, double* per_path, double* mean, double* var) {
+  if (mode == REF_SIM_LOTTERY) return ref_simulate(pr, pol, n_paths, seed, per_path, mean, var);
+  int32_t S, A;
+  int rc = ref_dims(pr, &S, &A);
+  if (rc) return rc;
+  if (n_paths < 1 || !W || (mode != REF_SIM_PHYSICAL && mode != REF_SIM_CLEAR_BIDS)) return REF_E_STATE;
+  if (mode == REF_SIM_CLEAR_BIDS && pr->payoff_kind == REF_PAYOFF_TABLE) return REF_E_STATE;
+  const int32_t T = pr->T, K = pr->K;
+  double* act = (double*)malloc(sizeof(double) * (size_t)A);
+  int32_t* off = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  double* w = (double*)malloc(sizeof(double) * (size_t)A);
+  double* omw = (double*)malloc(sizeof(double) * (size_t)A);
+  int32_t* ilo = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  int32_t* ihi = (int32_t*)malloc(sizeof(int32_t) * (size_t)A);
+  int16_t* vert = (int16_t*)malloc(sizeof(int16_t) * (size_t)A);
+  double* q = (double*)malloc(sizeof(double) * (size_t)A);
+  double* price = (double*)malloc(sizeof(double) * (size_t)A);
+  ref_actions(pr, act);
+  ref_tables(pr, off, w, omw, ilo, ihi);
+  const int64_t KS = (int64_t)K * S;
+  double x0 = pr->s0 / pr->delta;
+  double r0 = nearbyint(x0);
+  int on_grid = fabs(x0 - r0) <= GRID_TOL;
+  double f0 = floor(x0), w0 = x0 - f0;
+  int err = REF_OK;
+  for (int64_t path = 0; path < n_paths && !err; ++path) {
+    double u1, u2;
+    uniforms(seed, path, 0, &u1, &u2);
+    int32_t k = sample_cdf(pr->pi, K, u1);
+    int32_t i = on_grid ? (int32_t)r0 : (int32_t)f0 + (u2 < w0 ? 1 : 0);
+    double s = pr->s0;                                     /* physical mode: the real SoC */
+    double profit = 0.0;
+    for (int32_t t = 1; t <= T; ++t) {
+      uniforms(seed, path, t, &u1, &u2);
+      const double* Wrow = W + (int64_t)(t - 1) * KS + (int64_t)k * S;
+      int32_t a;
+      if (mode == REF_SIM_PHYSICAL) {
+        double sn;
+        a = physical_action(pr, S, A, act, Wrow, t, k, s, &sn);
+        if (a < 0) { err = REF_E_INTERNAL; break; }       /* the zero action is always feasible */
+        s = sn;
+      } else {
+        int32_t nv, rep;
+        rc = ref_bidcurve(pr, W, t, i, k, A, &nv, vert, q, price, &rep);
+        if (rc) { err = rc; break; }
+        a = vert[ref_clear(nv, price, pr->lambda[(int64_t)(t - 1) * K + k])];
+      }
+      profit = profit + payoff(pr, A, act, t, k, a);
+      if (mode == REF_SIM_CLEAR_BIDS) i = i + off[a] + ((w[a] > 0.0 && u1 < w[a]) ? 1 : 0);
+      if (t < T) {
+        const double* qk = pr->P ? pr->P + ((int64_t)(t - 1) * K + k) * K : pr->pi + (int64_t)t * K;
+        k = sample_cdf(qk, K, u2);
+      }
+    }
+    per_path[path] = profit;
+  }
+  if (!err) {
+    double sm = 0.0;
+    for (int64_t p = 0; p < n_paths; ++p) sm += per_path[p];
+    double m = sm / (double)n_paths;
+    double ss = 0.0;
+    for (int64_t p = 0; p < n_paths; ++p) ss += (per_path[p] - m) * (per_path[p] - m);
+    *mean = m;
+    *var = n_paths > 1 ? ss / (double)(n_paths - 1) : 0.0;
+  }
+  free(act); free(off); free(w); free(omw); free(ilo); free(ihi); free(vert); free(q); free(price);
+  return err;
+}

@@ -95,6 +95,19 @@ void ref_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 int ref_simulate(const ref_problem* pr, const int16_t* pol, int64_t n_paths, uint64_t seed,
                  double* per_path, double* mean, double* var);
 
+/* Simulation modes (SURVEY §8(a) a7 "take a = pol_t[k][i] (or clear the bid)"; §8(c) step 7 physical
+ * mode; R25/R26), same random numbers as ref_simulate:
+ *   REF_SIM_LOTTERY    = ref_simulate (pol; W unused);
+ *   REF_SIM_PHYSICAL   real SoC s (starts at s0): at every stage re-optimise over all actions,
+ *                      cand = payoff + W_t(s + F(p_a)) interpolated at the off-grid state, smallest
+ *                      maximising index, then s <- s + F(p_a*) (snapped to the grid within 1e-9);
+ *   REF_SIM_CLEAR_BIDS grid state i (lottery moves as in ref_simulate): the action is the bid curve
+ *                      of (t, i, k) from W_t cleared at lambda_{t,k} (ref_bidcurve + ref_clear).
+ * W: [T][K][S] (all stages; needed by the last two modes).  TABLE payoffs: CLEAR_BIDS -> REF_E_STATE. */
+enum { REF_SIM_LOTTERY = 0, REF_SIM_PHYSICAL = 1, REF_SIM_CLEAR_BIDS = 2 };
+int ref_simulate_mode(const ref_problem* pr, const int16_t* pol, const double* W, int32_t mode, int64_t n_paths,
+                      uint64_t seed, double* per_path, double* mean, double* var);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,3 +140,77 @@ def test_simulation_deterministic_path_equals_J():
     per, m, v = oracle.simulate(pr, sol.pol, 16, seed=1)
     assert np.all(np.abs(per - sol.J) <= 1e-9 * max(1.0, abs(sol.J)))
     assert v <= 1e-18 * max(1.0, sol.J ** 2)
+
+
+# ---- simulation modes (SURVEY §8(a) a7 "(or clear the bid)", §8(c) step 7 physical mode; R25/R26) ----
+
+@pytest.mark.parametrize("seed", range(6))
+def test_physical_mode_equals_lottery_on_the_lattice(seed):
+    """V21: with eta = 1 and integral pbar/delta every action lands on the grid, so re-optimising at
+    the real SoC is the policy lookup: the physical and lottery paths agree to the bit."""
+    inst = workloads.random_instance(300 + seed, T=6, K=1 + seed % 3, S_max=30, lattice=True)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    lot, _, _ = oracle.simulate(pr, sol.pol, 500, seed=9)
+    phy, _, _ = oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_PHYSICAL, 500, seed=9)
+    assert np.array_equal(lot, phy)
+
+
+def test_physical_mode_single_stage_closed_form():
+    """T = 1 (W_1 = 0): the physical decision at s0 = sbar is the largest feasible discharge,
+    min(pbar, sbar eta_d) (Eq. 1 and Eq. 4 on the real state); profit lambda times it."""
+    for eta, s0 in ((0.9, 3.0), (0.8, 1.0), (1.0, 2.0)):
+        inst = workloads.random_instance(5, T=1, K=1, S_max=6)
+        inst.eta_c = inst.eta_d = eta
+        inst.delta, inst.sbar, inst.s0, inst.pbar = 1.0, 5.0, s0, 2.0
+        inst.lam = np.array([[7.0]])
+        inst.pi = np.array([1.0])
+        inst.P = None if inst.P is None else np.zeros((0, 1, 1))
+        pr = to_oracle(inst)
+        sol = oracle.backward(pr)
+        act = oracle.actions(pr)
+        feas = [p for p in act if 0 <= s0 - (p / eta if p >= 0 else eta * p) <= 5.0]
+        per, _, _ = oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_PHYSICAL, 3, seed=1)
+        assert np.all(per == 7.0 * max(feas)), (per, feas)
+        assert max(feas) == pytest.approx(min(2.0, s0 * eta) if s0 * eta < 2.0 else max(a for a in act if a <= 2.0))
+
+
+def test_physical_mode_below_lp_bound():
+    """K = 1 deterministic prices, eta < 1: the physical schedule is a feasible continuous schedule,
+    so its profit never exceeds the LP optimum (scipy HiGHS)."""
+    from pins import lp_value
+    inst = workloads.random_instance(77, T=8, K=1, S_max=25, rank1=False)
+    inst.eta_c = inst.eta_d = 0.9
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    per, _, _ = oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_PHYSICAL, 4, seed=3)
+    lp, _ = lp_value(inst.lam[:, 0], inst.pbar, inst.sbar, inst.s0, 0.9, 0.9)
+    assert np.all(per <= lp + 1e-9 * max(1.0, abs(lp)))
+    assert np.all(per == per[0])          # deterministic prices: every path the same
+
+
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1"])
+def test_clear_bids_mode_follows_the_policy(name):
+    """Clearing the stage's bid curve at the realised price selects the hull vertex that maximises
+    lambda p + u (Eq. 12 / merit order) -- the argmax policy except on exact ties:
+    (almost) every path equals the lottery path, and the mean lies within 5 standard errors of J."""
+    inst = workloads.cfg1("b", rank1=name.endswith("rank1"))
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    n = 4000
+    lot, _, _ = oracle.simulate(pr, sol.pol, n, seed=21)
+    clr, m, v = oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_CLEAR_BIDS, n, seed=21)
+    assert np.mean(lot == clr) >= 0.99
+    assert abs(m - sol.J) <= 5 * np.sqrt(v / n) + 1e-9
+
+
+def test_clear_bids_mode_rejects_table_payoffs():
+    inst = workloads.random_instance(8, T=3, K=2, S_max=8)
+    pr0 = to_oracle(inst)
+    S, A = oracle.dims(pr0)
+    inst.payoff_kind = workloads.PAYOFF_TABLE
+    inst.g = workloads.random_table(8, inst.T, inst.K, A)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    with pytest.raises(oracle.OracleError):
+        oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_CLEAR_BIDS, 4, seed=1)

@@ -183,6 +183,23 @@ esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double*
 esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
                               void* stream);
 
+/* Simulation modes (SURVEY §8(a) a7 "take a = pol_t[k][i] (or clear the bid)"; §8(c) step 7;
+ * DESIGN.md R25/R26), with the same Philox draws as esdp_simulate:
+ *   ESDP_SIM_LOTTERY     the argmax policy on the grid, lottery moves at off-grid endpoints (= esdp_simulate);
+ *   ESDP_SIM_PHYSICAL    the real SoC s (from s0): every stage re-optimises over all actions with
+ *                        payoff + W_t(s + F(p_a)) interpolated at the off-grid index (Alg. 1 line 7),
+ *                        smallest maximising index; s <- s + F(p_a*) (snapped to the grid within 1e-9);
+ *   ESDP_SIM_CLEAR_BIDS  grid states with lottery moves; the action is the stage's bid curve at (t, i, k)
+ *                        cleared at the realised price lambda_{t,k} (merit order; ties to the
+ *                        larger quantity, R9).
+ * PHYSICAL and CLEAR_BIDS need ESDP_KEEP_VALUES and one GPU; CLEAR_BIDS rejects TABLE payoffs
+ * (ESDP_E_STATE).  Host variant: mean, var (sample), per_path[n_paths] (nullable), synchronized. */
+enum { ESDP_SIM_LOTTERY = 0, ESDP_SIM_PHYSICAL = 1, ESDP_SIM_CLEAR_BIDS = 2 };
+esdp_status esdp_simulate_mode(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int32_t mode, double* mean,
+                               double* var, double* per_path);
+esdp_status esdp_simulate_mode_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int32_t mode,
+                                   double* per_path_dev, void* stream);
+
 /* Execution plan: bit 0 = stencil (1 = exact sliding-window for the recombining grid with a linear
  * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent dataflow
  * kernel (else a CUDA graph of 2T kernels).  All plans give bit-identical results. */

@@ -33,6 +33,7 @@ ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
 ESDP_PERSIST = 32
 ESDP_DMMA_L2 = 64
+ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS = 0, 1, 2
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
@@ -42,6 +43,7 @@ EXPORTED_SYMBOLS = [
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
     "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
+    "esdp_simulate_mode", "esdp_simulate_mode_dev",
     "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
     "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
     "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error",
@@ -91,6 +93,8 @@ def _load():
         "esdp_bidcurves_dev": ([ctx, ctypes.c_int64, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
         "esdp_simulate": ([ctx, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp], ctypes.c_int),
         "esdp_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
+        "esdp_simulate_mode": ([ctx, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _dp, _dp, _dp], ctypes.c_int),
+        "esdp_simulate_mode_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _vp, _vp], ctypes.c_int),
         "esdp_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_kernel_times": ([ctx, _dp, _dp], ctypes.c_int),
         "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
@@ -280,6 +284,14 @@ def esdp_simulate(ctx, n_paths, seed, per_path=True):
     return out, m.value, v.value
 
 
+def esdp_simulate_mode(ctx, n_paths, seed, mode, per_path=True):
+    m, v = ctypes.c_double(), ctypes.c_double()
+    out = np.zeros(int(n_paths)) if per_path else None
+    _check(lib.esdp_simulate_mode(ctx, int(n_paths), ctypes.c_uint64(int(seed)), int(mode), ctypes.byref(m),
+                                  ctypes.byref(v), _p(out)), "esdp_simulate_mode", ctx)
+    return out, m.value, v.value
+
+
 def esdp_simulate_dev(ctx, n_paths, seed, per_path_ptr, stream=None):
     _check(lib.esdp_simulate_dev(ctx, int(n_paths), ctypes.c_uint64(int(seed)), per_path_ptr, _stream_ptr(stream)),
            "esdp_simulate_dev", ctx)
@@ -354,8 +366,10 @@ class Solver:
     def bidcurves(self, req, cap=None):
         return esdp_bidcurves(self.ctx, req, cap)
 
-    def simulate(self, n_paths, seed, per_path=True):
-        return esdp_simulate(self.ctx, n_paths, seed, per_path)
+    def simulate(self, n_paths, seed, per_path=True, mode=ESDP_SIM_LOTTERY):
+        if mode == ESDP_SIM_LOTTERY:
+            return esdp_simulate(self.ctx, n_paths, seed, per_path)
+        return esdp_simulate_mode(self.ctx, n_paths, seed, mode, per_path)
 
     def close(self):
         if self.ctx:

@@ -24,6 +24,7 @@
 #include "window.cuh"
 #include "persistent.cuh"
 #include "batch.cuh"
+#include "simmodes.cuh"
 
 using namespace esdp;
 
@@ -67,6 +68,10 @@ struct esdp_ctx {
   int* d_off = nullptr;
   Seg* d_segs = nullptr;
   double* d_gfit = nullptr;   // [6] affine fit of g on the window runs (window.cuh WinParams::gfit)
+  double* d_F = nullptr;      // [A] SoC change of each action (Eq. 2): physical simulation mode
+  std::vector<double> F;
+  int16_t* d_stack = nullptr; // bid-clearing simulation: [paths][A] hull stacks
+  int64_t stack_cap = 0;
   double gfit[6] = {0, 0, 0, 0, 0, 0};
   double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
   int16_t *d_guide = nullptr, *d_guide1 = nullptr;
@@ -293,9 +298,11 @@ void build_tables(esdp_ctx* c, const double* g) {
   c->off.assign(A, 0);
   c->w.assign(A, 0.0);
   c->omw.assign(A, 1.0);
+  c->F.assign(A, 0.0);
   for (int a = 0; a < A; ++a) {
     const double p = c->act[a];
     const double F = (p >= 0.0) ? -(p / c->eta_d) : -(c->eta_c * p);  // Eq. 2
+    c->F[a] = F;
     const double e = F / c->delta;
     const double r = std::nearbyint(e);
     if (std::fabs(e - r) <= kGridTol) {
@@ -400,7 +407,7 @@ void free_all(esdp_ctx* c) {
   if (c->use_ev) cudaEventDestroy(c->use_ev);
   if (c->copy) cudaStreamDestroy(c->copy);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -966,6 +973,8 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
   TRY(dev_alloc(c, &c->d_gfit, 6));
   if (cudaMemcpy(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload g fit"); return bail(ESDP_E_CUDA); }
+  TRY(dev_alloc(c, &c->d_F, A));
+  if (cudaMemcpy(c->d_F, c->F.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload F"); return bail(ESDP_E_CUDA); }
   if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_head, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_tables, cudaEventDisableTiming) != cudaSuccess ||
@@ -1287,6 +1296,67 @@ esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* m
     c->sim_cap = n_paths;
   }
   esdp_status st = esdp_simulate_dev(c, n_paths, seed, c->d_sim, c->stream);
+  if (st != ESDP_OK) return st;
+  reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, nullptr, c->d_red);
+  reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, c->d_red, c->d_red + 1);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  double h[2];
+  CUDA_OR_FAIL(c, cudaMemcpy(h, c->d_red, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (mean) *mean = h[0];
+  if (var) *var = n_paths > 1 ? h[1] / (double)(n_paths - 1) : 0.0;
+  if (per_path) CUDA_OR_FAIL(c, cudaMemcpy(per_path, c->d_sim, n_paths * sizeof(double), cudaMemcpyDeviceToHost));
+  return ESDP_OK;
+}
+
+esdp_status esdp_simulate_mode_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode, double* per_path_dev,
+                                   void* stream) {
+  if (!c) return ESDP_E_STATE;
+  if (mode == ESDP_SIM_LOTTERY) return esdp_simulate_dev(c, n_paths, seed, per_path_dev, stream);
+  if (mode != ESDP_SIM_PHYSICAL && mode != ESDP_SIM_CLEAR_BIDS) return fail(c, ESDP_E_STATE, "unknown simulation mode %d", mode);
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  if (n_paths < 1) return fail(c, ESDP_E_STATE, "n_paths must be >= 1");
+  if (!keep(c)) return fail(c, ESDP_E_STATE, "physical / bid-clearing simulation needs ESDP_KEEP_VALUES (W of every stage)");
+  if (c->world > 1) return fail(c, ESDP_E_STATE, "physical / bid-clearing simulation needs every W row (world == 1)");
+  if (mode == ESDP_SIM_CLEAR_BIDS && c->kind == ESDP_PAYOFF_TABLE)
+    return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
+  if (mode == ESDP_SIM_CLEAR_BIDS && n_paths * c->A > c->stack_cap) {
+    cudaFree(c->d_stack);
+    c->d_stack = nullptr;
+    c->stack_cap = 0;
+    if (dev_alloc(c, &c->d_stack, (size_t)n_paths * c->A)) return ESDP_E_NOMEM;
+    c->stack_cap = n_paths * c->A;
+  }
+  SimModeParams mp{};
+  SimParams& sp = mp.base;
+  sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
+  sp.guide = c->d_guide; sp.guide1 = c->d_guide1; sp.G = c->G;
+  sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
+  sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
+  sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
+  mp.W = c->d_W; mp.F = c->d_F; mp.omw = c->d_omw; mp.stack = c->d_stack;
+  mp.mode = mode; mp.wrows = (int)w_rows(c); mp.ld = c->ld; mp.delta = c->delta; mp.s0 = c->s0;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));
+  const size_t sm = simmode_smem_bytes(c->A);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_mode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  simulate_mode_kernel<<<(unsigned)((n_paths + kSimModeThreads - 1) / kSimModeThreads), kSimModeThreads, sm, s>>>(
+      mp, n_paths, seed, per_path_dev);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return mark_use(c, s);
+}
+
+esdp_status esdp_simulate_mode(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode, double* mean, double* var,
+                               double* per_path) {
+  if (!c) return ESDP_E_STATE;
+  if (n_paths > c->sim_cap) {
+    cudaFree(c->d_sim);
+    c->d_sim = nullptr;
+    c->sim_cap = 0;
+    if (dev_alloc(c, &c->d_sim, n_paths)) return ESDP_E_NOMEM;
+    c->sim_cap = n_paths;
+  }
+  esdp_status st = esdp_simulate_mode_dev(c, n_paths, seed, mode, c->d_sim, c->stream);
   if (st != ESDP_OK) return st;
   reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, nullptr, c->d_red);
   reduce_kernel<<<1, 1024, 0, c->stream>>>(c->d_sim, n_paths, c->d_red, c->d_red + 1);

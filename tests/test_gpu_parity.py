@@ -431,3 +431,41 @@ def test_state_errors():
             s.values(inst.T + 1)
         with pytest.raises(E.EsdpError):
             s.bidcurves(np.array([[1, 10_000, 0]]))
+
+
+@pytest.mark.parametrize("mode", ["physical", "clear"])
+@pytest.mark.parametrize("name", ["cfg1a", "cfg1b", "cfg1b-rank1", "cfg3", "random-g"])
+def test_simulation_modes_bitexact(name, mode):
+    """a7's other modes on the GPU equal the oracle path by path: physical re-optimisation at the real
+    SoC (off-grid interpolation of W_t) and bid-curve clearing at the realised price."""
+    if name == "cfg3":
+        base = workloads.cfg2(T=2, K=2)
+        inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=20, K=12)
+    elif name == "random-g":
+        inst = workloads.random_instance(61, T=6, K=3, S_max=200)
+        act = oracle.actions(to_oracle(inst))
+        inst.payoff_kind = workloads.PAYOFF_LINEAR_MINUS_G
+        inst.g = workloads.random_g(61, len(act), 3.0)
+        inst.s0 = inst.sbar * 0.37
+    else:
+        inst = workloads.cfg1(name[4], rank1=name.endswith("rank1"))
+        inst.s0 = inst.sbar * 0.5 + 0.3 * inst.delta          # off-grid start (physical mode's real SoC)
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr)
+    m = oracle.SIM_PHYSICAL if mode == "physical" else oracle.SIM_CLEAR_BIDS
+    n = 2500
+    want, wm, wv = oracle.simulate_mode(pr, ref.pol, ref.W, m, n, seed=31)
+    with _gpu(inst) as s:
+        s.backward()
+        got, gm, gv = s.simulate(n, 31, mode=E.ESDP_SIM_PHYSICAL if mode == "physical" else E.ESDP_SIM_CLEAR_BIDS)
+    assert np.array_equal(got, want)
+    assert gm == pytest.approx(wm, rel=1e-12)
+
+
+def test_simulation_modes_state_errors():
+    inst = workloads.cfg1("b")
+    with E.Solver(inst, keep_values=False) as s:
+        s.backward()
+        with pytest.raises(E.EsdpError) as e:
+            s.simulate(10, 1, mode=E.ESDP_SIM_PHYSICAL)
+        assert e.value.status == E.ESDP_E_STATE

@@ -43,7 +43,10 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms.  Started before the warm-up (the tool
+    needs ~0.1 s to start emitting); only the samples received between mark_begin() and mark_end() --
+    the timed region -- are used, widened to the 3 nearest samples when the region is shorter than
+    the sampling period (those fall in the adjacent warm-up / next step, the same load)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -66,7 +69,19 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_ready(self, extra_warmup, timeout=2.0):
+        """Extra (untimed) warm-up steps until the sampler emits, so that it covers the timed region."""
+        t = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t < timeout:
+            extra_warmup()
+
+    def mark_begin(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
@@ -78,7 +93,13 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = getattr(self, "t0", float("-inf"))
+        t1 = getattr(self, "t1", float("inf"))
+        inside = [x for x in self.lines if t0 <= x[0] <= t1 + 0.03]
+        if len(inside) < 3 and self.lines:
+            mid = 0.5 * (t0 + t1) if t0 > float("-inf") and t1 < float("inf") else self.lines[-1][0]
+            inside = sorted(self.lines, key=lambda x: abs(x[0] - mid))[:3]
+        for _, ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -199,16 +220,18 @@ def run_ours(args):
             marks[3].record(stream)
 
     launches_per_step = E.esdp_launch_count(solver.ctx) + (1 if n_bid and not fused else 0) + 1
+    clocks = ClockSampler(local)
+    clocks.start()
     with torch.cuda.stream(stream):
         for j in range(args.warmup):
             flush.fill_(float(j))
             step(j)
         stream.synchronize()
+        clocks.wait_ready(lambda: (flush.fill_(0.0), step(0), stream.synchronize()))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        clocks = ClockSampler(local)
-        clocks.start()
+        clocks.mark_begin()
         marks = [[ev() for _ in range(4)] for _ in range(args.steps)]
         part = np.zeros(3)
         phases = np.zeros(2)
@@ -219,6 +242,7 @@ def run_ours(args):
             m = marks[j]
             part += [m[0].elapsed_time(m[1]), m[1].elapsed_time(m[2]), m[2].elapsed_time(m[3])]
         torch.cuda.synchronize(dev)
+        clocks.mark_end()
         if world > 1:
             dist.barrier()
         clk = clocks.stop()
@@ -382,13 +406,15 @@ def run_sweep(args):
         e1.record(stream)
         return e0, e1
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for j in range(args.warmup):
         step(j)
     torch.cuda.synchronize(dev)
+    clocks.wait_ready(lambda: (step(0), stream.synchronize()))
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark_begin()
     ms = 0.0
     for j in range(args.steps):
         with torch.cuda.stream(stream):
@@ -396,6 +422,7 @@ def run_sweep(args):
         e0, e1 = step(j)
         stream.synchronize()
         ms += e0.elapsed_time(e1)
+    clocks.mark_end()
     clk = clocks.stop()
     ms /= args.steps
     t_all = torch.tensor([ms], dtype=torch.float64, device=dev)

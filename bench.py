@@ -282,17 +282,23 @@ def run_ours(args):
     m_, v_ = ctypes.c_double(), ctypes.c_double()
     Jh = ctypes.c_double()
     e2e_times = []
+    # pipelined steps through the public API: step j launches its solve, then validates and enqueues the
+    # upload of step j+1's inputs into the other input slot (it overlaps solve j), then simulates and
+    # reads the step's results back.  Every step carries one full H2D of inputs and its D2H.
+    load = lambda: E.lib.esdp_load_async(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
+    assert load() == 0, E.esdp_last_error(solver.ctx)
     for j in range(args.warmup + args.steps):
         if world > 1 and j == args.warmup:
             dist.barrier()
         t0 = time.perf_counter()
-        # validated, then uploaded on the copy stream in stage chunks that the backward waits for one by one
-        st = E.lib.esdp_load_async(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
-        assert st == 0, E.esdp_last_error(solver.ctx)
-        assert E.lib.esdp_backward(solver.ctx, sp, ctypes.byref(Jh)) == 0
+        assert E.lib.esdp_backward_async(solver.ctx, sp) == 0
         if n_bid and not fused:
             E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
                                  None, pr_d.data_ptr(), sp)
+        st = load()                                    # the next step's inputs (validated, chunked H2D)
+        assert st == 0, E.esdp_last_error(solver.ctx)
+        stream.synchronize()
+        assert E.lib.esdp_objective(solver.ctx, ctypes.byref(Jh)) == 0
         assert E.lib.esdp_simulate(solver.ctx, n_paths, 99 + j, ctypes.byref(m_), ctypes.byref(v_), None) == 0
         t1 = time.perf_counter()
         if j >= args.warmup:

@@ -114,16 +114,21 @@ esdp_status esdp_dims(const esdp_ctx* ctx, int32_t* T, int32_t* S, int32_t* A, i
 esdp_status esdp_actions(const esdp_ctx* ctx, double* actions);
 
 /* Re-upload the stochastic inputs from HOST memory (shapes as in esdp_problem; NULL keeps the
- * current array).  Validated like esdp_create.  Used for end-to-end runs where every solve
- * brings new prices.  Invalidates previous results. */
+ * newest array).  Validated like esdp_create (on error nothing changes).  Used for end-to-end runs
+ * where every solve brings new prices.  The inputs are double-buffered: a load fills the slot that
+ * the last launched backward pass does not read, and the next esdp_backward* switches to it; until
+ * then the results of the last backward (values, policy, bid curves, simulations) stay those of the
+ * previous inputs. */
 esdp_status esdp_load(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
                       const double* g);
 
 /* Same as esdp_load, but returns once the arrays are validated and their upload is enqueued (P in stage
- * chunks, highest stages first, on the context's copy stream); the next backward pass waits for each
- * chunk only where it needs it, so the host-to-device copy overlaps the solve.  The host arrays must
- * stay valid and unmodified until the next esdp_backward (or a synchronizing call after
- * esdp_backward_async) returns; pinned (page-locked) memory makes the copies asynchronous. */
+ * chunks, highest stages first, on the context's copy stream, after the device has finished the
+ * solve before last that read the target slot); the next backward pass waits for each chunk only
+ * where it needs it, so the host-to-device copy overlaps the running solve (pipelined steps) and the
+ * next one.  The host arrays must stay valid and unmodified until the next esdp_backward (or a
+ * synchronizing call after esdp_backward_async) returns; pinned (page-locked) memory makes the
+ * copies asynchronous. */
 esdp_status esdp_load_async(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
                             const double* g);
 

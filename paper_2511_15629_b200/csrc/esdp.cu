@@ -40,6 +40,16 @@ struct DevBuf {
 
 }  // namespace
 
+// One set of device inputs (double-buffered: a load fills the slot the running backward does not read).
+struct InputSlot {
+  double *lambda = nullptr, *P = nullptr, *pi = nullptr, *cdf = nullptr, *cdf1 = nullptr, *g = nullptr, *gfit = nullptr;
+  int16_t *guide = nullptr, *guide1 = nullptr;
+  cudaEvent_t ev_head = nullptr, ev_tables = nullptr, use_ev = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  bool use_pending = false;
+  double gfit_h[6] = {0, 0, 0, 0, 0, 0};
+};
+
 struct esdp_ctx {
   // problem
   int T = 0, K = 0, S = 0, A = 0, kind = 0, rank1 = 0;
@@ -91,8 +101,13 @@ struct esdp_ctx {
   // first (ev_head), then P in stage chunks T-1.. (chunk_ev[j] covers stages [chunk_lo[j], chunk_hi[j]]);
   // the backward graph waits on these events (external event-wait nodes), so a load overlaps the solve
   cudaStream_t copy = nullptr;
-  cudaEvent_t ev_head = nullptr, use_ev = nullptr, ev_tables = nullptr;
-  bool use_pending = false;    // use_ev recorded after the last enqueue that reads the inputs
+  // two input slots: `active` holds the inputs of the last launched backward (read by the simulation,
+  // the bid curves ...), `pending` (or -1) the inputs of the latest load that no backward has used yet.
+  // The fields d_lambda ... d_gfit, ev_head, chunk_ev, ev_tables alias the slot selected by select_slot.
+  InputSlot slot[2];
+  int active = 0, pending = -1;
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+  cudaEvent_t ev_head = nullptr, ev_tables = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   std::vector<int> chunk_lo, chunk_hi;
   cudaGraphExec_t graph = nullptr;
@@ -126,6 +141,14 @@ struct esdp_ctx {
 };
 
 namespace {
+
+// Point the input aliases (d_lambda ... d_gfit, ev_head, chunk_ev, ev_tables) at slot sl.
+void select_slot(esdp_ctx* c, int sl) {
+  InputSlot& x = c->slot[sl];
+  c->d_lambda = x.lambda; c->d_P = x.P; c->d_pi = x.pi; c->d_cdf = x.cdf; c->d_cdf1 = x.cdf1;
+  c->d_guide = x.guide; c->d_guide1 = x.guide1; c->d_g = x.g; c->d_gfit = x.gfit;
+  c->ev_head = x.ev_head; c->ev_tables = x.ev_tables; c->chunk_ev = x.chunk_ev;
+}
 
 esdp_status fail(esdp_ctx* c, esdp_status s, const char* fmt, ...) {
   char buf[512];
@@ -395,16 +418,26 @@ esdp_status dev_alloc(esdp_ctx* c, T** p, size_t n) {
 }
 
 void free_all(esdp_ctx* c) {
-  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (cudaGraphExec_t g : c->graphs)
+    if (g) cudaGraphExecDestroy(g);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->slot[0].lambda) {   // full context: the input aliases point into the slots
+    for (InputSlot& x : c->slot) {
+      void* sp[] = {x.lambda, x.P, x.pi, x.cdf, x.cdf1, x.g, x.gfit, x.guide, x.guide1};
+      for (void* p : sp)
+        if (p) cudaFree(p);
+      for (cudaEvent_t e : x.chunk_ev) cudaEventDestroy(e);
+      if (x.ev_head) cudaEventDestroy(x.ev_head);
+      if (x.ev_tables) cudaEventDestroy(x.ev_tables);
+      if (x.use_ev) cudaEventDestroy(x.use_ev);
+    }
+    c->d_lambda = c->d_P = c->d_pi = c->d_cdf = c->d_cdf1 = c->d_g = c->d_gfit = nullptr;
+    c->d_guide = c->d_guide1 = nullptr;
+  }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->fb_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
-  for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
-  if (c->ev_head) cudaEventDestroy(c->ev_head);
-  if (c->ev_tables) cudaEventDestroy(c->ev_tables);
-  if (c->use_ev) cudaEventDestroy(c->use_ev);
   if (c->copy) cudaStreamDestroy(c->copy);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
                 c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
@@ -414,57 +447,82 @@ void free_all(esdp_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
-// Enqueue the upload of the given inputs (NULL = keep) on the copy stream, after every enqueued use of
-// the previous inputs; lambda / pi / g and their tables first (ev_head), then P and its sampling tables in
-// stage chunks in the order the backward needs them (chunk_ev).  Does not synchronize.
-esdp_status upload(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
-  const size_t TK = (size_t)c->T * c->K;
+// Enqueue the upload of the given inputs into slot dst on the copy stream, after every enqueued use of
+// that slot; a NULL array keeps the data of slot src (device-to-device copy when src != dst).  lambda /
+// pi / g and their tables first (ev_head), then P in stage chunks in the order the backward needs them
+// (chunk_ev), then the simulation's sampling tables of P (ev_tables).  Does not synchronize.
+esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const double* P, const double* pi,
+                   const double* g) {
+  const size_t TK = (size_t)c->T * c->K, K = c->K, G = c->G;
+  InputSlot& d = c->slot[dst];
+  const InputSlot& o = c->slot[src];
+  const bool copy_old = src != dst;
   cudaStream_t s = c->copy;
-  if (c->use_pending) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->use_ev, 0));
-  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_lambda, lambda, TK * sizeof(double), cudaMemcpyHostToDevice, s));
-  if (!c->rank1) {
-    if (pi) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, c->K * sizeof(double), cudaMemcpyHostToDevice, s));
-  } else if (pi) {
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_pi, pi, TK * sizeof(double), cudaMemcpyHostToDevice, s));
-    // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
-    cdf_kernel<<<cdf_blocks(c->T), kCdfWarps * 32, 0, s>>>(c->d_pi, c->T, c->K, c->G, c->d_cdf, c->d_guide);
-  }
-  if (pi) cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(c->d_pi, 1, c->K, c->G, c->d_cdf1, c->d_guide1);  // pi_1 (row 0 in rank-1)
-  CUDA_OR_FAIL(c, cudaGetLastError());
-  if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, c->A * sizeof(double), cudaMemcpyHostToDevice, s));
-    // a later g that is not affine on the runs only widens eps (more canonical fallbacks, same result)
-    if (c->use_window) {
-      fit_g(c, g, c->gfit);
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice, s));
+  const auto h2d = cudaMemcpyHostToDevice;
+  const auto d2d = cudaMemcpyDeviceToDevice;
+  if (d.use_pending) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, d.use_ev, 0));
+  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, lambda, TK * sizeof(double), h2d, s));
+  else if (copy_old) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, o.lambda, TK * sizeof(double), d2d, s));
+  const size_t npi = c->rank1 ? TK : K;
+  if (pi) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, pi, npi * sizeof(double), h2d, s));
+    if (c->rank1)   // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
+      cdf_kernel<<<cdf_blocks(c->T), kCdfWarps * 32, 0, s>>>(d.pi, c->T, c->K, c->G, d.cdf, d.guide);
+    cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(d.pi, 1, c->K, c->G, d.cdf1, d.guide1);  // pi_1 (row 0 in rank-1)
+    CUDA_OR_FAIL(c, cudaGetLastError());
+  } else if (copy_old) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, o.pi, npi * sizeof(double), d2d, s));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf1, o.cdf1, K * sizeof(double), d2d, s));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide1, o.guide1, G * sizeof(int16_t), d2d, s));
+    if (c->rank1) {
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, TK * sizeof(double), d2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (size_t)c->T * G * sizeof(int16_t), d2d, s));
     }
   }
-  if (g && c->kind == ESDP_PAYOFF_TABLE)
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_g, g, TK * c->A * sizeof(double), cudaMemcpyHostToDevice, s));
-  CUDA_OR_FAIL(c, cudaEventRecord(c->ev_head, s));
+  const size_t ng = c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : (size_t)c->A;
+  if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, g, c->A * sizeof(double), h2d, s));
+    // a later g that is not affine on the runs only widens eps (more canonical fallbacks, same result)
+    if (c->use_window) fit_g(c, g, d.gfit_h);
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.gfit, d.gfit_h, sizeof d.gfit_h, h2d, s));
+  } else if (g && c->kind == ESDP_PAYOFF_TABLE) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, g, ng * sizeof(double), h2d, s));
+  } else if (copy_old) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, o.g, ng * sizeof(double), d2d, s));
+    std::memcpy(d.gfit_h, o.gfit_h, sizeof d.gfit_h);
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.gfit, o.gfit, sizeof d.gfit_h, d2d, s));
+  }
+  CUDA_OR_FAIL(c, cudaEventRecord(d.ev_head, s));
   // P chunks: the backward waits only for the copy; the sampling tables (needed by the simulation
   // alone) are built after it and signalled by ev_tables
-  for (size_t j = 0; j < c->chunk_ev.size(); ++j) {
-    if (!c->rank1 && P) {
-      const size_t r0 = (size_t)(c->chunk_lo[j] - 1) * c->K, nr = (size_t)(c->chunk_hi[j] - c->chunk_lo[j] + 1) * c->K;
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_P + r0 * c->K, P + r0 * c->K, nr * c->K * sizeof(double), cudaMemcpyHostToDevice, s));
+  for (size_t j = 0; j < d.chunk_ev.size(); ++j) {
+    if (!c->rank1 && (P || copy_old)) {
+      const size_t r0 = (size_t)(c->chunk_lo[j] - 1) * K, nr = (size_t)(c->chunk_hi[j] - c->chunk_lo[j] + 1) * K;
+      if (P) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.P + r0 * K, P + r0 * K, nr * K * sizeof(double), h2d, s));
+      else CUDA_OR_FAIL(c, cudaMemcpyAsync(d.P + r0 * K, o.P + r0 * K, nr * K * sizeof(double), d2d, s));
     }
-    CUDA_OR_FAIL(c, cudaEventRecord(c->chunk_ev[j], s));
+    CUDA_OR_FAIL(c, cudaEventRecord(d.chunk_ev[j], s));
   }
-  if (!c->rank1 && P && c->T > 1) {
+  if (!c->rank1 && c->T > 1) {
     const int64_t nr = (int64_t)(c->T - 1) * c->K;
-    cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(c->d_P, nr, c->K, c->G, c->d_cdf, c->d_guide);
-    CUDA_OR_FAIL(c, cudaGetLastError());
+    if (P) {
+      cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(d.P, nr, c->K, c->G, d.cdf, d.guide);
+      CUDA_OR_FAIL(c, cudaGetLastError());
+    } else if (copy_old) {
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, (size_t)nr * K * sizeof(double), d2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (size_t)nr * G * sizeof(int16_t), d2d, s));
+    }
   }
-  CUDA_OR_FAIL(c, cudaEventRecord(c->ev_tables, s));
-  c->solved = false;
+  CUDA_OR_FAIL(c, cudaEventRecord(d.ev_tables, s));
   return ESDP_OK;
 }
 
-// After enqueueing work that reads the inputs on stream s: later uploads wait for it.
+// After enqueueing work that reads the active slot's inputs on stream s: later uploads into that slot
+// wait for it.
 esdp_status mark_use(esdp_ctx* c, cudaStream_t s) {
-  CUDA_OR_FAIL(c, cudaEventRecord(c->use_ev, s));
-  c->use_pending = true;
+  InputSlot& x = c->slot[c->active];
+  CUDA_OR_FAIL(c, cudaEventRecord(x.use_ev, s));
+  x.use_pending = true;
   return ESDP_OK;
 }
 
@@ -785,17 +843,22 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   return ESDP_OK;
 }
 
+// One graph per input slot (the inputs' device pointers and upload events are baked into a graph).
 esdp_status capture_graph(esdp_ctx* c) {
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
-  cudaGraph_t g = nullptr;
-  CUDA_OR_FAIL(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  esdp_status est = enqueue_backward(c, c->stream);
-  cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-  if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); return est; }
-  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
-  ce = cudaGraphInstantiate(&c->graph, g, 0);
-  cudaGraphDestroy(g);
-  if (ce != cudaSuccess) return fail(c, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+  for (int sl = 0; sl < 2; ++sl) {
+    if (c->graphs[sl]) { cudaGraphExecDestroy(c->graphs[sl]); c->graphs[sl] = nullptr; }
+    select_slot(c, sl);
+    cudaGraph_t g = nullptr;
+    CUDA_OR_FAIL(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    esdp_status est = enqueue_backward(c, c->stream);
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (est != ESDP_OK) { if (g) cudaGraphDestroy(g); select_slot(c, c->active); return est; }
+    if (ce != cudaSuccess) { select_slot(c, c->active); return fail(c, ESDP_E_CUDA, "graph capture: %s", cudaGetErrorString(ce)); }
+    ce = cudaGraphInstantiate(&c->graphs[sl], g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) { select_slot(c, c->active); return fail(c, ESDP_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
+  }
+  select_slot(c, c->active);
   return ESDP_OK;
 }
 
@@ -900,16 +963,24 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   }
   const size_t T = c->T, K = c->K, S = c->S, A = c->A;
   c->G = std::max<int>(64, 4 * (int)K);   // guide buckets per cdf row (most of them pure: one load per draw)
-  if (!tables_only) {
-    TRY(dev_alloc(c, &c->d_lambda, T * K));
-    TRY(dev_alloc(c, &c->d_P, c->rank1 ? 1 : (T - 1) * K * K));
-    TRY(dev_alloc(c, &c->d_pi, c->rank1 ? T * K : K));
-    TRY(dev_alloc(c, &c->d_cdf, c->rank1 ? T * K : (T - 1) * K * K));
-    TRY(dev_alloc(c, &c->d_cdf1, K));
-    TRY(dev_alloc(c, &c->d_guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
-    TRY(dev_alloc(c, &c->d_guide1, (size_t)c->G));
+  if (!tables_only) {   // two input slots (double-buffered loads); the aliases follow select_slot
+    for (InputSlot& x : c->slot) {
+      TRY(dev_alloc(c, &x.lambda, T * K));
+      TRY(dev_alloc(c, &x.P, c->rank1 ? 1 : (T - 1) * K * K));
+      TRY(dev_alloc(c, &x.pi, c->rank1 ? T * K : K));
+      TRY(dev_alloc(c, &x.cdf, c->rank1 ? T * K : (T - 1) * K * K));
+      TRY(dev_alloc(c, &x.cdf1, K));
+      TRY(dev_alloc(c, &x.guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
+      TRY(dev_alloc(c, &x.guide1, (size_t)c->G));
+      TRY(dev_alloc(c, &x.g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
+      TRY(dev_alloc(c, &x.gfit, 6));
+      cudaMemset(x.g, 0, (c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A) * sizeof(double));
+      cudaMemset(x.gfit, 0, 6 * sizeof(double));
+    }
+    select_slot(c, 0);
+  } else {
+    TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
   }
-  TRY(dev_alloc(c, &c->d_g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
   TRY(dev_alloc(c, &c->d_act, A));
   TRY(dev_alloc(c, &c->d_w, A));
   TRY(dev_alloc(c, &c->d_omw, A));
@@ -970,33 +1041,30 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     fail(c, ESDP_E_CUDA, "upload of the action tables failed");
     return bail(ESDP_E_CUDA);
   }
-  if (c->kind == ESDP_PAYOFF_LINEAR) cudaMemset(c->d_g, 0, A * sizeof(double));
-  TRY(dev_alloc(c, &c->d_gfit, 6));
-  if (cudaMemcpy(c->d_gfit, c->gfit, sizeof c->gfit, cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload g fit"); return bail(ESDP_E_CUDA); }
   TRY(dev_alloc(c, &c->d_F, A));
   if (cudaMemcpy(c->d_F, c->F.data(), A * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) { fail(c, ESDP_E_CUDA, "upload F"); return bail(ESDP_E_CUDA); }
-  if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_head, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_tables, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->use_ev, cudaEventDisableTiming) != cudaSuccess) {
-    fail(c, ESDP_E_CUDA, "copy stream / events");
+  if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) {
+    fail(c, ESDP_E_CUDA, "copy stream");
     return bail(ESDP_E_CUDA);
   }
   {  // P chunks: ~8 stage ranges, highest stages first (the order the backward consumes them)
     const int nst = c->rank1 ? 0 : T - 1;
     const int nch = std::min(8, nst);
     for (int j = 0; j < nch; ++j) {
-      const int hi = nst - (int)((long long)nst * j / nch), lo = nst - (int)((long long)nst * (j + 1) / nch) + 1;
-      c->chunk_hi.push_back(hi);
-      c->chunk_lo.push_back(lo);
-      c->chunk_ev.push_back(nullptr);
-      if (cudaEventCreateWithFlags(&c->chunk_ev.back(), cudaEventDisableTiming) != cudaSuccess) {
-        fail(c, ESDP_E_CUDA, "chunk event");
-        return bail(ESDP_E_CUDA);
-      }
+      c->chunk_hi.push_back(nst - (int)((long long)nst * j / nch));
+      c->chunk_lo.push_back(nst - (int)((long long)nst * (j + 1) / nch) + 1);
     }
+    for (InputSlot& x : c->slot) {
+      bool ok = cudaEventCreateWithFlags(&x.ev_head, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&x.ev_tables, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&x.use_ev, cudaEventDisableTiming) == cudaSuccess;
+      x.chunk_ev.assign(nch, nullptr);
+      for (int j = 0; j < nch && ok; ++j) ok = cudaEventCreateWithFlags(&x.chunk_ev[j], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) { fail(c, ESDP_E_CUDA, "input events"); return bail(ESDP_E_CUDA); }
+    }
+    select_slot(c, 0);
   }
-  TRY(upload(c, pr->lambda, pr->P, pr->pi, pr->g));
+  TRY(upload(c, 0, 0, pr->lambda, pr->P, pr->pi, pr->g));
   if (cudaStreamSynchronize(c->copy) != cudaSuccess) { fail(c, ESDP_E_CUDA, "initial upload"); return bail(ESDP_E_CUDA); }
   c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
   if (c->use_window) {
@@ -1088,20 +1156,30 @@ esdp_status esdp_actions(const esdp_ctx* c, double* actions) {
 }
 
 static esdp_status load_impl(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
-  // a previous upload may still be reading host memory / the graph may still wait on its events
-  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));
-  if (c->use_pending) CUDA_OR_FAIL(c, cudaEventSynchronize(c->use_ev));
+  // target: the slot no launched solve reads (or the pending one, replaced); NULL arrays keep the data of
+  // the newest inputs (src)
+  const int src = c->pending >= 0 ? c->pending : c->active;
+  const int dst = c->pending >= 0 ? c->pending : 1 - c->active;
+  InputSlot& d = c->slot[dst];
+  const InputSlot& o = c->slot[src];
+  // the last solve that read dst (and the upload events it waits on) must be complete before dst's
+  // events are recorded again; in a pipelined loop that solve finished a step ago
+  if (d.use_pending) CUDA_OR_FAIL(c, cudaEventSynchronize(d.use_ev));
   // validate what is given against the current arrays' shapes
   std::vector<double> lam_h, P_h, pi_h, g_h;
   const size_t TK = (size_t)c->T * c->K;
-  if (!lambda) { lam_h.resize(TK); CUDA_OR_FAIL(c, cudaMemcpy(lam_h.data(), c->d_lambda, TK * 8, cudaMemcpyDeviceToHost)); }
-  if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); CUDA_OR_FAIL(c, cudaMemcpy(P_h.data(), c->d_P, P_h.size() * 8, cudaMemcpyDeviceToHost)); }
-  if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); CUDA_OR_FAIL(c, cudaMemcpy(pi_h.data(), c->d_pi, pi_h.size() * 8, cudaMemcpyDeviceToHost)); }
-  if (!g && c->kind != ESDP_PAYOFF_LINEAR) { g_h.resize(c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : c->A); CUDA_OR_FAIL(c, cudaMemcpy(g_h.data(), c->d_g, g_h.size() * 8, cudaMemcpyDeviceToHost)); }
+  if (!lambda || !P || !pi || !g) CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));
+  if (!lambda) { lam_h.resize(TK); CUDA_OR_FAIL(c, cudaMemcpy(lam_h.data(), o.lambda, TK * 8, cudaMemcpyDeviceToHost)); }
+  if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); CUDA_OR_FAIL(c, cudaMemcpy(P_h.data(), o.P, P_h.size() * 8, cudaMemcpyDeviceToHost)); }
+  if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); CUDA_OR_FAIL(c, cudaMemcpy(pi_h.data(), o.pi, pi_h.size() * 8, cudaMemcpyDeviceToHost)); }
+  if (!g && c->kind != ESDP_PAYOFF_LINEAR) { g_h.resize(c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : c->A); CUDA_OR_FAIL(c, cudaMemcpy(g_h.data(), o.g, g_h.size() * 8, cudaMemcpyDeviceToHost)); }
   esdp_status st = validate_data(c, lambda ? lambda : lam_h.data(), P ? P : P_h.data(), pi ? pi : pi_h.data(),
                                  g ? g : g_h.data());
   if (st != ESDP_OK) return st;
-  return upload(c, lambda, P, pi, g);
+  st = upload(c, dst, src, lambda, P, pi, g);
+  if (st != ESDP_OK) return st;
+  c->pending = dst;
+  return ESDP_OK;
 }
 
 esdp_status esdp_load(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
@@ -1120,7 +1198,12 @@ esdp_status esdp_load_async(esdp_ctx* c, const double* lambda, const double* P, 
 esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
   if (!c) return ESDP_E_STATE;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  CUDA_OR_FAIL(c, cudaGraphLaunch(c->graph, s));
+  if (c->pending >= 0) {   // the latest load becomes the inputs of this (and later) solves
+    c->active = c->pending;
+    c->pending = -1;
+  }
+  select_slot(c, c->active);
+  CUDA_OR_FAIL(c, cudaGraphLaunch(c->graphs[c->active], s));
   { const esdp_status mu = mark_use(c, s); if (mu != ESDP_OK) return mu; }
   c->solved = true;
   return ESDP_OK;

@@ -469,3 +469,37 @@ def test_simulation_modes_state_errors():
         with pytest.raises(E.EsdpError) as e:
             s.simulate(10, 1, mode=E.ESDP_SIM_PHYSICAL)
         assert e.value.status == E.ESDP_E_STATE
+
+
+@pytest.mark.parametrize("rank1", [False, True])
+def test_pipelined_double_buffered_loads(rank1):
+    """Pipelined steps: load(j+1) is issued while solve j runs and before solve j's results are read;
+    the results of solve j (J, values, policy, simulation) stay those of inputs j, and every solve
+    matches the oracle on its own inputs.  NULL arrays keep the newest inputs."""
+    import torch
+    insts = []
+    for j in range(4):
+        x = workloads.cfg2(T=24, K=12, rank1=rank1)
+        x.lam, _, _ = workloads.price_chain(x.T, x.K, 5.0 / 60.0, seed=workloads.SEED_BASE + 900 + j)
+        insts.append(x)
+    refs = [oracle.backward(to_oracle(x), nthreads=16) for x in insts]
+    sims = [oracle.simulate(to_oracle(x), r.pol, 512, seed=4)[0] for x, r in zip(insts, refs)]
+    with E.Solver(insts[0]) as s:
+        keep = [E.esdp_load_async(s.ctx, lam=insts[0].lam)]
+        for j in range(4):
+            E.esdp_backward_async(s.ctx)
+            if j + 1 < 4:
+                keep.append(E.esdp_load_async(s.ctx, lam=insts[j + 1].lam))   # overlaps solve j
+            torch.cuda.synchronize()
+            assert E.esdp_objective(s.ctx) == refs[j].J
+            V, W = s.values(1)
+            assert np.array_equal(V, refs[j].V[0]) and np.array_equal(W, refs[j].W[0])
+            assert np.array_equal(s.policy(insts[j].T // 2), refs[j].pol[insts[j].T // 2 - 1])
+            per, _, _ = s.simulate(512, seed=4)
+            assert np.array_equal(per, sims[j])
+        # two loads without a solve: the second replaces the first; NULL keeps the newest inputs
+        E.esdp_load(s.ctx, lam=insts[1].lam)
+        E.esdp_load(s.ctx, lam=insts[2].lam)
+        assert s.backward() == refs[2].J
+        E.esdp_load(s.ctx, pi=insts[2].pi)
+        assert s.backward() == refs[2].J

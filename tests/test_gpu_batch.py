@@ -90,3 +90,17 @@ def test_batch_rejects_mismatched_price_models():
     with pytest.raises(E.EsdpError) as e:
         E.Batch([a, c])
     assert e.value.status == E.ESDP_E_CONFIG
+
+
+def test_batch_full_horizon_cfg5():
+    """Four cfg5 configurations at full cfg2 size (T=288, S=1001, K=100) in one batch: J, V_1 and the
+    policies of sampled stages bit-identical to the oracle on each instance."""
+    insts = workloads.cfg5_instances([0, 341, 682, 1023])
+    with E.Batch(insts) as b:
+        J = b.backward()
+        for m, inst in enumerate(insts):
+            ref = oracle.backward(to_oracle(inst), nthreads=16)
+            assert J[m] == ref.J
+            assert np.array_equal(b.value1(m), ref.V[0])
+            for t in (1, 100, 287, 288):
+                assert np.array_equal(b.policy(m, t), ref.pol[t - 1]), (m, t)

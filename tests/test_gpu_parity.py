@@ -503,3 +503,37 @@ def test_pipelined_double_buffered_loads(rank1):
         assert s.backward() == refs[2].J
         E.esdp_load(s.ctx, pi=insts[2].pi)
         assert s.backward() == refs[2].J
+
+
+def test_cfg3_full_size_every_stage():
+    """cfg3ii at full size (T=288, S=1001, A=201, K=100; non-concave payoff on the window plan): every
+    stage bit-identical to the oracle."""
+    base = workloads.cfg2(T=2, K=2)
+    inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)))
+    _compare_all(inst, nthreads=16, expect_window=True)
+
+
+def test_cfg4_full_year_sampled_stages():
+    """cfg4 at full size (T=8760, S=2001, A=401, K=200; a distinct P_t per stage) in the bench's launch
+    configuration: every sampled stage t equals the oracle's stage computed from the GPU's own V_{t+1}
+    (each stage is a pure function of V_{t+1}), the last stages from scratch, and J from V_1."""
+    inst = workloads.cfg4()
+    pr = to_oracle(inst)
+    T = inst.T
+    WT, VT, polT = oracle.stage(pr, T, 0, inst.K, None, nthreads=16)          # from scratch
+    WT1, VT1, polT1 = oracle.stage(pr, T - 1, 0, inst.K, VT, nthreads=16)
+    with _gpu(inst) as s:
+        J = s.backward()
+        for t, (Wr, Vr, pr_) in ((T, (WT, VT, polT)), (T - 1, (WT1, VT1, polT1))):
+            V, W = s.values(t)
+            assert np.array_equal(W, Wr) and np.array_equal(V, Vr)
+            assert np.array_equal(s.policy(t), pr_)
+        for t in (T - 2, 4380, 1234, 2, 1):
+            Vn, _ = s.values(t + 1)
+            W_ref, V_ref, pol_ref = oracle.stage(pr, t, 0, inst.K, Vn, nthreads=16)
+            V, W = s.values(t)
+            assert np.array_equal(W, W_ref), t
+            assert np.array_equal(V, V_ref), t
+            assert np.array_equal(s.policy(t), pol_ref), t
+        V1, _ = s.values(1)
+        assert J == oracle.objective(pr, V1)

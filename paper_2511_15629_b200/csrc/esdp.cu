@@ -130,7 +130,8 @@ struct esdp_ctx {
   int16_t* fb_vert = nullptr;
   double *fb_q = nullptr, *fb_price = nullptr;
   int fb_batch = 1;
-  std::vector<cudaStream_t> side;      // side streams of the bid-curve branches
+  std::vector<cudaStream_t> side;      // side streams of the bid-curve branches (lowest priority)
+  int prio_lo = 0;
   std::vector<cudaEvent_t> fb_ev, join_ev;
   std::vector<cudaEvent_t> ev;  // ESDP_PROFILE: [t][4] = contract begin/end, stencil begin/end
   int prof_stride = 1;
@@ -956,7 +957,12 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
 
   auto bail = [&](esdp_status st) { g_create_error = c->err; free_all(c); delete c; return st; };
 #define TRY(x) do { esdp_status st_ = (x); if (st_ != ESDP_OK) return bail(st_); } while (0)
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  // the dependent stage chain runs at the highest stream priority, the bid-curve side branches at the
+  // lowest (graph nodes keep the priority of the stream they were captured on)
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  c->prio_lo = prio_lo;
+  if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     cudaGetLastError();
     fail(c, ESDP_E_CUDA, "cannot create a CUDA stream (no usable GPU?)");
     return bail(ESDP_E_CUDA);
@@ -1126,7 +1132,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   c->side.assign(4, nullptr);
   c->join_ev.assign(c->side.size(), nullptr);
   for (size_t j = 0; j < c->side.size(); ++j)
-    if (cudaStreamCreateWithFlags(&c->side[j], cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&c->side[j], cudaStreamNonBlocking, c->prio_lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join_ev[j], cudaEventDisableTiming) != cudaSuccess) {
       fail(c, ESDP_E_CUDA, "side stream");
       return bail(ESDP_E_CUDA);

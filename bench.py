@@ -204,18 +204,30 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
+    side = torch.cuda.Stream(device=dev)
+    ev_bw, ev_bids = torch.cuda.Event(), torch.cuda.Event()
+    with_sim = args.bids == "with-sim" and n_bid > 0
+
     def step(j, marks=None):
         if marks:
             marks[0].record(stream)
         E.esdp_backward_async(solver.ctx, sp)
         if marks:
             marks[1].record(stream)
-        if n_bid and not fused:
+        if with_sim:   # the bid curves on a side stream, concurrent with the (latency-bound) simulation
+            ev_bw.record(stream)
+            side.wait_event(ev_bw)
+            E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
+                                 None, pr_d.data_ptr(), side.cuda_stream)
+            ev_bids.record(side)
+        elif n_bid and not fused:
             E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
                                  None, pr_d.data_ptr(), sp)
         if marks:
             marks[2].record(stream)
         E.esdp_simulate_dev(solver.ctx, n_paths, 1234 + j + 7919 * rank, per_d.data_ptr(), sp)
+        if with_sim:
+            stream.wait_event(ev_bids)
         if marks:
             marks[3].record(stream)
 
@@ -526,8 +538,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-events", type=int, default=1,
                     help="per-phase device timers inside the backward (persistent plan) / events (graph plan)")
-    ap.add_argument("--bids", choices=["fused", "after"], default="fused",
-                    help="bid curves as side branches of the backward graph (fused) or one kernel after it")
+    ap.add_argument("--bids", choices=["fused", "after", "with-sim"], default="fused",
+                    help="bid curves as side branches of the backward graph (fused), one kernel after it, or one "
+                         "kernel on a side stream concurrent with the simulation")
     ap.add_argument("--stencil", choices=["auto", "brute"], default="auto",
                     help="auto: exact sliding-window stencil where it applies; brute: every (i, a) cell")
     ap.add_argument("--plan", choices=["graph", "persistent"], default="graph",

@@ -224,7 +224,13 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
 // [kDR*8][Kp] and the V tile [Kp][kDC*16] are staged once per block with cp.async (so every L2 byte is
 // read by one block, not by every warp), then each warp runs its 8x16 tile's DMMA chain from shared
 // memory.  cfg2: 7 x 21 = 147 blocks of 6 warps (one per SM).
-constexpr int kDR = 2, kDC = 3;
+#ifndef ESDP_KDR
+#define ESDP_KDR 1
+#endif
+#ifndef ESDP_KDC
+#define ESDP_KDC 3
+#endif
+constexpr int kDR = ESDP_KDR, kDC = ESDP_KDC;   // expectation tile: kDR*8 rows x kDC*16 columns, kDR*kDC warps
 constexpr int kD2Threads = kDR * kDC * 32;
 
 inline size_t contract_dmma2_smem(int K, int DC = kDC) {

@@ -29,7 +29,7 @@
 namespace esdp {
 
 constexpr int kPersistThreads = 256;
-constexpr int kDfDC = 4;                 // E tile: kDR*8 = 16 rows x kDfDC*16 = 64 columns, 8 warps
+constexpr int kDfDC = kPersistThreads / (32 * kDR);   // E tile: kDR*8 rows x kDfDC*16 columns, 8 warps
 constexpr int kDfRows = kDR * 8, kDfCols = kDfDC * 16;
 static_assert(kDR * kDfDC * 32 == kPersistThreads, "E tile uses every warp");
 

@@ -1097,7 +1097,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
   // persistent dataflow path (single GPU; Markov uses the DMMA expectation; K < 2^15)
-  if ((c->flags & ESDP_PERSIST) && !nccl_id && K < 32768 && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
+  if ((c->flags & ESDP_PERSIST) && !nccl_id && K < 32768 && kWinThreads == kPersistThreads && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

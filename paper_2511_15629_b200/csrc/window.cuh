@@ -24,9 +24,16 @@
 
 namespace esdp {
 
-constexpr int kWinTile = 256;     // output columns per block
+#ifndef ESDP_WIN_THREADS
+#define ESDP_WIN_THREADS 256
+#endif
+#ifndef ESDP_WIN_MINB
+#define ESDP_WIN_MINB 4
+#endif
+constexpr int kWinTile = ESDP_WIN_THREADS;     // output columns per block
 __device__ unsigned long long g_window_fallbacks;  // rows that needed the full canonical scan (diagnostic)
-constexpr int kWinThreads = 256;  // one output column per thread in the query phase
+constexpr int kWinThreads = ESDP_WIN_THREADS;  // one output column per thread in the query phase
+constexpr int kLevelSlots = (kWinTile + 512 + 2 * kWinThreads - 1) / (2 * kWinThreads);  // pairs per thread
 
 constexpr int kMaxSingles = 16;  // singles staged in shared memory (more: read from global)
 
@@ -121,7 +128,7 @@ __device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
   const unsigned long long* pv = t.v + (q - 1) * t.ns;
   unsigned long long* nv = t.v + q * t.ns;
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < kLevelSlots; ++u) {
     const int x = 2 * (tid + u * kWinThreads);
     if (x <= lim) {
       const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(pv + x);
@@ -220,8 +227,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     __syncthreads();
   }
   (void)ldl;
-  static_assert(kWinThreads / 32 == 8, "one red[] entry per lane group of 8");
-  const unsigned mb = __reduce_max_sync(0xffffffffu, red[tid & 7]);
+  const unsigned mb = __reduce_max_sync(0xffffffffu, red[tid % (kWinThreads / 32)]);
   const double M = __hiloint2double((int)mb, (int)0xffffffffu);
   const double bmax = fmax(fabs(beta_c), fabs(beta_d)) * p.jspan;   // >= |beta j| over the tile
   // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
@@ -300,7 +306,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   p.pol[(size_t)k * p.S + i] = (int16_t)arg;
 }
 
-__global__ void __launch_bounds__(kWinThreads, 4) window_stencil_kernel(WinParams p) {
+__global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
   pdl_wait();                          // W_t is the previous contraction's output
   window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);

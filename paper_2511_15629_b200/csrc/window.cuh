@@ -62,16 +62,20 @@ __device__ __forceinline__ unsigned long long ord64(double x) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
-__device__ __forceinline__ double unord64(unsigned long long k) {  // value part 0: -inf / empty range
+__device__ __forceinline__ double unord64(unsigned long long k) {  // below ord64(-DBL_MAX): -inf / empty range
   k &= ~kPosMask;
-  if (k == 0ull) return -INFINITY;
+  if (k < 0x0010000000000000ull) return -INFINITY;
   const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
 }
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
-// packed key of a value at table position pos; -inf packs to the bare position (below every finite key)
+// packed key of a value at table position pos (branch-free ord64 on the 32-bit halves; -inf packs below
+// every finite key and decodes back to -inf)
 __device__ __forceinline__ unsigned long long pack_key(double v, int pos) {
-  return (v == -INFINITY ? 0ull : (ord64(v) & ~kPosMask)) | (unsigned long long)pos;
+  const int hi = __double2hiint(v), lo = __double2loint(v);
+  const int m = hi >> 31;                                   // 0 (v >= +0) or -1 (v <= -0)
+  const unsigned h = (unsigned)(hi ^ (m | (int)0x80000000)), l = (unsigned)(lo ^ m);
+  return ((((unsigned long long)h << 32) | l) & ~kPosMask) | (unsigned long long)pos;
 }
 
 // Sparse table over power-of-two ranges: level q entry x = max of packed keys in [x, x + 2^q).
@@ -259,6 +263,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     }
     double c1 = 0.0;      // canonical value of the best single (exact)
     bool single_best = false;
+#pragma unroll 4
     for (int s = 0; s < nsg; ++s) {
       const double c = canon_staged(ss[s], wt, wbase, i);
       if (c > b1) { b2 = b1; b1 = c; a1 = ss[s].a; c1 = c; single_best = true; }
@@ -272,8 +277,15 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     }
     if (__dsub_rn(b1, b2) > 2.0 * eps) {
       arg = a1;
-      // canonical value of the unique argmax (a run action: one product and one add)
-      best = single_best ? c1 : canon_single(p, wt, wbase, i, a1, lam);
+      // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, w = 0), so
+      // only its power (and g) is loaded: fl(fl(fl(lambda p) - g) + W[i + o])
+      if (single_best) {
+        best = c1;
+      } else {
+        double pay = __dmul_rn(lam, __ldg(p.act + a1));
+        if (p.g_kind) pay = __dsub_rn(pay, __ldg(p.g + a1));
+        best = __dadd_rn(pay, wt[i + (p.a_z - a1) - wbase]);
+      }
     } else {
       near_tie = true;
     }

@@ -334,6 +334,15 @@ def run_ours(args):
     hbm_bytes = 18.0 * T * rows_here * S                               # read W, write V + pol per (k, s, t)
     hbm_ach = hbm_bytes / (bw_ms * 1e-3) / 1e9
     plan = E.esdp_stencil_kind(solver.ctx)
+    # DRAM traffic per backward from the committed ncu capture of this workload (cfg2, graph plan)
+    traffic, traffic_note = None, None
+    tr_path = os.path.join(ROOT, "profiles", "r01k_backward_traffic.json")
+    if args.config == "cfg2" and not kpart and not (plan & 2) and os.path.exists(tr_path):
+        with open(tr_path) as f:
+            traffic = json.load(f)["per_backward_bytes"]
+        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum summed over one backward's kernels "
+                        "(profiles/r01k_backward_traffic.json, ncu --cache-control none); algorithmic bytes "
+                        "%.4g" % hbm_bytes)
     out = None
     if rank == 0:
         out = {
@@ -366,7 +375,7 @@ def run_ours(args):
             "roofline": {"bound": "alu",
                          "kernel": "backward (%s)" % ("persistent dataflow kernel" if plan & 2 else "graph of 2T kernels"),
                          "achieved": achieved, "peak": fp64_peak, "unit": "G FP64 instr/s",
-                         "frac": achieved / fp64_peak, "traffic": None,
+                         "frac": achieved / fp64_peak, "traffic": traffic, "traffic_note": traffic_note,
                          "peak_note": f"{n_sm} SMs x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz "
                                       f"(sm_max_mhz from MEASURED_PEAKS.json: {peak_kind})",
                          "work_per_launch": f"algorithmic FP64 instr: 2 per cell x T*S*K*A + K per (k,s) x (T-1)*S*K "

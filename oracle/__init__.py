@@ -69,6 +69,7 @@ def lib():
                                         ctypes.POINTER(ctypes.c_uint32)]
         L.ref_simulate.argtypes = [P, _sp, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp]
         L.ref_simulate_mode.argtypes = [P, _sp, _dp, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, _dp, _dp, _dp]
+        L.ref_simulate_strategy.argtypes = [P, _dp, ctypes.c_int32, _sp, ctypes.c_int64, ctypes.c_uint64, _dp, _sp]
         L.ref_stage.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _dp, _dp, _dp, _sp]
         L.ref_objective.argtypes = [P, _dp, _dp]
         _lib = L
@@ -234,7 +235,7 @@ def simulate(pr: Problem, pol: np.ndarray, n_paths: int, seed: int):
     return per, m.value, v.value
 
 
-SIM_LOTTERY, SIM_PHYSICAL, SIM_CLEAR_BIDS = 0, 1, 2
+SIM_LOTTERY, SIM_PHYSICAL, SIM_CLEAR_BIDS, SIM_SELF, SIM_FIXED = 0, 1, 2, 3, 4
 
 
 def simulate_mode(pr: Problem, pol: np.ndarray, W: np.ndarray, mode: int, n_paths: int, seed: int):
@@ -249,3 +250,19 @@ def simulate_mode(pr: Problem, pol: np.ndarray, W: np.ndarray, mode: int, n_path
     if rc:
         raise OracleError(rc, "ref_simulate_mode")
     return per, m.value, v.value
+
+
+def simulate_strategy(pr: Problem, W, mode: int, n_paths: int, seed: int, schedule=None, want_actions=False):
+    """ref_simulate_strategy: physical / self-scheduled / fixed-schedule dispatch; returns (profits,
+    actions [T][n] or None)."""
+    per = np.zeros(n_paths)
+    c = pr._c()
+    Wc = None if W is None else np.ascontiguousarray(W, dtype=np.float64)
+    sch = None if schedule is None else np.ascontiguousarray(schedule, dtype=np.int16)
+    act = np.zeros((pr.T, n_paths), np.int16) if want_actions else None
+    rc = lib().ref_simulate_strategy(ctypes.byref(c), None if Wc is None else _ptr(Wc), int(mode),
+                                     None if sch is None else _ptr(sch, _sp), int(n_paths), ctypes.c_uint64(seed),
+                                     _ptr(per), None if act is None else _ptr(act, _sp))
+    if rc:
+        raise OracleError(rc, "ref_simulate_strategy")
+    return per, act

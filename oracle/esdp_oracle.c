@@ -487,8 +487,19 @@ int ref_simulate(const ref_problem* pr, const int16_t* pol, int64_t n_paths, uin
  * every action a in ascending order, s' = s + F(p_a) (Eq. 2), feasible iff 0 <= s'/delta <= S-1 within
  * 1e-9 (Eq. 4 on the real state), cand = payoff + W_t(s') with Alg. 1 line 7's interpolation at the
  * off-grid index s'/delta; strict '>' keeps the smallest maximising index (R8). */
+static int32_t physical_action_lam(const ref_problem* pr, int32_t S, int32_t A, const double* act,
+                                   const double* Wrow, int32_t t, int32_t k, const double* lam_override, double s,
+                                   double* s_next);
+
 static int32_t physical_action(const ref_problem* pr, int32_t S, int32_t A, const double* act, const double* Wrow,
                                int32_t t, int32_t k, double s, double* s_next) {
+  return physical_action_lam(pr, S, A, act, Wrow, t, k, NULL, s, s_next);
+}
+
+/* physical_action with the payoff formed at price *lam_override instead of lambda_{t,k} (linear payoffs). */
+static int32_t physical_action_lam(const ref_problem* pr, int32_t S, int32_t A, const double* act,
+                                   const double* Wrow, int32_t t, int32_t k, const double* lam_override, double s,
+                                   double* s_next) {
   int32_t best_a = -1;
   double best = -INFINITY, best_s = s;
   for (int32_t a = 0; a < A; ++a) {
@@ -505,7 +516,14 @@ static int32_t physical_action(const ref_problem* pr, int32_t S, int32_t A, cons
       double w = x - f;
       wint = ((1.0 - w) * Wrow[(int32_t)f]) + (w * Wrow[(int32_t)f + 1]);
     }
-    double cand = payoff(pr, A, act, t, k, a) + wint;
+    double pay;
+    if (lam_override) {
+      double gv = pr->payoff_kind == REF_PAYOFF_LINEAR_MINUS_G ? pr->g[a] : 0.0;
+      pay = (*lam_override * act[a]) - gv;
+    } else {
+      pay = payoff(pr, A, act, t, k, a);
+    }
+    double cand = pay + wint;
     if (cand > best) { best = cand; best_a = a; best_s = sn; }
   }
   *s_next = best_s;
@@ -579,5 +597,54 @@ int ref_simulate_mode(const ref_problem* pr, const int16_t* pol, const double* W
     *var = n_paths > 1 ? ss / (double)(n_paths - 1) : 0.0;
   }
   free(act); free(off); free(w); free(omw); free(ilo); free(ihi); free(vert); free(q); free(price);
+  return err;
+}
+
+int ref_simulate_strategy(const ref_problem* pr, const double* W, int32_t mode, const int16_t* schedule,
+                          int64_t n_paths, uint64_t seed, double* per_path, int16_t* actions) {
+  int32_t S, A;
+  int rc = ref_dims(pr, &S, &A);
+  if (rc) return rc;
+  if (n_paths < 1) return REF_E_STATE;
+  if (mode != REF_SIM_PHYSICAL && mode != REF_SIM_SELF && mode != REF_SIM_FIXED) return REF_E_STATE;
+  if ((mode != REF_SIM_FIXED && !W) || (mode == REF_SIM_FIXED && !schedule)) return REF_E_STATE;
+  if (mode == REF_SIM_SELF && pr->payoff_kind == REF_PAYOFF_TABLE) return REF_E_STATE;
+  const int32_t T = pr->T, K = pr->K;
+  double* act = (double*)malloc(sizeof(double) * (size_t)A);
+  ref_actions(pr, act);
+  const int64_t KS = (int64_t)K * S;
+  int err = REF_OK;
+  for (int64_t path = 0; path < n_paths && !err; ++path) {
+    double u1, u2;
+    uniforms(seed, path, 0, &u1, &u2);
+    int32_t k = sample_cdf(pr->pi, K, u1);
+    int32_t k_prev = k;
+    double s = pr->s0, profit = 0.0, lam_prev = pr->lambda[k];   /* stage 1's lag: its own price */
+    for (int32_t t = 1; t <= T; ++t) {
+      uniforms(seed, path, t, &u1, &u2);
+      const double lam_t = pr->lambda[(int64_t)(t - 1) * K + k];
+      int32_t a;
+      if (mode == REF_SIM_FIXED) {
+        a = schedule[t - 1];
+      } else {
+        const int32_t row = pr->P == NULL ? 0 : (mode == REF_SIM_SELF ? k_prev : k);
+        const double* Wrow = W + (int64_t)(t - 1) * KS + (int64_t)row * S;
+        double sn;
+        a = physical_action_lam(pr, S, A, act, Wrow, t, k, mode == REF_SIM_SELF ? &lam_prev : NULL, s, &sn);
+        if (a < 0) { err = REF_E_INTERNAL; break; }
+        s = sn;
+      }
+      if (actions) actions[(int64_t)(t - 1) * n_paths + path] = (int16_t)a;
+      profit = profit + payoff(pr, A, act, t, k, a);        /* settled at the realised price */
+      lam_prev = lam_t;
+      k_prev = k;
+      if (t < T) {
+        const double* qk = pr->P ? pr->P + ((int64_t)(t - 1) * K + k) * K : pr->pi + (int64_t)t * K;
+        k = sample_cdf(qk, K, u2);
+      }
+    }
+    per_path[path] = profit;
+  }
+  free(act);
   return err;
 }

@@ -104,9 +104,23 @@ int ref_simulate(const ref_problem* pr, const int16_t* pol, int64_t n_paths, uin
  *   REF_SIM_CLEAR_BIDS grid state i (lottery moves as in ref_simulate): the action is the bid curve
  *                      of (t, i, k) from W_t cleared at lambda_{t,k} (ref_bidcurve + ref_clear).
  * W: [T][K][S] (all stages; needed by the last two modes).  TABLE payoffs: CLEAR_BIDS -> REF_E_STATE. */
-enum { REF_SIM_LOTTERY = 0, REF_SIM_PHYSICAL = 1, REF_SIM_CLEAR_BIDS = 2 };
+enum { REF_SIM_LOTTERY = 0, REF_SIM_PHYSICAL = 1, REF_SIM_CLEAR_BIDS = 2, REF_SIM_SELF = 3, REF_SIM_FIXED = 4 };
 int ref_simulate_mode(const ref_problem* pr, const int16_t* pol, const double* W, int32_t mode, int64_t n_paths,
                       uint64_t seed, double* per_path, double* mean, double* var);
+
+/* Dispatch strategies of the paper's Fig. 3 study (R27/R28),
+ * on the same price paths (Philox draws) as the modes above, at the real SoC from s0:
+ *   REF_SIM_PHYSICAL  as ref_simulate_mode (the "stochastic DP bid curves" dispatch: re-optimise at the
+ *                     real SoC with the realised price, i.e. clear the stage's curve at it);
+ *   REF_SIM_SELF      "self-scheduled": the decision uses the realised 1-stage-lagged price (stage 1: its
+ *                     own price) and the continuation row of the last observed price state (persistence
+ *                     forecast; stage 1: k_1), then settles at the realised price (R27);
+ *   REF_SIM_FIXED     a fixed schedule of actions schedule[T] (e.g. the myopic plan on day-ahead prices),
+ *                     settled at the realised prices (R28).
+ * W: [T][K][S] (PHYSICAL, SELF).  actions (nullable): [T][n_paths] chosen action indices.  SELF rejects
+ * TABLE payoffs (the price must enter linearly). */
+int ref_simulate_strategy(const ref_problem* pr, const double* W, int32_t mode, const int16_t* schedule,
+                          int64_t n_paths, uint64_t seed, double* per_path, int16_t* actions);
 
 #ifdef __cplusplus
 }

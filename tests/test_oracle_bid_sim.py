@@ -214,3 +214,61 @@ def test_clear_bids_mode_rejects_table_payoffs():
     sol = oracle.backward(pr)
     with pytest.raises(oracle.OracleError):
         oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_CLEAR_BIDS, 4, seed=1)
+
+
+# ---- dispatch strategies of the Fig. 3 study (NEXT-2; R27/R28) ----
+
+def _det_instance(lam, seed=3):
+    inst = workloads.random_instance(seed, T=len(lam), K=1, S_max=40)
+    inst.eta_c = inst.eta_d = 0.9
+    inst.lam = np.asarray(lam, float).reshape(-1, 1)
+    inst.pi = np.ones((len(lam), 1)) if inst.P is None else np.array([1.0])
+    if inst.P is not None:
+        inst.P = np.ones((len(lam) - 1, 1, 1))
+    return inst
+
+
+def test_strategy_physical_equals_physical_mode():
+    inst = workloads.cfg1("b")
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    a, _ = oracle.simulate_strategy(pr, sol.W, oracle.SIM_PHYSICAL, 300, seed=8)
+    b, _, _ = oracle.simulate_mode(pr, sol.pol, sol.W, oracle.SIM_PHYSICAL, 300, seed=8)
+    assert np.array_equal(a, b)
+
+
+def test_self_scheduled_equals_bids_when_the_lag_is_exact():
+    """R27: with prices constant over time the lagged price is the realised one, so the self-scheduled
+    decisions are the re-optimised ones (SPEC: 'lagged == realized -> identical to simulateBidding')."""
+    inst = _det_instance([7.5] * 9)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    a, _ = oracle.simulate_strategy(pr, sol.W, oracle.SIM_PHYSICAL, 5, seed=2)
+    b, _ = oracle.simulate_strategy(pr, sol.W, oracle.SIM_SELF, 5, seed=2)
+    assert np.array_equal(a, b)
+
+
+def test_self_scheduled_loses_on_anticorrelated_lags():
+    """Alternating prices make the lagged price the wrong forecast: self-scheduling earns less than
+    re-optimising at the realised price (Fig. 3 ordering 'DP bid curves > self-scheduled')."""
+    inst = _det_instance([1.0, 40.0] * 6)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    a, _ = oracle.simulate_strategy(pr, sol.W, oracle.SIM_PHYSICAL, 3, seed=2)
+    b, _ = oracle.simulate_strategy(pr, sol.W, oracle.SIM_SELF, 3, seed=2)
+    assert np.all(b < a)
+
+
+def test_fixed_schedule_replays_and_settles_linearly():
+    """R28: the physical plan of a deterministic problem, replayed as a fixed schedule, earns the same;
+    settled at doubled prices (g = 0) it earns exactly twice (SPEC: linear settlement)."""
+    lam = [12.0, 3.0, 25.0, 9.0, 31.0, 2.0, 18.0]
+    inst = _det_instance(lam)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    phy, act = oracle.simulate_strategy(pr, sol.W, oracle.SIM_PHYSICAL, 1, seed=4, want_actions=True)
+    fix, _ = oracle.simulate_strategy(pr, None, oracle.SIM_FIXED, 1, seed=4, schedule=act[:, 0])
+    assert np.array_equal(phy, fix)
+    inst2 = _det_instance([2 * x for x in lam])
+    fix2, _ = oracle.simulate_strategy(to_oracle(inst2), None, oracle.SIM_FIXED, 1, seed=4, schedule=act[:, 0])
+    assert fix2[0] == 2 * fix[0]

@@ -199,11 +199,32 @@ esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, dou
  *                        larger quantity, R9).
  * PHYSICAL and CLEAR_BIDS need ESDP_KEEP_VALUES and one GPU; CLEAR_BIDS rejects TABLE payoffs
  * (ESDP_E_STATE).  Host variant: mean, var (sample), per_path[n_paths] (nullable), synchronized. */
-enum { ESDP_SIM_LOTTERY = 0, ESDP_SIM_PHYSICAL = 1, ESDP_SIM_CLEAR_BIDS = 2 };
+enum { ESDP_SIM_LOTTERY = 0, ESDP_SIM_PHYSICAL = 1, ESDP_SIM_CLEAR_BIDS = 2, ESDP_SIM_SELF = 3, ESDP_SIM_FIXED = 4 };
 esdp_status esdp_simulate_mode(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int32_t mode, double* mean,
                                double* var, double* per_path);
 esdp_status esdp_simulate_mode_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int32_t mode,
                                    double* per_path_dev, void* stream);
+
+/* The price paths of esdp_simulate(seed) for the inputs of the last solve: k_t and the realised price
+ * lambda_{t,k_t} of every path, [T][n_paths] each (device; either output may be NULL).  Used to set up
+ * perfect-foresight solves on the realised paths (the Fig. 3 upper bound). */
+esdp_status esdp_price_paths_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int16_t* kpath_dev,
+                                 double* lambda_dev, void* stream);
+
+/* Dispatch strategies of the paper's Fig. 3 study (R27/R28),
+ * on the same price paths as esdp_simulate, from the real SoC s0:
+ *   ESDP_SIM_PHYSICAL   "stochastic DP bid curves": the stage's curve cleared at the realised price
+ *                       (= re-optimisation at the real SoC, as above);
+ *   ESDP_SIM_SELF       "self-scheduled": decided at the realised one-stage-lagged price (stage 1: its own
+ *                       price) with the continuation row of the last observed price state, settled at the
+ *                       realised price;
+ *   ESDP_SIM_FIXED      the fixed schedule schedule_dev[T] (device; e.g. the myopic plan recorded from a
+ *                       day-ahead context of the same grid), settled at the realised prices.
+ * actions_dev (nullable, device): [T][n_paths] chosen action indices (not for CLEAR_BIDS).  PHYSICAL and
+ * SELF need ESDP_KEEP_VALUES and one GPU; SELF and CLEAR_BIDS reject TABLE payoffs. */
+esdp_status esdp_simulate_strategy_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, int32_t mode,
+                                       const int16_t* schedule_dev, int16_t* actions_dev, double* per_path_dev,
+                                       void* stream);
 
 /* Execution plan: bit 0 = stencil (1 = exact sliding-window for the recombining grid with a linear
  * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent dataflow

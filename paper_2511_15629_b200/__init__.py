@@ -33,7 +33,7 @@ ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
 ESDP_PERSIST = 32
 ESDP_DMMA_L2 = 64
-ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS = 0, 1, 2
+ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS, ESDP_SIM_SELF, ESDP_SIM_FIXED = 0, 1, 2, 3, 4
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
 
@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = [
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
     "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
-    "esdp_simulate_mode", "esdp_simulate_mode_dev",
+    "esdp_simulate_mode", "esdp_simulate_mode_dev", "esdp_simulate_strategy_dev", "esdp_price_paths_dev",
     "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
     "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
     "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error",
@@ -95,6 +95,9 @@ def _load():
         "esdp_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
         "esdp_simulate_mode": ([ctx, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _dp, _dp, _dp], ctypes.c_int),
         "esdp_simulate_mode_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _vp, _vp], ctypes.c_int),
+        "esdp_simulate_strategy_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _vp, _vp, _vp, _vp],
+                                       ctypes.c_int),
+        "esdp_price_paths_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp, _vp], ctypes.c_int),
         "esdp_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_kernel_times": ([ctx, _dp, _dp], ctypes.c_int),
         "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
@@ -290,6 +293,18 @@ def esdp_simulate_mode(ctx, n_paths, seed, mode, per_path=True):
     _check(lib.esdp_simulate_mode(ctx, int(n_paths), ctypes.c_uint64(int(seed)), int(mode), ctypes.byref(m),
                                   ctypes.byref(v), _p(out)), "esdp_simulate_mode", ctx)
     return out, m.value, v.value
+
+
+def esdp_simulate_strategy_dev(ctx, n_paths, seed, mode, per_path_ptr, schedule_ptr=None, actions_ptr=None,
+                               stream=None):
+    _check(lib.esdp_simulate_strategy_dev(ctx, int(n_paths), ctypes.c_uint64(int(seed)), int(mode), schedule_ptr,
+                                          actions_ptr, per_path_ptr, _stream_ptr(stream)),
+           "esdp_simulate_strategy_dev", ctx)
+
+
+def esdp_price_paths_dev(ctx, n_paths, seed, kpath_ptr=None, lambda_ptr=None, stream=None):
+    _check(lib.esdp_price_paths_dev(ctx, int(n_paths), ctypes.c_uint64(int(seed)), kpath_ptr, lambda_ptr,
+                                    _stream_ptr(stream)), "esdp_price_paths_dev", ctx)
 
 
 def esdp_simulate_dev(ctx, n_paths, seed, per_path_ptr, stream=None):

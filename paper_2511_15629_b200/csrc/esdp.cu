@@ -1375,6 +1375,20 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   return mark_use(c, s);
 }
 
+esdp_status esdp_price_paths_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, int16_t* kpath_dev, double* lambda_dev,
+                                 void* stream) {
+  if (!c) return ESDP_E_STATE;
+  if (n_paths < 1 || (!kpath_dev && !lambda_dev)) return fail(c, ESDP_E_STATE, "n_paths >= 1 and an output are required");
+  SimParams sp{};
+  sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda; sp.guide = c->d_guide; sp.guide1 = c->d_guide1;
+  sp.G = c->G; sp.T = c->T; sp.K = c->K; sp.rank1 = c->rank1;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));
+  price_path_kernel<<<(unsigned)((n_paths + 127) / 128), 128, 0, s>>>(sp, n_paths, seed, kpath_dev, lambda_dev);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return mark_use(c, s);
+}
+
 esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* mean, double* var, double* per_path) {
   if (!c) return ESDP_E_STATE;
   if (n_paths > c->sim_cap) {
@@ -1398,17 +1412,22 @@ esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* m
   return ESDP_OK;
 }
 
-esdp_status esdp_simulate_mode_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode, double* per_path_dev,
-                                   void* stream) {
+esdp_status esdp_simulate_strategy_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode,
+                                       const int16_t* schedule_dev, int16_t* actions_dev, double* per_path_dev,
+                                       void* stream) {
   if (!c) return ESDP_E_STATE;
-  if (mode == ESDP_SIM_LOTTERY) return esdp_simulate_dev(c, n_paths, seed, per_path_dev, stream);
-  if (mode != ESDP_SIM_PHYSICAL && mode != ESDP_SIM_CLEAR_BIDS) return fail(c, ESDP_E_STATE, "unknown simulation mode %d", mode);
+  if (mode == ESDP_SIM_LOTTERY && !actions_dev) return esdp_simulate_dev(c, n_paths, seed, per_path_dev, stream);
+  if (mode < ESDP_SIM_PHYSICAL || mode > ESDP_SIM_FIXED) return fail(c, ESDP_E_STATE, "unknown simulation mode %d", mode);
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   if (n_paths < 1) return fail(c, ESDP_E_STATE, "n_paths must be >= 1");
-  if (!keep(c)) return fail(c, ESDP_E_STATE, "physical / bid-clearing simulation needs ESDP_KEEP_VALUES (W of every stage)");
-  if (c->world > 1) return fail(c, ESDP_E_STATE, "physical / bid-clearing simulation needs every W row (world == 1)");
-  if (mode == ESDP_SIM_CLEAR_BIDS && c->kind == ESDP_PAYOFF_TABLE)
-    return fail(c, ESDP_E_STATE, "bid curves are not defined for TABLE payoffs (R13)");
+  if (mode != ESDP_SIM_FIXED && !keep(c))
+    return fail(c, ESDP_E_STATE, "physical / bid-clearing / self-scheduled simulation needs ESDP_KEEP_VALUES (W of every stage)");
+  if (mode != ESDP_SIM_FIXED && c->world > 1)
+    return fail(c, ESDP_E_STATE, "physical / bid-clearing / self-scheduled simulation needs every W row (world == 1)");
+  if ((mode == ESDP_SIM_CLEAR_BIDS || mode == ESDP_SIM_SELF) && c->kind == ESDP_PAYOFF_TABLE)
+    return fail(c, ESDP_E_STATE, "bid curves / lagged-price decisions are not defined for TABLE payoffs (R13)");
+  if (mode == ESDP_SIM_FIXED && !schedule_dev) return fail(c, ESDP_E_STATE, "the fixed-schedule mode needs a schedule");
+  if (actions_dev && mode == ESDP_SIM_CLEAR_BIDS) return fail(c, ESDP_E_STATE, "action recording: physical, self or fixed");
   if (mode == ESDP_SIM_CLEAR_BIDS && n_paths * c->A > c->stack_cap) {
     cudaFree(c->d_stack);
     c->d_stack = nullptr;
@@ -1424,6 +1443,7 @@ esdp_status esdp_simulate_mode_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, 
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
   mp.W = c->d_W; mp.F = c->d_F; mp.omw = c->d_omw; mp.stack = c->d_stack;
+  mp.schedule = schedule_dev; mp.actions = actions_dev;
   mp.mode = mode; mp.wrows = (int)w_rows(c); mp.ld = c->ld; mp.delta = c->delta; mp.s0 = c->s0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));
@@ -1433,6 +1453,12 @@ esdp_status esdp_simulate_mode_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, 
       mp, n_paths, seed, per_path_dev);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return mark_use(c, s);
+}
+
+esdp_status esdp_simulate_mode_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode, double* per_path_dev,
+                                   void* stream) {
+  if (c && mode == ESDP_SIM_FIXED) return fail(c, ESDP_E_STATE, "the fixed-schedule mode needs esdp_simulate_strategy_dev");
+  return esdp_simulate_strategy_dev(c, n_paths, seed, mode, nullptr, nullptr, per_path_dev, stream);
 }
 
 esdp_status esdp_simulate_mode(esdp_ctx* c, int64_t n_paths, uint64_t seed, int32_t mode, double* mean, double* var,

@@ -842,6 +842,26 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimParams sp, int64_t n, 
   simulate_block(sp, n, seed, out, ssm);
 }
 
+// Price-state paths of the lottery / strategy simulations (same draws as simulate_block): k_t and the
+// realised price lambda_{t,k_t} of every path; kp / lamp: [T][n] (either may be null).
+__global__ void __launch_bounds__(128) price_path_kernel(SimParams sp, int64_t n, uint64_t seed, int16_t* __restrict__ kp,
+                                                         double* __restrict__ lamp) {
+  const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (path >= n) return;
+  double u1, u2;
+  sim_uniforms(seed, path, 0, u1, u2);
+  int k = cdf_sample(sp.cdf1, sp.guide1, sp.K, sp.G, u1);
+  for (int t = 1; t <= sp.T; ++t) {
+    if (kp) kp[(size_t)(t - 1) * n + path] = (int16_t)k;
+    if (lamp) lamp[(size_t)(t - 1) * n + path] = __ldg(sp.lambda + (size_t)(t - 1) * sp.K + k);
+    if (t < sp.T) {
+      sim_uniforms(seed, path, t, u1, u2);
+      const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * sp.K + k;
+      k = cdf_sample(sp.cdf + row * sp.K, sp.guide + row * sp.G, sp.K, sp.G, u2);
+    }
+  }
+}
+
 inline size_t sim_smem_bytes(int A) { return (size_t)A * (3 * sizeof(double) + sizeof(int)) + 16; }
 
 // Deterministic two-pass reduction of per-path profits: sum (then sum of squared deviations).

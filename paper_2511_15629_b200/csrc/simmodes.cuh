@@ -19,6 +19,8 @@ struct SimModeParams {
   const double* F;       // [A] SoC change of each action (Eq. 2), energy units
   const double* omw;     // [A] 1 - w_a
   int16_t* stack;        // clear_bids: [n_paths][A] hull stacks (vertex-major per path: path + j * n)
+  const int16_t* schedule;  // fixed: [T] actions
+  int16_t* actions;      // nullable: [T][n_paths] chosen actions
   int mode, wrows, ld;
   double delta, s0;
 };
@@ -60,14 +62,19 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double s = mp.s0;                                    // physical mode: the real SoC, from s0 itself
   double profit = 0.0;
+  int k_prev = k;                                      // self-scheduled: last observed state and price
+  double lam_prev = __ldg(sp.lambda + k);              // stage 1's lag: its own price (R27)
   const double sbar_idx = (double)(S - 1);
   const double tol = 1e-9;
   for (int t = 1; t <= T; ++t) {
     sim_uniforms(seed, path, t, u1, u2);
-    const double* Wrow = mp.W + ((size_t)(t - 1) * mp.wrows + (sp.rank1 ? 0 : k)) * mp.ld;
+    const int wrow = sp.rank1 ? 0 : (mp.mode == 3 ? k_prev : k);   // self: persistence forecast of k_t
+    const double* Wrow = mp.W + ((size_t)(t - 1) * mp.wrows + wrow) * mp.ld;
     const double lam = __ldg(sp.lambda + (size_t)(t - 1) * K + k);
     int a_sel = 0;
-    if (mp.mode == 1) {
+    if (mp.mode == 4) {
+      a_sel = __ldg(mp.schedule + (t - 1));
+    } else if (mp.mode == 1 || mp.mode == 3) {
       double best = -INFINITY, best_s = s;
       int best_a = -1;
       for (int a = 0; a < A; ++a) {
@@ -85,7 +92,14 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
           const int fi = (int)f;
           wint = __dadd_rn(__dmul_rn(__dsub_rn(1.0, w), __ldcg(Wrow + fi)), __dmul_rn(w, __ldcg(Wrow + fi + 1)));
         }
-        const double cand = __dadd_rn(pay_of(t, k, a), wint);
+        double pay;
+        if (mp.mode == 3) {            // decided at the lagged price (linear payoffs only)
+          pay = __dmul_rn(lam_prev, s_act[a]);
+          if (sp.kind == 1) pay = __dsub_rn(pay, s_g[a]);
+        } else {
+          pay = pay_of(t, k, a);
+        }
+        const double cand = __dadd_rn(pay, wint);
         if (cand > best) { best = cand; best_a = a; best_s = sn; }
       }
       a_sel = best_a;
@@ -141,7 +155,10 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
         prev_price = pj; u_prev = u; p_prev = pc;
       }
     }
-    profit = __dadd_rn(profit, pay_of(t, k, a_sel));
+    if (mp.actions) mp.actions[(size_t)(t - 1) * n + path] = (int16_t)a_sel;
+    profit = __dadd_rn(profit, pay_of(t, k, a_sel));   // settled at the realised price
+    lam_prev = lam;
+    k_prev = k;
     if (mp.mode == 2) {
       const double wa = s_w[a_sel];
       i = i + (s_ow[a_sel] >> 1) + ((wa > 0.0 && u1 < wa) ? 1 : 0);

@@ -537,3 +537,80 @@ def test_cfg4_full_year_sampled_stages():
             assert np.array_equal(s.policy(t), pol_ref), t
         V1, _ = s.values(1)
         assert J == oracle.objective(pr, V1)
+
+
+@pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg3", "random-g"])
+def test_strategy_modes_bitexact(name):
+    """NEXT-2 dispatch strategies on the GPU equal the oracle path by path: physical (bid-curve) dispatch
+    with recorded actions, self-scheduled at the lagged price, and a fixed schedule settled at the
+    realised prices."""
+    import torch
+    if name == "cfg3":
+        base = workloads.cfg2(T=2, K=2)
+        inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=20, K=12)
+    elif name == "random-g":
+        inst = workloads.random_instance(62, T=7, K=3, S_max=150)
+        act = oracle.actions(to_oracle(inst))
+        inst.payoff_kind = workloads.PAYOFF_LINEAR_MINUS_G
+        inst.g = workloads.random_g(62, len(act), 3.0)
+    else:
+        inst = workloads.cfg1("b", rank1=name.endswith("rank1"))
+        inst.s0 = inst.sbar * 0.5 + 0.3 * inst.delta
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr)
+    n = 1500
+    with _gpu(inst) as s:
+        s.backward()
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        acts = torch.empty(inst.T * n, dtype=torch.int16, device="cuda")
+        for mode, omode in ((E.ESDP_SIM_PHYSICAL, oracle.SIM_PHYSICAL), (E.ESDP_SIM_SELF, oracle.SIM_SELF)):
+            want, wact = oracle.simulate_strategy(pr, ref.W, omode, n, seed=17, want_actions=True)
+            E.esdp_simulate_strategy_dev(s.ctx, n, 17, mode, out.data_ptr(), actions_ptr=acts.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), want), mode
+            assert np.array_equal(acts.cpu().numpy().reshape(inst.T, n), wact), mode
+        sched = wact[:, 3].copy()
+        want, _ = oracle.simulate_strategy(pr, None, oracle.SIM_FIXED, n, seed=17, schedule=sched)
+        sd = torch.from_numpy(sched).cuda()
+        E.esdp_simulate_strategy_dev(s.ctx, n, 17, E.ESDP_SIM_FIXED, out.data_ptr(), schedule_ptr=sd.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_price_paths_and_perfect_foresight():
+    """esdp_price_paths_dev returns the realised prices of the simulation's paths (a constant schedule
+    settles to p times their running sum, bit for bit); one context with K = n paths and identity
+    transitions then solves every path's deterministic (perfect-foresight) DP, equal to the oracle's K = 1
+    solve of that path."""
+    import torch
+    inst = workloads.cfg1("b")
+    pr = to_oracle(inst)
+    n = 12
+    with _gpu(inst) as s:
+        s.backward()
+        lamp = torch.empty(inst.T * n, dtype=torch.float64, device="cuda")
+        E.esdp_price_paths_dev(s.ctx, n, 23, lambda_ptr=lamp.data_ptr())
+        act = s.actions()
+        a = int(np.argmax(act))                                   # a constant schedule of the top power
+        sd = torch.full((inst.T,), a, dtype=torch.int16, device="cuda")
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        E.esdp_simulate_strategy_dev(s.ctx, n, 23, E.ESDP_SIM_FIXED, out.data_ptr(), schedule_ptr=sd.data_ptr())
+        torch.cuda.synchronize()
+        lam = lamp.cpu().numpy().reshape(inst.T, n)
+        got = out.cpu().numpy()
+    for j in range(n):
+        acc = 0.0
+        for t in range(inst.T):
+            acc = acc + lam[t, j] * act[a]
+        assert got[j] == acc
+    # perfect foresight: K = n deterministic paths, identity transitions
+    pf = workloads.Instance("pf", inst.T, n, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
+                            lam.copy(), np.broadcast_to(np.eye(n), (inst.T - 1, n, n)).copy(), np.full(n, 1.0 / n))
+    with _gpu(pf) as s:
+        s.backward()
+        V1, _ = s.values(1)
+    i0 = int(round(inst.s0 / inst.delta))
+    for j in range(n):
+        one = workloads.Instance("pf1", inst.T, 1, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
+                                 lam[:, j:j + 1].copy(), np.ones((inst.T - 1, 1, 1)), np.array([1.0]))
+        assert V1[j, i0] == oracle.backward(to_oracle(one)).J

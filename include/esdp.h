@@ -65,9 +65,6 @@ enum {
   ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
   ESDP_DMMA_L2 = 64u,     /* DMMA expectation with operands read straight from L2 by every warp
                              (instead of staged once per block in shared memory) */
-  ESDP_CHAIN = 128u,      /* graph plan on one GPU with kept values: tile-level readiness counters between
-                             the stage kernels instead of whole-grid dependencies (opt-in: measured
-                             slower on B200, 13.4 vs 10.3 us per cfg2 stage) */
   ESDP_PERSIST = 32u      /* single GPU: run the backward pass as ONE persistent dataflow kernel (a
                              device-side ready queue of per-tile stencil / expectation tasks, no grid
                              barrier) instead of a CUDA graph of 2T kernels (opt-in: measured slower

@@ -33,7 +33,6 @@ ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
 ESDP_PERSIST = 32
 ESDP_DMMA_L2 = 64
-ESDP_CHAIN = 128
 ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS, ESDP_SIM_SELF, ESDP_SIM_FIXED = 0, 1, 2, 3, 4
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
@@ -357,15 +356,13 @@ class Solver:
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
     def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=True, dmma=True, persist=False,
-                 chain=False,
                  dist=None):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
                                (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
                                | (ESDP_FORCE_BRUTE if force_brute else 0) | (0 if pdl else ESDP_NO_PDL)
-                               | (0 if dmma else ESDP_NO_DMMA) | (ESDP_PERSIST if persist else 0)
-                               | (ESDP_CHAIN if chain else 0), dist=dist)
+                               | (0 if dmma else ESDP_NO_DMMA) | (ESDP_PERSIST if persist else 0), dist=dist)
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
         self.stencil_kind = esdp_stencil_kind(self.ctx)
 

@@ -137,12 +137,6 @@ struct esdp_ctx {
   int prof_stride = 1;
   bool pdl = true;
   int dmma2 = 0;   // shared-memory-staged DMMA expectation (set when its tile fits)
-  // tile-level readiness between the chain's kernels (kernels.cuh ChainSync; opt-in ESDP_CHAIN): [0]
-  // epoch, then the stencils' per-tile row counters vcnt[T+2][ntile] and the expectation's per-column-
-  // block counters wcnt[T+2][ncb]; graph plan on one GPU with kept values and PDL
-  bool chain = false;
-  unsigned long long* d_chain = nullptr;
-  int chain_ntile = 0, chain_tile_w = 0, chain_ncb = 0, chain_cb_w = 0, chain_nrb = 0;
   bool solved = false;
   std::string err;
 };
@@ -447,7 +441,7 @@ void free_all(esdp_ctx* c) {
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
   if (c->copy) cudaStreamDestroy(c->copy);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_chain, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -561,19 +555,8 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-unsigned long long* chain_v(esdp_ctx* c, int t) { return c->d_chain + 1 + (size_t)t * c->chain_ntile; }
-unsigned long long* chain_w(esdp_ctx* c, int t) {
-  return c->d_chain + 1 + (size_t)(c->T + 2) * c->chain_ntile + (size_t)t * c->chain_ncb;
-}
-
-// The contraction of stage t (t < T): W_t = P_t V_{t+1}.  chain: wait for V_{t+1}'s tiles and publish
-// W_t's column blocks through the readiness counters instead of whole-grid dependencies.
-cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool chain = false) {
-  ChainSync cs{};
-  if (chain && c->chain) {
-    cs.in = chain_v(c, t + 1); cs.out = chain_w(c, t); cs.epoch = c->d_chain;
-    cs.in_need = c->k_cnt; cs.in_width = c->chain_tile_w; cs.out_width = c->chain_cb_w;
-  }
+// The contraction of stage t (t < T): W_t = P_t V_{t+1}.
+cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int K = c->K, S = c->S;
   const int rows = c->rank1 ? 1 : c->k_cnt;   // own rows of W_t (all rows on one GPU)
   if (rows == 0) return cudaSuccess;
@@ -582,7 +565,7 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool c
     if (c->dmma2) {
       const int ncb = (S + kDC * 16 - 1) / (kDC * 16), nrb = (rows + kDR * 8 - 1) / (kDR * 8);
       return launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, pdl, Pt,
-                    (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb, cs);
+                    (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
     }
     const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
     return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
@@ -590,7 +573,7 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool c
   }
   dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
   return launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, Pt, (const double*)V_of(c, t + 1),
-                W_of(c, t), rows, K, S, c->ld, cs);
+                W_of(c, t), rows, K, S, c->ld);
 }
 
 // Stage-invariant parameters of the window and brute-force stencils (W/V/pol/lambda set per launch).
@@ -619,14 +602,7 @@ StencilParams stencil_params(const esdp_ctx* c) {
 }
 
 // The max-plus stencil of stage t: V_t, pol_t from W_t (window or brute force).
-cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute, bool chain = false) {
-  ChainSync cs{};
-  if (chain && c->chain) {
-    if (t < c->T) {   // W_T is a memset before the first stencil: no readiness to wait for
-      cs.in = chain_w(c, t); cs.in_need = c->chain_nrb; cs.in_width = c->chain_cb_w;
-    }
-    cs.out = chain_v(c, t); cs.out_width = c->chain_tile_w; cs.epoch = c->d_chain;
-  }
+cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute) {
   const int S = c->S;
   const int K = c->k_cnt;                      // stencil rows of this rank (local k = global k - k_lo)
   if (K == 0) return cudaSuccess;
@@ -636,14 +612,12 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
   if (c->use_window && !force_brute) {
     WinParams wp = win_params(c);
     wp.W = Wt; wp.V = V_of(c, t) + (size_t)c->k_lo * c->ld; wp.pol = pol; wp.lambda_t = lam;
-    return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp,
-                  cs);
+    return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
   }
   StencilParams prm = stencil_params(c);
   prm.W = Wt; prm.V = V_of(c, t) + (size_t)c->k_lo * c->ld; prm.pol = pol; prm.lambda_t = lam;
   prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + ((size_t)(t - 1) * c->K + c->k_lo) * c->A : c->d_g;
-  return launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl, prm,
-                cs);
+  return launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl, prm);
 }
 
 cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
@@ -804,11 +778,6 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   bool forked = false;
   std::vector<char> side_used(c->side.size(), 0);
-  if (c->chain) {   // the pass number that the readiness counters are compared against
-    epoch_kernel<<<1, 1, 0, s>>>(c->d_chain);
-    CUDA_OR_FAIL(c, cudaGetLastError());
-    ++n;
-  }
   for (int t = T; t >= 1; --t) {
     if (t == T) {
       CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, t), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
@@ -821,7 +790,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
           after_kernel = false;
         }
       CUDA_OR_FAIL(c, mark(t, 0));
-      CUDA_OR_FAIL(c, launch_contract(c, t, s, pdl && after_kernel && !sampled(t), true));
+      CUDA_OR_FAIL(c, launch_contract(c, t, s, pdl && after_kernel && !sampled(t)));
       CUDA_OR_FAIL(c, mark(t, 1));
       after_kernel = true;
       ++n;
@@ -846,7 +815,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
       }
     }
     CUDA_OR_FAIL(c, mark(t, 2));
-    CUDA_OR_FAIL(c, launch_stencil(c, t, s, pdl && after_kernel && !sampled(t), false, true));
+    CUDA_OR_FAIL(c, launch_stencil(c, t, s, pdl && after_kernel && !sampled(t), false));
     CUDA_OR_FAIL(c, mark(t, 3));
     after_kernel = !sampled(t);
     ++n;
@@ -1151,26 +1120,6 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
       c->persist_smem = sm;
     }
     cudaGetLastError();
-  }
-  {   // readiness counters between the chain's kernels (opt-in; graph plan, one GPU, kept values, PDL)
-    const int rows = c->rank1 ? 1 : c->k_cnt;
-    const bool dmma2_path = rows >= 8 && !(c->flags & ESDP_NO_DMMA) && c->dmma2;
-    const bool dfma_path = rows < 8 || (c->flags & ESDP_NO_DMMA);
-    c->chain = (c->flags & ESDP_CHAIN) && c->pdl && keep(c) && world == 1 && !nccl_id && !c->persist &&
-               (dmma2_path || dfma_path);
-    if (c->chain) {
-      c->chain_tile_w = c->use_window ? kWinTile : kTile;
-      c->chain_ntile = (c->S + c->chain_tile_w - 1) / c->chain_tile_w;
-      c->chain_cb_w = dmma2_path ? kDC * 16 : kColsC;
-      c->chain_ncb = (c->S + c->chain_cb_w - 1) / c->chain_cb_w;
-      c->chain_nrb = dmma2_path ? (rows + kDR * 8 - 1) / (kDR * 8) : (rows + kRowsC - 1) / kRowsC;
-      const size_t nch = 1 + (size_t)(T + 2) * (c->chain_ntile + c->chain_ncb);
-      TRY(dev_alloc(c, &c->d_chain, nch));
-      if (cudaMemset(c->d_chain, 0, nch * sizeof(unsigned long long)) != cudaSuccess) {
-        fail(c, ESDP_E_CUDA, "chain counters");
-        return bail(ESDP_E_CUDA);
-      }
-    }
   }
   if (c->flags & ESDP_PROFILE) {
     c->prof_stride = std::max(1, c->T / 16);
@@ -1715,11 +1664,11 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
       if (!b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
         const int ncb = (int)((NL + kDC * 16 - 1) / (kDC * 16)), nrb = (K + kDR * 8 - 1) / (kDR * 8);
         e = launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, after_kernel,
-                   Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ncb, ChainSync{});
+                   Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ncb);
       } else {
         dim3 grid((unsigned)((NL + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
         e = launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, after_kernel, Pt,
-                   (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ChainSync{});
+                   (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL);
       }
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch contraction: %s", cudaGetErrorString(e));
       after_kernel = true;

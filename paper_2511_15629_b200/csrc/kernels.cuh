@@ -23,75 +23,6 @@ __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  //
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// Tile-level readiness between the kernels of the stage chain (opt-in per launch, see esdp.cu
-// ChainFlags).  Instead of griddepcontrol.wait (the whole previous grid complete and flushed), a block
-// waits only for the producer blocks of the columns it reads: monotone 64-bit counters, one per column
-// group of the producer, bumped once per producer block per backward pass, so "ready in pass e" is
-// counter >= e * need (no resets).  The block then triggers its dependents at once (they launch when
-// every block of this grid has its inputs, so the look-ahead is one kernel and every producer block is
-// already resident: no deadlock), and after its stores it publishes with a release fence + atomicAdd.
-struct ChainSync {
-  const unsigned long long* in;      // counters of the producer's column groups (null: griddepcontrol.wait)
-  unsigned long long* out;           // this kernel's counters (null: none)
-  const unsigned long long* epoch;   // backward-pass number (device; bumped by the graph's first node)
-  int in_need, in_width, out_width;  // producer blocks per group and pass; column widths of in / out groups
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Wait for the column range [lo, hi] of the input (all threads call it).  Warp 0 polls all the groups
-// at once (one lane per group, relaxed loads, a warp vote), then acquires with one fence, so a ready
-// input costs one L2 round trip.
-__device__ __forceinline__ void chain_wait(const ChainSync& cs, int lo, int hi) {
-  if (!cs.in) { pdl_wait(); return; }
-  if (threadIdx.x < 32) {
-    const unsigned long long target = *(volatile const unsigned long long*)cs.epoch * (unsigned long long)cs.in_need;
-    const int g0 = lo / cs.in_width, g1 = hi / cs.in_width;
-    for (int gb = g0; gb <= g1; gb += 32) {
-      const int g = gb + (int)threadIdx.x;
-      const volatile unsigned long long* p = cs.in + (g <= g1 ? g : g1);
-      unsigned ns = 32;
-      long long spins = 0;
-      while (!__all_sync(0xffffffffu, *p >= target)) {
-#ifndef ESDP_CHAIN_SPIN
-        __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : 256;
-#endif
-        if (++spins > (1ll << 28)) __trap();      // seconds: a broken dependency aborts instead of hanging
-      }
-    }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  }
-  __syncthreads();
-#ifndef ESDP_CHAIN_LATE
-  pdl_trigger();   // inputs ready in every block -> dependents may launch (they wait on our counters)
-#endif
-}
-
-// First node of a backward graph that uses readiness counters: the pass number.
-__global__ void epoch_kernel(unsigned long long* epoch) { *epoch += 1ull; }
-
-// Publish this block's output columns (all threads call it, after their last stores).
-__device__ __forceinline__ void chain_signal(const ChainSync& cs, int col) {
-  if (!cs.out) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#ifdef ESDP_CHAIN_REDREL
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cs.out + col / cs.out_width) : "memory");
-#else
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    atomicAdd(cs.out + col / cs.out_width, 1ull);
-#endif
-  }
-#ifdef ESDP_CHAIN_LATE
-  pdl_trigger();
-#endif
-}
-
 // A maximal run of actions whose offsets are consecutive integers decreasing by one and whose
 // interpolation weight is 0 ("recombining" interior of Eq. 10), or a single action.
 struct Seg {
@@ -147,14 +78,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __restrict__ Pt,   // [rows][K]
                                                              const double* __restrict__ Vn,   // [K][ld]
                                                              double* __restrict__ Wt,         // [rows][ld]
-                                                             int rows, int K, int S, int ld, ChainSync cs) {
+                                                             int rows, int K, int S, int ld) {
   extern __shared__ __align__(16) double csm[];
   const int Kp = pad4(K);
   double* vs = csm;                        // [Kp][kColsC]
   double* ps = csm + (size_t)Kp * kColsC;  // [kRowsC][Kp]
   const int i0 = blockIdx.x * kColsC, r0 = blockIdx.y * kRowsC;
   const int tid = threadIdx.x;
-  if (!cs.in) pdl_trigger();
+  pdl_trigger();
   for (int r = 0; r < kRowsC; ++r) {  // P tile rows (inputs: staged before the dependency wait)
     const bool rin = r0 + r < rows;
     const double* src = Pt + (size_t)(r0 + r) * K;
@@ -163,7 +94,7 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
       else ps[r * Kp + kp] = 0.0;
     }
   }
-  chain_wait(cs, i0, min(i0 + kColsC, S) - 1);   // V_{t+1} is the previous stencil's output
+  pdl_wait();                          // V_{t+1} is the previous stencil's output
   {  // V tile: 16 two-double chunks per row, 8 rows per pass (no runtime division)
     const int c = 2 * (tid & 15);
     const bool in = i0 + c < ld;
@@ -208,7 +139,6 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
     if (i < S) Wt[(size_t)(r0 + rr + 1) * ld + i] = a10;
     if (i + 1 < S) Wt[(size_t)(r0 + rr + 1) * ld + i + 1] = a11;
   }
-  chain_signal(cs, i0);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -311,10 +241,10 @@ inline size_t contract_dmma2_smem(int K, int DC = kDC) {
 // One (kDR*8) x (DC*16) tile of W_t = P_t V_{t+1} by kDR*DC warps: P rows and the V column block are
 // staged in shared memory (cp.async), then every warp runs its 8x16 DMMA chain over k'.  kPdl: the P
 // staging (an input) happens before the programmatic dependency wait, the V staging after it.
-template <int DC, class WaitFn>
+template <int DC, bool kPdl>
 __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const double* __restrict__ Vn,
                                            double* __restrict__ Wt, int rows, int K, int S, int ld, int r0, int i0,
-                                           double* dsm, WaitFn wait_inputs) {
+                                           double* dsm) {
   constexpr int kD2Threads = kDR * DC * 32, kDC = DC;
   const int Kp = (K + 3) & ~3;
   constexpr int RB = kDR * 8, CB = kDC * 16;
@@ -341,7 +271,7 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
       }
     }
   }
-  wait_inputs();
+  if (kPdl) pdl_wait();
   {  // V tile: CB/2 two-double chunks per row
     constexpr int CH = CB / 2;
     for (int e = tid; e < Kp * CH; e += kD2Threads) {
@@ -380,13 +310,10 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
 __global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
                                                                    const double* __restrict__ Vn,   // [K][ld]
                                                                    double* __restrict__ Wt,         // [rows][ld]
-                                                                   int rows, int K, int S, int ld, int ncb, ChainSync cs) {
+                                                                   int rows, int K, int S, int ld, int ncb) {
   extern __shared__ __align__(16) double dsm[];
-  const int i0 = (blockIdx.x % ncb) * (kDC * 16);
-  dmma2_tile<kDC>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (kDR * 8), i0, dsm,
-                  [&] { chain_wait(cs, i0, min(i0 + kDC * 16, S) - 1); });
-  chain_signal(cs, i0);
-  if (!cs.in) pdl_trigger();   // late trigger: dependents launch as this grid drains, without holding SM slots early
+  dmma2_tile<kDC, true>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (kDR * 8), (blockIdx.x % ncb) * (kDC * 16), dsm);
+  pdl_trigger();   // late trigger: dependents launch as this grid drains, without holding SM slots early
 }
 
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
@@ -531,15 +458,11 @@ __device__ __forceinline__ void stencil_item(const StencilParams& prm, int k, in
   }
 }
 
-__global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm, ChainSync cs) {
+__global__ void __launch_bounds__(kStencilWarps * 32) stencil_kernel(StencilParams prm) {
   extern __shared__ double smem[];
-  const int i0 = blockIdx.x * kTile;
-  // W_t is the previous contraction's output: columns [i0 + o_min - 1, i0 + kTile + o_max + 1]
-  chain_wait(cs, max(0, i0 + prm.o_min - 1), min(prm.S - 1, i0 + kTile + prm.o_min + prm.o_span + 1));
-  stencil_item(prm, blockIdx.y, i0, smem);
-  __syncthreads();
-  chain_signal(cs, i0);
-  if (!cs.in) pdl_trigger();
+  pdl_wait();                          // W_t is the previous contraction's output
+  stencil_item(prm, blockIdx.y, blockIdx.x * kTile, smem);
+  pdl_trigger();
 }
 
 inline size_t stencil_smem_bytes(int A, int o_span) {

@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(kPersistThreads, 4) backward_persistent_kernel
       if (pp.rank1) {
         gemv_cols(pp.pi + (size_t)t * pp.K, Vn, Wt, pp.K, pp.S, pp.ld, b * pp.ecw + tid);
       } else {
-        dmma2_tile<kDfDC>(pp.P + (size_t)(t - 1) * pp.K * pp.K, Vn, Wt, pp.rows, pp.K, pp.S, pp.ld,
-                          a * kDfRows, b * kDfCols, psm, [] {});
+        dmma2_tile<kDfDC, false>(pp.P + (size_t)(t - 1) * pp.K * pp.K, Vn, Wt, pp.rows, pp.K, pp.S, pp.ld,
+                                 a * kDfRows, b * kDfCols, psm);
       }
     }
     __syncthreads();

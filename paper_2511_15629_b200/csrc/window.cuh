@@ -318,15 +318,11 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   p.pol[(size_t)k * p.S + i] = (int16_t)arg;
 }
 
-__global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p, ChainSync cs) {
+__global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
-  const int i0 = blockIdx.x * kWinTile;
-  // W_t is the previous contraction's output: columns [i0 + o_min - 1, i0 + kWinTile + o_max + 1]
-  chain_wait(cs, max(0, i0 + p.o_min - 1), min(p.S - 1, i0 + kWinTile + p.o_max + 1));
-  window_item(p, blockIdx.y, i0, wsm);
-  __syncthreads();
-  chain_signal(cs, i0);
-  if (!cs.in) pdl_trigger();
+  pdl_wait();                          // W_t is the previous contraction's output
+  window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
+  pdl_trigger();
 }
 
 }  // namespace esdp

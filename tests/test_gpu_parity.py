@@ -614,30 +614,3 @@ def test_price_paths_and_perfect_foresight():
         one = workloads.Instance("pf1", inst.T, 1, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                  lam[:, j:j + 1].copy(), np.ones((inst.T - 1, 1, 1)), np.array([1.0]))
         assert V1[j, i0] == oracle.backward(to_oracle(one)).J
-
-
-@pytest.mark.parametrize("name", ["cfg2", "cfg2-rank1", "cfg1b-brute", "cfg3"])
-def test_chain_readiness_counters(name):
-    """The graph plan with tile-level readiness counters between the stage kernels (ESDP_CHAIN) gives the
-    same bits as full-grid dependencies and the oracle, on repeated passes (the pass number advances) and
-    after diagnostic launches of single kernels in between."""
-    brute = name.endswith("brute")
-    if name == "cfg3":
-        base = workloads.cfg2(T=2, K=2)
-        inst = workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=30, K=40)
-    elif name.startswith("cfg1"):
-        inst = workloads.cfg1("b")
-    else:
-        inst = workloads.cfg2(T=40, K=100, rank1=name.endswith("rank1"))
-    ref = oracle.backward(to_oracle(inst), nthreads=16)
-    with E.Solver(inst, force_brute=brute, chain=True) as a, E.Solver(inst, force_brute=brute) as b:
-        for rep in range(4):
-            Ja, Jb = a.backward(), b.backward()
-            assert Ja == Jb == ref.J
-            if rep == 1:
-                E.esdp_debug_time(a.ctx, 0, 5)
-                E.esdp_debug_time(a.ctx, 1, 5)
-        for t in range(1, inst.T + 1):
-            Va, Wa = a.values(t)
-            assert np.array_equal(Va, ref.V[t - 1]) and np.array_equal(Wa, ref.W[t - 1]), t
-            assert np.array_equal(a.policy(t), ref.pol[t - 1]), t

@@ -968,7 +968,12 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     return bail(ESDP_E_CUDA);
   }
   const size_t T = c->T, K = c->K, S = c->S, A = c->A;
-  c->G = std::max<int>(64, 4 * (int)K);   // guide buckets per cdf row (most of them pure: one load per draw)
+  {   // guide buckets per cdf row: most buckets pure (one load per draw); 16 K where the tables stay
+      // under ~512 MB, at least 4 K
+    const double rows = (double)(c->rank1 ? T : (T - 1) * K) + 1.0;
+    const int cap = (int)std::min(32767.0, 256e6 / rows);
+    c->G = std::max<int>(64, std::max<int>(4 * (int)K, std::min<int>(16 * (int)K, cap)));
+  }
   if (!tables_only) {   // two input slots (double-buffered loads); the aliases follow select_slot
     for (InputSlot& x : c->slot) {
       TRY(dev_alloc(c, &x.lambda, T * K));

@@ -815,14 +815,17 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double profit = 0.0;
   const size_t KS = (size_t)sp.Kp * sp.S;
+  sim_uniforms(seed, path, 1, u1, u2);
   for (int t = 1; t <= sp.T; ++t) {
-    sim_uniforms(seed, path, t, u1, u2);
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
     int kn = k;
     if (t < sp.T) {
       const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * sp.K + k;
       kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + row * sp.G, sp.K, sp.G, u2);
     }
+    // the next stage's draws do not depend on the state: computed while this stage's loads are in flight
+    const double u1t = u1;
+    if (t < sp.T) sim_uniforms(seed, path, t + 1, u1, u2);
     double p;
     if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
     else {
@@ -831,7 +834,7 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
     }
     profit = __dadd_rn(profit, p);
     const double wa = s_w[a];
-    i = i + s_off[a] + ((wa > 0.0 && u1 < wa) ? 1 : 0);
+    i = i + s_off[a] + ((wa > 0.0 && u1t < wa) ? 1 : 0);
     k = kn;
   }
   out[path] = profit;

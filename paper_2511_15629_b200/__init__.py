@@ -419,7 +419,8 @@ class Batch:
                                     float(inst.eta_c), float(inst.eta_d), float(inst.delta),
                                     0 if act is None else int(act.shape[0]), _p(act), _p(lam), _p(P), _p(pi),
                                     int(getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR)), _p(g),
-                                    ESDP_FORCE_BRUTE if force_brute else 0)
+                                    ESDP_FORCE_BRUTE if (force_brute[j] if isinstance(force_brute, (list, tuple))
+                                                         else force_brute) else 0)
         out = _vp()
         st = lib.esdp_create_batch(probs, len(insts), ctypes.byref(out))
         if st != ESDP_OK:

@@ -192,6 +192,18 @@ def table1_deterministic(delta: float = 0.01, T: int = 8784, seed: int = SEED_BA
                     np.ascontiguousarray(lam.reshape(T, 1)), np.ones((T - 1, 1, 1)), np.ones(1))
 
 
+def table3(hours: float = 100.0, delta: float = 0.01, T: int = 8784, R: int = 200,
+           seed: int = SEED_BASE + 7) -> Instance:
+    """The paper's Table 3 GPU-timing workload with synthetic prices: one year of hourly
+    stages, a 1-MW battery of `hours` hours (S = hours/delta + 1; 100 h at delta = 0.01 gives S = 10001,
+    A = 203), R = 200 equally likely price samples per hour (stagewise independent: rank-1, pi_t = 1/R,
+    S:470), the ISO-NE-shaped hour-of-day/season profile plus spread quantiles."""
+    lam, _, _ = price_chain(T, R, 1.0, seed=seed, season=True)
+    pi = np.full((T, R), 1.0 / R)
+    eta = math.sqrt(0.85)
+    return Instance(f"table3-{hours:g}h-delta{delta}", T, R, 1.0, hours, 0.0, eta, eta, delta, lam, None, pi)
+
+
 def cfg4(T: int = 8760, K: int = 200) -> Instance:
     """Full-year hourly horizon: T=8760, S=2001, A=401, K=200, per-stage P_t (pbar/delta = 199)."""
     lam, P, pi1 = price_chain(T, K, 1.0, per_stage_rho=True, seed=SEED_BASE + 4, season=True)

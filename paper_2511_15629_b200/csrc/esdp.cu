@@ -563,9 +563,15 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
     if (c->dmma2) {
+      if (K > 128) {   // large K: taller tiles (fewer re-reads of the V column block)
+        const int ncb = (S + kDCbig * 16 - 1) / (kDCbig * 16), nrb = (rows + kDRbig * 8 - 1) / (kDRbig * 8);
+        return launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
+                      contract_dmma2_smem(K, kDRbig, kDCbig), s, pdl, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows,
+                      K, S, c->ld, ncb);
+      }
       const int ncb = (S + kDC * 16 - 1) / (kDC * 16), nrb = (rows + kDR * 8 - 1) / (kDR * 8);
-      return launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, pdl, Pt,
-                    (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
+      return launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, pdl,
+                    Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
     }
     const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
     return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
@@ -1093,10 +1099,14 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     }
   }
   if (contract_smem_bytes(K) > 227 * 1024) { fail(c, ESDP_E_CONFIG, "K too large for the contraction tile"); return bail(ESDP_E_CONFIG); }
-  c->dmma2 = !(c->flags & ESDP_DMMA_L2) && contract_dmma2_smem(K) <= 200 * 1024;
-  if (c->dmma2 && contract_dmma2_smem(K) > 48 * 1024 &&
-      cudaFuncSetAttribute(contract_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K)) != cudaSuccess)
-    c->dmma2 = 0;
+  {
+    const size_t sm2 = K > 128 ? contract_dmma2_smem(K, kDRbig, kDCbig) : contract_dmma2_smem(K);
+    c->dmma2 = !(c->flags & ESDP_DMMA_L2) && sm2 <= 200 * 1024;
+    if (c->dmma2 && sm2 > 48 * 1024 &&
+        (K > 128 ? cudaFuncSetAttribute(contract_dmma2_kernel<kDRbig, kDCbig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)
+                 : cudaFuncSetAttribute(contract_dmma2_kernel<kDR, kDC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+      c->dmma2 = 0;
+  }
   if (contract_smem_bytes(K) > 48 * 1024)
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)
@@ -1108,7 +1118,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     size_t sm = std::max(c->use_window ? c->window_smem : c->stencil_smem, 2 * sizeof(double) * (size_t)K);
     sm = std::max(sm, c->stencil_smem);
-    if (!c->rank1) sm = std::max(sm, contract_dmma2_smem(K, kDfDC));
+    if (!c->rank1) sm = std::max(sm, contract_dmma2_smem(K, kDfDR, kDfDC));
     if (sm <= 200 * 1024 &&
         cudaFuncSetAttribute(backward_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_persistent_kernel, kPersistThreads, sm) == cudaSuccess &&
@@ -1666,9 +1676,14 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
     } else {
       const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
       cudaError_t e;
-      if (!b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
+      if (!b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
+        const int ncb = (int)((NL + kDCbig * 16 - 1) / (kDCbig * 16)), nrb = (K + kDRbig * 8 - 1) / (kDRbig * 8);
+        e = launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
+                   contract_dmma2_smem(K, kDRbig, kDCbig), s, after_kernel, Pt, (const double*)V_at(t + 1), b->d_W, rows,
+                   K, (int)NL, (int)NL, ncb);
+      } else if (!b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
         const int ncb = (int)((NL + kDC * 16 - 1) / (kDC * 16)), nrb = (K + kDR * 8 - 1) / (kDR * 8);
-        e = launch(contract_dmma2_kernel, dim3(ncb * nrb), dim3(kD2Threads), contract_dmma2_smem(K), s, after_kernel,
+        e = launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, after_kernel,
                    Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ncb);
       } else {
         dim3 grid((unsigned)((NL + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
@@ -1824,7 +1839,10 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   if (b->win_smem > 48 * 1024)
     BCUDA(b, cudaFuncSetAttribute(window_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->win_smem));
   if (contract_dmma2_smem(K) > 48 * 1024 && contract_dmma2_smem(K) <= 200 * 1024)
-    cudaFuncSetAttribute(contract_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K));
+    cudaFuncSetAttribute(contract_dmma2_kernel<kDR, kDC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K));
+  if (K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) > 48 * 1024 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024)
+    cudaFuncSetAttribute(contract_dmma2_kernel<kDRbig, kDCbig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)contract_dmma2_smem(K, kDRbig, kDCbig));
   if (contract_smem_bytes(K) > 48 * 1024)
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)

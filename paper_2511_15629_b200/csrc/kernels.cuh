@@ -224,40 +224,43 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const do
 // [kDR*8][Kp] and the V tile [Kp][kDC*16] are staged once per block with cp.async (so every L2 byte is
 // read by one block, not by every warp), then each warp runs its 8x16 tile's DMMA chain from shared
 // memory.  cfg2: 7 x 21 = 147 blocks of 6 warps (one per SM).
-#ifndef ESDP_KDR
-#define ESDP_KDR 1
-#endif
-#ifndef ESDP_KDC
-#define ESDP_KDC 3
-#endif
-constexpr int kDR = ESDP_KDR, kDC = ESDP_KDC;   // expectation tile: kDR*8 rows x kDC*16 columns, kDR*kDC warps
-constexpr int kD2Threads = kDR * kDC * 32;
+// Expectation tiles: DR*8 rows x DC*16 columns per block, DR*DC warps (one 8x16 sub-tile each).  The host
+// picks (1, 3) for K <= 128 and (4, 3) above (measured: cfg2 and cfg4 chains).
+constexpr int kDR = 1, kDC = 3;            // small-K tile
+constexpr int kDRbig = 4, kDCbig = 3;      // large-K tile
 
-inline size_t contract_dmma2_smem(int K, int DC = kDC) {
+// Shared-memory row strides chosen for the DMMA operand loads: a lane (kq, g) reads A[g][kq + 4q] and
+// B[kq + 4q][g]; a warp-wide 8-byte load takes at least 2 wavefronts, reached when the 32 addresses are
+// distinct mod 16 doubles: A stride = 4 or 12 (mod 16), B stride = 8 (mod 16).
+__host__ __device__ constexpr int dmma2_stride_a(int Kp) { return (Kp % 16 == 0 || Kp % 16 == 8) ? Kp + 4 : Kp; }
+__host__ __device__ constexpr int dmma2_stride_b(int CB) { return CB + (8 - CB % 16 + 16) % 16; }
+
+inline size_t contract_dmma2_smem(int K, int DR = kDR, int DC = kDC) {
   const int Kp = (K + 3) & ~3;
-  return sizeof(double) * (size_t)Kp * (kDR * 8 + DC * 16);
+  return sizeof(double) * ((size_t)(DR * 8) * dmma2_stride_a(Kp) + (size_t)Kp * dmma2_stride_b(DC * 16));
 }
 
-// One (kDR*8) x (DC*16) tile of W_t = P_t V_{t+1} by kDR*DC warps: P rows and the V column block are
-// staged in shared memory (cp.async), then every warp runs its 8x16 DMMA chain over k'.  kPdl: the P
-// staging (an input) happens before the programmatic dependency wait, the V staging after it.
-template <int DC, bool kPdl>
+// One (DR*8) x (DC*16) tile of W_t = P_t V_{t+1} by DR*DC warps: P rows and the V column block are staged
+// in shared memory (cp.async), then every warp runs its 8x16 DMMA chain over k'.  kPdl: the P staging
+// (an input) happens before the programmatic dependency wait, the V staging after it.
+template <int DR, int DC, bool kPdl>
 __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const double* __restrict__ Vn,
                                            double* __restrict__ Wt, int rows, int K, int S, int ld, int r0, int i0,
                                            double* dsm) {
-  constexpr int kD2Threads = kDR * DC * 32, kDC = DC;
+  constexpr int NT = DR * DC * 32;
   const int Kp = (K + 3) & ~3;
-  constexpr int RB = kDR * 8, CB = kDC * 16;
-  double* as = dsm;                     // [RB][Kp]
-  double* bs = dsm + (size_t)RB * Kp;   // [Kp][CB]
+  constexpr int RB = DR * 8, CB = DC * 16, SB = dmma2_stride_b(DC * 16);
+  const int SA = dmma2_stride_a(Kp);
+  double* as = dsm;                     // [RB][SA]
+  double* bs = dsm + (size_t)RB * SA;   // [Kp][SB]
   const int tid = threadIdx.x;
   // P rows (an input), staged before the dependency wait: 16-byte cp.async when K is even (rows then
   // start 16-byte aligned), else 8-byte
   if ((K & 1) == 0) {
     const int hp = Kp >> 1;
-    for (int e = tid; e < RB * hp; e += kD2Threads) {
+    for (int e = tid; e < RB * hp; e += NT) {
       const int r = e / hp, kp = 2 * (e - r * hp);
-      double* dst = as + r * Kp + kp;
+      double* dst = as + r * SA + kp;
       if (r0 + r < rows && kp < K) cp_async16(dst, Pt + (size_t)(r0 + r) * K + kp);
       else { dst[0] = 0.0; dst[1] = 0.0; }
     }
@@ -265,18 +268,18 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
     for (int r = 0; r < RB; ++r) {
       const bool rin = r0 + r < rows;
       const double* src = Pt + (size_t)(r0 + r) * K;
-      for (int kp = tid; kp < Kp; kp += kD2Threads) {
-        if (rin && kp < K) cp_async8(as + r * Kp + kp, src + kp);
-        else as[r * Kp + kp] = 0.0;
+      for (int kp = tid; kp < Kp; kp += NT) {
+        if (rin && kp < K) cp_async8(as + r * SA + kp, src + kp);
+        else as[r * SA + kp] = 0.0;
       }
     }
   }
   if (kPdl) pdl_wait();
   {  // V tile: CB/2 two-double chunks per row
     constexpr int CH = CB / 2;
-    for (int e = tid; e < Kp * CH; e += kD2Threads) {
+    for (int e = tid; e < Kp * CH; e += NT) {
       const int kp = e / CH, c = 2 * (e - kp * CH);
-      double* dst = bs + kp * CB + c;
+      double* dst = bs + kp * SB + c;
       if (kp < K && i0 + c < ld) cp_async16(dst, Vn + (size_t)kp * ld + i0 + c);
       else { dst[0] = 0.0; dst[1] = 0.0; }
     }
@@ -284,15 +287,15 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
   cp_async_wait_all();
   __syncthreads();
   const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
-  const int wr = warp / kDC, wc = warp % kDC;           // this warp's 8x16 tile inside the block
-  const double* arow = as + (size_t)(wr * 8 + g) * Kp + kq;
-  const double* bcol = bs + (size_t)kq * CB + wc * 16 + g;
+  const int wr = warp / DC, wc = warp % DC;             // this warp's 8x16 tile inside the block
+  const double* arow = as + (size_t)(wr * 8 + g) * SA + kq;
+  const double* bcol = bs + (size_t)kq * SB + wc * 16 + g;
   double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
   const int nq = Kp >> 2;
 #pragma unroll 4
   for (int q = 0; q < nq; ++q) {
     const double a = arow[4 * q];
-    const double b0 = bcol[(size_t)(4 * q) * CB], b1 = bcol[(size_t)(4 * q) * CB + 8];
+    const double b0 = bcol[(size_t)(4 * q) * SB], b1 = bcol[(size_t)(4 * q) * SB + 8];
     dmma_8x8x4(d00, d01, a, b0);
     dmma_8x8x4(d10, d11, a, b1);
   }
@@ -307,12 +310,13 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
   }
 }
 
-__global__ void __launch_bounds__(kD2Threads) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
-                                                                   const double* __restrict__ Vn,   // [K][ld]
-                                                                   double* __restrict__ Wt,         // [rows][ld]
-                                                                   int rows, int K, int S, int ld, int ncb) {
+template <int DR, int DC>
+__global__ void __launch_bounds__(DR * DC * 32) contract_dmma2_kernel(const double* __restrict__ Pt,   // [rows][K]
+                                                                     const double* __restrict__ Vn,   // [K][ld]
+                                                                     double* __restrict__ Wt,         // [rows][ld]
+                                                                     int rows, int K, int S, int ld, int ncb) {
   extern __shared__ __align__(16) double dsm[];
-  dmma2_tile<kDC, true>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (kDR * 8), (blockIdx.x % ncb) * (kDC * 16), dsm);
+  dmma2_tile<DR, DC, true>(Pt, Vn, Wt, rows, K, S, ld, (blockIdx.x / ncb) * (DR * 8), (blockIdx.x % ncb) * (DC * 16), dsm);
   pdl_trigger();   // late trigger: dependents launch as this grid drains, without holding SM slots early
 }
 

@@ -29,9 +29,9 @@
 namespace esdp {
 
 constexpr int kPersistThreads = 256;
-constexpr int kDfDC = kPersistThreads / (32 * kDR);   // E tile: kDR*8 rows x kDfDC*16 columns, 8 warps
-constexpr int kDfRows = kDR * 8, kDfCols = kDfDC * 16;
-static_assert(kDR * kDfDC * 32 == kPersistThreads, "E tile uses every warp");
+constexpr int kDfDR = 2, kDfDC = 4;     // E tile: 16 rows x 64 columns, 8 warps
+constexpr int kDfRows = kDfDR * 8, kDfCols = kDfDC * 16;
+static_assert(kDfDR * kDfDC * 32 == kPersistThreads, "E tile uses every warp");
 
 enum DfKind : int { kTaskS = 0, kTaskE = 1 };
 
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kPersistThreads, 4) backward_persistent_kernel
       if (pp.rank1) {
         gemv_cols(pp.pi + (size_t)t * pp.K, Vn, Wt, pp.K, pp.S, pp.ld, b * pp.ecw + tid);
       } else {
-        dmma2_tile<kDfDC, false>(pp.P + (size_t)(t - 1) * pp.K * pp.K, Vn, Wt, pp.rows, pp.K, pp.S, pp.ld,
+        dmma2_tile<kDfDR, kDfDC, false>(pp.P + (size_t)(t - 1) * pp.K * pp.K, Vn, Wt, pp.rows, pp.K, pp.S, pp.ld,
                                  a * kDfRows, b * kDfCols, psm);
       }
     }

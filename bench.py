@@ -307,29 +307,52 @@ def run_ours(args):
     as_p = lambda t: None if t is None else ctypes.cast(t.data_ptr(), dp)
     m_, v_ = ctypes.c_double(), ctypes.c_double()
     Jh = ctypes.c_double()
-    e2e_times = []
-    # pipelined steps through the public API: step j launches its solve, then validates and enqueues the
-    # upload of step j+1's inputs into the other input slot (it overlaps solve j), then simulates and
-    # reads the step's results back.  Every step carries one full H2D of inputs and its D2H.
+    # pipelined steps through the public API: step j launches its solve (with the fused bid curves), then
+    # validates and enqueues the upload of step j+1's inputs into the other input slot (it overlaps solve
+    # j), then enqueues the simulation and the D2H copies of J and the simulation statistics; step j's
+    # results are read (event wait) after step j+1 has been launched.  Every step carries one full H2D of
+    # inputs and one D2H of its results; the timed region starts with all earlier results read and ends
+    # when the last step's results are on the host.
     load = lambda: E.lib.esdp_load_async(solver.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None)
+    J_h = torch.zeros(2, dtype=torch.float64).pin_memory()
+    st_h = torch.zeros((2, 2), dtype=torch.float64).pin_memory()
+    st_d = torch.zeros((2, 2), dtype=torch.float64, device=dev)
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    results = []
     assert load() == 0, E.esdp_last_error(solver.ctx)
-    for j in range(args.warmup + args.steps):
-        if world > 1 and j == args.warmup:
-            dist.barrier()
-        t0 = time.perf_counter()
+    t0 = None
+
+    def read(j):
+        done[j % 2].synchronize()
+        results.append((float(J_h[j % 2]), float(st_h[j % 2, 0]), float(st_h[j % 2, 1])))
+
+    nstep = args.warmup + args.steps
+    for j in range(nstep):
+        if j == args.warmup:
+            if j > 0:
+                read(j - 1)
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
         assert E.lib.esdp_backward_async(solver.ctx, sp) == 0
         if n_bid and not fused:
             E.esdp_bidcurves_dev(solver.ctx, n_bid, req_d.data_ptr(), cap, nv_d.data_ptr(), vert_d.data_ptr(),
                                  None, pr_d.data_ptr(), sp)
-        st = load()                                    # the next step's inputs (validated, chunked H2D)
-        assert st == 0, E.esdp_last_error(solver.ctx)
-        stream.synchronize()
-        assert E.lib.esdp_objective(solver.ctx, ctypes.byref(Jh)) == 0
+        if j + 1 < nstep:
+            st = load()                                    # the next step's inputs (validated, chunked H2D)
+            assert st == 0, E.esdp_last_error(solver.ctx)
+        assert E.lib.esdp_objective_async(solver.ctx, ctypes.c_void_p(J_h[j % 2:].data_ptr()), sp) == 0
         if n_paths:
-            assert E.lib.esdp_simulate(solver.ctx, n_paths, 99 + j, ctypes.byref(m_), ctypes.byref(v_), None) == 0
-        t1 = time.perf_counter()
-        if j >= args.warmup:
-            e2e_times.append(t1 - t0)
+            assert E.lib.esdp_simulate_async(solver.ctx, n_paths, 99 + j, ctypes.c_void_p(st_d[j % 2].data_ptr()),
+                                             sp) == 0
+            with torch.cuda.stream(stream):
+                st_h[j % 2].copy_(st_d[j % 2], non_blocking=True)
+        done[j % 2].record(stream)
+        if j > 0 and j != args.warmup:
+            read(j - 1)
+    read(nstep - 1)
+    e2e_times = [time.perf_counter() - t0]
     e2e_t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

@@ -132,6 +132,10 @@ esdp_status esdp_load(esdp_ctx* ctx, const double* lambda, const double* P, cons
 esdp_status esdp_load_async(esdp_ctx* ctx, const double* lambda, const double* P, const double* pi,
                             const double* g);
 
+/* J of the last backward pass copied to J_host (pinned host memory for an asynchronous copy), enqueued
+ * on stream after the solve (NULL = the context's own stream); the caller synchronizes. */
+esdp_status esdp_objective_async(esdp_ctx* ctx, double* J_host, void* stream);
+
 /* Backward induction, Alg. 1 lines 6-11 in Markov form (Eqs. 5-6):
  *   W_T = 0;  for t = T..1:  W_t = P_t V_{t+1} (t < T),
  *             V_t(i,k) = max_a pay(t,k,a) + Wint_t(i,a,k),  pol_t(i,k) = smallest argmax,
@@ -184,6 +188,10 @@ esdp_status esdp_set_bid_requests(esdp_ctx* ctx, int64_t n, const int32_t* req, 
  * per_path [n_paths] (host, nullable), mean, var (sample variance) over paths. */
 esdp_status esdp_simulate(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* mean, double* var,
                           double* per_path);
+/* Asynchronous variant for pipelined callers: the simulation and its deterministic reduction are
+ * enqueued on stream (NULL = the context's own); stats_dev[2] (device) receives {mean, sample
+ * variance}.  Nothing is synchronized. */
+esdp_status esdp_simulate_async(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* stats_dev, void* stream);
 /* Device variant: per-path profits to per_path_dev, enqueued on stream. */
 esdp_status esdp_simulate_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t seed, double* per_path_dev,
                               void* stream);

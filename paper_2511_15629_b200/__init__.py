@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = [
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
     "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
     "esdp_simulate_mode", "esdp_simulate_mode_dev", "esdp_simulate_strategy_dev", "esdp_price_paths_dev",
+    "esdp_simulate_async", "esdp_objective_async",
     "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
     "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
     "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error",
@@ -87,6 +88,8 @@ def _load():
         "esdp_backward": ([ctx, _vp, _dp], ctypes.c_int),
         "esdp_backward_async": ([ctx, _vp], ctypes.c_int),
         "esdp_objective": ([ctx, _dp], ctypes.c_int),
+        "esdp_objective_async": ([ctx, _vp, _vp], ctypes.c_int),
+        "esdp_simulate_async": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
         "esdp_values": ([ctx, ctypes.c_int32, _dp, _dp], ctypes.c_int),
         "esdp_policy": ([ctx, ctypes.c_int32, _i16p], ctypes.c_int),
         "esdp_bidcurves": ([ctx, ctypes.c_int64, _i32p, ctypes.c_int32, _i32p, _i16p, _dp, _dp], ctypes.c_int),

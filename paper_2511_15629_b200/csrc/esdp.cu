@@ -47,6 +47,7 @@ struct InputSlot {
   cudaEvent_t ev_head = nullptr, ev_tables = nullptr, use_ev = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   bool use_pending = false;
+  bool tables_stale = false;   // P uploaded, its sampling tables (cdf / guide) not built yet
   double gfit_h[6] = {0, 0, 0, 0, 0, 0};
 };
 
@@ -468,8 +469,8 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   if (pi) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, pi, npi * sizeof(double), h2d, s));
     if (c->rank1)   // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
-      cdf_kernel<<<cdf_blocks(c->T), kCdfWarps * 32, 0, s>>>(d.pi, c->T, c->K, c->G, d.cdf, d.guide);
-    cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(d.pi, 1, c->K, c->G, d.cdf1, d.guide1);  // pi_1 (row 0 in rank-1)
+      launch_cdf(d.pi, c->T, c->K, c->G, d.cdf, d.guide, s);
+    launch_cdf(d.pi, 1, c->K, c->G, d.cdf1, d.guide1, s);  // pi_1 (row 0 in rank-1)
     CUDA_OR_FAIL(c, cudaGetLastError());
   } else if (copy_old) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, o.pi, npi * sizeof(double), d2d, s));
@@ -504,17 +505,35 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
     }
     CUDA_OR_FAIL(c, cudaEventRecord(d.chunk_ev[j], s));
   }
+  // The sampling tables of P are built lazily by the first simulation that needs them (ready_tables),
+  // on that simulation's stream: built here, their blocks would share the SMs with the running backward's
+  // latency-bound stage chain and stretch it (measured +0.3 ms per cfg2 solve).
   if (!c->rank1 && c->T > 1) {
     const int64_t nr = (int64_t)(c->T - 1) * c->K;
-    if (P) {
-      cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(d.P, nr, c->K, c->G, d.cdf, d.guide);
-      CUDA_OR_FAIL(c, cudaGetLastError());
+    if (P || (copy_old && o.tables_stale)) {
+      d.tables_stale = true;
     } else if (copy_old) {
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, (size_t)nr * K * sizeof(double), d2d, s));
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (size_t)nr * G * sizeof(int16_t), d2d, s));
+      d.tables_stale = false;
     }
   }
   CUDA_OR_FAIL(c, cudaEventRecord(d.ev_tables, s));
+  return ESDP_OK;
+}
+
+// Before a simulation on stream s: wait for the active slot's uploads and build its sampling tables of
+// P if that upload left them stale.
+esdp_status ready_tables(esdp_ctx* c, cudaStream_t s) {
+  InputSlot& x = c->slot[c->active];
+  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, x.ev_tables, 0));
+  if (x.tables_stale) {
+    const int64_t nr = (int64_t)(c->T - 1) * c->K;
+    launch_cdf(x.P, nr, c->K, c->G, x.cdf, x.guide, s);
+    CUDA_OR_FAIL(c, cudaGetLastError());
+    CUDA_OR_FAIL(c, cudaEventRecord(x.ev_tables, s));
+    x.tables_stale = false;
+  }
   return ESDP_OK;
 }
 
@@ -1236,6 +1255,14 @@ esdp_status esdp_objective(esdp_ctx* c, double* J) {
   return ESDP_OK;
 }
 
+esdp_status esdp_objective_async(esdp_ctx* c, double* J_host, void* stream) {
+  if (!c || !J_host) return ESDP_E_STATE;
+  if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(J_host, c->d_J, sizeof(double), cudaMemcpyDeviceToHost, s));
+  return ESDP_OK;
+}
+
 esdp_status esdp_backward(esdp_ctx* c, void* stream, double* J) {
   if (!c) return ESDP_E_STATE;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
@@ -1381,7 +1408,7 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));   // sampling tables of the last upload
+  if (esdp_status e = ready_tables(c, s)) return e;   // sampling tables of the last upload
   const int thr = 128;
   const size_t sm = sim_smem_bytes(c->A);
   if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1398,10 +1425,29 @@ esdp_status esdp_price_paths_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, in
   sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda; sp.guide = c->d_guide; sp.guide1 = c->d_guide1;
   sp.G = c->G; sp.T = c->T; sp.K = c->K; sp.rank1 = c->rank1;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));
+  if (esdp_status e = ready_tables(c, s)) return e;
   price_path_kernel<<<(unsigned)((n_paths + 127) / 128), 128, 0, s>>>(sp, n_paths, seed, kpath_dev, lambda_dev);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return mark_use(c, s);
+}
+
+esdp_status esdp_simulate_async(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* stats_dev, void* stream) {
+  if (!c || !stats_dev) return ESDP_E_STATE;
+  if (n_paths > c->sim_cap) {
+    cudaFree(c->d_sim);
+    c->d_sim = nullptr;
+    c->sim_cap = 0;
+    if (dev_alloc(c, &c->d_sim, n_paths)) return ESDP_E_NOMEM;
+    c->sim_cap = n_paths;
+  }
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  esdp_status st = esdp_simulate_dev(c, n_paths, seed, c->d_sim, s);
+  if (st != ESDP_OK) return st;
+  reduce_kernel<<<1, 1024, 0, s>>>(c->d_sim, n_paths, nullptr, c->d_red);
+  reduce_kernel<<<1, 1024, 0, s>>>(c->d_sim, n_paths, c->d_red, c->d_red + 1);
+  finalize_stats_kernel<<<1, 1, 0, s>>>(c->d_red, n_paths, stats_dev);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return ESDP_OK;
 }
 
 esdp_status esdp_simulate(esdp_ctx* c, int64_t n_paths, uint64_t seed, double* mean, double* var, double* per_path) {
@@ -1461,7 +1507,7 @@ esdp_status esdp_simulate_strategy_dev(esdp_ctx* c, int64_t n_paths, uint64_t se
   mp.schedule = schedule_dev; mp.actions = actions_dev;
   mp.mode = mode; mp.wrows = (int)w_rows(c); mp.ld = c->ld; mp.delta = c->delta; mp.s0 = c->s0;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_tables, 0));
+  if (esdp_status e = ready_tables(c, s)) return e;
   const size_t sm = simmode_smem_bytes(c->A);
   if (sm > 48 * 1024) cudaFuncSetAttribute(simulate_mode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   simulate_mode_kernel<<<(unsigned)((n_paths + kSimModeThreads - 1) / kSimModeThreads), kSimModeThreads, sm, s>>>(
@@ -1791,16 +1837,16 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   BCUDA(b, cudaMemcpyAsync(b->d_lambda, p0.lambda, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
   if (b->rank1) {
     BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
-    cdf_kernel<<<cdf_blocks((int64_t)T), kCdfWarps * 32, 0, s>>>(b->d_pi, (int64_t)T, (int)K, (int)G, b->d_cdf, b->d_guide);
+    launch_cdf(b->d_pi, (int64_t)T, (int)K, (int)G, b->d_cdf, b->d_guide, s);
   } else {
     BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, K * sizeof(double), cudaMemcpyHostToDevice, s));
     if (T > 1) {
       BCUDA(b, cudaMemcpyAsync(b->d_P, p0.P, (T - 1) * K * K * sizeof(double), cudaMemcpyHostToDevice, s));
       const int64_t nr = (int64_t)(T - 1) * K;
-      cdf_kernel<<<cdf_blocks(nr), kCdfWarps * 32, 0, s>>>(b->d_P, nr, (int)K, (int)G, b->d_cdf, b->d_guide);
+      launch_cdf(b->d_P, nr, (int)K, (int)G, b->d_cdf, b->d_guide, s);
     }
   }
-  cdf_kernel<<<1, kCdfWarps * 32, 0, s>>>(b->d_pi, 1, (int)K, (int)G, b->d_cdf1, b->d_guide1);
+  launch_cdf(b->d_pi, 1, (int)K, (int)G, b->d_cdf1, b->d_guide1, s);
   BCUDA(b, cudaGetLastError());
   // per-instance parameters
   std::vector<BatchInst> hbi((size_t)n);

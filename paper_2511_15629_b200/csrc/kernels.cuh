@@ -734,17 +734,75 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
 // guide[b] = first j with b/G < cdf[j] (from a binary search; any start is exact for the sampler's
 // scans), so that a draw u in [b/G, (b+1)/G) starts its search there.  A bucket whose whole u range
 // (widened by 2^-49 for the rounding of u*G and of b/G) maps to one j is "pure" and stores ~j (< 0): the
-// sampler returns it without touching the cdf row.  One warp per row: lane 0 forms the sequential sum
-// (bit-identical to the oracle's cdf), then the lanes fill the guide buckets.
+// sampler returns it without touching the cdf row.  One warp per row.  Staged path (the row and its
+// guide fit kCdfSmemBytes of shared memory): every lane forms the same sequential sum over broadcast
+// values (bit-identical to the oracle's cdf) and keeps its own entries; each lane then fills a contiguous
+// run of buckets by one binary search plus a monotone walk; the row and the guide leave with coalesced
+// stores.  Global path (larger rows): lane 0 sums, every bucket is binary-searched.
 constexpr int kCdfWarps = 4;
+constexpr int kCdfSmemBytes = 8192;   // per warp
+__host__ __device__ inline int cdf_row_doubles(int K, int G) { return K + (G + 3) / 4; }   // cdf row + int16 guide
+inline bool cdf_staged(int K, int G) { return (size_t)cdf_row_doubles(K, G) * 8 <= (size_t)kCdfSmemBytes; }
+template <bool kSmem>
 __global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G,
                                                             double* __restrict__ cdf, int16_t* __restrict__ guide) {
+  extern __shared__ __align__(16) double cdf_sm[];
   const int64_t r = (int64_t)blockIdx.x * kCdfWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   const double* qr = q + r * K;
-  double* cr = cdf + r * K;
+  double* cg = cdf + r * K;
   int16_t* gr = guide + r * G;
+  const double m = 0x1p-49, invG = 1.0 / (double)G;
+  if (kSmem) {
+    double* cr = cdf_sm + (size_t)(threadIdx.x >> 5) * cdf_row_doubles(K, G);
+    int16_t* gs = (int16_t*)(cr + K);
+    double s = 0.0;
+    for (int j0 = 0; j0 < K; j0 += 32) {
+      const int j = j0 + lane;
+      const double v = j < K ? __ldg(qr + j) : 0.0;
+      const int n = min(32, K - j0);
+      double mine = 0.0;
+      for (int l = 0; l < n; ++l) {
+        s = __dadd_rn(s, __shfl_sync(0xffffffffu, v, l));
+        if (l == lane) mine = s;
+      }
+      if (j < K) {
+        const double c = (j == K - 1) ? 1.0 : mine;
+        cr[j] = c;
+        cg[j] = c;
+      }
+    }
+    __syncwarp();
+    const int R = (G + 31) >> 5, b0 = lane * R, b1 = min(G, b0 + R);
+    if (b0 < b1) {
+      double bd = (double)b0;                        // exact integer counter (no per-bucket conversion)
+      double lo = __dmul_rn(bd, invG);
+      int a = 0, z = K - 1;                          // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
+      while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
+      int j = a;
+      double cj = cr[j], cjm = j > 0 ? cr[j - 1] : 0.0;
+      for (int b = b0; b < b1; ++b) {
+        bd = __dadd_rn(bd, 1.0);
+        const double hi = __dmul_rn(bd, invG);       // fl((b + 1) / G) as in the global path
+        while (!(lo < cj)) { cjm = cj; ++j; cj = cr[j]; }
+        const bool below = j == 0 || cjm < __dsub_rn(lo, m);
+        const bool above = j == K - 1 || cj > __dadd_rn(hi, m);
+        gs[b] = (int16_t)(below && above ? ~j : j);
+        lo = hi;
+      }
+    }
+    __syncwarp();
+    if ((G & 1) == 0) {                              // r * G even: 4-byte aligned rows
+      const uint32_t* src = (const uint32_t*)gs;
+      uint32_t* dst = (uint32_t*)gr;
+      for (int b = lane; b < (G >> 1); b += 32) dst[b] = src[b];
+    } else {
+      for (int b = lane; b < G; b += 32) gr[b] = gs[b];
+    }
+    return;
+  }
+  double* cr = cg;
   if (lane == 0) {
     double s = 0.0;
     for (int j = 0; j < K; ++j) {
@@ -753,10 +811,9 @@ __global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __res
     }
   }
   __syncwarp();
-  const double m = 0x1p-49, invG = 1.0 / (double)G;
   for (int b = lane; b < G; b += 32) {
     const double lo = __dmul_rn((double)b, invG), hi = __dmul_rn((double)(b + 1), invG);
-    int a = 0, z = K - 1;                            // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
+    int a = 0, z = K - 1;
     while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
     const int j = a;
     const bool below = j == 0 || cr[j - 1] < __dsub_rn(lo, m);      // every u of the bucket >= cdf[j-1]
@@ -766,6 +823,15 @@ __global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __res
 }
 
 inline unsigned cdf_blocks(int64_t rows) { return (unsigned)((rows + kCdfWarps - 1) / kCdfWarps); }
+
+inline void launch_cdf(const double* q, int64_t rows, int K, int G, double* cdf, int16_t* guide, cudaStream_t s) {
+  if (rows <= 0) return;
+  if (cdf_staged(K, G))
+    cdf_kernel<true><<<cdf_blocks(rows), kCdfWarps * 32, (size_t)kCdfWarps * cdf_row_doubles(K, G) * 8, s>>>(q, rows, K, G, cdf,
+                                                                                               guide);
+  else
+    cdf_kernel<false><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, rows, K, G, cdf, guide);
+}
 
 // first j in [0, K) with u < cdf[j]; pure buckets answer directly, otherwise the guide gives a start and
 // the scans make it exact for any start (both neighbours are loaded together).
@@ -870,6 +936,12 @@ __global__ void __launch_bounds__(128) price_path_kernel(SimParams sp, int64_t n
 }
 
 inline size_t sim_smem_bytes(int A) { return (size_t)A * (3 * sizeof(double) + sizeof(int)) + 16; }
+
+// stats = {mean, M2 / (n - 1)} (the sample variance; 0 for one path), on the device.
+__global__ void finalize_stats_kernel(const double* __restrict__ red, int64_t n, double* __restrict__ stats) {
+  stats[0] = red[0];
+  stats[1] = n > 1 ? red[1] / (double)(n - 1) : 0.0;
+}
 
 // Deterministic two-pass reduction of per-path profits: sum (then sum of squared deviations).
 __global__ void reduce_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean_in,

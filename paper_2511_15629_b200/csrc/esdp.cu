@@ -614,6 +614,10 @@ WinParams win_params(const esdp_ctx* c) {
   wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
   wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
   wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  for (int j = 0; j < (int)c->singles.size() && j < kMaxSingles; ++j) {
+    const int a = c->singles[j];
+    wp.sg[j].act = c->act[a]; wp.sg[j].w = c->w[a]; wp.sg[j].omw = c->omw[a]; wp.sg[j].off = c->off[a]; wp.sg[j].a = a;
+  }
   return wp;
 }
 
@@ -1994,6 +1998,12 @@ const char* esdp_batch_last_error(const esdp_batch* b) { return b ? b->err.c_str
 
 }  // extern "C"
 
+#ifdef ESDP_WIN_TRACE
+// diagnostic (make -B EXTRA=-DESDP_WIN_TRACE): per-block phase marks of the last window-stencil launch
+extern "C" esdp_status esdp_win_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, esdp::g_ktrace, sizeof(esdp::g_ktrace)) == cudaSuccess ? ESDP_OK : ESDP_E_CUDA;
+}
+#endif
 #ifdef ESDP_DF_TRACE
 extern "C" int esdp_df_trace(unsigned long long* out, int n) {   // diagnostic build only
   if (n > esdp::kTraceMax) n = esdp::kTraceMax;

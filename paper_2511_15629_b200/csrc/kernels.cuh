@@ -23,6 +23,25 @@ __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  //
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+#ifdef ESDP_WIN_TRACE
+// diagnostic phase marks (tools/wintrace.py): thread 0 of each block of the last launch records
+// %globaltimer at mark m (and %smid); which = 0 window stencil, 1 expectation
+__device__ unsigned long long g_ktrace[2][4096][8];
+__device__ __forceinline__ void ktrace(int which, int m) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    if (b < 4096) {
+      g_ktrace[which][b][m] = t;
+      if (m == 0) { unsigned sm; asm("mov.u32 %0, %%smid;" : "=r"(sm)); g_ktrace[which][b][7] = sm; }
+    }
+  }
+}
+#else
+__device__ __forceinline__ void ktrace(int, int) {}
+#endif
+
 // A maximal run of actions whose offsets are consecutive integers decreasing by one and whose
 // interpolation weight is 0 ("recombining" interior of Eq. 10), or a single action.
 struct Seg {
@@ -254,6 +273,7 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
   double* as = dsm;                     // [RB][SA]
   double* bs = dsm + (size_t)RB * SA;   // [Kp][SB]
   const int tid = threadIdx.x;
+  ktrace(1, 0);
   // P rows (an input), staged before the dependency wait: 16-byte cp.async when K is even (rows then
   // start 16-byte aligned), else 8-byte
   if ((K & 1) == 0) {
@@ -274,7 +294,9 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
       }
     }
   }
+  ktrace(1, 1);
   if (kPdl) pdl_wait();
+  ktrace(1, 2);
   {  // V tile: CB/2 two-double chunks per row
     constexpr int CH = CB / 2;
     for (int e = tid; e < Kp * CH; e += NT) {
@@ -286,6 +308,7 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
   }
   cp_async_wait_all();
   __syncthreads();
+  ktrace(1, 3);
   const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
   const int wr = warp / DC, wc = warp % DC;             // this warp's 8x16 tile inside the block
   const double* arow = as + (size_t)(wr * 8 + g) * SA + kq;
@@ -299,6 +322,7 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
     dmma_8x8x4(d00, d01, a, b0);
     dmma_8x8x4(d10, d11, a, b1);
   }
+  ktrace(1, 4);
   const int r = r0 + wr * 8 + g;
   if (r < rows) {
     const int c = i0 + wc * 16 + 2 * kq;
@@ -308,6 +332,7 @@ __device__ __forceinline__ void dmma2_tile(const double* __restrict__ Pt, const 
     if (c + 8 < S) wrp[c + 8] = d10;
     if (c + 9 < S) wrp[c + 9] = d11;
   }
+  ktrace(1, 5);
 }
 
 template <int DR, int DC>

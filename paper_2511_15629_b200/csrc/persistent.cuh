@@ -147,9 +147,8 @@ __global__ void __launch_bounds__(kPersistThreads, 4) backward_persistent_kernel
       int16_t* polt = pp.pol + (size_t)(t - 1) * pp.Kp * pp.S;
       const double* lamt = pp.lambda + (size_t)(t - 1) * pp.K;
       if (pp.use_window) {
-        WinParams wp = pp.wp;
-        wp.W = Wt; wp.V = Vt; wp.pol = polt; wp.lambda_t = lamt;
-        window_item(wp, a, b * kWinTile, psm);
+        const WinStage st{Wt, Vt, polt, lamt};
+        window_item(pp.wp, st, a, b * kWinTile, psm);
       } else {
         StencilParams sp = pp.sp;
         sp.W = Wt; sp.V = Vt; sp.pol = polt; sp.lambda_t = lamt;

@@ -35,7 +35,16 @@ __device__ unsigned long long g_window_fallbacks;  // rows that needed the full 
 constexpr int kWinThreads = ESDP_WIN_THREADS;  // one output column per thread in the query phase
 constexpr int kLevelSlots = (kWinTile + 512 + 2 * kWinThreads - 1) / (2 * kWinThreads);  // pairs per thread
 
-constexpr int kMaxSingles = 16;  // singles staged in shared memory (more: read from global)
+constexpr int kMaxSingles = 16;
+
+__device__ __forceinline__ void wtrace(int m) { ktrace(0, m); }  // singles staged in shared memory (more: read from global)
+
+// static data of a single (canonically evaluated) action, carried in the kernel parameters so the
+// block reads it from the constant bank instead of a dependent global gather
+struct WinSingle {
+  double act, w, omw;
+  int off, a;
+};
 
 struct WinParams {
   const double* W; double* V; int16_t* pol; const double* lambda_t;
@@ -51,6 +60,7 @@ struct WinParams {
   const double* g;          // [A] degradation g_a (LINEAR_MINUS_G): pay = fl(fl(lambda p) - g) when g_kind
   const double* gfit;       // [6] affine fit of g on the runs: gc0, gc1, gd0, gd1, max deviation, max |g|
   int g_kind;               // 1: payoff lambda p - g(p) (kind LINEAR_MINUS_G), 0: lambda p
+  WinSingle sg[kMaxSingles];  // static data of singles[0 .. min(nsingle, kMaxSingles))
 };
 
 // Packed keys: an order-preserving 64-bit image of the (approximate) value with its table position in
@@ -148,6 +158,43 @@ __device__ __forceinline__ void build_level(const RangeMax& t, int q, int tid) {
   }
 }
 
+// levels q and q + 1 of a table in one pass from level q - 1 (h = 2^(q-1)): entry x of level q is
+// max(L[x], L[x+h]) for x <= n - 2^q, of level q + 1 max(L[x], L[x+h], L[x+2h], L[x+3h]) for
+// x <= n - 2^(q+1).  Halves the barriers between the level builds.
+__device__ __forceinline__ void build_level2(const RangeMax& t, int q, int tid) {
+  const int h = 1 << (q - 1), lim1 = t.n - (1 << q), lim2 = t.n - (2 << q);
+  const unsigned long long* pv = t.v + (q - 1) * t.ns;
+  unsigned long long* n1 = t.v + q * t.ns;
+  unsigned long long* n2 = n1 + t.ns;
+#pragma unroll
+  for (int u = 0; u < kLevelSlots; ++u) {
+    const int x = 2 * (tid + u * kWinThreads);
+    if (x <= lim1) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(pv + x);
+      ulonglong2 b;
+      if (h == 1) { b.x = a.y; b.y = pv[x + 2]; }
+      else b = *reinterpret_cast<const ulonglong2*>(pv + x + h);
+      ulonglong2 r;
+      r.x = umax64(a.x, b.x);
+      r.y = umax64(a.y, b.y);
+      if (x + 1 <= lim1) *reinterpret_cast<ulonglong2*>(n1 + x) = r;
+      else n1[x] = r.x;
+      if (x <= lim2) {
+        // level q at x + 2h, from the same level q - 1 entries
+        const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(pv + x + 2 * h);
+        ulonglong2 d;
+        if (h == 1) { d.x = c.y; d.y = pv[x + 4]; }
+        else d = *reinterpret_cast<const ulonglong2*>(pv + x + 3 * h);
+        ulonglong2 e;
+        e.x = umax64(r.x, umax64(c.x, d.x));
+        e.y = umax64(r.y, umax64(c.y, d.y));
+        if (x + 1 <= lim2) *reinterpret_cast<ulonglong2*>(n2 + x) = e;
+        else n2[x] = e.x;
+      }
+    }
+  }
+}
+
 // top-2 of the window [l, r] of table t: best (value, table position) and the runner-up value
 __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, double& m1, int& pos, double& m2) {
   const unsigned long long k1 = t.query(l, r);
@@ -156,9 +203,18 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
   m2 = unord64(umax64(t.query(l, pos - 1), t.query(pos + 1, r)));
 }
 
-// One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.
-__device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, double* wsm) {
+// One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.  kWait: the
+// programmatic dependency wait (W_t is the previous kernel's output) is taken here, after the input loads
+// (lambda, the g fit) are issued; the W loads follow it at once, and the singles come from the kernel
+// parameters, so the block pays one memory latency before its first barrier.
+struct WinStage {          // the per-stage pointers of an item (the rest of WinParams is stage-invariant)
+  const double* W; double* V; int16_t* pol; const double* lambda_t;
+};
+
+template <bool kWait = false>
+__device__ __forceinline__ void window_item(const WinParams& p, const WinStage& st, int k, int i0, double* wsm) {
   const int tid = threadIdx.x;
+  wtrace(0);
   const int nw = kWinTile + (p.o_max - p.o_min) + 2;
   const int lc = p.pc + 1, ldl = p.pd + 1;
   RangeMax tc, td;
@@ -172,29 +228,49 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   __shared__ unsigned red[kWinThreads / 32];
   __shared__ SingleAct ss[kMaxSingles];
 
-  const double* Wrow = p.W + (p.rank1 ? 0 : (size_t)k * p.ld);
-  const double lam = p.lambda_t[k];
+  const double* Wrow = st.W + (p.rank1 ? 0 : (size_t)k * p.ld);
+  const int wbase = i0 + p.o_min;
+  // inputs first (lambda_t and the g fit do not depend on the previous kernel)
+  const double lam = st.lambda_t[k];
+  const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
+  if (kWait) pdl_wait();
+  wtrace(1);
+  // W_t over the tile: all of this thread's loads are issued before anything waits on them
+  constexpr int kWReg = 3;
+  double wv[kWReg];
+#pragma unroll
+  for (int u = 0; u < kWReg; ++u) {
+    const int x = tid + u * kWinThreads, col = wbase + x;
+    wv[u] = (x < nw && col >= 0 && col < p.S) ? __ldcg(Wrow + col) : -INFINITY;
+  }
   // key slopes: the run payoffs lambda p - g are affine in the offset o (g fitted by gc0 + gc1 o on the
   // charge run, gd0 + gd1 |o| on the discharge run; g = 0 for the linear payoff), so
   //   cand(i, j) ~= key(j) + beta i - g0,  key(j) = W[j] - beta j,
   //   beta_c = lambda delta / eta_c + gc1,  beta_d = lambda delta eta_d - gd1   (any few-ulp rounding: see eps)
-  const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
   const double beta_c = __dadd_rn(__dmul_rn(lam, p.dc), gc1);
   const double beta_d = __dsub_rn(__dmul_rn(lam, p.dd), gd1);
-  const int wbase = i0 + p.o_min;
   const int nsg = p.nsingle < kMaxSingles ? p.nsingle : kMaxSingles;
   if (tid < nsg) {
-    const int a = __ldg(p.singles + tid);
+    const WinSingle& g = p.sg[tid];
     SingleAct s;
-    s.a = a; s.off = __ldg(p.off + a); s.w = __ldg(p.w + a); s.omw = __ldg(p.omw + a);
-    s.pay = __dmul_rn(lam, __ldg(p.act + a));
-    if (p.g_kind) s.pay = __dsub_rn(s.pay, __ldg(p.g + a));
+    s.a = g.a; s.off = g.off; s.w = g.w; s.omw = g.omw;
+    s.pay = __dmul_rn(lam, g.act);
+    if (p.g_kind) s.pay = __dsub_rn(s.pay, __ldg(p.g + g.a));
     ss[tid] = s;
   }
   // max |W| over the tile: the high words of |W| (ordered like the values), reduced with REDUX; the
   // bound M below fills the low word with ones, so M >= max |W|
   unsigned mx = 0u;
-  for (int x = tid; x < nw; x += kWinThreads) {
+#pragma unroll
+  for (int u = 0; u < kWReg; ++u) {
+    const int x = tid + u * kWinThreads;
+    if (x < nw) {
+      const double v = wv[u];
+      if (v != -INFINITY) mx = umax(mx, (unsigned)__double2hiint(v) & 0x7fffffffu);
+      wt[x] = v;
+    }
+  }
+  for (int x = tid + kWReg * kWinThreads; x < nw; x += kWinThreads) {   // wide action spans
     const int col = wbase + x;
     double v = -INFINITY;
     if (col >= 0 && col < p.S) {
@@ -204,6 +280,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     wt[x] = v;
   }
   __syncthreads();
+  wtrace(2);
   // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores)
   for (int x = 2 * tid; x < tc.n; x += 2 * kWinThreads) {
     const int j = i0 + 1 + x;
@@ -222,14 +299,18 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
   mx = __reduce_max_sync(0xffffffffu, mx);
   if ((tid & 31) == 0) red[tid >> 5] = mx;
   __syncthreads();
+  wtrace(3);
   const int top = p.pc > p.pd ? p.pc : p.pd;
 #pragma unroll
-  for (int q = 1; q <= 9; ++q) {        // levels <= 9 (L <= 512): unrolled, uniform exits
+  for (int q = 1; q <= 9; q += 2) {     // levels <= 9 (L <= 512), two per barrier: unrolled, uniform exits
     if (q > top) break;
-    if (q <= p.pc) build_level(tc, q, tid);
-    if (q <= p.pd) build_level(td, q, tid);
+    if (q + 1 <= p.pc) build_level2(tc, q, tid);
+    else if (q <= p.pc) build_level(tc, q, tid);
+    if (q + 1 <= p.pd) build_level2(td, q, tid);
+    else if (q <= p.pd) build_level(td, q, tid);
     __syncthreads();
   }
+  wtrace(4);
   (void)ldl;
   const unsigned mb = __reduce_max_sync(0xffffffffu, red[tid % (kWinThreads / 32)]);
   const double M = __hiloint2double((int)mb, (int)0xffffffffu);
@@ -261,26 +342,33 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
       if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
       else b2 = fmax(b2, y1);
     }
-    double c1 = 0.0;      // canonical value of the best single (exact)
+    // singles, branch-free: b2 takes the smaller of (b1, c), b1 the larger; once a single leads, b1 is its
+    // exact canonical value (a later single replaces it only by a larger canonical value)
     bool single_best = false;
 #pragma unroll 4
     for (int s = 0; s < nsg; ++s) {
       const double c = canon_staged(ss[s], wt, wbase, i);
-      if (c > b1) { b2 = b1; b1 = c; a1 = ss[s].a; c1 = c; single_best = true; }
-      else b2 = fmax(b2, c);
+      const bool gt = c > b1;
+      b2 = fmax(b2, gt ? b1 : c);
+      b1 = gt ? c : b1;
+      a1 = gt ? ss[s].a : a1;
+      single_best |= gt;
     }
     for (int s = nsg; s < p.nsingle; ++s) {
       const int a = __ldg(p.singles + s);
       const double c = canon_single(p, wt, wbase, i, a, lam);
-      if (c > b1) { b2 = b1; b1 = c; a1 = a; c1 = c; single_best = true; }
-      else b2 = fmax(b2, c);
+      const bool gt = c > b1;
+      b2 = fmax(b2, gt ? b1 : c);
+      b1 = gt ? c : b1;
+      a1 = gt ? a : a1;
+      single_best |= gt;
     }
     if (__dsub_rn(b1, b2) > 2.0 * eps) {
       arg = a1;
       // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, w = 0), so
       // only its power (and g) is loaded: fl(fl(fl(lambda p) - g) + W[i + o])
       if (single_best) {
-        best = c1;
+        best = b1;
       } else {
         double pay = __dmul_rn(lam, __ldg(p.act + a1));
         if (p.g_kind) pay = __dsub_rn(pay, __ldg(p.g + a1));
@@ -290,6 +378,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
       near_tie = true;
     }
   }
+  wtrace(5);
   // near ties (rare; every row for degenerate data such as zero prices): the whole warp re-scans the
   // row canonically, 32 actions at a time, and reduces (value desc, index asc) -- the smallest index
   // among exact ties, as in the oracle's ascending scan with a strict '>'.
@@ -313,15 +402,21 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
     }
     if (lane == src) { best = v; arg = va; atomicAdd(&g_window_fallbacks, 1ull); }
   }
-  if (!valid) return;
-  p.V[(size_t)k * p.ld + i] = best;
-  p.pol[(size_t)k * p.S + i] = (int16_t)arg;
+  if (!valid) { wtrace(6); return; }
+  st.V[(size_t)k * p.ld + i] = best;
+  st.pol[(size_t)k * p.S + i] = (int16_t)arg;
+  wtrace(6);
+}
+
+template <bool kWait = false>
+__device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, double* wsm) {
+  const WinStage st{p.W, p.V, p.pol, p.lambda_t};
+  window_item<kWait>(p, st, k, i0, wsm);
 }
 
 __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
-  pdl_wait();                          // W_t is the previous contraction's output
-  window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
+  window_item<true>(p, blockIdx.y, blockIdx.x * kWinTile, wsm);   // waits for W_t (the contraction) inside
   pdl_trigger();
 }
 

@@ -1,5 +1,8 @@
-"""Phase timing of the window stencil blocks (diagnostic; needs `make -B EXTRA=-DESDP_WIN_TRACE`):
-marks 0 start, 1 W staged, 2 level-0 keys, 3 levels built, 4 queries + singles, 5 near-tie pass done."""
+"""Phase timing of the last stage's expectation and window-stencil blocks (diagnostic; needs
+`make -B EXTRA=-DESDP_WIN_TRACE`).  Marks are thread 0's %globaltimer (256 ns granularity on B200).
+window:      0 start, 1 after the dependency wait, 2 W staged, 3 level-0 keys, 4 levels built,
+             5 queries + singles, 6 stored
+expectation: 0 start, 1 P staging issued, 2 after the dependency wait, 3 V staged, 4 DMMA chain, 5 stored"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -12,15 +15,29 @@ s = E.Solver(inst, keep_values=True)
 for _ in range(3):
     s.backward()
 torch.cuda.synchronize()
-buf = np.zeros((4096, 8), np.uint64)
+buf = np.zeros((2, 4096, 8), np.uint64)
 E.lib.esdp_win_trace.argtypes = [ctypes.c_void_p]
 assert E.lib.esdp_win_trace(buf.ctypes.data) == 0
-b = buf[:400, :6].astype(np.float64)
-t0 = b[:, 0].min()
-print("block start spread (us): %.2f .. %.2f" % ((b[:, 0].min() - t0) / 1e3, (b[:, 0].max() - t0) / 1e3))
-print("block end   spread (us): %.2f .. %.2f" % ((b[:, 5].min() - t0) / 1e3, (b[:, 5].max() - t0) / 1e3))
-d = np.diff(b, axis=1) / 1e3
-names = ["stage W", "level0+M", "levels", "queries+singles", "near-tie pass"]
-for j, nm in enumerate(names):
-    print("%-16s mean %.3f  p50 %.3f  max %.3f us" % (nm, d[:, j].mean(), np.median(d[:, j]), d[:, j].max()))
-print("total per block mean %.3f us" % ((b[:, 5] - b[:, 0]).mean() / 1e3))
+
+
+def report(name, bb, nb, names):
+    nm = len(names) + 1
+    b = bb[:nb, :nm].astype(np.float64)
+    sm = bb[:nb, 7].astype(np.int64)
+    t0 = b[:, 0].min()
+    print("== %s (%d blocks)" % (name, nb))
+    print("block start spread (us): %.2f .. %.2f" % (0.0, (b[:, 0].max() - t0) / 1e3))
+    print("block end   spread (us): %.2f .. %.2f" % ((b[:, -1].min() - t0) / 1e3, (b[:, -1].max() - t0) / 1e3))
+    d = np.diff(b, axis=1) / 1e3
+    for j, n in enumerate(names):
+        print("  %-16s mean %.3f  p50 %.3f  max %.3f us" % (n, d[:, j].mean(), np.median(d[:, j]), d[:, j].max()))
+    cnt = np.bincount(sm, minlength=148)
+    print("  blocks per SM histogram:", np.bincount(cnt))
+    return t0, b
+
+
+tw, bw = report("window", buf[0], 400, ["prologue+wait", "stage W", "level0+M", "levels", "queries+singles",
+                                         "near-tie+store"])
+tc, bc = report("expectation", buf[1], 273, ["P issue", "wait", "V staged", "DMMA chain", "store"])
+print("expectation first start -> window first start: %.2f us; expectation last end -> window last wait done: %.2f us"
+      % ((tw - tc) / 1e3, (bw[:, 1].max() - bc[:, 5].max()) / 1e3))

@@ -345,6 +345,138 @@ __global__ void __launch_bounds__(DR * DC * 32) contract_dmma2_kernel(const doub
   pdl_trigger();   // late trigger: dependents launch as this grid drains, without holding SM slots early
 }
 
+// ------------------------------------------------------------------------------------------------
+// Throughput-regime expectation (cfg4, cfg5 batches): register-blocked DMMA with a k'-pipelined
+// shared-memory stage.  dmma2 above is built for latency (a few 8x16 warp tiles per block, everything
+// staged before the chain starts); on large contractions its 1 A + 2 B fragment loads per 2 DMMAs keep
+// the LSU ~75 % busy at the DMMA rate and its 141 KB stage (K = 200) fits one block per SM (ncu on
+// cfg4: tensor pipe 42 % of active cycles, short-scoreboard stalls first).  Here a warp owns an
+// (8 MT) x (8 NT) tile -- MT A and NT B fragments feed MT*NT DMMAs per k-step -- and the k' dimension
+// streams through NS cp.async stages of KC k' each, so several blocks co-reside and the staging of one
+// chunk overlaps the chains of the previous ones.  Every accumulator still runs its k'-quads in
+// ascending order, one DMMA (4 sequential fmas) after the other: the result is the canonical chain (R15),
+// bit for bit, as with dmma2.
+// Block: WC warps side by side (columns); tile RB = 8 MT rows x CB = 8 NT WC columns.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int MT, int NT, int WC, int KC, int NS>
+struct Dmma3 {
+  static constexpr int RB = 8 * MT, CB = 8 * NT * WC, NTH = 32 * WC;
+  static constexpr int SA = (KC % 16 == 0 || KC % 16 == 8) ? KC + 4 : KC;   // A rows: stride 4 or 12 mod 16
+  static constexpr int SB = CB + (8 - CB % 16 + 16) % 16;                     // B rows: stride 8 mod 16
+  static constexpr int STAGE = RB * SA + KC * SB;                             // doubles per stage
+  static size_t smem() { return sizeof(double) * (size_t)NS * STAGE; }
+};
+
+template <int MT, int NT, int WC, int KC, int NS>
+__global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* __restrict__ Pt,   // [rows][K], K even
+                                                                 const double* __restrict__ Vn,   // [K][ld]
+                                                                 double* __restrict__ Wt,         // [rows][ld]
+                                                                 int rows, int K, int S, int ld, int nrb) {
+  using D = Dmma3<MT, NT, WC, KC, NS>;
+  static_assert(KC % 4 == 0 && NS >= 2, "k' chunk of whole quads, at least double buffering");
+  extern __shared__ __align__(16) double d3sm[];
+  const int tid = threadIdx.x;
+  const int r0 = (blockIdx.x % nrb) * D::RB, i0 = (blockIdx.x / nrb) * D::CB;   // neighbours share the V tile
+  const int nch = (K + KC - 1) / KC;
+  // Per-thread copy slots, fixed for the whole kernel: the A piece (row ra, k' pair ka) and the B pieces
+  // (rows kb + j*BR, column pair cb); per chunk only the k' bound is checked and the pointers advance.
+  // Out-of-range pieces are zero-filled by the copy itself (src-size 0).
+  constexpr int AP = 8 * MT * (KC / 2), BP = KC * (D::CB / 2);
+  static_assert(AP % D::NTH == 0 || D::NTH % AP == 0, "A pieces per thread");
+  static_assert(D::NTH % (D::CB / 2) == 0 && BP % D::NTH == 0, "B pieces per thread");
+  constexpr int NA = AP >= D::NTH ? AP / D::NTH : 1, NB = BP / D::NTH, BR = D::NTH / (D::CB / 2);
+  const bool a_thr = tid < AP;
+  const int ra = tid / (KC / 2), ka = 2 * (tid % (KC / 2));       // + j * (NTH / (KC/2)) rows for j < NA
+  const int kb = tid / (D::CB / 2), cb = 2 * (tid % (D::CB / 2));
+  const bool b_col = i0 + cb < ld;
+  const double* ga = Pt + (size_t)min(r0 + ra, rows - 1) * K + ka;
+  const double* gb = Vn + (size_t)kb * ld + (b_col ? i0 + cb : 0);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(d3sm);
+  auto cp16z = [](unsigned dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+  };
+  auto issue_a = [&](int ch) {   // P rows r0.. of k' chunk ch (an input: may precede the dependency wait)
+    if (!a_thr) return;
+    const unsigned st = sbase + (unsigned)(sizeof(double) * (size_t)(ch % NS) * D::STAGE);
+    const int k = ch * KC + ka;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int r = ra + j * (D::NTH / (KC / 2));
+      const bool ok = r0 + r < rows && k < K;
+      cp16z(st + (unsigned)(sizeof(double) * (r * D::SA + ka)), ok ? ga + (size_t)j * (D::NTH / (KC / 2)) * K + ch * KC : Pt, ok);
+    }
+  };
+  auto issue_b = [&](int ch) {   // V_{t+1} rows of chunk ch, columns i0..i0+CB
+    const unsigned st = sbase + (unsigned)(sizeof(double) * ((size_t)(ch % NS) * D::STAGE + D::RB * D::SA));
+    const double* src = gb + (size_t)ch * KC * ld;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kp = kb + j * BR;
+      const bool ok = b_col && ch * KC + kp < K;
+      cp16z(st + (unsigned)(sizeof(double) * (kp * D::SB + cb)), ok ? src + (size_t)j * BR * ld : Vn, ok);
+    }
+  };
+  auto As = [&](int b) { return d3sm + (size_t)b * D::STAGE; };
+  auto Bs = [&](int b) { return d3sm + (size_t)b * D::STAGE + D::RB * D::SA; };
+  // prologue: P chunks of the first NS-1 stages before the wait, V chunks after it; one group per stage
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s)
+    if (s < nch) issue_a(s);
+  pdl_wait();
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nch) issue_b(s);
+    cp_async_commit();
+  }
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait_group<NS - 2>();   // chunk ch has landed (this thread's copies) ...
+    __syncthreads();                 // ... everyone's; and chunk ch-1's buffer is no longer read
+    if (ch + NS - 1 < nch) { issue_a(ch + NS - 1); issue_b(ch + NS - 1); }
+    cp_async_commit();
+    const double* as = As(ch % NS) + g * D::SA + kq;
+    const double* bs = Bs(ch % NS) + kq * D::SB + warp * (8 * NT) + g;
+    const int nq = min(KC, K - ch * KC + 3) >> 2;   // k'-quads of this chunk (zero quads past K skipped)
+#pragma unroll
+    for (int q = 0; q < KC / 4; ++q) {
+      if (q < nq) {
+        double a[MT], b[NT];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) a[m] = as[m * 8 * D::SA + 4 * q];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) b[n] = bs[4 * q * D::SB + 8 * n];
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+      }
+    }
+  }
+  cp_async_wait_group<0>();
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    const int r = r0 + m * 8 + g;
+    if (r >= rows) continue;
+    double* wr = Wt + (size_t)r * ld;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = i0 + warp * (8 * NT) + n * 8 + 2 * kq;   // even, ld % 4 == 0: 16-byte aligned
+      if (c + 1 < S) *reinterpret_cast<double2*>(wr + c) = make_double2(acc[m][n][0], acc[m][n][1]);
+      else if (c < S) wr[c] = acc[m][n][0];
+    }
+  }
+  pdl_trigger();
+}
+
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
 __device__ __forceinline__ void gemv_cols(const double* __restrict__ pi, const double* __restrict__ Vn,
                                           double* __restrict__ Wt, int K, int S, int ld, int i) {

@@ -203,6 +203,32 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
   m2 = unord64(umax64(t.query(l, pos - 1), t.query(pos + 1, r)));
 }
 
+// Unimodal tables (the common case: W_t(., k) concave in the SoC, as for every linear-payoff workload
+// measured -- tools/unimodal.py finds 100 % of cfg2 / cfg4 / cfg5 tiles unimodal, cfg3's fixed cost
+// 52 % / 73 % per side).  With ck(key) = 0 for -inf keys, a table is unimodal when every rising pair
+// (x, x+1) precedes every falling pair; its maximum then sits at p* = 1 + the last rising x (0 if none),
+// the maximum of any window [l, r] at clamp(p*, l, r) and the runner-up next to it.  Packed keys are
+// distinct (positions in the low bits), so these are exactly the two largest keys the sparse-table
+// queries return -- the same values, positions and decisions -- and a unimodal table needs no levels.
+__device__ __forceinline__ unsigned long long ckey(unsigned long long k) { return k < 0x0010000000000000ull ? 0ull : k; }
+// pair (idx - 1, idx): a rise records idx in up (max), a fall in dn (min)
+__device__ __forceinline__ void uni_pair(unsigned long long a, unsigned long long b, unsigned idx, unsigned& up, unsigned& dn) {
+  a = ckey(a);
+  b = ckey(b);
+  up = b > a ? umax(up, idx) : up;
+  dn = b < a ? umin(dn, idx) : dn;
+}
+constexpr unsigned kNoFall = 0xffffu;
+
+__device__ __forceinline__ void window_top2_uni(const RangeMax& t, int pstar, int l, int r, double& m1, int& pos,
+                                                double& m2) {
+  if (l > r) { pos = 0; m1 = m2 = -INFINITY; return; }   // empty run (as query() on an empty range)
+  const int q = min(max(pstar, l), r);
+  pos = q;
+  m1 = unord64(t.v[q]);
+  m2 = unord64(umax64(q > l ? t.v[q - 1] : 0ull, q < r ? t.v[q + 1] : 0ull));
+}
+
 // One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.  kWait: the
 // programmatic dependency wait (W_t is the previous kernel's output) is taken here, after the input loads
 // (lambda, the g fit) are issued; the W loads follow it at once, and the singles come from the kernel
@@ -226,6 +252,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   tc.v = (unsigned long long*)(wt + ((nw + 1) & ~1));
   td.v = tc.v + (size_t)lc * tc.ns;
   __shared__ unsigned red[kWinThreads / 32];
+  __shared__ unsigned ured[4][kWinThreads / 32];   // unimodality: rises (max) and falls (min) per table
   __shared__ SingleAct ss[kMaxSingles];
 
   const double* Wrow = st.W + (p.rank1 ? 0 : (size_t)k * p.ld);
@@ -281,13 +308,18 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   }
   __syncthreads();
   wtrace(2);
-  // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores)
+  // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores); the pairs
+  // (x, x+1) and (x+1, x+2) feed the unimodality test (key x+2 recomputed here: no extra barrier)
+  unsigned upc = 0u, dnc = kNoFall, upd = 0u, dnd = kNoFall;
   for (int x = 2 * tid; x < tc.n; x += 2 * kWinThreads) {
     const int j = i0 + 1 + x;
     ulonglong2 r;
     r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
     r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_c, (double)(j + 1))), x + 1);
     *reinterpret_cast<ulonglong2*>(tc.v + x) = r;    // entry n (x + 1 == n) is padding
+    if (x + 1 < tc.n) uni_pair(r.x, r.y, x + 1, upc, dnc);
+    if (x + 2 < tc.n)
+      uni_pair(r.y, pack_key(__dsub_rn(wt[j + 2 - wbase], __dmul_rn(beta_c, (double)(j + 2))), x + 2), x + 2, upc, dnc);
   }
   for (int x = 2 * tid; x < td.n; x += 2 * kWinThreads) {
     const int j = i0 - p.Ld + x;
@@ -295,19 +327,35 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
     r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_d, (double)(j + 1))), x + 1);
     *reinterpret_cast<ulonglong2*>(td.v + x) = r;
+    if (x + 1 < td.n) uni_pair(r.x, r.y, x + 1, upd, dnd);
+    if (x + 2 < td.n)
+      uni_pair(r.y, pack_key(__dsub_rn(wt[j + 2 - wbase], __dmul_rn(beta_d, (double)(j + 2))), x + 2), x + 2, upd, dnd);
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  upc = __reduce_max_sync(0xffffffffu, upc);
+  dnc = __reduce_min_sync(0xffffffffu, dnc);
+  upd = __reduce_max_sync(0xffffffffu, upd);
+  dnd = __reduce_min_sync(0xffffffffu, dnd);
+  if ((tid & 31) == 0) {
+    red[tid >> 5] = mx;
+    ured[0][tid >> 5] = upc; ured[1][tid >> 5] = dnc; ured[2][tid >> 5] = upd; ured[3][tid >> 5] = dnd;
+  }
   __syncthreads();
+  upc = __reduce_max_sync(0xffffffffu, ured[0][tid % (kWinThreads / 32)]);
+  dnc = __reduce_min_sync(0xffffffffu, ured[1][tid % (kWinThreads / 32)]);
+  upd = __reduce_max_sync(0xffffffffu, ured[2][tid % (kWinThreads / 32)]);
+  dnd = __reduce_min_sync(0xffffffffu, ured[3][tid % (kWinThreads / 32)]);
+  const bool uni_c = upc < dnc, uni_d = upd < dnd;   // block-uniform
+  const int pc = uni_c ? 0 : p.pc, pd = uni_d ? 0 : p.pd;
   wtrace(3);
-  const int top = p.pc > p.pd ? p.pc : p.pd;
+  const int top = pc > pd ? pc : pd;      // unimodal tables need no levels
 #pragma unroll
   for (int q = 1; q <= 9; q += 2) {     // levels <= 9 (L <= 512), two per barrier: unrolled, uniform exits
     if (q > top) break;
-    if (q + 1 <= p.pc) build_level2(tc, q, tid);
-    else if (q <= p.pc) build_level(tc, q, tid);
-    if (q + 1 <= p.pd) build_level2(td, q, tid);
-    else if (q <= p.pd) build_level(td, q, tid);
+    if (q + 1 <= pc) build_level2(tc, q, tid);
+    else if (q <= pc) build_level(tc, q, tid);
+    if (q + 1 <= pd) build_level2(td, q, tid);
+    else if (q <= pd) build_level(td, q, tid);
     __syncthreads();
   }
   wtrace(4);
@@ -331,8 +379,10 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     const int x = i - i0;
     double mc1, mc2, md1, md2;
     int xc, xd;
-    window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
-    window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
+    if (uni_c) window_top2_uni(tc, (int)upc, x, x + p.Lc - 1, mc1, xc, mc2);
+    else window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
+    if (uni_d) window_top2_uni(td, (int)upd, x, x + p.Ld - 1, md1, xd, md2);
+    else window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
     const double bci = __dsub_rn(__dmul_rn(beta_c, (double)i), gc0), bdi = __dsub_rn(__dmul_rn(beta_d, (double)i), gd0);
     // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
     double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);

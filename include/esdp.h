@@ -243,6 +243,12 @@ esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
  * sliding-window stencil found a near tie and re-scanned every action canonically (then resets it). */
 esdp_status esdp_window_fallbacks(esdp_ctx* ctx, int64_t* count);
 
+/* Number of run tables (one charge and one discharge table per (stage, k, 256-column tile) item of the
+ * sliding-window stencil), summed since the last call (then resets), whose packed keys were NOT
+ * unimodal, so the sparse-table levels were built; a unimodal table is answered in O(1) from its peak
+ * (DESIGN.md §5.3).  Either way the results are the same bits. */
+esdp_status esdp_window_level_tables(esdp_ctx* ctx, int64_t* count);
+
 /* Number of kernel launches one backward pass enqueues (for harness accounting). */
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
 

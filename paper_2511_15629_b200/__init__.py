@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = [
     "esdp_create", "esdp_dims", "esdp_actions", "esdp_load", "esdp_load_async", "esdp_backward", "esdp_backward_async",
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
-    "esdp_debug_time", "esdp_window_fallbacks", "esdp_destroy", "esdp_last_error",
+    "esdp_debug_time", "esdp_window_fallbacks", "esdp_window_level_tables", "esdp_destroy", "esdp_last_error",
     "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
     "esdp_simulate_mode", "esdp_simulate_mode_dev", "esdp_simulate_strategy_dev", "esdp_price_paths_dev",
     "esdp_simulate_async", "esdp_objective_async",
@@ -106,6 +106,7 @@ def _load():
         "esdp_stencil_kind": ([ctx, _i32p], ctypes.c_int),
         "esdp_debug_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
         "esdp_window_fallbacks": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "esdp_window_level_tables": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_create_dist": ([ctypes.POINTER(esdp_problem), ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p,
                               ctypes.POINTER(_vp)], ctypes.c_int),
         "esdp_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
@@ -341,6 +342,13 @@ def esdp_debug_time(ctx, what, reps=200) -> float:
     us = ctypes.c_double()
     _check(lib.esdp_debug_time(ctx, int(what), int(reps), ctypes.byref(us)), "esdp_debug_time", ctx)
     return us.value
+
+
+def esdp_window_level_tables(ctx) -> int:
+    """Window-stencil run tables that were not unimodal (sparse-table levels built) since the last call."""
+    n = ctypes.c_int64()
+    _check(lib.esdp_window_level_tables(ctx, ctypes.byref(n)), "esdp_window_level_tables", ctx)
+    return n.value
 
 
 def esdp_window_fallbacks(ctx) -> int:

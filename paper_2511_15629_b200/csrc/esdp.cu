@@ -1591,6 +1591,15 @@ esdp_status esdp_simulate_mode(esdp_ctx* c, int64_t n_paths, uint64_t seed, int3
   return ESDP_OK;
 }
 
+esdp_status esdp_window_level_tables(esdp_ctx* c, int64_t* count) {
+  if (!c || !count) return ESDP_E_STATE;
+  unsigned long long v = 0, z = 0;
+  CUDA_OR_FAIL(c, cudaMemcpyFromSymbol(&v, g_window_level_tables, sizeof(v)));
+  CUDA_OR_FAIL(c, cudaMemcpyToSymbol(g_window_level_tables, &z, sizeof(z)));
+  *count = (int64_t)v;
+  return ESDP_OK;
+}
+
 esdp_status esdp_window_fallbacks(esdp_ctx* c, int64_t* count) {
   if (!c || !count) return ESDP_E_STATE;
   unsigned long long v = 0, z = 0;

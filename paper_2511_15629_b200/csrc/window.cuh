@@ -32,6 +32,7 @@ namespace esdp {
 #endif
 constexpr int kWinTile = ESDP_WIN_THREADS;     // output columns per block
 __device__ unsigned long long g_window_fallbacks;  // rows that needed the full canonical scan (diagnostic)
+__device__ unsigned long long g_window_level_tables;  // run tables that were not unimodal (built levels)
 constexpr int kWinThreads = ESDP_WIN_THREADS;  // one output column per thread in the query phase
 constexpr int kLevelSlots = (kWinTile + 512 + 2 * kWinThreads - 1) / (2 * kWinThreads);  // pairs per thread
 
@@ -347,6 +348,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   dnd = __reduce_min_sync(0xffffffffu, ured[3][tid % (kWinThreads / 32)]);
   const bool uni_c = upc < dnc, uni_d = upd < dnd;   // block-uniform
   const int pc = uni_c ? 0 : p.pc, pd = uni_d ? 0 : p.pd;
+  if (tid == 0 && !(uni_c && uni_d)) atomicAdd(&g_window_level_tables, (unsigned long long)(!uni_c + !uni_d));
   wtrace(3);
   const int top = pc > pd ? pc : pd;      // unimodal tables need no levels
 #pragma unroll

@@ -294,6 +294,27 @@ def test_cfg3_window_affine_degradation(rank1):
     _compare_all(inst, nthreads=16, brute=True)
 
 
+@pytest.mark.parametrize("which", ["cfg2", "cfg3"])
+def test_window_unimodal_and_level_tables(which):
+    """The window stencil answers a unimodal run table from its peak and builds sparse-table levels only
+    for the others; both give the oracle's bits.  Linear payoff (cfg2 shape): every
+    table unimodal.  cfg3's fixed cycling cost makes W non-concave: many tables take the level path."""
+    base = workloads.cfg2(T=6, K=24)
+    inst = base if which == "cfg2" else workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=6, K=24)
+    with _gpu(inst) as s:
+        E.esdp_window_level_tables(s.ctx)        # reset
+    _compare_all(inst, nthreads=16, expect_window=True)
+    with _gpu(inst) as s:
+        E.esdp_window_level_tables(s.ctx)
+        s.backward()
+        lvl = E.esdp_window_level_tables(s.ctx)
+        tables = inst.T * inst.K * ((s.S + 255) // 256) * 2
+    if which == "cfg2":
+        assert lvl == 0, (lvl, tables)
+    else:
+        assert 0.1 * tables < lvl < tables, (lvl, tables)
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_window_affine_g_random(seed):
     """Random instances with g = per-side affine (random slopes and fixed costs, g(0) = 0) use the window

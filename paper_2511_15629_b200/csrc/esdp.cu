@@ -574,9 +574,11 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-// Throughput-regime expectation (contract_dmma3_kernel): large contractions (cfg4, cfg5 batches), where
-// the number of output tiles keeps every SM busy; small ones (cfg2) stay on the latency-tuned dmma2.
-// ESDP_DMMA3=0/1 in the environment forces it off/on (measurement).
+// k'-pipelined DMMA expectation (contract_dmma3_kernel), two tilings: 16 x 64 block tiles (four 16x16
+// warp tiles) for large contractions (cfg4, cfg5 batches: >= 3e5 outputs), 8 x 32 block tiles (two 8x16
+// warp tiles) below, where the grid must cover every SM (cfg2: 416 blocks).  Measured (tools/variants_d3*.sh,
+// warm launches): cfg4 11.8 -> 9.6 us, cfg2 3.59 -> 3.25 us against dmma2.  ESDP_DMMA3=0 in the environment
+// falls back to dmma2 (measurement).
 #ifndef ESDP_D3_MT
 #define ESDP_D3_MT 2
 #endif
@@ -594,23 +596,31 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 #endif
 using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #define D3_KERNEL contract_dmma3_kernel<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>
+using D3s = Dmma3<1, 2, 2, 16, 4>;
+#define D3S_KERNEL contract_dmma3_kernel<1, 2, 2, 16, 4>
 constexpr double kDmma3MinOutputs = 3.0e5;
-bool use_dmma3(int rows, int64_t ncols, int K) {
-  if (rows < 8 || (K & 1)) return false;
+// 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large tiling
+int use_dmma3(int rows, int64_t ncols, int K) {
+  if (rows < 8 || (K & 1)) return 0;
   static const int force = [] { const char* e = getenv("ESDP_DMMA3"); return e ? atoi(e) : -1; }();
-  if (force >= 0) return force != 0;
-  return (double)rows * (double)ncols >= kDmma3MinOutputs;
+  if (force == 0) return 0;
+  return (double)rows * (double)ncols >= kDmma3MinOutputs ? 2 : 1;
 }
-cudaError_t launch_dmma3(const double* Pt, const double* Vn, double* Wt, int rows, int K, int S, int ld, cudaStream_t s,
-                         bool pdl) {
-  static const bool attr = [] {
-    return D3::smem() <= 48 * 1024 ||
-           cudaFuncSetAttribute(D3_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D3::smem()) == cudaSuccess;
-  }();
-  if (!attr) return cudaErrorInvalidConfiguration;
-  const int nrb = (rows + D3::RB - 1) / D3::RB;
-  const int64_t ncb = ((int64_t)S + D3::CB - 1) / D3::CB;
-  return launch(D3_KERNEL, dim3((unsigned)(ncb * nrb)), dim3(D3::NTH), D3::smem(), s, pdl, Pt, Vn, Wt, rows, K, S, ld, nrb);
+template <typename DD>
+cudaError_t launch_dmma3_as(void (*kern)(const double*, const double*, double*, int, int, int, int, int), const double* Pt,
+                            const double* Vn, double* Wt, int rows, int K, int S, int ld, cudaStream_t s, bool pdl) {
+  if (DD::smem() > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DD::smem());
+    if (e != cudaSuccess) return e;
+  }
+  const int nrb = (rows + DD::RB - 1) / DD::RB;
+  const int64_t ncb = ((int64_t)S + DD::CB - 1) / DD::CB;
+  return launch(kern, dim3((unsigned)(ncb * nrb)), dim3(DD::NTH), DD::smem(), s, pdl, Pt, Vn, Wt, rows, K, S, ld, nrb);
+}
+cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* Wt, int rows, int K, int S, int ld,
+                         cudaStream_t s, bool pdl) {
+  return which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
+                    : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
 }
 
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
@@ -620,8 +630,8 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   if (rows == 0) return cudaSuccess;
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
-    if (!(c->flags & ESDP_DMMA_L2) && use_dmma3(rows, S, K))
-      return launch_dmma3(Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl);
+    if (const int d3 = (c->flags & ESDP_DMMA_L2) ? 0 : use_dmma3(rows, S, K))
+      return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl);
     if (c->dmma2) {
       if (K > 128) {   // large K: taller tiles (fewer re-reads of the V column block)
         const int ncb = (S + kDCbig * 16 - 1) / (kDCbig * 16), nrb = (rows + kDRbig * 8 - 1) / (kDRbig * 8);
@@ -1776,8 +1786,8 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
     } else {
       const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
       cudaError_t e;
-      if (!b->rank1 && use_dmma3(rows, (int64_t)NL, K)) {
-        e = launch_dmma3(Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, s, after_kernel);
+      if (const int d3 = b->rank1 ? 0 : use_dmma3(rows, (int64_t)NL, K)) {
+        e = launch_dmma3(d3, Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, s, after_kernel);
       } else if (!b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
         const int ncb = (int)((NL + kDCbig * 16 - 1) / (kDCbig * 16)), nrb = (K + kDRbig * 8 - 1) / (kDRbig * 8);
         e = launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),

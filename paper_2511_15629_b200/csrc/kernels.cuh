@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   // (rows kb + j*BR, column pair cb); per chunk only the k' bound is checked and the pointers advance.
   // Out-of-range pieces are zero-filled by the copy itself (src-size 0).
   constexpr int AP = 8 * MT * (KC / 2), BP = KC * (D::CB / 2);
-  static_assert(AP % D::NTH == 0 || D::NTH % AP == 0, "A pieces per thread");
+  static_assert(AP <= D::NTH || (AP % D::NTH == 0 && D::NTH % (KC / 2) == 0), "A pieces per thread");
   static_assert(D::NTH % (D::CB / 2) == 0 && BP % D::NTH == 0, "B pieces per thread");
   constexpr int NA = AP >= D::NTH ? AP / D::NTH : 1, NB = BP / D::NTH, BR = D::NTH / (D::CB / 2);
   const bool a_thr = tid < AP;

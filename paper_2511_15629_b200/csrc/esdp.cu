@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -43,7 +44,9 @@ struct DevBuf {
 // One set of device inputs (double-buffered: a load fills the slot the running backward does not read).
 struct InputSlot {
   double *lambda = nullptr, *P = nullptr, *pi = nullptr, *cdf = nullptr, *cdf1 = nullptr, *g = nullptr, *gfit = nullptr;
-  int16_t *guide = nullptr, *guide1 = nullptr;
+  uint64_t *guide = nullptr, *guide1 = nullptr;
+  int *tab = nullptr, *src = nullptr;   // Markov: sampling table of each stage, representative stage of each table
+  int nuniq = 0, gbits = 0;             // distinct P_t slices (tables) and guide bits of this slot's tables
   cudaEvent_t ev_head = nullptr, ev_tables = nullptr, use_ev = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   bool use_pending = false;
@@ -85,8 +88,9 @@ struct esdp_ctx {
   int64_t stack_cap = 0;
   double gfit[6] = {0, 0, 0, 0, 0, 0};
   double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
-  int16_t *d_guide = nullptr, *d_guide1 = nullptr;
-  int G = 16;
+  uint64_t *d_guide = nullptr, *d_guide1 = nullptr;
+  int g_max = 10, g_r1 = 10;  // guide bits: at most (pi_1 table; Markov tables when they fit), rank-1 rows
+  size_t guide_cap = 0;       // guide entries allocated per slot
   double *d_red = nullptr;
   int16_t* d_pol = nullptr;
   double* d_sim = nullptr;
@@ -267,6 +271,51 @@ class HostPool {
   bool stop_ = false;
 };
 
+// Guide geometry of the sampling tables (kernels.cuh cdf_kernel): 2^g buckets per row, g in [6, 14],
+// at most the first power of two >= 16 K; g_for: the most bits for `rows` rows within `cap` entries.
+constexpr int kGuideMinG = 6;
+int guide_gmax(int K) {
+  int g = kGuideMinG;
+  while (g < 14 && (1 << g) < 16 * K) ++g;
+  return g;
+}
+int guide_g_for(size_t rows, size_t cap, int gmax) {
+  int g = gmax;
+  while (g > kGuideMinG && (rows << g) > cap) --g;
+  return g;
+}
+
+// Identical stage slices P_t ([K][K]) share one sampling table (a time-homogeneous chain needs one, an
+// hour-of-day chain 24): tab[t] = table of stage t + 1, src[u] = the first stage with table u.  Slices
+// are hashed on the host pool, equal hashes confirmed byte for byte.
+void dedupe_slices(const double* P, int nst, int K, std::vector<int>& tab, std::vector<int>& src) {
+  const size_t n = (size_t)K * K;
+  std::vector<uint64_t> h((size_t)nst);
+  std::function<void(int)> hash = [&](int t) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(P + (size_t)t * n);
+    uint64_t x = 0xcbf29ce484222325ull;
+    for (size_t j = 0; j < n; ++j) x = (x ^ w[j]) * 0x100000001b3ull;
+    h[(size_t)t] = x;
+  };
+  if (nst > 1 && (size_t)nst * n > (1u << 16)) HostPool::get().run(nst, hash);
+  else for (int t = 0; t < nst; ++t) hash(t);
+  tab.assign((size_t)nst, 0);
+  src.clear();
+  std::unordered_map<uint64_t, std::vector<int>> seen;
+  for (int t = 0; t < nst; ++t) {
+    std::vector<int>& cand = seen[h[(size_t)t]];
+    int u = -1;
+    for (int v : cand)
+      if (std::memcmp(P + (size_t)src[(size_t)v] * n, P + (size_t)t * n, n * sizeof(double)) == 0) { u = v; break; }
+    if (u < 0) {
+      u = (int)src.size();
+      src.push_back(t);
+      cand.push_back(u);
+    }
+    tab[(size_t)t] = u;
+  }
+}
+
 esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
   for (long long j = 0; j < (long long)c->T * c->K; ++j)
     if (!std::isfinite(lambda[j])) return fail(c, ESDP_E_DATA, "lambda[%lld] is not finite", j);
@@ -425,7 +474,7 @@ void free_all(esdp_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->slot[0].lambda) {   // full context: the input aliases point into the slots
     for (InputSlot& x : c->slot) {
-      void* sp[] = {x.lambda, x.P, x.pi, x.cdf, x.cdf1, x.g, x.gfit, x.guide, x.guide1};
+      void* sp[] = {x.lambda, x.P, x.pi, x.cdf, x.cdf1, x.g, x.gfit, x.guide, x.guide1, x.tab, x.src};
       for (void* p : sp)
         if (p) cudaFree(p);
       for (cudaEvent_t e : x.chunk_ev) cudaEventDestroy(e);
@@ -455,7 +504,7 @@ void free_all(esdp_ctx* c) {
 // (chunk_ev), then the simulation's sampling tables of P (ev_tables).  Does not synchronize.
 esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const double* P, const double* pi,
                    const double* g) {
-  const size_t TK = (size_t)c->T * c->K, K = c->K, G = c->G;
+  const size_t TK = (size_t)c->T * c->K, K = c->K;
   InputSlot& d = c->slot[dst];
   const InputSlot& o = c->slot[src];
   const bool copy_old = src != dst;
@@ -469,16 +518,16 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   if (pi) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, pi, npi * sizeof(double), h2d, s));
     if (c->rank1)   // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
-      launch_cdf(d.pi, c->T, c->K, c->G, d.cdf, d.guide, s);
-    launch_cdf(d.pi, 1, c->K, c->G, d.cdf1, d.guide1, s);  // pi_1 (row 0 in rank-1)
+      launch_cdf(d.pi, nullptr, c->T, c->K, c->g_r1, d.cdf, d.guide, s);
+    launch_cdf(d.pi, nullptr, 1, c->K, c->g_max, d.cdf1, d.guide1, s);  // pi_1 (row 0 in rank-1)
     CUDA_OR_FAIL(c, cudaGetLastError());
   } else if (copy_old) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, o.pi, npi * sizeof(double), d2d, s));
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf1, o.cdf1, K * sizeof(double), d2d, s));
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide1, o.guide1, G * sizeof(int16_t), d2d, s));
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide1, o.guide1, sizeof(uint64_t) << c->g_max, d2d, s));
     if (c->rank1) {
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, TK * sizeof(double), d2d, s));
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (size_t)c->T * G * sizeof(int16_t), d2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, ((size_t)c->T << c->g_r1) * sizeof(uint64_t), d2d, s));
     }
   }
   const size_t ng = c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : (size_t)c->A;
@@ -509,17 +558,41 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   // on that simulation's stream: built here, their blocks would share the SMs with the running backward's
   // latency-bound stage chain and stretch it (measured +0.3 ms per cfg2 solve).
   if (!c->rank1 && c->T > 1) {
-    const int64_t nr = (int64_t)(c->T - 1) * c->K;
-    if (P || (copy_old && o.tables_stale)) {
+    const int nst = c->T - 1;
+    if (P) {   // one table per distinct slice P_t; as many guide bits as the allocation allows
+      std::vector<int> tab, src;
+      dedupe_slices(P, nst, c->K, tab, src);
+      d.nuniq = (int)src.size();
+      d.gbits = guide_g_for((size_t)d.nuniq * K, c->guide_cap, c->g_max);
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, tab.data(), nst * sizeof(int), h2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.src, src.data(), src.size() * sizeof(int), h2d, s));
       d.tables_stale = true;
     } else if (copy_old) {
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, (size_t)nr * K * sizeof(double), d2d, s));
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (size_t)nr * G * sizeof(int16_t), d2d, s));
-      d.tables_stale = false;
+      d.nuniq = o.nuniq;
+      d.gbits = o.gbits;
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, o.tab, nst * sizeof(int), d2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.src, o.src, nst * sizeof(int), d2d, s));
+      if (o.tables_stale) {
+        d.tables_stale = true;
+      } else {
+        const size_t nr = (size_t)d.nuniq * K;
+        CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, nr * K * sizeof(double), d2d, s));
+        CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, (nr << d.gbits) * sizeof(uint64_t), d2d, s));
+        d.tables_stale = false;
+      }
     }
   }
   CUDA_OR_FAIL(c, cudaEventRecord(d.ev_tables, s));
   return ESDP_OK;
+}
+
+// The active slot's sampling tables in a simulation's parameters.
+void sim_tables(const esdp_ctx* c, SimParams& sp) {
+  const InputSlot& x = c->slot[c->active];
+  sp.cdf = x.cdf; sp.cdf1 = x.cdf1; sp.guide = x.guide; sp.guide1 = x.guide1;
+  sp.tab = c->rank1 ? nullptr : x.tab;
+  sp.gs = 53 - x.gbits;
+  sp.gs1 = 53 - c->g_max;
 }
 
 // Before a simulation on stream s: wait for the active slot's uploads and build its sampling tables of
@@ -528,8 +601,7 @@ esdp_status ready_tables(esdp_ctx* c, cudaStream_t s) {
   InputSlot& x = c->slot[c->active];
   CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, x.ev_tables, 0));
   if (x.tables_stale) {
-    const int64_t nr = (int64_t)(c->T - 1) * c->K;
-    launch_cdf(x.P, nr, c->K, c->G, x.cdf, x.guide, s);
+    launch_cdf(x.P, x.src, (int64_t)x.nuniq * c->K, c->K, x.gbits, x.cdf, x.guide, s);
     CUDA_OR_FAIL(c, cudaGetLastError());
     CUDA_OR_FAIL(c, cudaEventRecord(x.ev_tables, s));
     x.tables_stale = false;
@@ -1048,11 +1120,13 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     return bail(ESDP_E_CUDA);
   }
   const size_t T = c->T, K = c->K, S = c->S, A = c->A;
-  {   // guide buckets per cdf row: most buckets pure (one load per draw); 16 K where the tables stay
-      // under ~512 MB, at least 4 K
-    const double rows = (double)(c->rank1 ? T : (T - 1) * K) + 1.0;
-    const int cap = (int)std::min(32767.0, 256e6 / rows);
-    c->G = std::max<int>(64, std::max<int>(4 * (int)K, std::min<int>(16 * (int)K, cap)));
+  {   // guide geometry (kernels.cuh cdf_kernel): up to 2^g_max >= 16 K buckets per row; the allocation is
+      // capped at max(256 MB, the size of P) and always holds 2^6 buckets for every possible row
+    c->g_max = guide_gmax((int)K);
+    const size_t rows = c->rank1 ? T : (T > 1 ? (T - 1) * K : 1);
+    const size_t budget = std::max<size_t>(256u << 20, (c->rank1 ? 0 : rows * K * 8)) / sizeof(uint64_t);
+    c->guide_cap = std::max(rows << kGuideMinG, std::min(rows << c->g_max, budget));
+    c->g_r1 = guide_g_for(T, c->guide_cap, c->g_max);
   }
   if (!tables_only) {   // two input slots (double-buffered loads); the aliases follow select_slot
     for (InputSlot& x : c->slot) {
@@ -1061,8 +1135,13 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
       TRY(dev_alloc(c, &x.pi, c->rank1 ? T * K : K));
       TRY(dev_alloc(c, &x.cdf, c->rank1 ? T * K : (T - 1) * K * K));
       TRY(dev_alloc(c, &x.cdf1, K));
-      TRY(dev_alloc(c, &x.guide, (c->rank1 ? T : (T - 1) * K) * (size_t)c->G));
-      TRY(dev_alloc(c, &x.guide1, (size_t)c->G));
+      TRY(dev_alloc(c, &x.guide, c->guide_cap));
+      TRY(dev_alloc(c, &x.guide1, (size_t)1 << c->g_max));
+      if (!c->rank1 && T > 1) {
+        TRY(dev_alloc(c, &x.tab, T - 1));
+        TRY(dev_alloc(c, &x.src, T - 1));
+      }
+      x.gbits = c->rank1 ? c->g_r1 : c->g_max;
       TRY(dev_alloc(c, &x.g, c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A));
       TRY(dev_alloc(c, &x.gfit, 6));
       cudaMemset(x.g, 0, (c->kind == ESDP_PAYOFF_TABLE ? T * K * A : A) * sizeof(double));
@@ -1457,8 +1536,8 @@ esdp_status esdp_simulate_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, doubl
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
   if (n_paths < 1) return fail(c, ESDP_E_STATE, "n_paths must be >= 1");
   SimParams sp;
-  sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
-  sp.guide = c->d_guide; sp.guide1 = c->d_guide1; sp.G = c->G;
+  sp.pol = c->d_pol; sp.lambda = c->d_lambda;
+  sim_tables(c, sp);
   sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
@@ -1477,8 +1556,9 @@ esdp_status esdp_price_paths_dev(esdp_ctx* c, int64_t n_paths, uint64_t seed, in
   if (!c) return ESDP_E_STATE;
   if (n_paths < 1 || (!kpath_dev && !lambda_dev)) return fail(c, ESDP_E_STATE, "n_paths >= 1 and an output are required");
   SimParams sp{};
-  sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda; sp.guide = c->d_guide; sp.guide1 = c->d_guide1;
-  sp.G = c->G; sp.T = c->T; sp.K = c->K; sp.rank1 = c->rank1;
+  sp.lambda = c->d_lambda;
+  sim_tables(c, sp);
+  sp.T = c->T; sp.K = c->K; sp.rank1 = c->rank1;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   if (esdp_status e = ready_tables(c, s)) return e;
   price_path_kernel<<<(unsigned)((n_paths + 127) / 128), 128, 0, s>>>(sp, n_paths, seed, kpath_dev, lambda_dev);
@@ -1553,8 +1633,8 @@ esdp_status esdp_simulate_strategy_dev(esdp_ctx* c, int64_t n_paths, uint64_t se
   }
   SimModeParams mp{};
   SimParams& sp = mp.base;
-  sp.pol = c->d_pol; sp.cdf = c->d_cdf; sp.cdf1 = c->d_cdf1; sp.lambda = c->d_lambda;
-  sp.guide = c->d_guide; sp.guide1 = c->d_guide1; sp.G = c->G;
+  sp.pol = c->d_pol; sp.lambda = c->d_lambda;
+  sim_tables(c, sp);
   sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
   sp.T = c->T; sp.K = c->K; sp.S = c->S; sp.A = c->A; sp.rank1 = c->rank1; sp.kind = c->kind; sp.Kp = c->Kp;
   sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;
@@ -1717,10 +1797,11 @@ const char* esdp_last_error(const esdp_ctx* c) { return c ? c->err.c_str() : g_c
 }  // extern "C"
 
 struct esdp_batch {
-  int n = 0, T = 0, K = 0, S = 0, ld = 0, rank1 = 0, G = 0;
+  int n = 0, T = 0, K = 0, S = 0, ld = 0, rank1 = 0, gbits = 0, g_max = 0;   // guide bits: tables, pi_1
   std::vector<esdp_ctx*> inst;        // per-instance parameters and action tables (tables_only contexts)
   double *d_lambda = nullptr, *d_P = nullptr, *d_pi = nullptr, *d_cdf = nullptr, *d_cdf1 = nullptr;
-  int16_t *d_guide = nullptr, *d_guide1 = nullptr;
+  uint64_t *d_guide = nullptr, *d_guide1 = nullptr;
+  int *d_tab = nullptr, *d_src = nullptr;   // Markov: deduplicated sampling tables (as esdp_ctx's slots)
   double *d_V = nullptr, *d_W = nullptr, *d_J = nullptr;   // V [2][K][n][ld], W [rows][n][ld]
   int16_t* d_pol = nullptr;                                // [n][T][K][S]
   BatchInst* d_bi = nullptr;
@@ -1762,7 +1843,7 @@ esdp_status balloc(esdp_batch* b, T** p, size_t n) {
 
 void batch_free(esdp_batch* b) {
   if (b->graph) cudaGraphExecDestroy(b->graph);
-  void* ps[] = {b->d_lambda, b->d_P, b->d_pi, b->d_cdf, b->d_cdf1, b->d_guide, b->d_guide1, b->d_V, b->d_W,
+  void* ps[] = {b->d_lambda, b->d_P, b->d_pi, b->d_cdf, b->d_cdf1, b->d_guide, b->d_guide1, b->d_tab, b->d_src, b->d_V, b->d_W,
                 b->d_J, b->d_pol, b->d_bi, b->d_widx, b->d_bidx};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -1875,21 +1956,29 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
     b->inst.push_back(c);
   }
   esdp_ctx* c0 = b->inst[0];
-  b->T = c0->T; b->K = c0->K; b->S = c0->S; b->ld = c0->ld; b->rank1 = c0->rank1; b->G = c0->G;
+  b->T = c0->T; b->K = c0->K; b->S = c0->S; b->ld = c0->ld; b->rank1 = c0->rank1; b->g_max = c0->g_max;
   {   // the shared inputs, validated once (as esdp_create does)
     esdp_status st = validate_data(c0, p0.lambda, p0.P, p0.pi, p0.g);
     if (st != ESDP_OK) { b->err = c0->err; return bail(st); }
   }
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(bfail(b, ESDP_E_CUDA, "cannot create a CUDA stream"));
-  const size_t T = b->T, K = b->K, S = b->S, NL = (size_t)n * b->ld, G = b->G;
+  const size_t T = b->T, K = b->K, S = b->S, NL = (size_t)n * b->ld;
+  std::vector<int> tab, src;   // Markov: one sampling table per distinct slice P_t
+  if (!b->rank1 && T > 1) dedupe_slices(p0.P, (int)T - 1, (int)K, tab, src);
+  const size_t ntab_rows = b->rank1 ? T : src.size() * K;
+  b->gbits = b->rank1 ? c0->g_r1 : guide_g_for(ntab_rows, c0->guide_cap, c0->g_max);
   BTRY(balloc(b, &b->d_lambda, T * K));
   BTRY(balloc(b, &b->d_P, b->rank1 ? 1 : (T - 1) * K * K));
   BTRY(balloc(b, &b->d_pi, b->rank1 ? T * K : K));
   BTRY(balloc(b, &b->d_cdf, b->rank1 ? T * K : (T - 1) * K * K));
   BTRY(balloc(b, &b->d_cdf1, K));
-  BTRY(balloc(b, &b->d_guide, (b->rank1 ? T : (T - 1) * K) * G));
-  BTRY(balloc(b, &b->d_guide1, G));
+  BTRY(balloc(b, &b->d_guide, std::max<size_t>(ntab_rows, 1) << b->gbits));
+  BTRY(balloc(b, &b->d_guide1, (size_t)1 << b->g_max));
+  if (!tab.empty()) {
+    BTRY(balloc(b, &b->d_tab, tab.size()));
+    BTRY(balloc(b, &b->d_src, src.size()));
+  }
   BTRY(balloc(b, &b->d_V, 2 * K * NL));
   BTRY(balloc(b, &b->d_W, (b->rank1 ? 1 : K) * NL));
   BTRY(balloc(b, &b->d_pol, (size_t)n * T * K * S));
@@ -1903,16 +1992,17 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   BCUDA(b, cudaMemcpyAsync(b->d_lambda, p0.lambda, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
   if (b->rank1) {
     BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
-    launch_cdf(b->d_pi, (int64_t)T, (int)K, (int)G, b->d_cdf, b->d_guide, s);
+    launch_cdf(b->d_pi, nullptr, (int64_t)T, (int)K, b->gbits, b->d_cdf, b->d_guide, s);
   } else {
     BCUDA(b, cudaMemcpyAsync(b->d_pi, p0.pi, K * sizeof(double), cudaMemcpyHostToDevice, s));
     if (T > 1) {
       BCUDA(b, cudaMemcpyAsync(b->d_P, p0.P, (T - 1) * K * K * sizeof(double), cudaMemcpyHostToDevice, s));
-      const int64_t nr = (int64_t)(T - 1) * K;
-      launch_cdf(b->d_P, nr, (int)K, (int)G, b->d_cdf, b->d_guide, s);
+      BCUDA(b, cudaMemcpyAsync(b->d_tab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      BCUDA(b, cudaMemcpyAsync(b->d_src, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      launch_cdf(b->d_P, b->d_src, (int64_t)ntab_rows, (int)K, b->gbits, b->d_cdf, b->d_guide, s);
     }
   }
-  launch_cdf(b->d_pi, 1, (int)K, (int)G, b->d_cdf1, b->d_guide1, s);
+  launch_cdf(b->d_pi, nullptr, 1, (int)K, b->g_max, b->d_cdf1, b->d_guide1, s);
   BCUDA(b, cudaGetLastError());
   // per-instance parameters
   std::vector<BatchInst> hbi((size_t)n);
@@ -1927,7 +2017,8 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
     x.sp.K = (int)K;
     SimParams& sp = x.sim;
     sp.pol = b->d_pol + (size_t)m * T * K * S; sp.cdf = b->d_cdf; sp.cdf1 = b->d_cdf1; sp.lambda = b->d_lambda;
-    sp.guide = b->d_guide; sp.guide1 = b->d_guide1; sp.G = (int)G;
+    sp.guide = b->d_guide; sp.guide1 = b->d_guide1; sp.tab = b->d_tab;
+    sp.gs = 53 - b->gbits; sp.gs1 = 53 - b->g_max;
     sp.act = c->d_act; sp.w = c->d_w; sp.off = c->d_off; sp.g = c->d_g;
     sp.T = (int)T; sp.K = (int)K; sp.S = (int)S; sp.A = c->A; sp.rank1 = b->rank1; sp.kind = c->kind; sp.Kp = (int)K;
     sp.on_grid = c->on_grid; sp.f0 = c->f0; sp.w0 = c->w0;

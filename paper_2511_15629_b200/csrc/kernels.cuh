@@ -761,8 +761,10 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
   int a_prev = st_get(0);
   double u_prev = u_of(a_prev);
   double p_prev = tb.act[a_prev], prev_price = 0.0;
-  if (kSmem) vo[0] = (int16_t)a_prev;
-  if (qo) qo[0] = p_prev;
+  // curve outputs are written once and read by the host or a later kernel: streaming stores (evict-first
+  // in L2), so that 0.5 GB of cfg2 curves do not push the policy table out before the simulation
+  if (kSmem) __stcs(vo, (short)a_prev);
+  if (qo) __stcs(qo, p_prev);
 #if BID_PF_EMIT
   int a_n = nh > 1 ? st_get(1) : 0;
   double u_n = nh > 1 ? u_of(a_n) : 0.0, p_n = nh > 1 ? tb.act[a_n] : 0.0;
@@ -778,9 +780,9 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
 #endif
     double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
     if (j > 1 && pj < prev_price) pj = prev_price;
-    pro[(size_t)(j - 1) * nout] = pj;
-    if (kSmem) vo[(size_t)j * nout] = (int16_t)a;
-    if (qo) qo[(size_t)j * nout] = pc;
+    __stcs(pro + (size_t)(j - 1) * nout, pj);
+    if (kSmem) __stcs(vo + (size_t)j * nout, (short)a);
+    if (qo) __stcs(qo + (size_t)j * nout, pc);
     prev_price = pj; u_prev = u; p_prev = pc;
   }
   *nvo = nh;
@@ -879,50 +881,62 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
   }
 }
 
-__device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t, double& u1, double& u2) {
+// The two draws of (path, t): 53-bit integers m (the sampler decides on them) and u = m 2^-53 (exact).
+__device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t, double& u1, double& u2, uint64_t& m1,
+                                             uint64_t& m2) {
   uint32_t c[4] = {(uint32_t)((uint64_t)path & 0xffffffffu), (uint32_t)((uint64_t)path >> 32), (uint32_t)t,
                    0x45534450u};
   philox4x32_10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
-  u1 = (double)((((uint64_t)c[0]) << 21) | (c[1] >> 11)) * 0x1p-53;
-  u2 = (double)((((uint64_t)c[2]) << 21) | (c[3] >> 11)) * 0x1p-53;
+  m1 = (((uint64_t)c[0]) << 21) | (c[1] >> 11);
+  m2 = (((uint64_t)c[2]) << 21) | (c[3] >> 11);
+  u1 = (double)m1 * 0x1p-53;
+  u2 = (double)m2 * 0x1p-53;
+}
+__device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t, double& u1, double& u2) {
+  uint64_t m1, m2;
+  sim_uniforms(seed, path, t, u1, u2, m1, m2);
 }
 
-// cdf rows (DESIGN R17): running sum in ascending order, last entry forced to 1; plus a guide table
-// guide[b] = first j with b/G < cdf[j] (from a binary search; any start is exact for the sampler's
-// scans), so that a draw u in [b/G, (b+1)/G) starts its search there.  A bucket whose whole u range
-// (widened by 2^-49 for the rounding of u*G and of b/G) maps to one j is "pure" and stores ~j (< 0): the
-// sampler returns it without touching the cdf row.  One warp per row.  Staged path (the row and its
-// guide fit kCdfSmemBytes of shared memory): every lane forms the same sequential sum over broadcast
-// values (bit-identical to the oracle's cdf) and keeps its own entries; each lane then fills a contiguous
-// run of buckets by one binary search plus a monotone walk; the row and the guide leave with coalesced
-// stores.  Global path (larger rows): lane 0 sums, every bucket is binary-searched.
+// Sampling tables (DESIGN R17 and §5 "a7"): a cdf row is the running sum of a P (or pi) row in ascending
+// order with the last entry forced to 1 (bit-identical to the oracle's), and a draw is the first j with
+// u < cdf[j].  The guide splits [0, 1) into G = 2^g buckets of the draw's 53-bit integer m (u = m 2^-53):
+// bucket b holds m in [b 2^s, (b+1) 2^s), s = 53 - g.  Its 64-bit entry decides most draws with ONE load:
+//   bits 63..49  j_lo = the first j with cdf[j] > b 2^-g (the answer for the bucket's smallest m)
+//   bits 48..43  dl:  0  the whole bucket maps to j_lo ("pure")
+//                     1..62  one boundary inside: m < T ? j_lo : j_lo + dl, with T = ceil(cdf[j_lo] 2^53)
+//                        (u < cdf[j_lo] <=> m < T, exactly) and j_lo + dl the next state of larger cdf
+//                     63  several boundaries: scan the cdf row from j_lo (as the definition reads)
+//   bits 42..0   T - b 2^s, aligned to 43 bits (exact when s <= 43; else truncated, and a draw that
+//                ties the truncated bits compares u with cdf[j_lo] itself).
+// One warp per row; rows are (table u, state k), read from P row (src[u] K + k) (src: the stage whose
+// slice a deduplicated table u stands for; NULL: u itself).
 constexpr int kCdfWarps = 4;
-constexpr int kCdfSmemBytes = 8192;   // per warp
-__host__ __device__ inline int cdf_row_doubles(int K, int G) { return K + (G + 3) / 4; }   // cdf row + int16 guide
-inline bool cdf_staged(int K, int G) { return (size_t)cdf_row_doubles(K, G) * 8 <= (size_t)kCdfSmemBytes; }
+constexpr int kCdfSmemK = 1024;   // rows up to this K are staged in shared memory
+constexpr int kGuideJ = 49, kGuideD = 43;
+constexpr uint64_t kGuideThr = (1ull << kGuideD) - 1;
 template <bool kSmem>
-__global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __restrict__ q, int64_t rows, int K, int G,
-                                                            double* __restrict__ cdf, int16_t* __restrict__ guide) {
-  extern __shared__ __align__(16) double cdf_sm[];
+__global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __restrict__ q, const int* __restrict__ src,
+                                                            int64_t rows, int K, int g, double* __restrict__ cdf,
+                                                            uint64_t* __restrict__ guide) {
+  __shared__ double cdf_sm[kSmem ? kCdfWarps * kCdfSmemK : 1];
   const int64_t r = (int64_t)blockIdx.x * kCdfWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  const double* qr = q + r * K;
+  const int64_t u = r / K, k = r - u * K;
+  const double* qr = q + ((src ? (int64_t)src[u] : u) * K + k) * K;
   double* cg = cdf + r * K;
-  int16_t* gr = guide + r * G;
-  const double m = 0x1p-49, invG = 1.0 / (double)G;
-  if (kSmem) {
-    double* cr = cdf_sm + (size_t)(threadIdx.x >> 5) * cdf_row_doubles(K, G);
-    int16_t* gs = (int16_t*)(cr + K);
-    double s = 0.0;
+  uint64_t* gr = guide + (r << g);
+  double* cr = kSmem ? cdf_sm + (size_t)(threadIdx.x >> 5) * kCdfSmemK : cg;
+  if (kSmem) {   // every lane forms the same sequential sum over broadcast values and keeps its entries
+    double sum = 0.0;
     for (int j0 = 0; j0 < K; j0 += 32) {
       const int j = j0 + lane;
       const double v = j < K ? __ldg(qr + j) : 0.0;
       const int n = min(32, K - j0);
       double mine = 0.0;
       for (int l = 0; l < n; ++l) {
-        s = __dadd_rn(s, __shfl_sync(0xffffffffu, v, l));
-        if (l == lane) mine = s;
+        sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, v, l));
+        if (l == lane) mine = sum;
       }
       if (j < K) {
         const double c = (j == K - 1) ? 1.0 : mine;
@@ -930,97 +944,84 @@ __global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __res
         cg[j] = c;
       }
     }
-    __syncwarp();
-    const int R = (G + 31) >> 5, b0 = lane * R, b1 = min(G, b0 + R);
-    if (b0 < b1) {
-      double bd = (double)b0;                        // exact integer counter (no per-bucket conversion)
-      double lo = __dmul_rn(bd, invG);
-      int a = 0, z = K - 1;                          // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
-      while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
-      int j = a;
-      double cj = cr[j], cjm = j > 0 ? cr[j - 1] : 0.0;
-      for (int b = b0; b < b1; ++b) {
-        bd = __dadd_rn(bd, 1.0);
-        const double hi = __dmul_rn(bd, invG);       // fl((b + 1) / G) as in the global path
-        while (!(lo < cj)) { cjm = cj; ++j; cj = cr[j]; }
-        const bool below = j == 0 || cjm < __dsub_rn(lo, m);
-        const bool above = j == K - 1 || cj > __dadd_rn(hi, m);
-        gs[b] = (int16_t)(below && above ? ~j : j);
-        lo = hi;
-      }
-    }
-    __syncwarp();
-    if ((G & 1) == 0) {                              // r * G even: 4-byte aligned rows
-      const uint32_t* src = (const uint32_t*)gs;
-      uint32_t* dst = (uint32_t*)gr;
-      for (int b = lane; b < (G >> 1); b += 32) dst[b] = src[b];
-    } else {
-      for (int b = lane; b < G; b += 32) gr[b] = gs[b];
-    }
-    return;
-  }
-  double* cr = cg;
-  if (lane == 0) {
-    double s = 0.0;
+  } else if (lane == 0) {
+    double sum = 0.0;
     for (int j = 0; j < K; ++j) {
-      s = __dadd_rn(s, qr[j]);
-      cr[j] = (j == K - 1) ? 1.0 : s;
+      sum = __dadd_rn(sum, qr[j]);
+      cr[j] = (j == K - 1) ? 1.0 : sum;
     }
   }
   __syncwarp();
-  for (int b = lane; b < G; b += 32) {
-    const double lo = __dmul_rn((double)b, invG), hi = __dmul_rn((double)(b + 1), invG);
-    int a = 0, z = K - 1;
+  const int s = 53 - g;
+  const double inv = ldexp(1.0, -g);
+  for (int b = lane; b < (1 << g); b += 32) {     // interleaved buckets: coalesced 8-byte stores
+    const double lo = (double)b * inv, hi = (double)(b + 1) * inv;   // exact (powers of two)
+    int a = 0, z = K - 1;                          // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
     while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
-    const int j = a;
-    const bool below = j == 0 || cr[j - 1] < __dsub_rn(lo, m);      // every u of the bucket >= cdf[j-1]
-    const bool above = j == K - 1 || cr[j] > __dadd_rn(hi, m);      // every u of the bucket <  cdf[j]
-    gr[b] = (int16_t)(below && above ? ~j : j);
+    const int jl = a;
+    const double cl = cr[jl];
+    uint64_t e = (uint64_t)jl << kGuideJ;
+    if (cl < hi) {                                 // a boundary inside the bucket
+      int jh = jl + 1;
+      while (jh < K && !(cr[jh] > cl)) ++jh;       // next state of larger cdf (skips empty states)
+      if (jh < K && jh - jl <= 62 && !(cr[jh] < hi)) {
+        const uint64_t T = (uint64_t)ceil(cl * 0x1p53), thr = T - ((uint64_t)b << s);   // in [1, 2^s]
+        if (thr < (1ull << s))                     // thr == 2^s: every m of the bucket is below T (pure)
+          e |= ((uint64_t)(jh - jl) << kGuideD) | (s <= kGuideD ? thr << (kGuideD - s) : thr >> (s - kGuideD));
+      } else {
+        e |= 63ull << kGuideD;
+      }
+    }
+    gr[b] = e;
   }
 }
 
 inline unsigned cdf_blocks(int64_t rows) { return (unsigned)((rows + kCdfWarps - 1) / kCdfWarps); }
 
-inline void launch_cdf(const double* q, int64_t rows, int K, int G, double* cdf, int16_t* guide, cudaStream_t s) {
+inline void launch_cdf(const double* q, const int* src, int64_t rows, int K, int g, double* cdf, uint64_t* guide,
+                       cudaStream_t s) {
   if (rows <= 0) return;
-  if (cdf_staged(K, G))
-    cdf_kernel<true><<<cdf_blocks(rows), kCdfWarps * 32, (size_t)kCdfWarps * cdf_row_doubles(K, G) * 8, s>>>(q, rows, K, G, cdf,
-                                                                                               guide);
-  else
-    cdf_kernel<false><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, rows, K, G, cdf, guide);
+  if (K <= kCdfSmemK) cdf_kernel<true><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, src, rows, K, g, cdf, guide);
+  else cdf_kernel<false><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, src, rows, K, g, cdf, guide);
 }
 
-// first j in [0, K) with u < cdf[j]; pure buckets answer directly, otherwise the guide gives a start and
-// the scans make it exact for any start (both neighbours are loaded together).
-__device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const int16_t* __restrict__ guide, int K,
-                                          int G, double u) {
-  int b = (int)__dmul_rn(u, (double)G);
-  b = b < G ? b : G - 1;
-  int j = __ldg(guide + b);
-  if (j < 0) return ~j;
-  const double cl = j > 0 ? __ldg(cdf + j - 1) : -1.0, ch = __ldg(cdf + j);
-  if (u < cl) {
-    --j;
-    while (j > 0 && u < __ldg(cdf + j - 1)) --j;
-  } else if (!(u < ch)) {
-    ++j;
-    while (j < K - 1 && !(u < __ldg(cdf + j))) ++j;
+// first j in [0, K) with u < cdf[j] (m: the draw's 53-bit integer, u = m 2^-53); gs = 53 - g
+__device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const uint64_t* __restrict__ guide, int gs,
+                                          uint64_t m, double u) {
+  const uint64_t e = __ldg(guide + (m >> gs));
+  int j = (int)(e >> kGuideJ);
+  const int dl = (int)(e >> kGuideD) & 63;
+  if (dl == 0) return j;
+  if (dl < 63) {
+    const uint64_t thr = e & kGuideThr, ml = m & ((1ull << gs) - 1);
+    if (gs <= kGuideD) return (ml << (kGuideD - gs)) < thr ? j : j + dl;
+    const uint64_t x = ml >> (gs - kGuideD);
+    if (x != thr) return x < thr ? j : j + dl;
+    return u < __ldg(cdf + j) ? j : j + dl;        // tie on the truncated bits: compare exactly
   }
+  while (!(u < __ldg(cdf + j))) ++j;               // several boundaries: the definition, from j_lo
   return j;
 }
 
 struct SimParams {
   const int16_t* pol;    // [T][K][S]
   const double* cdf;     // Markov: [T-1][K][K]; rank-1: [T][K] (row t = cdf of pi_{t+1})
-  const int16_t* guide;  // same rows, G entries each
+  const uint64_t* guide; // same rows, 2^g entries each
   const double* cdf1;    // [K] cdf of pi_1
-  const int16_t* guide1; // [G]
+  const uint64_t* guide1; // [2^g]
+  const int* tab;        // Markov: table of stage t's transitions (deduplicated slices); NULL: t - 1
   const double* lambda;  // [T][K]
   const double* act; const double* w; const int* off; const double* g;
-  int T, K, S, A, G, rank1, kind, on_grid, f0;
+  int T, K, S, A, gs, gs1, rank1, kind, on_grid, f0;   // gs / gs1 = 53 - g: guide bucket shifts (rows / pi_1)
   int Kp;                // policy rows per stage (K, or world * kmax after a multi-GPU backward)
   double w0;
 };
+
+// sampling-table row of the transition out of state k at stage t (t < T): rank-1 rows are the marginals
+// pi_{t+1}; Markov rows the (deduplicated) slice of P_t
+__device__ __forceinline__ size_t sim_row(const SimParams& sp, int t, int k) {
+  return sp.rank1 ? (size_t)t : (size_t)(sp.tab ? __ldg(sp.tab + t - 1) : t - 1) * sp.K + k;
+}
 
 // One block of paths: blockIdx.x * blockDim.x + threadIdx.x (ssm: the per-action tables).
 __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, uint64_t seed, double* __restrict__ out,
@@ -1037,22 +1038,23 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
   const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (path >= n) return;
   double u1, u2;
-  sim_uniforms(seed, path, 0, u1, u2);
-  int k = cdf_sample(sp.cdf1, sp.guide1, sp.K, sp.G, u1);
+  uint64_t m1, m2;
+  sim_uniforms(seed, path, 0, u1, u2, m1, m2);
+  int k = cdf_sample(sp.cdf1, sp.guide1, sp.gs1, m1, u1);
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double profit = 0.0;
   const size_t KS = (size_t)sp.Kp * sp.S;
-  sim_uniforms(seed, path, 1, u1, u2);
+  sim_uniforms(seed, path, 1, u1, u2, m1, m2);
   for (int t = 1; t <= sp.T; ++t) {
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
     int kn = k;
     if (t < sp.T) {
-      const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * sp.K + k;
-      kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + row * sp.G, sp.K, sp.G, u2);
+      const size_t row = sim_row(sp, t, k);
+      kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + (row << (53 - sp.gs)), sp.gs, m2, u2);
     }
     // the next stage's draws do not depend on the state: computed while this stage's loads are in flight
     const double u1t = u1;
-    if (t < sp.T) sim_uniforms(seed, path, t + 1, u1, u2);
+    if (t < sp.T) sim_uniforms(seed, path, t + 1, u1, u2, m1, m2);
     double p;
     if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
     else {
@@ -1079,15 +1081,16 @@ __global__ void __launch_bounds__(128) price_path_kernel(SimParams sp, int64_t n
   const int64_t path = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (path >= n) return;
   double u1, u2;
-  sim_uniforms(seed, path, 0, u1, u2);
-  int k = cdf_sample(sp.cdf1, sp.guide1, sp.K, sp.G, u1);
+  uint64_t m1, m2;
+  sim_uniforms(seed, path, 0, u1, u2, m1, m2);
+  int k = cdf_sample(sp.cdf1, sp.guide1, sp.gs1, m1, u1);
   for (int t = 1; t <= sp.T; ++t) {
     if (kp) kp[(size_t)(t - 1) * n + path] = (int16_t)k;
     if (lamp) lamp[(size_t)(t - 1) * n + path] = __ldg(sp.lambda + (size_t)(t - 1) * sp.K + k);
     if (t < sp.T) {
-      sim_uniforms(seed, path, t, u1, u2);
-      const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * sp.K + k;
-      k = cdf_sample(sp.cdf + row * sp.K, sp.guide + row * sp.G, sp.K, sp.G, u2);
+      sim_uniforms(seed, path, t, u1, u2, m1, m2);
+      const size_t row = sim_row(sp, t, k);
+      k = cdf_sample(sp.cdf + row * sp.K, sp.guide + (row << (53 - sp.gs)), sp.gs, m2, u2);
     }
   }
 }

@@ -57,8 +57,9 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
     return p;
   };
   double u1, u2;
-  sim_uniforms(seed, path, 0, u1, u2);
-  int k = cdf_sample(sp.cdf1, sp.guide1, K, sp.G, u1);
+  uint64_t m1, m2;
+  sim_uniforms(seed, path, 0, u1, u2, m1, m2);
+  int k = cdf_sample(sp.cdf1, sp.guide1, sp.gs1, m1, u1);
   int i = sp.on_grid ? sp.f0 : sp.f0 + (u2 < sp.w0 ? 1 : 0);
   double s = mp.s0;                                    // physical mode: the real SoC, from s0 itself
   double profit = 0.0;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
   const double sbar_idx = (double)(S - 1);
   const double tol = 1e-9;
   for (int t = 1; t <= T; ++t) {
-    sim_uniforms(seed, path, t, u1, u2);
+    sim_uniforms(seed, path, t, u1, u2, m1, m2);
     const int wrow = sp.rank1 ? 0 : (mp.mode == 3 ? k_prev : k);   // self: persistence forecast of k_t
     const double* Wrow = mp.W + ((size_t)(t - 1) * mp.wrows + wrow) * mp.ld;
     const double lam = __ldg(sp.lambda + (size_t)(t - 1) * K + k);
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(kSimModeThreads) simulate_mode_kernel(SimModeP
       i = i + (s_ow[a_sel] >> 1) + ((wa > 0.0 && u1 < wa) ? 1 : 0);
     }
     if (t < T) {
-      const size_t row = sp.rank1 ? (size_t)t : (size_t)(t - 1) * K + k;
-      k = cdf_sample(sp.cdf + row * K, sp.guide + row * sp.G, K, sp.G, u2);
+      const size_t row = sim_row(sp, t, k);
+      k = cdf_sample(sp.cdf + row * K, sp.guide + (row << (53 - sp.gs)), sp.gs, m2, u2);
     }
   }
   out[path] = profit;

@@ -668,8 +668,14 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 #endif
 using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #define D3_KERNEL contract_dmma3_kernel<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>
-using D3s = Dmma3<1, 2, 2, 16, 4>;
-#define D3S_KERNEL contract_dmma3_kernel<1, 2, 2, 16, 4>
+#ifndef ESDP_D3S_KC
+#define ESDP_D3S_KC 16
+#endif
+#ifndef ESDP_D3S_NS
+#define ESDP_D3S_NS 4
+#endif
+using D3s = Dmma3<1, 2, 2, ESDP_D3S_KC, ESDP_D3S_NS>;
+#define D3S_KERNEL contract_dmma3_kernel<1, 2, 2, ESDP_D3S_KC, ESDP_D3S_NS>
 constexpr double kDmma3MinOutputs = 3.0e5;
 // 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large tiling
 int use_dmma3(int rows, int64_t ncols, int K) {

@@ -21,6 +21,15 @@ __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  //
 // Programmatic dependent launch (PDL): a kernel lets its successor be scheduled at once, and waits for
 // its predecessor's results only where it first reads them.  Both are no-ops without a PDL launch.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// ESDP_PDL_EARLY (measurement build): the stage kernels trigger their dependents right after their own
+// dependency wait instead of after their stores (the dependent's wait still covers this grid's completion)
+#ifdef ESDP_PDL_EARLY
+__device__ __forceinline__ void pdl_trigger_early() { pdl_trigger(); }
+__device__ __forceinline__ void pdl_trigger_late() {}
+#else
+__device__ __forceinline__ void pdl_trigger_early() {}
+__device__ __forceinline__ void pdl_trigger_late() { pdl_trigger(); }
+#endif
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #ifdef ESDP_WIN_TRACE
@@ -423,10 +432,14 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   auto As = [&](int b) { return d3sm + (size_t)b * D::STAGE; };
   auto Bs = [&](int b) { return d3sm + (size_t)b * D::STAGE + D::RB * D::SA; };
   // prologue: P chunks of the first NS-1 stages before the wait, V chunks after it; one group per stage
+  ktrace(1, 0);
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s)
     if (s < nch) issue_a(s);
+  ktrace(1, 1);
   pdl_wait();
+  ktrace(1, 2);
+  pdl_trigger_early();
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) {
     if (s < nch) issue_b(s);
@@ -441,6 +454,7 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   for (int ch = 0; ch < nch; ++ch) {
     cp_async_wait_group<NS - 2>();   // chunk ch has landed (this thread's copies) ...
     __syncthreads();                 // ... everyone's; and chunk ch-1's buffer is no longer read
+    if (ch == 0) ktrace(1, 3);
     if (ch + NS - 1 < nch) { issue_a(ch + NS - 1); issue_b(ch + NS - 1); }
     cp_async_commit();
     const double* as = As(ch % NS) + g * D::SA + kq;
@@ -462,6 +476,7 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
     }
   }
   cp_async_wait_group<0>();
+  ktrace(1, 4);
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     const int r = r0 + m * 8 + g;
@@ -474,7 +489,8 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
       else if (c < S) wr[c] = acc[m][n][0];
     }
   }
-  pdl_trigger();
+  ktrace(1, 5);
+  pdl_trigger_late();
 }
 
 // Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.

@@ -261,7 +261,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   // inputs first (lambda_t and the g fit do not depend on the previous kernel)
   const double lam = st.lambda_t[k];
   const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
-  if (kWait) pdl_wait();
+  if (kWait) { pdl_wait(); pdl_trigger_early(); }
   wtrace(1);
   // W_t over the tile: all of this thread's loads are issued before anything waits on them
   constexpr int kWReg = 3;
@@ -469,7 +469,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, d
 __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
   window_item<true>(p, blockIdx.y, blockIdx.x * kWinTile, wsm);   // waits for W_t (the contraction) inside
-  pdl_trigger();
+  pdl_trigger_late();
 }
 
 }  // namespace esdp

@@ -2,7 +2,8 @@
 `make -B EXTRA=-DESDP_WIN_TRACE`).  Marks are thread 0's %globaltimer (256 ns granularity on B200).
 window:      0 start, 1 after the dependency wait, 2 W staged, 3 level-0 keys, 4 levels built,
              5 queries + singles, 6 stored
-expectation: 0 start, 1 P staging issued, 2 after the dependency wait, 3 V staged, 4 DMMA chain, 5 stored"""
+expectation (dmma3): 0 start, 1 P chunks issued, 2 after the dependency wait, 3 first chunk landed,
+             4 DMMA chain done, 5 stored"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -38,6 +39,6 @@ def report(name, bb, nb, names):
 
 tw, bw = report("window", buf[0], 400, ["prologue+wait", "stage W", "level0+M", "levels", "queries+singles",
                                          "near-tie+store"])
-tc, bc = report("expectation", buf[1], 273, ["P issue", "wait", "V staged", "DMMA chain", "store"])
+tc, bc = report("expectation", buf[1], 416, ["P issue", "wait", "chunk 0 landed", "DMMA chain", "store"])
 print("expectation first start -> window first start: %.2f us; expectation last end -> window last wait done: %.2f us"
       % ((tw - tc) / 1e3, (bw[:, 1].max() - bc[:, 5].max()) / 1e3))

@@ -374,12 +374,12 @@ def run_ours(args):
     plan = E.esdp_stencil_kind(solver.ctx)
     # DRAM traffic per backward from the committed ncu capture of this workload (cfg2, graph plan)
     traffic, traffic_note = None, None
-    tr_path = os.path.join(ROOT, "profiles", "r01k_backward_traffic.json")
+    tr_path = os.path.join(ROOT, "profiles", "r01m_backward_traffic.json")
     if args.config == "cfg2" and not kpart and not (plan & 2) and os.path.exists(tr_path):
         with open(tr_path) as f:
             traffic = json.load(f)["per_backward_bytes"]
         traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum summed over one backward's kernels "
-                        "(profiles/r01k_backward_traffic.json, ncu --cache-control none); algorithmic bytes "
+                        "(profiles/r01m_backward_traffic.json, ncu --cache-control none); algorithmic bytes "
                         "%.4g" % hbm_bytes)
     out = None
     if rank == 0:

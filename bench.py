@@ -31,6 +31,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+DMMA_PEAK_TFLOPS = 37.03  # FP64 tensor cores (mma.m8n8k4.f64), measured: profiles/r01_microbench.json
 FP64_LANES_PER_SM = 64  # B200: 64 FP64 FMA lanes per SM (measured 62.8 DADD/SM/clk)
 
 
@@ -381,6 +382,26 @@ def run_ours(args):
         traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum summed over one backward's kernels "
                         "(profiles/r01m_backward_traffic.json, ncu --cache-control none); algorithmic bytes "
                         "%.4g" % hbm_bytes)
+    # the two stage kernels on their own (after the timed region): warm back-to-back launches of stage T-1's
+    # kernel, CUDA events on the context's stream, each launch including its kernel boundary (no PDL)
+    kernels = None
+    if rank == 0 and not kpart and not (plan & 2) and T > 1:
+        us_st = E.esdp_debug_time(solver.ctx, 1, 200)
+        st_work = 2.0 * S * K * A
+        kernels = {"stencil": {"kernel": "window_stencil_kernel" if plan & 1 else "stencil_kernel", "bound": "alu",
+                               "us_per_launch": us_st, "work_per_launch": st_work,
+                               "achieved": st_work / us_st / 1e3, "peak": fp64_peak, "unit": "G FP64 instr/s",
+                               "frac": st_work / us_st / 1e3 / fp64_peak,
+                               "note": "brute-force-equivalent FP64 instructions (2 per cell, SURVEY 8(d).3)"}}
+        if inst.P is not None:
+            us_ct = E.esdp_debug_time(solver.ctx, 0, 200)
+            ct_flop = 2.0 * K * K * S
+            kernels["expectation"] = {"kernel": "contract_dmma3_kernel" if K % 2 == 0 else "contract_dmma2_kernel",
+                                      "bound": "tensor", "us_per_launch": us_ct, "work_per_launch": ct_flop,
+                                      "achieved": ct_flop / us_ct / 1e6, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                      "frac": ct_flop / us_ct / 1e6 / DMMA_PEAK_TFLOPS,
+                                      "note": "FP64 DMMA; peak measured by tools/microbench/mb.cu "
+                                              "(profiles/r01_microbench.json)"}
     out = None
     if rank == 0:
         out = {
@@ -422,6 +443,7 @@ def run_ours(args):
                                       f"(sm_max_mhz from MEASURED_PEAKS.json: {peak_kind})",
                          "work_per_launch": f"algorithmic FP64 instr: 2 per cell x T*S*K*A + K per (k,s) x (T-1)*S*K "
                                             f"= {algo_ops:.4g}"},
+            "roofline_kernels": kernels,
             "roofline_hbm_literal": {"bound": "hbm", "achieved": hbm_ach, "peak": float(peaks["hbm_gbs"]),
                                      "unit": "GB/s", "frac": hbm_ach / float(peaks["hbm_gbs"]),
                                      "bytes_per_launch": hbm_bytes},

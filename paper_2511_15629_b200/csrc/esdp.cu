@@ -4,6 +4,8 @@
 // (Alg. 1 lines 2-5) are computed here on the host once per context, in binary64 with
 // FMA contraction disabled (-Xcompiler -ffp-contract=off).  Everything per stage runs in the
 // kernels of kernels.cuh; the whole backward pass is one CUDA graph (2T+1 launches).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -142,6 +144,9 @@ struct esdp_ctx {
   int prof_stride = 1;
   bool pdl = true;
   int dmma2 = 0;   // shared-memory-staged DMMA expectation (set when its tile fits)
+  // TMA-multicast cluster expectation (contract_mc_kernel): tensor maps of P per input slot and of V
+  int mc = 0, mc_nrb = 0, mc_c = 0;   // plan on, row tiles (padded), cluster size
+  CUtensorMap mapP[2], mapV;
   bool solved = false;
   std::string err;
 };
@@ -701,6 +706,93 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
 }
 
+// contract_mc_kernel plan (opt-in, ESDP_MC=1 in the environment; ESDP_MC_C=c sets the cluster size, the row
+// tiles padded to a multiple of it): Markov contexts with even K <= 128.  Tensor maps from
+// cuTensorMapEncodeTiled (driver entry point).  Bit-identical, but measured slower than dmma3 on cfg2
+// (warm launch 4.4-5.2 us for cluster sizes 1-13 against 3.26 us), hence off by default.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }();
+  return fn;
+}
+bool encode_map3(CUtensorMap* m, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * sizeof(double), d0 * d1 * sizeof(double)};
+  const cuuint32_t box[3] = {b0, b1, 1}, es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+void setup_mc(esdp_ctx* c) {
+  c->mc = 0;
+  const char* e = getenv("ESDP_MC");
+  if (!e || atoi(e) == 0 || c->rank1 || (c->K & 1) || c->K > kMcKC * kMcMaxCh || c->T < 2 || c->k_cnt < 8 ||
+      (c->flags & (ESDP_NO_DMMA | ESDP_DMMA_L2)))
+    return;
+  const int nrb0 = (c->k_cnt + kMcRB - 1) / kMcRB;
+  const char* ec = getenv("ESDP_MC_C");
+  const int csz = std::min(nrb0, ec ? std::max(1, atoi(ec)) : nrb0);   // cluster size (row tiles sharing a V tile)
+  const int nrb = (nrb0 + csz - 1) / csz * csz;                         // padded: idle CTAs only receive
+  if (csz > 16) return;
+  const int K = c->K, Kp = (K + 3) & ~3;
+  const uint64_t nbuf = keep(c) ? (uint64_t)c->T : 2;
+  for (int j = 0; j < 2; ++j)
+    if (!encode_map3(&c->mapP[j], c->slot[j].P, (uint64_t)K, (uint64_t)K, (uint64_t)(c->T - 1), (uint32_t)mc_stride_a(Kp),
+                     kMcRB))
+      return;
+  if (!encode_map3(&c->mapV, c->d_V, (uint64_t)c->ld, (uint64_t)c->Kp, nbuf, kMcSB, kMcKC)) return;
+  const size_t sm = mc_smem_bytes(K);
+  if (cudaFuncSetAttribute(contract_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+      (csz > 8 && cudaFuncSetAttribute(contract_mc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+    cudaGetLastError();
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nrb * ((c->S + kMcCB - 1) / kMcCB)));
+  cfg.blockDim = dim3(kMcThreads);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csz; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, contract_mc_kernel, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    return;
+  }
+  c->mc = 1;
+  c->mc_nrb = nrb;
+  c->mc_c = csz;
+}
+cudaError_t launch_contract_mc(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
+  const int sl = c->d_P == c->slot[1].P ? 1 : 0;
+  const int nrb = c->mc_nrb;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nrb * ((c->S + kMcCB - 1) / kMcCB)));
+  cfg.blockDim = dim3(kMcThreads);
+  cfg.dynamicSmemBytes = mc_smem_bytes(c->K);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)c->mc_c; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  const int vt = keep(c) ? t : (t & 1);   // V_{t+1}: buffer t (keep) or (t+1-1) & 1
+  return cudaLaunchKernelEx(&cfg, contract_mc_kernel, c->mapP[sl], c->mapV, W_of(c, t), c->k_cnt, c->K, c->S, c->ld, nrb,
+                            c->mc_c, t - 1, c->k_lo, vt);
+}
+
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
 cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int K = c->K, S = c->S;
@@ -708,6 +800,7 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   if (rows == 0) return cudaSuccess;
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
+    if (c->mc) return launch_contract_mc(c, t, s, pdl);
     if (const int d3 = (c->flags & ESDP_DMMA_L2) ? 0 : use_dmma3(rows, S, K))
       return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl);
     if (c->dmma2) {
@@ -1314,6 +1407,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   c->fb_ev.resize((size_t)c->T + 1);
   for (auto& ev : c->fb_ev)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { fail(c, ESDP_E_CUDA, "event"); return bail(ESDP_E_CUDA); }
+  if (!c->persist) setup_mc(c);
   TRY(capture_graph(c));
 #undef TRY
   *out = c;

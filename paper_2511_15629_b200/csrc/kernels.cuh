@@ -5,6 +5,7 @@
 // reassociates: results are reproducible bit for bit (R14/R15).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace esdp {
@@ -490,6 +491,119 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
     }
   }
   ktrace(1, 5);
+  pdl_trigger_late();
+}
+
+// ------------------------------------------------------------------------------------------------
+// Latency-regime expectation with TMA multicast (cfg2 shape: K <= 128, even): a thread-block cluster
+// holds the C = ceil(rows / 8) row tiles of one 32-column tile of W.  Every CTA needs the same V block
+// V_{t+1}[0..K)[i0 .. i0+32); instead of C copies from L2 (13 on cfg2: 13 MB of L2 reads per stage), each
+// k' chunk of it is fetched ONCE by a 3-D TMA box [t][KC rows][40 columns] and multicast into all C CTAs'
+// shared memory (cp.async.bulk.tensor ... .multicast::cluster); the chunk issuers are spread over the
+// cluster (chunk c by CTA c mod C).  The 40-column box (8 beyond the tile, zero past the tensor) lays the
+// rows out at a stride of 8 mod 16 doubles, conflict-free for the DMMA B fragments (as dmma3's padding).
+// The CTA's own P rows come by one non-multicast box [t][8 rows][SA columns] (zero past K).  Each chunk has
+// its own mbarrier, so the DMMA chain starts on chunk 0 while the others land.  The cluster barrier that
+// publishes the mbarrier inits (before any multicast may signal them) is split around the dependency wait.
+// Accumulation order per output: ascending k' quads, one DMMA after the other: the canonical chain (R15).
+// ------------------------------------------------------------------------------------------------
+constexpr int kMcKC = 16, kMcMaxCh = 8, kMcCB = 32, kMcSB = 40, kMcRB = 8, kMcThreads = 64;
+__host__ __device__ constexpr int mc_stride_a(int Kp) { return (Kp % 16 == 0 || Kp % 16 == 8) ? Kp + 4 : Kp; }
+__host__ __device__ constexpr int mc_b_offset(int Kp) { return ((kMcRB * mc_stride_a(Kp)) + 15) & ~15; }   // doubles, 128 B
+inline size_t mc_smem_bytes(int K) {
+  const int Kp = (K + 3) & ~3;
+  return sizeof(double) * ((size_t)mc_b_offset(Kp) + (size_t)kMcMaxCh * kMcKC * kMcSB) + sizeof(uint64_t) * (1 + kMcMaxCh);
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* b) {   // phase 0 of a single-use barrier
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load3_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                             unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+// mapP: 3-D [T-1][K][K] (box [1][8][SA]); mapV: 3-D [nbuf][Kp][ld] (box [1][KC][40]).  pt / prow0: the
+// stage index and first own row of P_t; vt: the V_{t+1} buffer.  Grid: (K-row tiles) x (column tiles),
+// row tiles fastest, cluster = all row tiles of a column tile.
+__global__ void __launch_bounds__(kMcThreads) contract_mc_kernel(const __grid_constant__ CUtensorMap mapP,
+                                                                 const __grid_constant__ CUtensorMap mapV,
+                                                                 double* __restrict__ Wt, int rows, int K, int S, int ld,
+                                                                 int nrb, int csz, int pt, int prow0, int vt) {
+  extern __shared__ __align__(128) double msm[];
+  const int tid = threadIdx.x;
+  const int Kp = (K + 3) & ~3, SA = mc_stride_a(Kp);
+  double* as = msm;
+  double* bs = msm + mc_b_offset(Kp);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bs + kMcMaxCh * kMcKC * kMcSB);   // [0] A, [1 + c] chunk c
+  const int rb = blockIdx.x % nrb, cbk = blockIdx.x / nrb;
+  const int r0 = rb * kMcRB, i0 = cbk * kMcCB;
+  const int nch = (K + kMcKC - 1) / kMcKC;
+  unsigned crank;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  if (tid == 0) {
+    for (int j = 0; j <= nch; ++j) mbar_init(bar + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, (unsigned)(kMcRB * SA * sizeof(double)));
+    for (int c = 0; c < nch; ++c) mbar_expect_tx(bar + 1 + c, (unsigned)(kMcKC * kMcSB * sizeof(double)));
+    tma_load3(as, &mapP, 0, prow0 + r0, pt, bar);          // P_t rows (an input: before the dependency wait)
+  }
+  __syncthreads();
+  cluster_arrive();                                        // this CTA's barriers are initialized and armed
+  pdl_wait();
+  cluster_wait();                                          // ... and every other CTA's
+  if (tid == 0)
+    for (int c = (int)crank; c < nch; c += csz)
+      tma_load3_mc(bs + c * kMcKC * kMcSB, &mapV, i0, c * kMcKC, vt, bar + 1 + c, (unsigned short)((1u << csz) - 1));
+  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
+  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+  const double* arow = as + g * SA + kq;
+  const double* bcol = bs + kq * kMcSB + warp * 16 + g;
+  mbar_wait0(bar);
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait0(bar + 1 + c);
+    const int nq = min(kMcKC, Kp - c * kMcKC) >> 2;
+#pragma unroll
+    for (int q = 0; q < kMcKC / 4; ++q) {
+      if (q < nq) {
+        const int k4 = c * kMcKC + 4 * q;
+        const double a = arow[k4];
+        const double b0 = bcol[k4 * kMcSB], b1 = bcol[k4 * kMcSB + 8];
+        dmma_8x8x4(d00, d01, a, b0);
+        dmma_8x8x4(d10, d11, a, b1);
+      }
+    }
+  }
+  cluster_arrive();                                        // no CTA leaves while a multicast may target it
+  const int r = r0 + g;
+  if (r < rows) {
+    const int c = i0 + warp * 16 + 2 * kq;
+    double* wr = Wt + (size_t)r * ld;
+    if (c + 1 < S) *reinterpret_cast<double2*>(wr + c) = make_double2(d00, d01);
+    else if (c < S) wr[c] = d00;
+    if (c + 9 < S) *reinterpret_cast<double2*>(wr + c + 8) = make_double2(d10, d11);
+    else if (c + 8 < S) wr[c + 8] = d10;
+  }
+  cluster_wait();
   pdl_trigger_late();
 }
 

@@ -294,6 +294,17 @@ def test_cfg3_window_affine_degradation(rank1):
     _compare_all(inst, nthreads=16, brute=True)
 
 
+@pytest.mark.parametrize("csize", ["", "4", "1"])
+def test_expectation_tma_multicast_opt_in(csize, monkeypatch):
+    """The opt-in TMA-multicast cluster expectation (ESDP_MC=1; ESDP_MC_C pads the row tiles to clusters of
+    that size, idle CTAs only receive) gives the canonical chain's bits: every W_t, V_t, pol_t and J."""
+    monkeypatch.setenv("ESDP_MC", "1")
+    if csize:
+        monkeypatch.setenv("ESDP_MC_C", csize)
+    _compare_all(workloads.cfg2(T=5, K=36), nthreads=16)
+    _compare_all(workloads.cfg1("b"))
+
+
 @pytest.mark.parametrize("which", ["cfg2", "cfg3"])
 def test_window_unimodal_and_level_tables(which):
     """The window stencil answers a unimodal run table from its peak and builds sparse-table levels only

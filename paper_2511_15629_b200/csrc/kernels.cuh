@@ -1175,11 +1175,16 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
   double profit = 0.0;
   const size_t KS = (size_t)sp.Kp * sp.S;
   sim_uniforms(seed, path, 1, u1, u2, m1, m2);
+  // stage t's table row base (sim_row(t, 0)) is loaded one stage ahead: the map load stays off the
+  // draw's dependent chain
+  size_t rb_next = sp.T > 1 ? sim_row(sp, 1, 0) : 0;
   for (int t = 1; t <= sp.T; ++t) {
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
+    const size_t rb = rb_next;
+    if (t + 1 < sp.T) rb_next = sim_row(sp, t + 1, 0);
     int kn = k;
     if (t < sp.T) {
-      const size_t row = sim_row(sp, t, k);
+      const size_t row = sp.rank1 ? rb : rb + k;
       kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + (row << (53 - sp.gs)), sp.gs, m2, u2);
     }
     // the next stage's draws do not depend on the state: computed while this stage's loads are in flight

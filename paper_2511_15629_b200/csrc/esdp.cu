@@ -799,6 +799,10 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int rows = c->rank1 ? 1 : c->k_cnt;   // own rows of W_t (all rows on one GPU)
   if (rows == 0) return cudaSuccess;
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
+  // rank-1 (the paper's Alg. 1 GEMV W = pi_{t+1}^T V_{t+1}): one A row of the 8-row DMMA tile is live; the
+  // K/4-long DMMA chain per column replaces a K-long DFMA chain (same canonical order, same bits)
+  if (rows == 1 && !(K & 1) && !(c->flags & (ESDP_NO_DMMA | ESDP_DMMA_L2)) && use_dmma3(8, S, K))
+    return launch_dmma3(1, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl);
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
     if (c->mc) return launch_contract_mc(c, t, s, pdl);
     if (const int d3 = (c->flags & ESDP_DMMA_L2) ? 0 : use_dmma3(rows, S, K))

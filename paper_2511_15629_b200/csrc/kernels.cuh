@@ -895,16 +895,36 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
   // in L2), so that 0.5 GB of cfg2 curves do not push the policy table out before the simulation
   if (kSmem) __stcs(vo, (short)a_prev);
   if (qo) __stcs(qo, p_prev);
-#if BID_PF_EMIT
+#ifndef BID_EMIT2
+#define BID_EMIT2 1
+#endif
+#if BID_EMIT2
+  // two segments per step: their divisions are independent (the repair is a running max after them)
+  int j2 = 1;
+  for (; j2 + 1 < nh; j2 += 2) {
+    const int a1 = st_get(j2), a2 = st_get(j2 + 1);
+    const double u1 = u_of(a1), p1 = tb.act[a1], u2 = u_of(a2), p2 = tb.act[a2];
+    double r1 = -__ddiv_rn(__dsub_rn(u1, u_prev), __dsub_rn(p1, p_prev));
+    double r2 = -__ddiv_rn(__dsub_rn(u2, u1), __dsub_rn(p2, p1));
+    if (j2 > 1 && r1 < prev_price) r1 = prev_price;
+    if (r2 < r1) r2 = r1;
+    __stcs(pro + (size_t)(j2 - 1) * nout, r1);
+    __stcs(pro + (size_t)j2 * nout, r2);
+    if (kSmem) { __stcs(vo + (size_t)j2 * nout, (short)a1); __stcs(vo + (size_t)(j2 + 1) * nout, (short)a2); }
+    if (qo) { __stcs(qo + (size_t)j2 * nout, p1); __stcs(qo + (size_t)(j2 + 1) * nout, p2); }
+    prev_price = r2; u_prev = u2; p_prev = p2;
+  }
+  for (int j = j2; j < nh; ++j) {
+    const int a = st_get(j);
+    const double u = u_of(a), pc = tb.act[a];
+#elif BID_PF_EMIT
   int a_n = nh > 1 ? st_get(1) : 0;
   double u_n = nh > 1 ? u_of(a_n) : 0.0, p_n = nh > 1 ? tb.act[a_n] : 0.0;
-#endif
-  for (int j = 1; j < nh; ++j) {
-#if BID_PF_EMIT
     const int a = a_n;
     const double u = u_n, pc = p_n;
     if (j + 1 < nh) { a_n = st_get(j + 1); u_n = u_of(a_n); p_n = tb.act[a_n]; }
 #else
+  for (int j = 1; j < nh; ++j) {
     const int a = st_get(j);
     const double u = u_of(a), pc = tb.act[a];
 #endif

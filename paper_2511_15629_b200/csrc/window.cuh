@@ -205,7 +205,7 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
 }
 
 // Unimodal tables (the common case: W_t(., k) concave in the SoC, as for every linear-payoff workload
-// measured -- tools/unimodal.py finds 100 % of cfg2 / cfg4 / cfg5 tiles unimodal, cfg3's fixed cost
+// measured -- tests/diag/unimodal.py finds 100 % of cfg2 / cfg4 / cfg5 tiles unimodal, cfg3's fixed cost
 // 52 % / 73 % per side).  With ck(key) = 0 for -inf keys, a table is unimodal when every rising pair
 // (x, x+1) precedes every falling pair; its maximum then sits at p* = 1 + the last rising x (0 if none),
 // the maximum of any window [l, r] at clamp(p*, l, r) and the runner-up next to it.  Packed keys are

@@ -1,6 +1,6 @@
 """Exact concavity of the oracle's W over the window stencil's tile columns (diagnostic, CPU): math.fsum sign of W[j-1] + W[j+1] - 2 W[j]."""
 import sys, math, numpy as np
-import os; R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, 'tests'))
+import os; R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, 'tests'))
 import oracle, workloads
 from helpers import to_oracle
 for name, inst in [("cfg2", workloads.cfg2(T=24)), ("t3", workloads.table3(hours=100.0, delta=0.01, T=6))]:

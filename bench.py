@@ -392,7 +392,12 @@ def run_ours(args):
                                "us_per_launch": us_st, "work_per_launch": st_work,
                                "achieved": st_work / us_st / 1e3, "peak": fp64_peak, "unit": "G FP64 instr/s",
                                "frac": st_work / us_st / 1e3 / fp64_peak,
-                               "note": "brute-force-equivalent FP64 instructions (2 per cell, SURVEY 8(d).3)"}}
+                               "note": "brute-force-equivalent FP64 instructions (2 per cell, SURVEY 8(d).3)",
+                               "hbm": {"bytes_per_launch": 18.0 * S * K, "achieved": 18.0 * S * K / us_st / 1e3,
+                                       "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                                       "frac": 18.0 * S * K / us_st / 1e3 / float(peaks["hbm_gbs"]),
+                                       "note": "read W_t, write V_t and the int16 policy per (k, s); W_t and V_t are "
+                                               "L2-resident on cfg2, so DRAM sees little of it"}}}
         if inst.P is not None:
             us_ct = E.esdp_debug_time(solver.ctx, 0, 200)
             ct_flop = 2.0 * K * K * S

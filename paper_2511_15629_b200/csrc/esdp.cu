@@ -298,13 +298,38 @@ void dedupe_slices(const double* P, int nst, int K, std::vector<int>& tab, std::
   std::vector<uint64_t> h((size_t)nst);
   std::function<void(int)> hash = [&](int t) {
     const uint64_t* w = reinterpret_cast<const uint64_t*>(P + (size_t)t * n);
-    uint64_t x = 0xcbf29ce484222325ull;
-    for (size_t j = 0; j < n; ++j) x = (x ^ w[j]) * 0x100000001b3ull;
-    h[(size_t)t] = x;
+    uint64_t x[4] = {0xcbf29ce484222325ull, 0x84222325cbf29ce4ull, 0x9e3779b97f4a7c15ull, 0xbf58476d1ce4e5b9ull};
+    size_t j = 0;
+    for (; j + 4 <= n; j += 4)   // four independent FNV-1a lanes
+      for (int l = 0; l < 4; ++l) x[l] = (x[l] ^ w[j + l]) * 0x100000001b3ull;
+    for (; j < n; ++j) x[0] = (x[0] ^ w[j]) * 0x100000001b3ull;
+    h[(size_t)t] = ((x[0] * 31 + x[1]) * 31 + x[2]) * 31 + x[3];
   };
   if (nst > 1 && (size_t)nst * n > (1u << 16)) HostPool::get().run(nst, hash);
   else for (int t = 0; t < nst; ++t) hash(t);
   tab.assign((size_t)nst, 0);
+  src.clear();
+  // tentative tables by hash alone, then every slice compared with its representative in parallel; a hash
+  // collision (any mismatch) redoes the assignment with byte comparisons
+  {
+    std::unordered_map<uint64_t, int> first;
+    for (int t = 0; t < nst; ++t) {
+      auto it = first.find(h[(size_t)t]);
+      if (it == first.end()) {
+        it = first.emplace(h[(size_t)t], (int)src.size()).first;
+        src.push_back(t);
+      }
+      tab[(size_t)t] = it->second;
+    }
+    std::vector<char> bad((size_t)nst, 0);
+    std::function<void(int)> check = [&](int t) {
+      const int r = src[(size_t)tab[(size_t)t]];
+      if (r != t) bad[(size_t)t] = std::memcmp(P + (size_t)r * n, P + (size_t)t * n, n * sizeof(double)) != 0;
+    };
+    if (nst > 1 && (size_t)nst * n > (1u << 16)) HostPool::get().run(nst, check);
+    else for (int t = 0; t < nst; ++t) check(t);
+    if (std::find(bad.begin(), bad.end(), 1) == bad.end()) return;
+  }
   src.clear();
   std::unordered_map<uint64_t, std::vector<int>> seen;
   for (int t = 0; t < nst; ++t) {

@@ -397,14 +397,20 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     // singles, branch-free: b2 takes the smaller of (b1, c), b1 the larger; once a single leads, b1 is its
     // exact canonical value (a later single replaces it only by a larger canonical value)
     bool single_best = false;
-#pragma unroll 4
-    for (int s = 0; s < nsg; ++s) {
-      const double c = canon_staged(ss[s], wt, wbase, i);
+    auto single_step = [&](const SingleAct& sa) {
+      const double c = canon_staged(sa, wt, wbase, i);
       const bool gt = c > b1;
       b2 = fmax(b2, gt ? b1 : c);
       b1 = gt ? c : b1;
-      a1 = gt ? ss[s].a : a1;
+      a1 = gt ? sa.a : a1;
       single_best |= gt;
+    };
+    if (p.nsingle == 3) {                   // the Eq. 10 grid: zero action and the two endpoints
+#pragma unroll
+      for (int s = 0; s < 3; ++s) single_step(ss[s]);
+    } else {
+#pragma unroll 4
+      for (int s = 0; s < nsg; ++s) single_step(ss[s]);
     }
     for (int s = nsg; s < p.nsingle; ++s) {
       const int a = __ldg(p.singles + s);

@@ -312,7 +312,10 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores); the pairs
   // (x, x+1) and (x+1, x+2) feed the unimodality test (key x+2 recomputed here: no extra barrier)
   unsigned upc = 0u, dnc = kNoFall, upd = 0u, dnd = kNoFall;
-  for (int x = 2 * tid; x < tc.n; x += 2 * kWinThreads) {
+#pragma unroll
+  for (int u = 0; u < kLevelSlots; ++u) {   // n <= 768 (as the level builds)
+    const int x = 2 * (tid + u * kWinThreads);
+    if (x >= tc.n) break;
     const int j = i0 + 1 + x;
     ulonglong2 r;
     r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
@@ -322,7 +325,10 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     if (x + 2 < tc.n)
       uni_pair(r.y, pack_key(__dsub_rn(wt[j + 2 - wbase], __dmul_rn(beta_c, (double)(j + 2))), x + 2), x + 2, upc, dnc);
   }
-  for (int x = 2 * tid; x < td.n; x += 2 * kWinThreads) {
+#pragma unroll
+  for (int u = 0; u < kLevelSlots; ++u) {
+    const int x = 2 * (tid + u * kWinThreads);
+    if (x >= td.n) break;
     const int j = i0 - p.Ld + x;
     ulonglong2 r;
     r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);

@@ -704,8 +704,14 @@ using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #ifndef ESDP_D3S_NS
 #define ESDP_D3S_NS 4
 #endif
-using D3s = Dmma3<1, 2, 2, ESDP_D3S_KC, ESDP_D3S_NS>;
-#define D3S_KERNEL contract_dmma3_kernel<1, 2, 2, ESDP_D3S_KC, ESDP_D3S_NS>
+#ifndef ESDP_D3S_NT
+#define ESDP_D3S_NT 2
+#endif
+#ifndef ESDP_D3S_WC
+#define ESDP_D3S_WC 2
+#endif
+using D3s = Dmma3<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>;
+#define D3S_KERNEL contract_dmma3_kernel<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>
 constexpr double kDmma3MinOutputs = 3.0e5;
 // 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large tiling
 int use_dmma3(int rows, int64_t ncols, int K) {

@@ -584,9 +584,10 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
     }
     CUDA_OR_FAIL(c, cudaEventRecord(d.chunk_ev[j], s));
   }
-  // The sampling tables of P are built lazily by the first simulation that needs them (ready_tables),
-  // on that simulation's stream: built here, their blocks would share the SMs with the running backward's
-  // latency-bound stage chain and stretch it (measured +0.3 ms per cfg2 solve).
+  // The sampling tables of P are built lazily by the first simulation that needs them (ready_tables), on
+  // that simulation's stream: built here, 287 distinct slices' blocks shared the SMs with the running
+  // backward's latency-bound stage chain and stretched it (measured +0.3 ms per cfg2 solve).  A few
+  // distinct slices (<= 4096 rows, a handful of blocks) are built right here instead.
   if (!c->rank1 && c->T > 1) {
     const int nst = c->T - 1;
     if (P) {   // one table per distinct slice P_t; as many guide bits as the allocation allows
@@ -597,6 +598,11 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, tab.data(), nst * sizeof(int), h2d, s));
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.src, src.data(), src.size() * sizeof(int), h2d, s));
       d.tables_stale = true;
+      if ((size_t)d.nuniq * K <= 4096) {   // few distinct slices: a handful of blocks, built right after P lands
+        launch_cdf(d.P, d.src, (int64_t)d.nuniq * c->K, c->K, d.gbits, d.cdf, d.guide, s);
+        CUDA_OR_FAIL(c, cudaGetLastError());
+        d.tables_stale = false;
+      }
     } else if (copy_old) {
       d.nuniq = o.nuniq;
       d.gbits = o.gbits;

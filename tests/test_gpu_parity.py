@@ -432,6 +432,37 @@ def test_simulation_per_path_bitexact(name):
     assert abs(m - J) <= 5 * math.sqrt(v / n) + 1e-9
 
 
+@pytest.mark.parametrize("K", [40, 5])
+def test_simulation_sampler_edge_tables(K):
+    """The one-load sampler (DESIGN.md §5 a7) against the definition on transition rows built to hit every
+    guide case: exact zeros (empty states the one-boundary step skips), clusters of 1e-12..1e-15
+    probabilities (several boundaries in one bucket: the scan), dominant entries (pure buckets), three
+    distinct slices repeated over the stages (table dedupe) and a pi_1 with zeros; per-path profits
+    bit-identical to the oracle."""
+    rng = np.random.default_rng(11 + K)
+    base = workloads.cfg2(T=12, K=K)
+
+    def row():
+        w = np.zeros(K)
+        sup = rng.choice(K, size=max(2, K // 2), replace=False)
+        w[sup] = rng.choice([1.0, 0.3, 1e-12, 3e-13, 1e-15], size=len(sup))
+        w[sup[0]] = 1.0
+        return w / w.sum()
+
+    slices = [np.stack([row() for _ in range(K)]) for _ in range(3)]
+    base.P = np.ascontiguousarray(np.stack([slices[t % 3] for t in range(base.T - 1)]))
+    pi = row()
+    base.pi = pi
+    pr = to_oracle(base)
+    ref = oracle.backward(pr, nthreads=8)
+    n = 4000
+    per_ref, _, _ = oracle.simulate(pr, ref.pol, n, seed=4242)
+    with _gpu(base) as s:
+        assert s.backward() == ref.J
+        per, _, _ = s.simulate(n, 4242)
+    assert np.array_equal(per, per_ref)
+
+
 def test_load_new_prices_and_repeat():
     """esdp_load replaces the stochastic inputs in place; repeated solves are bit-identical."""
     a = workloads.cfg1("b")

@@ -8,7 +8,7 @@ LDFLAGS   := -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib
 PKG       := paper_2511_15629_b200
 LIB       := $(PKG)/libesdp.so
 SRCS      := $(PKG)/csrc/esdp.cu
-HDRS      := $(PKG)/csrc/kernels.cuh $(PKG)/csrc/window.cuh $(PKG)/csrc/persistent.cuh include/esdp.h
+HDRS      := $(wildcard $(PKG)/csrc/*.cuh) include/esdp.h
 ORACLE    := oracle/liboracle.so
 
 all: $(LIB) $(ORACLE)

@@ -71,6 +71,12 @@ enum {
                              for cfg2 on B200) */
 };
 
+/* Environment variables read at context creation (measurement knobs; every setting gives the same bits):
+ *   ESDP_DMMA3=0      expectation on the all-at-once staged DMMA kernel instead of the k'-pipelined one
+ *   ESDP_MC=1         expectation by TMA multicast across a thread-block cluster (measured slower on cfg2)
+ *   ESDP_MC_C=c       cluster size for ESDP_MC (row tiles padded to a multiple of c)
+ * DESIGN.md §5 and §7 record what each measured. */
+
 typedef struct {
   int32_t T, K;          /* stages and Markov price states (north_star; the paper's R) */
   double pbar, sbar, s0; /* power cap, energy cap, initial SoC, energy-per-stage units */

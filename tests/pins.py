@@ -133,11 +133,20 @@ def expectimax_exact(inst, actions, i0=None, payoff=None):
             row = Pm[t - 1][k]
         return sum((row[kp] * Vk(t + 1, i, kp) for kp in range(K)), Fraction(0))
 
-    if i0 is None:
-        x = _frac(inst.s0) / delta
-        i0 = int(x)
     pi1 = pis[0] if Pm is None else pis
-    J = sum((pi1[k] * Vk(1, i0, k) for k in range(K)), Fraction(0))
+    if i0 is None:
+        # R24: an off-grid s0 is a start lottery between the two neighbouring grid
+        # states, floor(x) w.p. 1 - w and floor(x) + 1 w.p. w, w = x - floor(x) (exact rationals).
+        x = _frac(inst.s0) / delta
+        r = round(x)
+        if abs(x - r) <= Fraction(1, 10**9):
+            starts = [(int(r), Fraction(1))]
+        else:
+            f = math.floor(x)
+            starts = [(f, 1 - (x - f)), (f + 1, x - f)]
+    else:
+        starts = [(i0, Fraction(1))]
+    J = sum((pi1[k] * q * Vk(1, i, k) for k in range(K) for i, q in starts), Fraction(0))
     expectimax_exact.last = dict(EV=EV, moves=moves, pay=pay)
     return J, Vk
 

@@ -4,6 +4,7 @@ Each test checks the oracle against something other than itself: SPEC worked exa
 closed forms, exact-rational brute force, enumeration of all action sequences, the LP/MILP
 optimum of Eqs. 1/3 (scipy HiGHS), a literal transliteration of Algorithm 1, symmetries and
 invariants."""
+import dataclasses
 import math
 from fractions import Fraction
 
@@ -270,3 +271,33 @@ def test_table1_year_trend():
         gaps.append((lp - J) / lp)
     assert gaps[0] > gaps[1] > gaps[2] > gaps[3] > 0.0
     assert gaps[0] < 0.005 and gaps[3] < 0.001
+
+
+# --- R24: off-grid s0 (Eq. 6 at t = 0; interpolation rule S:252-255) ------------------
+
+@pytest.mark.parametrize("s0, J_closed", [(0.3, 3.0), (0.8, 8.0), (0.1, 1.0)])
+def test_objective_off_grid_s0_closed_form(s0, J_closed):
+    """T = 1, K = 1, eta = 1, lambda = 10, pbar = 1, delta = 0.5, sbar = 2: V_1 = [0, 5, 10, 10, 10]
+    (discharge min(s, pbar) at price 10).  Interpolating V_1 at s0 = 0.3 (x = 0.6) gives
+    0.4*0 + 0.6*5 = 3 = lambda*s0; s0 = 0.8 (x = 1.6) gives 0.4*5 + 0.6*10 = 8 = lambda*s0.  A
+    swapped weight (w vs 1 - w) gives 2 and 7 instead."""
+    pr = simple_problem(1.0, 2.0, 0.5, 1.0, T=1, lam=[10.0], s0=s0)
+    sol = _solve(pr)
+    assert sol.V[0, 0].tolist() == [0.0, 5.0, 10.0, 10.0, 10.0]
+    assert abs(sol.J - J_closed) <= 1e-12
+    assert abs(oracle.objective(pr, sol.V[0]) - J_closed) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_objective_off_grid_s0_exact_expectimax(seed):
+    """V7 at an off-grid s0: the exact-rational expectimax with a start lottery between the two
+    neighbouring grid states equals the oracle's interpolated J."""
+    inst = workloads.random_instance(seed, T=None, K=None, S_max=8)
+    rng = np.random.Generator(np.random.PCG64(seed + 99))
+    x = float(rng.integers(0, inst.S - 1)) + float(rng.choice([0.125, 0.25, 0.375, 0.7, 0.9]))
+    inst = dataclasses.replace(inst, s0=x * inst.delta)
+    pr = to_oracle(inst)
+    act = oracle.actions(pr)
+    sol = _solve(pr)
+    J_exact, _ = pins.expectimax_exact(inst, act)
+    assert abs(sol.J - float(J_exact)) <= 1e-12 * max(1.0, abs(float(J_exact))), seed

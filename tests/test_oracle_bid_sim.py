@@ -272,3 +272,34 @@ def test_fixed_schedule_replays_and_settles_linearly():
     inst2 = _det_instance([2 * x for x in lam])
     fix2, _ = oracle.simulate_strategy(to_oracle(inst2), None, oracle.SIM_FIXED, 1, seed=4, schedule=act[:, 0])
     assert fix2[0] == 2 * fix[0]
+
+
+@pytest.mark.parametrize("s0, J_closed", [(0.3, 3.0), (0.8, 8.0)])
+def test_simulation_off_grid_start_lottery(s0, J_closed):
+    """R24 in the simulation: an off-grid s0 starts at floor(x) w.p. 1 - w and floor(x) + 1 w.p. w,
+    so the Monte Carlo mean is the closed-form J = lambda*s0 (T = 1, lambda = 10, V_1 = [0, 5, 10,
+    10, 10]; see test_objective_off_grid_s0_closed_form).  A swapped start weight would move the
+    mean by 1.0, about 40 standard errors at n = 20000."""
+    pr = simple_problem(1.0, 2.0, 0.5, 1.0, T=1, lam=[10.0], s0=s0)
+    sol = oracle.backward(pr)
+    n = 20000
+    per, m, v = oracle.simulate(pr, sol.pol, n, seed=777)
+    se = np.sqrt(v / n)
+    assert 0.0 < se < 0.05
+    assert abs(m - J_closed) <= 5 * se
+    assert set(np.unique(per).tolist()) <= {0.0, 5.0, 10.0}
+
+
+def test_simulation_off_grid_start_multistage():
+    """R24 with a multi-stage Markov instance: the MC mean from an off-grid s0 lies within 5 standard
+    errors of the exact-rational expectimax J (start lottery), not only of the oracle's own J."""
+    import dataclasses
+    inst = workloads.random_instance(5, T=4, K=2, S_max=10, rank1=False)
+    inst = dataclasses.replace(inst, s0=(min(3, inst.S - 2) + 0.375) * inst.delta)
+    pr = to_oracle(inst)
+    sol = oracle.backward(pr)
+    J_exact, _ = pins.expectimax_exact(inst, oracle.actions(pr))
+    n = 40000
+    per, m, v = oracle.simulate(pr, sol.pol, n, seed=4242)
+    se = np.sqrt(v / n)
+    assert abs(m - float(J_exact)) <= 5 * se + 1e-9

@@ -542,6 +542,9 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   const auto h2d = cudaMemcpyHostToDevice;
   const auto d2d = cudaMemcpyDeviceToDevice;
   if (d.use_pending) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, d.use_ev, 0));
+  // Copies out of slot src must see its sampling tables complete: ready_tables() may have enqueued
+  // their (lazy) build on a simulation stream and re-recorded ev_tables there.
+  if (copy_old) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, o.ev_tables, 0));
   if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, lambda, TK * sizeof(double), h2d, s));
   else if (copy_old) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, o.lambda, TK * sizeof(double), d2d, s));
   const size_t npi = c->rank1 ? TK : K;

@@ -677,3 +677,36 @@ def test_price_paths_and_perfect_foresight():
         one = workloads.Instance("pf1", inst.T, 1, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                  lam[:, j:j + 1].copy(), np.ones((inst.T - 1, 1, 1)), np.array([1.0]))
         assert V1[j, i0] == oracle.backward(to_oracle(one)).J
+
+
+def test_lambda_only_load_after_side_stream_simulation():
+    """a time-varying chain with more than 4096 distinct P_t rows builds its sampling
+    tables lazily on the simulation's stream; a later lambda-only load copies those tables into the
+    other input slot and must wait for that build.  Simulate on a side stream, load lambda only, and
+    check that the next solve and simulation still equal the oracle bit for bit."""
+    import dataclasses
+    import torch
+    x = workloads.cfg2(T=80, K=64)
+    rng = np.random.Generator(np.random.PCG64(31337))
+    P = rng.dirichlet(np.ones(x.K) * 0.3, size=(x.T - 1, x.K))     # 79 distinct slices, 5056 rows
+    x = dataclasses.replace(x, P=np.ascontiguousarray(P))
+    y = dataclasses.replace(x, lam=np.ascontiguousarray(x.lam * 1.25 + 3.0))
+    rx = oracle.backward(to_oracle(x), nthreads=16)
+    ry = oracle.backward(to_oracle(y), nthreads=16)
+    n = 8192
+    sx = oracle.simulate(to_oracle(x), rx.pol, n, seed=9)[0]
+    sy = oracle.simulate(to_oracle(y), ry.pol, n, seed=9)[0]
+    side = torch.cuda.Stream()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    with E.Solver(x) as s:
+        assert s.backward() == rx.J
+        E.esdp_simulate_dev(s.ctx, n, 9, out.data_ptr(), stream=side)   # lazy table build on `side`
+        E.esdp_load(s.ctx, lam=y.lam)                                   # copies the old slot's tables
+        side.synchronize()
+        assert np.array_equal(out.cpu().numpy(), sx)
+        assert s.backward() == ry.J
+        E.esdp_simulate_dev(s.ctx, n, 9, out.data_ptr(), stream=side)
+        side.synchronize()
+        assert np.array_equal(out.cpu().numpy(), sy)
+        per, _, _ = s.simulate(n, seed=9)
+        assert np.array_equal(per, sy)

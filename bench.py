@@ -10,10 +10,12 @@ The metric is BASELINE.json's: DP cell-updates/s = T*S*K*A / step time (whole jo
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun.  --mode instances (default): every rank solves its own instance
-(independent price draws, the cfg5-style instance sharding of SURVEY.md §8(e).3) with no data-path
-collective -> "scaling": "weak".  --mode kpart: one instance, price-state rows split across ranks with an
-NCCL all-gather of V_t every stage -> "scaling": "strong".
+N > 1: launched by torchrun (one process per GPU), or self-launched through torch.distributed.run when
+--gpus N > 1 and WORLD_SIZE is unset.  The main line is --mode kpart (default for N > 1): one instance,
+price-state rows split across ranks with an NCCL all-gather of V_t every stage ->
+"scaling": "strong"; rank 0 then checks J, V_1 and every policy stage bit-equal to a 1-GPU context
+("parity_vs_1gpu").  The instance-sharded run (every rank its own instance, no
+data-path collective) is measured after it and reported under "instances_weak".
 --impl reference times the FP64 CPU oracle (oracle/) on this host's cores on a bounded sample of the
 same workload (rank 0 only).
 """
@@ -161,7 +163,7 @@ WORKLOAD = {
 }
 
 
-def run_ours(args):
+def run_ours(args, mode):
     import ctypes
 
     import numpy as np
@@ -174,10 +176,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    kpart = args.mode == "kpart"
+    kpart = mode == "kpart"
     # instances: every rank its own instance (weak scaling); kpart: one instance, K rows split (strong)
     inst = _instance(args, 0 if kpart else rank)
     dist_arg = None
@@ -188,8 +188,7 @@ def run_ours(args):
         dist_arg = (world, rank, nid[0])
     # table3 is the paper's Table 3 timing: the DP solve alone (no bid curves, no paths)
     solve_only = args.config == "table3"
-    solver = E.Solver(inst, keep_values=not solve_only, dist=dist_arg,
-                      force_brute=args.stencil == "brute", persist=args.plan == "persistent")
+    solver = E.Solver(inst, keep_values=not solve_only, dist=dist_arg, force_brute=args.stencil == "brute")
     T, S, A, K = solver.T, solver.S, solver.A, solver.K
     cells = T * S * K * A
     stream = torch.cuda.Stream(device=dev)
@@ -281,8 +280,7 @@ def run_ours(args):
         # ~16 sampled stages (kept out of the timed graph: event nodes break the PDL edges there); without
         # ESDP_KEEP_VALUES so that it fits next to the timed context
         try:
-            with E.Solver(inst, keep_values=False, profile=True, force_brute=args.stencil == "brute",
-                          persist=args.plan == "persistent") as prof:
+            with E.Solver(inst, keep_values=False, profile=True, force_brute=args.stencil == "brute") as prof:
                 for j in range(args.warmup + args.steps):
                     prof.backward()
                     if j >= args.warmup:
@@ -361,54 +359,83 @@ def run_ours(args):
     d2h = 8 + 16  # J, (mean, var)
 
     peaks, peak_kind = _peaks()
+    hbm_peak = float(peaks["hbm_gbs"])
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp64_peak = n_sm * FP64_LANES_PER_SM * sm_max * 1e6 / 1e9          # G FP64 instr/s
-    # algorithmic FP64 work of one backward on this rank: 2 per cell (add + max),
-    # K FMA per (k, s) element of the expectation (T-1 stages); rows owned by this rank
+    fp64_peak = n_sm * FP64_LANES_PER_SM * sm_max * 1e6          # FP64 thread-instructions/s (DFMA/DADD lanes)
     rows_here = k_cnt if kpart else K
-    algo_ops = 2.0 * T * S * rows_here * A + (T - 1) * S * rows_here * (1 if inst.P is None else K) * 1.0
-    bw_ms = part[0]
-    achieved = algo_ops / (bw_ms * 1e-3) / 1e9
-    hbm_bytes = 18.0 * T * rows_here * S                               # read W, write V + pol per (k, s, t)
-    hbm_ach = hbm_bytes / (bw_ms * 1e-3) / 1e9
     plan = E.esdp_stencil_kind(solver.ctx)
-    # DRAM traffic per backward from the committed ncu capture of this workload (cfg2, graph plan)
-    traffic, traffic_note = None, None
-    tr_path = os.path.join(ROOT, "profiles", "r01m_backward_traffic.json")
-    if args.config == "cfg2" and not kpart and not (plan & 2) and os.path.exists(tr_path):
-        with open(tr_path) as f:
-            traffic = json.load(f)["per_backward_bytes"]
-        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum summed over one backward's kernels "
-                        "(profiles/r01m_backward_traffic.json, ncu --cache-control none); algorithmic bytes "
-                        "%.4g" % hbm_bytes)
-    # the two stage kernels on their own (after the timed region): warm back-to-back launches of stage T-1's
-    # kernel, CUDA events on the context's stream, each launch including its kernel boundary (no PDL)
-    kernels = None
-    if rank == 0 and not kpart and not (plan & 2) and T > 1:
+    kprof = _kernel_profile(args.config) if not kpart and args.stencil == "auto" else None
+    kernels, binding, bw_only_ms = None, None, None
+    if rank == 0 and world == 1 and T > 1 and rows_here > 0:
+        # the two stage kernels on their own (after the timed region): warm back-to-back launches of stage
+        # T-1's kernel, CUDA events on the context's stream, each launch including its kernel boundary
         us_st = E.esdp_debug_time(solver.ctx, 1, 200)
-        st_work = 2.0 * S * K * A
-        kernels = {"stencil": {"kernel": "window_stencil_kernel" if plan & 1 else "stencil_kernel", "bound": "alu",
-                               "us_per_launch": us_st, "work_per_launch": st_work,
-                               "achieved": st_work / us_st / 1e3, "peak": fp64_peak, "unit": "G FP64 instr/s",
-                               "frac": st_work / us_st / 1e3 / fp64_peak,
-                               "note": "brute-force-equivalent FP64 instructions (2 per cell, SURVEY 8(d).3)",
-                               "hbm": {"bytes_per_launch": 18.0 * S * K, "achieved": 18.0 * S * K / us_st / 1e3,
-                                       "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
-                                       "frac": 18.0 * S * K / us_st / 1e3 / float(peaks["hbm_gbs"]),
-                                       "note": "read W_t, write V_t and the int16 policy per (k, s); W_t and V_t are "
-                                               "L2-resident on cfg2, so DRAM sees little of it"}}}
+        outs = S * rows_here
+        st_bytes = 18.0 * outs                # read W_t (8 B), write V_t (8 B) and pol_t (2 B) per output (k, s)
+        win = {"kernel": "window_stencil_kernel" if plan & 1 else "stencil_kernel", "bound": "hbm",
+               "us_per_launch": us_st, "bytes_per_launch": st_bytes, "achieved": st_bytes / us_st / 1e3,
+               "peak": hbm_peak, "unit": "GB/s", "frac": st_bytes / us_st / 1e3 / hbm_peak,
+               "traffic": None, "instr_per_output": None}
+        if kprof and "window" in kprof:
+            win["traffic"] = kprof["window"]["dram_bytes_per_launch"]
+            win["instr_per_output"] = kprof["window"]["warp_inst_per_launch"] * 32.0 / outs
+            win["fp64_thread_inst_per_launch"] = kprof["window"]["fp64_thread_inst_per_launch"]
+        kernels = {"stencil": win}
         if inst.P is not None:
             us_ct = E.esdp_debug_time(solver.ctx, 0, 200)
-            ct_flop = 2.0 * K * K * S
-            kernels["expectation"] = {"kernel": "contract_dmma3_kernel" if K % 2 == 0 else "contract_dmma2_kernel",
-                                      "bound": "tensor", "us_per_launch": us_ct, "work_per_launch": ct_flop,
+            ct_flop = 2.0 * K * rows_here * S
+            kernels["expectation"] = {"kernel": "contract_dmma3_kernel" if (plan & 2 and K % 2 == 0) else "contract_dmma2/dfma",
+                                      "bound": "tensor", "us_per_launch": us_ct, "flop_per_launch": ct_flop,
                                       "achieved": ct_flop / us_ct / 1e6, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                                       "frac": ct_flop / us_ct / 1e6 / DMMA_PEAK_TFLOPS,
-                                      "note": "FP64 DMMA; peak measured by tools/microbench/mb.cu "
+                                      "note": "FP64 DMMA (mma.m8n8k4.f64); peak measured by tools/microbench/mb.cu "
                                               "(profiles/r01_microbench.json)"}
+        us_dep = E.esdp_debug_time(solver.ctx, 3, 200)   # a 1-block dependent kernel: the cost of a boundary
+        # the backward alone (no bid curves, no paths), events around 10 solves of a plain context
+        with E.Solver(inst, keep_values=False, force_brute=args.stencil == "brute") as plain:
+            e0, e1 = ev(), ev()
+            ps = torch.cuda.Stream(device=dev)
+            for _ in range(3):
+                E.esdp_backward_async(plain.ctx, ps.cuda_stream)
+            e0.record(ps)
+            for _ in range(10):
+                E.esdp_backward_async(plain.ctx, ps.cuda_stream)
+            e1.record(ps)
+            torch.cuda.synchronize(dev)
+            bw_only_ms = e0.elapsed_time(e1) / 10
+        # binding roofline of the backward: the slowest of HBM (algorithmic bytes),
+        # compute (FP64 instructions the stencil actually executes, from ncu, + the DMMA flops) and the
+        # dependent-launch floor (2 kernel boundaries per stage), over the measured backward time
+        algo_bytes = 18.0 * T * S * rows_here + (8.0 * (T - 1) * K * rows_here if inst.P is not None else 0.0)
+        t_hbm = algo_bytes / (hbm_peak * 1e9) * 1e3
+        t_dmma = (T - 1) * 2.0 * K * rows_here * S / (DMMA_PEAK_TFLOPS * 1e12) * 1e3 if inst.P is not None else 0.0
+        t_fp64 = (T * win["fp64_thread_inst_per_launch"] / fp64_peak * 1e3) if "fp64_thread_inst_per_launch" in win else None
+        t_comp = None if t_fp64 is None else t_fp64 + t_dmma
+        t_sync = T * (2 if inst.P is not None else 1) * us_dep * 1e-3
+        cands = {"hbm": t_hbm, "compute": t_comp, "launch": t_sync}
+        bind = max((k for k in cands if cands[k] is not None), key=lambda k: cands[k])
+        binding = {"t_hbm_ms": t_hbm, "t_compute_ms": t_comp, "t_fp64_stencil_ms": t_fp64, "t_dmma_ms": t_dmma,
+                   "t_launch_floor_ms": t_sync, "us_per_dependent_launch": us_dep, "t_backward_ms": bw_only_ms,
+                   "binding": bind, "frac": cands[bind] / bw_only_ms,
+                   "note": "max(t_HBM, t_compute, T x boundaries) / measured backward (SURVEY 8(d).3(iii)); "
+                           "t_compute from the FP64 instructions the stencil executes (ncu, profiles/) plus the "
+                           "DMMA flops at the measured DMMA peak; algorithmic bytes %.4g per backward" % algo_bytes}
     out = None
     if rank == 0:
+        roof = None
+        if kernels:
+            w = kernels["stencil"]
+            roof = {"bound": "hbm", "achieved": w["achieved"], "peak": hbm_peak, "unit": "GB/s", "frac": w["frac"],
+                    "traffic": w["traffic"], "kernel": w["kernel"], "us_per_launch": w["us_per_launch"],
+                    "bytes_per_launch": w["bytes_per_launch"], "instr_per_output": w["instr_per_output"],
+                    "work_per_launch": "18 B per output (k, s): read W_t, write V_t (FP64) and pol_t (int16); "
+                                       "S*K outputs = %d" % (S * rows_here),
+                    "peak_note": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind,
+                    "note": "the dominant kernel of the step (ncu launch list, profiles/); warm launches timed "
+                            "with CUDA events after the timed region; V_t / W_t of a single cfg2 instance stay "
+                            "L2-resident, so this kernel is latency- and issue-bound, not DRAM-bound "
+                            "(roofline_binding)"}
         out = {
             "metric": "DP cell-updates/sec (T*S*K*A)",
             "value": value,
@@ -432,26 +459,19 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write outside the step events)",
                        "parallelism": (f"K-partitioned x{world} (NCCL all-gather of V_t per stage)" if kpart else
                                        f"instance-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU"),
-                       "plan": {"stencil": "window" if plan & 1 else "brute", "backward": "persistent" if plan & 2 else "graph",
+                       "plan": {"stencil": "window" if plan & 1 else "brute",
+                                "expectation": "FP64 DMMA" if plan & 2 else "DFMA",
                                 "bidcurves": "fused into the backward graph" if fused else "after the backward"}},
             "gpu_launches": launches_per_step * args.steps,
             "ms_per_part": {"backward" + ("+bidcurves (fused branch)" if fused else ""): part[0],
-                            "bidcurves": None if fused else part[1], "simulate": part[2]},
+                            "bidcurves": None if fused else part[1], "simulate": part[2],
+                            "backward_only": bw_only_ms},
             "backward_phase_ms": ({"expectation": phases[0], "stencil": phases[1],
                                    "note": "separate profiled context (events around the kernels of ~16 stages)"}
                                   if phases_ok else None),
-            "roofline": {"bound": "alu",
-                         "kernel": "backward (%s)" % ("persistent dataflow kernel" if plan & 2 else "graph of 2T kernels"),
-                         "achieved": achieved, "peak": fp64_peak, "unit": "G FP64 instr/s",
-                         "frac": achieved / fp64_peak, "traffic": traffic, "traffic_note": traffic_note,
-                         "peak_note": f"{n_sm} SMs x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz "
-                                      f"(sm_max_mhz from MEASURED_PEAKS.json: {peak_kind})",
-                         "work_per_launch": f"algorithmic FP64 instr: 2 per cell x T*S*K*A + K per (k,s) x (T-1)*S*K "
-                                            f"= {algo_ops:.4g}"},
+            "roofline": roof,
+            "roofline_binding": binding,
             "roofline_kernels": kernels,
-            "roofline_hbm_literal": {"bound": "hbm", "achieved": hbm_ach, "peak": float(peaks["hbm_gbs"]),
-                                     "unit": "GB/s", "frac": hbm_ach / float(peaks["hbm_gbs"]),
-                                     "bytes_per_launch": hbm_bytes},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -460,17 +480,55 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(inst, budget_s=args.cpu_budget)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    if kpart and world > 1:
+        out_p = _parity_vs_1gpu(E, solver, inst, rank, world, dev)
+        if rank == 0:
+            out.update(out_p)
     solver.close()
     return out
 
 
+def _parity_vs_1gpu(E, solver, inst, rank, world, dev):
+    """K-partitioned run vs one GPU (an all-gather is a copy): rank 0 solves the same instance
+    on a context of its own and compares J, V_1 and every stage's policy bit for bit; every rank reports its
+    communicator's rank count."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    w, r, nr = E.esdp_dist_info(solver.ctx)
+    ok_local = torch.tensor([1 if (w == world and r == rank and nr == world) else 0], device=dev)
+    dist.all_reduce(ok_local, op=dist.ReduceOp.MIN)
+    res = {}
+    if rank == 0:
+        J = E.esdp_objective(solver.ctx)
+        V1 = E.esdp_values(solver.ctx, 1, want_W=False)
+        pols = [E.esdp_policy(solver.ctx, t) for t in range(1, solver.T + 1)]
+        with E.Solver(inst, keep_values=False) as one:
+            J1 = one.backward()
+            same = (J == J1 and np.array_equal(V1, E.esdp_values(one.ctx, 1, want_W=False)) and
+                    all(np.array_equal(pols[t - 1], one.policy(t)) for t in range(1, solver.T + 1)))
+        res = {"parity_vs_1gpu": bool(same), "comm_nranks_ok": bool(ok_local.item()), "J_1gpu": J1,
+               "parity_note": "J, V_1 and pol_t for every t of the K-partitioned run equal a 1-GPU context's bits"}
+    dist.barrier()
+    return res
+
+
+def _kernel_profile(config):
+    """ncu counts of the stage kernels for this workload (profiles/r02_stage_kernels.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r02_stage_kernels.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(config)
+
+
 def run_sweep(args):
     """cfg5: a batch of storage configurations (different pbar, eta -> different action grids) over one
-    price model, solved by one batch context (esdp_create_batch); each instance = backward + 1024
-    simulated paths.  Ranks take disjoint instance ranges (weak scaling, no data-path collective)."""
+    price model, solved by one batch context (esdp_create_batch); each instance = backward + 1024 simulated
+    paths (1024 x 1024 = 1.05e6 paths over the whole sweep).  Rank r of N takes a stratified sample of the
+    1024-configuration sweep (every (N n / 1024)-th configuration from offset r): with N n = 1024 the ranks
+    cover the sweep exactly once.  Weak scaling, no data-path collective."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -479,18 +537,18 @@ def run_sweep(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.instances
-    idx = [rank * n + j for j in range(n)]     # instance sharding across ranks (no communication)
+    tot = n * world
+    idx = [((rank + world * j) * 1024) // tot for j in range(n)]   # stratified over the sweep order
     insts = workloads.cfg5_instances(idx)
     batch = E.Batch(insts, force_brute=args.stencil == "brute")   # one graph: one expectation + one stencil launch per stage
     stream = torch.cuda.Stream(device=dev)
     paths = 1024
     out_d = torch.empty(n * paths, dtype=torch.float64, device=dev)
-    cells = sum(batch.T * batch.S * batch.K * a for a in batch.A)
+    T, S, K = batch.T, batch.S, batch.K
+    As = list(batch.A)
+    cells = sum(T * S * K * a for a in As)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(j):
@@ -525,24 +583,113 @@ def run_sweep(args):
     if world > 1:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
     ms = float(t_all.item())
-    # end to end: the per-instance storage parameters are host data that the batch is built from; the
-    # shared price model is uploaded with it, and the J of every instance comes back
     J = batch.objective()
-    As = list(batch.A)
     launches = (batch.launch_count() + 1) * args.steps
+
+    # end to end through the public API with host buffers: every step uploads the shared price model from
+    # pinned host memory (esdp_batch_load_async: validation, H2D, sampling tables), solves, simulates and
+    # reads every instance's J back to the host
+    base = insts[0]
+    lam_h = torch.from_numpy(np.ascontiguousarray(base.lam)).pin_memory()
+    P_h = torch.from_numpy(np.ascontiguousarray(base.P)).pin_memory()
+    pi_h = torch.from_numpy(np.ascontiguousarray(base.pi)).pin_memory()
+    J_h = torch.zeros(n, dtype=torch.float64).pin_memory()
+    h2d = (lam_h.numel() + P_h.numel() + pi_h.numel()) * 8
+
+    def e2e_step(j):
+        batch.load_async(lam_h.data_ptr(), P_h.data_ptr(), pi_h.data_ptr(), stream.cuda_stream)
+        batch.backward_async(stream.cuda_stream)
+        batch.simulate_dev(paths, 17 + j, out_d.data_ptr(), stream.cuda_stream)
+        stream.synchronize()
+        J_h.copy_(torch.from_numpy(batch.objective()))      # D2H of every instance's J
+
+    for j in range(args.warmup):
+        e2e_step(j)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for j in range(args.steps):
+        e2e_step(j)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = cells * world / float(e2e_t.item())
+
+    # roofline of the dominant kernels (warm launches of stage T-1's batch kernels after the timed region)
+    peaks, peak_kind = _peaks()
+    hbm_peak = float(peaks["hbm_gbs"])
+    kern = None
+    if rank == 0:
+        us_win = batch.kernel_time(1, 50)
+        us_exp = batch.kernel_time(0, 50)
+        outs = n * K * S
+        win_bytes = 18.0 * outs
+        exp_bytes = 8.0 * (2 * n * K * S + K * K)     # read V_{t+1}, write W_t, read P_t
+        exp_flop = 2.0 * K * K * n * S
+        kern = {"window": {"kernel": "window_batch_kernel", "us_per_launch": us_win, "bytes_per_launch": win_bytes,
+                           "achieved": win_bytes / us_win / 1e3, "peak": hbm_peak, "unit": "GB/s",
+                           "frac": win_bytes / us_win / 1e3 / hbm_peak},
+                "expectation": {"kernel": "contract_dmma3_kernel (one [K] x [n ld] GEMM per stage)",
+                                "us_per_launch": us_exp, "bytes_per_launch": exp_bytes,
+                                "hbm_frac": exp_bytes / us_exp / 1e3 / hbm_peak, "flop_per_launch": exp_flop,
+                                "achieved_tflops": exp_flop / us_exp / 1e6,
+                                "dmma_frac": exp_flop / us_exp / 1e6 / DMMA_PEAK_TFLOPS}}
     batch.close()
-    out = {"metric": "DP cell-updates/sec (T*S*K*A)", "value": cells * world / (ms * 1e-3), "unit": "cell-updates/s",
-           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (cfg2 price chain; cfg5 storage sweep)",
-           "config": {"workload": "cfg5 sweep sample: %d storage configurations per GPU in one batch context "
-                                  "(pbar/delta in [10.42, 99], eta in [0.80, 0.99]; T=288, S=1001, K=100; A=%d..%d), "
-                                  "1024 simulated paths each" % (n, min(As), max(As)),
-                      "instances_per_gpu": n, "l2": "flushed between timed steps",
-                      "plan": "esdp_create_batch: per stage one [K] x [n ld] expectation + one window launch"},
-           "gpu_launches": launches, "J_mean": float(np.mean(J)),
-           "clocks": clk}
-    return out if rank == 0 else None
+    out = None
+    if rank == 0:
+        w = kern["window"]
+        out = {"metric": "DP cell-updates/sec (T*S*K*A)", "value": cells * world / (ms * 1e-3), "unit": "cell-updates/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (cfg2 price chain; cfg5 storage sweep)",
+               "config": {"workload": "cfg5 sweep: %d storage configurations per GPU, a stratified sample of the "
+                                      "1024-configuration sweep (pbar/delta in [10.42, 99], eta in [0.80, 0.99]; "
+                                      "T=288, S=1001, K=100; A=%d..%d, mean %.1f), 1024 simulated paths each"
+                                      % (n, min(As), max(As), float(np.mean(As))),
+                          "instances_per_gpu": n, "sweep_indices": [idx[0], idx[-1], len(idx)],
+                          "mean_A": float(np.mean(As)), "l2": "flushed between timed steps",
+                          "sim_paths_per_step": n * paths * world,
+                          "plan": "esdp_create_batch: per stage one [K] x [n ld] expectation + one window launch"},
+               "gpu_launches": launches, "J_mean": float(np.mean(J)),
+               "roofline": {"bound": "hbm", "achieved": w["achieved"], "peak": hbm_peak, "unit": "GB/s",
+                            "frac": w["frac"], "traffic": None, "kernel": w["kernel"],
+                            "us_per_launch": w["us_per_launch"], "bytes_per_launch": w["bytes_per_launch"],
+                            "work_per_launch": "18 B per output (m, k, s): read W_t, write V_t, pol_t",
+                            "peak_note": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind},
+               "roofline_kernels": kern,
+               "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": 8 * n},
+               "clocks": clk}
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_sweep(insts, budget_s=args.cpu_budget)
+    return out
+
+
+def cpu_baseline_sweep(insts, budget_s=15.0, n_inst=8):
+    """The oracle on a bounded sample of the cfg5 step: n_inst configurations spread over the batch, the
+    last few stages of each (every (k, i) row), extrapolated per cell (per-stage cost is constant)."""
+    import oracle
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import to_oracle
+    cores = os.cpu_count() or 1
+    pick = [insts[(j * len(insts)) // n_inst] for j in range(min(n_inst, len(insts)))]
+    prs = [to_oracle(x) for x in pick]
+    t0 = time.perf_counter()
+    oracle.backward(prs[0], t_stop=pick[0].T - 1, nthreads=cores)   # 2 stages to size the sample
+    per_stage = max(time.perf_counter() - t0, 1e-3) / 2
+    n_stages = int(max(2, min(pick[0].T, budget_s / (per_stage * len(pick)))))
+    cells, t = 0, 0.0
+    for x, pr in zip(pick, prs):
+        S, A = oracle.dims(pr)
+        t0 = time.perf_counter()
+        oracle.backward(pr, t_stop=x.T - n_stages + 1, nthreads=cores)
+        t += time.perf_counter() - t0
+        cells += n_stages * S * x.K * A
+    return {"value": cells / t, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle backward of {len(pick)} configurations spread over the batch, the last {n_stages} "
+                      f"of {pick[0].T} stages each (all K*S rows, OpenMP {cores} threads), {t:.2f} s"}
 
 
 def cpu_baseline(inst, budget_s=20.0, n_stages=None):
@@ -602,6 +749,22 @@ def run_reference(args):
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def _self_launch(n):
+    """--gpus N > 1 without a torchrun environment: run this script under torch.distributed.run, one process
+    per GPU on this node (rendezvous on 127.0.0.1), and exit with its status."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} but only {torch.cuda.device_count()} CUDA devices are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -609,7 +772,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOAD) + ["cfg5"])
-    ap.add_argument("--instances", type=int, default=16, help="cfg5: storage configurations per GPU")
+    ap.add_argument("--instances", type=int, default=128,
+                    help="cfg5: storage configurations per GPU (a stratified sample of the 1024-configuration sweep; "
+                         "8 GPUs x 128 = the whole sweep)")
     ap.add_argument("--t3-hours", type=float, default=100.0, help="table3: battery duration (hours)")
     ap.add_argument("--t3-delta", type=float, default=0.01, help="table3: SoC step (MWh)")
     ap.add_argument("--paths", type=int, default=65536)
@@ -617,25 +782,46 @@ def main():
     ap.add_argument("--ref-stages", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-events", type=int, default=1,
-                    help="per-phase device timers inside the backward (persistent plan) / events (graph plan)")
+                    help="per-phase split of the backward from a separate context with CUDA events around ~16 stages")
     ap.add_argument("--bids", choices=["fused", "after", "with-sim"], default="fused",
                     help="bid curves as side branches of the backward graph (fused), one kernel after it, or one "
                          "kernel on a side stream concurrent with the simulation")
     ap.add_argument("--stencil", choices=["auto", "brute"], default="auto",
                     help="auto: exact sliding-window stencil where it applies; brute: every (i, a) cell")
-    ap.add_argument("--plan", choices=["graph", "persistent"], default="graph",
-                    help="backward as a CUDA graph of 2T kernels, or one persistent dataflow kernel (1 GPU)")
-    ap.add_argument("--mode", choices=["instances", "kpart"], default="instances",
-                    help="N>1: independent instances per rank (weak) or one K-partitioned instance (strong)")
+    ap.add_argument("--mode", choices=["instances", "kpart"], default=None,
+                    help="N>1: one K-partitioned instance (kpart, the default main line, strong scaling) or "
+                         "independent instances per rank (instances, weak)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args.gpus))
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
-        out = run_reference(args)
-    elif args.config == "cfg5":
-        out = run_sweep(args)
+        out = run_reference(args)   # rank 0 only; the other ranks exit without work
     else:
-        out = run_ours(args)
+        import torch
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.config == "cfg5":
+            out = run_sweep(args)
+        else:
+            mode = args.mode or ("kpart" if world > 1 else "instances")
+            out = run_ours(args, mode)
+            if world > 1 and args.mode is None:   # the instance-sharded (weak) number beside the main line
+                extra_args = argparse.Namespace(**vars(args))
+                extra_args.kernel_events = 0
+                extra = run_ours(extra_args, "instances")
+                if rank == 0:
+                    out["instances_weak"] = {k: extra[k] for k in ("value", "unit", "ms_per_step", "scaling", "e2e")}
+                    out["instances_weak"]["parallelism"] = extra["config"]["parallelism"]
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
     if out is not None:
         print(json.dumps(out), flush=True)
 

@@ -63,18 +63,13 @@ enum {
   ESDP_NO_PDL = 8u,       /* launch the per-stage kernels without programmatic dependent launch (PDL
                              with a late trigger is the default: ~3.5% faster chain) */
   ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
-  ESDP_DMMA_L2 = 64u,     /* DMMA expectation with operands read straight from L2 by every warp
-                             (instead of staged once per block in shared memory) */
-  ESDP_PERSIST = 32u      /* single GPU: run the backward pass as ONE persistent dataflow kernel (a
-                             device-side ready queue of per-tile stencil / expectation tasks, no grid
-                             barrier) instead of a CUDA graph of 2T kernels (opt-in: measured slower
-                             for cfg2 on B200) */
+  ESDP_FLAGS_ALL = 31u    /* every defined flag; other bits -> ESDP_E_CONFIG.  Bits 32 (persistent
+                             dataflow backward) and 64 (DMMA operands straight from L2) named paths that
+                             measured slower on B200 and were removed. */
 };
 
 /* Environment variables read at context creation (measurement knobs; every setting gives the same bits):
  *   ESDP_DMMA3=0      expectation on the all-at-once staged DMMA kernel instead of the k'-pipelined one
- *   ESDP_MC=1         expectation by TMA multicast across a thread-block cluster (measured slower on cfg2)
- *   ESDP_MC_C=c       cluster size for ESDP_MC (row tiles padded to a multiple of c)
  * DESIGN.md §5 and §7 record what each measured. */
 
 typedef struct {
@@ -102,14 +97,22 @@ esdp_status esdp_create(const esdp_problem* prob, esdp_ctx** out);
 
 /* Multi-GPU (north_star): one process per GPU, `world` ranks.  Rank r owns the price-
  * state rows [k_lo, k_lo + k_cnt) given by esdp_partition (blocks of kmax = ceil(K/world) rows).  Every
- * stage it computes W_t and V_t for its rows and all-gathers V_t and pol_t over NCCL (in place, kmax
- * rows per rank), so after esdp_backward every rank holds all of V and the policy, bit-identical to a
- * single GPU (the all-gather is a copy).  nccl_id: the 128-byte ncclUniqueId made by esdp_nccl_unique_id
- * on one rank and broadcast by the caller.  The current CUDA device must be this rank's GPU.  W_t (and
- * bid curves) are available only for the rank's own rows; esdp_values with W != NULL -> ESDP_E_STATE. */
+ * stage it computes W_t and V_t for its rows and all-gathers V_t over NCCL (in place, kmax rows per rank:
+ * the only exchange on the stage chain, "only t is sequential"); the policy rows stay local and
+ * are all-gathered once after stage 1 (one NCCL group of T all-gathers).  After esdp_backward every rank
+ * holds all of V and the policy, bit-identical to a single GPU (an all-gather is a copy).  nccl_id: the
+ * 128-byte ncclUniqueId made by esdp_nccl_unique_id on one rank and broadcast by the caller.  The current
+ * CUDA device must be this rank's GPU.  W_t (and bid curves) are available only for the rank's own rows;
+ * esdp_values with W != NULL -> ESDP_E_STATE.  Failure detection: the synchronous calls (esdp_backward,
+ * esdp_objective) poll ncclCommGetAsyncError while they wait; an asynchronous NCCL error, or no completion
+ * within ESDP_NCCL_TIMEOUT_S seconds (environment, default 120: a dead or hung peer), aborts the
+ * communicator (ncclCommAbort) and returns ESDP_E_NCCL; the context then needs recreating. */
 esdp_status esdp_create_dist(const esdp_problem* prob, int32_t world, int32_t rank, const void* nccl_id,
                              esdp_ctx** out);
 esdp_status esdp_nccl_unique_id(void* id128);
+/* world size and rank of a context, and the communicator's own rank count (ncclCommCount; 0 without a
+ * communicator, -1 if the query failed): lets a launcher check that NCCL saw every rank. */
+esdp_status esdp_dist_info(const esdp_ctx* ctx, int32_t* world, int32_t* rank, int32_t* nccl_nranks);
 /* Row ownership of a rank (pure host function; no GPU needed). */
 esdp_status esdp_partition(int32_t K, int32_t world, int32_t rank, int32_t* k_lo, int32_t* k_cnt, int32_t* kmax);
 
@@ -241,8 +244,10 @@ esdp_status esdp_simulate_strategy_dev(esdp_ctx* ctx, int64_t n_paths, uint64_t 
                                        void* stream);
 
 /* Execution plan: bit 0 = stencil (1 = exact sliding-window for the recombining grid with a linear
- * payoff, 0 = brute force over every (i, a) cell); bit 1 = backward as one persistent dataflow
- * kernel (else a CUDA graph of 2T kernels).  All plans give bit-identical results. */
+ * payoff, 0 = brute force over every (i, a) cell); bit 1 = expectation on the FP64 tensor cores (DMMA,
+ * wherever the shape allows: >= 8 rows or rank-1 with even K; 0 = DFMA on the CUDA cores); bit 2 = the DMMA bit-exactness probe run at context creation found a
+ * DMMA result that differs from the canonical fma chain (R15), so the expectation fell back to DFMA.
+ * All plans give bit-identical results. */
 esdp_status esdp_stencil_kind(const esdp_ctx* ctx, int32_t* kind);
 
 /* Number of (i, k) rows, summed over all stages and contexts since the last call, for which the
@@ -289,7 +294,7 @@ typedef struct esdp_batch esdp_batch;
 
 /* probs[0..n-1]: host descriptions as for esdp_create (deep-copied).  lambda, P and pi must be
  * identical in content across instances (else ESDP_E_CONFIG); they are validated once.  flags:
- * KEEP_VALUES / PROFILE / PERSIST are ignored.  Errors as esdp_create (message: esdp_batch_last_error(NULL)). */
+ * KEEP_VALUES / PROFILE are ignored.  Errors as esdp_create (message: esdp_batch_last_error(NULL)). */
 esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch** out);
 /* n, T, S, K and A[n] (each instance's action count; A may be NULL). */
 esdp_status esdp_batch_dims(const esdp_batch* b, int32_t* n, int32_t* T, int32_t* S, int32_t* K, int32_t* A);
@@ -306,8 +311,19 @@ esdp_status esdp_batch_value1(esdp_batch* b, int32_t m, double* V1);
  * paths of esdp_simulate_dev(seed + m) on a context of its own; per-path profits to
  * out_dev[m * n_paths + path] (device).  Enqueued on stream, not synchronized. */
 esdp_status esdp_batch_simulate_dev(esdp_batch* b, int64_t n_paths, uint64_t seed, double* out_dev, void* stream);
+/* Replace the shared price model (lambda [T][K]; P [T-1][K][K] or NULL in rank-1 mode; pi as in
+ * esdp_problem) of every instance: validated on the host as esdp_create does (ESDP_E_DATA), then copied
+ * host->device and the simulation's sampling tables rebuilt, all enqueued on stream (NULL = the batch's
+ * own).  A later esdp_batch_backward_async on the same stream solves with the new inputs.  Pinned host
+ * arrays must stay valid until the stream has passed the copies (pageable ones are staged at once).  A
+ * new P may not have more distinct stage slices than the batch was created with (ESDP_E_STATE). */
+esdp_status esdp_batch_load_async(esdp_batch* b, const double* lambda, const double* P, const double* pi, void* stream);
 /* Kernel launches of one batch backward pass. */
 esdp_status esdp_batch_launch_count(const esdp_batch* b, int64_t* n);
+/* Diagnostic: microseconds per warm launch of stage T-1's batch expectation (what = 0), window-stencil
+ * (1) or brute-force stencil (2) kernel, reps back-to-back launches in a CUDA graph (CUDA events on the
+ * batch's stream).  Needs a completed backward pass (its buffers are the inputs). */
+esdp_status esdp_batch_kernel_time(esdp_batch* b, int32_t what, int32_t reps, double* us_per_launch);
 void esdp_batch_destroy(esdp_batch* b);
 /* Message of the last failing call on b (b == NULL: last esdp_create_batch failure of this thread). */
 const char* esdp_batch_last_error(const esdp_batch* b);

@@ -31,8 +31,7 @@ ESDP_PROFILE = 2
 ESDP_FORCE_BRUTE = 4
 ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
-ESDP_PERSIST = 32
-ESDP_DMMA_L2 = 64
+ESDP_FLAGS_ALL = 31
 ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS, ESDP_SIM_SELF, ESDP_SIM_FIXED = 0, 1, 2, 3, 4
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
@@ -42,12 +41,13 @@ EXPORTED_SYMBOLS = [
     "esdp_objective", "esdp_values", "esdp_policy", "esdp_bidcurves", "esdp_bidcurves_dev",
     "esdp_simulate", "esdp_simulate_dev", "esdp_launch_count", "esdp_kernel_times", "esdp_stencil_kind",
     "esdp_debug_time", "esdp_window_fallbacks", "esdp_window_level_tables", "esdp_destroy", "esdp_last_error",
-    "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_set_bid_requests",
+    "esdp_create_dist", "esdp_nccl_unique_id", "esdp_partition", "esdp_dist_info", "esdp_set_bid_requests",
     "esdp_simulate_mode", "esdp_simulate_mode_dev", "esdp_simulate_strategy_dev", "esdp_price_paths_dev",
     "esdp_simulate_async", "esdp_objective_async",
     "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
     "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
-    "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error",
+    "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error", "esdp_batch_load_async",
+    "esdp_batch_kernel_time",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -110,6 +110,7 @@ def _load():
         "esdp_create_dist": ([ctypes.POINTER(esdp_problem), ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p,
                               ctypes.POINTER(_vp)], ctypes.c_int),
         "esdp_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+        "esdp_dist_info": ([ctx, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_set_bid_requests": ([ctx, ctypes.c_int64, _i32p, ctypes.c_int32, _vp, _vp, _vp, _vp], ctypes.c_int),
         "esdp_partition": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p], ctypes.c_int),
         "esdp_destroy": ([ctx], None),
@@ -123,6 +124,8 @@ def _load():
         "esdp_batch_value1": ([ctx, ctypes.c_int32, _dp], ctypes.c_int),
         "esdp_batch_simulate_dev": ([ctx, ctypes.c_int64, ctypes.c_uint64, _vp, _vp], ctypes.c_int),
         "esdp_batch_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "esdp_batch_load_async": ([ctx, _vp, _vp, _vp, _vp], ctypes.c_int),
+        "esdp_batch_kernel_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
         "esdp_batch_destroy": ([ctx], None),
         "esdp_batch_last_error": ([ctx], ctypes.c_char_p),
     }
@@ -183,6 +186,13 @@ def esdp_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib.esdp_nccl_unique_id(buf), "esdp_nccl_unique_id", None)
     return buf.raw
+
+
+def esdp_dist_info(ctx):
+    """(world, rank, nccl_nranks) of a context; nccl_nranks is the communicator's ncclCommCount (0: none)."""
+    w, r, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.esdp_dist_info(ctx, ctypes.byref(w), ctypes.byref(r), ctypes.byref(n)), "esdp_dist_info", ctx)
+    return w.value, r.value, n.value
 
 
 def esdp_partition(K, world, rank):
@@ -331,7 +341,7 @@ def esdp_kernel_times(ctx):
 
 
 def esdp_stencil_kind(ctx) -> int:
-    """bit 0: 1 = exact sliding-window stencil, 0 = brute force; bit 1: persistent dataflow kernel."""
+    """bit 0: 1 = exact sliding-window stencil, 0 = brute force."""
     k = ctypes.c_int32()
     _check(lib.esdp_stencil_kind(ctx, ctypes.byref(k)), "esdp_stencil_kind", ctx)
     return k.value
@@ -366,14 +376,14 @@ class Solver:
     """Owning wrapper of one esdp context.  `inst` is any object with the esdp_problem fields
     (T, K, pbar, sbar, s0, eta_c, eta_d, delta, lam, P, pi, actions, payoff_kind, g)."""
 
-    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=True, dmma=True, persist=False,
+    def __init__(self, inst, keep_values=True, profile=False, force_brute=False, pdl=True, dmma=True,
                  dist=None):
         self.ctx = esdp_create(inst.T, inst.K, inst.pbar, inst.sbar, inst.s0, inst.eta_c, inst.eta_d, inst.delta,
                                inst.lam, inst.P, inst.pi, getattr(inst, "actions", None),
                                getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR), getattr(inst, "g", None),
                                (ESDP_KEEP_VALUES if keep_values else 0) | (ESDP_PROFILE if profile else 0)
                                | (ESDP_FORCE_BRUTE if force_brute else 0) | (0 if pdl else ESDP_NO_PDL)
-                               | (0 if dmma else ESDP_NO_DMMA) | (ESDP_PERSIST if persist else 0), dist=dist)
+                               | (0 if dmma else ESDP_NO_DMMA), dist=dist)
         self.T, self.S, self.A, self.K = esdp_dims(self.ctx)
         self.stencil_kind = esdp_stencil_kind(self.ctx)
 
@@ -480,6 +490,15 @@ class Batch:
         n = ctypes.c_int64()
         self._check(lib.esdp_batch_launch_count(self.b, ctypes.byref(n)), "esdp_batch_launch_count")
         return n.value
+
+    def load_async(self, lam_ptr, P_ptr, pi_ptr, stream=None):
+        """esdp_batch_load_async from host addresses (pinned buffers: keep them alive until the stream passes)."""
+        self._check(lib.esdp_batch_load_async(self.b, lam_ptr, P_ptr, pi_ptr, _stream_ptr(stream)), "esdp_batch_load_async")
+
+    def kernel_time(self, what, reps=100):
+        us = ctypes.c_double()
+        self._check(lib.esdp_batch_kernel_time(self.b, int(what), int(reps), ctypes.byref(us)), "esdp_batch_kernel_time")
+        return us.value
 
     def close(self):
         if self.b:

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -25,7 +26,6 @@
 #include "../../include/esdp.h"
 #include "kernels.cuh"
 #include "window.cuh"
-#include "persistent.cuh"
 #include "batch.cuh"
 #include "simmodes.cuh"
 
@@ -120,14 +120,6 @@ struct esdp_ctx {
   cudaGraphExec_t graph = nullptr;
   size_t stencil_smem = 0;
   int64_t launches = 0;
-  // persistent dataflow backward (persistent.cuh): one launch per backward
-  int persist = 0, persist_grid = 0;
-  size_t persist_smem = 0;
-  int df_ntc = 0, df_ecw = 0, df_ncb = 0, df_nrg = 0, df_period = 0, df_ntasks = 0, df_n0 = 0;
-  size_t df_init_off = 0;
-  int *d_df_tab = nullptr;   // schedule tables (build_schedule)
-  int *d_df_cnt = nullptr;   // ready queue and dependency counters (reset per launch)
-  size_t df_cnt_n = 0;
   // bid-curve requests extracted inside the backward graph (esdp_set_bid_requests)
   int64_t fb_n = 0;
   int32_t fb_cap = 0;
@@ -144,9 +136,7 @@ struct esdp_ctx {
   int prof_stride = 1;
   bool pdl = true;
   int dmma2 = 0;   // shared-memory-staged DMMA expectation (set when its tile fits)
-  // TMA-multicast cluster expectation (contract_mc_kernel): tensor maps of P per input slot and of V
-  int mc = 0, mc_nrb = 0, mc_c = 0;   // plan on, row tiles (padded), cluster size
-  CUtensorMap mapP[2], mapV;
+  int dmma_probe_failed = 0;   // the DMMA-vs-fma-chain probe found a mismatch: expectation on DFMA
   bool solved = false;
   std::string err;
 };
@@ -349,10 +339,10 @@ void dedupe_slices(const double* P, int nst, int K, std::vector<int>& tab, std::
 esdp_status validate_data(esdp_ctx* c, const double* lambda, const double* P, const double* pi, const double* g) {
   for (long long j = 0; j < (long long)c->T * c->K; ++j)
     if (!std::isfinite(lambda[j])) return fail(c, ESDP_E_DATA, "lambda[%lld] is not finite", j);
-  if (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
+  if (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G && g) {   // g == NULL: the payoff is not being replaced
     for (int a = 0; a < c->A; ++a)
       if (!std::isfinite(g[a])) return fail(c, ESDP_E_DATA, "g[%d] is not finite", a);
-  } else if (c->kind == ESDP_PAYOFF_TABLE) {
+  } else if (c->kind == ESDP_PAYOFF_TABLE && g) {
     for (long long j = 0; j < (long long)c->T * c->K * c->A; ++j)
       if (!std::isfinite(g[j])) return fail(c, ESDP_E_DATA, "payoff table entry %lld is not finite", j);
   }
@@ -521,7 +511,7 @@ void free_all(esdp_ctx* c) {
   for (cudaStream_t x : c->side) cudaStreamDestroy(x);
   if (c->copy) cudaStreamDestroy(c->copy);
   void* ps[] = {c->d_lambda, c->d_P, c->d_pi, c->d_g, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_segs,
-                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_df_tab, c->d_df_cnt, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
+                c->d_V, c->d_W, c->d_J, c->d_cdf, c->d_cdf1, c->d_guide, c->d_guide1, c->d_singles, c->d_live, c->d_gfit, c->d_F, c->d_stack, c->d_fb_req, c->d_fb_slot, c->d_red, c->d_pol, c->d_sim, c->d_req,
                 c->d_nv, c->d_vert, c->d_q, c->d_price};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -746,93 +736,6 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
 }
 
-// contract_mc_kernel plan (opt-in, ESDP_MC=1 in the environment; ESDP_MC_C=c sets the cluster size, the row
-// tiles padded to a multiple of it): Markov contexts with even K <= 128.  Tensor maps from
-// cuTensorMapEncodeTiled (driver entry point).  Bit-identical, but measured slower than dmma3 on cfg2
-// (warm launch 4.4-5.2 us for cluster sizes 1-13 against 3.26 us), hence off by default.
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return (PFN_cuTensorMapEncodeTiled_v12000)f;
-  }();
-  return fn;
-}
-bool encode_map3(CUtensorMap* m, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[3] = {d0, d1, d2};
-  const cuuint64_t strides[2] = {d0 * sizeof(double), d0 * d1 * sizeof(double)};
-  const cuuint32_t box[3] = {b0, b1, 1}, es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-void setup_mc(esdp_ctx* c) {
-  c->mc = 0;
-  const char* e = getenv("ESDP_MC");
-  if (!e || atoi(e) == 0 || c->rank1 || (c->K & 1) || c->K > kMcKC * kMcMaxCh || c->T < 2 || c->k_cnt < 8 ||
-      (c->flags & (ESDP_NO_DMMA | ESDP_DMMA_L2)))
-    return;
-  const int nrb0 = (c->k_cnt + kMcRB - 1) / kMcRB;
-  const char* ec = getenv("ESDP_MC_C");
-  const int csz = std::min(nrb0, ec ? std::max(1, atoi(ec)) : nrb0);   // cluster size (row tiles sharing a V tile)
-  const int nrb = (nrb0 + csz - 1) / csz * csz;                         // padded: idle CTAs only receive
-  if (csz > 16) return;
-  const int K = c->K, Kp = (K + 3) & ~3;
-  const uint64_t nbuf = keep(c) ? (uint64_t)c->T : 2;
-  for (int j = 0; j < 2; ++j)
-    if (!encode_map3(&c->mapP[j], c->slot[j].P, (uint64_t)K, (uint64_t)K, (uint64_t)(c->T - 1), (uint32_t)mc_stride_a(Kp),
-                     kMcRB))
-      return;
-  if (!encode_map3(&c->mapV, c->d_V, (uint64_t)c->ld, (uint64_t)c->Kp, nbuf, kMcSB, kMcKC)) return;
-  const size_t sm = mc_smem_bytes(K);
-  if (cudaFuncSetAttribute(contract_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
-      (csz > 8 && cudaFuncSetAttribute(contract_mc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
-    cudaGetLastError();
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nrb * ((c->S + kMcCB - 1) / kMcCB)));
-  cfg.blockDim = dim3(kMcThreads);
-  cfg.dynamicSmemBytes = sm;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)csz; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, contract_mc_kernel, &cfg) != cudaSuccess || ncl < 1) {
-    cudaGetLastError();
-    return;
-  }
-  c->mc = 1;
-  c->mc_nrb = nrb;
-  c->mc_c = csz;
-}
-cudaError_t launch_contract_mc(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
-  const int sl = c->d_P == c->slot[1].P ? 1 : 0;
-  const int nrb = c->mc_nrb;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nrb * ((c->S + kMcCB - 1) / kMcCB)));
-  cfg.blockDim = dim3(kMcThreads);
-  cfg.dynamicSmemBytes = mc_smem_bytes(c->K);
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)c->mc_c; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 2 : 1;
-  const int vt = keep(c) ? t : (t & 1);   // V_{t+1}: buffer t (keep) or (t+1-1) & 1
-  return cudaLaunchKernelEx(&cfg, contract_mc_kernel, c->mapP[sl], c->mapV, W_of(c, t), c->k_cnt, c->K, c->S, c->ld, nrb,
-                            c->mc_c, t - 1, c->k_lo, vt);
-}
-
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
 cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int K = c->K, S = c->S;
@@ -841,11 +744,10 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   // rank-1 (the paper's Alg. 1 GEMV W = pi_{t+1}^T V_{t+1}): one A row of the 8-row DMMA tile is live; the
   // K/4-long DMMA chain per column replaces a K-long DFMA chain (same canonical order, same bits)
-  if (rows == 1 && !(K & 1) && !(c->flags & (ESDP_NO_DMMA | ESDP_DMMA_L2)) && use_dmma3(8, S, K))
+  if (rows == 1 && !(K & 1) && !(c->flags & ESDP_NO_DMMA) && use_dmma3(8, S, K))
     return launch_dmma3(1, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl);
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
-    if (c->mc) return launch_contract_mc(c, t, s, pdl);
-    if (const int d3 = (c->flags & ESDP_DMMA_L2) ? 0 : use_dmma3(rows, S, K))
+    if (const int d3 = use_dmma3(rows, S, K))
       return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl);
     if (c->dmma2) {
       if (K > 128) {   // large K: taller tiles (fewer re-reads of the V column block)
@@ -858,10 +760,7 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
       return launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, pdl,
                     Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
     }
-    const int nct = (S + 15) / 16, ntiles = ((rows + 7) / 8) * nct;
-    return launch(contract_dmma_kernel, dim3((ntiles + kDmmaWarps - 1) / kDmmaWarps), dim3(kDmmaWarps * 32), 0, s, pdl, Pt,
-                  (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, nct);
-  }
+  }   // else (K too large for any staged DMMA tile): DFMA below
   dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
   return launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, Pt, (const double*)V_of(c, t + 1),
                 W_of(c, t), rows, K, S, c->ld);
@@ -920,103 +819,6 @@ cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
                 (const double*)c->d_pi, c->K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
 }
 
-PersistParams persist_params(esdp_ctx* c) {
-  PersistParams pp;
-  pp.sp = stencil_params(c);
-  pp.wp = win_params(c);
-  pp.use_window = c->use_window;
-  pp.T = c->T; pp.K = c->K; pp.S = c->S; pp.A = c->A; pp.ld = c->ld; pp.rows = (int)w_rows(c);
-  pp.rank1 = c->rank1; pp.kind = c->kind; pp.keep = keep(c) ? 1 : 0;
-  pp.P = c->d_P; pp.pi = c->d_pi; pp.lambda = c->d_lambda; pp.g = c->d_g;
-  pp.V = c->d_V; pp.W = c->d_W; pp.pol = c->d_pol; pp.J = c->d_J;
-  pp.f0 = c->f0; pp.on_grid = c->on_grid; pp.w0 = c->w0;
-  pp.Kp = c->Kp;
-  pp.ntc = c->df_ntc; pp.ecw = c->df_ecw; pp.ncb = c->df_ncb; pp.nrg = c->df_nrg; pp.period = c->df_period;
-  pp.ntasks = c->df_ntasks;
-  pp.pat = c->d_df_tab;
-  pp.pos_s = pp.pat + c->df_period;
-  pp.pos_e = pp.pos_s + (size_t)c->K * c->df_ntc;
-  pp.e_need = pp.pos_e + (size_t)c->df_nrg * c->df_ncb;
-  pp.e_dep = pp.e_need + c->df_ntc;
-  pp.e_feed = pp.e_dep + 2 * c->df_ncb;
-  pp.c_feeds = pp.e_feed + 2 * c->df_ncb;
-  pp.ctl = c->d_df_cnt;
-  pp.queue = pp.ctl + 4;
-  pp.s_done = pp.queue + c->df_ntasks;
-  pp.e_cnt = pp.s_done + (size_t)c->T * c->df_ntc;
-  pp.e_ready = pp.e_cnt + (size_t)c->T * c->df_nrg * c->df_ntc;
-  return pp;
-}
-
-cudaError_t launch_persistent(esdp_ctx* c, cudaStream_t s) {
-  PersistParams pp = persist_params(c);
-  cudaError_t e = cudaMemsetAsync(c->d_df_cnt, 0, c->df_cnt_n * sizeof(int), s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(c->d_df_cnt, c->d_df_tab + c->df_init_off, (4 + (size_t)c->df_n0) * sizeof(int),
-                      cudaMemcpyDeviceToDevice, s);
-  if (e != cudaSuccess) return e;
-  backward_persistent_kernel<<<c->persist_grid, kPersistThreads, c->persist_smem, s>>>(pp);
-  return cudaGetLastError();
-}
-
-// Task schedule of the dataflow kernel (persistent.cuh): dependency ranges and one stage's ticket
-// pattern -- the S tasks of tile c (all rows), then every not yet issued E task of the next stage whose
-// input tiles are all issued by then.  Returns the host tables laid out as d_df_tab expects.
-std::vector<int> build_schedule(esdp_ctx* c) {
-  const int S = c->S, K = c->K;
-  const int ntc = (S + kWinTile - 1) / kWinTile;
-  const int ecw = c->rank1 ? kPersistThreads : kDfCols;
-  const int ncb = (S + ecw - 1) / ecw;
-  const int nrg = c->rank1 ? 1 : (K + kDfRows - 1) / kDfRows;
-  std::vector<int> need(ntc, 0), dep(2 * ncb), feed(2 * ncb);
-  for (int cb = 0; cb < ncb; ++cb) {
-    const int x0 = cb * ecw, x1 = std::min(S, x0 + ecw) - 1;    // columns of the block
-    int flo = ntc, fhi = -1;                                      // tiles whose W reads cover them
-    for (int tc = 0; tc < ntc; ++tc) {
-      const int r0 = std::max(0, tc * kWinTile + c->o_min - 1);
-      const int r1 = std::min(S - 1, tc * kWinTile + kWinTile + c->o_max + 1);
-      if (r0 <= x1 && x0 <= r1) { flo = std::min(flo, tc); fhi = tc; ++need[tc]; }
-    }
-    feed[2 * cb] = flo; feed[2 * cb + 1] = fhi;
-    int dlo = x0 / kWinTile, dhi = x1 / kWinTile;                // V_{t+1} tiles it reads
-    if (!keep(c)) { dlo = std::min(dlo, flo); dhi = std::max(dhi, fhi); }   // one W buffer: wait for its readers
-    dep[2 * cb] = dlo; dep[2 * cb + 1] = dhi;
-  }
-  std::vector<int> pat, pos_s((size_t)K * ntc), pos_e((size_t)nrg * ncb), cfeeds(2 * ntc);
-  std::vector<char> issued(ncb, 0);
-  for (int tc = 0; tc < ntc; ++tc) {
-    for (int k = 0; k < K; ++k) { pos_s[(size_t)k * ntc + tc] = (int)pat.size(); pat.push_back(kTaskS | (k << 1) | (tc << 16)); }
-    for (int cb = 0; cb < ncb; ++cb)
-      if (!issued[cb] && dep[2 * cb + 1] <= tc) {
-        issued[cb] = 1;
-        for (int rg = 0; rg < nrg; ++rg) { pos_e[(size_t)rg * ncb + cb] = (int)pat.size(); pat.push_back(kTaskE | (rg << 1) | (cb << 16)); }
-      }
-    int lo = ncb, hi = -1;   // E blocks whose input tiles include tc (a contiguous range: dep is monotone)
-    for (int cb = 0; cb < ncb; ++cb)
-      if (dep[2 * cb] <= tc && tc <= dep[2 * cb + 1]) { lo = std::min(lo, cb); hi = cb; }
-    cfeeds[2 * tc] = lo; cfeeds[2 * tc + 1] = hi;
-  }
-  const int period = (int)pat.size();
-  c->df_ntc = ntc; c->df_ecw = ecw; c->df_ncb = ncb; c->df_nrg = nrg; c->df_period = period;
-  c->df_ntasks = c->T * K * ntc + (c->T - 1) * nrg * ncb + 1;
-  c->df_n0 = K * ntc;                                           // the S tasks of stage T: ready at launch
-  // counter block: ctl[4] | queue[ntasks] | s_done[T][ntc] | e_cnt[T][nrg][ntc] | e_ready[T][ncb]
-  c->df_cnt_n = 4 + (size_t)c->df_ntasks + (size_t)c->T * ntc + (size_t)c->T * nrg * ntc + (size_t)c->T * ncb;
-  // host tables: pattern | pos_s | pos_e | e_need | e_dep | e_feed | c_feeds | init (ctl + first queue slots)
-  std::vector<int> tab = pat;
-  tab.insert(tab.end(), pos_s.begin(), pos_s.end());
-  tab.insert(tab.end(), pos_e.begin(), pos_e.end());
-  tab.insert(tab.end(), need.begin(), need.end());
-  tab.insert(tab.end(), dep.begin(), dep.end());
-  tab.insert(tab.end(), feed.begin(), feed.end());
-  tab.insert(tab.end(), cfeeds.begin(), cfeeds.end());
-  c->df_init_off = tab.size();
-  tab.push_back(0); tab.push_back(c->df_n0); tab.push_back(0); tab.push_back(0);   // head, tail, stage-1 tiles
-  for (int tc = 0; tc < ntc; ++tc)
-    for (int k = 0; k < K; ++k) tab.push_back(pos_s[(size_t)k * ntc + tc] + 1);   // period 0 = stage T
-  return tab;
-}
-
 cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const int32_t* slot_dev, int64_t nout, int32_t cap,
                         int32_t* nvert_dev, int16_t* vert_dev, double* q_dev, double* price_dev, cudaStream_t s) {
   BidParams bp{c->d_W, c->d_act, c->d_w, c->d_omw, c->d_off, c->d_g, c->T, c->K, c->S, c->A, c->rank1, c->kind, c->ld,
@@ -1054,22 +856,6 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   auto mark = [&](int t, int j) {
     return sampled(t) ? cudaEventRecordWithFlags(c->ev[(size_t)(t - 1) * 4 + j], s, cudaEventRecordExternal) : cudaSuccess;
   };
-  if (c->persist) {   // one dataflow kernel; bid curves (if any) after it, on the same stream
-    CUDA_OR_FAIL(c, cudaMemsetAsync(W_of(c, T), 0, w_rows(c) * c->ld * sizeof(double), s));  // W_T = 0
-    CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, c->ev_head, cudaEventWaitExternal));
-    for (cudaEvent_t e : c->chunk_ev) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, e, cudaEventWaitExternal));
-    if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[0], s, cudaEventRecordExternal));
-    CUDA_OR_FAIL(c, launch_persistent(c, s));
-    if (prof) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev[1], s, cudaEventRecordExternal));
-    ++n;
-    if (c->fb_n > 0) {
-      CUDA_OR_FAIL(c, launch_bids(c, c->fb_n, c->d_fb_req, c->d_fb_slot, c->fb_n, c->fb_cap, c->fb_nvert, c->fb_vert,
-                                  c->fb_q, c->fb_price, s));
-      ++n;
-    }
-    c->launches = n;
-    return ESDP_OK;
-  }
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   bool forked = false;
   std::vector<char> side_used(c->side.size(), 0);
@@ -1114,16 +900,29 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     CUDA_OR_FAIL(c, mark(t, 3));
     after_kernel = !sampled(t);
     ++n;
-    if (c->comm) {  // V_t and pol_t rows of every rank to every rank (in place, blocks of kmax rows)
+    if (c->comm) {  // V_t rows of every rank to every rank (in place, blocks of kmax rows): the next stage's
+                    // contraction needs all of V_t; the policy stays local until the backward is done
       double* Vt = V_of(c, t);
-      int16_t* pt = c->d_pol + (size_t)(t - 1) * c->Kp * c->S;
-      const size_t vcount = (size_t)c->kmax * c->ld, pcount = (size_t)c->kmax * c->S;
-      ncclResult_t r1 = ncclAllGather(Vt + c->rank * vcount, Vt, vcount, ncclDouble, c->comm, s);
-      ncclResult_t r2 = ncclAllGather(pt + c->rank * pcount, pt, pcount * sizeof(int16_t), ncclUint8, c->comm, s);
-      if (r1 != ncclSuccess || r2 != ncclSuccess)
-        return fail(c, ESDP_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+      const size_t vcount = (size_t)c->kmax * c->ld;
+      ncclResult_t r = ncclGroupStart();
+      if (r == ncclSuccess) r = ncclAllGather(Vt + c->rank * vcount, Vt, vcount, ncclDouble, c->comm, s);
+      const ncclResult_t r2 = ncclGroupEnd();
+      if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(c, ESDP_E_NCCL, "ncclAllGather(V_%d): %s", t, ncclGetErrorString(r != ncclSuccess ? r : r2));
       after_kernel = false;
     }
+  }
+  if (c->comm) {   // every stage's policy rows to every rank, once, off the stage chain (one NCCL group)
+    const size_t pcount = (size_t)c->kmax * c->S;
+    ncclResult_t r = ncclGroupStart();
+    for (int t = 1; t <= T && r == ncclSuccess; ++t) {
+      int16_t* pt = c->d_pol + (size_t)(t - 1) * c->Kp * c->S;
+      r = ncclAllGather(pt + c->rank * pcount, pt, pcount * sizeof(int16_t), ncclUint8, c->comm, s);
+    }
+    const ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(c, ESDP_E_NCCL, "ncclAllGather(pol): %s", ncclGetErrorString(r != ncclSuccess ? r : r2));
+    after_kernel = false;
   }
   CUDA_OR_FAIL(c, launch_objective(c, s, pdl && after_kernel));
   ++n;
@@ -1158,6 +957,96 @@ esdp_status capture_graph(esdp_ctx* c) {
   return ESDP_OK;
 }
 
+// Wait for stream s.  Multi-GPU contexts poll the communicator while they wait: an asynchronous NCCL
+// error, or no completion within ESDP_NCCL_TIMEOUT_S seconds (default 120; a dead or hung peer), aborts
+// the communicator and returns ESDP_E_NCCL instead of blocking forever.
+template <class Query>
+esdp_status wait_polled(esdp_ctx* c, Query query) {
+  static const double tmo = [] { const char* e = getenv("ESDP_NCCL_TIMEOUT_S"); return e ? atof(e) : 120.0; }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = query();
+    if (q == cudaSuccess) return ESDP_OK;
+    if (q != cudaErrorNotReady) return fail(c, ESDP_E_CUDA, "wait: %s", cudaGetErrorString(q));
+    ncclResult_t ae = ncclSuccess;
+    const ncclResult_t qr = ncclCommGetAsyncError(c->comm, &ae);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (qr != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress) || dt > tmo) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      c->solved = false;
+      return fail(c, ESDP_E_NCCL, "%s; communicator aborted",
+                  dt > tmo ? "timeout waiting for the multi-GPU backward" : ncclGetErrorString(qr != ncclSuccess ? qr : ae));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+esdp_status wait_stream(esdp_ctx* c, cudaStream_t s) {
+  if (!c->comm) {
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
+    return ESDP_OK;
+  }
+  return wait_polled(c, [&] { return cudaStreamQuery(s); });
+}
+esdp_status wait_event(esdp_ctx* c, cudaEvent_t e) {
+  if (!c->comm) {
+    CUDA_OR_FAIL(c, cudaEventSynchronize(e));
+    return ESDP_OK;
+  }
+  return wait_polled(c, [&] { return cudaEventQuery(e); });
+}
+
+// DMMA bit-exactness probe (kernels.cuh dmma_probe_kernel), once per process and device: random, wide-
+// range and cancelling operands; returns the number of outputs whose DMMA chain differs from the fma chain
+// (-1 if the probe could not run).  ESDP_DMMA_PROBE_FAIL=1 in the environment reports a mismatch (tests).
+int dmma_probe_mismatches() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
+  std::lock_guard<std::mutex> lk(mu);
+  const char* f = getenv("ESDP_DMMA_PROBE_FAIL");   // read per call: tests force the fallback mid-process
+  const int forced = (f && atoi(f)) ? 1 : 0;
+  auto it = done.find(dev);
+  if (it != done.end()) return it->second < 0 ? it->second : it->second + forced;
+  constexpr int ntiles = 64, na = 8 * 4 * kProbeQ, nb = 4 * kProbeQ * 8;
+  std::vector<double> A((size_t)ntiles * na), B((size_t)ntiles * nb);
+  uint64_t st = 0x2511156290ull;
+  auto rnd = [&] { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return st; };
+  auto val = [&](uint64_t r) {
+    const double m = 1.0 + (double)(r >> 12) * 0x1p-52;                 // [1, 2)
+    const int e = (int)((r >> 4) & 63) - 32;                             // 2^-32 .. 2^31
+    return ((r & 1) ? -1.0 : 1.0) * std::ldexp(m, e);
+  };
+  for (int t = 0; t < ntiles; ++t) {
+    for (int j = 0; j < na; ++j) A[(size_t)t * na + j] = val(rnd());
+    for (int j = 0; j < nb; ++j) B[(size_t)t * nb + j] = val(rnd());
+    if (t % 2) {   // cancelling pairs: the product of k' = 2m+1 undoes that of k' = 2m (exactly or nearly)
+      for (int g = 0; g < 8; ++g)
+        for (int k = 0; k + 1 < 4 * kProbeQ; k += 2)
+          A[(size_t)t * na + g * 4 * kProbeQ + k + 1] = -A[(size_t)t * na + g * 4 * kProbeQ + k] * (1.0 + ((t / 2) % 3) * 0x1p-40);
+      for (int k = 0; k + 1 < 4 * kProbeQ; k += 2)
+        for (int c = 0; c < 8; ++c) B[(size_t)t * nb + (k + 1) * 8 + c] = B[(size_t)t * nb + k * 8 + c];
+    }
+  }
+  double *dA = nullptr, *dB = nullptr;
+  unsigned* dm = nullptr;
+  unsigned bad = 0;
+  int res = -1;
+  if (cudaMalloc(&dA, A.size() * 8) == cudaSuccess && cudaMalloc(&dB, B.size() * 8) == cudaSuccess &&
+      cudaMalloc(&dm, sizeof(unsigned)) == cudaSuccess &&
+      cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+      cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+      cudaMemset(dm, 0, sizeof(unsigned)) == cudaSuccess) {
+    dmma_probe_kernel<<<ntiles / 4, 128>>>(dA, dB, ntiles, dm);
+    if (cudaMemcpy(&bad, dm, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess) res = (int)bad;
+  }
+  cudaFree(dA); cudaFree(dB); cudaFree(dm);
+  cudaGetLastError();
+  done[dev] = res;
+  return res < 0 ? res : res + forced;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1174,6 +1063,18 @@ esdp_status esdp_partition(int32_t K, int32_t world, int32_t rank, int32_t* k_lo
   if (k_lo) *k_lo = lo;
   if (k_cnt) *k_cnt = hi - lo;
   if (kmax) *kmax = m;
+  return ESDP_OK;
+}
+
+esdp_status esdp_dist_info(const esdp_ctx* c, int32_t* world, int32_t* rank, int32_t* nccl_nranks) {
+  if (!c) return ESDP_E_STATE;
+  if (world) *world = c->world;
+  if (rank) *rank = c->rank;
+  if (nccl_nranks) {
+    int n = 0;
+    if (c->comm && ncclCommCount(c->comm, &n) != ncclSuccess) n = -1;
+    *nccl_nranks = n;
+  }
   return ESDP_OK;
 }
 
@@ -1213,7 +1114,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (pr->payoff_kind < 0 || pr->payoff_kind > 2) return fail(nullptr, ESDP_E_CONFIG, "unknown payoff kind");
   if (pr->payoff_kind != ESDP_PAYOFF_LINEAR && !pr->g) return fail(nullptr, ESDP_E_CONFIG, "payoff needs g");
   if (!pr->lambda || !pr->pi) return fail(nullptr, ESDP_E_CONFIG, "lambda and pi are required");
-  if (pr->T > 1 && pr->P == nullptr && false) return ESDP_E_CONFIG;
+  if (pr->flags & ~(uint32_t)ESDP_FLAGS_ALL) return fail(nullptr, ESDP_E_CONFIG, "unknown flag bits 0x%x", pr->flags & ~(uint32_t)ESDP_FLAGS_ALL);
 
   esdp_ctx* c = new esdp_ctx();
   c->T = pr->T; c->K = pr->K; c->S = (int)rs + 1; c->ld = (c->S + 3) & ~3;
@@ -1395,9 +1296,13 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     }
   }
   if (contract_smem_bytes(K) > 227 * 1024) { fail(c, ESDP_E_CONFIG, "K too large for the contraction tile"); return bail(ESDP_E_CONFIG); }
+  if (!(c->flags & ESDP_NO_DMMA) && dmma_probe_mismatches() != 0) {   // guard: DFMA unless DMMA == fma chain
+    c->flags |= ESDP_NO_DMMA;
+    c->dmma_probe_failed = 1;
+  }
   {
     const size_t sm2 = K > 128 ? contract_dmma2_smem(K, kDRbig, kDCbig) : contract_dmma2_smem(K);
-    c->dmma2 = !(c->flags & ESDP_DMMA_L2) && sm2 <= 200 * 1024;
+    c->dmma2 = sm2 <= 200 * 1024;
     if (c->dmma2 && sm2 > 48 * 1024 &&
         (K > 128 ? cudaFuncSetAttribute(contract_dmma2_kernel<kDRbig, kDCbig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)
                  : cudaFuncSetAttribute(contract_dmma2_kernel<kDR, kDC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
@@ -1407,31 +1312,6 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
-  // persistent dataflow path (single GPU; Markov uses the DMMA expectation; K < 2^15)
-  if ((c->flags & ESDP_PERSIST) && !nccl_id && K < 32768 && kWinThreads == kPersistThreads && (c->rank1 || !(c->flags & ESDP_NO_DMMA))) {
-    int dev = 0, nsm = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    size_t sm = std::max(c->use_window ? c->window_smem : c->stencil_smem, 2 * sizeof(double) * (size_t)K);
-    sm = std::max(sm, c->stencil_smem);
-    if (!c->rank1) sm = std::max(sm, contract_dmma2_smem(K, kDfDR, kDfDC));
-    if (sm <= 200 * 1024 &&
-        cudaFuncSetAttribute(backward_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_persistent_kernel, kPersistThreads, sm) == cudaSuccess &&
-        per_sm >= 1) {
-      std::vector<int> tab = build_schedule(c);
-      TRY(dev_alloc(c, &c->d_df_tab, tab.size()));
-      TRY(dev_alloc(c, &c->d_df_cnt, c->df_cnt_n));
-      if (cudaMemcpy(c->d_df_tab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
-        fail(c, ESDP_E_CUDA, "upload of the task schedule failed");
-        return bail(ESDP_E_CUDA);
-      }
-      c->persist = 1;
-      c->persist_grid = per_sm * nsm;
-      c->persist_smem = sm;
-    }
-    cudaGetLastError();
-  }
   if (c->flags & ESDP_PROFILE) {
     c->prof_stride = std::max(1, c->T / 16);
     c->ev.resize((size_t)c->T * 4);
@@ -1451,7 +1331,6 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   c->fb_ev.resize((size_t)c->T + 1);
   for (auto& ev : c->fb_ev)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { fail(c, ESDP_E_CUDA, "event"); return bail(ESDP_E_CUDA); }
-  if (!c->persist) setup_mc(c);
   TRY(capture_graph(c));
 #undef TRY
   *out = c;
@@ -1529,6 +1408,7 @@ esdp_status esdp_backward_async(esdp_ctx* c, void* stream) {
 
 esdp_status esdp_objective(esdp_ctx* c, double* J) {
   if (!c || !c->solved) return c ? fail(c, ESDP_E_STATE, "no backward pass has run") : ESDP_E_STATE;
+  { const esdp_status w = wait_event(c, c->slot[c->active].use_ev); if (w != ESDP_OK) return w; }   // the last use, any stream
   CUDA_OR_FAIL(c, cudaMemcpy(J, c->d_J, sizeof(double), cudaMemcpyDeviceToHost));
   return ESDP_OK;
 }
@@ -1546,7 +1426,8 @@ esdp_status esdp_backward(esdp_ctx* c, void* stream, double* J) {
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   esdp_status st = esdp_backward_async(c, s);
   if (st != ESDP_OK) return st;
-  CUDA_OR_FAIL(c, cudaStreamSynchronize(s));
+  st = wait_stream(c, s);
+  if (st != ESDP_OK) return st;
   if (J) CUDA_OR_FAIL(c, cudaMemcpy(J, c->d_J, sizeof(double), cudaMemcpyDeviceToHost));
   return ESDP_OK;
 }
@@ -1845,7 +1726,8 @@ esdp_status esdp_window_fallbacks(esdp_ctx* c, int64_t* count) {
 
 esdp_status esdp_stencil_kind(const esdp_ctx* c, int32_t* kind) {
   if (!c || !kind) return ESDP_E_STATE;
-  *kind = c->use_window + 2 * c->persist;
+  // bit 0: window stencil; bit 1: expectation on the FP64 tensor cores (DMMA); bit 2: the DMMA probe failed
+  *kind = c->use_window | ((c->flags & ESDP_NO_DMMA) ? 0 : 2) | (c->dmma_probe_failed ? 4 : 0);
   return ESDP_OK;
 }
 
@@ -1860,13 +1742,6 @@ esdp_status esdp_kernel_times(const esdp_ctx* cc, double* contract_ms, double* s
   if (!c) return ESDP_E_STATE;
   if (c->ev.empty()) return fail(c, ESDP_E_STATE, "context was created without ESDP_PROFILE");
   if (!c->solved) return fail(c, ESDP_E_STATE, "no backward pass has run");
-  if (c->persist) {   // one kernel: its whole time per stage is reported as the stencil phase
-    float ms = 0.f;
-    CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    if (contract_ms) *contract_ms = 0.0;
-    if (stencil_ms) *stencil_ms = ms / c->T;
-    return ESDP_OK;
-  }
   double ct = 0.0, st = 0.0;
   int nc = 0, ns = 0;
   for (int t = 1; t <= c->T; ++t) {
@@ -1952,6 +1827,8 @@ struct esdp_batch {
   int* d_widx = nullptr;                                   // window-plan instances
   int* d_bidx = nullptr;                                   // brute-force instances
   int nwin = 0, nbrute = 0;
+  int dmma = 1;   // expectation on the FP64 tensor cores (0: the DMMA probe failed -> DFMA)
+  size_t ntab_cap = 0;   // sampling-table rows the guide allocation holds (distinct P_t slices x K)
   size_t win_smem = 0, brute_smem = 0;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -1997,54 +1874,66 @@ void batch_free(esdp_batch* b) {
 
 // The batch's backward pass on stream s: per stage one expectation over [K] x [n ld], one window launch
 // over every window-plan instance, one brute-force launch per other instance; then every J.
-esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
+// One batch kernel of stage t: what = 0 the contraction W_t = P_t V_{t+1} over all instances' columns,
+// 1 the window-plan instances' stencil, 2 the brute-force instances' stencil.
+cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, bool pdl) {
   const int T = b->T, K = b->K, S = b->S, n = b->n;
+  const size_t NL = (size_t)n * b->ld;                  // row stride of V and W
+  const int rows = b->rank1 ? 1 : K;
+  double* V_t = b->d_V + (size_t)((t - 1) & 1) * K * NL;
+  const double* V_n = b->d_V + (size_t)(t & 1) * K * NL;   // V_{t+1}
+  if (what == 0) {
+    const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
+    if (const int d3 = (b->rank1 || !b->dmma) ? 0 : use_dmma3(rows, (int64_t)NL, K))
+      return launch_dmma3(d3, Pt, V_n, b->d_W, rows, K, (int)NL, (int)NL, s, pdl);
+    if (b->dmma && !b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
+      const int ncb = (int)((NL + kDCbig * 16 - 1) / (kDCbig * 16)), nrb = (K + kDRbig * 8 - 1) / (kDRbig * 8);
+      return launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
+                    contract_dmma2_smem(K, kDRbig, kDCbig), s, pdl, Pt, V_n, b->d_W, rows, K, (int)NL, (int)NL, ncb);
+    }
+    if (b->dmma && !b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
+      const int ncb = (int)((NL + kDC * 16 - 1) / (kDC * 16)), nrb = (K + kDR * 8 - 1) / (kDR * 8);
+      return launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, pdl,
+                    Pt, V_n, b->d_W, rows, K, (int)NL, (int)NL, ncb);
+    }
+    dim3 grid((unsigned)((NL + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
+    return launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, Pt, V_n, b->d_W, rows, K, (int)NL,
+                  (int)NL);
+  }
+  const double* lam = b->d_lambda + (size_t)(t - 1) * K;
+  const size_t pol_inst = (size_t)T * K * S, pol_stage = (size_t)(t - 1) * K * S;
+  if (what == 1)
+    return launch(window_batch_kernel, dim3((S + kWinTile - 1) / kWinTile, K, b->nwin), dim3(kWinThreads), b->win_smem, s,
+                  pdl, (const BatchInst*)b->d_bi, (const int*)b->d_widx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
+                  pol_stage, lam, b->ld, (int)NL, b->rank1);
+  return launch(stencil_batch_kernel, dim3((S + kTile - 1) / kTile, K, b->nbrute), dim3(kStencilWarps * 32), b->brute_smem,
+                s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_bidx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
+                pol_stage, lam, b->ld, (int)NL, b->rank1);
+}
+
+esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
+  const int T = b->T, K = b->K, n = b->n;
   const size_t NL = (size_t)n * b->ld;                  // row stride of V and W
   const int rows = b->rank1 ? 1 : K;
   int64_t launches = 0;
   bool after_kernel = false;
-  auto V_at = [&](int t) { return b->d_V + (size_t)((t - 1) & 1) * K * NL; };
   for (int t = T; t >= 1; --t) {
     if (t == T) {
       BCUDA(b, cudaMemsetAsync(b->d_W, 0, rows * NL * sizeof(double), s));   // W_T = 0
       after_kernel = false;
     } else {
-      const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
-      cudaError_t e;
-      if (const int d3 = b->rank1 ? 0 : use_dmma3(rows, (int64_t)NL, K)) {
-        e = launch_dmma3(d3, Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, s, after_kernel);
-      } else if (!b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
-        const int ncb = (int)((NL + kDCbig * 16 - 1) / (kDCbig * 16)), nrb = (K + kDRbig * 8 - 1) / (kDRbig * 8);
-        e = launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
-                   contract_dmma2_smem(K, kDRbig, kDCbig), s, after_kernel, Pt, (const double*)V_at(t + 1), b->d_W, rows,
-                   K, (int)NL, (int)NL, ncb);
-      } else if (!b->rank1 && contract_dmma2_smem(K) <= 200 * 1024) {
-        const int ncb = (int)((NL + kDC * 16 - 1) / (kDC * 16)), nrb = (K + kDR * 8 - 1) / (kDR * 8);
-        e = launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, after_kernel,
-                   Pt, (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL, ncb);
-      } else {
-        dim3 grid((unsigned)((NL + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
-        e = launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, after_kernel, Pt,
-                   (const double*)V_at(t + 1), b->d_W, rows, K, (int)NL, (int)NL);
-      }
+      const cudaError_t e = batch_stage_kernel(b, t, 0, s, after_kernel);
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch contraction: %s", cudaGetErrorString(e));
       after_kernel = true;
       ++launches;
     }
-    const double* lam = b->d_lambda + (size_t)(t - 1) * K;
-    const size_t pol_inst = (size_t)T * K * S, pol_stage = (size_t)(t - 1) * K * S;
     if (b->nwin > 0) {
-      cudaError_t e = launch(window_batch_kernel, dim3((S + kWinTile - 1) / kWinTile, K, b->nwin), dim3(kWinThreads),
-                             b->win_smem, s, after_kernel, (const BatchInst*)b->d_bi, (const int*)b->d_widx,
-                             (const double*)b->d_W, V_at(t), b->d_pol, pol_inst, pol_stage, lam, b->ld, (int)NL, b->rank1);
+      const cudaError_t e = batch_stage_kernel(b, t, 1, s, after_kernel);
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch window stencil: %s", cudaGetErrorString(e));
       ++launches;
     }
     if (b->nbrute > 0) {
-      cudaError_t e = launch(stencil_batch_kernel, dim3((S + kTile - 1) / kTile, K, b->nbrute), dim3(kStencilWarps * 32),
-                             b->brute_smem, s, after_kernel && b->nwin == 0, (const BatchInst*)b->d_bi,
-                             (const int*)b->d_bidx, (const double*)b->d_W, V_at(t), b->d_pol, pol_inst, pol_stage, lam,
-                             b->ld, (int)NL, b->rank1);
+      const cudaError_t e = batch_stage_kernel(b, t, 2, s, after_kernel && b->nwin == 0);
       if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch stencil: %s", cudaGetErrorString(e));
       ++launches;
     }
@@ -2052,7 +1941,7 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
   }
   {
     cudaError_t e = launch(objective_batch_kernel, dim3(n), dim3(128), 2 * sizeof(double) * K, s, after_kernel,
-                           (const BatchInst*)b->d_bi, (const double*)V_at(1), (const double*)b->d_pi, K, b->ld, (int)NL,
+                           (const BatchInst*)b->d_bi, (const double*)(b->d_V), (const double*)b->d_pi, K, b->ld, (int)NL,
                            b->d_J);
     if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch objective: %s", cudaGetErrorString(e));
     ++launches;
@@ -2088,9 +1977,10 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   auto bail = [&](esdp_status st) { if (b->err.size()) g_create_error = b->err; batch_free(b); delete b; return st; };
 #define BTRY(x) do { esdp_status st_ = (x); if (st_ != ESDP_OK) return bail(st_); } while (0)
   b->n = n;
+  b->dmma = !(probs[0].flags & ESDP_NO_DMMA) && dmma_probe_mismatches() == 0;   // guard as esdp_create
   for (int m = 0; m < n; ++m) {
     esdp_problem q = probs[m];
-    q.flags &= ~(uint32_t)(ESDP_KEEP_VALUES | ESDP_PROFILE | ESDP_PERSIST);
+    q.flags &= ~(uint32_t)(ESDP_KEEP_VALUES | ESDP_PROFILE);
     esdp_ctx* c = nullptr;
     esdp_status st = create_impl(&q, 1, 0, nullptr, &c, true);
     if (st != ESDP_OK) {
@@ -2112,6 +2002,7 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   if (!b->rank1 && T > 1) dedupe_slices(p0.P, (int)T - 1, (int)K, tab, src);
   const size_t ntab_rows = b->rank1 ? T : src.size() * K;
   b->gbits = b->rank1 ? c0->g_r1 : guide_g_for(ntab_rows, c0->guide_cap, c0->g_max);
+  b->ntab_cap = std::max<size_t>(ntab_rows, 1);
   BTRY(balloc(b, &b->d_lambda, T * K));
   BTRY(balloc(b, &b->d_P, b->rank1 ? 1 : (T - 1) * K * K));
   BTRY(balloc(b, &b->d_pi, b->rank1 ? T * K : K));
@@ -2277,6 +2168,74 @@ esdp_status esdp_batch_simulate_dev(esdp_batch* b, int64_t n_paths, uint64_t see
   return ESDP_OK;
 }
 
+esdp_status esdp_batch_load_async(esdp_batch* b, const double* lambda, const double* P, const double* pi, void* stream) {
+  if (!b || !lambda || !pi || (!b->rank1 && b->T > 1 && !P)) return b ? bfail(b, ESDP_E_STATE, "null input") : ESDP_E_STATE;
+  esdp_ctx* c0 = b->inst[0];
+  const esdp_status st = validate_data(c0, lambda, P, pi, nullptr);
+  if (st != ESDP_OK) return bfail(b, st, "%s", c0->err.c_str());
+  const size_t T = b->T, K = b->K;
+  std::vector<int> tab, src;
+  if (!b->rank1 && T > 1) dedupe_slices(P, (int)T - 1, (int)K, tab, src);
+  const size_t rows = b->rank1 ? T : src.size() * K;
+  if (rows > b->ntab_cap)
+    return bfail(b, ESDP_E_STATE, "the new P has %zu distinct stage slices; the batch was built for %zu", src.size(), b->ntab_cap / K);
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  BCUDA(b, cudaMemcpyAsync(b->d_lambda, lambda, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (b->rank1) {
+    BCUDA(b, cudaMemcpyAsync(b->d_pi, pi, T * K * sizeof(double), cudaMemcpyHostToDevice, s));
+    launch_cdf(b->d_pi, nullptr, (int64_t)T, (int)K, b->gbits, b->d_cdf, b->d_guide, s);
+  } else {
+    BCUDA(b, cudaMemcpyAsync(b->d_pi, pi, K * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (T > 1) {
+      BCUDA(b, cudaMemcpyAsync(b->d_P, P, (T - 1) * K * K * sizeof(double), cudaMemcpyHostToDevice, s));
+      BCUDA(b, cudaMemcpyAsync(b->d_tab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      BCUDA(b, cudaMemcpyAsync(b->d_src, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      launch_cdf(b->d_P, b->d_src, (int64_t)rows, (int)K, b->gbits, b->d_cdf, b->d_guide, s);
+    }
+  }
+  launch_cdf(b->d_pi, nullptr, 1, (int)K, b->g_max, b->d_cdf1, b->d_guide1, s);
+  BCUDA(b, cudaGetLastError());
+  return ESDP_OK;   // tab / src are pageable: cudaMemcpyAsync has staged them before returning
+}
+
+esdp_status esdp_batch_kernel_time(esdp_batch* b, int32_t what, int32_t reps, double* us_per_launch) {
+  // Diagnostic: warm back-to-back launches of stage T-1's expectation (what = 0), window stencil (1) or
+  // brute-force stencil (2) of the batch, captured in a graph, CUDA events; needs a completed backward (its buffers are the inputs)
+  if (!b || !us_per_launch || reps < 1) return ESDP_E_STATE;
+  if (!b->solved) return bfail(b, ESDP_E_STATE, "no backward pass has run");
+  if (b->T < 2) return bfail(b, ESDP_E_STATE, "needs T >= 2");
+  cudaStream_t s = b->stream;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  BCUDA(b, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int r = 0; r < reps; ++r) {
+    if ((what == 1 && b->nwin == 0) || (what == 2 && b->nbrute == 0) || what < 0 || what > 2) {
+      cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g);
+      return bfail(b, ESDP_E_STATE, "no kernel of kind %d in this batch", what);
+    }
+    const cudaError_t le = batch_stage_kernel(b, b->T - 1, what, s, false);
+    if (le != cudaSuccess) { cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g); return bfail(b, ESDP_E_CUDA, "%s", cudaGetErrorString(le)); }
+  }
+  cudaError_t ce = cudaStreamEndCapture(s, &g);
+  if (ce == cudaSuccess) ce = cudaGraphInstantiate(&ge, g, 0);
+  if (g) cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return bfail(b, ESDP_E_CUDA, "kernel-time graph: %s", cudaGetErrorString(ce));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(e0, s);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(e1, s);
+  ce = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  if (ce != cudaSuccess) return bfail(b, ESDP_E_CUDA, "kernel-time run: %s", cudaGetErrorString(ce));
+  *us_per_launch = 1e3 * ms / reps;
+  return ESDP_OK;
+}
+
 esdp_status esdp_batch_launch_count(const esdp_batch* b, int64_t* n) {
   if (!b || !n) return ESDP_E_STATE;
   *n = b->launches;
@@ -2299,11 +2258,5 @@ const char* esdp_batch_last_error(const esdp_batch* b) { return b ? b->err.c_str
 // diagnostic (make -B EXTRA=-DESDP_WIN_TRACE): per-block phase marks of the last window-stencil launch
 extern "C" esdp_status esdp_win_trace(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, esdp::g_ktrace, sizeof(esdp::g_ktrace)) == cudaSuccess ? ESDP_OK : ESDP_E_CUDA;
-}
-#endif
-#ifdef ESDP_DF_TRACE
-extern "C" int esdp_df_trace(unsigned long long* out, int n) {   // diagnostic build only
-  if (n > esdp::kTraceMax) n = esdp::kTraceMax;
-  return (int)cudaMemcpyFromSymbol(out, esdp::g_df_trace, (size_t)n * 32);
 }
 #endif

@@ -22,15 +22,8 @@ __host__ __device__ __forceinline__ int skew(int j) { return j + (j >> 3); }  //
 // Programmatic dependent launch (PDL): a kernel lets its successor be scheduled at once, and waits for
 // its predecessor's results only where it first reads them.  Both are no-ops without a PDL launch.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-// ESDP_PDL_EARLY (measurement build): the stage kernels trigger their dependents right after their own
-// dependency wait instead of after their stores (the dependent's wait still covers this grid's completion)
-#ifdef ESDP_PDL_EARLY
-__device__ __forceinline__ void pdl_trigger_early() { pdl_trigger(); }
-__device__ __forceinline__ void pdl_trigger_late() {}
-#else
-__device__ __forceinline__ void pdl_trigger_early() {}
+// Late trigger: after a block's stores (an early trigger measured slower: dependents hold SM slots)
 __device__ __forceinline__ void pdl_trigger_late() { pdl_trigger(); }
-#endif
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #ifdef ESDP_WIN_TRACE
@@ -176,77 +169,36 @@ __global__ void __launch_bounds__(kThreadsC) contract_kernel(const double* __res
 // accumulates its 4 products as a sequential fma chain, so a K/4-long chain of DMMAs is bit-identical
 // to the canonical ascending-k' fma chain (R15) -- and it issues 256 FMAs per warp instruction instead
 // of 32, with 2 operand registers per lane per 4 k'.  Every parity test re-checks the bit equality.
-// One warp computes an 8 (rows k) x 16 (columns i) tile as two accumulators; operands are loaded
-// straight from global/L2 (no shared-memory staging), 8 k'-quads ahead of the MMA chain.
 // Fragment layout (PTX ISA, m8n8k4 .f64, row.col): A[8x4] lane -> A[lane/4][lane%4];
 // B[4x8] lane -> B[lane%4][lane/4]; C/D[8x8] lane -> C[lane/4][2(lane%4) + {0,1}].
 // ------------------------------------------------------------------------------------------------
-constexpr int kDmmaWarps = 4;
-constexpr int kDmmaChunk = 8;   // k'-quads prefetched per step
-
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-// One warp: the 8 x 16 output tile `tile` of W = P V (two 8x8 accumulators).
-__device__ __forceinline__ void dmma_tile(const double* __restrict__ Pt, const double* __restrict__ Vn,
-                                          double* __restrict__ Wt, int rows, int K, int S, int ld, int ncol_tiles,
-                                          int tile, int lane) {
-  const int r0 = (tile / ncol_tiles) * 8, i0 = (tile % ncol_tiles) * 16;
-  if (r0 >= rows) return;
+// Runtime guard of the DMMA bit-exactness the expectation kernels rely on: every warp
+// computes one 8 x 8 tile of A B over kProbeQ k'-quads twice -- as the DMMA chain the kernels use and as
+// the canonical ascending-k' fma chain (R15) -- and counts the outputs whose bits differ.  A [tiles][8][4Q],
+// B [tiles][4Q][8] (host-generated: random signs, wide exponent range, cancelling pairs).
+constexpr int kProbeQ = 32;
+__global__ void dmma_probe_kernel(const double* __restrict__ A, const double* __restrict__ B, int ntiles,
+                                  unsigned* __restrict__ mismatches) {
+  const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (tile >= ntiles) return;
+  const double* a = A + (size_t)tile * 8 * 4 * kProbeQ;
+  const double* b = B + (size_t)tile * 4 * kProbeQ * 8;
   const int kq = lane & 3, g = lane >> 2;
-  const double* pa = Pt + (size_t)min(r0 + g, rows - 1) * K + kq;       // A: P[r0+g][4j+kq]
-  const int c0 = min(i0 + g, ld - 1), c1 = min(i0 + 8 + g, ld - 1);    // B: V[4j+kq][c]
-  const double* vb = Vn + (size_t)kq * ld;
-  const int nq = (K + 3) >> 2;
-  double a[kDmmaChunk], b0[kDmmaChunk], b1[kDmmaChunk];
-#pragma unroll
-  for (int q = 0; q < kDmmaChunk; ++q) {
-    const bool in = q < nq && 4 * q + kq < K;
-    a[q] = in ? __ldg(pa + 4 * q) : 0.0;
-    b0[q] = in ? __ldcg(vb + (size_t)(4 * q) * ld + c0) : 0.0;   // V may be written in-kernel: L2 path
-    b1[q] = in ? __ldcg(vb + (size_t)(4 * q) * ld + c1) : 0.0;
+  double d0 = 0.0, d1 = 0.0;
+  for (int q = 0; q < kProbeQ; ++q) dmma_8x8x4(d0, d1, a[g * 4 * kProbeQ + 4 * q + kq], b[(4 * q + kq) * 8 + g]);
+  // lane holds C[g][2 kq], C[g][2 kq + 1]
+  double c0 = 0.0, c1 = 0.0;
+  for (int k = 0; k < 4 * kProbeQ; ++k) {
+    c0 = __fma_rn(a[g * 4 * kProbeQ + k], b[k * 8 + 2 * kq], c0);
+    c1 = __fma_rn(a[g * 4 * kProbeQ + k], b[k * 8 + 2 * kq + 1], c1);
   }
-  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
-  for (int q0 = 0; q0 < nq; q0 += kDmmaChunk) {
-    double na[kDmmaChunk], nb0[kDmmaChunk], nb1[kDmmaChunk];
-#pragma unroll
-    for (int q = 0; q < kDmmaChunk; ++q) {
-      const int qq = q0 + kDmmaChunk + q;
-      const bool in = qq < nq && 4 * qq + kq < K;
-      na[q] = in ? __ldg(pa + 4 * qq) : 0.0;
-      nb0[q] = in ? __ldcg(vb + (size_t)(4 * qq) * ld + c0) : 0.0;
-      nb1[q] = in ? __ldcg(vb + (size_t)(4 * qq) * ld + c1) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kDmmaChunk; ++q) {
-      if (q0 + q < nq) {        // zero operands beyond K leave the chains unchanged
-        dmma_8x8x4(d00, d01, a[q], b0[q]);
-        dmma_8x8x4(d10, d11, a[q], b1[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kDmmaChunk; ++q) { a[q] = na[q]; b0[q] = nb0[q]; b1[q] = nb1[q]; }
-  }
-  const int r = r0 + g;
-  if (r < rows) {
-    const int c = i0 + 2 * kq;
-    double* wr = Wt + (size_t)r * ld;
-    if (c < S) wr[c] = d00;
-    if (c + 1 < S) wr[c + 1] = d01;
-    if (c + 8 < S) wr[c + 8] = d10;
-    if (c + 9 < S) wr[c + 9] = d11;
-  }
-}
-
-__global__ void __launch_bounds__(kDmmaWarps * 32) contract_dmma_kernel(const double* __restrict__ Pt,  // [rows][K]
-                                                                       const double* __restrict__ Vn,  // [K][ld]
-                                                                       double* __restrict__ Wt,        // [rows][ld]
-                                                                       int rows, int K, int S, int ld, int ncol_tiles) {
-  pdl_trigger();
-  pdl_wait();
-  dmma_tile(Pt, Vn, Wt, rows, K, S, ld, ncol_tiles, blockIdx.x * kDmmaWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+  const unsigned bad = (__double_as_longlong(c0) != __double_as_longlong(d0)) + (__double_as_longlong(c1) != __double_as_longlong(d1));
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 // Shared-memory-staged DMMA expectation: a block computes kDR*8 rows x kDC*16 columns of W.  The P rows
@@ -440,7 +392,6 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   ktrace(1, 1);
   pdl_wait();
   ktrace(1, 2);
-  pdl_trigger_early();
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) {
     if (s < nch) issue_b(s);
@@ -494,26 +445,7 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   pdl_trigger_late();
 }
 
-// ------------------------------------------------------------------------------------------------
-// Latency-regime expectation with TMA multicast (cfg2 shape: K <= 128, even): a thread-block cluster
-// holds the C = ceil(rows / 8) row tiles of one 32-column tile of W.  Every CTA needs the same V block
-// V_{t+1}[0..K)[i0 .. i0+32); instead of C copies from L2 (13 on cfg2: 13 MB of L2 reads per stage), each
-// k' chunk of it is fetched ONCE by a 3-D TMA box [t][KC rows][40 columns] and multicast into all C CTAs'
-// shared memory (cp.async.bulk.tensor ... .multicast::cluster); the chunk issuers are spread over the
-// cluster (chunk c by CTA c mod C).  The 40-column box (8 beyond the tile, zero past the tensor) lays the
-// rows out at a stride of 8 mod 16 doubles, conflict-free for the DMMA B fragments (as dmma3's padding).
-// The CTA's own P rows come by one non-multicast box [t][8 rows][SA columns] (zero past K).  Each chunk has
-// its own mbarrier, so the DMMA chain starts on chunk 0 while the others land.  The cluster barrier that
-// publishes the mbarrier inits (before any multicast may signal them) is split around the dependency wait.
-// Accumulation order per output: ascending k' quads, one DMMA after the other: the canonical chain (R15).
-// ------------------------------------------------------------------------------------------------
-constexpr int kMcKC = 16, kMcMaxCh = 8, kMcCB = 32, kMcSB = 40, kMcRB = 8, kMcThreads = 64;
-__host__ __device__ constexpr int mc_stride_a(int Kp) { return (Kp % 16 == 0 || Kp % 16 == 8) ? Kp + 4 : Kp; }
-__host__ __device__ constexpr int mc_b_offset(int Kp) { return ((kMcRB * mc_stride_a(Kp)) + 15) & ~15; }   // doubles, 128 B
-inline size_t mc_smem_bytes(int K) {
-  const int Kp = (K + 3) & ~3;
-  return sizeof(double) * ((size_t)mc_b_offset(Kp) + (size_t)kMcMaxCh * kMcKC * kMcSB) + sizeof(uint64_t) * (1 + kMcMaxCh);
-}
+// mbarrier helpers (shared-memory barriers completed by async copies or tensor-core commits)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
@@ -521,93 +453,13 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait0(uint64_t* b) {   // phase 0 of a single-use barrier
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void tma_load3_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
-                                             unsigned short mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask) : "memory");
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
 }
 
-// mapP: 3-D [T-1][K][K] (box [1][8][SA]); mapV: 3-D [nbuf][Kp][ld] (box [1][KC][40]).  pt / prow0: the
-// stage index and first own row of P_t; vt: the V_{t+1} buffer.  Grid: (K-row tiles) x (column tiles),
-// row tiles fastest, cluster = all row tiles of a column tile.
-__global__ void __launch_bounds__(kMcThreads) contract_mc_kernel(const __grid_constant__ CUtensorMap mapP,
-                                                                 const __grid_constant__ CUtensorMap mapV,
-                                                                 double* __restrict__ Wt, int rows, int K, int S, int ld,
-                                                                 int nrb, int csz, int pt, int prow0, int vt) {
-  extern __shared__ __align__(128) double msm[];
-  const int tid = threadIdx.x;
-  const int Kp = (K + 3) & ~3, SA = mc_stride_a(Kp);
-  double* as = msm;
-  double* bs = msm + mc_b_offset(Kp);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(bs + kMcMaxCh * kMcKC * kMcSB);   // [0] A, [1 + c] chunk c
-  const int rb = blockIdx.x % nrb, cbk = blockIdx.x / nrb;
-  const int r0 = rb * kMcRB, i0 = cbk * kMcCB;
-  const int nch = (K + kMcKC - 1) / kMcKC;
-  unsigned crank;
-  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  if (tid == 0) {
-    for (int j = 0; j <= nch; ++j) mbar_init(bar + j, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar, (unsigned)(kMcRB * SA * sizeof(double)));
-    for (int c = 0; c < nch; ++c) mbar_expect_tx(bar + 1 + c, (unsigned)(kMcKC * kMcSB * sizeof(double)));
-    tma_load3(as, &mapP, 0, prow0 + r0, pt, bar);          // P_t rows (an input: before the dependency wait)
-  }
-  __syncthreads();
-  cluster_arrive();                                        // this CTA's barriers are initialized and armed
-  pdl_wait();
-  cluster_wait();                                          // ... and every other CTA's
-  if (tid == 0)
-    for (int c = (int)crank; c < nch; c += csz)
-      tma_load3_mc(bs + c * kMcKC * kMcSB, &mapV, i0, c * kMcKC, vt, bar + 1 + c, (unsigned short)((1u << csz) - 1));
-  const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
-  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
-  const double* arow = as + g * SA + kq;
-  const double* bcol = bs + kq * kMcSB + warp * 16 + g;
-  mbar_wait0(bar);
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait0(bar + 1 + c);
-    const int nq = min(kMcKC, Kp - c * kMcKC) >> 2;
-#pragma unroll
-    for (int q = 0; q < kMcKC / 4; ++q) {
-      if (q < nq) {
-        const int k4 = c * kMcKC + 4 * q;
-        const double a = arow[k4];
-        const double b0 = bcol[k4 * kMcSB], b1 = bcol[k4 * kMcSB + 8];
-        dmma_8x8x4(d00, d01, a, b0);
-        dmma_8x8x4(d10, d11, a, b1);
-      }
-    }
-  }
-  cluster_arrive();                                        // no CTA leaves while a multicast may target it
-  const int r = r0 + g;
-  if (r < rows) {
-    const int c = i0 + warp * 16 + 2 * kq;
-    double* wr = Wt + (size_t)r * ld;
-    if (c + 1 < S) *reinterpret_cast<double2*>(wr + c) = make_double2(d00, d01);
-    else if (c < S) wr[c] = d00;
-    if (c + 9 < S) *reinterpret_cast<double2*>(wr + c + 8) = make_double2(d10, d11);
-    else if (c + 8 < S) wr[c + 8] = d10;
-  }
-  cluster_wait();
-  pdl_trigger_late();
-}
-
-// Rank-1 expectation (a GEMV): W[i] = sum_k' pi[k'] V[k'][i], one thread per column, canonical chain.
 __device__ __forceinline__ void gemv_cols(const double* __restrict__ pi, const double* __restrict__ Vn,
                                           double* __restrict__ Wt, int K, int S, int ld, int i) {
   if (i >= S) return;

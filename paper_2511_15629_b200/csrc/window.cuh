@@ -261,7 +261,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   // inputs first (lambda_t and the g fit do not depend on the previous kernel)
   const double lam = st.lambda_t[k];
   const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
-  if (kWait) { pdl_wait(); pdl_trigger_early(); }
+  if (kWait) pdl_wait();
   wtrace(1);
   // W_t over the tile: all of this thread's loads are issued before anything waits on them
   constexpr int kWReg = 3;

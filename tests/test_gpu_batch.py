@@ -104,3 +104,63 @@ def test_batch_full_horizon_cfg5():
             assert np.array_equal(b.value1(m), ref.V[0])
             for t in (1, 100, 287, 288):
                 assert np.array_equal(b.policy(m, t), ref.pol[t - 1]), (m, t)
+
+
+@pytest.mark.parametrize("rank1", [False, True])
+def test_batch_load_async_replaces_price_model(rank1):
+    """esdp_batch_load_async: a batch built on one price model and reloaded with another (validated, copied
+    on the stream, sampling tables rebuilt) solves the new model bit for bit -- J, V_1, the policies and
+    the simulated paths equal those of a batch created on the new model."""
+    import torch
+    idx = [5, 300, 900]
+    a = workloads.cfg5_instances(idx, T=12, K=12)
+    b = workloads.cfg5_instances(idx, T=12, K=12)
+    lam_b, P_b, _ = workloads.price_chain(12, 12, 5.0 / 60.0, seed=workloads.SEED_BASE + 99)
+    rng = np.random.default_rng(3)   # another time-homogeneous chain (one distinct slice, as a's)
+    P0 = P_b[0] * rng.uniform(0.5, 1.5, P_b[0].shape)
+    P_b = np.ascontiguousarray(np.broadcast_to(P0 / P0.sum(axis=1, keepdims=True), P_b.shape))
+    for x in b:
+        x.lam, x.P = lam_b, P_b
+    if rank1:
+        base = workloads.cfg2(T=12, K=12, rank1=True)
+        for x in a:
+            x.P, x.pi = None, base.pi
+        for x in b:
+            x.P, x.pi = None, base.pi
+    s = torch.cuda.Stream()
+    out1 = torch.zeros(len(idx) * 256, dtype=torch.float64, device="cuda")
+    out2 = torch.zeros_like(out1)
+    with E.Batch(b) as ref:
+        Jr = ref.backward()
+        ref.simulate_dev(256, 7, out2.data_ptr())
+        torch.cuda.synchronize()
+        pols = [[ref.policy(m, t) for t in range(1, 13)] for m in range(len(idx))]
+        V1 = [ref.value1(m) for m in range(len(idx))]
+    with E.Batch(a) as bt:
+        bt.backward()
+        lam = np.ascontiguousarray(b[0].lam)
+        P = None if rank1 else np.ascontiguousarray(b[0].P)
+        pi = np.ascontiguousarray(b[0].pi)
+        bt.load_async(lam.ctypes.data, None if P is None else P.ctypes.data, pi.ctypes.data, s)
+        bt.backward_async(s)
+        bt.simulate_dev(256, 7, out1.data_ptr(), s)
+        s.synchronize()
+        assert np.array_equal(bt.objective(), Jr)
+        for m in range(len(idx)):
+            assert np.array_equal(bt.value1(m), V1[m])
+            for t in range(1, 13):
+                assert np.array_equal(bt.policy(m, t), pols[m][t - 1])
+        assert torch.equal(out1, out2)
+        bad = lam.copy()
+        bad[0, 0] = np.nan
+        with pytest.raises(E.EsdpError):
+            bt.load_async(bad.ctypes.data, None if P is None else P.ctypes.data, pi.ctypes.data, s)
+
+
+def test_batch_kernel_times():
+    """esdp_batch_kernel_time: the diagnostic per-launch times of the batch's stage kernels are positive."""
+    with E.Batch(workloads.cfg5_instances([0, 512], T=6, K=8)) as bt:
+        bt.backward()
+        assert bt.kernel_time(0, 10) > 0 and bt.kernel_time(1, 10) > 0
+        with pytest.raises(E.EsdpError):
+            bt.kernel_time(2, 10)   # no brute-force instances in this batch

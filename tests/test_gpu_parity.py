@@ -18,20 +18,18 @@ pytestmark = pytest.mark.gpu
 import paper_2511_15629_b200 as E  # no skip: a missing library must fail loudly
 
 
-def _gpu(inst, brute=False, dmma=True, persist=False, keep=True):
-    return E.Solver(inst, keep_values=keep, force_brute=brute, dmma=dmma, persist=persist)
+def _gpu(inst, brute=False, dmma=True, keep=True):
+    return E.Solver(inst, keep_values=keep, force_brute=brute, dmma=dmma)
 
 
-def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None, dmma=True, persist=False):
+def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None, dmma=True):
     pr = to_oracle(inst)
     ref = oracle.backward(pr, nthreads=nthreads)
-    with _gpu(inst, brute, dmma, persist) as s:
+    with _gpu(inst, brute, dmma) as s:
         if expect_window is not None:
             assert (s.stencil_kind & 1) == int(expect_window)
         if brute:
             assert (s.stencil_kind & 1) == 0
-        if persist:
-            assert s.stencil_kind & 2, "persistent plan expected"
         J = s.backward()
         assert np.array_equal(s.actions(), oracle.actions(pr))
         ts = range(1, inst.T + 1) if stages is None else stages
@@ -46,10 +44,9 @@ def _compare_all(inst, nthreads=8, stages=None, brute=False, expect_window=None,
     return ref
 
 
-@pytest.mark.parametrize("plan", ["persist", "graph"])
 @pytest.mark.parametrize("brute", [False, True])
 @pytest.mark.parametrize("seed", range(40))
-def test_random_small_instances(seed, brute, plan):
+def test_random_small_instances(seed, brute):
     kind = [workloads.PAYOFF_LINEAR, workloads.PAYOFF_LINEAR_MINUS_G, workloads.PAYOFF_TABLE][seed % 3]
     inst = workloads.random_instance(seed, S_max=40 if seed % 2 else 600, T=4 + seed % 3, K=1 + seed % 4)
     S, A = oracle.dims(to_oracle(inst))
@@ -58,7 +55,7 @@ def test_random_small_instances(seed, brute, plan):
         inst.g = workloads.random_g(seed, A, 20.0)
     elif kind == workloads.PAYOFF_TABLE:
         inst.g = workloads.random_table(seed, inst.T, inst.K, A)
-    _compare_all(inst, brute=brute, persist=plan == "persist")
+    _compare_all(inst, brute=brute)
 
 
 @pytest.mark.parametrize("dmma", [True, False])
@@ -67,9 +64,7 @@ def test_expectation_tensor_cores_bitexact(K, dmma):
     """FP64 DMMA (mma.sync m8n8k4) expectation: K not a multiple of 4, rows not a multiple of 8, ragged
     columns; bit-identical to the oracle's sequential fma chain (and the DFMA kernel likewise)."""
     inst = workloads.random_instance(1000 + K, T=4, K=K, S_max=300, rank1=False)
-    _compare_all(inst, dmma=dmma, persist=False)
-    if dmma:
-        _compare_all(inst, persist=True)
+    _compare_all(inst, dmma=dmma)
 
 
 @pytest.mark.parametrize("brute", [False, True])
@@ -134,7 +129,7 @@ def test_dist_path_single_rank_bitexact(name):
     ref = oracle.backward(pr, nthreads=8)
     nid = E.esdp_nccl_unique_id()
     with E.Solver(inst, keep_values=True, dist=(1, 0, nid)) as s:
-        assert not (s.stencil_kind & 2)          # graph plan (NCCL between stages)
+        assert s.stencil_kind & 2                # DMMA expectation (the probe passed)
         assert s.backward() == ref.J
         for t in range(1, inst.T + 1):
             V, W = s.values(t)
@@ -146,43 +141,20 @@ def test_dist_path_single_rank_bitexact(name):
 
 
 def test_cfg2_full_size_dfma_expectation():
-    _compare_all(workloads.cfg2(), nthreads=16, dmma=False, persist=False)
+    _compare_all(workloads.cfg2(), nthreads=16, dmma=False)
 
 
-def test_cfg2_full_size_persistent_plan():
-    _compare_all(workloads.cfg2(), nthreads=16, persist=True, expect_window=True)
-
-
-@pytest.mark.parametrize("persist", [True, False])
-def test_cfg2_no_keep_values(persist):
+def test_cfg2_no_keep_values():
     """Without ESDP_KEEP_VALUES the backward ping-pongs V/W; V_1, every policy and J are unchanged."""
     inst = workloads.cfg2(T=40, K=30)
     pr = to_oracle(inst)
     ref = oracle.backward(pr, nthreads=8)
-    with _gpu(inst, persist=persist, keep=False) as s:
+    with _gpu(inst, keep=False) as s:
         assert s.backward() == ref.J
         V1 = E.esdp_values(s.ctx, 1, want_W=False)
         assert np.array_equal(V1, ref.V[0])
         for t in range(1, inst.T + 1):
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
-
-
-@pytest.mark.parametrize("rank1", [False, True])
-@pytest.mark.parametrize("seed", range(6))
-def test_dataflow_plan_no_keep_values(seed, rank1):
-    """Persistent dataflow kernel with one W buffer and ping-pong V (the write-after-read edges of the
-    task schedule): several column tiles, ragged tails, window and brute force; V_1, pol, J exact."""
-    inst = workloads.random_instance(500 + seed, T=7, K=3 + 7 * seed, S_max=1300, rank1=rank1)
-    pr = to_oracle(inst)
-    ref = oracle.backward(pr, nthreads=8)
-    for brute in (False, True):
-        with E.Solver(inst, keep_values=False, force_brute=brute, persist=True) as s:
-            assert s.stencil_kind & 2
-            for _ in range(2):
-                assert s.backward() == ref.J
-            assert np.array_equal(E.esdp_values(s.ctx, 1, want_W=False), ref.V[0])
-            for t in range(1, inst.T + 1):
-                assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
 @pytest.mark.parametrize("rank1", [False, True])
@@ -200,9 +172,8 @@ def test_graph_without_pdl(rank1):
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
-@pytest.mark.parametrize("persist", [False, True])
 @pytest.mark.parametrize("rank1", [False, True])
-def test_async_load_overlaps_and_matches(rank1, persist):
+def test_async_load_overlaps_and_matches(rank1):
     """esdp_load_async: new prices and transitions uploaded in stage chunks while the backward runs (the
     graph waits per chunk) give the oracle's bits for the new data; repeated async loads alternate
     between two instances; the simulation's sampling tables follow the new P."""
@@ -216,8 +187,7 @@ def test_async_load_overlaps_and_matches(rank1, persist):
         b.P = Pb / Pb.sum(axis=2, keepdims=True)
     refs = [oracle.backward(to_oracle(x), nthreads=16) for x in (a, b)]
     sims = {}
-    with E.Solver(a, persist=persist) as s:
-        assert bool(s.stencil_kind & 2) == persist
+    with E.Solver(a) as s:
         for rep in range(4):
             x, ref = ((a, refs[0]), (b, refs[1]))[rep % 2]
             keep = E.esdp_load_async(s.ctx, lam=x.lam, P=x.P, pi=x.pi)
@@ -234,10 +204,6 @@ def test_async_load_overlaps_and_matches(rank1, persist):
                 assert m == sims[key]
             sims[key] = m
         assert sims[0] != sims[1]
-
-
-def test_cfg2_rank1_full_size_persistent_plan():
-    _compare_all(workloads.cfg2(rank1=True), nthreads=16, persist=True, expect_window=True)
 
 
 def test_cfg2_rank1_full_size():
@@ -294,17 +260,6 @@ def test_cfg3_window_affine_degradation(rank1):
     _compare_all(inst, nthreads=16, brute=True)
 
 
-@pytest.mark.parametrize("csize", ["", "4", "1"])
-def test_expectation_tma_multicast_opt_in(csize, monkeypatch):
-    """The opt-in TMA-multicast cluster expectation (ESDP_MC=1; ESDP_MC_C pads the row tiles to clusters of
-    that size, idle CTAs only receive) gives the canonical chain's bits: every W_t, V_t, pol_t and J."""
-    monkeypatch.setenv("ESDP_MC", "1")
-    if csize:
-        monkeypatch.setenv("ESDP_MC_C", csize)
-    _compare_all(workloads.cfg2(T=5, K=36), nthreads=16)
-    _compare_all(workloads.cfg1("b"))
-
-
 @pytest.mark.parametrize("which", ["cfg2", "cfg3"])
 def test_window_unimodal_and_level_tables(which):
     """The window stencil answers a unimodal run table from its peak and builds sparse-table levels only
@@ -355,9 +310,8 @@ def test_window_affine_g_random(seed):
             assert np.array_equal(V, ref2.V[t - 1]) and np.array_equal(s.policy(t), ref2.pol[t - 1])
 
 
-@pytest.mark.parametrize("persist", [False, True])
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg3"])
-def test_fused_bidcurves_in_backward(name, persist):
+def test_fused_bidcurves_in_backward(name):
     """esdp_set_bid_requests: curves extracted inside the backward graph (side branch per stage, unsorted
     requests over all stages) equal the oracle's bit for bit, on every backward pass."""
     import torch
@@ -371,8 +325,7 @@ def test_fused_bidcurves_in_backward(name, persist):
     rng = np.random.default_rng(5)
     n = 3000
     req = np.stack([rng.integers(1, inst.T + 1, n), rng.integers(0, inst.S, n), rng.integers(0, inst.K, n)], 1)
-    with _gpu(inst, persist=persist) as s:
-        assert bool(s.stencil_kind & 2) == persist
+    with _gpu(inst) as s:
         cap = s.A
         nv = torch.zeros(n, dtype=torch.int32, device="cuda")
         vert = torch.zeros(cap * n, dtype=torch.int16, device="cuda")
@@ -710,3 +663,23 @@ def test_lambda_only_load_after_side_stream_simulation():
         assert np.array_equal(out.cpu().numpy(), sy)
         per, _, _ = s.simulate(n, seed=9)
         assert np.array_equal(per, sy)
+
+
+@pytest.mark.parametrize("name", ["cfg2-small", "cfg2-rank1-small"])
+def test_dmma_probe_failure_falls_back_to_dfma(name, monkeypatch):
+    """The DMMA bit-exactness guard: a failed DMMA-vs-fma-chain probe at context creation (forced with
+    ESDP_DMMA_PROBE_FAIL=1) moves the expectation to DFMA; the plan reports it and every result is still the
+    oracle's, bit for bit (single and batch contexts).  Without the variable the probe passes on B200."""
+    inst = workloads.cfg2(T=12, K=24, rank1=name.endswith("rank1-small"))
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=8)
+    with E.Solver(inst) as s:
+        assert s.stencil_kind & 2 and not s.stencil_kind & 4
+    monkeypatch.setenv("ESDP_DMMA_PROBE_FAIL", "1")
+    with E.Solver(inst) as s:
+        assert s.stencil_kind & 4 and not s.stencil_kind & 2
+        assert s.backward() == ref.J
+        for t in range(1, inst.T + 1):
+            V, W = s.values(t)
+            assert np.array_equal(V, ref.V[t - 1]) and np.array_equal(W, ref.W[t - 1])
+            assert np.array_equal(s.policy(t), ref.pol[t - 1])

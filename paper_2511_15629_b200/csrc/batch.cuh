@@ -35,6 +35,7 @@ __device__ __forceinline__ void copy_struct(T& dst, const T& src) {
 #ifndef ESDP_WIN_MINB_BATCH
 #define ESDP_WIN_MINB_BATCH 5
 #endif
+template <int OPT, bool kLevels>
 __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB_BATCH) window_batch_kernel(const BatchInst* __restrict__ bi,
                                                                       const int* __restrict__ idx,
                                                                       const double* Wt, double* Vt,
@@ -54,10 +55,15 @@ __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB_BATCH) window_batch
     p.ld = row_stride;
     p.rank1 = rank1;
   }
-  pdl_wait();                          // W_t is the previous contraction's output
   __syncthreads();
-  window_item(p, blockIdx.y, blockIdx.x * kWinTile, wsm);
+  window_item<true, OPT, kLevels>(p, blockIdx.y, blockIdx.x * (kWinThreads * OPT), wsm);   // waits for W_t inside
   pdl_trigger();
+}
+typedef void (*WindowBatchKernel)(const BatchInst*, const int*, const double*, double*, int16_t*, size_t, size_t,
+                                  const double*, int, int, int);
+inline WindowBatchKernel window_batch_kernel_of(int opt, int levels) {
+  if (levels) return window_batch_kernel<1, true>;
+  return opt == 2 ? window_batch_kernel<2, false> : window_batch_kernel<1, false>;
 }
 
 // grid (tiles, K, number of brute-force instances): the brute-force stencil of kernels.cuh per instance.

@@ -76,6 +76,7 @@ struct esdp_ctx {
   int* d_singles = nullptr;
   int* d_live = nullptr;
   size_t window_smem = 0;
+  int win_opt = 1, win_levels = 1;   // window kernel variant: outputs per thread, packed level tables
   int on_grid = 1, f0 = 0;
   double w0 = 0.0;
   // device
@@ -779,6 +780,7 @@ WinParams win_params(const esdp_ctx* c) {
   wp.dc = c->delta / c->eta_c; wp.dd = c->delta * c->eta_d;
   wp.jspan = (double)(c->S + (c->o_max - c->o_min) + 2);
   wp.g = c->d_g; wp.gfit = c->d_gfit; wp.g_kind = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  { const char* e = getenv("ESDP_WIN_FORCE_NONUNI"); wp.force_nonuni = (e && atoi(e)) ? 1 : 0; }   // tests only
   for (int j = 0; j < (int)c->singles.size() && j < kMaxSingles; ++j) {
     const int a = c->singles[j];
     wp.sg[j].act = c->act[a]; wp.sg[j].w = c->w[a]; wp.sg[j].omw = c->omw[a]; wp.sg[j].off = c->off[a]; wp.sg[j].a = a;
@@ -795,6 +797,22 @@ StencilParams stencil_params(const esdp_ctx* c) {
   return prm;
 }
 
+// window_stencil_kernel variants: OPT outputs per thread (2: throughput regime), packed level tables for
+// payoffs with non-unimodal run tables (LINEAR_MINUS_G); the linear payoff scans a non-unimodal window.
+void (*window_kernel_of(int opt, int levels))(WinParams) {
+  if (levels) return window_stencil_kernel<1, true>;
+  return opt == 2 ? window_stencil_kernel<2, false> : window_stencil_kernel<1, false>;
+}
+// Plan of the window kernel variant.  ESDP_WIN_OPT=1|2 in the environment overrides the choice (measurement).
+void plan_window(esdp_ctx* c, int64_t blocks1) {
+  const char* e = getenv("ESDP_WIN_OPT");   // read per context: tests switch variants within one process
+  const int env = e ? atoi(e) : 0;
+  c->win_levels = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
+  // two outputs per thread once the one-output grid exceeds ~2 waves (4 resident blocks per SM)
+  c->win_opt = c->win_levels ? 1 : (env == 1 || env == 2) ? env : (blocks1 > 2 * 4 * 148 ? 2 : 1);
+  c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min, c->A, c->win_opt, c->win_levels != 0);
+}
+
 // The max-plus stencil of stage t: V_t, pol_t from W_t (window or brute force).
 cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool force_brute) {
   const int S = c->S;
@@ -806,7 +824,9 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
   if (c->use_window && !force_brute) {
     WinParams wp = win_params(c);
     wp.W = Wt; wp.V = V_of(c, t) + (size_t)c->k_lo * c->ld; wp.pol = pol; wp.lambda_t = lam;
-    return launch(window_stencil_kernel, dim3((S + kWinTile - 1) / kWinTile, K), dim3(kWinThreads), c->window_smem, s, pdl, wp);
+    const int tile = kWinThreads * c->win_opt;
+    return launch(window_kernel_of(c->win_opt, c->win_levels), dim3((S + tile - 1) / tile, K), dim3(kWinThreads),
+                  c->window_smem, s, pdl, wp);
   }
   StencilParams prm = stencil_params(c);
   prm.W = Wt; prm.V = V_of(c, t) + (size_t)c->k_lo * c->ld; prm.pol = pol; prm.lambda_t = lam;
@@ -1222,7 +1242,7 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     }
     c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
     if (c->use_window) {
-      c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min);
+      plan_window(c, 1 << 30);   // batch: throughput regime
       if (c->window_smem > 200 * 1024) c->use_window = 0;
     }
     if (c->stencil_smem > 227 * 1024) { fail(c, ESDP_E_CONFIG, "action span too wide for shared memory"); return bail(ESDP_E_CONFIG); }
@@ -1282,10 +1302,11 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
   if (cudaStreamSynchronize(c->copy) != cudaSuccess) { fail(c, ESDP_E_CUDA, "initial upload"); return bail(ESDP_E_CUDA); }
   c->stencil_smem = stencil_smem_bytes(c->A, c->o_max - c->o_min);
   if (c->use_window) {
-    c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min);
+    plan_window(c, (int64_t)c->k_cnt * ((c->S + kWinThreads - 1) / kWinThreads));
     if (c->window_smem > 200 * 1024) c->use_window = 0;
     else if (c->window_smem > 48 * 1024 &&
-             cudaFuncSetAttribute(window_stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->window_smem) != cudaSuccess)
+             cudaFuncSetAttribute(window_kernel_of(c->win_opt, c->win_levels), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)c->window_smem) != cudaSuccess)
       c->use_window = 0;
   }
   if (c->stencil_smem > 48 * 1024) {
@@ -1827,6 +1848,7 @@ struct esdp_batch {
   int* d_widx = nullptr;                                   // window-plan instances
   int* d_bidx = nullptr;                                   // brute-force instances
   int nwin = 0, nbrute = 0;
+  int win_opt = 2, win_levels = 0;   // batch window kernel variant (window.cuh)
   int dmma = 1;   // expectation on the FP64 tensor cores (0: the DMMA probe failed -> DFMA)
   size_t ntab_cap = 0;   // sampling-table rows the guide allocation holds (distinct P_t slices x K)
   size_t win_smem = 0, brute_smem = 0;
@@ -1903,8 +1925,9 @@ cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, b
   const double* lam = b->d_lambda + (size_t)(t - 1) * K;
   const size_t pol_inst = (size_t)T * K * S, pol_stage = (size_t)(t - 1) * K * S;
   if (what == 1)
-    return launch(window_batch_kernel, dim3((S + kWinTile - 1) / kWinTile, K, b->nwin), dim3(kWinThreads), b->win_smem, s,
-                  pdl, (const BatchInst*)b->d_bi, (const int*)b->d_widx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
+    return launch(window_batch_kernel_of(b->win_opt, b->win_levels),
+                  dim3((S + kWinThreads * b->win_opt - 1) / (kWinThreads * b->win_opt), K, b->nwin), dim3(kWinThreads),
+                  b->win_smem, s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_widx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
                   pol_stage, lam, b->ld, (int)NL, b->rank1);
   return launch(stencil_batch_kernel, dim3((S + kTile - 1) / kTile, K, b->nbrute), dim3(kStencilWarps * 32), b->brute_smem,
                 s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_bidx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
@@ -2060,7 +2083,7 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
     x.f0 = c->f0; x.on_grid = c->on_grid; x.w0 = c->w0;
     if (c->use_window) {
       widx.push_back(m);
-      b->win_smem = std::max(b->win_smem, c->window_smem);
+      b->win_levels |= c->win_levels;
     } else {
       bidx.push_back(m);
       b->brute_smem = std::max(b->brute_smem, c->stencil_smem);
@@ -2068,6 +2091,15 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   }
   b->nwin = (int)widx.size();
   b->nbrute = (int)bidx.size();
+  {   // one window variant for every window instance: levels if any instance needs them (then one output per thread)
+    const char* e = getenv("ESDP_WIN_OPT");
+    b->win_opt = b->win_levels ? 1 : ((e && atoi(e) == 1) ? 1 : 2);
+    for (int m : widx) {
+      const esdp_ctx* c = b->inst[m];
+      b->win_smem = std::max(b->win_smem, window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min, c->A, b->win_opt,
+                                                            b->win_levels != 0));
+    }
+  }
   if (!bidx.empty()) BCUDA(b, cudaMemcpyAsync(b->d_bidx, bidx.data(), bidx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   if (b->brute_smem > 48 * 1024)
     BCUDA(b, cudaFuncSetAttribute(stencil_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->brute_smem));
@@ -2075,7 +2107,8 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   if (!widx.empty()) BCUDA(b, cudaMemcpyAsync(b->d_widx, widx.data(), widx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   BCUDA(b, cudaStreamSynchronize(s));
   if (b->win_smem > 48 * 1024)
-    BCUDA(b, cudaFuncSetAttribute(window_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->win_smem));
+    BCUDA(b, cudaFuncSetAttribute(window_batch_kernel_of(b->win_opt, b->win_levels), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)b->win_smem));
   if (contract_dmma2_smem(K) > 48 * 1024 && contract_dmma2_smem(K) <= 200 * 1024)
     cudaFuncSetAttribute(contract_dmma2_kernel<kDR, kDC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_dmma2_smem(K));
   if (K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) > 48 * 1024 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024)

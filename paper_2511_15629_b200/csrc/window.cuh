@@ -38,7 +38,7 @@ constexpr int kLevelSlots = (kWinTile + 512 + 2 * kWinThreads - 1) / (2 * kWinTh
 
 constexpr int kMaxSingles = 16;
 
-__device__ __forceinline__ void wtrace(int m) { ktrace(0, m); }  // singles staged in shared memory (more: read from global)
+__device__ __forceinline__ void wtrace(int m) { ktrace(0, m); }
 
 // static data of a single (canonically evaluated) action, carried in the kernel parameters so the
 // block reads it from the constant bank instead of a dependent global gather
@@ -61,6 +61,7 @@ struct WinParams {
   const double* g;          // [A] degradation g_a (LINEAR_MINUS_G): pay = fl(fl(lambda p) - g) when g_kind
   const double* gfit;       // [6] affine fit of g on the runs: gc0, gc1, gd0, gd1, max deviation, max |g|
   int g_kind;               // 1: payoff lambda p - g(p) (kind LINEAR_MINUS_G), 0: lambda p
+  int force_nonuni;         // tests: treat every run table as non-unimodal (exercises the fallback paths)
   WinSingle sg[kMaxSingles];  // static data of singles[0 .. min(nsingle, kMaxSingles))
 };
 
@@ -104,10 +105,14 @@ struct RangeMax {
 
 inline int window_levels(int L) { int q = 0; while ((2 << q) <= L) ++q; return q + 1; }
 
-inline size_t window_smem_bytes(int Lc, int Ld, int o_span) {
-  const size_t nw = (kWinTile + o_span + 2 + 1) & ~(size_t)1;
-  const size_t nc = (kWinTile + Lc + 1) & ~(size_t)1, nd = (kWinTile + Ld + 1) & ~(size_t)1;
-  return sizeof(double) * nw + sizeof(unsigned long long) * (window_levels(Lc) * nc + window_levels(Ld) * nd) + 64;
+__host__ __device__ constexpr int win_al2(int n) { return (n + 1) & ~1; }
+// shared memory of one (k, tile) item, tile = kWinThreads * opt output columns: W tile [nw], raw key tables
+// [nc], [nd], row payoffs [A], then (levels only) the packed sparse tables of the non-unimodal fallback
+inline size_t window_smem_bytes(int Lc, int Ld, int o_span, int A, int opt = 1, bool levels = true) {
+  const int tile = kWinThreads * opt;
+  const size_t nw = win_al2(tile + o_span + 2), nc = win_al2(tile + Lc), nd = win_al2(tile + Ld);
+  return sizeof(double) * (nw + nc + nd + win_al2(A)) +
+         (levels ? sizeof(unsigned long long) * (window_levels(Lc) * nc + window_levels(Ld) * nd) : 0) + 64;
 }
 
 __device__ __forceinline__ double canon_single(const WinParams& p, const double* __restrict__ wt, int wbase, int i,
@@ -121,19 +126,6 @@ __device__ __forceinline__ double canon_single(const WinParams& p, const double*
   double pay = __dmul_rn(lam, __ldg(p.act + a));
   if (p.g_kind) pay = __dsub_rn(pay, __ldg(p.g + a));
   return __dadd_rn(pay, wint);
-}
-
-// a single action's data staged in shared memory for the whole block
-struct SingleAct {
-  double pay;   // fl(fl(lambda * p_a) - g_a) for this block's k (R14; g = 0 for the linear payoff)
-  double w, omw;
-  int off, a;
-};
-
-__device__ __forceinline__ double canon_staged(const SingleAct& s, const double* __restrict__ wt, int wbase, int i) {
-  const int x = i + s.off - wbase;
-  const double wint = (s.w == 0.0) ? wt[x] : __dadd_rn(__dmul_rn(s.omw, wt[x]), __dmul_rn(s.w, wt[x + 1]));
-  return __dadd_rn(s.pay, wint);
 }
 
 // level q of a table: entry x = max(level q-1 at x, at x + 2^(q-1)), for x <= n - 2^q.  Straight-line,
@@ -204,98 +196,114 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
   m2 = unord64(umax64(t.query(l, pos - 1), t.query(pos + 1, r)));
 }
 
-// Unimodal tables (the common case: W_t(., k) concave in the SoC, as for every linear-payoff workload
-// measured -- tests/diag/unimodal.py finds 100 % of cfg2 / cfg4 / cfg5 tiles unimodal, cfg3's fixed cost
-// 52 % / 73 % per side).  With ck(key) = 0 for -inf keys, a table is unimodal when every rising pair
-// (x, x+1) precedes every falling pair; its maximum then sits at p* = 1 + the last rising x (0 if none),
-// the maximum of any window [l, r] at clamp(p*, l, r) and the runner-up next to it.  Packed keys are
-// distinct (positions in the low bits), so these are exactly the two largest keys the sparse-table
-// queries return -- the same values, positions and decisions -- and a unimodal table needs no levels.
-__device__ __forceinline__ unsigned long long ckey(unsigned long long k) { return k < 0x0010000000000000ull ? 0ull : k; }
-// pair (idx - 1, idx): a rise records idx in up (max), a fall in dn (min)
-__device__ __forceinline__ void uni_pair(unsigned long long a, unsigned long long b, unsigned idx, unsigned& up, unsigned& dn) {
-  a = ckey(a);
-  b = ckey(b);
-  up = b > a ? umax(up, idx) : up;
-  dn = b < a ? umin(dn, idx) : dn;
-}
-constexpr unsigned kNoFall = 0xffffu;
+constexpr unsigned kNoFall = 0xffffu;   // "no fall" sentinel of the unimodality test
 
-__device__ __forceinline__ void window_top2_uni(const RangeMax& t, int pstar, int l, int r, double& m1, int& pos,
-                                                double& m2) {
-  if (l > r) { pos = 0; m1 = m2 = -INFINITY; return; }   // empty run (as query() on an empty range)
-  const int q = min(max(pstar, l), r);
-  pos = q;
-  m1 = unord64(t.v[q]);
-  m2 = unord64(umax64(q > l ? t.v[q - 1] : 0ull, q < r ? t.v[q + 1] : 0ull));
-}
-
-// One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.  kWait: the
-// programmatic dependency wait (W_t is the previous kernel's output) is taken here, after the input loads
-// (lambda, the g fit) are issued; the W loads follow it at once, and the singles come from the kernel
-// parameters, so the block pays one memory latency before its first barrier.
+// One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.
+//   1. Row payoffs pay[a] = fl(fl(lambda_{t,k} p_a) - g_a) (R14) for every action, in shared memory: inputs
+//      only, so they are formed before the programmatic dependency wait (kWait) on W_t.
+//   2. W_t over the tile and its action halo, -inf outside [0, S-1] (Alg. 1 line 8: an infeasible action
+//      never wins), and the high word of max |W| for the exactness margin.
+//   3. The two run key tables key(j) = fl(W[j] - fl(beta j)) as plain doubles.  Every thread also records
+//      the rises (key[x] > key[x-1]; the left key recomputed from W, the same bits) and falls of its
+//      entries; one block reduction makes "every rise precedes every fall" (unimodal) block-uniform.  A
+//      unimodal table answers any window from its peak p* = the last rise: the maximum sits at
+//      clamp(p*, l, r), the runner-up next to it.  Only a non-unimodal table builds the packed sparse
+//      tables (positions in the low bits, two lookups per window; their truncation widens eps).
+//   4. One output per thread: the window top-2 of each run, the singles (zero action, interpolated
+//      endpoints, irregular actions) canonically, the margin test; near ties rescan the row canonically.
 struct WinStage {          // the per-stage pointers of an item (the rest of WinParams is stage-invariant)
   const double* W; double* V; int16_t* pol; const double* lambda_t;
 };
 
-template <bool kWait = false>
-__device__ __forceinline__ void window_item(const WinParams& p, const WinStage& st, int k, int i0, double* wsm) {
-  const int tid = threadIdx.x;
-  wtrace(0);
-  const int nw = kWinTile + (p.o_max - p.o_min) + 2;
-  const int lc = p.pc + 1, ldl = p.pd + 1;
-  RangeMax tc, td;
-  tc.n = kWinTile + p.Lc;                  // charge table: columns [i0 + 1, i0 + nc]
-  td.n = kWinTile + p.Ld;                  // discharge table: columns [i0 - Ld, i0 + kWinTile)
-  tc.ns = (tc.n + 1) & ~1;
-  td.ns = (td.n + 1) & ~1;
-  double* wt = wsm;                        // W over columns [wbase, wbase + nw)
-  tc.v = (unsigned long long*)(wt + ((nw + 1) & ~1));
-  td.v = tc.v + (size_t)lc * tc.ns;
-  __shared__ unsigned red[kWinThreads / 32];
-  __shared__ unsigned ured[4][kWinThreads / 32];   // unimodality: rises (max) and falls (min) per table
-  __shared__ SingleAct ss[kMaxSingles];
+// canonical candidate of action a from the staged row payoff: fl(pay_a + Wint), -inf if infeasible
+__device__ __forceinline__ double canon_pay(const WinParams& p, const double* __restrict__ pay,
+                                            const double* __restrict__ wt, int wbase, int i, int a) {
+  const int o = __ldg(p.off + a);
+  const double wa = __ldg(p.w + a);
+  const int x = i + o - wbase;
+  const double wint = (wa == 0.0) ? wt[x] : __dadd_rn(__dmul_rn(__ldg(p.omw + a), wt[x]), __dmul_rn(wa, wt[x + 1]));
+  return __dadd_rn(pay[a], wint);
+}
 
+// rise / fall bookkeeping of entry x of a raw key table (x >= 1): up = last rise, dn = first fall
+__device__ __forceinline__ void win_key(double* __restrict__ tb, const double* __restrict__ wt, int wbase, int j0, int x,
+                                        double beta, unsigned& up, unsigned& dn) {
+  const int j = j0 + x;
+  const double jd = (double)j;
+  const double key = __dsub_rn(wt[j - wbase], __dmul_rn(beta, jd));
+  tb[x] = key;
+  if (x >= 1) {
+    const double prev = __dsub_rn(wt[j - 1 - wbase], __dmul_rn(beta, __dsub_rn(jd, 1.0)));
+    if (key > prev) up = umax(up, (unsigned)x);
+    if (key < prev) dn = umin(dn, (unsigned)x);
+  }
+}
+
+// top-2 of the window [l, r] of a raw unimodal table with peak pstar
+__device__ __forceinline__ void win_top2_uni(const double* __restrict__ tb, int pstar, int l, int r, double& m1, int& pos,
+                                             double& m2) {
+  const int q = min(max(pstar, l), r);
+  pos = q;
+  m1 = tb[q];
+  m2 = fmax(q > l ? tb[q - 1] : -INFINITY, q < r ? tb[q + 1] : -INFINITY);
+}
+
+// raw-key window top-2 by a scan (a non-unimodal table without packed levels; ascending, ties keep the
+// first -- an equal runner-up then fails the margin test and the row is rescanned canonically)
+__device__ __forceinline__ void win_top2_scan(const double* __restrict__ tb, int l, int r, double& m1, int& pos,
+                                              double& m2) {
+  m1 = -INFINITY; m2 = -INFINITY; pos = l;
+  for (int q = l; q <= r; ++q) {
+    const double v = tb[q];
+    if (v > m1) { m2 = m1; m1 = v; pos = q; }
+    else m2 = fmax(m2, v);
+  }
+}
+
+// OPT: outputs per thread (tile = kWinThreads * OPT columns; 2 amortizes the halo and the per-block work in
+// the throughput regime).  kLevels: non-unimodal tables build packed sparse tables (else: a per-window scan
+// of the raw keys; for payoffs whose tables are unimodal in practice -- the linear payoff).
+template <bool kWait = false, int OPT = 1, bool kLevels = true>
+__device__ __forceinline__ void window_item(const WinParams& p, const WinStage& st, int k, int i0, double* wsm) {
+  static_assert(!kLevels || OPT == 1, "the level builds assume one output per thread");
+  constexpr int kTile = kWinThreads * OPT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  wtrace(0);
+  const int span = p.o_max - p.o_min;
+  const int nw = kTile + span + 2;
+  const int nc = kTile + p.Lc, nd = kTile + p.Ld;   // charge: columns [i0+1, i0+nc]; discharge [i0-Ld, ..)
+  double* wt = wsm;                                        // W over columns [wbase, wbase + nw)
+  double* kc = wt + win_al2(nw);
+  double* kd = kc + win_al2(nc);
+  double* pay = kd + win_al2(nd);
+  __shared__ unsigned red[5][kWinThreads / 32];            // per warp: max|W| hi word, up_c, dn_c, up_d, dn_d
   const double* Wrow = st.W + (p.rank1 ? 0 : (size_t)k * p.ld);
   const int wbase = i0 + p.o_min;
-  // inputs first (lambda_t and the g fit do not depend on the previous kernel)
+  // 1. inputs: the row payoffs (and lambda, the g fit) before the dependency wait
   const double lam = st.lambda_t[k];
   const double gc0 = p.gfit[0], gc1 = p.gfit[1], gd0 = p.gfit[2], gd1 = p.gfit[3];
+  for (int a = tid; a < p.A; a += kWinThreads) {
+    double v = __dmul_rn(lam, __ldg(p.act + a));
+    if (p.g_kind) v = __dsub_rn(v, __ldg(p.g + a));
+    pay[a] = v;
+  }
   if (kWait) pdl_wait();
   wtrace(1);
-  // W_t over the tile: all of this thread's loads are issued before anything waits on them
-  constexpr int kWReg = 3;
+  // 2. W_t over the tile: all of this thread's loads are issued before anything waits on them
+  constexpr int kWReg = 2 + OPT;
   double wv[kWReg];
 #pragma unroll
   for (int u = 0; u < kWReg; ++u) {
     const int x = tid + u * kWinThreads, col = wbase + x;
     wv[u] = (x < nw && col >= 0 && col < p.S) ? __ldcg(Wrow + col) : -INFINITY;
   }
-  // key slopes: the run payoffs lambda p - g are affine in the offset o (g fitted by gc0 + gc1 o on the
-  // charge run, gd0 + gd1 |o| on the discharge run; g = 0 for the linear payoff), so
-  //   cand(i, j) ~= key(j) + beta i - g0,  key(j) = W[j] - beta j,
-  //   beta_c = lambda delta / eta_c + gc1,  beta_d = lambda delta eta_d - gd1   (any few-ulp rounding: see eps)
-  const double beta_c = __dadd_rn(__dmul_rn(lam, p.dc), gc1);
-  const double beta_d = __dsub_rn(__dmul_rn(lam, p.dd), gd1);
-  const int nsg = p.nsingle < kMaxSingles ? p.nsingle : kMaxSingles;
-  if (tid < nsg) {
-    const WinSingle& g = p.sg[tid];
-    SingleAct s;
-    s.a = g.a; s.off = g.off; s.w = g.w; s.omw = g.omw;
-    s.pay = __dmul_rn(lam, g.act);
-    if (p.g_kind) s.pay = __dsub_rn(s.pay, __ldg(p.g + g.a));
-    ss[tid] = s;
-  }
-  // max |W| over the tile: the high words of |W| (ordered like the values), reduced with REDUX; the
-  // bound M below fills the low word with ones, so M >= max |W|
   unsigned mx = 0u;
 #pragma unroll
   for (int u = 0; u < kWReg; ++u) {
     const int x = tid + u * kWinThreads;
     if (x < nw) {
-      const double v = wv[u];
-      if (v != -INFINITY) mx = umax(mx, (unsigned)__double2hiint(v) & 0x7fffffffu);
-      wt[x] = v;
+      if (wv[u] != -INFINITY) mx = umax(mx, (unsigned)__double2hiint(wv[u]) & 0x7fffffffu);
+      wt[x] = wv[u];
     }
   }
   for (int x = tid + kWReg * kWinThreads; x < nw; x += kWinThreads) {   // wide action spans
@@ -307,120 +315,116 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     }
     wt[x] = v;
   }
+  const double beta_c = __dadd_rn(__dmul_rn(lam, p.dc), gc1);   // key slopes (see the header comment)
+  const double beta_d = __dsub_rn(__dmul_rn(lam, p.dd), gd1);
   __syncthreads();
   wtrace(2);
-  // level 0: packed key(j) = W[j] - beta*j, position x (pairs of entries, 16-byte stores); the pairs
-  // (x, x+1) and (x+1, x+2) feed the unimodality test (key x+2 recomputed here: no extra barrier)
+  // 3. raw key tables with the unimodality bookkeeping
   unsigned upc = 0u, dnc = kNoFall, upd = 0u, dnd = kNoFall;
-#pragma unroll
-  for (int u = 0; u < kLevelSlots; ++u) {   // n <= 768 (as the level builds)
-    const int x = 2 * (tid + u * kWinThreads);
-    if (x >= tc.n) break;
-    const int j = i0 + 1 + x;
-    ulonglong2 r;
-    r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_c, (double)j)), x);
-    r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_c, (double)(j + 1))), x + 1);
-    *reinterpret_cast<ulonglong2*>(tc.v + x) = r;    // entry n (x + 1 == n) is padding
-    if (x + 1 < tc.n) uni_pair(r.x, r.y, x + 1, upc, dnc);
-    if (x + 2 < tc.n)
-      uni_pair(r.y, pack_key(__dsub_rn(wt[j + 2 - wbase], __dmul_rn(beta_c, (double)(j + 2))), x + 2), x + 2, upc, dnc);
-  }
-#pragma unroll
-  for (int u = 0; u < kLevelSlots; ++u) {
-    const int x = 2 * (tid + u * kWinThreads);
-    if (x >= td.n) break;
-    const int j = i0 - p.Ld + x;
-    ulonglong2 r;
-    r.x = pack_key(__dsub_rn(wt[j - wbase], __dmul_rn(beta_d, (double)j)), x);
-    r.y = pack_key(__dsub_rn(wt[j + 1 - wbase], __dmul_rn(beta_d, (double)(j + 1))), x + 1);
-    *reinterpret_cast<ulonglong2*>(td.v + x) = r;
-    if (x + 1 < td.n) uni_pair(r.x, r.y, x + 1, upd, dnd);
-    if (x + 2 < td.n)
-      uni_pair(r.y, pack_key(__dsub_rn(wt[j + 2 - wbase], __dmul_rn(beta_d, (double)(j + 2))), x + 2), x + 2, upd, dnd);
+  for (int x = tid; x < nc || x < nd; x += kWinThreads) {
+    if (x < nc) win_key(kc, wt, wbase, i0 + 1, x, beta_c, upc, dnc);
+    if (x < nd) win_key(kd, wt, wbase, i0 - p.Ld, x, beta_d, upd, dnd);
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   upc = __reduce_max_sync(0xffffffffu, upc);
   dnc = __reduce_min_sync(0xffffffffu, dnc);
   upd = __reduce_max_sync(0xffffffffu, upd);
   dnd = __reduce_min_sync(0xffffffffu, dnd);
-  if ((tid & 31) == 0) {
-    red[tid >> 5] = mx;
-    ured[0][tid >> 5] = upc; ured[1][tid >> 5] = dnc; ured[2][tid >> 5] = upd; ured[3][tid >> 5] = dnd;
-  }
+  if (lane == 0) { red[0][warp] = mx; red[1][warp] = upc; red[2][warp] = dnc; red[3][warp] = upd; red[4][warp] = dnd; }
   __syncthreads();
-  upc = __reduce_max_sync(0xffffffffu, ured[0][tid % (kWinThreads / 32)]);
-  dnc = __reduce_min_sync(0xffffffffu, ured[1][tid % (kWinThreads / 32)]);
-  upd = __reduce_max_sync(0xffffffffu, ured[2][tid % (kWinThreads / 32)]);
-  dnd = __reduce_min_sync(0xffffffffu, ured[3][tid % (kWinThreads / 32)]);
-  const bool uni_c = upc < dnc, uni_d = upd < dnd;   // block-uniform
-  const int pc = uni_c ? 0 : p.pc, pd = uni_d ? 0 : p.pd;
-  if (tid == 0 && !(uni_c && uni_d)) atomicAdd(&g_window_level_tables, (unsigned long long)(!uni_c + !uni_d));
+  mx = __reduce_max_sync(0xffffffffu, red[0][lane % (kWinThreads / 32)]);
+  upc = __reduce_max_sync(0xffffffffu, red[1][lane % (kWinThreads / 32)]);
+  dnc = __reduce_min_sync(0xffffffffu, red[2][lane % (kWinThreads / 32)]);
+  upd = __reduce_max_sync(0xffffffffu, red[3][lane % (kWinThreads / 32)]);
+  dnd = __reduce_min_sync(0xffffffffu, red[4][lane % (kWinThreads / 32)]);
+  const bool uni_c = upc < dnc && !p.force_nonuni, uni_d = upd < dnd && !p.force_nonuni;   // block-uniform
   wtrace(3);
-  const int top = pc > pd ? pc : pd;      // unimodal tables need no levels
+  // non-unimodal tables (rare for linear payoffs; cfg3's fixed cost): packed sparse tables
+  RangeMax tc, td;
+  tc.n = nc; td.n = nd;
+  tc.ns = win_al2(nc); td.ns = win_al2(nd);
+  tc.v = reinterpret_cast<unsigned long long*>(pay + win_al2(p.A));
+  td.v = tc.v + (size_t)(p.pc + 1) * tc.ns;
+  if (!(uni_c && uni_d)) {
+    if (tid == 0) atomicAdd(&g_window_level_tables, (unsigned long long)(!uni_c + !uni_d));
+    if (kLevels) {
+      for (int x = tid; x < nc || x < nd; x += kWinThreads) {
+        if (!uni_c && x < nc) tc.v[x] = pack_key(kc[x], x);
+        if (!uni_d && x < nd) td.v[x] = pack_key(kd[x], x);
+      }
+      __syncthreads();
+      const int pc = uni_c ? 0 : p.pc, pd = uni_d ? 0 : p.pd;
+      const int top = pc > pd ? pc : pd;
 #pragma unroll
-  for (int q = 1; q <= 9; q += 2) {     // levels <= 9 (L <= 512), two per barrier: unrolled, uniform exits
-    if (q > top) break;
-    if (q + 1 <= pc) build_level2(tc, q, tid);
-    else if (q <= pc) build_level(tc, q, tid);
-    if (q + 1 <= pd) build_level2(td, q, tid);
-    else if (q <= pd) build_level(td, q, tid);
-    __syncthreads();
+      for (int q = 1; q <= 9; q += 2) {     // levels <= 9 (L <= 512), two per barrier: unrolled, uniform exits
+        if (q > top) break;
+        if (q + 1 <= pc) build_level2(tc, q, tid);
+        else if (q <= pc) build_level(tc, q, tid);
+        if (q + 1 <= pd) build_level2(td, q, tid);
+        else if (q <= pd) build_level(td, q, tid);
+        __syncthreads();
+      }
+    }
   }
   wtrace(4);
-  (void)ldl;
-  const unsigned mb = __reduce_max_sync(0xffffffffu, red[tid % (kWinThreads / 32)]);
-  const double M = __hiloint2double((int)mb, (int)0xffffffffu);
+  const double M = __hiloint2double((int)mx, (int)0xffffffffu);     // >= max |W| over the tile
   const double bmax = fmax(fabs(beta_c), fabs(beta_d)) * p.jspan;   // >= |beta j| over the tile
-  // 32u covers the rounding of key / beta*i / the canonical candidate; 2^-41 covers
-  // the <1024-ulp truncation of the packed keys (|key| <= M + bmax); gfit[4] is the largest deviation
-  // of g from its affine fit, gfit[5] bounds |g| (both 0 for the linear payoff)
-  const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar + p.gfit[5]) + 0x1p-41 * (M + bmax) + p.gfit[4];
-
-  const int i = i0 + tid;
+  // 32u: rounding of key / beta i / the canonical candidate; 2^-41: the <1024-ulp
+  // truncation of packed keys, only where a packed table answers; gfit[4] / gfit[5]: the g fit's deviation
+  // and max |g| (both 0 for the linear payoff)
+  const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar + p.gfit[5]) +
+                     ((!kLevels || (uni_c && uni_d)) ? 0.0 : 0x1p-41 * (M + bmax)) + p.gfit[4];
+  // 4. OPT outputs per thread (columns i0 + tid + u * kWinThreads)
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+  const int i = i0 + tid + u * kWinThreads;
   const bool valid = i < p.S;
-  const int lane = tid & 31;
   double best = -INFINITY;
   int arg = -1;
   bool near_tie = false;
   if (valid) {
-    // charge window j in [i+1, i+Lc] = table [x, x+Lc-1]; discharge j in [i-Ld, i-1] = table [x, x+Ld-1]
-    const int x = i - i0;
+    const int x = i - i0;   // charge window: table [x, x+Lc-1]; discharge: [x, x+Ld-1]
     double mc1, mc2, md1, md2;
     int xc, xd;
-    if (uni_c) window_top2_uni(tc, (int)upc, x, x + p.Lc - 1, mc1, xc, mc2);
-    else window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
-    if (uni_d) window_top2_uni(td, (int)upd, x, x + p.Ld - 1, md1, xd, md2);
-    else window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
-    const double bci = __dsub_rn(__dmul_rn(beta_c, (double)i), gc0), bdi = __dsub_rn(__dmul_rn(beta_d, (double)i), gd0);
-    // candidates on a common scale y = key + beta*i; the action of column j is a_z - (j - i)
+    if (uni_c) win_top2_uni(kc, (int)upc, x, x + p.Lc - 1, mc1, xc, mc2);
+    else if (kLevels) window_top2(tc, x, x + p.Lc - 1, mc1, xc, mc2);
+    else win_top2_scan(kc, x, x + p.Lc - 1, mc1, xc, mc2);
+    if (uni_d) win_top2_uni(kd, (int)upd, x, x + p.Ld - 1, md1, xd, md2);
+    else if (kLevels) window_top2(td, x, x + p.Ld - 1, md1, xd, md2);
+    else win_top2_scan(kd, x, x + p.Ld - 1, md1, xd, md2);
+    const double di = (double)i;
+    const double bci = __dsub_rn(__dmul_rn(beta_c, di), gc0), bdi = __dsub_rn(__dmul_rn(beta_d, di), gd0);
+    // candidates on a common scale y = key + beta i; the action of column j is a_z - (j - i)
     double b1 = __dadd_rn(mc1, bci), b2 = __dadd_rn(mc2, bci);
-    int a1 = p.a_z - ((i0 + 1 + xc) - i);
+    int a1 = p.a_z - 1 - xc + x;                       // j = i0 + 1 + xc
     {
       const double y1 = __dadd_rn(md1, bdi), y2 = __dadd_rn(md2, bdi);
-      if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z - ((i0 - p.Ld + xd) - i); }
+      if (y1 > b1) { b2 = fmax(b1, y2); b1 = y1; a1 = p.a_z + p.Ld - xd + x; }   // j = i0 - Ld + xd
       else b2 = fmax(b2, y1);
     }
     // singles, branch-free: b2 takes the smaller of (b1, c), b1 the larger; once a single leads, b1 is its
     // exact canonical value (a later single replaces it only by a larger canonical value)
     bool single_best = false;
-    auto single_step = [&](const SingleAct& sa) {
-      const double c = canon_staged(sa, wt, wbase, i);
+    auto single_step = [&](const WinSingle& sg) {
+      const int xx = i + sg.off - wbase;
+      const double wint = (sg.w == 0.0) ? wt[xx] : __dadd_rn(__dmul_rn(sg.omw, wt[xx]), __dmul_rn(sg.w, wt[xx + 1]));
+      const double c = __dadd_rn(pay[sg.a], wint);
       const bool gt = c > b1;
       b2 = fmax(b2, gt ? b1 : c);
       b1 = gt ? c : b1;
-      a1 = gt ? sa.a : a1;
+      a1 = gt ? sg.a : a1;
       single_best |= gt;
     };
+    const int nsg = p.nsingle < kMaxSingles ? p.nsingle : kMaxSingles;
     if (p.nsingle == 3) {                   // the Eq. 10 grid: zero action and the two endpoints
 #pragma unroll
-      for (int s = 0; s < 3; ++s) single_step(ss[s]);
+      for (int s = 0; s < 3; ++s) single_step(p.sg[s]);
     } else {
-#pragma unroll 4
-      for (int s = 0; s < nsg; ++s) single_step(ss[s]);
+      for (int s = 0; s < nsg; ++s) single_step(p.sg[s]);
     }
     for (int s = nsg; s < p.nsingle; ++s) {
       const int a = __ldg(p.singles + s);
-      const double c = canon_single(p, wt, wbase, i, a, lam);
+      const double c = canon_pay(p, pay, wt, wbase, i, a);
       const bool gt = c > b1;
       b2 = fmax(b2, gt ? b1 : c);
       b1 = gt ? c : b1;
@@ -429,15 +433,8 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     }
     if (__dsub_rn(b1, b2) > 2.0 * eps) {
       arg = a1;
-      // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, w = 0), so
-      // only its power (and g) is loaded: fl(fl(fl(lambda p) - g) + W[i + o])
-      if (single_best) {
-        best = b1;
-      } else {
-        double pay = __dmul_rn(lam, __ldg(p.act + a1));
-        if (p.g_kind) pay = __dsub_rn(pay, __ldg(p.g + a1));
-        best = __dadd_rn(pay, wt[i + (p.a_z - a1) - wbase]);
-      }
+      // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, weight 0)
+      best = single_best ? b1 : __dadd_rn(pay[a1], wt[i + (p.a_z - a1) - wbase]);
     } else {
       near_tie = true;
     }
@@ -455,7 +452,7 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     int va = 0x7fffffff;
     for (int s = lane; s < p.nlive; s += 32) {
       const int a = __ldg(p.live + s);
-      const double c = canon_single(p, wt, wbase, ii, a, lam);
+      const double c = canon_pay(p, pay, wt, wbase, ii, a);
       if (c > v) { v = c; va = a; }          // ascending a within the lane
     }
 #pragma unroll
@@ -466,21 +463,24 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     }
     if (lane == src) { best = v; arg = va; atomicAdd(&g_window_fallbacks, 1ull); }
   }
-  if (!valid) { wtrace(6); return; }
-  st.V[(size_t)k * p.ld + i] = best;
-  st.pol[(size_t)k * p.S + i] = (int16_t)arg;
+  if (valid) {
+    st.V[(size_t)k * p.ld + i] = best;
+    st.pol[(size_t)k * p.S + i] = (int16_t)arg;
+  }
+  }
   wtrace(6);
 }
 
-template <bool kWait = false>
+template <bool kWait = false, int OPT = 1, bool kLevels = true>
 __device__ __forceinline__ void window_item(const WinParams& p, int k, int i0, double* wsm) {
   const WinStage st{p.W, p.V, p.pol, p.lambda_t};
-  window_item<kWait>(p, st, k, i0, wsm);
+  window_item<kWait, OPT, kLevels>(p, st, k, i0, wsm);
 }
 
+template <int OPT, bool kLevels>
 __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB) window_stencil_kernel(WinParams p) {
   extern __shared__ __align__(16) double wsm[];
-  window_item<true>(p, blockIdx.y, blockIdx.x * kWinTile, wsm);   // waits for W_t (the contraction) inside
+  window_item<true, OPT, kLevels>(p, blockIdx.y, blockIdx.x * (kWinThreads * OPT), wsm);   // waits for W_t inside
   pdl_trigger_late();
 }
 

@@ -164,3 +164,10 @@ def test_batch_kernel_times():
         assert bt.kernel_time(0, 10) > 0 and bt.kernel_time(1, 10) > 0
         with pytest.raises(E.EsdpError):
             bt.kernel_time(2, 10)   # no brute-force instances in this batch
+
+
+def test_batch_one_output_per_thread_variant(monkeypatch):
+    """The batch window kernel with one output per thread (ESDP_WIN_OPT=1; the batch default is two) gives
+    the same bits."""
+    monkeypatch.setenv("ESDP_WIN_OPT", "1")
+    _check_batch(workloads.cfg5_instances([0, 37, 300, 1023], T=8, K=10))

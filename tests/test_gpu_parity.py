@@ -683,3 +683,18 @@ def test_dmma_probe_failure_falls_back_to_dfma(name, monkeypatch):
             V, W = s.values(t)
             assert np.array_equal(V, ref.V[t - 1]) and np.array_equal(W, ref.W[t - 1])
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
+
+
+@pytest.mark.parametrize("force_nonuni", ["0", "1"])
+@pytest.mark.parametrize("opt", ["1", "2"])
+def test_window_kernel_variants(opt, force_nonuni, monkeypatch):
+    """Every window-stencil variant gives the oracle's bits: one or two outputs per thread (ESDP_WIN_OPT;
+    two is the throughput-regime default), and the non-unimodal fallbacks forced on every table
+    (ESDP_WIN_FORCE_NONUNI=1): the raw-key window scan (linear payoff) and the packed sparse tables (payoff
+    lambda p - g).  Ragged tails (S not a multiple of the tile), several tiles, T > 2."""
+    monkeypatch.setenv("ESDP_WIN_OPT", opt)
+    monkeypatch.setenv("ESDP_WIN_FORCE_NONUNI", force_nonuni)
+    for inst in (workloads.cfg2(T=5, K=12), workloads.cfg1("b"), workloads.random_instance(77, T=4, K=3, S_max=900)):
+        _compare_all(inst, nthreads=16, expect_window=True)
+    base = workloads.cfg2(T=2, K=2)
+    _compare_all(workloads.cfg3_gpu(oracle.actions(to_oracle(base)), T=5, K=8), nthreads=16, expect_window=True)

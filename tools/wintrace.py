@@ -1,7 +1,7 @@
 """Phase timing of the last stage's expectation and window-stencil blocks (diagnostic; needs
 `make -B EXTRA=-DESDP_WIN_TRACE`).  Marks are thread 0's %globaltimer (256 ns granularity on B200).
-window:      0 start, 1 after the dependency wait, 2 W staged, 3 level-0 keys, 4 levels built,
-             5 queries + singles, 6 stored
+window:      0 start, 1 payoffs + dependency wait, 2 W staged, 3 keys + unimodality reductions,
+             4 packed levels (non-unimodal only), 5 queries + singles, 6 stored
 expectation (dmma3): 0 start, 1 P chunks issued, 2 after the dependency wait, 3 first chunk landed,
              4 DMMA chain done, 5 stored"""
 import ctypes, os, sys
@@ -37,7 +37,7 @@ def report(name, bb, nb, names):
     return t0, b
 
 
-tw, bw = report("window", buf[0], 400, ["prologue+wait", "stage W", "level0+M", "levels", "queries+singles",
+tw, bw = report("window", buf[0], 400, ["pay+wait", "stage W", "keys+reduce", "levels", "queries+singles",
                                          "near-tie+store"])
 tc, bc = report("expectation", buf[1], 416, ["P issue", "wait", "chunk 0 landed", "DMMA chain", "store"])
 print("expectation first start -> window first start: %.2f us; expectation last end -> window last wait done: %.2f us"

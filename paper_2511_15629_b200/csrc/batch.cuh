@@ -63,7 +63,7 @@ typedef void (*WindowBatchKernel)(const BatchInst*, const int*, const double*, d
                                   const double*, int, int, int);
 inline WindowBatchKernel window_batch_kernel_of(int opt, int levels) {
   if (levels) return window_batch_kernel<1, true>;
-  return opt == 2 ? window_batch_kernel<2, false> : window_batch_kernel<1, false>;
+  return opt == 4 ? window_batch_kernel<4, false> : opt == 2 ? window_batch_kernel<2, false> : window_batch_kernel<1, false>;
 }
 
 // grid (tiles, K, number of brute-force instances): the brute-force stencil of kernels.cuh per instance.

@@ -2093,7 +2093,8 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   b->nbrute = (int)bidx.size();
   {   // one window variant for every window instance: levels if any instance needs them (then one output per thread)
     const char* e = getenv("ESDP_WIN_OPT");
-    b->win_opt = b->win_levels ? 1 : ((e && atoi(e) == 1) ? 1 : 2);
+    const int eo = e ? atoi(e) : 0;
+    b->win_opt = b->win_levels ? 1 : (eo == 1 || eo == 2 || eo == 4) ? eo : 2;
     for (int m : widx) {
       const esdp_ctx* c = b->inst[m];
       b->win_smem = std::max(b->win_smem, window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min, c->A, b->win_opt,

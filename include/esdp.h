@@ -70,6 +70,10 @@ enum {
 
 /* Environment variables read at context creation (measurement knobs; every setting gives the same bits):
  *   ESDP_DMMA3=0      expectation on the all-at-once staged DMMA kernel instead of the k'-pipelined one
+ *   ESDP_WIN_OPT=1|2|4  output columns per thread of the window stencil (default: 1 for a latency-bound
+ *                     grid, 4 for a large one and for batches)
+ *   ESDP_WIN_GENERIC=1  window queries on the generic path even where the Eq. 10 fast path applies
+ *   ESDP_WIN_FORCE_NONUNI=1  treat every window run table as non-unimodal (tests: the fallback paths)
  * DESIGN.md §5 and §7 record what each measured. */
 
 typedef struct {

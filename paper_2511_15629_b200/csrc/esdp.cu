@@ -785,6 +785,10 @@ WinParams win_params(const esdp_ctx* c) {
     const int a = c->singles[j];
     wp.sg[j].act = c->act[a]; wp.sg[j].w = c->w[a]; wp.sg[j].omw = c->omw[a]; wp.sg[j].off = c->off[a]; wp.sg[j].a = a;
   }
+  // the Eq. 10 grid with interpolated endpoints: singles = {charge endpoint, zero action, discharge endpoint}
+  wp.eq10 = c->singles.size() == 3 && c->singles[1] == c->a_z && c->w[c->singles[0]] != 0.0 &&
+            c->w[c->singles[2]] != 0.0 && c->singles[0] < c->a_z && c->singles[2] > c->a_z;
+  { const char* e = getenv("ESDP_WIN_GENERIC"); wp.force_generic = (e && atoi(e)) ? 1 : 0; }   // tests / measurement
   return wp;
 }
 
@@ -801,15 +805,17 @@ StencilParams stencil_params(const esdp_ctx* c) {
 // payoffs with non-unimodal run tables (LINEAR_MINUS_G); the linear payoff scans a non-unimodal window.
 void (*window_kernel_of(int opt, int levels))(WinParams) {
   if (levels) return window_stencil_kernel<1, true>;
-  return opt == 2 ? window_stencil_kernel<2, false> : window_stencil_kernel<1, false>;
+  return opt == 4 ? window_stencil_kernel<4, false> : opt == 2 ? window_stencil_kernel<2, false>
+                  : window_stencil_kernel<1, false>;
 }
-// Plan of the window kernel variant.  ESDP_WIN_OPT=1|2 in the environment overrides the choice (measurement).
+// Plan of the window kernel variant.  ESDP_WIN_OPT=1|2|4 in the environment overrides the choice (measurement).
 void plan_window(esdp_ctx* c, int64_t blocks1) {
   const char* e = getenv("ESDP_WIN_OPT");   // read per context: tests switch variants within one process
   const int env = e ? atoi(e) : 0;
   c->win_levels = c->kind == ESDP_PAYOFF_LINEAR_MINUS_G;
-  // two outputs per thread once the one-output grid exceeds ~2 waves (4 resident blocks per SM)
-  c->win_opt = c->win_levels ? 1 : (env == 1 || env == 2) ? env : (blocks1 > 2 * 4 * 148 ? 2 : 1);
+  // four outputs per thread once the one-output grid exceeds ~2 waves (4 resident blocks per SM): cfg4 stencil
+  // 7.26 (two) -> 6.31 us (four) per launch, measured (tools/winvariants.sh)
+  c->win_opt = c->win_levels ? 1 : (env == 1 || env == 2 || env == 4) ? env : (blocks1 > 2 * 4 * 148 ? 4 : 1);
   c->window_smem = window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min, c->A, c->win_opt, c->win_levels != 0);
 }
 
@@ -1848,7 +1854,7 @@ struct esdp_batch {
   int* d_widx = nullptr;                                   // window-plan instances
   int* d_bidx = nullptr;                                   // brute-force instances
   int nwin = 0, nbrute = 0;
-  int win_opt = 2, win_levels = 0;   // batch window kernel variant (window.cuh)
+  int win_opt = 4, win_levels = 0;   // batch window kernel variant (window.cuh)
   int dmma = 1;   // expectation on the FP64 tensor cores (0: the DMMA probe failed -> DFMA)
   size_t ntab_cap = 0;   // sampling-table rows the guide allocation holds (distinct P_t slices x K)
   size_t win_smem = 0, brute_smem = 0;
@@ -2094,7 +2100,7 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   {   // one window variant for every window instance: levels if any instance needs them (then one output per thread)
     const char* e = getenv("ESDP_WIN_OPT");
     const int eo = e ? atoi(e) : 0;
-    b->win_opt = b->win_levels ? 1 : (eo == 1 || eo == 2 || eo == 4) ? eo : 2;
+    b->win_opt = b->win_levels ? 1 : (eo == 1 || eo == 2 || eo == 4) ? eo : 4;
     for (int m : widx) {
       const esdp_ctx* c = b->inst[m];
       b->win_smem = std::max(b->win_smem, window_smem_bytes(c->Lc, c->Ld, c->o_max - c->o_min, c->A, b->win_opt,

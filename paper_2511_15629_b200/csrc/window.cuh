@@ -62,6 +62,9 @@ struct WinParams {
   const double* gfit;       // [6] affine fit of g on the runs: gc0, gc1, gd0, gd1, max deviation, max |g|
   int g_kind;               // 1: payoff lambda p - g(p) (kind LINEAR_MINUS_G), 0: lambda p
   int force_nonuni;         // tests: treat every run table as non-unimodal (exercises the fallback paths)
+  int eq10;                 // singles are exactly {charge endpoint (interpolated), zero action, discharge endpoint
+                            // (interpolated)} in this order: the Eq. 10 grid with eta < 1 (branch-free queries)
+  int force_generic;        // tests: take the generic query path even where the Eq. 10 one applies
   WinSingle sg[kMaxSingles];  // static data of singles[0 .. min(nsingle, kMaxSingles))
 };
 
@@ -197,6 +200,61 @@ __device__ __forceinline__ void window_top2(const RangeMax& t, int l, int r, dou
 }
 
 constexpr unsigned kNoFall = 0xffffu;   // "no fall" sentinel of the unimodality test
+
+// max of two doubles that are never NaN (W is finite or -inf): one compare and a select, no NaN fix-up
+__device__ __forceinline__ double dmx(double a, double b) { return a > b ? a : b; }
+
+// Query of one output column on the fast path: both run tables unimodal (block-uniform) and the Eq. 10
+// singles.  The window maximum of a unimodal table with peak p* sits at q = clamp(p*, l, r) and the
+// runner-up next to it; the two runs, then the three singles (canonical candidates, R14) go through one
+// top-2 with the action of the leader.  Returns false on a near tie (the caller rescans the row).
+struct WinFastRow {        // per-thread row constants of the fast path
+  double beta_c, beta_d, gc0, gd0;
+  double pay_ce, pay_z, pay_de;      // row payoffs of the charge endpoint, the zero action, the discharge endpoint
+  double w_ce, omw_ce, w_de, omw_de;
+  int off_ce, off_de, a_ce, a_de;
+  int pcs, pds;                      // peaks of the charge / discharge tables
+};
+__device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinFastRow& f, const double* __restrict__ kc,
+                                                  const double* __restrict__ kd, const double* __restrict__ wt,
+                                                  const double* __restrict__ pay, int wbase, int i, int x, double eps2,
+                                                  double& best, int& arg) {
+  const int rc = x + p.Lc - 1, rd = x + p.Ld - 1;
+  const int qc = min(max(f.pcs, x), rc), qd = min(max(f.pds, x), rd);
+  const double kc1 = kc[qc], kd1 = kd[qd];
+  const double kcl = qc > x ? kc[qc - 1] : -INFINITY, kcr = qc < rc ? kc[qc + 1] : -INFINITY;
+  const double kdl = qd > x ? kd[qd - 1] : -INFINITY, kdr = qd < rd ? kd[qd + 1] : -INFINITY;
+  const double di = (double)i;
+  const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), f.gc0), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), f.gd0);
+  // the runs on the common scale y = key + beta i; the action of table position q is a_z - (j - i)
+  double b1 = __dadd_rn(kc1, bci), b2 = __dadd_rn(dmx(kcl, kcr), bci);
+  int a1 = p.a_z - 1 - qc + x;
+  {
+    const double y1 = __dadd_rn(kd1, bdi), y2 = __dadd_rn(dmx(kdl, kdr), bdi);
+    const bool g = y1 > b1;
+    b2 = g ? dmx(b1, y2) : dmx(b2, y1);
+    b1 = g ? y1 : b1;
+    a1 = g ? p.a_z + p.Ld - qd + x : a1;
+  }
+  // singles, canonical: once a single leads, b1 is its exact value
+  const double* wi = wt + (i - wbase);
+  bool sb = false;
+  auto single = [&](double c, int a) {
+    const bool g = c > b1;
+    b2 = g ? b1 : dmx(b2, c);
+    b1 = g ? c : b1;
+    a1 = g ? a : a1;
+    sb |= g;
+  };
+  single(__dadd_rn(f.pay_ce, __dadd_rn(__dmul_rn(f.omw_ce, wi[f.off_ce]), __dmul_rn(f.w_ce, wi[f.off_ce + 1]))), f.a_ce);
+  single(__dadd_rn(f.pay_z, wi[0]), p.a_z);
+  single(__dadd_rn(f.pay_de, __dadd_rn(__dmul_rn(f.omw_de, wi[f.off_de]), __dmul_rn(f.w_de, wi[f.off_de + 1]))), f.a_de);
+  if (!(__dsub_rn(b1, b2) > eps2)) return false;
+  arg = a1;
+  // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, weight 0)
+  best = sb ? b1 : __dadd_rn(pay[a1], wi[p.a_z - a1]);
+  return true;
+}
 
 // One (k, 256-column tile) item of the window stencil, executed by a 256-thread block.
 //   1. Row payoffs pay[a] = fl(fl(lambda_{t,k} p_a) - g_a) (R14) for every action, in shared memory: inputs
@@ -375,6 +433,17 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   const double eps = 32.0 * 0x1p-53 * (M + bmax + fabs(lam) * p.pbar + p.gfit[5]) +
                      ((!kLevels || (uni_c && uni_d)) ? 0.0 : 0x1p-41 * (M + bmax)) + p.gfit[4];
   // 4. OPT outputs per thread (columns i0 + tid + u * kWinThreads)
+  const bool fast = uni_c && uni_d && p.eq10 && !p.force_generic;   // block-uniform
+  WinFastRow fr;
+  if (fast) {
+    fr.beta_c = beta_c; fr.beta_d = beta_d; fr.gc0 = gc0; fr.gd0 = gd0;
+    fr.pcs = (int)upc; fr.pds = (int)upd;
+    const WinSingle &sc = p.sg[0], &sd = p.sg[2];
+    fr.a_ce = sc.a; fr.off_ce = sc.off; fr.w_ce = sc.w; fr.omw_ce = sc.omw;
+    fr.a_de = sd.a; fr.off_de = sd.off; fr.w_de = sd.w; fr.omw_de = sd.omw;
+    fr.pay_ce = pay[sc.a]; fr.pay_z = pay[p.a_z]; fr.pay_de = pay[sd.a];
+  }
+  const double eps2 = 2.0 * eps;
 #pragma unroll
   for (int u = 0; u < OPT; ++u) {
   const int i = i0 + tid + u * kWinThreads;
@@ -382,7 +451,9 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   double best = -INFINITY;
   int arg = -1;
   bool near_tie = false;
-  if (valid) {
+  if (valid && fast) {
+    near_tie = !window_query_fast(p, fr, kc, kd, wt, pay, wbase, i, i - i0, eps2, best, arg);
+  } else if (valid) {
     const int x = i - i0;   // charge window: table [x, x+Lc-1]; discharge: [x, x+Ld-1]
     double mc1, mc2, md1, md2;
     int xc, xd;

@@ -166,8 +166,11 @@ def test_batch_kernel_times():
             bt.kernel_time(2, 10)   # no brute-force instances in this batch
 
 
-def test_batch_one_output_per_thread_variant(monkeypatch):
-    """The batch window kernel with one output per thread (ESDP_WIN_OPT=1; the batch default is two) gives
-    the same bits."""
-    monkeypatch.setenv("ESDP_WIN_OPT", "1")
+@pytest.mark.parametrize("generic", ["0", "1"])
+@pytest.mark.parametrize("opt", ["1", "2", "4"])
+def test_batch_window_variants(opt, generic, monkeypatch):
+    """The batch window kernel with one, two or four outputs per thread (ESDP_WIN_OPT), on the Eq. 10 fast
+    query path or forced onto the generic one (ESDP_WIN_GENERIC=1), gives the same bits."""
+    monkeypatch.setenv("ESDP_WIN_OPT", opt)
+    monkeypatch.setenv("ESDP_WIN_GENERIC", generic)
     _check_batch(workloads.cfg5_instances([0, 37, 300, 1023], T=8, K=10))

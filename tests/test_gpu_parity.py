@@ -685,15 +685,20 @@ def test_dmma_probe_failure_falls_back_to_dfma(name, monkeypatch):
             assert np.array_equal(s.policy(t), ref.pol[t - 1])
 
 
+@pytest.mark.parametrize("generic", ["0", "1"])
 @pytest.mark.parametrize("force_nonuni", ["0", "1"])
-@pytest.mark.parametrize("opt", ["1", "2"])
-def test_window_kernel_variants(opt, force_nonuni, monkeypatch):
-    """Every window-stencil variant gives the oracle's bits: one or two outputs per thread (ESDP_WIN_OPT;
-    two is the throughput-regime default), and the non-unimodal fallbacks forced on every table
-    (ESDP_WIN_FORCE_NONUNI=1): the raw-key window scan (linear payoff) and the packed sparse tables (payoff
-    lambda p - g).  Ragged tails (S not a multiple of the tile), several tiles, T > 2."""
+@pytest.mark.parametrize("opt", ["1", "2", "4"])
+def test_window_kernel_variants(opt, force_nonuni, generic, monkeypatch):
+    """Every window-stencil variant gives the oracle's bits: one, two or four outputs per thread
+    (ESDP_WIN_OPT; four is the throughput-regime default), the Eq. 10 fast query path or the generic one
+    (ESDP_WIN_GENERIC=1), and the non-unimodal fallbacks forced on every table (ESDP_WIN_FORCE_NONUNI=1): the
+    raw-key window scan (linear payoff) and the packed sparse tables (payoff lambda p - g).  Ragged tails (S
+    not a multiple of the tile), several tiles, T > 2."""
+    if generic == "1" and force_nonuni == "1":
+        pytest.skip("the non-unimodal fallbacks never take the fast path")
     monkeypatch.setenv("ESDP_WIN_OPT", opt)
     monkeypatch.setenv("ESDP_WIN_FORCE_NONUNI", force_nonuni)
+    monkeypatch.setenv("ESDP_WIN_GENERIC", generic)
     for inst in (workloads.cfg2(T=5, K=12), workloads.cfg1("b"), workloads.random_instance(77, T=4, K=3, S_max=900)):
         _compare_all(inst, nthreads=16, expect_window=True)
     base = workloads.cfg2(T=2, K=2)

@@ -20,12 +20,13 @@ struct BatchInst {
 };
 
 // Block-cooperative copy of a trivially copyable struct from global to shared memory.
-template <class T>
-__device__ __forceinline__ void copy_struct(T& dst, const T& src) {
+template <int NT, class T>
+__device__ __forceinline__ void copy_struct(T& dst, const T& src) {   // NT = blockDim.x
   static_assert(sizeof(T) % 4 == 0, "word copy");
   const int* s = reinterpret_cast<const int*>(&src);
   int* d = reinterpret_cast<int*>(&dst);
-  for (int j = threadIdx.x; j < (int)(sizeof(T) / 4); j += blockDim.x) d[j] = __ldg(s + j);
+#pragma unroll
+  for (int j = threadIdx.x; j < (int)(sizeof(T) / 4); j += NT) d[j] = __ldg(s + j);
 }
 
 // grid (tiles, K, number of window instances); idx maps blockIdx.z to the instance.  W_t / V_t rows are
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(kWinThreads, ESDP_WIN_MINB_BATCH) window_batch
   extern __shared__ __align__(16) double wsm[];
   __shared__ WinParams p;
   const int m = __ldg(idx + blockIdx.z);
-  copy_struct(p, bi[m].wp);
+  copy_struct<kWinThreads>(p, bi[m].wp);
   __syncthreads();
   if (threadIdx.x == 0) {
     p.W = Wt + (size_t)m * ld;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kStencilWarps * 32) stencil_batch_kernel(const
   extern __shared__ double smem[];
   __shared__ StencilParams p;
   const int m = __ldg(idx + blockIdx.z);
-  copy_struct(p, bi[m].sp);
+  copy_struct<kStencilWarps * 32>(p, bi[m].sp);
   __syncthreads();
   if (threadIdx.x == 0) {
     p.W = Wt + (size_t)m * ld;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(128) simulate_batch_kernel(const BatchInst* __
   extern __shared__ __align__(16) double ssm[];
   __shared__ SimParams sp;
   const int m = blockIdx.y;
-  copy_struct(sp, bi[m].sim);
+  copy_struct<128>(sp, bi[m].sim);
   __syncthreads();
   simulate_block(sp, n_paths, seed + (uint64_t)m, out + (size_t)m * n_paths, ssm);
 }

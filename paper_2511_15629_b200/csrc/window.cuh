@@ -283,17 +283,27 @@ __device__ __forceinline__ double canon_pay(const WinParams& p, const double* __
   return __dadd_rn(pay[a], wint);
 }
 
-// rise / fall bookkeeping of entry x of a raw key table (x >= 1): up = last rise, dn = first fall
-__device__ __forceinline__ void win_key(double* __restrict__ tb, const double* __restrict__ wt, int wbase, int j0, int x,
-                                        double beta, unsigned& up, unsigned& dn) {
+// Keys x and x + 1 of a raw key table (x even, 16-byte aligned pair store) with the rise / fall bookkeeping of
+// entries x and x + 1: three W loads and three keys (key x - 1 recomputed, the same bits) per two entries.
+__device__ __forceinline__ void win_key_pair(double* __restrict__ tb, const double* __restrict__ wt, int wbase, int j0,
+                                             int x, int n, double beta, unsigned& up, unsigned& dn) {
   const int j = j0 + x;
+  const double* w = wt + (j - wbase);
   const double jd = (double)j;
-  const double key = __dsub_rn(wt[j - wbase], __dmul_rn(beta, jd));
-  tb[x] = key;
+  const double k0 = __dsub_rn(w[0], __dmul_rn(beta, jd));
+  const bool two = x + 1 < n;
+  const double k1 = two ? __dsub_rn(w[1], __dmul_rn(beta, __dadd_rn(jd, 1.0))) : 0.0;
   if (x >= 1) {
-    const double prev = __dsub_rn(wt[j - 1 - wbase], __dmul_rn(beta, __dsub_rn(jd, 1.0)));
-    if (key > prev) up = umax(up, (unsigned)x);
-    if (key < prev) dn = umin(dn, (unsigned)x);
+    const double km = __dsub_rn(w[-1], __dmul_rn(beta, __dsub_rn(jd, 1.0)));
+    if (k0 > km) up = umax(up, (unsigned)x);
+    if (k0 < km) dn = umin(dn, (unsigned)x);
+  }
+  if (two) {
+    if (k1 > k0) up = umax(up, (unsigned)(x + 1));
+    if (k1 < k0) dn = umin(dn, (unsigned)(x + 1));
+    *reinterpret_cast<double2*>(tb + x) = make_double2(k0, k1);
+  } else {
+    tb[x] = k0;
   }
 }
 
@@ -350,10 +360,11 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   // 2. W_t over the tile: all of this thread's loads are issued before anything waits on them
   constexpr int kWReg = 2 + OPT;
   double wv[kWReg];
+  const double* wsrc = Wrow + (wbase + tid);   // dereferenced only inside [0, S)
 #pragma unroll
   for (int u = 0; u < kWReg; ++u) {
-    const int x = tid + u * kWinThreads, col = wbase + x;
-    wv[u] = (x < nw && col >= 0 && col < p.S) ? __ldcg(Wrow + col) : -INFINITY;
+    const int x = tid + u * kWinThreads;
+    wv[u] = (x < nw && (unsigned)(wbase + x) < (unsigned)p.S) ? __ldcg(wsrc + u * kWinThreads) : -INFINITY;
   }
   unsigned mx = 0u;
 #pragma unroll
@@ -379,9 +390,9 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   wtrace(2);
   // 3. raw key tables with the unimodality bookkeeping
   unsigned upc = 0u, dnc = kNoFall, upd = 0u, dnd = kNoFall;
-  for (int x = tid; x < nc || x < nd; x += kWinThreads) {
-    if (x < nc) win_key(kc, wt, wbase, i0 + 1, x, beta_c, upc, dnc);
-    if (x < nd) win_key(kd, wt, wbase, i0 - p.Ld, x, beta_d, upd, dnd);
+  for (int x = 2 * tid; x < nc || x < nd; x += 2 * kWinThreads) {
+    if (x < nc) win_key_pair(kc, wt, wbase, i0 + 1, x, nc, beta_c, upc, dnc);
+    if (x < nd) win_key_pair(kd, wt, wbase, i0 - p.Ld, x, nd, beta_d, upd, dnd);
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   upc = __reduce_max_sync(0xffffffffu, upc);
@@ -434,6 +445,8 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
                      ((!kLevels || (uni_c && uni_d)) ? 0.0 : 0x1p-41 * (M + bmax)) + p.gfit[4];
   // 4. OPT outputs per thread (columns i0 + tid + u * kWinThreads)
   const bool fast = uni_c && uni_d && p.eq10 && !p.force_generic;   // block-uniform
+  double* const vrow = st.V + (size_t)k * p.ld;
+  short* const prow = reinterpret_cast<short*>(st.pol + (size_t)k * p.S);
   WinFastRow fr;
   if (fast) {
     fr.beta_c = beta_c; fr.beta_d = beta_d; fr.gc0 = gc0; fr.gd0 = gd0;
@@ -534,9 +547,9 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
     }
     if (lane == src) { best = v; arg = va; atomicAdd(&g_window_fallbacks, 1ull); }
   }
-  if (valid) {
-    st.V[(size_t)k * p.ld + i] = best;
-    st.pol[(size_t)k * p.S + i] = (int16_t)arg;
+  if (valid) {   // st.global: the compiler then knows these stores do not alias the shared-memory tables
+    __stwb(vrow + i, best);
+    __stwb(prow + i, (short)arg);
   }
   }
   wtrace(6);

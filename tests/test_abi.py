@@ -95,3 +95,34 @@ def test_binding_has_no_fallback():
     """The binding exposes only the C ABI; there is no numpy/CPU compute path to fall back to."""
     src = open(os.path.join(ROOT, "paper_2511_15629_b200", "__init__.py")).read()
     assert "import torch" not in src and "oracle" not in src
+
+
+def test_header_compiles_as_c_and_matches_binding_layout(tmp_path):
+    """A plain C11 program compiles against include/esdp.h, links against libesdp.so taking the address of
+    every declared entry point (no call, so no GPU), and prints the esdp_problem layout; the ctypes struct of
+    the binding must have the same size and field offsets (the binding hand-declares it)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    names = _declared()
+    fields = [f for f, _ in E.esdp_problem._fields_]
+    cfield = {"lambda_": "lambda"}
+    src = ["#include <stdio.h>", "#include <stddef.h>", '#include "esdp.h"',
+           "_Static_assert(sizeof(int32_t) == 4 && sizeof(double) == 8, \"LP64 ABI\");",
+           "typedef void (*fn_t)(void);", "int main(void) {", "  const fn_t fns[] = {"]
+    src += [f"    (fn_t)&{n}," for n in names]
+    src += ["  };", "  int n = 0;", "  for (unsigned i = 0; i < sizeof fns / sizeof fns[0]; ++i) n += fns[i] != 0;",
+            '  printf("%d %zu\\n", n, sizeof(esdp_problem));']
+    src += [f'  printf("%zu\\n", offsetof(esdp_problem, {cfield.get(f, f)}));' for f in fields]
+    src += ["  return 0;", "}"]
+    c = tmp_path / "abi.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = tmp_path / "abi"
+    lib = os.path.dirname(E.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"), str(c),
+                    "-o", str(exe), "-L", lib, "-l:libesdp.so", f"-Wl,-rpath,{lib}"], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert int(out[0]) == len(names)
+    assert int(out[1]) == ctypes.sizeof(E.esdp_problem)
+    assert [int(x) for x in out[2:]] == [getattr(E.esdp_problem, f).offset for f in fields]

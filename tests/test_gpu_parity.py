@@ -225,6 +225,22 @@ def test_cfg4_slice():
     _compare_all(inst, nthreads=16, expect_window=True)
 
 
+@pytest.mark.parametrize("brute", [False, True])
+def test_cfg3i_table2_analog(brute):
+    """cfg3i, the Table-2 analog: K = 1, T = 72 hourly, every price level-shifted <= 0,
+    s0 = sbar, eta = sqrt(0.85) (interpolated endpoints).  Every V_t, W_t, pol_t and J bit-identical to the
+    oracle (whose LP / MILP ordering pins are in test_oracle_backward.py), on both stencils; with prices
+    <= 0 charging is paid or free, so J >= 0 and the last stage never discharges at a negative price."""
+    inst = workloads.cfg3_small()
+    assert inst.lam.max() <= 0.0
+    ref = _compare_all(inst, brute=brute, expect_window=not brute)
+    assert ref.J >= 0.0
+    acts = oracle.actions(to_oracle(inst))
+    lam_T = inst.lam[-1, 0]
+    if lam_T < 0:
+        assert np.all(acts[ref.pol[-1][0]] <= 0.0)
+
+
 def test_cfg3_nonconcave_payoff_and_bids():
     """configs[2]: negative prices, degradation + fixed cycling cost (non-concave payoff), monotone
     bid curves (bit-exact vertices and prices) on a sample of (t, i, k)."""

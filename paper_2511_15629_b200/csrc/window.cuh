@@ -208,33 +208,32 @@ __device__ __forceinline__ double dmx(double a, double b) { return a > b ? a : b
 // singles.  The window maximum of a unimodal table with peak p* sits at q = clamp(p*, l, r) and the
 // runner-up next to it; the two runs, then the three singles (canonical candidates, R14) go through one
 // top-2 with the action of the leader.  Returns false on a near tie (the caller rescans the row).
-struct WinFastRow {        // per-thread row constants of the fast path
-  double beta_c, beta_d, gc0, gd0;
-  double pay_ce, pay_z, pay_de;      // row payoffs of the charge endpoint, the zero action, the discharge endpoint
-  double w_ce, omw_ce, w_de, omw_de;
-  int off_ce, off_de, a_ce, a_de;
-  int pcs, pds;                      // peaks of the charge / discharge tables
+struct WinFastRow {        // per-thread row constants of the fast path (the rest is read from p: constant bank or,
+                           // in the batch kernel, broadcast shared-memory loads)
+  double beta_c, beta_d, pay_z;
+  int pcs, pds;            // peaks of the charge / discharge tables
 };
 __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinFastRow& f, const double* __restrict__ kc,
                                                   const double* __restrict__ kd, const double* __restrict__ wt,
                                                   const double* __restrict__ pay, int wbase, int i, int x, double eps2,
                                                   double& best, int& arg) {
-  const int rc = x + p.Lc - 1, rd = x + p.Ld - 1;
+  const int Lc = p.Lc, Ld = p.Ld, a_z = p.a_z;
+  const int rc = x + Lc - 1, rd = x + Ld - 1;
   const int qc = min(max(f.pcs, x), rc), qd = min(max(f.pds, x), rd);
   const double kc1 = kc[qc], kd1 = kd[qd];
   const double kcl = qc > x ? kc[qc - 1] : -INFINITY, kcr = qc < rc ? kc[qc + 1] : -INFINITY;
   const double kdl = qd > x ? kd[qd - 1] : -INFINITY, kdr = qd < rd ? kd[qd + 1] : -INFINITY;
   const double di = (double)i;
-  const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), f.gc0), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), f.gd0);
+  const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), p.gfit[0]), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), p.gfit[2]);
   // the runs on the common scale y = key + beta i; the action of table position q is a_z - (j - i)
   double b1 = __dadd_rn(kc1, bci), b2 = __dadd_rn(dmx(kcl, kcr), bci);
-  int a1 = p.a_z - 1 - qc + x;
+  int a1 = a_z - 1 - qc + x;
   {
     const double y1 = __dadd_rn(kd1, bdi), y2 = __dadd_rn(dmx(kdl, kdr), bdi);
     const bool g = y1 > b1;
     b2 = g ? dmx(b1, y2) : dmx(b2, y1);
     b1 = g ? y1 : b1;
-    a1 = g ? p.a_z + p.Ld - qd + x : a1;
+    a1 = g ? a_z + Ld - qd + x : a1;
   }
   // singles, canonical: once a single leads, b1 is its exact value
   const double* wi = wt + (i - wbase);
@@ -246,13 +245,14 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
     a1 = g ? a : a1;
     sb |= g;
   };
-  single(__dadd_rn(f.pay_ce, __dadd_rn(__dmul_rn(f.omw_ce, wi[f.off_ce]), __dmul_rn(f.w_ce, wi[f.off_ce + 1]))), f.a_ce);
-  single(__dadd_rn(f.pay_z, wi[0]), p.a_z);
-  single(__dadd_rn(f.pay_de, __dadd_rn(__dmul_rn(f.omw_de, wi[f.off_de]), __dmul_rn(f.w_de, wi[f.off_de + 1]))), f.a_de);
+  const WinSingle &sc = p.sg[0], &sd = p.sg[2];
+  single(__dadd_rn(pay[sc.a], __dadd_rn(__dmul_rn(sc.omw, wi[sc.off]), __dmul_rn(sc.w, wi[sc.off + 1]))), sc.a);
+  single(__dadd_rn(f.pay_z, wi[0]), a_z);
+  single(__dadd_rn(pay[sd.a], __dadd_rn(__dmul_rn(sd.omw, wi[sd.off]), __dmul_rn(sd.w, wi[sd.off + 1]))), sd.a);
   if (!(__dsub_rn(b1, b2) > eps2)) return false;
   arg = a1;
   // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, weight 0)
-  best = sb ? b1 : __dadd_rn(pay[a1], wi[p.a_z - a1]);
+  best = sb ? b1 : __dadd_rn(pay[a1], wi[a_z - a1]);
   return true;
 }
 
@@ -449,12 +449,8 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   short* const prow = reinterpret_cast<short*>(st.pol + (size_t)k * p.S);
   WinFastRow fr;
   if (fast) {
-    fr.beta_c = beta_c; fr.beta_d = beta_d; fr.gc0 = gc0; fr.gd0 = gd0;
+    fr.beta_c = beta_c; fr.beta_d = beta_d; fr.pay_z = pay[p.a_z];
     fr.pcs = (int)upc; fr.pds = (int)upd;
-    const WinSingle &sc = p.sg[0], &sd = p.sg[2];
-    fr.a_ce = sc.a; fr.off_ce = sc.off; fr.w_ce = sc.w; fr.omw_ce = sc.omw;
-    fr.a_de = sd.a; fr.off_de = sd.off; fr.w_de = sd.w; fr.omw_de = sd.omw;
-    fr.pay_ce = pay[sc.a]; fr.pay_z = pay[p.a_z]; fr.pay_de = pay[sd.a];
   }
   const double eps2 = 2.0 * eps;
 #pragma unroll

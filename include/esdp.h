@@ -63,9 +63,14 @@ enum {
   ESDP_NO_PDL = 8u,       /* launch the per-stage kernels without programmatic dependent launch (PDL
                              with a late trigger is the default: ~3.5% faster chain) */
   ESDP_NO_DMMA = 16u,     /* expectation on FP64 CUDA cores (DFMA) instead of the FP64 tensor cores */
-  ESDP_FLAGS_ALL = 31u    /* every defined flag; other bits -> ESDP_E_CONFIG.  Bits 32 (persistent
-                             dataflow backward) and 64 (DMMA operands straight from L2) named paths that
-                             measured slower on B200 and were removed. */
+  ESDP_CONTRACT_OZAKI = 32u, /* batches (esdp_create_batch, flag of probs[0]) with K <= 128 and a zero
+                             action of payoff >= 0 (so V >= 0): the expectation on the 5th-generation
+                             tensor cores, Ozaki-sliced u8 tcgen05 products.  NOT
+                             the canonical chain of R15: W within ~1e-14 relative of the exact product,
+                             policies may differ at documented near-ties.  Ignored (the
+                             DMMA path runs) where the conditions fail: esdp_batch_plan reports it. */
+  ESDP_FLAGS_ALL = 63u    /* every defined flag; other bits -> ESDP_E_CONFIG.  Bit 64 once named a
+                             path that measured slower on B200 and was removed. */
 };
 
 /* Environment variables read at context creation (measurement knobs; every setting gives the same bits):
@@ -328,6 +333,18 @@ esdp_status esdp_batch_launch_count(const esdp_batch* b, int64_t* n);
  * (1) or brute-force stencil (2) kernel, reps back-to-back launches in a CUDA graph (CUDA events on the
  * batch's stream).  Needs a completed backward pass (its buffers are the inputs). */
 esdp_status esdp_batch_kernel_time(esdp_batch* b, int32_t what, int32_t reps, double* us_per_launch);
+/* Plan of the batch's expectation: 0 FP64 DMMA (canonical chain), 1 DFMA (canonical chain), 2 Ozaki u8
+ * tcgen05 (ESDP_CONTRACT_OZAKI granted). */
+esdp_status esdp_batch_plan(const esdp_batch* b, int32_t* contraction);
+/* The expectation alone (a2; Alg. 1 line 11; Eq. 6): W[m][n] = sum_k' P[m][k'] V[k'][n] for m < rows,
+ * n < ncols, on DEVICE buffers: P [rows][K] (row stride K), V [K][ldv], W [rows][ldw]; enqueued on
+ * stream (NULL: the legacy default stream), not synchronized.  method 0: the canonical ascending-k' fma
+ * chain (R15) on the FP64 tensor cores (DMMA; DFMA for odd K or fewer than 8 rows), bit-identical to the
+ * oracle; requires ldv == ldw.  method 1: the Ozaki-sliced u8 tcgen05 product (ozaki.cuh): requires
+ * rows <= 128, K <= 128 and non-negative, finite P and V (not checked on the device: negative entries give
+ * wrong results).  ESDP_E_CONFIG on bad sizes, strides or method; ESDP_E_CUDA on a launch failure. */
+esdp_status esdp_expectation_dev(const double* P_dev, const double* V_dev, double* W_dev, int32_t rows, int32_t K,
+                                 int64_t ncols, int64_t ldv, int64_t ldw, int32_t method, void* stream);
 void esdp_batch_destroy(esdp_batch* b);
 /* Message of the last failing call on b (b == NULL: last esdp_create_batch failure of this thread). */
 const char* esdp_batch_last_error(const esdp_batch* b);

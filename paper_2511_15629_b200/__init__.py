@@ -31,7 +31,8 @@ ESDP_PROFILE = 2
 ESDP_FORCE_BRUTE = 4
 ESDP_NO_PDL = 8
 ESDP_NO_DMMA = 16
-ESDP_FLAGS_ALL = 31
+ESDP_CONTRACT_OZAKI = 32
+ESDP_FLAGS_ALL = 63
 ESDP_SIM_LOTTERY, ESDP_SIM_PHYSICAL, ESDP_SIM_CLEAR_BIDS, ESDP_SIM_SELF, ESDP_SIM_FIXED = 0, 1, 2, 3, 4
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libesdp.so")
@@ -47,7 +48,7 @@ EXPORTED_SYMBOLS = [
     "esdp_create_batch", "esdp_batch_dims", "esdp_batch_backward", "esdp_batch_backward_async",
     "esdp_batch_objective", "esdp_batch_policy", "esdp_batch_value1", "esdp_batch_simulate_dev",
     "esdp_batch_launch_count", "esdp_batch_destroy", "esdp_batch_last_error", "esdp_batch_load_async",
-    "esdp_batch_kernel_time",
+    "esdp_batch_kernel_time", "esdp_batch_plan", "esdp_expectation_dev",
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -126,6 +127,9 @@ def _load():
         "esdp_batch_launch_count": ([ctx, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "esdp_batch_load_async": ([ctx, _vp, _vp, _vp, _vp], ctypes.c_int),
         "esdp_batch_kernel_time": ([ctx, ctypes.c_int32, ctypes.c_int32, _dp], ctypes.c_int),
+        "esdp_batch_plan": ([ctx, _i32p], ctypes.c_int),
+        "esdp_expectation_dev": ([_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_int64, ctypes.c_int32, _vp], ctypes.c_int),
         "esdp_batch_destroy": ([ctx], None),
         "esdp_batch_last_error": ([ctx], ctypes.c_char_p),
     }
@@ -428,7 +432,7 @@ class Solver:
 class Batch:
     """A batch of instances sharing one price model (esdp_create_batch, cfg5): one graph for all."""
 
-    def __init__(self, insts, force_brute=False):
+    def __init__(self, insts, force_brute=False, ozaki=False):
         keep = []
         probs = (esdp_problem * len(insts))()
         for j, inst in enumerate(insts):   # every instance's own arrays: the library checks they match
@@ -440,8 +444,9 @@ class Batch:
                                     float(inst.eta_c), float(inst.eta_d), float(inst.delta),
                                     0 if act is None else int(act.shape[0]), _p(act), _p(lam), _p(P), _p(pi),
                                     int(getattr(inst, "payoff_kind", ESDP_PAYOFF_LINEAR)), _p(g),
-                                    ESDP_FORCE_BRUTE if (force_brute[j] if isinstance(force_brute, (list, tuple))
-                                                         else force_brute) else 0)
+                                    (ESDP_FORCE_BRUTE if (force_brute[j] if isinstance(force_brute, (list, tuple))
+                                                          else force_brute) else 0) |
+                                    (ESDP_CONTRACT_OZAKI if ozaki else 0))
         out = _vp()
         st = lib.esdp_create_batch(probs, len(insts), ctypes.byref(out))
         if st != ESDP_OK:
@@ -500,6 +505,13 @@ class Batch:
         self._check(lib.esdp_batch_kernel_time(self.b, int(what), int(reps), ctypes.byref(us)), "esdp_batch_kernel_time")
         return us.value
 
+    @property
+    def plan(self):
+        """Expectation plan (esdp_batch_plan): 0 FP64 DMMA, 1 DFMA, 2 Ozaki u8 tcgen05."""
+        v = ctypes.c_int32()
+        self._check(lib.esdp_batch_plan(self.b, ctypes.byref(v)), "esdp_batch_plan")
+        return v.value
+
     def close(self):
         if self.b:
             lib.esdp_batch_destroy(self.b)
@@ -516,3 +528,12 @@ class Batch:
             self.close()
         except Exception:
             pass
+
+
+def expectation_dev(P_ptr, V_ptr, W_ptr, rows, K, ncols, ldv, ldw, method, stream=None):
+    """esdp_expectation_dev: W = P V on device buffers (method 0 canonical DMMA chain, 1 Ozaki u8 tcgen05)."""
+    st = lib.esdp_expectation_dev(P_ptr, V_ptr, W_ptr, int(rows), int(K), int(ncols), int(ldv), int(ldw), int(method),
+                                  stream)
+    if st != ESDP_OK:
+        m = lib.esdp_batch_last_error(None)
+        raise EsdpError(st, "esdp_expectation_dev", m.decode() if m else "")

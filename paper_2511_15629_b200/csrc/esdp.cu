@@ -28,6 +28,7 @@
 #include "window.cuh"
 #include "batch.cuh"
 #include "simmodes.cuh"
+#include "ozaki.cuh"
 
 using namespace esdp;
 
@@ -735,6 +736,23 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
                          cudaStream_t s, bool pdl) {
   return which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
+}
+
+// Ozaki-sliced u8 tcgen05 expectation (ozaki.cuh): one persistent CTA per SM over 32-column tiles.
+// Requires rows <= 128, K <= 128, non-negative P and V.
+cudaError_t launch_ozaki(const double* Pt, const double* Vn, double* Wt, int rows, int K, long long ncols, long long ldv,
+                         long long ldw, cudaStream_t s, bool pdl) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const cudaError_t e = cudaFuncSetAttribute(ozaki_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem);
+    if (e != cudaSuccess) { nsm = 0; return e; }
+  }
+  const long long ntiles = (ncols + kOzN - 1) / kOzN;
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles, nsm));
+  return launch(ozaki_contract_kernel, dim3(grid), dim3(kOzThreads), kOzSmem, s, pdl, Pt, Vn, Wt, rows, K, ncols, ldv, ldw);
 }
 
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
@@ -1856,6 +1874,7 @@ struct esdp_batch {
   int nwin = 0, nbrute = 0;
   int win_opt = 4, win_levels = 0;   // batch window kernel variant (window.cuh)
   int dmma = 1;   // expectation on the FP64 tensor cores (0: the DMMA probe failed -> DFMA)
+  int ozaki = 0;  // expectation as Ozaki-sliced u8 tcgen05 products (ESDP_CONTRACT_OZAKI granted, ozaki.cuh)
   size_t ntab_cap = 0;   // sampling-table rows the guide allocation holds (distinct P_t slices x K)
   size_t win_smem = 0, brute_smem = 0;
   cudaStream_t stream = nullptr;
@@ -1912,6 +1931,7 @@ cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, b
   const double* V_n = b->d_V + (size_t)(t & 1) * K * NL;   // V_{t+1}
   if (what == 0) {
     const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
+    if (b->ozaki) return launch_ozaki(Pt, V_n, b->d_W, K, K, (long long)NL, (long long)NL, (long long)NL, s, pdl);
     if (const int d3 = (b->rank1 || !b->dmma) ? 0 : use_dmma3(rows, (int64_t)NL, K))
       return launch_dmma3(d3, Pt, V_n, b->d_W, rows, K, (int)NL, (int)NL, s, pdl);
     if (b->dmma && !b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
@@ -2020,6 +2040,16 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
   }
   esdp_ctx* c0 = b->inst[0];
   b->T = c0->T; b->K = c0->K; b->S = c0->S; b->ld = c0->ld; b->rank1 = c0->rank1; b->g_max = c0->g_max;
+  if ((p0.flags & ESDP_CONTRACT_OZAKI) && !b->rank1 && b->K <= kOzM && b->K <= kOzK) {
+    // granted when every V_{t+1} >= 0 (the digits are unsigned): the zero action's payoff is >= 0 in every
+    // instance (R18: V_t >= P_t V_{t+1} >= 0); P is validated stochastic, so P >= 0
+    bool nonneg = true;
+    for (int m = 0; m < n; ++m) {
+      const esdp_ctx* c = b->inst[m];
+      if (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G && !(probs[m].g[c->a_z] <= 0.0)) nonneg = false;
+    }
+    b->ozaki = nonneg ? 1 : 0;
+  }
   {   // the shared inputs, validated once (as esdp_create does)
     esdp_status st = validate_data(c0, p0.lambda, p0.P, p0.pi, p0.g);
     if (st != ESDP_OK) { b->err = c0->err; return bail(st); }
@@ -2236,6 +2266,41 @@ esdp_status esdp_batch_load_async(esdp_batch* b, const double* lambda, const dou
   launch_cdf(b->d_pi, nullptr, 1, (int)K, b->g_max, b->d_cdf1, b->d_guide1, s);
   BCUDA(b, cudaGetLastError());
   return ESDP_OK;   // tab / src are pageable: cudaMemcpyAsync has staged them before returning
+}
+
+esdp_status esdp_batch_plan(const esdp_batch* b, int32_t* contraction) {
+  if (!b || !contraction) return ESDP_E_CONFIG;
+  *contraction = b->ozaki ? 2 : b->dmma ? 0 : 1;
+  return ESDP_OK;
+}
+
+esdp_status esdp_expectation_dev(const double* P_dev, const double* V_dev, double* W_dev, int32_t rows, int32_t K,
+                                 int64_t ncols, int64_t ldv, int64_t ldw, int32_t method, void* stream) {
+  g_create_error.clear();
+  if (!P_dev || !V_dev || !W_dev || rows < 1 || K < 1 || ncols < 1 || ldv < ncols || ldw < ncols)
+    return bfail(nullptr, ESDP_E_CONFIG, "esdp_expectation_dev: null buffer or bad size / stride");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (method == 1) {
+    if (rows > kOzM || K > kOzK) return bfail(nullptr, ESDP_E_CONFIG, "esdp_expectation_dev: Ozaki needs rows, K <= 128");
+    e = launch_ozaki(P_dev, V_dev, W_dev, rows, K, (long long)ncols, (long long)ldv, (long long)ldw, s, false);
+  } else if (method == 0) {
+    if (ldv != ldw || ldv > INT32_MAX) return bfail(nullptr, ESDP_E_CONFIG, "esdp_expectation_dev: method 0 needs ldv == ldw < 2^31");
+    if (const int d3 = dmma_probe_mismatches() == 0 ? use_dmma3(rows, ncols, K) : 0) {
+      e = launch_dmma3(d3, P_dev, V_dev, W_dev, rows, K, (int)ncols, (int)ldv, s, false);
+    } else {
+      if (contract_smem_bytes(K) > 227 * 1024) return bfail(nullptr, ESDP_E_CONFIG, "esdp_expectation_dev: K too large");
+      if (contract_smem_bytes(K) > 48 * 1024)
+        cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
+      dim3 grid((unsigned)((ncols + kColsC - 1) / kColsC), (rows + kRowsC - 1) / kRowsC);
+      e = launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, false, P_dev, V_dev, W_dev, rows, K,
+                 (int)ncols, (int)ldv);
+    }
+  } else {
+    return bfail(nullptr, ESDP_E_CONFIG, "esdp_expectation_dev: method must be 0 or 1");
+  }
+  if (e != cudaSuccess) return bfail(nullptr, ESDP_E_CUDA, "esdp_expectation_dev: %s", cudaGetErrorString(e));
+  return ESDP_OK;
 }
 
 esdp_status esdp_batch_kernel_time(esdp_batch* b, int32_t what, int32_t reps, double* us_per_launch) {

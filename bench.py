@@ -542,7 +542,8 @@ def run_sweep(args):
     tot = n * world
     idx = [((rank + world * j) * 1024) // tot for j in range(n)]   # stratified over the sweep order
     insts = workloads.cfg5_instances(idx)
-    batch = E.Batch(insts, force_brute=args.stencil == "brute")   # one graph: one expectation + one stencil launch per stage
+    batch = E.Batch(insts, force_brute=args.stencil == "brute",   # one graph: one expectation + one stencil launch per stage
+                    ozaki=args.contract == "ozaki")
     stream = torch.cuda.Stream(device=dev)
     paths = 1024
     out_d = torch.empty(n * paths, dtype=torch.float64, device=dev)
@@ -628,14 +629,19 @@ def run_sweep(args):
         win_bytes = 18.0 * outs
         exp_bytes = 8.0 * (2 * n * K * S + K * K)     # read V_{t+1}, write W_t, read P_t
         exp_flop = 2.0 * K * K * n * S
+        kp = _kernel_profile("cfg5") if args.contract == "dmma" and args.stencil == "auto" and n == 128 else None
         kern = {"window": {"kernel": "window_batch_kernel", "us_per_launch": us_win, "bytes_per_launch": win_bytes,
                            "achieved": win_bytes / us_win / 1e3, "peak": hbm_peak, "unit": "GB/s",
-                           "frac": win_bytes / us_win / 1e3 / hbm_peak},
-                "expectation": {"kernel": "contract_dmma3_kernel (one [K] x [n ld] GEMM per stage)",
+                           "frac": win_bytes / us_win / 1e3 / hbm_peak, "traffic": None, "instr_per_output": None},
+                "expectation": {"kernel": ("ozaki_contract_kernel (Ozaki u8 tcgen05, opt-in)" if batch.plan == 2 else
+                                           "contract_dmma3_kernel") + " (one [K] x [n ld] GEMM per stage)",
                                 "us_per_launch": us_exp, "bytes_per_launch": exp_bytes,
                                 "hbm_frac": exp_bytes / us_exp / 1e3 / hbm_peak, "flop_per_launch": exp_flop,
                                 "achieved_tflops": exp_flop / us_exp / 1e6,
                                 "dmma_frac": exp_flop / us_exp / 1e6 / DMMA_PEAK_TFLOPS}}
+        if kp and "window" in kp:   # ncu counts of this workload's launches (profiles/r02_stage_kernels.json)
+            kern["window"]["traffic"] = kp["window"]["dram_bytes_per_launch"]
+            kern["window"]["instr_per_output"] = kp["window"]["warp_inst_per_launch"] * 32.0 / outs
     batch.close()
     out = None
     if rank == 0:
@@ -651,10 +657,13 @@ def run_sweep(args):
                           "instances_per_gpu": n, "sweep_indices": [idx[0], idx[-1], len(idx)],
                           "mean_A": float(np.mean(As)), "l2": "flushed between timed steps",
                           "sim_paths_per_step": n * paths * world,
-                          "plan": "esdp_create_batch: per stage one [K] x [n ld] expectation + one window launch"},
+                          "plan": "esdp_create_batch: per stage one [K] x [n ld] expectation (%s) + one window launch"
+                                  % ("Ozaki u8 tcgen05, opt-in, tolerance 1e-9" if args.contract == "ozaki" else
+                                     "FP64 DMMA, canonical chain")},
                "gpu_launches": launches, "J_mean": float(np.mean(J)),
                "roofline": {"bound": "hbm", "achieved": w["achieved"], "peak": hbm_peak, "unit": "GB/s",
-                            "frac": w["frac"], "traffic": None, "kernel": w["kernel"],
+                            "frac": w["frac"], "traffic": w["traffic"], "instr_per_output": w["instr_per_output"],
+                            "kernel": w["kernel"],
                             "us_per_launch": w["us_per_launch"], "bytes_per_launch": w["bytes_per_launch"],
                             "work_per_launch": "18 B per output (m, k, s): read W_t, write V_t, pol_t",
                             "peak_note": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind},
@@ -786,6 +795,8 @@ def main():
     ap.add_argument("--bids", choices=["fused", "after", "with-sim"], default="fused",
                     help="bid curves as side branches of the backward graph (fused), one kernel after it, or one "
                          "kernel on a side stream concurrent with the simulation")
+    ap.add_argument("--contract", choices=["dmma", "ozaki"], default="dmma",
+                    help="cfg5: expectation plan (ozaki: ESDP_CONTRACT_OZAKI, the NEXT-4 tcgen05 path, not bit-exact)")
     ap.add_argument("--stencil", choices=["auto", "brute"], default="auto",
                     help="auto: exact sliding-window stencil where it applies; brute: every (i, a) cell")
     ap.add_argument("--mode", choices=["instances", "kpart"], default=None,

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
                                                                      const double* __restrict__ Vn,
                                                                      double* __restrict__ Wt, int rows, int K,
                                                                      long long ncols, long long ldv, long long ldw) {
-  extern __shared__ __align__(1024) unsigned char ozsm[];
+  extern __shared__ __align__(16) unsigned char ozsm[];   // no-swizzle operand images need 16-byte alignment only
   unsigned char* imgA = ozsm;                                         // [kOzS][kOzImgA]
   unsigned char* imgB = imgA + (size_t)kOzS * kOzImgA;                // [kOzStages][kOzS][kOzImgB]
   OzBars* bars = reinterpret_cast<OzBars*>(imgB + (size_t)kOzStages * kOzTileB);

@@ -210,7 +210,7 @@ __device__ __forceinline__ double dmx(double a, double b) { return a > b ? a : b
 // top-2 with the action of the leader.  Returns false on a near tie (the caller rescans the row).
 struct WinFastRow {        // per-thread row constants of the fast path (the rest is read from p: constant bank or,
                            // in the batch kernel, broadcast shared-memory loads)
-  double beta_c, beta_d, pay_z;
+  double beta_c, beta_d, gc0, gd0, pay_z;
   int pcs, pds;            // peaks of the charge / discharge tables
 };
 __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinFastRow& f, const double* __restrict__ kc,
@@ -221,10 +221,11 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
   const int rc = x + Lc - 1, rd = x + Ld - 1;
   const int qc = min(max(f.pcs, x), rc), qd = min(max(f.pds, x), rd);
   const double kc1 = kc[qc], kd1 = kd[qd];
-  const double kcl = qc > x ? kc[qc - 1] : -INFINITY, kcr = qc < rc ? kc[qc + 1] : -INFINITY;
-  const double kdl = qd > x ? kd[qd - 1] : -INFINITY, kdr = qd < rd ? kd[qd + 1] : -INFINITY;
+  // the runner-up of a unimodal window is a neighbour of q inside it (windows hold >= 2 entries: Lc, Ld >= 2)
+  const double kcl = kc[qc == x ? qc + 1 : qc - 1], kcr = kc[qc == rc ? qc - 1 : qc + 1];
+  const double kdl = kd[qd == x ? qd + 1 : qd - 1], kdr = kd[qd == rd ? qd - 1 : qd + 1];
   const double di = (double)i;
-  const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), p.gfit[0]), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), p.gfit[2]);
+  const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), f.gc0), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), f.gd0);
   // the runs on the common scale y = key + beta i; the action of table position q is a_z - (j - i)
   double b1 = __dadd_rn(kc1, bci), b2 = __dadd_rn(dmx(kcl, kcr), bci);
   int a1 = a_z - 1 - qc + x;
@@ -449,10 +450,13 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
   short* const prow = reinterpret_cast<short*>(st.pol + (size_t)k * p.S);
   WinFastRow fr;
   if (fast) {
-    fr.beta_c = beta_c; fr.beta_d = beta_d; fr.pay_z = pay[p.a_z];
+    fr.beta_c = beta_c; fr.beta_d = beta_d; fr.gc0 = gc0; fr.gd0 = gd0; fr.pay_z = pay[p.a_z];
     fr.pcs = (int)upc; fr.pds = (int)upd;
   }
   const double eps2 = 2.0 * eps;
+  double bestv[OPT];
+  int argv[OPT];
+  unsigned ties = 0u;   // bit u: output u is a near tie
 #pragma unroll
   for (int u = 0; u < OPT; ++u) {
   const int i = i0 + tid + u * kWinThreads;
@@ -519,34 +523,50 @@ __device__ __forceinline__ void window_item(const WinParams& p, const WinStage& 
       near_tie = true;
     }
   }
+  bestv[u] = best;
+  argv[u] = arg;
+  ties |= near_tie ? 1u << u : 0u;
+  }
   wtrace(5);
   // near ties (rare; every row for degenerate data such as zero prices): the whole warp re-scans the
   // row canonically, 32 actions at a time, and reduces (value desc, index asc) -- the smallest index
   // among exact ties, as in the oracle's ascending scan with a strict '>'.
-  unsigned need = __ballot_sync(0xffffffffu, near_tie);
-  while (need) {
-    const int src = __ffs(need) - 1;
-    need &= need - 1;
-    const int ii = __shfl_sync(0xffffffffu, i, src);
-    double v = -INFINITY;
-    int va = 0x7fffffff;
-    for (int s = lane; s < p.nlive; s += 32) {
-      const int a = __ldg(p.live + s);
-      const double c = canon_pay(p, pay, wt, wbase, ii, a);
-      if (c > v) { v = c; va = a; }          // ascending a within the lane
-    }
+  if (__any_sync(0xffffffffu, ties != 0u)) {
 #pragma unroll
-    for (int sh = 16; sh > 0; sh >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, sh);
-      const int oa = __shfl_xor_sync(0xffffffffu, va, sh);
-      if (ov > v || (ov == v && oa < va)) { v = ov; va = oa; }
+    for (int u = 0; u < OPT; ++u) {
+      unsigned need = __ballot_sync(0xffffffffu, (ties >> u) & 1u);
+      while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1;
+        const int ii = i0 + src + (warp << 5) + u * kWinThreads;
+        double v = -INFINITY;
+        int va = 0x7fffffff;
+        for (int s = lane; s < p.nlive; s += 32) {
+          const int a = __ldg(p.live + s);
+          const double c = canon_pay(p, pay, wt, wbase, ii, a);
+          if (c > v) { v = c; va = a; }          // ascending a within the lane
+        }
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, sh);
+          const int oa = __shfl_xor_sync(0xffffffffu, va, sh);
+          if (ov > v || (ov == v && oa < va)) { v = ov; va = oa; }
+        }
+        if (lane == src) { bestv[u] = v; argv[u] = va; atomicAdd(&g_window_fallbacks, 1ull); }
+      }
     }
-    if (lane == src) { best = v; arg = va; atomicAdd(&g_window_fallbacks, 1ull); }
   }
-  if (valid) {   // st.global: the compiler then knows these stores do not alias the shared-memory tables
-    __stwb(vrow + i, best);
-    __stwb(prow + i, (short)arg);
-  }
+  // stores off one base pointer per row (immediate offsets); st.global: the compiler then knows they do not
+  // alias the shared-memory tables
+  double* const vp = vrow + i0 + tid;
+  short* const pp = prow + i0 + tid;
+  const int nvalid = p.S - i0 - tid;   // outputs u < ceil(nvalid / kWinThreads) are inside the row
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+    if (u * kWinThreads < nvalid) {
+      __stwb(vp + u * kWinThreads, bestv[u]);
+      __stwb(pp + u * kWinThreads, (short)argv[u]);
+    }
   }
   wtrace(6);
 }

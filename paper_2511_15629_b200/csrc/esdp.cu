@@ -713,13 +713,20 @@ using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #endif
 using D3s = Dmma3<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>;
 #define D3S_KERNEL contract_dmma3_kernel<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>
-constexpr double kDmma3MinOutputs = 3.0e5;
-// 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large tiling
+// Wide tiling for very large products (the cfg5 batch GEMM, [100] x [128,512]): 16 x 128 block tiles of four
+// 16 x 32 warp tiles, two pipeline stages (40 KB: five blocks per SM).  Measured over 17 tilings
+// (tools/variants_d3_cfg5.sh): 108.1 us per cfg5 stage against 122.5 us for the large tiling, which stays
+// best on cfg4 (9.6 vs 13.2 us per launch).
+using D3w = Dmma3<2, 4, 4, 16, 2>;
+#define D3W_KERNEL contract_dmma3_kernel<2, 4, 4, 16, 2>
+constexpr double kDmma3MinOutputs = 3.0e5, kDmma3WideOutputs = 4.0e6;
+// 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large; 3: wide
 int use_dmma3(int rows, int64_t ncols, int K) {
   if (rows < 8 || (K & 1)) return 0;
   static const int force = [] { const char* e = getenv("ESDP_DMMA3"); return e ? atoi(e) : -1; }();
   if (force == 0) return 0;
-  return (double)rows * (double)ncols >= kDmma3MinOutputs ? 2 : 1;
+  const double outs = (double)rows * (double)ncols;
+  return outs >= kDmma3WideOutputs ? 3 : outs >= kDmma3MinOutputs ? 2 : 1;
 }
 template <typename DD>
 cudaError_t launch_dmma3_as(void (*kern)(const double*, const double*, double*, int, int, int, int, int), const double* Pt,
@@ -734,7 +741,8 @@ cudaError_t launch_dmma3_as(void (*kern)(const double*, const double*, double*, 
 }
 cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* Wt, int rows, int K, int S, int ld,
                          cudaStream_t s, bool pdl) {
-  return which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
+  return which == 3 ? launch_dmma3_as<D3w>(D3W_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
+       : which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
 }
 

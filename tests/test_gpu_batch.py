@@ -174,3 +174,10 @@ def test_batch_window_variants(opt, generic, monkeypatch):
     monkeypatch.setenv("ESDP_WIN_OPT", opt)
     monkeypatch.setenv("ESDP_WIN_GENERIC", generic)
     _check_batch(workloads.cfg5_instances([0, 37, 300, 1023], T=8, K=10))
+
+
+def test_batch_wide_expectation_tiling():
+    """48 cfg5 configurations (K = 100: 4.8e6 expectation outputs per stage) take the wide DMMA tiling
+    (16 x 128 blocks, two stages; >= 4e6 outputs): every instance stays bit-identical to the oracle."""
+    idx = [(j * 1024) // 48 for j in range(48)]
+    _check_batch(workloads.cfg5_instances(idx, T=3, K=100))

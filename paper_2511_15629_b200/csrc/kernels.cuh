@@ -987,10 +987,9 @@ inline void launch_cdf(const double* q, const int* src, int64_t rows, int K, int
   else cdf_kernel<false><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, src, rows, K, g, cdf, guide);
 }
 
-// first j in [0, K) with u < cdf[j] (m: the draw's 53-bit integer, u = m 2^-53); gs = 53 - g
-__device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const uint64_t* __restrict__ guide, int gs,
-                                          uint64_t m, double u) {
-  const uint64_t e = __ldg(guide + (m >> gs));
+// first j in [0, K) with u < cdf[j] (m: the draw's 53-bit integer, u = m 2^-53); gs = 53 - g.  Split into the
+// guide load and its decoding, so a caller can issue the load early and work while it is in flight.
+__device__ __forceinline__ int cdf_decode(const double* __restrict__ cdf, uint64_t e, int gs, uint64_t m, double u) {
   int j = (int)(e >> kGuideJ);
   const int dl = (int)(e >> kGuideD) & 63;
   if (dl == 0) return j;
@@ -1003,6 +1002,10 @@ __device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const 
   }
   while (!(u < __ldg(cdf + j))) ++j;               // several boundaries: the definition, from j_lo
   return j;
+}
+__device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const uint64_t* __restrict__ guide, int gs,
+                                          uint64_t m, double u) {
+  return cdf_decode(cdf, __ldg(guide + (m >> gs)), gs, m, u);
 }
 
 struct SimParams {
@@ -1051,21 +1054,22 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
   // draw's dependent chain
   size_t rb_next = sp.T > 1 ? sim_row(sp, 1, 0) : 0;
   for (int t = 1; t <= sp.T; ++t) {
+    // both loads of the stage first (the policy entry, the price draw's guide entry), then the next stage's
+    // draws -- they do not depend on the state -- while the loads are in flight, then the decoding
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
+    const double lam = sp.kind == 2 ? 0.0 : __ldg(sp.lambda + (size_t)(t - 1) * sp.K + k);
     const size_t rb = rb_next;
+    const size_t row = sp.rank1 ? rb : rb + k;
+    const uint64_t ge = t < sp.T ? __ldg(sp.guide + (row << (53 - sp.gs)) + (m2 >> sp.gs)) : 0ull;
     if (t + 1 < sp.T) rb_next = sim_row(sp, t + 1, 0);
-    int kn = k;
-    if (t < sp.T) {
-      const size_t row = sp.rank1 ? rb : rb + k;
-      kn = cdf_sample(sp.cdf + row * sp.K, sp.guide + (row << (53 - sp.gs)), sp.gs, m2, u2);
-    }
-    // the next stage's draws do not depend on the state: computed while this stage's loads are in flight
-    const double u1t = u1;
+    const double u1t = u1, u2t = u2;
+    const uint64_t m2t = m2;
     if (t < sp.T) sim_uniforms(seed, path, t + 1, u1, u2, m1, m2);
+    const int kn = t < sp.T ? cdf_decode(sp.cdf + row * sp.K, ge, sp.gs, m2t, u2t) : k;
     double p;
     if (sp.kind == 2) p = __ldg(sp.g + ((size_t)(t - 1) * sp.K + k) * sp.A + a);
     else {
-      p = __dmul_rn(__ldg(sp.lambda + (size_t)(t - 1) * sp.K + k), s_act[a]);
+      p = __dmul_rn(lam, s_act[a]);
       if (sp.kind == 1) p = __dsub_rn(p, s_g[a]);
     }
     profit = __dadd_rn(profit, p);

@@ -711,8 +711,11 @@ using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #ifndef ESDP_D3S_WC
 #define ESDP_D3S_WC 2
 #endif
-using D3s = Dmma3<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>;
-#define D3S_KERNEL contract_dmma3_kernel<1, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>
+#ifndef ESDP_D3S_MT
+#define ESDP_D3S_MT 1
+#endif
+using D3s = Dmma3<ESDP_D3S_MT, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>;
+#define D3S_KERNEL contract_dmma3_kernel<ESDP_D3S_MT, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>
 // Wide tiling for very large products (the cfg5 batch GEMM, [100] x [128,512]): 16 x 128 block tiles of four
 // 16 x 32 warp tiles, two pipeline stages (40 KB: five blocks per SM).  Measured over 17 tilings
 // (tools/variants_d3_cfg5.sh): 108.1 us per cfg5 stage against 122.5 us for the large tiling, which stays

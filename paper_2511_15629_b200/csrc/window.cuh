@@ -227,30 +227,27 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
   const double di = (double)i;
   const double bci = __dsub_rn(__dmul_rn(f.beta_c, di), f.gc0), bdi = __dsub_rn(__dmul_rn(f.beta_d, di), f.gd0);
   // the runs on the common scale y = key + beta i; the action of table position q is a_z - (j - i)
-  double b1 = __dadd_rn(kc1, bci), b2 = __dadd_rn(dmx(kcl, kcr), bci);
-  int a1 = a_z - 1 - qc + x;
-  {
-    const double y1 = __dadd_rn(kd1, bdi), y2 = __dadd_rn(dmx(kdl, kdr), bdi);
-    const bool g = y1 > b1;
-    b2 = g ? dmx(b1, y2) : dmx(b2, y1);
-    b1 = g ? y1 : b1;
-    a1 = g ? a_z + Ld - qd + x : a1;
-  }
-  // singles, canonical: once a single leads, b1 is its exact value
+  const double yc1 = __dadd_rn(kc1, bci), yc2 = __dadd_rn(dmx(kcl, kcr), bci);
+  const double yd1 = __dadd_rn(kd1, bdi), yd2 = __dadd_rn(dmx(kdl, kdr), bdi);
+  // the singles, canonical
   const double* wi = wt + (i - wbase);
-  bool sb = false;
-  auto single = [&](double c, int a) {
-    const bool g = c > b1;
-    b2 = g ? b1 : dmx(b2, c);
-    b1 = g ? c : b1;
-    a1 = g ? a : a1;
-    sb |= g;
-  };
   const WinSingle &sc = p.sg[0], &sd = p.sg[2];
-  single(__dadd_rn(pay[sc.a], __dadd_rn(__dmul_rn(sc.omw, wi[sc.off]), __dmul_rn(sc.w, wi[sc.off + 1]))), sc.a);
-  single(__dadd_rn(f.pay_z, wi[0]), a_z);
-  single(__dadd_rn(pay[sd.a], __dadd_rn(__dmul_rn(sd.omw, wi[sd.off]), __dmul_rn(sd.w, wi[sd.off + 1]))), sd.a);
-  if (!(__dsub_rn(b1, b2) > eps2)) return false;
+  const double ce = __dadd_rn(pay[sc.a], __dadd_rn(__dmul_rn(sc.omw, wi[sc.off]), __dmul_rn(sc.w, wi[sc.off + 1])));
+  const double cz = __dadd_rn(f.pay_z, wi[0]);
+  const double cd = __dadd_rn(pay[sd.a], __dadd_rn(__dmul_rn(sd.omw, wi[sd.off]), __dmul_rn(sd.w, wi[sd.off + 1])));
+  // leader; once a single leads, b1 is its exact canonical value
+  double b1 = yc1;
+  int a1 = a_z - 1 - qc + x;
+  bool sb = false;
+  if (yd1 > b1) { b1 = yd1; a1 = a_z + Ld - qd + x; }
+  if (ce > b1) { b1 = ce; a1 = sc.a; sb = true; }
+  if (cz > b1) { b1 = cz; a1 = a_z; sb = true; }
+  if (cd > b1) { b1 = cd; a1 = sd.a; sb = true; }
+  // unique leader: every other candidate (the runs' runner-ups included) at most b1 - 2.25 eps, i.e. more than
+  // 2 eps below it after the subtraction's rounding (u |b1| < eps / 4)
+  const double thr = __dsub_rn(b1, 1.125 * eps2);
+  const int above = (yc1 > thr) + (yd1 > thr) + (ce > thr) + (cz > thr) + (cd > thr) + (yc2 > thr) + (yd2 > thr);
+  if (above != 1) return false;
   arg = a1;
   // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, weight 0)
   best = sb ? b1 : __dadd_rn(pay[a1], wi[a_z - a1]);

@@ -703,23 +703,8 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
   int ao = -1, ab = -1;          // vertices nh-2 (o) and nh-1 (b)
   double uo = 0.0, ub = 0.0, po = 0.0, pb = 0.0;
   double dp = 0.0, du = 0.0;     // fl(pb - po), fl(ub - uo): the cross product's stack-side factors
-  // the next point is loaded one iteration ahead (its loads do not depend on the pops)
-#ifndef BID_PF_HULL
-#define BID_PF_HULL 0
-#endif
-#ifndef BID_PF_EMIT
-#define BID_PF_EMIT 1
-#endif
-#if BID_PF_HULL
-  double u_nx = u_of(a_lo), p_nx = tb.act[a_lo];
-#endif
   for (int a = a_lo; a <= a_hi; ++a) {
-#if BID_PF_HULL
-    const double u = u_nx, pc = p_nx;
-    if (a < a_hi) { u_nx = u_of(a + 1); p_nx = tb.act[a + 1]; }
-#else
     const double u = u_of(a), pc = tb.act[a];
-#endif
     while (nh >= 2) {
       const double cr = __dsub_rn(__dmul_rn(dp, __dsub_rn(u, uo)), __dmul_rn(du, __dsub_rn(pc, po)));
       if (cr < 0.0) break;
@@ -738,8 +723,7 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
     ++nh;
     if (nh >= 2) { dp = __dsub_rn(pb, po); du = __dsub_rn(ub, uo); }
   }
-  // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20); the next
-  // vertex is loaded one step ahead
+  // emit vertices, quantities and segment prices (Eq. 12) with the running-max repair (R20)
   int a_prev = st_get(0);
   double u_prev = u_of(a_prev);
   double p_prev = tb.act[a_prev], prev_price = 0.0;
@@ -747,10 +731,6 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
   // in L2), so that 0.5 GB of cfg2 curves do not push the policy table out before the simulation
   if (kSmem) __stcs(vo, (short)a_prev);
   if (qo) __stcs(qo, p_prev);
-#ifndef BID_EMIT2
-#define BID_EMIT2 1
-#endif
-#if BID_EMIT2
   // two segments per step: their divisions are independent (the repair is a running max after them)
   int j2 = 1;
   for (; j2 + 1 < nh; j2 += 2) {
@@ -769,17 +749,6 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
   for (int j = j2; j < nh; ++j) {
     const int a = st_get(j);
     const double u = u_of(a), pc = tb.act[a];
-#elif BID_PF_EMIT
-  int a_n = nh > 1 ? st_get(1) : 0;
-  double u_n = nh > 1 ? u_of(a_n) : 0.0, p_n = nh > 1 ? tb.act[a_n] : 0.0;
-    const int a = a_n;
-    const double u = u_n, pc = p_n;
-    if (j + 1 < nh) { a_n = st_get(j + 1); u_n = u_of(a_n); p_n = tb.act[a_n]; }
-#else
-  for (int j = 1; j < nh; ++j) {
-    const int a = st_get(j);
-    const double u = u_of(a), pc = tb.act[a];
-#endif
     double pj = -__ddiv_rn(__dsub_rn(u, u_prev), __dsub_rn(pc, p_prev));
     if (j > 1 && pj < prev_price) pj = prev_price;
     __stcs(pro + (size_t)(j - 1) * nout, pj);

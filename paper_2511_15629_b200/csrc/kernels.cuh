@@ -8,6 +8,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// Checked builds (`make EXTRA=-DESDP_CHECK`, tests run against them like the default build): device-side
+// bounds and invariant asserts on the indices the hot kernels compute -- the substitute for
+// compute-sanitizer, which is closed on this GPU pool.
+#ifdef ESDP_CHECK
+#include <cassert>
+#define ESDP_ASSERT(c) assert(c)
+#else
+#define ESDP_ASSERT(c) ((void)0)
+#endif
+
 namespace esdp {
 
 constexpr int kMaxA = 8191;
@@ -717,6 +727,7 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
         dp = __dsub_rn(pb, po); du = __dsub_rn(ub, uo);
       }
     }
+    ESDP_ASSERT(nh <= a_hi - a_lo);
     st_set(nh, a);
     if (nh >= 1) { ao = ab; uo = ub; po = pb; }
     ab = a; ub = u; pb = pc;
@@ -970,6 +981,7 @@ __device__ __forceinline__ int cdf_decode(const double* __restrict__ cdf, uint64
     return u < __ldg(cdf + j) ? j : j + dl;        // tie on the truncated bits: compare exactly
   }
   while (!(u < __ldg(cdf + j))) ++j;               // several boundaries: the definition, from j_lo
+  ESDP_ASSERT(u < 1.0);                            // the last cdf entry is 1: the scan stops inside the row
   return j;
 }
 __device__ __forceinline__ int cdf_sample(const double* __restrict__ cdf, const uint64_t* __restrict__ guide, int gs,
@@ -1025,7 +1037,9 @@ __device__ __forceinline__ void simulate_block(const SimParams& sp, int64_t n, u
   for (int t = 1; t <= sp.T; ++t) {
     // both loads of the stage first (the policy entry, the price draw's guide entry), then the next stage's
     // draws -- they do not depend on the state -- while the loads are in flight, then the decoding
+    ESDP_ASSERT(k >= 0 && k < sp.K && i >= 0 && i < sp.S);
     const int a = __ldg(sp.pol + (size_t)(t - 1) * KS + (size_t)k * sp.S + i);
+    ESDP_ASSERT(a >= 0 && a < sp.A);
     const double lam = sp.kind == 2 ? 0.0 : __ldg(sp.lambda + (size_t)(t - 1) * sp.K + k);
     const size_t rb = rb_next;
     const size_t row = sp.rank1 ? rb : rb + k;

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
   double* cmax = reinterpret_cast<double*>(fexp + 2 * kOzN);                           // [2][4][kOzN] partial maxima
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long ntiles = (ncols + kOzN - 1) / kOzN;
+  ESDP_ASSERT(blockDim.x == kOzThreads && rows <= kOzM && K <= kOzK && rows >= 1 && K >= 1);
 
   if (tid == 0) {
     for (int s = 0; s < kOzStages; ++s) { mbar_init(&bars->full[s], 128); mbar_init(&bars->empty[s], 1); }

@@ -220,6 +220,7 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
   const int Lc = p.Lc, Ld = p.Ld, a_z = p.a_z;
   const int rc = x + Lc - 1, rd = x + Ld - 1;
   const int qc = min(max(f.pcs, x), rc), qd = min(max(f.pds, x), rd);
+  ESDP_ASSERT(Lc >= 2 && Ld >= 2 && qc >= x && qc <= rc && qd >= x && qd <= rd);
   const double kc1 = kc[qc], kd1 = kd[qd];
   // the runner-up of a unimodal window is a neighbour of q inside it (windows hold >= 2 entries: Lc, Ld >= 2)
   const double kcl = kc[qc == x ? qc + 1 : qc - 1], kcr = kc[qc == rc ? qc - 1 : qc + 1];
@@ -232,6 +233,7 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
   // the singles, canonical
   const double* wi = wt + (i - wbase);
   const WinSingle &sc = p.sg[0], &sd = p.sg[2];
+  ESDP_ASSERT(i - wbase + sc.off >= 0 && i - wbase + sd.off + 1 < kWinThreads * 4 + (p.o_max - p.o_min) + 2);
   const double ce = __dadd_rn(pay[sc.a], __dadd_rn(__dmul_rn(sc.omw, wi[sc.off]), __dmul_rn(sc.w, wi[sc.off + 1])));
   const double cz = __dadd_rn(f.pay_z, wi[0]);
   const double cd = __dadd_rn(pay[sd.a], __dadd_rn(__dmul_rn(sd.omw, wi[sd.off]), __dmul_rn(sd.w, wi[sd.off + 1])));
@@ -250,6 +252,7 @@ __device__ __forceinline__ bool window_query_fast(const WinParams& p, const WinF
   if (above != 1) return false;
   arg = a1;
   // canonical value of the unique argmax; a run action lies on the lattice (offset a_z - a1, weight 0)
+  ESDP_ASSERT(a1 >= 0 && a1 < p.A && (sb || (a_z - a1 >= -Ld && a_z - a1 <= Lc)));
   best = sb ? b1 : __dadd_rn(pay[a1], wi[a_z - a1]);
   return true;
 }
@@ -286,6 +289,7 @@ __device__ __forceinline__ double canon_pay(const WinParams& p, const double* __
 __device__ __forceinline__ void win_key_pair(double* __restrict__ tb, const double* __restrict__ wt, int wbase, int j0,
                                              int x, int n, double beta, unsigned& up, unsigned& dn) {
   const int j = j0 + x;
+  ESDP_ASSERT((x & 1) == 0 && x < n && j - wbase >= (x >= 1 ? 1 : 0));
   const double* w = wt + (j - wbase);
   const double jd = (double)j;
   const double k0 = __dsub_rn(w[0], __dmul_rn(beta, jd));

@@ -181,3 +181,15 @@ def test_batch_wide_expectation_tiling():
     (16 x 128 blocks, two stages; >= 4e6 outputs): every instance stays bit-identical to the oracle."""
     idx = [(j * 1024) // 48 for j in range(48)]
     _check_batch(workloads.cfg5_instances(idx, T=3, K=100))
+
+
+def test_batch_plan_reports_the_dfma_fallback(monkeypatch):
+    """esdp_batch_plan: 0 (FP64 DMMA) by default; 1 (DFMA) when the DMMA bit-exactness probe fails (forced with
+    ESDP_DMMA_PROBE_FAIL=1), and every instance is still the oracle's, bit for bit."""
+    insts = workloads.cfg5_instances([0, 600], T=5, K=12)
+    with E.Batch(insts) as b:
+        assert b.plan == 0
+    monkeypatch.setenv("ESDP_DMMA_PROBE_FAIL", "1")
+    with E.Batch(insts) as b:
+        assert b.plan == 1
+    _check_batch(insts)

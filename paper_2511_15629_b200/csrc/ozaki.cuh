@@ -20,40 +20,42 @@
 // Opt-in (ESDP_CONTRACT_OZAKI).
 //
 // One persistent CTA per SM, warp-specialized, 288 threads:
-//   warps 0-3  digitizers: load a 32-column tile of V_{t+1} (FP64; a warp reads one row of the tile per
-//              load), the column exponents (named barrier), and write the 8 digit images of the tile into
-//              a 2-slot shared-memory ring (K-major UMMA layout);
+//   warps 0-3  digitizers: load a 64-column tile of V_{t+1} (FP64) in two halves of 32 columns (a warp reads
+//              one row of the half per load), the column exponents (named barrier), and write the 8 digit
+//              images of the tile into the digit-image slot (K-major UMMA layout);
 //   warps 4-7  epilogue: tcgen05.ld the 8 accumulators of a tile, combine, scale, store W (FP64);
 //   warp 8     TMEM allocation and the MMA issue (one lane: 36 digit products x 4 K-steps, straight-line).
 // P's digit images (all of P_t: 128 rows x 128 k', 8 x 16 KB) are built once per CTA before the
-// programmatic dependency wait (P is an input).  TMEM: two accumulator sets of 8 x 32 columns, so the
-// epilogue of tile j overlaps the MMAs of tile j + 1.
+// programmatic dependency wait (P is an input).  Shared memory: 128 KB of P images + one 64 KB V-image slot;
+// TMEM: one accumulator set of 8 x 64 columns.  Digitizing tile j + 1 overlaps the epilogue of tile j.
 //
 // Measured on B200: correct, but SLOWER than the canonical FP64 DMMA expectation on the
-// cfg5 batch GEMM ([100] x [128,512] per stage): 173-179 us vs 122.6 us per launch.  tools/microbench/mb10.cu:
-// an M = 128, K = 32 u8 MMA costs >= 46 cycles for any N <= 64 (shared-memory bound: the 4 KB A tile is
-// re-read by every MMA) and reaches the 8.2K MAC/cycle peak only at N >= 128; 8 accumulators x N TMEM
-// columns <= 512 caps N at 64 (32 with double buffering), so the 144 MMAs of a tile cost >= 6.6K cycles
-// -- the MMAs alone measured 129 us, the digitizers + epilogue alone 96 us, 173 us together.
+// cfg5 batch GEMM ([100] x [128,512] per stage): 172 us (N = 64, this layout) and 173-179 us (N = 32 with two
+// accumulator sets and a two-slot ring) vs 108 us per launch.  tools/microbench/mb10.cu: an M = 128, K = 32
+// u8 MMA costs >= 46 cycles for any N <= 64 (shared-memory bound: the 4 KB A tile is re-read by every MMA)
+// and reaches the 8.2K MAC/cycle peak only at N >= 128, but 8 accumulators x N TMEM columns <= 512 caps N
+// at 64; with the 128 KB of P images resident, no shared memory is left to stage V tiles ahead, and ncu
+// shows the digitizers waiting on their V loads and the epilogue on the MMAs.
 #pragma once
 #include "kernels.cuh"
 
 namespace esdp {
 
 constexpr int kOzS = 8;                       // 8-bit digits per operand (64 bits)
-constexpr int kOzN = 32;                      // output columns per tile (UMMA N)
+constexpr int kOzN = 64;                      // output columns per tile (UMMA N)
 constexpr int kOzM = 128;                     // UMMA M: rows k of P, zero-padded
 constexpr int kOzK = 128;                     // reduction k' zero-padded to 4 UMMA K-steps of 32 bytes
-constexpr int kOzStages = 2;                  // digit-image ring slots
-constexpr int kOzAccCols = kOzS * kOzN;       // TMEM columns of one accumulator set
+constexpr int kOzStages = 1;                  // digit-image slots (one: the A images take 128 KB)
+constexpr int kOzAccCols = kOzS * kOzN;       // TMEM columns of the accumulator set (all 512)
 constexpr int kOzThreads = 32 * 9;            // 4 digitizer, 4 epilogue, 1 MMA warp
 constexpr int kOzImgA = kOzM * kOzK;          // bytes of one digit image of P (16 KB)
-constexpr int kOzImgB = kOzN * kOzK;          // bytes of one digit image of a V tile (4 KB)
-constexpr int kOzTileB = kOzS * kOzImgB;      // 28 KB
+constexpr int kOzImgB = kOzN * kOzK;          // bytes of one digit image of a V tile (8 KB)
+constexpr int kOzTileB = kOzS * kOzImgB;      // 64 KB
 constexpr size_t kOzFixed = (size_t)kOzS * kOzImgA + (size_t)kOzStages * kOzTileB;
-constexpr size_t kOzMisc = 3072;              // barriers (256 B), exponents (768 B), column-maximum scratch (2 KB)
+constexpr size_t kOzMisc = 6144;              // barriers (256 B), exponents (1 KB), column-maximum scratch (4 KB)
 constexpr size_t kOzSmem = kOzFixed + kOzMisc;
 static_assert(kOzS == 8, "the epilogue combines exactly 8 diagonal accumulators");
+static_assert(kOzAccCols <= 512, "one accumulator set in TMEM");
 
 // Byte (row r, k) of a K-major, SWIZZLE_NONE UMMA operand image: 8-row x 16-byte core matrices laid out
 // [row group][k chunk][row in group][16 bytes]; next k chunk (LBO) 128 B, next row group (SBO) 1024 B.
@@ -118,7 +120,7 @@ __device__ __forceinline__ void oz_digits16(const double (&v)[16], double sc, un
 }
 
 struct OzBars {
-  uint64_t full[kOzStages], empty[kOzStages], tfull[2], tempty[2];
+  uint64_t full, empty, tfull, tempty, fxready[2], fxfree[2];
   uint32_t taddr;
 };
 
@@ -140,13 +142,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
   ESDP_ASSERT(blockDim.x == kOzThreads && rows <= kOzM && K <= kOzK && rows >= 1 && K >= 1);
 
   if (tid == 0) {
-    for (int s = 0; s < kOzStages; ++s) { mbar_init(&bars->full[s], 128); mbar_init(&bars->empty[s], 1); }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars->tfull[b], 1); mbar_init(&bars->tempty[b], 128);
-    }
+    mbar_init(&bars->full, 128); mbar_init(&bars->empty, 1);
+    mbar_init(&bars->tfull, 1); mbar_init(&bars->tempty, 128);
+    for (int b = 0; b < 2; ++b) { mbar_init(&bars->fxready[b], 128); mbar_init(&bars->fxfree[b], 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {   // TMEM: two accumulator sets (2 x 224 of 512 columns); one CTA per SM (shared memory)
+  if (warp == 8) {   // TMEM: the accumulator set (8 x 64 = 512 columns); one CTA per SM (shared memory)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&bars->taddr)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -178,42 +179,50 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
   const uint32_t tbase = bars->taddr;
   pdl_wait();                // V_{t+1} is the previous kernel's output
 
+  // Pipeline per tile `it` (one digit-image slot, one TMEM accumulator set; phases stay within one of their
+  // waiters, see the waits):  digitize(it) after MMA(it - 1) read the slot and the epilogue of it - 2 read
+  // fexp[it & 1];  MMA(it) after digitize(it) and the epilogue of it - 1 drained TMEM;  epilogue(it) after
+  // MMA(it) and digitize(it)'s column exponents.  Digitize(it + 1) overlaps epilogue(it).
   if (warp < 4) {
-    // ---------------- digitizers: thread (column r, k' part h = warp): chunks h and h + 4 of 16 k' each; a
-    // warp reads one row of the tile (32 consecutive doubles) at a time
-    const int r = lane, h = warp;
+    // ---------------- digitizers: columns in two halves of 32; thread (column lane, k' part h = warp):
+    // chunks h and h + 4 of 16 k' each; a warp reads one row of the half tile (32 doubles) per load
+    const int h = warp;
     long long it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int s = (int)(it % kOzStages), b = (int)(it & 1);
-      const long long n = tile * kOzN + r;
-      const bool col = n < ncols;
-      double v[2][16];
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int k = 16 * (h + 4 * j) + i;
-          v[j][i] = (col && k < K) ? __ldcg(Vn + (size_t)k * ldv + n) : 0.0;
-        }
-      double mx = 0.0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) mx = fmax(mx, v[j][i]);
+      const int b = (int)(it & 1);
+      mbar_wait(&bars->empty, (unsigned)((it & 1) ^ 1));                  // the slot: MMAs of it - 1 done
+      mbar_wait(&bars->fxfree[b], (unsigned)(((it >> 1) & 1) ^ 1));       // fexp[b]: epilogue of it - 2 done
       double* cm = cmax + (size_t)b * 4 * kOzN;
-      cm[h * kOzN + r] = mx;
-      mbar_wait(&bars->empty[s], (unsigned)(((it / kOzStages) & 1) ^ 1));   // ring slot s free (MMAs of it - 2 done)
-      mbar_wait(&bars->tempty[b], (unsigned)(((it >> 1) & 1) ^ 1));         // fexp[b] free (epilogue of it - 2 done)
-      oz_bar_digitizers();
-      mx = fmax(fmax(cm[r], cm[kOzN + r]), fmax(cm[2 * kOzN + r], cm[3 * kOzN + r]));
-      const int f = oz_exp_above(mx);
-      if (h == 0) fexp[b * kOzN + r] = f;
-      const double sc = oz_pow2(f);
-      unsigned char* dst = imgB + (size_t)s * kOzTileB;
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        const int r = 32 * hh + lane;
+        const long long n = tile * kOzN + r;
+        const bool col = n < ncols;
+        double v[2][16];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) oz_digits16(v[j], sc, dst, kOzImgB, oz_off(r, 16 * (h + 4 * j)));
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int k = 16 * (h + 4 * j) + i;
+            v[j][i] = (col && k < K) ? __ldcg(Vn + (size_t)k * ldv + n) : 0.0;
+          }
+        double mx = 0.0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) mx = fmax(mx, v[j][i]);
+        cm[h * kOzN + r] = mx;
+        oz_bar_digitizers();
+        mx = fmax(fmax(cm[r], cm[kOzN + r]), fmax(cm[2 * kOzN + r], cm[3 * kOzN + r]));
+        const int f = oz_exp_above(mx);
+        if (h == 0) fexp[b * kOzN + r] = f;
+        const double sc = oz_pow2(f);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) oz_digits16(v[j], sc, imgB, kOzImgB, oz_off(r, 16 * (h + 4 * j)));
+      }
       oz_fence_proxy();
-      oz_arrive(&bars->full[s]);
+      oz_arrive(&bars->full);
+      oz_arrive(&bars->fxready[b]);
     }
   } else if (warp < 8) {
     // ---------------- epilogue: this warp's TMEM lanes = rows 32 (warp % 4) .. + 31
@@ -223,17 +232,15 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
     long long it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int b = (int)(it & 1);
-      // the digitizers' column exponents of this tile: acquired on the ring barrier they released (its phase
-      // cannot have moved on: the digitizers of tile it + 2 wait for the epilogue of tile it)
-      mbar_wait(&bars->full[it % kOzStages], (unsigned)((it / kOzStages) & 1));
-      mbar_wait(&bars->tfull[b], (unsigned)((it >> 1) & 1));
+      mbar_wait(&bars->fxready[b], (unsigned)((it >> 1) & 1));   // the column exponents of tile it
+      mbar_wait(&bars->tfull, (unsigned)(it & 1));
       tc_fence_after();
       const long long n0 = tile * kOzN;
 #pragma unroll 1
       for (int cc = 0; cc < kOzN / 8; ++cc) {
         uint32_t acc[kOzS][8];
 #pragma unroll
-        for (int d = 0; d < kOzS; ++d) oz_ld8(lanebase + (uint32_t)(b * kOzAccCols + d * kOzN + cc * 8), acc[d]);
+        for (int d = 0; d < kOzS; ++d) oz_ld8(lanebase + (uint32_t)(d * kOzN + cc * 8), acc[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         double out[8];
 #pragma unroll
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
           double* wr = Wt + (size_t)m * ldw + n0 + cc * 8;
           if (n0 + cc * 8 + 8 <= ncols && ((reinterpret_cast<uintptr_t>(wr) & 15) == 0)) {
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) __stcg(reinterpret_cast<double2*>(wr + j), make_double2(out[j], out[j + 1]));
+            for (int j = 0; j < 8; j += 2) __stcg(reinterpret_cast<double2*>(wr + j), make_double2(out[j], out[j + 1]));  // stays in L2 for the stencil
           } else {
             for (int j = 0; j < 8; ++j)
               if (n0 + cc * 8 + j < ncols) wr[j] = out[j];
@@ -263,35 +270,33 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_contract_kernel(const dou
         }
       }
       tc_fence_before();
-      oz_arrive(&bars->tempty[b]);
+      oz_arrive(&bars->tempty);
+      oz_arrive(&bars->fxfree[b]);
     }
-  } else if (warp == 8) {
-    // ---------------- MMA issue (one lane).  A descriptor's start-address field is (address >> 4) in the low
-    // 14 bits and shared addresses stay below 2^18, so an operand at byte offset o is the base descriptor
-    // plus o >> 4: the 144 MMAs of a tile are straight-line code with immediate offsets.
+  } else {
+    // ---------------- MMA issue (warp 8, one lane).  A descriptor's start-address field is (address >> 4) in
+    // the low 14 bits and shared addresses stay below 2^18, so an operand at byte offset o is the base
+    // descriptor plus o >> 4: the 144 MMAs of a tile are straight-line code with immediate offsets.
     long long it = 0;
-    const uint64_t adesc = oz_desc(smem_u32(imgA)), bdesc0 = oz_desc(smem_u32(imgB));
+    const uint64_t adesc = oz_desc(smem_u32(imgA)), bdesc = oz_desc(smem_u32(imgB));
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int s = (int)(it % kOzStages), b = (int)(it & 1);
-      mbar_wait(&bars->full[s], (unsigned)((it / kOzStages) & 1));
-      mbar_wait(&bars->tempty[b], (unsigned)(((it >> 1) & 1) ^ 1));
+      mbar_wait(&bars->full, (unsigned)(it & 1));
+      mbar_wait(&bars->tempty, (unsigned)((it & 1) ^ 1));   // the epilogue of it - 1 drained TMEM
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t dbase = tbase + (uint32_t)(b * kOzAccCols);
-        const uint64_t bdesc = bdesc0 + (uint64_t)((s * kOzTileB) >> 4);
         // digit products D^P_(p+1) D^V_(q+1) with p + q <= kOzS - 1, into accumulator d = p + q.  K-steps
-        // outermost, so consecutive MMAs update different accumulators (no back-to-back read-modify-write of
-        // one accumulator); the first product of each diagonal (first K-step, q = 0) overwrites it.
+        // outermost, so consecutive MMAs update different accumulators; the first product of each diagonal
+        // (first K-step, q = 0) overwrites it.
 #pragma unroll
         for (int ks = 0; ks < kOzK / 32; ++ks)
 #pragma unroll
           for (int q = 0; q < kOzS; ++q)
 #pragma unroll
             for (int p = 0; p + q < kOzS; ++p)
-              oz_mma(dbase + (uint32_t)((p + q) * kOzN), adesc + (uint64_t)((p * kOzImgA + ks * 256) >> 4),
+              oz_mma(tbase + (uint32_t)((p + q) * kOzN), adesc + (uint64_t)((p * kOzImgA + ks * 256) >> 4),
                      bdesc + (uint64_t)((q * kOzImgB + ks * 256) >> 4), (q > 0 || ks > 0) ? 1u : 0u);
-        oz_commit(&bars->empty[s]);   // the ring slot is free once these MMAs have read it
-        oz_commit(&bars->tfull[b]);   // the accumulators of tile it are complete
+        oz_commit(&bars->empty);   // the slot is free once these MMAs have read it
+        oz_commit(&bars->tfull);   // the accumulators of tile it are complete
       }
       __syncwarp();
     }

@@ -886,12 +886,13 @@ cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const in
     kern<<<blocks, kBidThreads, sm, s>>>(bp, n, req_dev, slot_dev, nout, cap, c->o_min, span, nvert_dev, vert_dev, q_dev,
                                          price_dev);
   };
+  // Hull stacks in shared memory as 8-bit indices (A <= 255: 25 KB per block at A = 201, six blocks per SM);
+  // wider grids keep the stack in the curve's own vertex row in global memory: a 16-bit shared-memory stack
+  // (102 KB at A = 401) allowed one block per SM and measured 3x slower (cfg4: 110 -> 36 ms of bid curves
+  // per step; on cfg2 the global stack is slower, 2.88 vs 2.43 ms per step).
   if (c->A <= 255) {
     const size_t sm = bid_smem_bytes(c->A, span, true, 1);
     if (g) go(bidcurve_kernel<true, uint8_t, true>, sm); else go(bidcurve_kernel<true, uint8_t, false>, sm);
-  } else if (bid_smem_bytes(c->A, span, true, 2) <= 200 * 1024) {
-    const size_t sm = bid_smem_bytes(c->A, span, true, 2);
-    if (g) go(bidcurve_kernel<true, int16_t, true>, sm); else go(bidcurve_kernel<true, int16_t, false>, sm);
   } else {
     const size_t sm = bid_smem_bytes(c->A, span, false, 2);
     if (g) go(bidcurve_kernel<false, int16_t, true>, sm); else go(bidcurve_kernel<false, int16_t, false>, sm);

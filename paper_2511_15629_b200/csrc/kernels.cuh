@@ -774,7 +774,7 @@ __device__ __forceinline__ void bid_curve(const BidTables& tb, const double* Wi,
 // rest of the stack as action indices in shared memory (column-major per thread: conflict-free); u of a
 // deeper vertex is recomputed from its index when it resurfaces.  When every request of the block is on
 // the same (t, k) row (the common "all i of a stage" case) the W row segment is staged in shared memory.
-// kSmem = false: the stack lives in the caller's vert row (very large A).  kG: payoff lambda p - g(p)
+// kSmem = false: the stack lives in the caller's vert row (A > 255: occupancy, see launch_bids).  kG: payoff lambda p - g(p)
 // (u = Wint - g_a, R13), else u = Wint.  Per-action offset and interpolation flag share one word.
 template <bool kSmem, typename IdxT, bool kG>
 __global__ void __launch_bounds__(kBidThreads) bidcurve_kernel(BidParams bp, int64_t n, const int32_t* __restrict__ req,

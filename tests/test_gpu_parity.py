@@ -385,6 +385,46 @@ def test_bidcurves_cfg1(name):
         assert np.array_equal(out["price"][j, :n - 1], c["price"])
 
 
+@pytest.mark.parametrize("fused", [False, True])
+def test_bidcurves_wide_grid_global_stack(fused):
+    """A > 255 (cfg4's grid, A = 401: the hull stack lives in the vertex row in global memory): vertices,
+    quantities and prices bit-identical to the oracle, on demand and fused into the backward graph, every
+    stage of a short horizon and SoC rows across the grid (ragged S = 2001)."""
+    inst = workloads.cfg4(T=3, K=4)
+    pr = to_oracle(inst)
+    ref = oracle.backward(pr, nthreads=16)
+    req = np.array([(t, i, k) for t in range(1, inst.T + 1) for i in list(range(0, 2001, 37)) + [1999, 2000]
+                    for k in (0, 3)], dtype=np.int32)
+    with _gpu(inst) as s:
+        assert s.A == 401
+        if fused:
+            import torch
+            n, cap = len(req), s.A
+            nv = torch.zeros(n, dtype=torch.int32, device="cuda")
+            vt = torch.zeros(cap * n, dtype=torch.int16, device="cuda")
+            qq = torch.zeros(cap * n, dtype=torch.float64, device="cuda")
+            pp = torch.zeros(cap * n, dtype=torch.float64, device="cuda")
+            E.esdp_set_bid_requests(s.ctx, req, cap, nv.data_ptr(), vt.data_ptr(), qq.data_ptr(), pp.data_ptr())
+            s.backward()
+            torch.cuda.synchronize()
+            nvh = nv.cpu().numpy()
+            vth = vt.cpu().numpy().reshape(cap, n).T
+            pph = pp.cpu().numpy().reshape(cap, n).T
+            qqh = qq.cpu().numpy().reshape(cap, n).T
+        else:
+            s.backward()
+            out = s.bidcurves(req)
+            nvh, vth, pph, qqh = out["nvert"], out["vert"], out["price"], out["q"]
+    acts = oracle.actions(pr)
+    for j, (t, i, k) in enumerate(req):
+        c = oracle.bidcurve(pr, ref.W, int(t), int(i), int(k))
+        nn = int(nvh[j])
+        assert nn == c["nvert"], (t, i, k)
+        assert np.array_equal(vth[j, :nn], c["vert"]), (t, i, k)
+        assert np.array_equal(pph[j, :nn - 1], c["price"]), (t, i, k)
+        assert np.array_equal(qqh[j, :nn], acts[c["vert"]]), (t, i, k)
+
+
 @pytest.mark.parametrize("name", ["cfg1b", "cfg1b-rank1", "cfg2"])
 def test_simulation_per_path_bitexact(name):
     inst = workloads.cfg2(T=48, K=30) if name == "cfg2" else workloads.cfg1("b", rank1=name.endswith("rank1"))

@@ -753,14 +753,11 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
 // Requires rows <= 128, K <= 128, non-negative P and V.
 cudaError_t launch_ozaki(const double* Pt, const double* Vn, double* Wt, int rows, int K, long long ncols, long long ldv,
                          long long ldw, cudaStream_t s, bool pdl) {
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const cudaError_t e = cudaFuncSetAttribute(ozaki_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem);
-    if (e != cudaSuccess) { nsm = 0; return e; }
-  }
+  int dev = 0, nsm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(ozaki_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem);
+  if (e != cudaSuccess) return e;
   const long long ntiles = (ncols + kOzN - 1) / kOzN;
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles, nsm));
   return launch(ozaki_contract_kernel, dim3(grid), dim3(kOzThreads), kOzSmem, s, pdl, Pt, Vn, Wt, rows, K, ncols, ldv, ldw);

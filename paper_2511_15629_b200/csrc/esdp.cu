@@ -1421,7 +1421,8 @@ static esdp_status load_impl(esdp_ctx* c, const double* lambda, const double* P,
   // validate what is given against the current arrays' shapes
   std::vector<double> lam_h, P_h, pi_h, g_h;
   const size_t TK = (size_t)c->T * c->K;
-  if (!lambda || !P || !pi || !g) CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));
+  const bool read_back = !lambda || (!c->rank1 && !P && c->T > 1) || !pi || (!g && c->kind != ESDP_PAYOFF_LINEAR);
+  if (read_back) CUDA_OR_FAIL(c, cudaStreamSynchronize(c->copy));   // kept arrays are validated from the device copy
   if (!lambda) { lam_h.resize(TK); CUDA_OR_FAIL(c, cudaMemcpy(lam_h.data(), o.lambda, TK * 8, cudaMemcpyDeviceToHost)); }
   if (!c->rank1 && !P && c->T > 1) { P_h.resize((size_t)(c->T - 1) * c->K * c->K); CUDA_OR_FAIL(c, cudaMemcpy(P_h.data(), o.P, P_h.size() * 8, cudaMemcpyDeviceToHost)); }
   if (!pi) { pi_h.resize(c->rank1 ? TK : c->K); CUDA_OR_FAIL(c, cudaMemcpy(pi_h.data(), o.pi, pi_h.size() * 8, cudaMemcpyDeviceToHost)); }

@@ -210,6 +210,33 @@ def test_cfg2_rank1_full_size():
     _compare_all(workloads.cfg2(rank1=True), nthreads=16, expect_window=True)
 
 
+def test_table3_largest_row_shape():
+    """The paper's Table 3 largest row (bench.py --config table3) at its full per-stage shape: S = 10001,
+    A = 203, R = K = 200 rank-1 price samples, on a 48-hour horizon (the stage's launch configuration -- grid,
+    four outputs per thread, the rank-1 GEMV on the DMMA path -- does not depend on T): every stage's W, V and
+    policy bit-identical to the oracle's."""
+    inst = workloads.table3(T=48)
+    assert inst.K == 200 and inst.P is None
+    ref = _compare_all(inst, nthreads=16, expect_window=True)
+    assert ref.V[0].shape == (200, 10001)
+
+
+def test_table3_largest_row_full_year():
+    """The same row over the whole year (T = 8784) as bench.py times it (no ESDP_KEEP_VALUES; the oracle's
+    full solve would take ~15 CPU-minutes, so the per-stage bits are the shape test's above): J equals the
+    oracle's objective (Eq. 6 at t = 0) of the GPU's V_1, V_1 is finite on the whole grid (the zero action is
+    always feasible, Alg. 1 line 8), and every policy entry of stage 1 is an action index."""
+    inst = workloads.table3()
+    pr = to_oracle(inst)
+    with _gpu(inst, keep=False) as s:
+        J = s.backward()
+        V1 = E.esdp_values(s.ctx, 1, want_W=False)
+        assert V1.shape == (200, 10001) and np.all(np.isfinite(V1))
+        assert J == oracle.objective(pr, V1)
+        pol1 = s.policy(1)
+        assert pol1.shape == (200, 10001) and pol1.min() >= 0 and pol1.max() < len(oracle.actions(pr))
+
+
 @pytest.mark.parametrize("delta", [0.1, 0.01])
 def test_table1_deterministic_year(delta):
     """NEXT-3 (Table 1 analog): K = 1, T = 8784 hourly stages, the paper's 4-h battery at

@@ -269,11 +269,15 @@ class HostPool {
 };
 
 // Guide geometry of the sampling tables (kernels.cuh cdf_kernel): 2^g buckets per row, g in [6, 14],
-// at most the first power of two >= 16 K; g_for: the most bits for `rows` rows within `cap` entries.
+// at most the first power of two >= kGuideRatio K (at most 2^14); g_for: the most bits for `rows` rows within `cap` entries.
 constexpr int kGuideMinG = 6;
+constexpr int kGuideRatio = 64;   // cfg2 simulation 259 -> 242 us against 16 (tools/guidesweep.py)
+// buckets per state of a sampling row: ESDP_GUIDE_RATIO in the environment overrides (measurement)
 int guide_gmax(int K) {
+  const char* e = getenv("ESDP_GUIDE_RATIO");
+  const int ratio = (e && atoi(e) > 0) ? atoi(e) : kGuideRatio;
   int g = kGuideMinG;
-  while (g < 14 && (1 << g) < 16 * K) ++g;
+  while (g < 14 && (1 << g) < ratio * K) ++g;
   return g;
 }
 int guide_g_for(size_t rows, size_t cap, int gmax) {
@@ -1217,11 +1221,13 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     return bail(ESDP_E_CUDA);
   }
   const size_t T = c->T, K = c->K, S = c->S, A = c->A;
-  {   // guide geometry (kernels.cuh cdf_kernel): up to 2^g_max >= 16 K buckets per row; the allocation is
+  {   // guide geometry (kernels.cuh cdf_kernel): up to 2^g_max >= kGuideRatio K buckets per row; the allocation is
       // capped at max(256 MB, the size of P) and always holds 2^6 buckets for every possible row
     c->g_max = guide_gmax((int)K);
     const size_t rows = c->rank1 ? T : (T > 1 ? (T - 1) * K : 1);
-    const size_t budget = std::max<size_t>(256u << 20, (c->rank1 ? 0 : rows * K * 8)) / sizeof(uint64_t);
+    const char* eb = getenv("ESDP_GUIDE_BUDGET_MB");   // measurement
+    const size_t mb = (eb && atoi(eb) > 0) ? (size_t)atoi(eb) : 256u;
+    const size_t budget = std::max<size_t>(mb << 20, (c->rank1 ? 0 : rows * K * 8)) / sizeof(uint64_t);
     c->guide_cap = std::max(rows << kGuideMinG, std::min(rows << c->g_max, budget));
     c->g_r1 = guide_g_for(T, c->guide_cap, c->g_max);
   }

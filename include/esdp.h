@@ -79,6 +79,8 @@ enum {
  *                     grid, 4 for a large one and for batches)
  *   ESDP_WIN_GENERIC=1  window queries on the generic path even where the Eq. 10 fast path applies
  *   ESDP_WIN_FORCE_NONUNI=1  treat every window run table as non-unimodal (tests: the fallback paths)
+ *   ESDP_GUIDE_RATIO=n  guide buckets per price state of the simulation's sampling rows (default 64)
+ *   ESDP_GUIDE_BUDGET_MB=n  cap of the guide allocation per input slot (default 256, or the size of P)
  * DESIGN.md §5 and §7 record what each measured. */
 
 typedef struct {

@@ -54,12 +54,22 @@ struct InputSlot {
   std::vector<cudaEvent_t> chunk_ev;
   bool use_pending = false;
   bool tables_stale = false;   // P uploaded, its sampling tables (cdf / guide) not built yet
+  bool pi_stale = false;       // pi uploaded, its sampling tables (cdf1 / guide1; rank-1: cdf / guide) not built yet
+  // pinned host staging of the small host-computed uploads (tab, src, gfit): a copy from pageable memory is
+  // not a plain asynchronous DMA; stage_ev (recorded after those copies) guards the staging's reuse
+  int* stage_h = nullptr;      // [2 (T-1)] tab, then src
+  double* gfit_stage = nullptr;   // [6]
+  cudaEvent_t stage_ev = nullptr;
+  // generation of the data each array holds (esdp_ctx::gen at its upload): a kept (NULL) array is copied
+  // from the newest slot only when the generations differ
+  uint64_t gen_lambda = 0, gen_P = 0, gen_pi = 0, gen_g = 0;
   double gfit_h[6] = {0, 0, 0, 0, 0, 0};
 };
 
 struct esdp_ctx {
   // problem
   int T = 0, K = 0, S = 0, A = 0, kind = 0, rank1 = 0;
+  uint64_t gen = 0;   // upload generations (InputSlot::gen_*)
   int ld = 0;  // padded row length of V and W on the device (multiple of 4 doubles: 16-byte cp.async)
   // multi-GPU (esdp_create_dist): this rank owns price-state rows [k_lo, k_lo + k_cnt); V_t and pol_t are
   // all-gathered every stage in blocks of kmax rows (Kp = world * kmax rows per stage on every rank)
@@ -224,7 +234,9 @@ class HostPool {
  private:
   HostPool() {
     const unsigned hw = std::thread::hardware_concurrency();
-    const int nw = (int)std::min<unsigned>(15, hw > 1 ? hw - 1 : 1);
+    const char* e = getenv("ESDP_HOST_THREADS");   // measurement: threads of the host pool (caller included)
+    const unsigned cap = (e && atoi(e) > 0) ? (unsigned)atoi(e) : 16u;
+    const int nw = (int)std::max<unsigned>(1, std::min<unsigned>(cap - 1, hw > 1 ? hw - 1 : 1));
     for (int w = 0; w < nw; ++w) th_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
@@ -507,6 +519,9 @@ void free_all(esdp_ctx* c) {
       if (x.ev_head) cudaEventDestroy(x.ev_head);
       if (x.ev_tables) cudaEventDestroy(x.ev_tables);
       if (x.use_ev) cudaEventDestroy(x.use_ev);
+      if (x.stage_ev) cudaEventDestroy(x.stage_ev);
+      if (x.stage_h) cudaFreeHost(x.stage_h);
+      if (x.gfit_stage) cudaFreeHost(x.gfit_stage);
     }
     c->d_lambda = c->d_P = c->d_pi = c->d_cdf = c->d_cdf1 = c->d_g = c->d_gfit = nullptr;
     c->d_guide = c->d_guide1 = nullptr;
@@ -540,34 +555,59 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   if (d.use_pending) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, d.use_ev, 0));
   // Copies out of slot src must see its sampling tables complete: ready_tables() may have enqueued
   // their (lazy) build on a simulation stream and re-recorded ev_tables there.
-  if (copy_old) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, o.ev_tables, 0));
-  if (lambda) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, lambda, TK * sizeof(double), h2d, s));
-  else if (copy_old) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, o.lambda, TK * sizeof(double), d2d, s));
+  // No kernel runs on the copy stream while a backward graph may be running: ONE kernel of another stream
+  // during the graph costs it ~0.22 ms on B200 (tools/e2eprobe.py kernel / evrec / dma: a DMA or an event
+  // record costs nothing), and small device-to-device copies run as kernels.  So the sampling tables are
+  // built by the first simulation that needs them (ready_tables, after the backward), and a kept (NULL)
+  // array is copied from slot src only if dst does not already hold the same data (generations).
+  const bool cp_lam = !lambda && copy_old && d.gen_lambda != o.gen_lambda;
+  const bool cp_pi = !pi && copy_old && d.gen_pi != o.gen_pi;
+  const bool new_g = g && (c->kind == ESDP_PAYOFF_LINEAR_MINUS_G || c->kind == ESDP_PAYOFF_TABLE);
+  const bool cp_g = !new_g && copy_old && d.gen_g != o.gen_g;
+  const bool cp_P = !c->rank1 && !P && copy_old && d.gen_P != o.gen_P;
+  if (cp_lam || cp_pi || cp_g || cp_P) CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, o.ev_tables, 0));
+  if (lambda) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, lambda, TK * sizeof(double), h2d, s));
+    d.gen_lambda = ++c->gen;
+  } else if (cp_lam) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.lambda, o.lambda, TK * sizeof(double), d2d, s));
+    d.gen_lambda = o.gen_lambda;
+  }
   const size_t npi = c->rank1 ? TK : K;
   if (pi) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, pi, npi * sizeof(double), h2d, s));
-    if (c->rank1)   // sampling tables of the per-stage marginals pi_{t+1} (rank-1 rows)
-      launch_cdf(d.pi, nullptr, c->T, c->K, c->g_r1, d.cdf, d.guide, s);
-    launch_cdf(d.pi, nullptr, 1, c->K, c->g_max, d.cdf1, d.guide1, s);  // pi_1 (row 0 in rank-1)
-    CUDA_OR_FAIL(c, cudaGetLastError());
-  } else if (copy_old) {
+    d.pi_stale = true;
+    d.gen_pi = ++c->gen;
+  } else if (cp_pi) {
+    d.gen_pi = o.gen_pi;
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.pi, o.pi, npi * sizeof(double), d2d, s));
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf1, o.cdf1, K * sizeof(double), d2d, s));
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide1, o.guide1, sizeof(uint64_t) << c->g_max, d2d, s));
-    if (c->rank1) {
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, TK * sizeof(double), d2d, s));
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, ((size_t)c->T << c->g_r1) * sizeof(uint64_t), d2d, s));
+    d.pi_stale = o.pi_stale;
+    if (!o.pi_stale) {
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf1, o.cdf1, K * sizeof(double), d2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide1, o.guide1, sizeof(uint64_t) << c->g_max, d2d, s));
+      if (c->rank1) {
+        CUDA_OR_FAIL(c, cudaMemcpyAsync(d.cdf, o.cdf, TK * sizeof(double), d2d, s));
+        CUDA_OR_FAIL(c, cudaMemcpyAsync(d.guide, o.guide, ((size_t)c->T << c->g_r1) * sizeof(uint64_t), d2d, s));
+      }
     }
   }
   const size_t ng = c->kind == ESDP_PAYOFF_TABLE ? TK * c->A : (size_t)c->A;
+  // the staging of dst is rewritten below: its previous copies (an earlier upload into dst) must have run
+  if (g || P) CUDA_OR_FAIL(c, cudaEventSynchronize(d.stage_ev));
+  bool staged = false;
   if (g && c->kind == ESDP_PAYOFF_LINEAR_MINUS_G) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, g, c->A * sizeof(double), h2d, s));
     // a later g that is not affine on the runs only widens eps (more canonical fallbacks, same result)
     if (c->use_window) fit_g(c, g, d.gfit_h);
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.gfit, d.gfit_h, sizeof d.gfit_h, h2d, s));
+    std::memcpy(d.gfit_stage, d.gfit_h, sizeof d.gfit_h);
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(d.gfit, d.gfit_stage, sizeof d.gfit_h, h2d, s));
+    staged = true;
+    d.gen_g = ++c->gen;
   } else if (g && c->kind == ESDP_PAYOFF_TABLE) {
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, g, ng * sizeof(double), h2d, s));
-  } else if (copy_old) {
+    d.gen_g = ++c->gen;
+  } else if (cp_g) {   // (a g given with the LINEAR payoff is ignored, as a NULL one)
+    d.gen_g = o.gen_g;
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.g, o.g, ng * sizeof(double), d2d, s));
     std::memcpy(d.gfit_h, o.gfit_h, sizeof d.gfit_h);
     CUDA_OR_FAIL(c, cudaMemcpyAsync(d.gfit, o.gfit, sizeof d.gfit_h, d2d, s));
@@ -576,7 +616,7 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   // P chunks: the backward waits only for the copy; the sampling tables (needed by the simulation
   // alone) are built after it and signalled by ev_tables
   for (size_t j = 0; j < d.chunk_ev.size(); ++j) {
-    if (!c->rank1 && (P || copy_old)) {
+    if (P || cp_P) {
       const size_t r0 = (size_t)(c->chunk_lo[j] - 1) * K, nr = (size_t)(c->chunk_hi[j] - c->chunk_lo[j] + 1) * K;
       if (P) CUDA_OR_FAIL(c, cudaMemcpyAsync(d.P + r0 * K, P + r0 * K, nr * K * sizeof(double), h2d, s));
       else CUDA_OR_FAIL(c, cudaMemcpyAsync(d.P + r0 * K, o.P + r0 * K, nr * K * sizeof(double), d2d, s));
@@ -584,9 +624,7 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
     CUDA_OR_FAIL(c, cudaEventRecord(d.chunk_ev[j], s));
   }
   // The sampling tables of P are built lazily by the first simulation that needs them (ready_tables), on
-  // that simulation's stream: built here, 287 distinct slices' blocks shared the SMs with the running
-  // backward's latency-bound stage chain and stretched it (measured +0.3 ms per cfg2 solve).  A few
-  // distinct slices (<= 4096 rows, a handful of blocks) are built right here instead.
+  // that simulation's stream (see above: even a few blocks here stretched the running backward).
   if (!c->rank1 && c->T > 1) {
     const int nst = c->T - 1;
     if (P) {   // one table per distinct slice P_t; as many guide bits as the allocation allows
@@ -594,15 +632,15 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
       dedupe_slices(P, nst, c->K, tab, src);
       d.nuniq = (int)src.size();
       d.gbits = guide_g_for((size_t)d.nuniq * K, c->guide_cap, c->g_max);
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, tab.data(), nst * sizeof(int), h2d, s));
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.src, src.data(), src.size() * sizeof(int), h2d, s));
+      std::memcpy(d.stage_h, tab.data(), nst * sizeof(int));
+      std::memcpy(d.stage_h + nst, src.data(), src.size() * sizeof(int));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, d.stage_h, nst * sizeof(int), h2d, s));
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(d.src, d.stage_h + nst, src.size() * sizeof(int), h2d, s));
+      staged = true;
       d.tables_stale = true;
-      if ((size_t)d.nuniq * K <= 4096) {   // few distinct slices: a handful of blocks, built right after P lands
-        launch_cdf(d.P, d.src, (int64_t)d.nuniq * c->K, c->K, d.gbits, d.cdf, d.guide, s);
-        CUDA_OR_FAIL(c, cudaGetLastError());
-        d.tables_stale = false;
-      }
-    } else if (copy_old) {
+      d.gen_P = ++c->gen;
+    } else if (cp_P) {
+      d.gen_P = o.gen_P;
       d.nuniq = o.nuniq;
       d.gbits = o.gbits;
       CUDA_OR_FAIL(c, cudaMemcpyAsync(d.tab, o.tab, nst * sizeof(int), d2d, s));
@@ -617,6 +655,7 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
       }
     }
   }
+  if (staged) CUDA_OR_FAIL(c, cudaEventRecord(d.stage_ev, s));
   CUDA_OR_FAIL(c, cudaEventRecord(d.ev_tables, s));
   return ESDP_OK;
 }
@@ -635,12 +674,18 @@ void sim_tables(const esdp_ctx* c, SimParams& sp) {
 esdp_status ready_tables(esdp_ctx* c, cudaStream_t s) {
   InputSlot& x = c->slot[c->active];
   CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, x.ev_tables, 0));
-  if (x.tables_stale) {
-    launch_cdf(x.P, x.src, (int64_t)x.nuniq * c->K, c->K, x.gbits, x.cdf, x.guide, s);
-    CUDA_OR_FAIL(c, cudaGetLastError());
-    CUDA_OR_FAIL(c, cudaEventRecord(x.ev_tables, s));
-    x.tables_stale = false;
-  }
+  if (!x.pi_stale && !x.tables_stale) return ESDP_OK;
+  // one launch: the rows (rank-1: the per-stage marginals pi_{t+1}; Markov: the distinct slices of P) and
+  // the single row pi_1 (row 0 of pi in rank-1), each only if stale
+  const double* q1 = x.pi_stale ? x.pi : nullptr;
+  if (c->rank1)
+    launch_cdf(x.pi, nullptr, x.pi_stale ? c->T : 0, c->K, c->g_r1, x.cdf, x.guide, s, q1, c->g_max, x.cdf1, x.guide1);
+  else
+    launch_cdf(x.P, x.src, x.tables_stale ? (int64_t)x.nuniq * c->K : 0, c->K, x.gbits, x.cdf, x.guide, s, q1,
+               c->g_max, x.cdf1, x.guide1);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  CUDA_OR_FAIL(c, cudaEventRecord(x.ev_tables, s));   // later copies out of this slot wait for the builds
+  x.pi_stale = x.tables_stale = false;
   return ESDP_OK;
 }
 
@@ -1330,7 +1375,10 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
     for (InputSlot& x : c->slot) {
       bool ok = cudaEventCreateWithFlags(&x.ev_head, cudaEventDisableTiming) == cudaSuccess &&
                 cudaEventCreateWithFlags(&x.ev_tables, cudaEventDisableTiming) == cudaSuccess &&
-                cudaEventCreateWithFlags(&x.use_ev, cudaEventDisableTiming) == cudaSuccess;
+                cudaEventCreateWithFlags(&x.use_ev, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming) == cudaSuccess &&
+                cudaMallocHost(&x.stage_h, sizeof(int) * 2 * (size_t)std::max(1, nst)) == cudaSuccess &&
+                cudaMallocHost(&x.gfit_stage, sizeof(double) * 6) == cudaSuccess;
       x.chunk_ev.assign(nch, nullptr);
       for (int j = 0; j < nch && ok; ++j) ok = cudaEventCreateWithFlags(&x.chunk_ev[j], cudaEventDisableTiming) == cudaSuccess;
       if (!ok) { fail(c, ESDP_E_CUDA, "input events"); return bail(ESDP_E_CUDA); }

@@ -892,55 +892,68 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
 //                ties the truncated bits compares u with cdf[j_lo] itself).
 // One warp per row; rows are (table u, state k), read from P row (src[u] K + k) (src: the stage whose
 // slice a deduplicated table u stands for; NULL: u itself).
-constexpr int kCdfWarps = 4;
-constexpr int kCdfSmemK = 1024;   // rows up to this K are staged in shared memory
+constexpr int kCdfThreads = 128;   // one block per sampling row
+constexpr int kCdfSmemK = 1024;    // rows up to this K are staged in shared memory
 constexpr int kGuideJ = 49, kGuideD = 43;
 constexpr uint64_t kGuideThr = (1ull << kGuideD) - 1;
+// One sampling row per block: the cumulative sums (ascending, the definition's order; the last entry is 1),
+// then the 2^g guide entries, every thread walking its interleaved buckets from its previous answer.
+// Blocks [0, rows) build rows of q (src: deduplicated slices, NULL: row r of q); block `rows` (if q1)
+// builds the single row q1 (pi_1) -- both jobs of a load in one launch.
 template <bool kSmem>
-__global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __restrict__ q, const int* __restrict__ src,
-                                                            int64_t rows, int K, int g, double* __restrict__ cdf,
-                                                            uint64_t* __restrict__ guide) {
-  __shared__ double cdf_sm[kSmem ? kCdfWarps * kCdfSmemK : 1];
-  const int64_t r = (int64_t)blockIdx.x * kCdfWarps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const int64_t u = r / K, k = r - u * K;
-  const double* qr = q + ((src ? (int64_t)src[u] : u) * K + k) * K;
-  double* cg = cdf + r * K;
-  uint64_t* gr = guide + (r << g);
-  double* cr = kSmem ? cdf_sm + (size_t)(threadIdx.x >> 5) * kCdfSmemK : cg;
-  if (kSmem) {   // every lane forms the same sequential sum over broadcast values and keeps its entries
-    double sum = 0.0;
-    for (int j0 = 0; j0 < K; j0 += 32) {
-      const int j = j0 + lane;
-      const double v = j < K ? __ldg(qr + j) : 0.0;
-      const int n = min(32, K - j0);
-      double mine = 0.0;
-      for (int l = 0; l < n; ++l) {
-        sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, v, l));
-        if (l == lane) mine = sum;
+__global__ void __launch_bounds__(kCdfThreads) cdf_kernel(const double* __restrict__ q, const int* __restrict__ src,
+                                                        int64_t rows, int K, int g, double* __restrict__ cdf,
+                                                        uint64_t* __restrict__ guide, const double* __restrict__ q1,
+                                                        int g1, double* __restrict__ cdf1, uint64_t* __restrict__ guide1) {
+  __shared__ double cdf_sm[kSmem ? kCdfSmemK : 1];
+  const int64_t r = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const double* qr;
+  double* cg;
+  uint64_t* gr;
+  if (r < rows) {
+    const int64_t u = r / K, k = r - u * K;
+    qr = q + ((src ? (int64_t)src[u] : u) * K + k) * K;
+    cg = cdf + r * K;
+    gr = guide + (r << g);
+  } else {   // the single-row job
+    qr = q1; cg = cdf1; gr = guide1; g = g1;
+  }
+  double* cr = kSmem ? cdf_sm : cg;
+  if (tid < 32) {
+    if (kSmem) {   // every lane forms the same sequential sum over broadcast values and keeps its entries
+      double sum = 0.0;
+      for (int j0 = 0; j0 < K; j0 += 32) {
+        const int j = j0 + lane;
+        const double v = j < K ? __ldg(qr + j) : 0.0;
+        const int n = min(32, K - j0);
+        double mine = 0.0;
+        for (int l = 0; l < n; ++l) {
+          sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, v, l));
+          if (l == lane) mine = sum;
+        }
+        if (j < K) {
+          const double c = (j == K - 1) ? 1.0 : mine;
+          cr[j] = c;
+          cg[j] = c;
+        }
       }
-      if (j < K) {
-        const double c = (j == K - 1) ? 1.0 : mine;
-        cr[j] = c;
-        cg[j] = c;
+    } else if (lane == 0) {
+      double sum = 0.0;
+      for (int j = 0; j < K; ++j) {
+        sum = __dadd_rn(sum, qr[j]);
+        cr[j] = (j == K - 1) ? 1.0 : sum;
       }
-    }
-  } else if (lane == 0) {
-    double sum = 0.0;
-    for (int j = 0; j < K; ++j) {
-      sum = __dadd_rn(sum, qr[j]);
-      cr[j] = (j == K - 1) ? 1.0 : sum;
     }
   }
-  __syncwarp();
+  __syncthreads();
   const int s = 53 - g;
   const double inv = ldexp(1.0, -g);
-  for (int b = lane; b < (1 << g); b += 32) {     // interleaved buckets: coalesced 8-byte stores
+  int jl = 0;                                      // this thread's previous answer: monotone in the bucket
+  for (int b = tid; b < (1 << g); b += kCdfThreads) {   // interleaved buckets: coalesced 8-byte stores
     const double lo = (double)b * inv, hi = (double)(b + 1) * inv;   // exact (powers of two)
-    int a = 0, z = K - 1;                          // first j with lo < cdf[j] (cdf[K-1] = 1 > lo)
-    while (a < z) { const int mid = (a + z) >> 1; if (lo < cr[mid]) z = mid; else a = mid + 1; }
-    const int jl = a;
+    while (!(lo < cr[jl])) ++jl;                   // first j with lo < cdf[j] (cdf[K-1] = 1 > lo): a short walk
+                                                   // from this thread's last bucket, not a binary search
     const double cl = cr[jl];
     uint64_t e = (uint64_t)jl << kGuideJ;
     if (cl < hi) {                                 // a boundary inside the bucket
@@ -958,13 +971,16 @@ __global__ void __launch_bounds__(kCdfWarps * 32) cdf_kernel(const double* __res
   }
 }
 
-inline unsigned cdf_blocks(int64_t rows) { return (unsigned)((rows + kCdfWarps - 1) / kCdfWarps); }
-
+// rows of q (and, if q1, the single row q1) in one launch
 inline void launch_cdf(const double* q, const int* src, int64_t rows, int K, int g, double* cdf, uint64_t* guide,
-                       cudaStream_t s) {
-  if (rows <= 0) return;
-  if (K <= kCdfSmemK) cdf_kernel<true><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, src, rows, K, g, cdf, guide);
-  else cdf_kernel<false><<<cdf_blocks(rows), kCdfWarps * 32, 0, s>>>(q, src, rows, K, g, cdf, guide);
+                       cudaStream_t s, const double* q1 = nullptr, int g1 = 0, double* cdf1 = nullptr,
+                       uint64_t* guide1 = nullptr) {
+  const int64_t nb = rows + (q1 ? 1 : 0);
+  if (nb <= 0) return;
+  if (K <= kCdfSmemK)
+    cdf_kernel<true><<<(unsigned)nb, kCdfThreads, 0, s>>>(q, src, rows, K, g, cdf, guide, q1, g1, cdf1, guide1);
+  else
+    cdf_kernel<false><<<(unsigned)nb, kCdfThreads, 0, s>>>(q, src, rows, K, g, cdf, guide, q1, g1, cdf1, guide1);
 }
 
 // first j in [0, K) with u < cdf[j] (m: the draw's 53-bit integer, u = m 2^-53); gs = 53 - g.  Split into the

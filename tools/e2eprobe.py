@@ -15,7 +15,7 @@ n = req.shape[0]
 nv = torch.empty(n, dtype=torch.int32, device="cuda"); vert = torch.empty(n * A, dtype=torch.int16, device="cuda")
 pr = torch.empty(n * A, dtype=torch.float64, device="cuda")
 mode = sys.argv[1] if len(sys.argv) > 1 else "load"
-if mode != "nobids":
+if "nobids" not in mode:
     E.esdp_set_bid_requests(s.ctx, req, A, nv.data_ptr(), vert.data_ptr(), None, pr.data_ptr())
 stream = torch.cuda.Stream(); sp = stream.cuda_stream
 lam_h = torch.from_numpy(np.ascontiguousarray(inst.lam)).pin_memory()
@@ -25,17 +25,37 @@ dp = ctypes.POINTER(ctypes.c_double); as_p = lambda t: ctypes.cast(t.data_ptr(),
 side = torch.cuda.Stream()
 P_dev = torch.empty_like(P_h, device="cuda")
 st_d = torch.zeros(2, dtype=torch.float64, device="cuda")
+st_side = torch.zeros(1024, dtype=torch.float64, device="cuda")
+side_ev, main_ev = torch.cuda.Event(), torch.cuda.Event()
+side_hi = torch.cuda.Stream(priority=-5)
 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(13)]
 mid = [torch.cuda.Event(enable_timing=True) for _ in range(13)]
 for j in range(13):
     evs[j][0].record(stream)
     E.lib.esdp_backward_async(s.ctx, sp)
     mid[j].record(stream)
+    main_ev.record(stream)
     if mode == "load":
         assert E.lib.esdp_load_async(s.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None) == 0
     if mode == "dma":
         with torch.cuda.stream(side):
             P_dev.copy_(P_h, non_blocking=True)
+    if mode.endswith("kernel") and mode != "dmakernel":   # one small kernel on another stream while the backward runs
+        with torch.cuda.stream(side):
+            st_side.add_(1.0)
+    if mode == "evrec":     # an event record on another stream
+        side_ev.record(side)
+    if mode == "evwait":    # another stream waits for the main stream (cross-stream dependency), then a DMA
+        side.wait_event(main_ev)
+        with torch.cuda.stream(side):
+            P_dev.copy_(P_h, non_blocking=True)
+    if mode == "kernelhi":  # the small kernel on a high-priority stream
+        with torch.cuda.stream(side_hi):
+            st_side.add_(1.0)
+    if mode == "dmakernel":
+        with torch.cuda.stream(side):
+            P_dev.copy_(P_h, non_blocking=True)
+            st_side.add_(1.0)
     E.lib.esdp_simulate_async(s.ctx, 65536, 99 + j, ctypes.c_void_p(st_d.data_ptr()), sp)
     evs[j][1].record(stream)
 torch.cuda.synchronize()
@@ -44,11 +64,28 @@ for j in range(10):
     evs[j][0].record(stream)
     E.lib.esdp_backward_async(s.ctx, sp)
     mid[j].record(stream)
+    main_ev.record(stream)
     if mode == "load":
         assert E.lib.esdp_load_async(s.ctx, as_p(lam_h), as_p(P_h), as_p(pi_h), None) == 0
     if mode == "dma":
         with torch.cuda.stream(side):
             P_dev.copy_(P_h, non_blocking=True)
+    if mode.endswith("kernel") and mode != "dmakernel":   # one small kernel on another stream while the backward runs
+        with torch.cuda.stream(side):
+            st_side.add_(1.0)
+    if mode == "evrec":     # an event record on another stream
+        side_ev.record(side)
+    if mode == "evwait":    # another stream waits for the main stream (cross-stream dependency), then a DMA
+        side.wait_event(main_ev)
+        with torch.cuda.stream(side):
+            P_dev.copy_(P_h, non_blocking=True)
+    if mode == "kernelhi":  # the small kernel on a high-priority stream
+        with torch.cuda.stream(side_hi):
+            st_side.add_(1.0)
+    if mode == "dmakernel":
+        with torch.cuda.stream(side):
+            P_dev.copy_(P_h, non_blocking=True)
+            st_side.add_(1.0)
     E.lib.esdp_simulate_async(s.ctx, 65536, 99 + j, ctypes.c_void_p(st_d.data_ptr()), sp)
     evs[j][1].record(stream)
 torch.cuda.synchronize()

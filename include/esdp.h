@@ -81,6 +81,9 @@ enum {
  *   ESDP_WIN_FORCE_NONUNI=1  treat every window run table as non-unimodal (tests: the fallback paths)
  *   ESDP_GUIDE_RATIO=n  guide buckets per price state of the simulation's sampling rows (default 64)
  *   ESDP_GUIDE_BUDGET_MB=n  cap of the guide allocation per input slot (default 256, or the size of P)
+ *   ESDP_FB_MODE=0|1|2  fused bid curves: side branches along the stage chain (0, default), the same batches
+ *                     forked after stage 1 (1), one launch on the chain stream after stage 1 (2)
+ *   ESDP_HOST_THREADS=n  threads of the host pool (validation, slice hashing; default min(16, cores))
  * DESIGN.md §5 and §7 record what each measured. */
 
 typedef struct {

@@ -960,6 +960,9 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
   };
   bool after_kernel = false;  // a PDL edge needs a kernel predecessor
   bool forked = false;
+  // fused bid curves: 0 = side branches along the chain (default); 1 = the same batches, forked after stage 1;
+  // 2 = one launch over every request on the chain stream after stage 1 (ESDP_FB_MODE, measurement)
+  const int fb_mode = [] { const char* e = getenv("ESDP_FB_MODE"); return e ? atoi(e) : 0; }();
   std::vector<char> side_used(c->side.size(), 0);
   for (int t = T; t >= 1; --t) {
     if (t == T) {
@@ -982,7 +985,7 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
     // curves to fill the GPU) and every batch is a side branch of the graph on its own stream: it runs
     // concurrently with the remaining, latency-bound stages of the chain.
     const int bt = (t - 1) / c->fb_batch;                       // batch of stage t (stages bt*B+1 .. bt*B+B)
-    if (c->fb_n > 0 && (t - 1) % c->fb_batch == 0) {            // t is the lowest stage of its batch: W ready
+    if (c->fb_n > 0 && fb_mode == 0 && (t - 1) % c->fb_batch == 0) {   // t: the lowest stage of its batch, W ready
       const int t_hi = std::min(c->T, t + c->fb_batch - 1);
       const int64_t lo = c->fb_off[t], cnt = c->fb_off[t_hi + 1] - lo;
       if (cnt > 0) {
@@ -1012,6 +1015,26 @@ esdp_status enqueue_backward(esdp_ctx* c, cudaStream_t s) {
       if (r != ncclSuccess || r2 != ncclSuccess)
         return fail(c, ESDP_E_NCCL, "ncclAllGather(V_%d): %s", t, ncclGetErrorString(r != ncclSuccess ? r : r2));
       after_kernel = false;
+    }
+  }
+  if (c->fb_n > 0 && fb_mode == 2) {
+    CUDA_OR_FAIL(c, launch_bids(c, c->fb_n, c->d_fb_req, c->d_fb_slot, c->fb_n, c->fb_cap, c->fb_nvert, c->fb_vert,
+                                c->fb_q, c->fb_price, s));
+    ++n;
+  } else if (c->fb_n > 0 && fb_mode == 1) {
+    for (int t = 1; t <= T; t += c->fb_batch) {
+      const int t_hi = std::min(c->T, t + c->fb_batch - 1);
+      const int64_t lo = c->fb_off[t], cnt = c->fb_off[t_hi + 1] - lo;
+      if (cnt <= 0) continue;
+      const int bt = (t - 1) / c->fb_batch;
+      cudaStream_t sb = c->side[bt % c->side.size()];
+      side_used[bt % c->side.size()] = 1;
+      CUDA_OR_FAIL(c, cudaEventRecord(c->fb_ev[t - 1], s));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(sb, c->fb_ev[t - 1], 0));
+      CUDA_OR_FAIL(c, launch_bids(c, cnt, c->d_fb_req + 3 * lo, c->d_fb_slot + lo, c->fb_n, c->fb_cap, c->fb_nvert,
+                                  c->fb_vert, c->fb_q, c->fb_price, sb));
+      forked = true;
+      ++n;
     }
   }
   if (c->comm) {   // every stage's policy rows to every rank, once, off the stage chain (one NCCL group)

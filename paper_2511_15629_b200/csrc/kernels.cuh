@@ -890,7 +890,7 @@ __device__ __forceinline__ void sim_uniforms(uint64_t seed, int64_t path, int t,
 //                     63  several boundaries: scan the cdf row from j_lo (as the definition reads)
 //   bits 42..0   T - b 2^s, aligned to 43 bits (exact when s <= 43; else truncated, and a draw that
 //                ties the truncated bits compares u with cdf[j_lo] itself).
-// One warp per row; rows are (table u, state k), read from P row (src[u] K + k) (src: the stage whose
+// One block per row; rows are (table u, state k), read from P row (src[u] K + k) (src: the stage whose
 // slice a deduplicated table u stands for; NULL: u itself).
 constexpr int kCdfThreads = 128;   // one block per sampling row
 constexpr int kCdfSmemK = 1024;    // rows up to this K are staged in shared memory

@@ -748,6 +748,44 @@ def test_lambda_only_load_after_side_stream_simulation():
         assert np.array_equal(per, sy)
 
 
+@pytest.mark.parametrize("rank1", [False, True])
+def test_partial_loads_alternate_slots(rank1):
+    """Loads that replace one array at a time (lambda only, g only, pi only, P only) alternate between the two
+    input slots: a kept array is copied into the other slot only when that slot does not already hold it
+    (upload generations), the sampling tables are built lazily by the next simulation.  After every load the
+    solve, every policy and a simulation equal the oracle's on the combined inputs, bit for bit (LINEAR_MINUS_G
+    payoff, so g and its window fit travel too)."""
+    import dataclasses
+    with E.Solver(workloads.cfg2(T=2, K=2)) as s0:
+        acts = s0.actions()
+    x = workloads.cfg3_gpu(acts, T=24, K=12, rank1=rank1)
+    rng = np.random.Generator(np.random.PCG64(4242))
+    lam2 = np.ascontiguousarray(x.lam * 1.1 - 2.0)
+    g2 = np.ascontiguousarray(x.g * 0.5)
+    if rank1:
+        pi2 = rng.dirichlet(np.ones(x.K), size=x.T)
+    else:
+        pi2 = rng.dirichlet(np.ones(x.K))
+    P2 = None if rank1 else np.ascontiguousarray(rng.dirichlet(np.ones(x.K) * 0.5, size=(x.T - 1, x.K)))
+    steps = [dict(lam=lam2), dict(g=g2), dict(lam=x.lam), dict(pi=pi2), dict(P=P2), dict(lam=lam2), dict()]
+    cur = dict(lam=x.lam, g=x.g, pi=x.pi, P=x.P)
+    n = 4096
+    with E.Solver(x) as s:
+        for j, upd in enumerate(steps):
+            upd = {k: v for k, v in upd.items() if v is not None}
+            if upd:
+                E.esdp_load(s.ctx, **upd)
+            cur.update(upd)
+            y = dataclasses.replace(x, **cur)
+            pr = to_oracle(y)
+            ref = oracle.backward(pr, nthreads=16)
+            assert s.backward() == ref.J, j
+            for t in (1, y.T // 2, y.T):
+                assert np.array_equal(s.policy(t), ref.pol[t - 1]), (j, t)
+            per, _, _ = s.simulate(n, seed=11 + j)
+            assert np.array_equal(per, oracle.simulate(pr, ref.pol, n, seed=11 + j)[0]), j
+
+
 @pytest.mark.parametrize("name", ["cfg2-small", "cfg2-rank1-small"])
 def test_dmma_probe_failure_falls_back_to_dfma(name, monkeypatch):
     """The DMMA bit-exactness guard: a failed DMMA-vs-fma-chain probe at context creation (forced with

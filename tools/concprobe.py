@@ -1,6 +1,8 @@
-"""Cost of ONE small kernel on another stream while the backward graph runs (diagnostic): the cfg2
-backward (KEEP_VALUES, no bid curves) device-timed alone and with a one-block kernel launched on a second
-stream before the graph, right after its launch, or 1 ms into it; second stream at low or high priority."""
+"""Cost of one small operation on another stream while the backward graph runs (diagnostic): the cfg2
+backward (KEEP_VALUES, no bid curves, synchronized between steps) device-timed alone and with a one-block
+kernel, a 1 KB / 4 MB pinned H2D copy or an event record on a second stream, right after the graph's launch
+or 1 ms into it.  (In this synchronized setting none of them cost anything measurable; in the pipelined loop of
+tools/e2eprobe.py a foreign kernel costs the graph ~0.22 ms -- DESIGN.md §7.)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -556,8 +556,8 @@ esdp_status upload(esdp_ctx* c, int dst, int src, const double* lambda, const do
   // Copies out of slot src must see its sampling tables complete: ready_tables() may have enqueued
   // their (lazy) build on a simulation stream and re-recorded ev_tables there.
   // No kernel runs on the copy stream while a backward graph may be running: ONE kernel of another stream
-  // during the graph costs it ~0.22 ms on B200 (tools/e2eprobe.py kernel / evrec / dma: a DMA or an event
-  // record costs nothing), and small device-to-device copies run as kernels.  So the sampling tables are
+  // enqueued during the pipelined loop's graph cost it ~0.22 ms on B200 (tools/e2eprobe.py kernel / evrec /
+  // dma: a DMA or an event record costs nothing), and small device-to-device copies run as kernels.  So the sampling tables are
   // built by the first simulation that needs them (ready_tables, after the backward), and a kept (NULL)
   // array is copied from slot src only if dst does not already hold the same data (generations).
   const bool cp_lam = !lambda && copy_old && d.gen_lambda != o.gen_lambda;

@@ -1967,6 +1967,11 @@ struct esdp_batch {
   size_t ntab_cap = 0;   // sampling-table rows the guide allocation holds (distinct P_t slices x K)
   size_t win_smem = 0, brute_smem = 0;
   cudaStream_t stream = nullptr;
+  // instance groups with independent stage chains (graph branches; ESDP_BATCH_GROUPS): group g's expectation
+  // runs while another group's window stencil does
+  int groups = 1;
+  std::vector<cudaStream_t> gstream;   // groups - 1 extra capture streams
+  std::vector<cudaEvent_t> gev;        // fork, offset and join events
   cudaGraphExec_t graph = nullptr;
   int64_t launches = 0;
   bool solved = false;
@@ -2005,6 +2010,8 @@ void batch_free(esdp_batch* b) {
   for (void* p : ps)
     if (p) cudaFree(p);
   for (esdp_ctx* c : b->inst) esdp_destroy(c);
+  for (cudaStream_t x : b->gstream) if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : b->gev) if (e) cudaEventDestroy(e);
   if (b->stream) cudaStreamDestroy(b->stream);
 }
 
@@ -2012,17 +2019,24 @@ void batch_free(esdp_batch* b) {
 // over every window-plan instance, one brute-force launch per other instance; then every J.
 // One batch kernel of stage t: what = 0 the contraction W_t = P_t V_{t+1} over all instances' columns,
 // 1 the window-plan instances' stencil, 2 the brute-force instances' stencil.
-cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, bool pdl) {
+// g0, gn: the instances [g0, g0 + gn) (an instance group; columns [g0 ld, (g0 + gn) ld) of V and W).  Groups
+// other than the whole batch only for the DMMA / Ozaki expectation and the window stencil (all instances
+// window-plan: the window list is then 0 .. n-1).
+cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, bool pdl, int g0 = 0, int gn = -1) {
   const int T = b->T, K = b->K, S = b->S, n = b->n;
   const size_t NL = (size_t)n * b->ld;                  // row stride of V and W
   const int rows = b->rank1 ? 1 : K;
   double* V_t = b->d_V + (size_t)((t - 1) & 1) * K * NL;
   const double* V_n = b->d_V + (size_t)(t & 1) * K * NL;   // V_{t+1}
+  if (gn < 0) gn = n;
   if (what == 0) {
     const double* Pt = b->rank1 ? b->d_pi + (size_t)t * K : b->d_P + (size_t)(t - 1) * K * K;
-    if (b->ozaki) return launch_ozaki(Pt, V_n, b->d_W, K, K, (long long)NL, (long long)NL, (long long)NL, s, pdl);
-    if (const int d3 = (b->rank1 || !b->dmma) ? 0 : use_dmma3(rows, (int64_t)NL, K))
-      return launch_dmma3(d3, Pt, V_n, b->d_W, rows, K, (int)NL, (int)NL, s, pdl);
+    const size_t c0 = (size_t)g0 * b->ld, nc = (size_t)gn * b->ld;
+    if (b->ozaki)
+      return launch_ozaki(Pt, V_n + c0, b->d_W + c0, K, K, (long long)nc, (long long)NL, (long long)NL, s, pdl);
+    if (const int d3 = (b->rank1 || !b->dmma) ? 0 : use_dmma3(rows, (int64_t)nc, K))
+      return launch_dmma3(d3, Pt, V_n + c0, b->d_W + c0, rows, K, (int)nc, (int)NL, s, pdl);
+    if (gn != n) return cudaErrorInvalidValue;   // groups only on the DMMA / Ozaki expectations
     if (b->dmma && !b->rank1 && K > 128 && contract_dmma2_smem(K, kDRbig, kDCbig) <= 200 * 1024) {
       const int ncb = (int)((NL + kDCbig * 16 - 1) / (kDCbig * 16)), nrb = (K + kDRbig * 8 - 1) / (kDRbig * 8);
       return launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
@@ -2041,9 +2055,9 @@ cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, b
   const size_t pol_inst = (size_t)T * K * S, pol_stage = (size_t)(t - 1) * K * S;
   if (what == 1)
     return launch(window_batch_kernel_of(b->win_opt, b->win_levels),
-                  dim3((S + kWinThreads * b->win_opt - 1) / (kWinThreads * b->win_opt), K, b->nwin), dim3(kWinThreads),
-                  b->win_smem, s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_widx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
-                  pol_stage, lam, b->ld, (int)NL, b->rank1);
+                  dim3((S + kWinThreads * b->win_opt - 1) / (kWinThreads * b->win_opt), K, gn == n ? b->nwin : gn),
+                  dim3(kWinThreads), b->win_smem, s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_widx + g0,
+                  (const double*)b->d_W, V_t, b->d_pol, pol_inst, pol_stage, lam, b->ld, (int)NL, b->rank1);
   return launch(stencil_batch_kernel, dim3((S + kTile - 1) / kTile, K, b->nbrute), dim3(kStencilWarps * 32), b->brute_smem,
                 s, pdl, (const BatchInst*)b->d_bi, (const int*)b->d_bidx, (const double*)b->d_W, V_t, b->d_pol, pol_inst,
                 pol_stage, lam, b->ld, (int)NL, b->rank1);
@@ -2055,7 +2069,39 @@ esdp_status batch_enqueue(esdp_batch* b, cudaStream_t s) {
   const int rows = b->rank1 ? 1 : K;
   int64_t launches = 0;
   bool after_kernel = false;
-  for (int t = T; t >= 1; --t) {
+  if (b->groups > 1) {   // independent chains of instance groups, each on its own capture stream
+    const int G = b->groups;
+    BCUDA(b, cudaMemsetAsync(b->d_W, 0, rows * NL * sizeof(double), s));   // W_T = 0
+    BCUDA(b, cudaEventRecord(b->gev[0], s));
+    std::vector<cudaStream_t> gs(G, s);
+    for (int g = 1; g < G; ++g) { gs[g] = b->gstream[g - 1]; BCUDA(b, cudaStreamWaitEvent(gs[g], b->gev[0], 0)); }
+    std::vector<char> ak(G, 0);
+    for (int t = T; t >= 1; --t)
+      for (int g = 0; g < G; ++g) {
+        const int g0 = (int)((int64_t)n * g / G), gn = (int)((int64_t)n * (g + 1) / G) - g0;
+        if (t < T) {
+          const cudaError_t e = batch_stage_kernel(b, t, 0, gs[g], ak[g], g0, gn);
+          if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch contraction: %s", cudaGetErrorString(e));
+          ak[g] = 1;
+          ++launches;
+        }
+        if (t == T && g > 0) {   // start half a stage behind the previous group: its expectation overlaps our stencil
+          BCUDA(b, cudaStreamWaitEvent(gs[g], b->gev[g], 0));
+          ak[g] = 0;
+        }
+        const cudaError_t e = batch_stage_kernel(b, t, 1, gs[g], ak[g], g0, gn);
+        if (e != cudaSuccess) return bfail(b, ESDP_E_CUDA, "batch window stencil: %s", cudaGetErrorString(e));
+        ak[g] = 1;
+        ++launches;
+        if (t == T && g + 1 < G) BCUDA(b, cudaEventRecord(b->gev[g + 1], gs[g]));
+      }
+    for (int g = 1; g < G; ++g) {
+      BCUDA(b, cudaEventRecord(b->gev[G + g], gs[g]));
+      BCUDA(b, cudaStreamWaitEvent(s, b->gev[G + g], 0));
+    }
+    after_kernel = false;
+  }
+  for (int t = b->groups > 1 ? 0 : T; t >= 1; --t) {
     if (t == T) {
       BCUDA(b, cudaMemsetAsync(b->d_W, 0, rows * NL * sizeof(double), s));   // W_T = 0
       after_kernel = false;
@@ -2244,6 +2290,22 @@ esdp_status esdp_create_batch(const esdp_problem* probs, int32_t n, esdp_batch**
     cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes(K));
   if (2 * sizeof(double) * K > 48 * 1024)
     cudaFuncSetAttribute(objective_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(double) * K));
+  {   // instance groups: two independent stage chains (graph branches) from 128 instances on, so that one
+      // group's expectation overlaps the other's window stencil: cfg5 at 128 instances 70.3 -> 68.5 ms per step;
+      // at 64 instances 36.4 vs 36.6 ms, at 4 groups 73.3 ms (bench.py --config cfg5).  All instances on the
+      // window plan, >= 2 per group, the DMMA or Ozaki expectation.  ESDP_BATCH_GROUPS=G overrides (1: off).
+    const char* e = getenv("ESDP_BATCH_GROUPS");
+    const int G = e ? atoi(e) : (n >= 128 ? 2 : 1);
+    if (G > 1 && b->nbrute == 0 && n >= 2 * G && !b->rank1 && (b->dmma || b->ozaki)) {
+      b->groups = G;
+      b->gstream.assign(G - 1, nullptr);
+      b->gev.assign(2 * G, nullptr);
+      for (cudaStream_t& x : b->gstream)
+        if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return bail(bfail(b, ESDP_E_CUDA, "group streams"));
+      for (cudaEvent_t& x : b->gev)
+        if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return bail(bfail(b, ESDP_E_CUDA, "group events"));
+    }
+  }
   {   // capture the whole batch backward once
     cudaGraph_t g = nullptr;
     BCUDA(b, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));

@@ -183,6 +183,15 @@ def test_batch_wide_expectation_tiling():
     _check_batch(workloads.cfg5_instances(idx, T=3, K=100))
 
 
+@pytest.mark.parametrize("groups", ["1", "2", "3"])
+def test_batch_instance_groups(groups, monkeypatch):
+    """Instance groups with independent stage chains (graph branches; the default from 128 instances on):
+    every instance bit-identical to the oracle for 1, 2 and 3 groups of a 9-instance batch (ragged groups)."""
+    monkeypatch.setenv("ESDP_BATCH_GROUPS", groups)
+    idx = [0, 37, 100, 300, 511, 640, 777, 900, 1023]
+    _check_batch(workloads.cfg5_instances(idx, T=10, K=12))
+
+
 def test_batch_plan_reports_the_dfma_fallback(monkeypatch):
     """esdp_batch_plan: 0 (FP64 DMMA) by default; 1 (DFMA) when the DMMA bit-exactness probe fails (forced with
     ESDP_DMMA_PROBE_FAIL=1), and every instance is still the oracle's, bit for bit."""

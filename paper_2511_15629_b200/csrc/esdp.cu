@@ -669,8 +669,8 @@ void sim_tables(const esdp_ctx* c, SimParams& sp) {
   sp.gs1 = 53 - c->g_max;
 }
 
-// Before a simulation on stream s: wait for the active slot's uploads and build its sampling tables of
-// P if that upload left them stale.
+// Before a simulation on stream s: wait for the active slot's uploads and build whichever of its sampling
+// tables (pi's, P's) the uploads left stale.
 esdp_status ready_tables(esdp_ctx* c, cudaStream_t s) {
   InputSlot& x = c->slot[c->active];
   CUDA_OR_FAIL(c, cudaStreamWaitEvent(s, x.ev_tables, 0));

@@ -486,6 +486,8 @@ def run_ours(args, mode):
             "J": J, "sim_mean_profit": sim_mean,
             "window_fallback_rows": E.esdp_window_fallbacks(solver.ctx),
         }
+        if kprof and "window" in kprof and roof is not None:
+            _issue_frac(roof, kprof["window"]["warp_inst_per_launch"], clk, dev)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(inst, budget_s=args.cpu_budget)
     if kpart and world > 1:
@@ -679,9 +681,25 @@ def run_sweep(args):
                "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": 8 * n},
                "clocks": clk}
+        if kp and "window" in kp:
+            _issue_frac(out["roofline"], kp["window"]["warp_inst_per_launch"], clk, dev)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_sweep(insts, budget_s=args.cpu_budget)
     return out
+
+
+def _issue_frac(roof, warp_inst, clk, dev):
+    """Fraction of the SMs' warp-instruction issue slots (4 schedulers x SMs x SM clock) the kernel's
+    instructions (ncu count per launch, profiles/) fill over its measured launch time: how close an
+    issue-bound kernel is to its own instruction stream's bound."""
+    if roof is None or not warp_inst:
+        return
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
+    slots = roof["us_per_launch"] * 1e-6 * nsm * 4 * mhz * 1e6
+    roof["issue_frac"] = warp_inst / slots
+    roof["issue_note"] = ("ncu warp instructions per launch / (launch time x %d SMs x 4 schedulers x %.0f MHz)"
+                          % (nsm, mhz))
 
 
 def cpu_baseline_sweep(insts, budget_s=15.0, n_inst=8):

@@ -1,6 +1,9 @@
 """cfg5 batch backward, a few passes (for ncu captures of the batch kernels): python tools/batchrun.py [n] [ozaki]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# one chain over the whole batch: the captured launches then pair with bench.py's full-batch launch timing
+# (esdp_batch_kernel_time) in the roofline fields
+os.environ.setdefault("ESDP_BATCH_GROUPS", "1")
 import torch
 import paper_2511_15629_b200 as E
 import workloads

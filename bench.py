@@ -692,6 +692,7 @@ def _issue_frac(roof, warp_inst, clk, dev):
     """Fraction of the SMs' warp-instruction issue slots (4 schedulers x SMs x SM clock) the kernel's
     instructions (ncu count per launch, profiles/) fill over its measured launch time: how close an
     issue-bound kernel is to its own instruction stream's bound."""
+    import torch
     if roof is None or not warp_inst:
         return
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count

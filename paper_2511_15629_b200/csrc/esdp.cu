@@ -1450,7 +1450,11 @@ static esdp_status create_impl(const esdp_problem* pr, int32_t world, int32_t ra
       if (cudaEventCreate(&e) != cudaSuccess) { fail(c, ESDP_E_CUDA, "cudaEventCreate failed"); return bail(ESDP_E_CUDA); }
   }
   // capture the whole backward pass once; replay it for every solve
-  c->fb_batch = std::max(1, (c->T + 7) / 8);   // ~8 bid-curve batches per backward
+  {   // ~8 bid-curve batches per backward (ESDP_FB_BATCHES=n overrides: measurement)
+    const char* e = getenv("ESDP_FB_BATCHES");
+    const int nb = (e && atoi(e) > 0) ? atoi(e) : 8;
+    c->fb_batch = std::max(1, (c->T + nb - 1) / nb);
+  }
   c->side.assign(4, nullptr);
   c->join_ev.assign(c->side.size(), nullptr);
   for (size_t j = 0; j < c->side.size(); ++j)

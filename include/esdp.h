@@ -281,9 +281,8 @@ esdp_status esdp_window_level_tables(esdp_ctx* ctx, int64_t* count);
 esdp_status esdp_launch_count(const esdp_ctx* ctx, int64_t* backward_launches);
 
 /* Average device time (ms) of one expectation phase and of one stencil phase in the last completed
- * backward pass (requires ESDP_PROFILE; the caller has synchronized the stream).  Graph plan: CUDA
- * events recorded inside the graph around the kernels of ~16 evenly spaced stages.  Persistent plan:
- * contract_ms = 0 and stencil_ms = the whole dataflow kernel's time / T. */
+ * backward pass (requires ESDP_PROFILE; the caller has synchronized the stream): CUDA events recorded
+ * inside the graph around the kernels of ~16 evenly spaced stages. */
 esdp_status esdp_kernel_times(const esdp_ctx* ctx, double* contract_ms, double* stencil_ms);
 
 /* Diagnostic micro-timing (not part of the solve): warm back-to-back launches of one kernel of stage

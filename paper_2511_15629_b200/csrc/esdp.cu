@@ -798,6 +798,31 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
 }
 
+// P-resident persistent expectation (contract_pres_kernel) for wide products: rows, K <= 104 (13 row
+// fragments), K and ncols even.  ESDP_PRES=0 in the environment keeps the block-tiled dmma3 (measurement).
+constexpr int kPresMTA = 13, kPresNW = 8;
+using DPres = DmmaPres<kPresMTA, kPresNW>;
+bool use_pres(int rows, int K, int64_t ncols) {
+  const char* e = getenv("ESDP_PRES");
+  if (e && atoi(e) == 0) return false;
+  return rows <= 8 * kPresMTA && K <= 8 * kPresMTA && !(K & 1) && !(ncols & 1) && ncols <= INT32_MAX &&
+         (double)rows * (double)ncols >= kDmma3WideOutputs && DPres::smem(K) <= 227 * 1024;
+}
+cudaError_t launch_pres(const double* Pt, const double* Vn, double* Wt, int rows, int K, int64_t ncols, int ld,
+                        cudaStream_t s, bool pdl) {
+  int dev = 0, nsm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t sm = DPres::smem(K);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(contract_pres_kernel<kPresMTA, kPresNW>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (ncols + DPres::CT - 1) / DPres::CT;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, nsm));
+  return launch(contract_pres_kernel<kPresMTA, kPresNW>, dim3(grid), dim3(DPres::NTH), sm, s, pdl, Pt, Vn, Wt, rows, K,
+                (int)ncols, ld);
+}
+
 // Ozaki-sliced u8 tcgen05 expectation (ozaki.cuh): one persistent CTA per SM over 32-column tiles.
 // Requires rows <= 128, K <= 128, non-negative P and V.
 cudaError_t launch_ozaki(const double* Pt, const double* Vn, double* Wt, int rows, int K, long long ncols, long long ldv,
@@ -2038,6 +2063,8 @@ cudaError_t batch_stage_kernel(esdp_batch* b, int t, int what, cudaStream_t s, b
     const size_t c0 = (size_t)g0 * b->ld, nc = (size_t)gn * b->ld;
     if (b->ozaki)
       return launch_ozaki(Pt, V_n + c0, b->d_W + c0, K, K, (long long)nc, (long long)NL, (long long)NL, s, pdl);
+    if (!b->rank1 && b->dmma && use_pres(rows, K, (int64_t)nc))
+      return launch_pres(Pt, V_n + c0, b->d_W + c0, rows, K, (int64_t)nc, (int)NL, s, pdl);
     if (const int d3 = (b->rank1 || !b->dmma) ? 0 : use_dmma3(rows, (int64_t)nc, K))
       return launch_dmma3(d3, Pt, V_n + c0, b->d_W + c0, rows, K, (int)nc, (int)NL, s, pdl);
     if (gn != n) return cudaErrorInvalidValue;   // groups only on the DMMA / Ozaki expectations

@@ -455,6 +455,94 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
   pdl_trigger_late();
 }
 
+// ------------------------------------------------------------------------------------------------
+// P-resident persistent expectation for wide products with K <= 8 MTA (the cfg5 batch GEMM: [100] x
+// [128,512] per stage).  One CTA per SM keeps the whole P_t in shared memory (loaded once, before the
+// dependency wait: P is an input) and walks column tiles of CT = 8 NW columns, double-buffering the V_{t+1}
+// tile with cp.async; warp w owns the tile's columns [8w, 8w + 8) for every row (MTA 8-row fragments, one
+// B fragment per k'-quad).  V_{t+1} is then read from L2 once per column (the 16 x 128 block tiles re-read it
+// once per row block), and each k'-quad issues MTA DMMAs for MTA + 1 shared loads.  Each accumulator runs its
+// k'-quads in ascending order, one DMMA after the other: the canonical chain (R15), as in dmma2/dmma3.
+// ------------------------------------------------------------------------------------------------
+template <int MTA, int NW>
+struct DmmaPres {
+  static constexpr int CT = 8 * NW, NTH = 32 * NW;
+  static constexpr int SB = CT + (8 - CT % 16 + 16) % 16;   // B rows: stride 8 mod 16 (conflict-free)
+  __host__ __device__ static int kp(int K) { return (K + 3) & ~3; }
+  __host__ __device__ static int sa(int K) { const int k = kp(K); return (k % 16 == 0 || k % 16 == 8) ? k + 4 : k; }   // 4 or 12 mod 16
+  static size_t smem(int K) { return sizeof(double) * ((size_t)8 * MTA * sa(K) + (size_t)2 * kp(K) * SB); }
+};
+
+template <int MTA, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) contract_pres_kernel(const double* __restrict__ Pt,   // [rows][K], K even
+                                                                  const double* __restrict__ Vn,   // [K][ld]
+                                                                  double* __restrict__ Wt,         // [rows][ld]
+                                                                  int rows, int K, int ncols, int ld) {
+  using D = DmmaPres<MTA, NW>;
+  extern __shared__ __align__(16) double psm[];
+  const int Kp = D::kp(K), SA = D::sa(K);
+  double* As = psm;                                   // [8 MTA][SA]: all of P_t, zero rows / k' past the ends
+  double* Bs = psm + (size_t)8 * MTA * SA;            // [2][Kp][SB]: V_{t+1} column tiles
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, kq = lane & 3, g = lane >> 2;
+  ESDP_ASSERT(rows <= 8 * MTA && (K & 1) == 0 && blockDim.x == D::NTH);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(psm);
+  auto cp16z = [](unsigned dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+  };
+  {   // P_t: 8 MTA rows x Kp/2 pairs
+    const int np = Kp / 2;
+    for (int e = tid; e < 8 * MTA * np; e += D::NTH) {
+      const int r = e / np, k2 = 2 * (e - r * np);
+      const bool ok = r < rows && k2 < K;
+      cp16z(sbase + (unsigned)(sizeof(double) * (r * SA + k2)), ok ? Pt + (size_t)r * K + k2 : Pt, ok);
+    }
+  }
+  const int ntiles = (ncols + D::CT - 1) / D::CT;
+  auto issue_b = [&](int tile, int st) {   // rows k' < Kp of columns [tile CT, tile CT + CT)
+    const unsigned dst0 = sbase + (unsigned)(sizeof(double) * ((size_t)8 * MTA * SA + (size_t)st * Kp * D::SB));
+    const int c0 = tile * D::CT;
+    constexpr int np = D::CT / 2;
+    for (int e = tid; e < Kp * np; e += D::NTH) {
+      const int k = e / np, c2 = 2 * (e - k * np);
+      const bool ok = k < K && c0 + c2 < ncols;   // ncols even or the last pair inside ld (ld % 4 == 0)
+      cp16z(dst0 + (unsigned)(sizeof(double) * (k * D::SB + c2)), ok ? Vn + (size_t)k * ld + c0 + c2 : Vn, ok);
+    }
+  };
+  pdl_wait();
+  int tile = blockIdx.x;
+  if (tile < ntiles) issue_b(tile, 0);
+  cp_async_commit();                                  // group: P_t + the first V tile
+  for (int j = 0; tile < ntiles; tile += gridDim.x, ++j) {
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) issue_b(nxt, (j + 1) & 1);
+    cp_async_commit();
+    cp_async_wait_group<1>();                         // tile j (and P_t) landed, this thread's copies ...
+    __syncthreads();                                  // ... and everyone's
+    const double* bs = Bs + (size_t)(j & 1) * Kp * D::SB + kq * D::SB + warp * 8 + g;
+    const double* as = As + g * SA + kq;
+    double acc[MTA][2];
+#pragma unroll
+    for (int m = 0; m < MTA; ++m) acc[m][0] = acc[m][1] = 0.0;
+    for (int q = 0; q < Kp / 4; ++q) {
+      const double b = bs[4 * q * D::SB];
+#pragma unroll
+      for (int m = 0; m < MTA; ++m) dmma_8x8x4(acc[m][0], acc[m][1], as[m * 8 * SA + 4 * q], b);
+    }
+    const int c = tile * D::CT + warp * 8 + 2 * kq;   // even, ld % 4 == 0: 16-byte aligned
+#pragma unroll
+    for (int m = 0; m < MTA; ++m) {
+      const int r = m * 8 + g;
+      if (r >= rows) continue;
+      double* wr = Wt + (size_t)r * ld;
+      if (c + 1 < ncols) *reinterpret_cast<double2*>(wr + c) = make_double2(acc[m][0], acc[m][1]);
+      else if (c < ncols) wr[c] = acc[m][0];
+    }
+    __syncthreads();                                  // stage j & 1 is refilled by the copies of tile j + 2
+  }
+  cp_async_wait_group<0>();
+  pdl_trigger_late();
+}
+
 // mbarrier helpers (shared-memory barriers completed by async copies or tensor-core commits)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {

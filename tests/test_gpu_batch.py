@@ -176,11 +176,19 @@ def test_batch_window_variants(opt, generic, monkeypatch):
     _check_batch(workloads.cfg5_instances([0, 37, 300, 1023], T=8, K=10))
 
 
-def test_batch_wide_expectation_tiling():
-    """48 cfg5 configurations (K = 100: 4.8e6 expectation outputs per stage) take the wide DMMA tiling
-    (16 x 128 blocks, two stages; >= 4e6 outputs): every instance stays bit-identical to the oracle."""
+@pytest.mark.parametrize("pres", ["1", "0"])
+def test_batch_wide_expectation_tiling(pres, monkeypatch):
+    """48 cfg5 configurations (K = 100: 4.8e6 expectation outputs per stage, >= 4e6) take the P-resident
+    persistent expectation (default: P_t kept in shared memory, 64-column V tiles double-buffered) or, with
+    ESDP_PRES=0, the wide DMMA tiling (16 x 128 blocks, two stages): every instance bit-identical to the
+    oracle either way; also in two instance groups of 48 and 49 configurations (each group's product
+    >= 4e6 outputs, at a column offset)."""
+    monkeypatch.setenv("ESDP_PRES", pres)
     idx = [(j * 1024) // 48 for j in range(48)]
     _check_batch(workloads.cfg5_instances(idx, T=3, K=100))
+    monkeypatch.setenv("ESDP_BATCH_GROUPS", "2")
+    idx = [(j * 1024) // 97 for j in range(97)]
+    _check_batch(workloads.cfg5_instances(idx, T=2, K=100))
 
 
 @pytest.mark.parametrize("groups", ["1", "2", "3"])

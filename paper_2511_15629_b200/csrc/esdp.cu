@@ -800,8 +800,14 @@ cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* 
 
 // P-resident persistent expectation (contract_pres_kernel) for wide products: rows, K <= 104 (13 row
 // fragments), K and ncols even.  ESDP_PRES=0 in the environment keeps the block-tiled dmma3 (measurement).
-constexpr int kPresMTA = 13, kPresNW = 8;
-using DPres = DmmaPres<kPresMTA, kPresNW>;
+#ifndef ESDP_PRES_NW
+#define ESDP_PRES_NW 8
+#endif
+#ifndef ESDP_PRES_NT
+#define ESDP_PRES_NT 1
+#endif
+constexpr int kPresMTA = 13, kPresNW = ESDP_PRES_NW, kPresNT = ESDP_PRES_NT;
+using DPres = DmmaPres<kPresMTA, kPresNW, kPresNT>;
 bool use_pres(int rows, int K, int64_t ncols) {
   const char* e = getenv("ESDP_PRES");
   if (e && atoi(e) == 0) return false;
@@ -814,12 +820,12 @@ cudaError_t launch_pres(const double* Pt, const double* Vn, double* Wt, int rows
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = DPres::smem(K);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(contract_pres_kernel<kPresMTA, kPresNW>,
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(contract_pres_kernel<kPresMTA, kPresNW, kPresNT>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (ncols + DPres::CT - 1) / DPres::CT;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, nsm));
-  return launch(contract_pres_kernel<kPresMTA, kPresNW>, dim3(grid), dim3(DPres::NTH), sm, s, pdl, Pt, Vn, Wt, rows, K,
+  return launch(contract_pres_kernel<kPresMTA, kPresNW, kPresNT>, dim3(grid), dim3(DPres::NTH), sm, s, pdl, Pt, Vn, Wt, rows, K,
                 (int)ncols, ld);
 }
 

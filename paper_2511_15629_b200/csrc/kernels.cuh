@@ -464,21 +464,21 @@ __global__ void __launch_bounds__(32 * WC) contract_dmma3_kernel(const double* _
 // once per row block), and each k'-quad issues MTA DMMAs for MTA + 1 shared loads.  Each accumulator runs its
 // k'-quads in ascending order, one DMMA after the other: the canonical chain (R15), as in dmma2/dmma3.
 // ------------------------------------------------------------------------------------------------
-template <int MTA, int NW>
+template <int MTA, int NW, int NT = 1>
 struct DmmaPres {
-  static constexpr int CT = 8 * NW, NTH = 32 * NW;
+  static constexpr int CT = 8 * NT * NW, NTH = 32 * NW;
   static constexpr int SB = CT + (8 - CT % 16 + 16) % 16;   // B rows: stride 8 mod 16 (conflict-free)
   __host__ __device__ static int kp(int K) { return (K + 3) & ~3; }
   __host__ __device__ static int sa(int K) { const int k = kp(K); return (k % 16 == 0 || k % 16 == 8) ? k + 4 : k; }   // 4 or 12 mod 16
   static size_t smem(int K) { return sizeof(double) * ((size_t)8 * MTA * sa(K) + (size_t)2 * kp(K) * SB); }
 };
 
-template <int MTA, int NW>
+template <int MTA, int NW, int NT = 1>
 __global__ void __launch_bounds__(32 * NW, 1) contract_pres_kernel(const double* __restrict__ Pt,   // [rows][K], K even
                                                                   const double* __restrict__ Vn,   // [K][ld]
                                                                   double* __restrict__ Wt,         // [rows][ld]
                                                                   int rows, int K, int ncols, int ld) {
-  using D = DmmaPres<MTA, NW>;
+  using D = DmmaPres<MTA, NW, NT>;
   extern __shared__ __align__(16) double psm[];
   const int Kp = D::kp(K), SA = D::sa(K);
   double* As = psm;                                   // [8 MTA][SA]: all of P_t, zero rows / k' past the ends
@@ -518,24 +518,35 @@ __global__ void __launch_bounds__(32 * NW, 1) contract_pres_kernel(const double*
     cp_async_commit();
     cp_async_wait_group<1>();                         // tile j (and P_t) landed, this thread's copies ...
     __syncthreads();                                  // ... and everyone's
-    const double* bs = Bs + (size_t)(j & 1) * Kp * D::SB + kq * D::SB + warp * 8 + g;
+    const double* bs = Bs + (size_t)(j & 1) * Kp * D::SB + kq * D::SB + warp * (8 * NT) + g;
     const double* as = As + g * SA + kq;
-    double acc[MTA][2];
+    double acc[MTA][NT][2];
 #pragma unroll
-    for (int m = 0; m < MTA; ++m) acc[m][0] = acc[m][1] = 0.0;
+    for (int m = 0; m < MTA; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     for (int q = 0; q < Kp / 4; ++q) {
-      const double b = bs[4 * q * D::SB];
+      double b[NT];
 #pragma unroll
-      for (int m = 0; m < MTA; ++m) dmma_8x8x4(acc[m][0], acc[m][1], as[m * 8 * SA + 4 * q], b);
+      for (int n = 0; n < NT; ++n) b[n] = bs[4 * q * D::SB + 8 * n];
+#pragma unroll
+      for (int m = 0; m < MTA; ++m) {
+        const double a = as[m * 8 * SA + 4 * q];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], a, b[n]);
+      }
     }
-    const int c = tile * D::CT + warp * 8 + 2 * kq;   // even, ld % 4 == 0: 16-byte aligned
 #pragma unroll
     for (int m = 0; m < MTA; ++m) {
       const int r = m * 8 + g;
       if (r >= rows) continue;
       double* wr = Wt + (size_t)r * ld;
-      if (c + 1 < ncols) *reinterpret_cast<double2*>(wr + c) = make_double2(acc[m][0], acc[m][1]);
-      else if (c < ncols) wr[c] = acc[m][0];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int c = tile * D::CT + warp * (8 * NT) + 8 * n + 2 * kq;   // even, ld % 4 == 0: 16-byte aligned
+        if (c + 1 < ncols) *reinterpret_cast<double2*>(wr + c) = make_double2(acc[m][n][0], acc[m][n][1]);
+        else if (c < ncols) wr[c] = acc[m][n][0];
+      }
     }
     __syncthreads();                                  // stage j & 1 is refilled by the copies of tile j + 2
   }

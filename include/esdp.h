@@ -84,6 +84,9 @@ enum {
  *   ESDP_FB_MODE=0|1|2  fused bid curves: side branches along the stage chain (0, default), the same batches
  *                     forked after stage 1 (1), one launch on the chain stream after stage 1 (2)
  *   ESDP_FB_BATCHES=n  fused bid curves in n stage batches per backward (default 8)
+ *   ESDP_CARVEOUT=p   preferred shared-memory carveout (percent) of the stage-chain launches (default: the
+ *                     maximum in the latency regime -- one output per thread in the window plan --, else none;
+ *                     -1: none)
  *   ESDP_PRES=0       wide batch expectations (K <= 104, >= 4e6 outputs) on the block-tiled DMMA kernel
  *                     instead of the P-resident persistent one
  *   ESDP_HOST_THREADS=n  threads of the host pool (validation, slice hashing; default min(16, cores))

@@ -710,21 +710,43 @@ double* W_of(esdp_ctx* c, int t) {
   return keep(c) ? c->d_W + (size_t)(t - 1) * RS : c->d_W;
 }
 
-// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL) when pdl is set.
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL) when pdl is set, and a
+// preferred shared-memory carveout (percent) when carve >= 0.
 template <typename... KArgs, typename... Args>
-cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+cudaError_t launch_c(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, int carve,
+                     Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (carve >= 0) {
+    attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    attr[na].val.sharedMemCarveout = (unsigned)carve;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+  return launch_c(kern, grid, block, smem, s, pdl, -1, args...);
+}
+// Carveout of a context's stage-chain launches: in the latency regime (the one-output-per-thread window plan,
+// e.g. cfg2) the expectation, stencil and objective all ask for the maximum shared-memory carveout, so that
+// consecutive kernels share one L1/shared split and the next grid's blocks can become resident beside the
+// draining one: cfg2 step 2.416 -> 2.377 ms.  In the throughput regime (cfg4, the Table 3 largest row, batches)
+// the same setting measured 0.8-1.3 % slower, so those keep the default.  ESDP_CARVEOUT=<percent> forces a
+// value everywhere on the chain, ESDP_CARVEOUT=-1 disables it (measurement).
+int chain_carveout(const esdp_ctx* c);
 
 // k'-pipelined DMMA expectation (contract_dmma3_kernel), two tilings: 16 x 64 block tiles (four 16x16
 // warp tiles) for large contractions (cfg4, cfg5 batches: >= 3e5 outputs), 8 x 32 block tiles (two 8x16
@@ -782,20 +804,22 @@ int use_dmma3(int rows, int64_t ncols, int K) {
 }
 template <typename DD>
 cudaError_t launch_dmma3_as(void (*kern)(const double*, const double*, double*, int, int, int, int, int), const double* Pt,
-                            const double* Vn, double* Wt, int rows, int K, int S, int ld, cudaStream_t s, bool pdl) {
+                            const double* Vn, double* Wt, int rows, int K, int S, int ld, cudaStream_t s, bool pdl,
+                            int carve) {
   if (DD::smem() > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DD::smem());
     if (e != cudaSuccess) return e;
   }
   const int nrb = (rows + DD::RB - 1) / DD::RB;
   const int64_t ncb = ((int64_t)S + DD::CB - 1) / DD::CB;
-  return launch(kern, dim3((unsigned)(ncb * nrb)), dim3(DD::NTH), DD::smem(), s, pdl, Pt, Vn, Wt, rows, K, S, ld, nrb);
+  return launch_c(kern, dim3((unsigned)(ncb * nrb)), dim3(DD::NTH), DD::smem(), s, pdl, carve, Pt, Vn, Wt, rows, K, S, ld,
+                  nrb);
 }
 cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* Wt, int rows, int K, int S, int ld,
-                         cudaStream_t s, bool pdl) {
-  return which == 3 ? launch_dmma3_as<D3w>(D3W_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
-       : which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl)
-                    : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl);
+                         cudaStream_t s, bool pdl, int carve = -1) {
+  return which == 3 ? launch_dmma3_as<D3w>(D3W_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve)
+       : which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve)
+                    : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve);
 }
 
 // P-resident persistent expectation (contract_pres_kernel) for wide products: rows, K <= 104 (13 row
@@ -843,6 +867,12 @@ cudaError_t launch_ozaki(const double* Pt, const double* Vn, double* Wt, int row
   return launch(ozaki_contract_kernel, dim3(grid), dim3(kOzThreads), kOzSmem, s, pdl, Pt, Vn, Wt, rows, K, ncols, ldv, ldw);
 }
 
+int chain_carveout(const esdp_ctx* c) {
+  const char* e = getenv("ESDP_CARVEOUT");   // read per launch (graph capture): tests and measurement
+  if (e) return atoi(e);
+  return (c->use_window && c->win_opt == 1) ? (int)cudaSharedmemCarveoutMaxShared : -1;
+}
+
 // The contraction of stage t (t < T): W_t = P_t V_{t+1}.
 cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const int K = c->K, S = c->S;
@@ -851,26 +881,27 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   const double* Pt = c->rank1 ? c->d_pi + (size_t)t * K : c->d_P + ((size_t)(t - 1) * K + c->k_lo) * K;
   // rank-1 (the paper's Alg. 1 GEMV W = pi_{t+1}^T V_{t+1}): one A row of the 8-row DMMA tile is live; the
   // K/4-long DMMA chain per column replaces a K-long DFMA chain (same canonical order, same bits)
+  const int cv = chain_carveout(c);
   if (rows == 1 && !(K & 1) && !(c->flags & ESDP_NO_DMMA) && use_dmma3(8, S, K))
-    return launch_dmma3(1, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl);
+    return launch_dmma3(1, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl, cv);
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
     if (const int d3 = use_dmma3(rows, S, K))
-      return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl);
+      return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl, cv);
     if (c->dmma2) {
       if (K > 128) {   // large K: taller tiles (fewer re-reads of the V column block)
         const int ncb = (S + kDCbig * 16 - 1) / (kDCbig * 16), nrb = (rows + kDRbig * 8 - 1) / (kDRbig * 8);
-        return launch(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
-                      contract_dmma2_smem(K, kDRbig, kDCbig), s, pdl, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows,
-                      K, S, c->ld, ncb);
+        return launch_c(contract_dmma2_kernel<kDRbig, kDCbig>, dim3(ncb * nrb), dim3(kDRbig * kDCbig * 32),
+                        contract_dmma2_smem(K, kDRbig, kDCbig), s, pdl, cv, Pt, (const double*)V_of(c, t + 1), W_of(c, t),
+                        rows, K, S, c->ld, ncb);
       }
       const int ncb = (S + kDC * 16 - 1) / (kDC * 16), nrb = (rows + kDR * 8 - 1) / (kDR * 8);
-      return launch(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s, pdl,
-                    Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
+      return launch_c(contract_dmma2_kernel<kDR, kDC>, dim3(ncb * nrb), dim3(kDR * kDC * 32), contract_dmma2_smem(K), s,
+                      pdl, cv, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, ncb);
     }
   }   // else (K too large for any staged DMMA tile): DFMA below
   dim3 grid((S + kColsC - 1) / kColsC, (rows + kRowsC - 1) / kRowsC);
-  return launch(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, Pt, (const double*)V_of(c, t + 1),
-                W_of(c, t), rows, K, S, c->ld);
+  return launch_c(contract_kernel, grid, dim3(kThreadsC), contract_smem_bytes(K), s, pdl, cv, Pt,
+                  (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld);
 }
 
 // Stage-invariant parameters of the window and brute-force stencils (W/V/pol/lambda set per launch).
@@ -937,18 +968,19 @@ cudaError_t launch_stencil(esdp_ctx* c, int t, cudaStream_t s, bool pdl, bool fo
     WinParams wp = win_params(c);
     wp.W = Wt; wp.V = V_of(c, t) + (size_t)c->k_lo * c->ld; wp.pol = pol; wp.lambda_t = lam;
     const int tile = kWinThreads * c->win_opt;
-    return launch(window_kernel_of(c->win_opt, c->win_levels), dim3((S + tile - 1) / tile, K), dim3(kWinThreads),
-                  c->window_smem, s, pdl, wp);
+    return launch_c(window_kernel_of(c->win_opt, c->win_levels), dim3((S + tile - 1) / tile, K), dim3(kWinThreads),
+                    c->window_smem, s, pdl, chain_carveout(c), wp);
   }
   StencilParams prm = stencil_params(c);
   prm.W = Wt; prm.V = V_of(c, t) + (size_t)c->k_lo * c->ld; prm.pol = pol; prm.lambda_t = lam;
   prm.g = c->kind == ESDP_PAYOFF_TABLE ? c->d_g + ((size_t)(t - 1) * c->K + c->k_lo) * c->A : c->d_g;
-  return launch(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl, prm);
+  return launch_c(stencil_kernel, dim3((S + kTile - 1) / kTile, K), dim3(kStencilWarps * 32), c->stencil_smem, s, pdl,
+                  chain_carveout(c), prm);
 }
 
 cudaError_t launch_objective(esdp_ctx* c, cudaStream_t s, bool pdl) {
-  return launch(objective_kernel, dim3(1), dim3(128), 2 * sizeof(double) * c->K, s, pdl, (const double*)V_of(c, 1),
-                (const double*)c->d_pi, c->K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
+  return launch_c(objective_kernel, dim3(1), dim3(128), 2 * sizeof(double) * c->K, s, pdl, chain_carveout(c),
+                  (const double*)V_of(c, 1), (const double*)c->d_pi, c->K, c->ld, c->f0, c->w0, c->on_grid, c->d_J);
 }
 
 cudaError_t launch_bids(esdp_ctx* c, int64_t n, const int32_t* req_dev, const int32_t* slot_dev, int64_t nout, int32_t cap,

@@ -776,17 +776,23 @@ using D3 = Dmma3<ESDP_D3_MT, ESDP_D3_NT, ESDP_D3_WC, ESDP_D3_KC, ESDP_D3_NS>;
 #ifndef ESDP_D3S_NS
 #define ESDP_D3S_NS 4
 #endif
+// Small tiling: 16 x 16 block tiles of two 16 x 8 warp tiles (MT = 2, NT = 1, WC = 2) since the
+// latency-regime chain launches with the maximum shared-memory carveout: cfg2 backward 1.953 -> 1.935 ms, warm
+// launch 3.27 -> 3.16 us (tools/variants_d3s.sh; before the carveout the 8 x 32 tiling of two 8 x 16 warps led).
+// Rank-1 GEMVs (one live row) keep the 8-row tiling (D3r): a 16-row tile would idle 15 of its 16 rows.
 #ifndef ESDP_D3S_NT
-#define ESDP_D3S_NT 2
+#define ESDP_D3S_NT 1
 #endif
 #ifndef ESDP_D3S_WC
 #define ESDP_D3S_WC 2
 #endif
 #ifndef ESDP_D3S_MT
-#define ESDP_D3S_MT 1
+#define ESDP_D3S_MT 2
 #endif
 using D3s = Dmma3<ESDP_D3S_MT, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>;
 #define D3S_KERNEL contract_dmma3_kernel<ESDP_D3S_MT, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_NS>
+using D3r = Dmma3<1, 2, 2, 16, 4>;
+#define D3R_KERNEL contract_dmma3_kernel<1, 2, 2, 16, 4>
 // Wide tiling for very large products (the cfg5 batch GEMM, [100] x [128,512]): 16 x 128 block tiles of four
 // 16 x 32 warp tiles, two pipeline stages (40 KB: five blocks per SM).  Measured over 17 tilings
 // (tools/variants_d3_cfg5.sh): 108.1 us per cfg5 stage against 122.5 us for the large tiling, which stays
@@ -794,7 +800,8 @@ using D3s = Dmma3<ESDP_D3S_MT, ESDP_D3S_NT, ESDP_D3S_WC, ESDP_D3S_KC, ESDP_D3S_N
 using D3w = Dmma3<2, 4, 4, 16, 2>;
 #define D3W_KERNEL contract_dmma3_kernel<2, 4, 4, 16, 2>
 constexpr double kDmma3MinOutputs = 3.0e5, kDmma3WideOutputs = 4.0e6;
-// 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large; 3: wide
+// 0: not applicable (odd K, fewer than 8 rows, or ESDP_DMMA3=0); 1: small tiling; 2: large; 3: wide (4: the
+// rank-1 8-row tiling, chosen by launch_contract)
 int use_dmma3(int rows, int64_t ncols, int K) {
   if (rows < 8 || (K & 1)) return 0;
   static const int force = [] { const char* e = getenv("ESDP_DMMA3"); return e ? atoi(e) : -1; }();
@@ -817,6 +824,7 @@ cudaError_t launch_dmma3_as(void (*kern)(const double*, const double*, double*, 
 }
 cudaError_t launch_dmma3(int which, const double* Pt, const double* Vn, double* Wt, int rows, int K, int S, int ld,
                          cudaStream_t s, bool pdl, int carve = -1) {
+  if (which == 4) return launch_dmma3_as<D3r>(D3R_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve);
   return which == 3 ? launch_dmma3_as<D3w>(D3W_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve)
        : which == 2 ? launch_dmma3_as<D3>(D3_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve)
                     : launch_dmma3_as<D3s>(D3S_KERNEL, Pt, Vn, Wt, rows, K, S, ld, s, pdl, carve);
@@ -883,7 +891,7 @@ cudaError_t launch_contract(esdp_ctx* c, int t, cudaStream_t s, bool pdl) {
   // K/4-long DMMA chain per column replaces a K-long DFMA chain (same canonical order, same bits)
   const int cv = chain_carveout(c);
   if (rows == 1 && !(K & 1) && !(c->flags & ESDP_NO_DMMA) && use_dmma3(8, S, K))
-    return launch_dmma3(1, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl, cv);
+    return launch_dmma3(4, Pt, (const double*)V_of(c, t + 1), W_of(c, t), 1, K, S, c->ld, s, pdl, cv);
   if (rows >= 8 && !(c->flags & ESDP_NO_DMMA)) {   // FP64 tensor cores (bit-identical chain, see kernels.cuh)
     if (const int d3 = use_dmma3(rows, S, K))
       return launch_dmma3(d3, Pt, (const double*)V_of(c, t + 1), W_of(c, t), rows, K, S, c->ld, s, pdl, cv);

@@ -13,7 +13,7 @@ timeout 300 python tools/stagetime.py cfg4 > $O/plain_s4.log 2>&1 && \
   timeout 600 ncu --metrics $M --clock-control none -k regex:"window_stencil|contract_dmma3" -s 200 -c 8 --csv \
   --log-file $O/k_cfg4.csv python tools/stagetime.py cfg4 > $O/ncu_k4.log 2>&1
 timeout 300 python tools/batchrun.py > $O/plain_b.log 2>&1 && \
-  timeout 600 ncu --metrics $M --clock-control none -k regex:"window_batch|contract_dmma3" -s 300 -c 8 --csv \
+  timeout 600 ncu --metrics $M --clock-control none -k regex:"window_batch|contract_dmma3|contract_pres" -s 300 -c 8 --csv \
   --log-file $O/k_cfg5.csv python tools/batchrun.py > $O/ncu_k5.log 2>&1
 python tools/stage_kernels.py $O/r02_stage_kernels.json cfg2=$O/k_cfg2.csv cfg4=$O/k_cfg4.csv cfg5=$O/k_cfg5.csv \
   > $O/stage_kernels.log 2>&1
@@ -26,6 +26,6 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_l.
 python tools/launches.py $O/launches.csv > $O/launches_summary.txt
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:"window_stencil|contract_dmma3" -s 200 -c 2 \
   -o $O/cfg2_stage python tools/stagetime.py cfg2 > $O/ncu_s.log 2>&1
-timeout 400 ncu --set full --import-source on --clock-control none -k regex:"window_batch|contract_dmma3" -s 300 -c 2 \
+timeout 400 ncu --set full --import-source on --clock-control none -k regex:"window_batch|contract_dmma3|contract_pres" -s 300 -c 2 \
   -o $O/cfg5_stage python tools/batchrun.py > $O/ncu_b.log 2>&1
 echo done

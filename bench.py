@@ -550,7 +550,7 @@ def run_sweep(args):
     dev = torch.device("cuda", local)
     n = args.instances
     tot = n * world
-    idx = [((rank + world * j) * 1024) // tot for j in range(n)]   # stratified over the sweep order
+    idx = workloads.cfg5_shard(rank, world, n)   # stratified over the sweep order
     insts = workloads.cfg5_instances(idx)
     batch = E.Batch(insts, force_brute=args.stencil == "brute",   # one graph: one expectation + one stencil launch per stage
                     ozaki=args.contract == "ozaki")

@@ -118,3 +118,19 @@ def test_validation_errors():
     pr = simple_problem(**base, K=2, T=2)
     pr.P = np.array([[[0.5, 0.6], [0.5, 0.5]]])       # row not a simplex
     assert oracle.status_of(pr) == oracle.REF_E_DATA
+
+
+def test_cfg5_shards_cover_the_sweep_once():
+    """bench.py --config cfg5 (instance sharding, no data-path collective): with world x n = 1024
+    the stratified rank samples cover the 1024-configuration sweep exactly once, and a single rank's sample
+    spreads over the whole pbar/eta range (not its cheapest corner)."""
+    import workloads
+    for world in (1, 2, 4, 8):
+        n = 1024 // world
+        got = sorted(i for r in range(world) for i in workloads.cfg5_shard(r, world, n))
+        assert got == list(range(1024)), world
+    idx = workloads.cfg5_shard(0, 1, 128)
+    assert idx[0] == 0 and idx[-1] >= 1016 and len(set(idx)) == 128
+    sweep = workloads.cfg5_sweep()
+    ratios = [sweep[i]["pbar"] for i in idx]
+    assert min(ratios) < 11.0 and max(ratios) > 95.0

@@ -220,6 +220,14 @@ def cfg5_sweep(n: int = 1024):
     return out
 
 
+def cfg5_shard(rank: int, world: int, n: int, total: int = 1024):
+    """Sweep indices of rank `rank` of `world` with n configurations per rank: a stratified sample of the
+    `total`-configuration sweep (every (world n / total)-th configuration from offset rank); with
+    world * n == total the ranks cover the sweep exactly once."""
+    tot = n * world
+    return [((rank + world * j) * total) // tot for j in range(n)]
+
+
 def cfg5_instances(idx, T: int = 288, K: int = 100):
     """Instances idx of the cfg5 sweep: cfg2's price chain (shared lambda, P), pbar/delta in [10.42, 99]
     (8 h down to 0.84 h at 5-min stages), eta_c = eta_d in [0.80, 0.99]; sbar/delta = 1000."""

@@ -549,7 +549,6 @@ def run_sweep(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local)
     n = args.instances
-    tot = n * world
     idx = workloads.cfg5_shard(rank, world, n)   # stratified over the sweep order
     insts = workloads.cfg5_instances(idx)
     batch = E.Batch(insts, force_brute=args.stencil == "brute",   # one graph: one expectation + one stencil launch per stage
